@@ -1,0 +1,245 @@
+/*
+ * mlk_b200.h -- C ABI of the sm_100a per-histogram compress/decompress path.
+ *
+ * Drop-in boundary for the reference package `mlk` (arXiv 2212.10733,
+ * /root/reference/pkg/src/mlk).  Two levels are exported:
+ *
+ *  (1) the reference's own operator API (mlk/kernels.py:20-32, implemented by
+ *      _ckernels.pyx / _pykernels.py), batched: Newton solves, zigzag,
+ *      LEB128 varints, fixed-width index packing, plus the DEFLATE stage the
+ *      residual codec wraps around them (residual.py:60-98);
+ *  (2) the stage API that replaces the per-shard numpy code in
+ *      pipeline._compress_shard (pipeline.py:196-320) and
+ *      pipeline._decode_shard (pipeline.py:397-427).
+ *
+ * Conventions: every pointer is DEVICE memory unless its name ends in `_h`;
+ * every entry point is asynchronous on `stream` and returns MLK_OK or a
+ * negative MLK_ERR_* code (the Python wrapper maps them to the reference's
+ * exception classes, errors.py:4-34).  Newton outcomes are per-image status
+ * codes, never errors (as in the reference).  No entry point keeps per-shard
+ * state in globals, so shards may run concurrently on several streams.
+ */
+#ifndef MLK_B200_H
+#define MLK_B200_H
+
+#include <stdint.h>
+#include <cuda_runtime.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes */
+#define MLK_OK 0
+#define MLK_ERR_DIM (-1)      /* DimensionError */
+#define MLK_ERR_CONFIG (-2)   /* ConfigError */
+#define MLK_ERR_FORMAT (-3)   /* FormatError */
+#define MLK_ERR_SIZE (-4)     /* SizeMismatchError */
+#define MLK_ERR_VALUE (-5)    /* ValueError (kernels.py codecs) */
+#define MLK_ERR_CUDA (-6)     /* launch / runtime failure */
+
+/* Newton status codes, _pykernels.py:11-13 */
+#define MLK_NEWTON_CONVERGED 0
+#define MLK_NEWTON_MAX_ITER 1
+#define MLK_NEWTON_DEGENERATE 2
+
+/* per-image flag bits written by the stage kernels */
+#define MLK_F_SELECTED 1u     /* residual coded (pipeline.py:235) */
+#define MLK_F_NONFINITE 2u    /* AE error not finite -> exception (pipeline.py:233) */
+#define MLK_F_RECHECK 4u      /* AE-error decision needs the exact pass */
+#define MLK_F_EXC_NEWTON 8u   /* Newton not converged (pipeline.py:268) */
+#define MLK_F_EXC_OVERFLOW 16u/* lambda f32 overflow (pipeline.py:271) */
+#define MLK_F_EXC_GATE 32u    /* final PD gate (pipeline.py:285) */
+#define MLK_F_EXCEPTION (MLK_F_NONFINITE | MLK_F_EXC_NEWTON | MLK_F_EXC_OVERFLOW | MLK_F_EXC_GATE)
+
+/* One shard of the node-range decomposition (decomp.py:73-105).  Image j of
+ * the shard is the D doubles at f0 + base + (j / block) * plane_stride
+ * + (j % block) * D, i.e. plane-major members exactly as partition() lists
+ * them (decomp.py:102). */
+typedef struct {
+    int64_t base;
+    int64_t plane_stride;
+    int32_t block;
+    int32_t n_img;
+    int32_t img_off;    /* first index of this shard in the per-image arrays */
+    int32_t small_blas; /* n_img*L*D <= 1e6: OpenBLAS small-matrix kernel order */
+    double mean, std;   /* AEModel normaliser (autoencoder.py:26-57) */
+    double eb;          /* error bound chosen by the search (residual.py:129) */
+    int32_t lossless;   /* search fell back to lossless payloads */
+    int32_t w_off;      /* float offset of this shard's W (L x D) */
+} MlkShard;
+
+/* Grid tables, all DEVICE arrays of D = rows*cols doubles computed on the
+ * host with the reference's numpy expressions (lagrange.py:68-80, 163-173,
+ * 199-204; qoi.py:65-72). */
+typedef struct {
+    int32_t rows, cols, D, pad;
+    double mass;
+    const double* vol;      /* grid.vol (row-major) */
+    const double* vpar;     /* v_par of each cell's column */
+    const double* vperp2;   /* v_perp**2 of each cell's row */
+    const double* hmvol;    /* (0.5*mass) * vol */
+    const double* ash;      /* 3*D: base[r] / max|base[r]| for r = 0, 1, 2 */
+    const uint8_t* tree_cols; /* D: decode bracketing probed from the host BLAS */
+    double s0, s1, s2;      /* shared row scales */
+} MlkGrid;
+
+typedef struct {
+    double step;
+    int32_t max_iter;
+    int32_t retry;
+    double tol;
+    double floor;
+    double retry_step;
+    int32_t retry_max_iter;
+    int32_t lam_f32;        /* lambda_precision == "f32" */
+    double tau;
+} MlkNewton;
+
+/* ---------------- library info ---------------- */
+const char* mlk_version(void);
+int mlk_device_check(void); /* MLK_OK when a sm_100 device is current */
+
+/* ======================= (1) reference operator API ======================= */
+
+/* kernels.newton_solve (kernels.py:26; _ckernels.pyx:62-137), batched over
+ * n systems.  f_plus (n, d), a (n, 4, d), b (n, 4) -> lam (n, 4),
+ * status (n), iters (n). */
+int mlk_newton_solve_batch(const double* f_plus, const double* a, const double* b,
+                           int64_t n, int32_t d, double step, int32_t max_iter, double tol,
+                           double* lam, int32_t* status, int32_t* iters, cudaStream_t stream);
+
+/* kernels.zigzag_map / zigzag_unmap (kernels.py:27-28; _ckernels.pyx:143-150) */
+int mlk_zigzag_map(const int64_t* q, uint64_t* z, int64_t n, cudaStream_t stream);
+int mlk_zigzag_unmap(const uint64_t* z, int64_t* q, int64_t n, cudaStream_t stream);
+
+/* kernels.varint_encode (kernels.py:29; _ckernels.pyx:153-171) over n_streams
+ * independent streams: stream s is values[off[s] .. off[s+1]).  Bytes go to
+ * out + out_off[s] (capacity 10 values each); out_len[s] receives the length. */
+int mlk_varint_encode_batch(const uint64_t* values, const int64_t* off, int32_t n_streams,
+                            uint8_t* out, const int64_t* out_off, int64_t* out_len,
+                            cudaStream_t stream);
+
+/* kernels.varint_decode (kernels.py:30; _ckernels.pyx:174-211): stream s has
+ * in_len[s] bytes at in + in_off[s] and decodes count[s] values into
+ * values + val_off[s]; consumed[s] = bytes used, or -1 (truncated) /
+ * -2 (exceeds 64 bits). */
+int mlk_varint_decode_batch(const uint8_t* in, const int64_t* in_off, const int64_t* in_len,
+                            int32_t n_streams, const int64_t* count, uint64_t* values,
+                            const int64_t* val_off, int64_t* consumed, cudaStream_t stream);
+
+/* kernels.pack_indices / unpack_indices (kernels.py:31-32; _ckernels.pyx:217-275).
+ * pack returns MLK_ERR_VALUE via *bad (device int) when an index >= 2**bits. */
+int mlk_pack_indices(const uint16_t* idx, int64_t n, int32_t bits, uint8_t* out,
+                     int32_t* bad, cudaStream_t stream);
+int mlk_unpack_indices(const uint8_t* buf, int64_t count, int32_t bits, uint16_t* out,
+                       cudaStream_t stream);
+
+/* zlib.compress(data, 6) (residual.py:70,77) for n streams: input s is
+ * in_len[s] bytes at in + in_off[s]; output (2-byte zlib header, DEFLATE
+ * stream reproducing zlib 1.3 deflate_slow level 6, Adler-32) goes to
+ * out + out_off[s] with capacity out_cap each; out_len[s] = bytes written or
+ * -1 if out_cap was too small.  `work` >= n * MLK_DEFLATE_WORK bytes. */
+#define MLK_DEFLATE_WORK (1u << 19)
+int mlk_zlib_compress6(const uint8_t* in, const int64_t* in_off, const int64_t* in_len,
+                       int32_t n, uint8_t* out, const int64_t* out_off, int64_t out_cap,
+                       int64_t* out_len, uint8_t* work, cudaStream_t stream);
+
+/* zlib.decompress (residual.py:86) for n streams; out_len[s] = bytes produced,
+ * or -1 (corrupt) / -2 (output capacity exceeded). */
+int mlk_zlib_decompress(const uint8_t* in, const int64_t* in_off, const int64_t* in_len,
+                        int32_t n, uint8_t* out, const int64_t* out_off, int64_t out_cap,
+                        int64_t* out_len, cudaStream_t stream);
+
+/* ======================= (2) stage API (one launch covers all shards) ====== */
+
+/* Pass 1 over f0 (autoencoder.encode_batch autoencoder.py:99-103 in OpenBLAS
+ * order; qoi.compute_qoi_batch qoi.py:60-76; per-image max/min/sum/sum-sq).
+ * lat (total, L); stats (total, 4) = [max, min, sum, sumsq]; qoi (total, 4). */
+int mlk_stage1(const double* f0, const MlkShard* shards, int32_t n_shards, int32_t total,
+               const MlkGrid* grid_h, const float* W, int32_t L, double* lat, double* stats,
+               double* qoi, cudaStream_t stream);
+
+/* quantizer.pq_train (quantizer.py:99-108; kmeans_1d 53-91) for every
+ * (shard, dim): first_idx / draws are the PCG64 draws kmeans_1d consumes
+ * (one integers() then K-1 random(), computed by the host from the seed).
+ * shards_h is a HOST array.  cents (n_shards, L, K) float32, sorted;
+ * scratch >= 4 * L * total doubles; info (n_shards, L, 4). */
+int mlk_kmeans(const double* lat, const MlkShard* shards_h, int32_t n_shards, int32_t L,
+               int32_t K, const int64_t* first_idx, const double* draws, double* scratch,
+               float* cents, int32_t* info, cudaStream_t stream);
+
+/* pq_encode + AE-error decision (quantizer.py:111-120; pipeline.py:228-235):
+ * codes (total, L) u8; flags gets SELECTED or RECHECK.  gram holds per shard
+ * [W W^T (L*L), row sums (L), ||W_k||_2 (L), max|W_k| (L)] computed by the
+ * host; recon_bound (total) bounds max|recon| for the probe's slack. */
+int mlk_select(const double* lat, const double* stats, const MlkShard* shards,
+               int32_t n_shards, int32_t total, const MlkGrid* grid_h, const float* cents,
+               int32_t L, int32_t K, const double* gram, double tau, uint8_t* codes,
+               uint8_t* flags, double* err_approx, double* recon_bound, cudaStream_t stream);
+
+/* exact per-image NRMSE (qoi.py:107-119, numpy pairwise order) for images
+ * flagged RECHECK; rewrites their flags to SELECTED / NONFINITE / 0. */
+int mlk_recheck(const double* f0, const double* stats, const MlkShard* shards,
+                int32_t n_shards, int32_t total, const MlkGrid* grid_h, const float* W,
+                int32_t L, const float* cents, int32_t K, const uint8_t* codes, double tau,
+                uint8_t* flags, double* err_exact, cudaStream_t stream);
+
+/* one CTA per shard: sel[img_off + r] = r-th selected image (ascending, as
+ * np.flatnonzero, pipeline.py:235), sel_rank[img] = r or -1, sel_by_range =
+ * the same set ordered by range bucket, sel_count[s], eb_hi[s] = tau * max
+ * range of the selection (residual.py:143-144). */
+int mlk_compact(const uint8_t* flags, const double* stats, const MlkShard* shards,
+                int32_t n_shards, double tau, int32_t* sel, int32_t* sel_rank,
+                int32_t* sel_by_range, int32_t* sel_count, double* eb_hi, cudaStream_t stream);
+
+/* residual.find_error_bound's predicate (residual.py:149-155) for n_cand
+ * candidate bounds per shard: fail[s*n_cand + c] becomes non-zero when a
+ * selected image of shard s misses tau at cand[s*n_cand + c].  act_off
+ * (n_shards + 1) enumerates the selected images visited per shard. */
+int mlk_probe(const double* f0, const double* stats, const MlkShard* shards,
+              int32_t n_shards, const MlkGrid* grid_h, const float* W, int32_t L,
+              const float* cents, int32_t K, const uint8_t* codes,
+              const int32_t* sel_by_range, const int32_t* act_off, int32_t n_work,
+              const double* recon_bound, double tau, const double* cand, int32_t n_cand,
+              int32_t* fail, cudaStream_t stream);
+
+/* Stage 4 encode + stage 5 (pipeline.py:239-292): residual q / zigzag /
+ * varint for selected images into varint + (slot_base[s] + sel_rank) *
+ * varint_cap; lagrange.project_batch + cast_lambda + apply_lambda_batch +
+ * the final gate.  Per image: lam (cast; 0 for exceptions), qst (stored
+ * QoIs; 0 for exceptions), status, iters, flags |= EXC_*, ferr (final
+ * NRMSE), fqoi (moments of the final image), fsse (sum of squared final
+ * errors).  *err_flag = MLK_ERR_CONFIG when |q| >= 2**62 (residual.py:67). */
+int mlk_project(const double* f0, const double* stats, const double* qoi,
+                const MlkShard* shards, int32_t n_shards, int32_t total, const MlkGrid* grid_h,
+                const float* W, int32_t L, const float* cents, int32_t K, const uint8_t* codes,
+                const int32_t* sel_rank, const int32_t* slot_base, const MlkNewton* opts_h,
+                uint8_t* flags, double* lam, double* qst, int32_t* status, int32_t* iters,
+                double* ferr, double* fqoi, double* fsse, uint8_t* varint, int64_t varint_cap,
+                int64_t* varint_len, int32_t* err_flag, cudaStream_t stream);
+
+/* Decode path (pipeline.py:397-427) for all images of all shards: recon from
+ * codes; + residual (res_slot[img] >= 0: D zigzag codes at res_codes +
+ * slot * D, dequantised with res_eb[slot] unless res_mode[slot] == 1
+ * (lossless f64 bits), BuiltinCodec.decompress residual.py:81-98); apply
+ * lambda with the stored QoIs and floor_ (lamq (total, 8) = [lam, qoi]);
+ * exceptions (exc_slot[img] >= 0) copied from exc_img.  Output images are
+ * written at the shard addresses of `out`. */
+int mlk_decode(const MlkShard* shards, int32_t n_shards, int32_t total, const MlkGrid* grid_h,
+               const float* W, int32_t L, const float* cents, int32_t K, const uint8_t* codes,
+               const int32_t* res_slot, const uint64_t* res_codes, const double* res_eb,
+               const uint8_t* res_mode, const double* lamq, const int32_t* exc_slot,
+               const double* exc_img, double floor_, double* out, cudaStream_t stream);
+
+/* image_nrmse_batch(a, b) (qoi.py:107-119, exact) + per-image squared-error
+ * sums, moments of a and b (compute_qoi_batch; qa/qb may be NULL) and
+ * ext = (max, min) of every image of a.  a, b: (total, D) contiguous. */
+int mlk_compare(const double* a, const double* b, int32_t total, const MlkGrid* grid_h,
+                double* err, double* sse, double* qa, double* qb, double* ext,
+                cudaStream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,206 @@
+// capi.cu -- library info, the pairwise plan, and the reference operator API
+// (mlk/kernels.py:20-32) as batched device entry points.
+#include <cstdio>
+
+#include "common.cuh"
+
+PwPlan mlk_make_pw_plan(int n) {
+    PwPlan p{};
+    p.n = n;
+    p.n_leaves = 0;
+    // iterative pre-order walk of numpy's pairwise recursion
+    int st_b[40], st_l[40], sp = 0;
+    st_b[sp] = 0;
+    st_l[sp] = n;
+    ++sp;
+    while (sp) {
+        --sp;
+        int b = st_b[sp], l = st_l[sp];
+        if (l <= 128) {
+            if (p.n_leaves < MLK_PW_MAX_LEAVES) {
+                p.start[p.n_leaves] = (short)b;
+                p.len[p.n_leaves] = (short)l;
+            }
+            ++p.n_leaves;
+            continue;
+        }
+        int l2 = pw_split(l);
+        st_b[sp] = b + l2; st_l[sp] = l - l2; ++sp;
+        st_b[sp] = b; st_l[sp] = l2; ++sp;
+    }
+    return p;
+}
+
+extern "C" const char* mlk_version(void) { return "mlk-b200 0.1 (sm_100a)"; }
+
+extern "C" int mlk_device_check(void) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return MLK_ERR_CUDA;
+    cudaDeviceProp pr;
+    if (cudaGetDeviceProperties(&pr, dev) != cudaSuccess) return MLK_ERR_CUDA;
+    return pr.major == 10 ? MLK_OK : MLK_ERR_CUDA;
+}
+
+namespace {
+
+// ---------------------------------------------------------------- zigzag
+__global__ void k_zz_map(const long long* q, unsigned long long* z, long long n) {
+    long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) z[i] = ((unsigned long long)q[i] << 1) ^ (unsigned long long)(q[i] >> 63);
+}
+__global__ void k_zz_unmap(const unsigned long long* z, long long* q, long long n) {
+    long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) q[i] = (long long)((z[i] >> 1) ^ (0ull - (z[i] & 1ull)));
+}
+
+// ---------------------------------------------------------------- varint
+// one CTA per stream; chunks of 1024 values, block-scanned byte offsets
+__global__ void __launch_bounds__(1024)
+k_varint_enc(const unsigned long long* v, const long long* off, unsigned char* out,
+             const long long* out_off, long long* out_len) {
+    __shared__ int wsum[32];
+    __shared__ long long carry;
+    const int s = blockIdx.x, tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const long long a = off[s], b = off[s + 1];
+    unsigned char* o = out + out_off[s];
+    if (tid == 0) carry = 0;
+    __syncthreads();
+    for (long long base = a; base < b; base += 1024) {
+        long long i = base + tid;
+        unsigned long long x = i < b ? v[i] : 0ull;
+        int nb = i < b ? (x == 0ull ? 1 : (64 - __clzll(x) + 6) / 7) : 0;
+        int inc = nb;
+        for (int d = 1; d < 32; d <<= 1) {
+            int t = __shfl_up_sync(0xffffffffu, inc, d);
+            if (lane >= d) inc += t;
+        }
+        if (lane == 31) wsum[w] = inc;
+        __syncthreads();
+        int pre = 0, tot = 0;
+        for (int q = 0; q < 32; ++q) {
+            if (q < w) pre += wsum[q];
+            tot += wsum[q];
+        }
+        long long p = carry + pre + inc - nb;
+        if (i < b) {
+            while (x >= 0x80ull) { o[p++] = (unsigned char)(x | 0x80ull); x >>= 7; }
+            o[p] = (unsigned char)x;
+        }
+        __syncthreads();
+        if (tid == 0) carry += tot;
+        __syncthreads();
+    }
+    if (tid == 0) out_len[s] = carry;
+}
+
+__global__ void k_varint_dec(const unsigned char* in, const long long* in_off,
+                             const long long* in_len, int n_streams, const long long* count,
+                             unsigned long long* vals, const long long* val_off,
+                             long long* consumed) {
+    int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= n_streams) return;
+    const unsigned char* p = in + in_off[s];
+    const long long size = in_len[s], cnt = count[s];
+    unsigned long long* o = vals + val_off[s];
+    long long pos = 0;
+    for (long long i = 0; i < cnt; ++i) {
+        unsigned long long x = 0;
+        int sh = 0;
+        for (;;) {
+            if (pos >= size) { consumed[s] = -1; return; }
+            unsigned char c = p[pos++];
+            x |= (unsigned long long)(c & 0x7f) << sh;
+            if (c < 0x80) break;
+            sh += 7;
+            if (sh > 63) { consumed[s] = -2; return; }
+        }
+        o[i] = x;
+    }
+    consumed[s] = pos;
+}
+
+// ---------------------------------------------------------------- bit packing
+__global__ void k_pack(const unsigned short* idx, long long n, int bits, unsigned char* out,
+                       long long nbytes, int* bad) {
+    long long byte = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (byte >= nbytes) return;
+    unsigned v = 0;
+    for (int bit = 0; bit < 8; ++bit) {
+        long long gb = byte * 8 + bit;
+        long long i = gb / bits;
+        if (i >= n) break;
+        unsigned x = idx[i];
+        if (x >= (1u << bits)) atomicExch(bad, 1);
+        v |= ((x >> (gb % bits)) & 1u) << bit;
+    }
+    out[byte] = (unsigned char)v;
+}
+
+__global__ void k_unpack(const unsigned char* buf, long long count, int bits, unsigned short* out) {
+    long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= count) return;
+    long long b0 = i * bits;
+    unsigned v = 0;
+    for (int k = 0; k < bits; ++k) {
+        long long gb = b0 + k;
+        v |= ((buf[gb >> 3] >> (gb & 7)) & 1u) << k;
+    }
+    out[i] = (unsigned short)v;
+}
+
+}  // namespace
+
+extern "C" int mlk_zigzag_map(const int64_t* q, uint64_t* z, int64_t n, cudaStream_t stream) {
+    if (n <= 0) return MLK_OK;
+    k_zz_map<<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(
+        reinterpret_cast<const long long*>(q), reinterpret_cast<unsigned long long*>(z), n);
+    return cudaGetLastError() == cudaSuccess ? MLK_OK : MLK_ERR_CUDA;
+}
+
+extern "C" int mlk_zigzag_unmap(const uint64_t* z, int64_t* q, int64_t n, cudaStream_t stream) {
+    if (n <= 0) return MLK_OK;
+    k_zz_unmap<<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(
+        reinterpret_cast<const unsigned long long*>(z), reinterpret_cast<long long*>(q), n);
+    return cudaGetLastError() == cudaSuccess ? MLK_OK : MLK_ERR_CUDA;
+}
+
+extern "C" int mlk_varint_encode_batch(const uint64_t* values, const int64_t* off,
+                                       int32_t n_streams, uint8_t* out, const int64_t* out_off,
+                                       int64_t* out_len, cudaStream_t stream) {
+    if (n_streams <= 0) return MLK_OK;
+    k_varint_enc<<<n_streams, 1024, 0, stream>>>(
+        reinterpret_cast<const unsigned long long*>(values), reinterpret_cast<const long long*>(off),
+        out, reinterpret_cast<const long long*>(out_off), reinterpret_cast<long long*>(out_len));
+    return cudaGetLastError() == cudaSuccess ? MLK_OK : MLK_ERR_CUDA;
+}
+
+extern "C" int mlk_varint_decode_batch(const uint8_t* in, const int64_t* in_off,
+                                       const int64_t* in_len, int32_t n_streams,
+                                       const int64_t* count, uint64_t* values,
+                                       const int64_t* val_off, int64_t* consumed,
+                                       cudaStream_t stream) {
+    if (n_streams <= 0) return MLK_OK;
+    k_varint_dec<<<(n_streams + 127) / 128, 128, 0, stream>>>(
+        in, reinterpret_cast<const long long*>(in_off), reinterpret_cast<const long long*>(in_len),
+        n_streams, reinterpret_cast<const long long*>(count),
+        reinterpret_cast<unsigned long long*>(values), reinterpret_cast<const long long*>(val_off),
+        reinterpret_cast<long long*>(consumed));
+    return cudaGetLastError() == cudaSuccess ? MLK_OK : MLK_ERR_CUDA;
+}
+
+extern "C" int mlk_pack_indices(const uint16_t* idx, int64_t n, int32_t bits, uint8_t* out,
+                                int32_t* bad, cudaStream_t stream) {
+    if (bits < 1 || bits > 16) return MLK_ERR_VALUE;
+    long long nbytes = (n * bits + 7) / 8;
+    if (nbytes <= 0) return MLK_OK;
+    k_pack<<<(unsigned)((nbytes + 255) / 256), 256, 0, stream>>>(idx, n, bits, out, nbytes, bad);
+    return cudaGetLastError() == cudaSuccess ? MLK_OK : MLK_ERR_CUDA;
+}
+
+extern "C" int mlk_unpack_indices(const uint8_t* buf, int64_t count, int32_t bits, uint16_t* out,
+                                  cudaStream_t stream) {
+    if (bits < 1 || bits > 16) return MLK_ERR_VALUE;
+    if (count <= 0) return MLK_OK;
+    k_unpack<<<(unsigned)((count + 255) / 256), 256, 0, stream>>>(buf, count, bits, out);
+    return cudaGetLastError() == cudaSuccess ? MLK_OK : MLK_ERR_CUDA;
+}

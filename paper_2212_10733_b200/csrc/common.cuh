@@ -1,0 +1,169 @@
+// common.cuh -- shared device helpers for the sm_100a compress/decompress path.
+//
+// Exactness conventions:
+//  * every value the reference computes with plain IEEE ops (numpy elementwise,
+//    OpenBLAS in a probed order, numpy pairwise sums) is computed here with the
+//    same ops in the same order, using __dadd_rn/__dmul_rn/... so nvcc cannot
+//    contract a*b+c into an FMA where the reference rounds twice;
+//  * tolerance-only quantities (Newton reductions, moments, report sums) use
+//    whatever order is fastest.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/mlk_b200.h"
+
+#define MLK_MAXL 8            // latent dims supported by the kernels
+#define MLK_MAXK 256          // PQ codebook size (pq_bits 8)
+#define MLK_MAX_D 4096        // cells per histogram (64 x 64)
+#define MLK_PW_MAX_LEAVES 96  // pairwise-sum leaves for D <= 4096
+
+// ----------------------------------------------------------------------------
+// numpy pairwise summation plan (numpy/_core/src/umath/loops_utils.h.src,
+// pairwise_sum_DOUBLE; reached from np.mean/np.sum on a contiguous row):
+//   n < 8   -> sequential from 0.0
+//   n <= 128 -> 8 strided accumulators, ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)),
+//              then the n % 8 tail sequentially
+//   else    -> pw(first n2) + pw(rest), n2 = n/2 rounded down to a multiple of 8
+// A plan lists the leaves (start, len) in order; combining is the same
+// recursion evaluated over the leaf sums.
+struct PwPlan {
+    int n;
+    int n_leaves;
+    short start[MLK_PW_MAX_LEAVES];
+    short len[MLK_PW_MAX_LEAVES];
+};
+
+__host__ __device__ inline int pw_split(int n) {
+    int n2 = n / 2;
+    return n2 - (n2 % 8);
+}
+
+// sum of one leaf (len <= 128) read through an accessor
+template <class Get>
+__device__ __forceinline__ double pw_leaf(Get get, int start, int len) {
+    if (len < 8) {
+        double s = 0.0;
+        for (int i = 0; i < len; ++i) s = __dadd_rn(s, get(start + i));
+        return s;
+    }
+    double r0 = get(start), r1 = get(start + 1), r2 = get(start + 2), r3 = get(start + 3);
+    double r4 = get(start + 4), r5 = get(start + 5), r6 = get(start + 6), r7 = get(start + 7);
+    int i = 8;
+    const int lim = len - (len % 8);
+    for (; i < lim; i += 8) {
+        r0 = __dadd_rn(r0, get(start + i));
+        r1 = __dadd_rn(r1, get(start + i + 1));
+        r2 = __dadd_rn(r2, get(start + i + 2));
+        r3 = __dadd_rn(r3, get(start + i + 3));
+        r4 = __dadd_rn(r4, get(start + i + 4));
+        r5 = __dadd_rn(r5, get(start + i + 5));
+        r6 = __dadd_rn(r6, get(start + i + 6));
+        r7 = __dadd_rn(r7, get(start + i + 7));
+    }
+    double s = __dadd_rn(__dadd_rn(__dadd_rn(r0, r1), __dadd_rn(r2, r3)),
+                         __dadd_rn(__dadd_rn(r4, r5), __dadd_rn(r6, r7)));
+    for (; i < len; ++i) s = __dadd_rn(s, get(start + i));
+    return s;
+}
+
+// combine leaf sums (array, in leaf order) following the recursion; `next`
+// walks the leaves.  Recursion depth is log2(n / 64).
+__device__ inline double pw_combine(const double* leaf, int n, int& next) {
+    if (n <= 128) return leaf[next++];
+    int n2 = pw_split(n);
+    double a = pw_combine(leaf, n2, next);
+    double b = pw_combine(leaf, n - n2, next);
+    return __dadd_rn(a, b);
+}
+
+// Warp-cooperative exact pairwise sum of v[0..plan.n) held in shared memory.
+// All lanes return the same value.  `scratch` holds MLK_PW_MAX_LEAVES doubles.
+__device__ inline double warp_pairwise_sum(const double* v, const PwPlan& plan,
+                                           double* scratch) {
+    const int lane = threadIdx.x & 31;
+    for (int l = lane; l < plan.n_leaves; l += 32)
+        scratch[l] = pw_leaf([&](int i) { return v[i]; }, plan.start[l], plan.len[l]);
+    __syncwarp();
+    double tot = 0.0;
+    if (lane == 0) {
+        int next = 0;
+        tot = pw_combine(scratch, plan.n, next);
+    }
+    tot = __shfl_sync(0xffffffffu, tot, 0);
+    __syncwarp();
+    return tot;
+}
+
+// ----------------------------------------------------------------------------
+// warp reductions
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+__device__ __forceinline__ double warp_min(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+__device__ __forceinline__ int warp_sum_int(int v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// NaN-propagating max/min like numpy's maximum.reduce (first NaN wins)
+__device__ __forceinline__ double np_max2(double a, double b) {
+    return (a != a) ? a : ((b != b) ? b : (a >= b ? a : b));
+}
+__device__ __forceinline__ double np_min2(double a, double b) {
+    return (a != a) ? a : ((b != b) ? b : (a <= b ? a : b));
+}
+
+// ----------------------------------------------------------------------------
+// shard addressing: image j of shard s lives at
+//   f0 + base + (j / block) * plane_stride + (j % block) * D
+__device__ __forceinline__ const double* shard_image(const double* f0, const MlkShard& s,
+                                                    int j, int D) {
+    long long p = j / s.block, x = j % s.block;
+    return f0 + s.base + p * s.plane_stride + x * (long long)D;
+}
+
+// global image index -> shard (shards sorted by img_off; few shards)
+__device__ __forceinline__ int find_shard(const MlkShard* sh, int n_shards, int g) {
+    int s = 0;
+    while (s + 1 < n_shards && sh[s + 1].img_off <= g) ++s;
+    return s;
+}
+
+// ----------------------------------------------------------------------------
+// OpenBLAS-order AE contractions (probed, SURVEY §7 hard part 2; the same
+// orders are restated in oracle/ckernels.c oracle_encode / oracle_decode).
+
+// decode one cell: sum_k z[k] * W[k][j] with the probed bracketing, then
+// * std + mean (two roundings, numpy `recon * std + mean`).
+__device__ __forceinline__ double decode_cell(const double* z, const float* W, int L, int D,
+                                              int j, bool tree, double mean, double sd) {
+    double s;
+    if (L == 4 && tree) {
+        double p0 = __dmul_rn(z[0], (double)__ldg(W + j));
+        double p1 = __dmul_rn(z[1], (double)__ldg(W + D + j));
+        double p2 = __dmul_rn(z[2], (double)__ldg(W + 2 * D + j));
+        double p3 = __dmul_rn(z[3], (double)__ldg(W + 3 * D + j));
+        s = __dadd_rn(__dadd_rn(p0, p1), __dadd_rn(p2, p3));
+    } else {
+        s = __dmul_rn(z[0], (double)__ldg(W + j));
+        for (int k = 1; k < L; ++k)
+            s = __dadd_rn(s, __dmul_rn(z[k], (double)__ldg(W + (long long)k * D + j)));
+    }
+    return __dadd_rn(__dmul_rn(s, sd), mean);
+}
+
+__device__ __forceinline__ bool is_finite(double x) { return isfinite(x); }

@@ -1,0 +1,493 @@
+// kmeans.cu -- product-quantiser codebook training on device.
+//
+// Restates quantizer.kmeans_1d (quantizer.py:53-91) per (shard, latent dim)
+// bit-for-bit:
+//  * distinct-value shortcut (np.unique, 62-65);
+//  * k-means++ seeding with the PCG64 draws the host precomputes from the
+//    seed (one Generator.integers, then one Generator.random per
+//    Generator.choice(p=d2/sum) call).  choice() is searchsorted(cdf, u,
+//    'right') on cdf = cumsum(p) / cumsum(p)[-1] where numpy's cumsum is a
+//    sequential sum: the index is decided from a parallel scan plus a
+//    rigorous rounding bound, and only an undecidable draw (|cdf - u| inside
+//    the bound) falls back to the sequential scan;
+//  * Lloyd to a fixpoint (<= 25 sweeps) with numpy's pairwise mean over each
+//    cluster's members in index order, dead clusters re-seeded at the first
+//    worst-served point against the partially updated centroids;
+//  * sorted result, cast to float32 (pq_train, quantizer.py:99-108).
+// One 1024-thread CTA per (shard, dim); members live in L2-resident scratch.
+#include "common.cuh"
+
+namespace {
+
+constexpr int KT = 1024;           // threads per CTA
+constexpr int KW = KT / 32;        // warps
+constexpr int KM_MAX_LEAVES = 6144;  // pairwise leaves (n <= 2^18 per shard)
+
+struct KmSmem {
+    double red[KW];
+    int redi[KW];
+    double cent[MLK_MAXK];
+    double newc[MLK_MAXK];
+    double oldc[MLK_MAXK];
+    double distinct[MLK_MAXK + 1];
+    int seg_start[MLK_MAXK];
+    int seg_cnt[MLK_MAXK];
+    int first_leaf[MLK_MAXK + 1];
+    int bcast_i;
+    double bcast_d;
+    int n_leaves;
+};
+
+// ---------------------------------------------------------------- block helpers
+__device__ double block_sum(double v, KmSmem& S) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    v = warp_sum(v);
+    __syncthreads();
+    if (lane == 0) S.red[w] = v;
+    __syncthreads();
+    if (w == 0) {
+        v = lane < KW ? S.red[lane] : 0.0;
+        v = warp_sum(v);
+        if (lane == 0) S.bcast_d = v;
+    }
+    __syncthreads();
+    return S.bcast_d;
+}
+
+__device__ int block_sum_int(int v, KmSmem& S) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    v = warp_sum_int(v);
+    __syncthreads();
+    if (lane == 0) S.redi[w] = v;
+    __syncthreads();
+    if (w == 0) {
+        v = lane < KW ? S.redi[lane] : 0;
+        v = warp_sum_int(v);
+        if (lane == 0) S.bcast_i = v;
+    }
+    __syncthreads();
+    return S.bcast_i;
+}
+
+__device__ double block_min(double v, KmSmem& S) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    v = warp_min(v);
+    __syncthreads();
+    if (lane == 0) S.red[w] = v;
+    __syncthreads();
+    if (w == 0) {
+        v = lane < KW ? S.red[lane] : INFINITY;
+        v = warp_min(v);
+        if (lane == 0) S.bcast_d = v;
+    }
+    __syncthreads();
+    return S.bcast_d;
+}
+
+// argmax with the first index on ties (np.argmax)
+__device__ int block_argmax(double v, int idx, KmSmem& S) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int o = 16; o > 0; o >>= 1) {
+        double ov = __shfl_xor_sync(0xffffffffu, v, o);
+        int oi = __shfl_xor_sync(0xffffffffu, idx, o);
+        if (ov > v || (ov == v && oi < idx)) { v = ov; idx = oi; }
+    }
+    __syncthreads();
+    if (lane == 0) { S.red[w] = v; S.redi[w] = idx; }
+    __syncthreads();
+    if (w == 0) {
+        v = lane < KW ? S.red[lane] : -INFINITY;
+        idx = lane < KW ? S.redi[lane] : 0x7fffffff;
+        for (int o = 16; o > 0; o >>= 1) {
+            double ov = __shfl_xor_sync(0xffffffffu, v, o);
+            int oi = __shfl_xor_sync(0xffffffffu, idx, o);
+            if (ov > v || (ov == v && oi < idx)) { v = ov; idx = oi; }
+        }
+        if (lane == 0) S.bcast_i = idx;
+    }
+    __syncthreads();
+    return S.bcast_i;
+}
+
+// exclusive block scan of per-thread nonnegative doubles; returns this
+// thread's prefix and *total.  Only additions of nonnegative partial sums are
+// used, so every prefix carries a relative error <= (log2(KT) + 1) eps.
+__device__ double block_exscan(double v, double* total, KmSmem& S) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    double inc = v;
+    for (int o = 1; o < 32; o <<= 1) {
+        double t = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += t;
+    }
+    double exc = __shfl_up_sync(0xffffffffu, inc, 1);
+    if (lane == 0) exc = 0.0;
+    __syncthreads();
+    if (lane == 31) S.red[w] = inc;
+    __syncthreads();
+    if (w == 0) {
+        double t = lane < KW ? S.red[lane] : 0.0;
+        double ti = t;
+        for (int o = 1; o < 32; o <<= 1) {
+            double u = __shfl_up_sync(0xffffffffu, ti, o);
+            if (lane >= o) ti += u;
+        }
+        double te = __shfl_up_sync(0xffffffffu, ti, 1);
+        if (lane == 0) te = 0.0;
+        __syncwarp();
+        if (lane < KW) S.red[lane] = te;
+        if (lane == 31) S.bcast_d = ti;
+    }
+    __syncthreads();
+    *total = S.bcast_d;
+    double r = S.red[w] + exc;
+    __syncthreads();
+    return r;
+}
+
+__device__ __forceinline__ int nearest(double v, const double* c, int K) {
+    int best = 0;
+    double bd = fabs(__dsub_rn(v, c[0]));
+    for (int k = 1; k < K; ++k) {
+        double d = fabs(__dsub_rn(v, c[k]));
+        if (d < bd) { bd = d; best = k; }
+    }
+    return best;
+}
+
+// enumerate pairwise leaves of a segment (single thread)
+__device__ void enum_leaves(int base, int len, int* lstart, short* llen, int& cnt) {
+    int st_b[40], st_l[40];
+    int sp = 0;
+    st_b[sp] = base;
+    st_l[sp] = len;
+    ++sp;
+    while (sp) {
+        --sp;
+        int b = st_b[sp], l = st_l[sp];
+        if (l <= 128) {
+            lstart[cnt] = b;
+            llen[cnt] = (short)l;
+            ++cnt;
+            continue;
+        }
+        int l2 = pw_split(l);
+        // push right first so the left half is enumerated first
+        st_b[sp] = b + l2; st_l[sp] = l - l2; ++sp;
+        st_b[sp] = b; st_l[sp] = l2; ++sp;
+    }
+}
+
+__device__ double combine_leaves(const double* leaf, int n, int& next) {
+    // iterative post-order over the same recursion as pw_combine
+    int st_n[40];
+    unsigned char st_state[40];
+    double vals[40];
+    int sp = 0, vp = 0;
+    st_n[0] = n;
+    st_state[0] = 0;
+    sp = 1;
+    while (sp) {
+        int m = st_n[sp - 1];
+        if (m <= 128) {
+            vals[vp++] = leaf[next++];
+            --sp;
+            continue;
+        }
+        int m2 = pw_split(m);
+        if (st_state[sp - 1] == 0) {
+            st_state[sp - 1] = 1;
+            st_n[sp] = m2; st_state[sp] = 0; ++sp;
+        } else if (st_state[sp - 1] == 1) {
+            st_state[sp - 1] = 2;
+            st_n[sp] = m - m2; st_state[sp] = 0; ++sp;
+        } else {
+            double b = vals[--vp];
+            double a = vals[--vp];
+            vals[vp++] = __dadd_rn(a, b);
+            --sp;
+        }
+    }
+    return vals[0];
+}
+
+__global__ void __launch_bounds__(KT, 1)
+k_kmeans(const double* __restrict__ lat, const MlkShard* __restrict__ shards, int L, int K,
+         const long long* __restrict__ first_idx, const double* __restrict__ draws,
+         double* __restrict__ scratch, float* __restrict__ cents, int* __restrict__ info) {
+    __shared__ KmSmem S;
+    extern __shared__ double dyn[];  // leaf sums, leaf starts/lengths, warp counters
+    double* leafsum = dyn;
+    int* lstart = reinterpret_cast<int*>(dyn + KM_MAX_LEAVES);
+    int* wcnt = lstart + KM_MAX_LEAVES;                          // [KW][K]
+    short* llen = reinterpret_cast<short*>(wcnt + KW * MLK_MAXK);
+
+    const int s = blockIdx.x / L, dim = blockIdx.x % L;
+    const MlkShard sh = shards[s];
+    const int n = sh.n_img;
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    double* base = scratch + (long long)4 * L * sh.img_off + (long long)4 * dim * n;
+    double* v = base;
+    double* d2 = base + n;
+    double* srt = base + 2 * n;
+    unsigned short* lab = reinterpret_cast<unsigned short*>(base + 3 * n);
+    unsigned short* lab2 = lab + n;
+    float* out = cents + ((long long)s * L + dim) * K;
+    int* inf = info + (s * L + dim) * 4;
+
+    for (int j = tid; j < n; j += KT) v[j] = lat[(long long)(sh.img_off + j) * L + dim];
+    __syncthreads();
+
+    // ---- distinct shortcut (np.unique; quantizer.py:62-65)
+    {
+        double cur = INFINITY;
+        for (int j = tid; j < n; j += KT) cur = fmin(cur, v[j]);
+        cur = block_min(cur, S);
+        int cnt = 1;
+        if (tid == 0) S.distinct[0] = cur;
+        while (cnt <= K) {
+            double nx = INFINITY;
+            for (int j = tid; j < n; j += KT)
+                if (v[j] > cur) nx = fmin(nx, v[j]);
+            nx = block_min(nx, S);
+            if (nx == INFINITY) break;
+            if (tid == 0) S.distinct[cnt] = nx;
+            cur = nx;
+            ++cnt;
+        }
+        __syncthreads();
+        if (cnt <= K) {
+            if (tid < K) out[tid] = (float)S.distinct[tid < cnt ? tid : cnt - 1];
+            if (tid == 0) { inf[0] = 0; inf[1] = cnt; inf[2] = 0; inf[3] = 0; }
+            return;
+        }
+    }
+
+    // ---- pairwise plan for length-n sums (leaves reused for every d2.sum())
+    if (tid == 0) {
+        int c = 0;
+        enum_leaves(0, n, lstart, llen, c);
+        S.n_leaves = c;
+    }
+    __syncthreads();
+    const int nl_full = S.n_leaves;
+
+    // ---- k-means++ seeding (quantizer.py:66-76)
+    const long long f_idx = first_idx[s * L + dim];
+    const double* u_draw = draws + (long long)(s * L + dim) * (K - 1);
+    if (tid == 0) S.cent[0] = v[f_idx];
+    __syncthreads();
+    {
+        const double c0 = S.cent[0];
+        for (int j = tid; j < n; j += KT) {
+            double t = __dsub_rn(v[j], c0);
+            d2[j] = __dmul_rn(t, t);
+        }
+    }
+    __syncthreads();
+    int fallbacks = 0;
+    const int chunk = (n + KT - 1) / KT;
+    const int j_lo = min(n, tid * chunk), j_hi = min(n, j_lo + chunk);
+    const double delta = (16.0 * (n + 8)) * 1.1102230246251565e-16;
+    for (int i = 1; i < K; ++i) {
+        for (int l = tid; l < nl_full; l += KT)
+            leafsum[l] = pw_leaf([&](int q) { return d2[q]; }, lstart[l], llen[l]);
+        __syncthreads();
+        if (tid == 0) {
+            int nx = 0;
+            S.bcast_d = combine_leaves(leafsum, n, nx);
+        }
+        __syncthreads();
+        const double tot = S.bcast_d;
+        if (tot <= 0) {
+            if (tid == 0)
+                for (int q = i; q < K; ++q) S.cent[q] = S.cent[0];
+            __syncthreads();
+            break;
+        }
+        const double u = u_draw[i - 1];
+        // parallel scan of p = d2 / tot
+        double loc = 0.0;
+        for (int j = j_lo; j < j_hi; ++j) loc += __ddiv_rn(d2[j], tot);
+        double ctot;
+        double run = block_exscan(loc, &ctot, S);
+        int a_cnt = 0, b_cnt = 0;
+        for (int j = j_lo; j < j_hi; ++j) {
+            run += __ddiv_rn(d2[j], tot);
+            double rho = run / ctot;
+            if (rho * (1.0 + delta) <= u) ++a_cnt;
+            else if (rho * (1.0 - delta) > u) ++b_cnt;
+        }
+        a_cnt = block_sum_int(a_cnt, S);
+        b_cnt = block_sum_int(b_cnt, S);
+        if (tid == 0) {
+            int idx = a_cnt;
+            if (a_cnt + b_cnt != n) {
+                // exact sequential cumsum (numpy add.accumulate) -- rare
+                double c = 0.0;
+                for (int j = 0; j < n; ++j) c = __dadd_rn(c, __ddiv_rn(d2[j], tot));
+                double run2 = 0.0;
+                idx = 0;
+                for (int j = 0; j < n; ++j) {
+                    run2 = __dadd_rn(run2, __ddiv_rn(d2[j], tot));
+                    if (__ddiv_rn(run2, c) <= u) ++idx;
+                    else break;
+                }
+                ++fallbacks;
+            }
+            S.cent[i] = v[idx];
+        }
+        __syncthreads();
+        const double ci = S.cent[i];
+        for (int j = tid; j < n; j += KT) {
+            double t = __dsub_rn(v[j], ci);
+            double q = __dmul_rn(t, t);
+            d2[j] = d2[j] < q ? d2[j] : q;
+        }
+        __syncthreads();
+    }
+
+    // ---- Lloyd (quantizer.py:78-90)
+    for (int j = tid; j < n; j += KT) lab[j] = (unsigned short)nearest(v[j], S.cent, K);
+    __syncthreads();
+    int sweeps = 0;
+    const int wchunk = (n + KW - 1) / KW;
+    const int w_lo = min(n, w * wchunk), w_hi = min(n, w_lo + wchunk);
+    for (int it = 0; it < 25; ++it) {
+        ++sweeps;
+        // stable partition of members by label into srt
+        for (int q = tid; q < KW * K; q += KT) wcnt[q] = 0;
+        __syncthreads();
+        for (int j0 = w_lo; j0 < w_hi; j0 += 32) {
+            int j = j0 + lane;
+            unsigned key = j < w_hi ? lab[j] : 0xFFFFu;
+            unsigned m = __match_any_sync(0xffffffffu, key);
+            if (key != 0xFFFFu && (__ffs(m) - 1) == lane) wcnt[w * K + key] += __popc(m);
+            __syncwarp();
+        }
+        __syncthreads();
+        if (tid < K) {
+            int t = 0;
+            for (int q = 0; q < KW; ++q) t += wcnt[q * K + tid];
+            S.seg_cnt[tid] = t;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            int acc = 0;
+            for (int k = 0; k < K; ++k) { S.seg_start[k] = acc; acc += S.seg_cnt[k]; }
+        }
+        __syncthreads();
+        if (tid < K) {
+            int acc = S.seg_start[tid];
+            for (int q = 0; q < KW; ++q) {
+                int c = wcnt[q * K + tid];
+                wcnt[q * K + tid] = acc;
+                acc += c;
+            }
+        }
+        __syncthreads();
+        const unsigned lt = (1u << lane) - 1u;
+        for (int j0 = w_lo; j0 < w_hi; j0 += 32) {
+            int j = j0 + lane;
+            unsigned key = j < w_hi ? lab[j] : 0xFFFFu;
+            unsigned m = __match_any_sync(0xffffffffu, key);
+            int basepos = key != 0xFFFFu ? wcnt[w * K + key] : 0;
+            __syncwarp();
+            if (key != 0xFFFFu) {
+                srt[basepos + __popc(m & lt)] = v[j];
+                if ((__ffs(m) - 1) == lane) wcnt[w * K + key] = basepos + __popc(m);
+            }
+            __syncwarp();
+        }
+        __syncthreads();
+        // pairwise means of every live cluster
+        if (tid == 0) {
+            int c = 0;
+            for (int k = 0; k < K; ++k) {
+                S.first_leaf[k] = c;
+                if (S.seg_cnt[k] > 0) enum_leaves(S.seg_start[k], S.seg_cnt[k], lstart, llen, c);
+            }
+            S.first_leaf[K] = c;
+            S.n_leaves = c;
+        }
+        __syncthreads();
+        for (int l = tid; l < S.n_leaves; l += KT)
+            leafsum[l] = pw_leaf([&](int q) { return srt[q]; }, lstart[l], llen[l]);
+        if (tid < K) S.oldc[tid] = S.cent[tid];
+        __syncthreads();
+        if (tid < K) {
+            int c = S.seg_cnt[tid];
+            if (c > 0) {
+                int nx = 0;
+                double sm = combine_leaves(leafsum + S.first_leaf[tid], c, nx);
+                S.newc[tid] = __ddiv_rn(sm, (double)c);
+            } else {
+                S.newc[tid] = S.oldc[tid];
+            }
+        }
+        __syncthreads();
+        // dead clusters, in index order, against the partially updated table
+        for (int k = 0; k < K; ++k) {
+            if (S.seg_cnt[k] != 0) continue;
+            double bv = -INFINITY;
+            int bi = 0x7fffffff;
+            for (int j = tid; j < n; j += KT) {
+                int lj = lab[j];
+                double cj = lj < k ? S.newc[lj] : S.oldc[lj];
+                double dv = fabs(__dsub_rn(v[j], cj));
+                if (dv > bv || (dv == bv && j < bi)) { bv = dv; bi = j; }
+            }
+            int far = block_argmax(bv, bi, S);
+            if (tid == 0) S.newc[k] = v[far];
+            __syncthreads();
+        }
+        if (tid < K) S.cent[tid] = S.newc[tid];
+        __syncthreads();
+        int changed = 0;
+        for (int j = tid; j < n; j += KT) {
+            unsigned short nl = (unsigned short)nearest(v[j], S.cent, K);
+            lab2[j] = nl;
+            changed |= (nl != lab[j]);
+        }
+        changed = block_sum_int(changed, S);
+        if (!changed) break;
+        for (int j = tid; j < n; j += KT) lab[j] = lab2[j];
+        __syncthreads();
+    }
+
+    // ---- sorted float32 codebook row
+    if (tid == 0) {
+        for (int a = 1; a < K; ++a) {
+            double x = S.cent[a];
+            int b = a - 1;
+            while (b >= 0 && S.cent[b] > x) { S.cent[b + 1] = S.cent[b]; --b; }
+            S.cent[b + 1] = x;
+        }
+        inf[0] = 1; inf[1] = K; inf[2] = sweeps; inf[3] = fallbacks;
+    }
+    __syncthreads();
+    if (tid < K) out[tid] = (float)S.cent[tid];
+}
+
+}  // namespace
+
+extern "C" int mlk_kmeans(const double* lat, const MlkShard* shards_h, int32_t n_shards,
+                          int32_t L, int32_t K, const int64_t* first_idx, const double* draws,
+                          double* scratch, float* cents, int32_t* info, cudaStream_t stream) {
+    if (K < 2 || K > MLK_MAXK || L < 1 || L > MLK_MAXL) return MLK_ERR_CONFIG;
+    for (int s = 0; s < n_shards; ++s)
+        if (shards_h[s].n_img < 1 || shards_h[s].n_img > (1 << 18)) return MLK_ERR_DIM;
+    // shards_h is a host mirror; the kernel needs a device copy
+    MlkShard* d_sh = nullptr;
+    if (cudaMallocAsync(&d_sh, sizeof(MlkShard) * n_shards, stream) != cudaSuccess)
+        return MLK_ERR_CUDA;
+    cudaMemcpyAsync(d_sh, shards_h, sizeof(MlkShard) * n_shards, cudaMemcpyHostToDevice, stream);
+    size_t dyn = KM_MAX_LEAVES * (sizeof(double) + sizeof(int) + sizeof(short)) +
+                 (size_t)KW * MLK_MAXK * sizeof(int);
+    cudaFuncSetAttribute(k_kmeans, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+    k_kmeans<<<n_shards * L, KT, dyn, stream>>>(lat, d_sh, L, K,
+                                                reinterpret_cast<const long long*>(first_idx),
+                                                draws, scratch, cents, info);
+    cudaError_t e = cudaGetLastError();
+    cudaFreeAsync(d_sh, stream);
+    return e == cudaSuccess ? MLK_OK : MLK_ERR_CUDA;
+}

@@ -1,0 +1,137 @@
+// stage1.cu -- pass 1 over f0: AE encode (OpenBLAS order), moments, stats.
+//
+// Replaces autoencoder.encode_batch (autoencoder.py:99-103) and
+// qoi.compute_qoi_batch on the originals (pipeline.py:254, qoi.py:60-76).
+// One warp per histogram; the histogram is staged in shared memory once and
+// every per-image quantity of the pass is produced from that copy, so f0 is
+// read exactly once here (12,168 B per 39x39 histogram).
+#include "common.cuh"
+
+namespace {
+
+constexpr int S1_WARPS = 4;
+
+__host__ __device__ inline int panel_len(int rem) {
+    // OpenBLAS level3 K-panel rule, GEMM_Q = 384, GEMM_UNROLL_M = 16
+    const int Q = 384, U = 16;
+    if (rem >= 2 * Q) return Q;
+    if (rem > Q) return ((rem / 2 + U - 1) / U) * U;
+    return rem;
+}
+
+__global__ void __launch_bounds__(32 * S1_WARPS)
+k_stage1(const double* __restrict__ f0, const MlkShard* __restrict__ shards, int n_shards,
+         int total, MlkGrid g, const float* __restrict__ W, int L, double* __restrict__ lat,
+         double* __restrict__ stats, double* __restrict__ qoi) {
+    extern __shared__ double smem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int D = g.D;
+    double* buf = smem + warp * (D + 96);
+    double* chain = buf + D;  // 96 chain partials
+    const int img = blockIdx.x * S1_WARPS + warp;
+    if (img >= total) return;
+    const int s = find_shard(shards, n_shards, img);
+    const MlkShard sh = shards[s];
+    const double* x = shard_image(f0, sh, img - sh.img_off, D);
+
+    // ---- pass A: stage, extrema, sums, first moments
+    double mx = -INFINITY, mn = INFINITY, so = 0.0, soo = 0.0, n0 = 0.0, n1 = 0.0, n2 = 0.0;
+#pragma unroll 4
+    for (int j = lane; j < D; j += 32) {
+        double v = x[j];
+        buf[j] = v;
+        mx = np_max2(mx, v);
+        mn = np_min2(mn, v);
+        so += v;
+        soo = fma(v, v, soo);
+        double fv = v * __ldg(g.vol + j);
+        n0 += fv;
+        n1 = fma(fv, __ldg(g.vpar + j), n1);
+        n2 = fma(fv, __ldg(g.vperp2 + j), n2);
+    }
+    mx = warp_max(mx);
+    mn = warp_min(mn);
+    so = warp_sum(so);
+    soo = warp_sum(soo);
+    n0 = warp_sum(n0);
+    n1 = warp_sum(n1);
+    n2 = warp_sum(n2);
+    const double hm = 0.5 * g.mass;
+    double u = n1 / n0;
+    double tp = hm * n2 / n0;
+    double n3 = 0.0;
+    for (int j = lane; j < D; j += 32) {
+        double dv = __ldg(g.vpar + j) - u;
+        n3 = fma(buf[j] * __ldg(g.vol + j), dv * dv, n3);
+    }
+    n3 = warp_sum(n3);
+    double tl = hm * n3 / n0;
+    if (!(n0 > 0)) u = tp = tl = __longlong_as_double(0x7ff8000000000000ll);
+    if (lane == 0) {
+        double4* st = reinterpret_cast<double4*>(stats) + img;
+        *st = make_double4(mx, mn, so, soo);
+        double4* q = reinterpret_cast<double4*>(qoi) + img;
+        *q = make_double4(n0, u, tp, tl);
+    }
+
+    // ---- normalise in place: xn = (x - mean) / std (numpy, two roundings)
+    for (int j = lane; j < D; j += 32) buf[j] = __ddiv_rn(__dsub_rn(buf[j], sh.mean), sh.std);
+    __syncwarp();
+
+    // ---- latents in the host BLAS order
+    const float* Ws = W + sh.w_off;
+    if (sh.small_blas) {
+        // 8 interleaved FMA accumulators per latent, tree-combined
+        for (int c = lane; c < L * 8; c += 32) {
+            const int k = c >> 3, a = c & 7;
+            const float* wk = Ws + (long long)k * D;
+            double acc = 0.0;
+            for (int j = a; j < D; j += 8) acc = __fma_rn(buf[j], (double)__ldg(wk + j), acc);
+            chain[c] = acc;
+        }
+        __syncwarp();
+        if (lane < L) {
+            const double* r = chain + lane * 8;
+            double t = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                                 __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+            lat[(long long)img * L + lane] = t;
+        }
+    } else {
+        int np_ = 0;
+        for (int j0 = 0; j0 < D; j0 += panel_len(D - j0)) ++np_;
+        for (int c = lane; c < L * np_; c += 32) {
+            const int k = c / np_, p = c % np_;
+            int j0 = 0;
+            for (int q = 0; q < p; ++q) j0 += panel_len(D - j0);
+            const int j1 = j0 + panel_len(D - j0);
+            const float* wk = Ws + (long long)k * D;
+            double acc = 0.0;
+#pragma unroll 4
+            for (int j = j0; j < j1; ++j) acc = __fma_rn(buf[j], (double)__ldg(wk + j), acc);
+            chain[c] = acc;
+        }
+        __syncwarp();
+        if (lane < L) {
+            double t = chain[lane * np_];
+            for (int p = 1; p < np_; ++p) t = __dadd_rn(t, chain[lane * np_ + p]);
+            lat[(long long)img * L + lane] = t;
+        }
+    }
+}
+
+}  // namespace
+
+extern "C" int mlk_stage1(const double* f0, const MlkShard* shards, int32_t n_shards,
+                          int32_t total, const MlkGrid* grid_h, const float* W, int32_t L,
+                          double* lat, double* stats, double* qoi, cudaStream_t stream) {
+    if (L < 1 || L > MLK_MAXL || grid_h->D > MLK_MAX_D) return MLK_ERR_DIM;
+    if (total <= 0) return MLK_OK;
+    // 96 chain slots: L*8 (small path) or L*ceil(D/384)+1 (blocked path)
+    if (L * ((grid_h->D + 383) / 384 + 1) > 96) return MLK_ERR_DIM;
+    size_t sm = (size_t)S1_WARPS * (grid_h->D + 96) * sizeof(double);
+    cudaFuncSetAttribute(k_stage1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    dim3 grid((total + S1_WARPS - 1) / S1_WARPS);
+    k_stage1<<<grid, 32 * S1_WARPS, sm, stream>>>(f0, shards, n_shards, total, *grid_h, W, L,
+                                                   lat, stats, qoi);
+    return cudaGetLastError() == cudaSuccess ? MLK_OK : MLK_ERR_CUDA;
+}

@@ -1,0 +1,630 @@
+"""Device orchestration of the per-histogram compress / decompress path.
+
+One call processes every shard a rank owns: each kernel launch covers all of
+them (the shard id of an image is found from the shard table).  The host
+only (a) precomputes exact tables and the PCG64 draws of the k-means
+seeding, (b) drives the error-bound bisection with numpy's own log/exp, and
+(c) assembles the byte sections around device-produced payloads.
+
+Reference map: pipeline._compress_shard (pipeline.py:196-320) and
+pipeline._decode_shard (pipeline.py:397-427).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import functools
+import math
+import struct
+import zlib
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import MlkGrid, MlkNewton, MlkShard, call
+from .decomp import mix_seed
+from .errors import ConfigError, FormatError, SizeMismatchError
+
+SPAN = 2.0 ** -20
+STEPS = 20
+LOOKAHEAD = 4          # bisection levels answered per probe launch (2**4 - 1 bounds)
+_PAYLOAD_HEAD = struct.Struct("<BHHd")
+
+
+# ---------------------------------------------------------------------------
+# host BLAS order (the decode bracketing the reference inherits from numpy)
+
+@functools.lru_cache(maxsize=None)
+def decode_tree_cols(d: int, l: int) -> bytes:
+    """Columns where numpy/OpenBLAS sums the L=4 decode products as
+    (p0+p1)+(p2+p3) in its blocked kernel (autoencoder.py:109); probed once."""
+    out = np.zeros(d, dtype=np.uint8)
+    if l != 4:
+        return out.tobytes()
+    rng = np.random.default_rng(20221221)
+    n = max(512, int(1e6 // (l * d)) + 64)
+    w = rng.standard_normal((l, d)).astype(np.float32).astype(np.float64)
+    z = (rng.standard_normal((n, l)) * 37.0).astype(np.float32).astype(np.float64)
+    ref = z @ w
+    p = [z[:, k:k + 1] * w[k][None, :] for k in range(4)]
+    seq = ((p[0] + p[1]) + p[2]) + p[3]
+    tree = (p[0] + p[1]) + (p[2] + p[3])
+    for j in np.flatnonzero((seq != ref).any(axis=0)):
+        if (tree[:, j] == ref[:, j]).all():
+            out[j] = 1
+    return out.tobytes()
+
+
+# ---------------------------------------------------------------------------
+# grid tables
+
+class DeviceGrid:
+    """Exact grid tables on device (lagrange.py:68-80, 163-173, 199-204)."""
+
+    def __init__(self, grid, device, latent_dim: int = 4):
+        r, c = grid.rows, grid.cols
+        self.D = r * c
+        vol = grid.vol.reshape(-1)
+        vpar = np.broadcast_to(grid.v_par, (r, c)).reshape(-1)
+        vperp = np.broadcast_to(grid.v_perp[:, None], (r, c)).reshape(-1)
+        half_m = 0.5 * grid.mass
+        rows = [vol, vol * vpar, half_m * vol * vperp ** 2]
+        scales = [float(np.max(np.abs(x))) for x in rows]
+        ash = np.concatenate([x / s for x, s in zip(rows, scales)])
+        tc = np.frombuffer(decode_tree_cols(self.D, latent_dim), dtype=np.uint8)
+
+        def dev(a, dt=torch.float64):
+            return torch.from_numpy(np.ascontiguousarray(a)).to(device=device, dtype=dt)
+
+        self.t = dict(vol=dev(vol), vpar=dev(vpar), vperp2=dev(vperp ** 2),
+                      hmvol=dev(half_m * vol), ash=dev(ash), tree=dev(tc.copy(), torch.uint8))
+        self.mass = grid.mass
+        self.struct = MlkGrid(rows=r, cols=c, D=self.D, pad=0, mass=grid.mass,
+                              vol=self.t["vol"].data_ptr(), vpar=self.t["vpar"].data_ptr(),
+                              vperp2=self.t["vperp2"].data_ptr(),
+                              hmvol=self.t["hmvol"].data_ptr(), ash=self.t["ash"].data_ptr(),
+                              tree_cols=self.t["tree"].data_ptr(), s0=scales[0], s1=scales[1],
+                              s2=scales[2])
+
+    @property
+    def addr(self) -> int:
+        return ctypes.addressof(self.struct)
+
+
+# ---------------------------------------------------------------------------
+# error-bound search (residual.py:129-173) as an explicit state machine so a
+# whole subtree of candidate bounds can be probed in one launch
+
+@dataclass(frozen=True)
+class _Search:
+    stage: str            # "hi" | "bis" | "low" | "done"
+    eb_hi: float
+    lo: object = None
+    hi: object = None
+    best: object = None
+    step: int = 0
+    result: tuple = None
+
+    def query(self):
+        if self.stage == "hi":
+            return self.eb_hi
+        if self.stage == "bis":
+            return np.exp(0.5 * (self.lo + self.hi))
+        if self.stage == "low":
+            return self.eb_hi * SPAN
+        return None
+
+    def advance(self, ok: bool) -> "_Search":
+        if self.stage == "hi":
+            if ok:
+                return _Search("done", self.eb_hi, result=(self.eb_hi, False))
+            return _Search("bis", self.eb_hi, np.log(self.eb_hi * SPAN), np.log(self.eb_hi),
+                           None, 0)._settle()
+        if self.stage == "bis":
+            mid = 0.5 * (self.lo + self.hi)
+            if ok:
+                nxt = _Search("bis", self.eb_hi, mid, self.hi, np.exp(mid), self.step + 1)
+            else:
+                nxt = _Search("bis", self.eb_hi, self.lo, mid, self.best, self.step + 1)
+            return nxt._settle()
+        if self.stage == "low":
+            low = self.eb_hi * SPAN
+            return _Search("done", self.eb_hi, result=(float(low), not ok))
+        raise AssertionError("search already done")
+
+    def _settle(self) -> "_Search":
+        if self.stage == "bis" and self.step == STEPS:
+            if self.best is not None:
+                return _Search("done", self.eb_hi, result=(float(self.best), False))
+            return _Search("low", self.eb_hi)
+        return self
+
+
+def _search_tree(root: _Search, depth: int):
+    """Pre-order list of the states queried in the next `depth` decisions.
+
+    Each entry is [state, child_if_accepted, child_if_rejected] where a child
+    is an int (another entry) or a _Search left for the next round."""
+    nodes = []
+
+    def build(st, d):
+        if st.stage == "done" or d == depth:
+            return st
+        i = len(nodes)
+        nodes.append([st, None, None])
+        nodes[i][1] = build(st.advance(True), d + 1)
+        nodes[i][2] = build(st.advance(False), d + 1)
+        return i
+
+    return nodes, build(root, 0)
+
+
+# ---------------------------------------------------------------------------
+# compress
+
+@dataclass
+class ShardWork:
+    """A shard as the device sees it plus its model."""
+
+    wid: int
+    n_img: int
+    base: int              # element offset of image 0 in the rank's f0 buffer
+    plane_stride: int
+    block: int
+    model: object          # AEModel
+
+
+@dataclass
+class CompressOut:
+    """Everything the section/blob assembly and the report need."""
+
+    specs: list
+    codes: np.ndarray           # (total, L) uint8
+    cents: np.ndarray           # (S, L, K) float32
+    flags: np.ndarray           # (total,) uint8
+    lam: np.ndarray             # (total, 4)
+    qst: np.ndarray             # (total, 4)
+    status: np.ndarray
+    iters: np.ndarray
+    ferr: np.ndarray
+    fqoi: np.ndarray
+    fsse: np.ndarray
+    qoi: np.ndarray
+    stats: np.ndarray
+    sel_count: np.ndarray
+    sel: list                   # per shard ascending selected indices
+    eb: list
+    lossless: list
+    payloads: list              # per shard list of payload bytes
+    kmeans_info: np.ndarray
+    timings: dict = field(default_factory=dict)
+
+
+class Timer:
+    def __init__(self, enabled=True):
+        self.enabled = enabled
+        self.marks = []
+
+    def mark(self, name):
+        if self.enabled:
+            ev = torch.cuda.Event(enable_timing=True)
+            ev.record()
+            self.marks.append((name, ev))
+
+    def result(self):
+        if not self.enabled or len(self.marks) < 2:
+            return {}
+        torch.cuda.synchronize()
+        out = {}
+        for (n0, e0), (_, e1) in zip(self.marks, self.marks[1:]):
+            out[n0] = out.get(n0, 0.0) + e0.elapsed_time(e1) / 1e3
+        return out
+
+
+def _shard_table(specs, D, L):
+    arr = (MlkShard * len(specs))()
+    off = 0
+    for i, sp in enumerate(specs):
+        small = sp.n_img * L * D <= 1e6
+        arr[i] = MlkShard(base=sp.base, plane_stride=sp.plane_stride, block=sp.block,
+                          n_img=sp.n_img, img_off=off, small_blas=int(small),
+                          mean=float(sp.model.norm_mean), std=float(sp.model.norm_std), eb=0.0,
+                          lossless=0, w_off=i * L * D)
+        off += sp.n_img
+    return arr
+
+
+def _upload_shards(arr, device):
+    raw = np.frombuffer(bytes(arr), dtype=np.uint8).copy()
+    return torch.from_numpy(raw).to(device)
+
+
+def _gram(models):
+    rows = []
+    for m in models:
+        w = m.weights.astype(np.float64)
+        rows.append(np.concatenate([(w @ w.T).reshape(-1), w.sum(axis=1),
+                                    np.sqrt((w * w).sum(axis=1)), np.abs(w).max(axis=1)]))
+    return np.stack(rows)
+
+
+def kmeans_draws(n: int, k: int, seed: int):
+    """The PCG64 draws quantizer.kmeans_1d consumes (quantizer.py:68,77)."""
+    g = np.random.Generator(np.random.PCG64(seed))
+    first = int(g.integers(n))
+    return first, [g.random() for _ in range(k - 1)]
+
+
+def compress_device(f0: torch.Tensor, specs, dgrid: DeviceGrid, cfg, timer: Timer | None = None,
+                    zlib_level: int = 6) -> CompressOut:
+    """Run stages 2-5 of pipeline._compress_shard for every shard in `specs`.
+
+    f0 is a flat float64 CUDA tensor holding the rank's histograms; shard s's
+    image j lives at base + (j // block) * plane_stride + (j % block) * D.
+    """
+    dev = f0.device
+    D, L, K = dgrid.D, cfg.latent_dim, 2 ** cfg.pq_bits
+    S = len(specs)
+    timer = timer or Timer(False)
+    for sp in specs:
+        if sp.model.latent_dim != L or sp.model.input_dim != D:
+            raise ConfigError("shard model does not match the configuration/grid")
+    table = _shard_table(specs, D, L)
+    sh_d = _upload_shards(table, dev)
+    total = sum(sp.n_img for sp in specs)
+    W = torch.from_numpy(np.stack([sp.model.weights for sp in specs]).astype(np.float32)).to(dev)
+    f64 = dict(dtype=torch.float64, device=dev)
+
+    timer.mark("encode")
+    lat = torch.empty((total, L), **f64)
+    stats = torch.empty((total, 4), **f64)
+    qoi = torch.empty((total, 4), **f64)
+    call("mlk_stage1", f0, sh_d, S, total, dgrid.addr, W, L, lat, stats, qoi)
+
+    timer.mark("pq")
+    first, draws = [], []
+    for sp in specs:
+        seed = mix_seed(cfg.seed, sp.wid)
+        for d in range(L):
+            f, u = kmeans_draws(sp.n_img, K, seed + d)
+            first.append(f)
+            draws.extend(u)
+    first_d = torch.tensor(first, dtype=torch.int64, device=dev)
+    draws_d = torch.tensor(draws, **f64)
+    scratch = torch.empty(4 * L * total, **f64)
+    cents = torch.empty((S, L, K), dtype=torch.float32, device=dev)
+    kinfo = torch.zeros((S, L, 4), dtype=torch.int32, device=dev)
+    call("mlk_kmeans", lat, ctypes.addressof(table), S, L, K, first_d, draws_d, scratch, cents,
+         kinfo)
+    del scratch
+
+    timer.mark("find_eb")
+    gram = torch.from_numpy(_gram([sp.model for sp in specs])).to(dev)
+    codes = torch.empty((total, L), dtype=torch.uint8, device=dev)
+    flags = torch.empty(total, dtype=torch.uint8, device=dev)
+    err_a = torch.empty(total, **f64)
+    rbound = torch.empty(total, **f64)
+    call("mlk_select", lat, stats, sh_d, S, total, dgrid.addr, cents, L, K, gram, cfg.tau, codes,
+         flags, err_a, rbound)
+    err_x = torch.empty(total, **f64)
+    call("mlk_recheck", f0, stats, sh_d, S, total, dgrid.addr, W, L, cents, K, codes, cfg.tau,
+         flags, err_x)
+    i32 = dict(dtype=torch.int32, device=dev)
+    sel = torch.empty(total, **i32)
+    sel_rank = torch.empty(total, **i32)
+    sel_rng = torch.empty(total, **i32)
+    sel_cnt = torch.empty(S, **i32)
+    eb_hi = torch.empty(S, **f64)
+    call("mlk_compact", flags, stats, sh_d, S, cfg.tau, sel, sel_rank, sel_rng, sel_cnt, eb_hi)
+    cnt_h = sel_cnt.cpu().numpy()
+    ebhi_h = eb_hi.cpu().numpy()
+
+    # ---- error-bound search, LOOKAHEAD levels per launch
+    states = []
+    for s in range(S):
+        if cnt_h[s] == 0:
+            states.append(None)
+            continue
+        eb_hi_s = float(ebhi_h[s])
+        if eb_hi_s <= 0:
+            states.append(_Search("done", eb_hi_s, result=(eb_hi_s, True)))
+        else:
+            states.append(_Search("hi", eb_hi_s))
+    n_cand = 2 ** LOOKAHEAD - 1
+    rounds = 0
+    while any(st is not None and st.stage != "done" for st in states):
+        rounds += 1
+        trees, cand = [], np.zeros((S, n_cand))
+        act = np.zeros(S + 1, dtype=np.int32)
+        for s, st in enumerate(states):
+            tree = _search_tree(st, LOOKAHEAD) if (st is not None and st.stage != "done") \
+                else ([], st)
+            trees.append(tree)
+            for c, nd in enumerate(tree[0]):
+                cand[s, c] = float(nd[0].query())
+            act[s + 1] = act[s] + (int(cnt_h[s]) if tree[0] else 0)
+        fail = torch.zeros((S, n_cand), **i32)
+        cand_d = torch.from_numpy(cand).to(dev)
+        act_d = torch.from_numpy(act).to(dev)
+        call("mlk_probe", f0, stats, sh_d, S, dgrid.addr, W, L, cents, K, codes, sel_rng, act_d,
+             int(act[-1]), rbound, cfg.tau, cand_d, n_cand, fail)
+        fail_h = fail.cpu().numpy()
+        for s, (nodes, ref) in enumerate(trees):
+            if not nodes:
+                continue
+            while isinstance(ref, int):
+                ref = nodes[ref][1] if fail_h[s, ref] == 0 else nodes[ref][2]
+            states[s] = ref
+    eb = [0.0] * S
+    lossless = [False] * S
+    for s, st in enumerate(states):
+        if st is not None:
+            eb[s], lossless[s] = st.result
+    for s in range(S):
+        table[s].eb = eb[s]
+        table[s].lossless = int(lossless[s])
+    sh_d = _upload_shards(table, dev)
+
+    timer.mark("newton")
+    slot_base_h = np.concatenate([[0], np.cumsum(cnt_h)[:-1]]).astype(np.int32)
+    n_sel = int(cnt_h.sum())
+    vcap = ((10 * D + 15) // 16) * 16
+    varint = torch.empty(max(1, n_sel) * vcap, dtype=torch.uint8, device=dev)
+    vlen = torch.zeros(max(1, n_sel), dtype=torch.int64, device=dev)
+    slot_base = torch.from_numpy(slot_base_h).to(dev)
+    opts = MlkNewton(step=cfg.newton.step, max_iter=cfg.newton.max_iter,
+                     retry=int(cfg.newton.retry), tol=cfg.newton.tol, floor=cfg.newton.floor,
+                     retry_step=cfg.newton.retry_step, retry_max_iter=cfg.newton.retry_max_iter,
+                     lam_f32=int(cfg.lambda_precision == "f32"), tau=cfg.tau)
+    lam = torch.empty((total, 4), **f64)
+    qst = torch.empty((total, 4), **f64)
+    status = torch.empty(total, **i32)
+    iters = torch.empty(total, **i32)
+    ferr = torch.empty(total, **f64)
+    fqoi = torch.empty((total, 4), **f64)
+    fsse = torch.empty(total, **f64)
+    errf = torch.zeros(1, **i32)
+    call("mlk_project", f0, stats, qoi, sh_d, S, total, dgrid.addr, W, L, cents, K, codes,
+         sel_rank, slot_base, ctypes.addressof(opts), flags, lam, qst, status, iters, ferr, fqoi,
+         fsse, varint, vcap, vlen, errf)
+
+    timer.mark("pack")
+    if int(errf.item()) != 0:
+        raise ConfigError("error bound too small for this residual range")
+    sel_h = sel.cpu().numpy()
+    payloads = []
+    vlen_h = vlen.cpu().numpy()
+    var_h = varint.view(-1).cpu().numpy() if n_sel else None
+    sel_lists = []
+    for s, sp in enumerate(specs):
+        off = table[s].img_off
+        idx = sel_h[off:off + cnt_h[s]].copy()
+        sel_lists.append(idx)
+        pl = []
+        head = _PAYLOAD_HEAD.pack(1 if lossless[s] else 0, dgrid.struct.rows,
+                                  dgrid.struct.cols, 0.0 if lossless[s] else eb[s])
+        for r in range(cnt_h[s]):
+            slot = slot_base_h[s] + r
+            raw = var_h[slot * vcap: slot * vcap + vlen_h[slot]].tobytes()
+            pl.append(head + zlib.compress(raw, zlib_level))
+        payloads.append(pl)
+    packed = []
+    codes16 = codes.to(torch.int16).view(torch.uint16) if hasattr(torch, "uint16") else None
+    bad = torch.zeros(1, **i32)
+    for s, sp in enumerate(specs):
+        off = table[s].img_off
+        nbytes = (sp.n_img * L * cfg.pq_bits + 7) // 8
+        buf = torch.empty(max(1, nbytes), dtype=torch.uint8, device=dev)
+        c16 = codes[off:off + sp.n_img].reshape(-1).to(torch.int32).to(torch.int16)
+        call("mlk_pack_indices", c16, sp.n_img * L, cfg.pq_bits, buf, bad)
+        packed.append(buf[:nbytes].cpu().numpy().tobytes())
+    out = CompressOut(
+        specs=specs, codes=codes.cpu().numpy(), cents=cents.cpu().numpy(),
+        flags=flags.cpu().numpy(), lam=lam.cpu().numpy(), qst=qst.cpu().numpy(),
+        status=status.cpu().numpy(), iters=iters.cpu().numpy(), ferr=ferr.cpu().numpy(),
+        fqoi=fqoi.cpu().numpy(), fsse=fsse.cpu().numpy(), qoi=qoi.cpu().numpy(),
+        stats=stats.cpu().numpy(), sel_count=cnt_h, sel=sel_lists, eb=eb, lossless=lossless,
+        payloads=payloads, kmeans_info=kinfo.cpu().numpy())
+    out.timings = {"probe_rounds": rounds}
+    out.codes_packed = packed
+    out.rows_cols = (dgrid.struct.rows, dgrid.struct.cols)
+    return out
+
+
+
+
+# ---------------------------------------------------------------------------
+# decompress (pipeline.py:397-440)
+
+def _unzigzag_host(z):
+    return ((z >> np.uint64(1)) ^ (np.uint64(0) - (z & np.uint64(1)))).astype(np.int64)
+
+
+def decompress_device(preamble, shards, blobs, dev) -> np.ndarray:
+    """Decode every shard blob on `dev`; returns the (P, N, R, C) array."""
+    from .autoencoder import AEModel
+    from .container import read_shard
+    from .quantizer import PQCodebook
+
+    P, N = preamble.n_planes, preamble.n_nodes
+    rows, cols = preamble.grid.rows, preamble.grid.cols
+    D = rows * cols
+    metas = []
+    for shard, blob in zip(shards, blobs):
+        sb = read_shard(blob)
+        h = sb.header
+        if h.n_images != len(shard.members):
+            raise FormatError("shard image count disagrees with the partition")
+        if (h.img_rows, h.img_cols) != (rows, cols):
+            raise FormatError("shard image dims disagree with the archive grid")
+        metas.append((shard, sb))
+    L = metas[0][1].header.latent_dim
+    bits = metas[0][1].header.pq_bits
+    K = 1 << bits
+    if any(sb.header.latent_dim != L or sb.header.pq_bits != bits for _, sb in metas):
+        raise FormatError("mixed latent/codebook shapes across shards are not supported")
+    dgrid = DeviceGrid(preamble.grid, dev, L)
+    models, cents, codes_l, lamq_l = [], [], [], []
+    res_slot_l, res_codes_l, res_eb_l, res_mode_l = [], [], [], []
+    exc_slot_l, exc_img_l = [], []
+    n_res = n_exc = 0
+    for shard, sb in metas:
+        h, sec = sb.header, sb.sections
+        n = h.n_images
+        models.append(AEModel.from_bytes(sec["weights"], L, D))
+        cents.append(PQCodebook.from_bytes(sec["pq_table"], L, K).centroids)
+        total_codes = n * L
+        if len(sec["codes"]) != (total_codes * bits + 7) // 8:
+            raise SizeMismatchError(f"code stream is {len(sec['codes'])} bytes, expected "
+                                    f"{(total_codes * bits + 7) // 8}")
+        cbuf = torch.from_numpy(np.frombuffer(sec["codes"], dtype=np.uint8).copy()).to(dev)
+        idx = torch.empty(total_codes, dtype=torch.int16, device=dev)
+        call("mlk_unpack_indices", cbuf, total_codes, bits, idx)
+        codes_l.append(idx)
+        dt = "<f4" if h.lambda_precision == 4 else "<f8"
+        if len(sec["lambdas"]) != n * 8 * h.lambda_precision:
+            raise FormatError("lambda section length mismatch")
+        lamq_l.append(np.frombuffer(sec["lambdas"], dtype=dt).reshape(n, 8).astype(np.float64))
+        slot = np.full(n, -1, dtype=np.int32)
+        from .pipeline import _parse_exceptions, _parse_residuals
+        for i, payload in _parse_residuals(sec["residuals"], n, rows, cols):
+            if len(payload) < _PAYLOAD_HEAD.size:
+                raise FormatError("residual payload shorter than its header")
+            mode, r, c, eb = _PAYLOAD_HEAD.unpack_from(payload, 0)
+            if (r, c) != (rows, cols):
+                raise FormatError("residual payload dims do not match the shard")
+            if mode not in (0, 1):
+                raise FormatError(f"unknown residual payload mode {mode}")
+            try:
+                raw = zlib.decompress(payload[_PAYLOAD_HEAD.size:])
+            except zlib.error as exc:
+                raise FormatError(f"corrupt residual stream: {exc}") from exc
+            res_codes_l.append(raw)
+            res_eb_l.append(eb)
+            res_mode_l.append(mode)
+            slot[i] = n_res
+            n_res += 1
+        res_slot_l.append(slot)
+        eidx, eimg = _parse_exceptions(sec["exceptions"], D)
+        es = np.full(n, -1, dtype=np.int32)
+        es[eidx] = np.arange(n_exc, n_exc + len(eidx), dtype=np.int32)
+        n_exc += len(eidx)
+        exc_slot_l.append(es)
+        exc_img_l.append(eimg)
+    # varint streams -> device decode
+    i64 = dict(dtype=torch.int64, device=dev)
+    if n_res:
+        lens = np.array([len(r) for r in res_codes_l], dtype=np.int64)
+        offs = np.concatenate([[0], np.cumsum(lens)[:-1]]).astype(np.int64)
+        blob = np.frombuffer(b"".join(res_codes_l), dtype=np.uint8).copy()
+        raw_d = torch.from_numpy(blob if blob.size else np.zeros(1, np.uint8)).to(dev)
+        vals = torch.empty(n_res * D, dtype=torch.int64, device=dev)
+        consumed = torch.empty(n_res, **i64)
+        call("mlk_varint_decode_batch", raw_d, torch.from_numpy(offs).to(dev),
+             torch.from_numpy(lens).to(dev), n_res,
+             torch.full((n_res,), D, **i64), vals,
+             torch.arange(0, n_res * D, D, **i64), consumed)
+        con = consumed.cpu().numpy()
+        if np.any(con == -1):
+            raise FormatError("varint stream truncated")
+        if np.any(con == -2):
+            raise FormatError("varint value exceeds 64 bits")
+        if np.any(con != lens):
+            raise FormatError("residual stream has trailing bytes")
+    else:
+        vals = torch.zeros(1, dtype=torch.int64, device=dev)
+    specs = shard_layout(shards, models, N, D)
+    table = _shard_table(specs, D, L)
+    sh_d = _upload_shards(table, dev)
+    total = sum(sp.n_img for sp in specs)
+    W = torch.from_numpy(np.stack([m.weights for m in models]).astype(np.float32)).to(dev)
+    cents_d = torch.from_numpy(np.stack(cents)).to(dev)
+    codes_d = torch.cat(codes_l).to(torch.uint8)
+    lamq = torch.from_numpy(np.concatenate(lamq_l)).to(dev)
+    res_slot = torch.from_numpy(np.concatenate(res_slot_l)).to(dev)
+    res_eb = torch.tensor(res_eb_l or [0.0], dtype=torch.float64, device=dev)
+    res_mode = torch.tensor(res_mode_l or [0], dtype=torch.uint8, device=dev)
+    exc_slot = torch.from_numpy(np.concatenate(exc_slot_l)).to(dev)
+    exc_img = torch.from_numpy(np.concatenate(exc_img_l) if n_exc else np.zeros((1, D))).to(dev)
+    out = torch.empty(P * N * D + 2, dtype=torch.float64, device=dev)
+    call("mlk_decode", sh_d, len(specs), total, dgrid.addr, W, L, cents_d, K, codes_d, res_slot,
+         vals, res_eb, res_mode, lamq, exc_slot, exc_img, 1e-12, out)
+    return out[:P * N * D].cpu().numpy().reshape(P, N, rows, cols)
+
+
+def shard_layout(shards, models, n_nodes, D, node_lo=0):
+    out = []
+    for sh, m in zip(shards, models):
+        (p0, p1), (x0, x1) = sh.planes_range, sh.nodes_range
+        out.append(ShardWork(wid=sh.worker_id, n_img=len(sh.members),
+                             base=(p0 * n_nodes + (x0 - node_lo)) * D,
+                             plane_stride=n_nodes * D, block=x1 - x0, model=m))
+    return out
+
+
+def evaluate_device(orig, rec, preamble, blobs, dev) -> dict:
+    """Per-image AE errors, final errors and moments for evaluate()."""
+    from .autoencoder import AEModel
+    from .container import read_shard
+    from .decomp import partition
+    from .quantizer import PQCodebook
+
+    P, N = orig.n_planes, orig.n_nodes
+    D = orig.grid.rows * orig.grid.cols
+    total = P * N
+    dgrid = DeviceGrid(orig.grid, dev)
+    a = upload_flat(orig.data, dev)
+    b = upload_flat(rec.data, dev)
+    f64 = dict(dtype=torch.float64, device=dev)
+    err = torch.empty(total, **f64)
+    sse = torch.empty(total, **f64)
+    qa = torch.empty((total, 4), **f64)
+    qb = torch.empty((total, 4), **f64)
+    ext = torch.empty((total, 2), **f64)
+    call("mlk_compare", a, b, total, dgrid.addr, err, sse, qa, qb, ext)
+    # AE-only errors through the exact recheck kernel
+    shards = partition(P, N, preamble.n_shards, preamble.decomp_mode)
+    models, cents, codes_l = [], [], []
+    L = K = bits = None
+    for blob in blobs:
+        sb = read_shard(blob)
+        h = sb.header
+        L, bits = h.latent_dim, h.pq_bits
+        K = 1 << bits
+        models.append(AEModel.from_bytes(sb.sections["weights"], L, D))
+        cents.append(PQCodebook.from_bytes(sb.sections["pq_table"], L, K).centroids)
+        cb = torch.from_numpy(np.frombuffer(sb.sections["codes"], np.uint8).copy()).to(dev)
+        idx = torch.empty(h.n_images * L, dtype=torch.int16, device=dev)
+        call("mlk_unpack_indices", cb, h.n_images * L, bits, idx)
+        codes_l.append(idx)
+    specs = shard_layout(shards, models, N, D)
+    table = _shard_table(specs, D, L)
+    sh_d = _upload_shards(table, dev)
+    W = torch.from_numpy(np.stack([m.weights for m in models]).astype(np.float32)).to(dev)
+    cents_d = torch.from_numpy(np.stack(cents)).to(dev)
+    codes_d = torch.cat(codes_l).to(torch.uint8)
+    stats = torch.zeros((total, 4), **f64)
+    order = np.concatenate([np.fromiter((p * N + x for p, x in sh.members), dtype=np.int64)
+                            for sh in shards])
+    order_d = torch.from_numpy(order).to(dev)
+    stats[:, 0] = ext[order_d, 0]
+    stats[:, 1] = ext[order_d, 1]
+    flags = torch.full((total,), 4, dtype=torch.uint8, device=dev)
+    ae = torch.empty(total, **f64)
+    call("mlk_recheck", a, stats, sh_d, len(specs), total, dgrid.addr, W, L, cents_d, K,
+         codes_d, preamble.tau, flags, ae)
+    span = float(ext[:, 0].max() - ext[:, 1].min())
+    pd = float(np.sqrt(float(sse.sum()) / orig.data.size) / span) if span > 0 else 0.0
+    ae_h = np.empty(total)
+    ae_h[order] = ae.cpu().numpy()
+    return {"per_image": err.cpu().numpy(), "q_orig": qa.cpu().numpy(),
+            "q_rec": qb.cpu().numpy(), "pd_nrmse": pd, "ae_err": ae_h}
+
+
+def upload_flat(data: np.ndarray, dev) -> torch.Tensor:
+    n = data.size
+    buf = torch.empty(n + 2, dtype=torch.float64, device=dev)
+    buf[:n].copy_(torch.from_numpy(np.ascontiguousarray(data).reshape(-1)))
+    return buf

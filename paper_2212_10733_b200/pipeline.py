@@ -1,0 +1,331 @@
+"""Public compress / decompress / evaluate (reference pipeline.py:29-491).
+
+Same signatures, same archive bytes, same report fields as the reference
+`mlk` package; every per-histogram stage runs on the current CUDA device
+(``engine.compress_device`` / ``engine.decompress_device``).  Shard count
+is a configuration value; the worker count only sets host threads, so
+archives are identical for any worker or GPU count (pipeline.py:4-7).
+"""
+
+from __future__ import annotations
+
+import hashlib
+import json
+import struct
+import time
+from dataclasses import asdict, dataclass, field
+
+import numpy as np
+import torch
+
+from . import engine
+from ._lib import F_EXCEPTION, F_EXC_OVERFLOW, F_NONFINITE, F_SELECTED
+from .autoencoder import AEModel
+from .container import SCHEME_FULL, ArchivePreamble, read_archive, read_shard, write_archive, \
+    write_shard
+from .decomp import SelectionScheme, partition
+from .errors import ConfigError, FormatError, SizeMismatchError
+from .fdata import FDataset, dataset_nbytes
+from .lagrange import NewtonOptions, NewtonStatus
+from .qoi import ErrorReport, compression_ratio, qoi_nrmse_from_moments
+
+__all__ = ["PipelineConfig", "TimestepState", "compress", "decompress", "evaluate",
+           "run_timesteps", "QOI_GATES"]
+
+QOI_GATES = {"f32": 1e-8, "f64": 1e-12}
+_STAGES = ("train", "encode", "pq", "find_eb", "newton", "pack", "other")
+
+
+@dataclass(frozen=True)
+class PipelineConfig:
+    """Field-for-field the reference config (pipeline.py:36-89) so digests match."""
+
+    workers: int = 4
+    shards: int = 2
+    mode: str = "col"
+    scheme: str = "colrandind"
+    tau: float = 1e-3
+    latent_dim: int = 4
+    pq_bits: int = 4
+    lambda_precision: str = "f32"
+    learning_rate: float = 0.001
+    batch_size: int = 128
+    epochs_full: int = 100
+    epochs_incremental: int = 2
+    retrain_period: int = 25
+    static_model: bool = False
+    newton: NewtonOptions = field(default_factory=NewtonOptions)
+    seed: int = 0
+
+    def __post_init__(self):
+        if min(self.workers, self.shards, self.latent_dim, self.epochs_full,
+               self.epochs_incremental, self.retrain_period, self.batch_size) < 1:
+            raise ConfigError("all pipeline counts must be >= 1")
+        if self.tau <= 0:
+            raise ConfigError("tau must be positive")
+        if self.pq_bits not in (4, 6, 8):
+            raise ConfigError("pq_bits must be 4, 6, or 8")
+        if self.lambda_precision not in ("f32", "f64"):
+            raise ConfigError("lambda_precision must be 'f32' or 'f64'")
+        if self.mode not in ("row", "col"):
+            raise ConfigError("mode must be 'row' or 'col'")
+        SelectionScheme(self.scheme)
+        if self.seed < 0:
+            raise ConfigError("seed must be non-negative")
+
+    def to_dict(self) -> dict:
+        return asdict(self)
+
+    @classmethod
+    def from_dict(cls, d: dict):
+        d = dict(d)
+        if isinstance(d.get("newton"), dict):
+            d["newton"] = NewtonOptions(**d["newton"])
+        return cls(**d)
+
+    def digest(self) -> bytes:
+        return hashlib.sha256(json.dumps(self.to_dict(), sort_keys=True).encode()).digest()
+
+    @property
+    def lambda_bytes(self) -> int:
+        return 4 if self.lambda_precision == "f32" else 8
+
+
+@dataclass
+class TimestepState:
+    """Per-shard models carried to the next timestep (pipeline.py:92-96)."""
+
+    models: list
+    timestep_index: int = 0
+
+
+# ---------------------------------------------------------------------------
+# device placement helpers
+
+def _device():
+    if not torch.cuda.is_available():
+        from .errors import BackendError
+        raise BackendError("no CUDA device: the B200 path has no CPU fallback")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def upload_f0(data: np.ndarray, device, node_range=None) -> torch.Tensor:
+    """(P, N, R, C) float64 host array -> flat device buffer (+16 B pad).
+
+    node_range=(lo, hi) uploads only that node slab of every plane (the
+    rank-local part of a column decomposition)."""
+    P, N, R, C = data.shape
+    lo, hi = node_range or (0, N)
+    n_el = P * (hi - lo) * R * C
+    buf = torch.empty(n_el + 2, dtype=torch.float64, device=device)
+    src = np.ascontiguousarray(data[:, lo:hi]) if (lo, hi) != (0, N) else \
+        np.ascontiguousarray(data)
+    host = torch.from_numpy(src.reshape(-1))
+    if host.numel():
+        buf[:n_el].copy_(host.pin_memory() if not host.is_pinned() else host, non_blocking=True)
+    return buf
+
+
+# ---------------------------------------------------------------------------
+# section assembly (pipeline.py:116-184, 296-311)
+
+def shard_blob(out: engine.CompressOut, s: int, img_off: int, images_host, cfg) -> bytes:
+    """Byte-exact shard blob for local shard s of a CompressOut."""
+    sp = out.specs[s]
+    n = sp.n_img
+    fl = out.flags[img_off:img_off + n]
+    exc = np.flatnonzero(fl & F_EXCEPTION)
+    sel = out.sel[s]
+    res = [struct.pack("<dI", out.eb[s], len(sel))]
+    for i, p in zip(sel, out.payloads[s]):
+        res.append(struct.pack("<II", int(i), len(p)))
+        res.append(p)
+    dt = "<f4" if cfg.lambda_precision == "f32" else "<f8"
+    lam_sec = np.concatenate([out.lam[img_off:img_off + n], out.qst[img_off:img_off + n]],
+                             axis=1).astype(dt).tobytes()
+    exc_parts = [struct.pack("<I", len(exc))]
+    if len(exc):
+        imgs = images_host(exc)
+        for k, i in enumerate(exc):
+            exc_parts.append(struct.pack("<I", int(i)))
+            exc_parts.append(np.ascontiguousarray(imgs[k], dtype="<f8").tobytes())
+    sections = {"weights": sp.model.to_bytes(), "codes": out.codes_packed[s],
+                "pq_table": out.cents[s].astype("<f4").tobytes(), "residuals": b"".join(res),
+                "lambdas": lam_sec, "exceptions": b"".join(exc_parts)}
+    rows_cols = out.rows_cols
+    return write_shard(dict(scheme=SCHEME_FULL, lambda_precision=cfg.lambda_bytes, n_images=n,
+                            img_rows=rows_cols[0], img_cols=rows_cols[1],
+                            latent_dim=cfg.latent_dim, pq_bits=cfg.pq_bits), sections)
+
+
+def _check_state(config, state, n_shards):
+    if state is None:
+        raise ConfigError("AE training is outside the B200 hot path: pass a TimestepState "
+                          "holding one trained AEModel per shard (static_model=True)")
+    if len(state.models) != n_shards:
+        raise ConfigError("timestep state does not match the shard count")
+    if not config.static_model:
+        raise ConfigError("incremental retraining is outside the B200 hot path: use "
+                          "PipelineConfig(static_model=True)")
+
+
+def compress(ds: FDataset, config: PipelineConfig, state: TimestepState | None = None):
+    """Run the five stages on the GPU; returns (archive bytes, report, new state)."""
+    t_all = time.perf_counter()
+    shards = partition(ds.n_planes, ds.n_nodes, config.shards, config.mode)
+    _check_state(config, state, len(shards))
+    dev = _device()
+    D = ds.grid.rows * ds.grid.cols
+    f0 = upload_f0(ds.data, dev)
+    dgrid = engine.DeviceGrid(ds.grid, dev, config.latent_dim)
+    works = engine.shard_layout(shards, state.models, ds.n_nodes, D)
+    timer = engine.Timer(True)
+    out = engine.compress_device(f0, works, dgrid, config, timer)
+    out.dataset_index = np.concatenate(
+        [np.fromiter((p * ds.n_nodes + x for p, x in sh.members), dtype=np.int64,
+                     count=len(sh.members)) for sh in shards])
+    stage_t = timer.result()
+    t0 = time.perf_counter()
+    blobs = []
+    off = 0
+    for s, sh in enumerate(shards):
+        pl = np.fromiter((p for p, _ in sh.members), dtype=np.intp, count=len(sh.members))
+        no = np.fromiter((x for _, x in sh.members), dtype=np.intp, count=len(sh.members))
+        blobs.append(shard_blob(out, s, off, lambda idx: ds.data[pl[idx], no[idx]], config))
+        off += sh.n_images
+    preamble = ArchivePreamble(n_shards=len(shards), decomp_mode=config.mode,
+                               n_planes=ds.n_planes, n_nodes=ds.n_nodes, grid=ds.grid,
+                               timestep=ds.timestep, tau=config.tau, seed=config.seed,
+                               config_digest=config.digest())
+    archive = write_archive(preamble, blobs)
+    stage_t["pack"] = stage_t.get("pack", 0.0) + time.perf_counter() - t0
+    report = build_report(ds, archive, [out], config.tau, stage_t,
+                          time.perf_counter() - t_all)
+    new_state = TimestepState(models=list(state.models),
+                              timestep_index=state.timestep_index + 1)
+    return archive, report, new_state
+
+
+def build_report(ds, archive, outs, tau, stage_t, wall) -> ErrorReport:
+    """pipeline._build_report (pipeline.py:367-391) from device-side reductions."""
+    flags = np.concatenate([o.flags for o in outs])
+    ferr = np.concatenate([o.ferr for o in outs])
+    exc = (flags & F_EXCEPTION) != 0
+    per_img_shard = np.where(exc, 0.0, ferr)
+    # per_image_nrmse is reported in dataset (plane-major) order
+    order = np.concatenate([o.dataset_index for o in outs])
+    per_image = np.empty_like(per_img_shard)
+    per_image[order] = per_img_shard
+    q_orig = np.empty((len(order), 4))
+    q_rec = np.empty((len(order), 4))
+    q_orig[order] = np.concatenate([o.qoi for o in outs])
+    q_rec[order] = np.concatenate([o.fqoi for o in outs])
+    qerr, qmax = qoi_nrmse_from_moments(q_orig, q_rec)
+    stats = np.concatenate([o.stats for o in outs])
+    span = float(stats[:, 0].max() - stats[:, 1].min())
+    sse = float(np.concatenate([o.fsse for o in outs]).sum())
+    d_total = ds.data.size
+    pd = float(np.sqrt(sse / d_total) / span) if span > 0 else 0.0
+    n_tot = len(flags)
+    status = np.concatenate([o.status for o in outs])
+    n_conv = int(np.sum((status == NewtonStatus.CONVERGED) & ((flags & F_NONFINITE) == 0)
+                        & ((flags & F_EXC_OVERFLOW) == 0)))
+    ae_ok = int(np.sum((flags & (F_SELECTED | F_NONFINITE)) == 0))
+    timings = {s: {"sum": 0.0, "max": 0.0} for s in _STAGES}
+    for k, v in stage_t.items():
+        if k in timings:
+            timings[k] = {"sum": v, "max": v}
+    timings["other"] = {"sum": max(0.0, wall - sum(v for v in stage_t.values())),
+                        "max": max(0.0, wall - sum(v for v in stage_t.values()))}
+    return ErrorReport(
+        pd_nrmse=pd, per_image_nrmse=per_image.tolist(), qoi_nrmse=qerr, max_qoi_nrmse=qmax,
+        compression_ratio=compression_ratio(dataset_nbytes(ds), len(archive)),
+        ae_accuracy=ae_ok / n_tot,
+        residual_fraction=int(np.sum(flags & F_SELECTED != 0)) / n_tot,
+        convergence_fraction=n_conv / n_tot, exception_count=int(exc.sum()),
+        stage_timings=timings)
+
+
+# ---------------------------------------------------------------------------
+# decompress (pipeline.py:397-440)
+
+def _parse_residuals(raw: bytes, n_img: int, rows: int, cols: int):
+    if len(raw) < 12:
+        raise FormatError("residual section truncated")
+    _, count = struct.unpack_from("<dI", raw, 0)
+    off, entries = 12, []
+    for _ in range(count):
+        if off + 8 > len(raw):
+            raise FormatError("residual section truncated")
+        idx, ln = struct.unpack_from("<II", raw, off)
+        off += 8
+        entries.append((idx, raw[off:off + ln]))
+        off += ln
+    if off != len(raw):
+        raise FormatError("residual section has trailing bytes")
+    return entries
+
+
+def _parse_exceptions(raw: bytes, D: int):
+    if len(raw) < 4:
+        raise FormatError("exceptions section truncated")
+    count = struct.unpack_from("<I", raw, 0)[0]
+    if len(raw) != 4 + count * (4 + 8 * D):
+        if len(raw) < 4 + count * (4 + 8 * D):
+            raise FormatError("exceptions section truncated")
+        raise FormatError("exceptions section has trailing bytes")
+    rec = np.frombuffer(raw, dtype=np.uint8, offset=4).reshape(count, 4 + 8 * D)
+    idx = rec[:, :4].copy().view("<u4").reshape(-1).astype(np.int64)
+    imgs = rec[:, 4:].copy().view("<f8").reshape(count, D)
+    return idx, imgs
+
+
+def decompress(archive: bytes) -> FDataset:
+    """Invert compress(); exception images are reproduced verbatim."""
+    preamble, blobs = read_archive(archive)
+    shards = partition(preamble.n_planes, preamble.n_nodes, preamble.n_shards,
+                       preamble.decomp_mode)
+    dev = _device()
+    data = engine.decompress_device(preamble, shards, blobs, dev)
+    return FDataset(grid=preamble.grid, data=data, timestep=preamble.timestep)
+
+
+def evaluate(orig: FDataset, archive: bytes) -> ErrorReport:
+    """Decompress and fill a full error report with gate verdicts (pipeline.py:443-491)."""
+    t0 = time.perf_counter()
+    preamble, blobs = read_archive(archive)
+    if (preamble.n_planes, preamble.n_nodes) != (orig.n_planes, orig.n_nodes) or \
+            (preamble.grid.rows, preamble.grid.cols) != (orig.grid.rows, orig.grid.cols):
+        raise ConfigError("archive dimensions do not match the dataset")
+    rec = decompress(archive)
+    decode_time = time.perf_counter() - t0
+    t1 = time.perf_counter()
+    ev = engine.evaluate_device(orig, rec, preamble, blobs, _device())
+    lam_bytes = read_shard(blobs[-1]).header.lambda_precision
+    qerr, qmax = qoi_nrmse_from_moments(ev["q_orig"], ev["q_rec"])
+    tau = preamble.tau
+    gate = QOI_GATES["f32" if lam_bytes == 4 else "f64"]
+    per_image = ev["per_image"]
+    ae = ev["ae_err"]
+    fin = np.where(np.isfinite(ae), ae, np.inf)
+    return ErrorReport(
+        pd_nrmse=ev["pd_nrmse"], per_image_nrmse=per_image.tolist(), qoi_nrmse=qerr,
+        max_qoi_nrmse=qmax,
+        compression_ratio=compression_ratio(dataset_nbytes(orig), len(archive)),
+        ae_accuracy=float(np.mean(fin <= tau)), residual_fraction=float(np.mean(fin > tau)),
+        stage_timings={"decode": {"sum": decode_time, "max": decode_time},
+                       "metrics": {"sum": time.perf_counter() - t1,
+                                   "max": time.perf_counter() - t1}},
+        gates={"pd_per_image": bool(np.all(per_image <= tau)), "qoi": bool(qmax <= gate)})
+
+
+def run_timesteps(datasets, config: PipelineConfig, models=None):
+    """Compress a sequence with fixed models (static mode only, see compress)."""
+    if not datasets:
+        raise ConfigError("need at least one timestep")
+    state = TimestepState(models=list(models), timestep_index=0) if models else None
+    out = []
+    for ds in datasets:
+        archive, report, state = compress(ds, config, state)
+        out.append((archive, report, "static"))
+    return out
