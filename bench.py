@@ -1,0 +1,349 @@
+"""Benchmark: per-histogram compress throughput on B200 (BASELINE.json metric).
+
+Workload (default): BASELINE.json configs[2] -- D3D-scale synthetic f0,
+8 planes x 16,395 nodes x 39x39 fp64 (131,160 histograms, 1.596 GB),
+S = 8 column shards, tau = 1e-3, f32 lambdas, static AE weights trained
+once by the reference (tests/golden/cfg3.npz).  At N GPUs rank r owns shards
+[8r/N, 8(r+1)/N) and only its node slab of f0 (strong scaling of one fixed
+archive; shard count never depends on N, so the archive is identical).
+
+  value : histograms/s of the device pipeline (f0 resident in HBM; step =
+          every stage of pipeline._compress_shard for the rank's shards,
+          shard blobs assembled, blob sizes exchanged over NCCL).
+  e2e   : the same metric through the public API (compress(ds, cfg, state)
+          at N=1: host f0 -> H2D -> device -> D2H -> archive bytes + report).
+Timing: CUDA events on the launching stream, barrier + synchronize on both
+sides, max over ranks.  Every step reads 1.6 GB of f0 (> 126 MB L2).
+
+--impl reference times the CPU oracle (numpy + C restatement of the
+reference, oracle/) with a thread per shard on this host's cores.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+
+import numpy as np  # noqa: E402
+
+CONFIGS = {
+    "cfg3": dict(P=8, N=16395, golden="cfg3", desc="configs[2]: 8 planes x 16,395 nodes"),
+    "cfg2": dict(P=1, N=16395, golden="cfg2", desc="configs[1]: 1 plane x 16,395 nodes"),
+}
+HIST_BYTES = 39 * 39 * 8
+METRIC = "histograms/s compressed (raw GB/s = hist/s x 12,168 B)"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="cfg3", choices=list(CONFIGS))
+    ap.add_argument("--tau", type=float, default=1e-3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--out", default=None)
+    return ap.parse_args()
+
+
+def corpus(P, N):
+    from paper_2212_10733_b200 import fdata
+    g = fdata.make_grid(39, 39, 5.0, 5.0, 1.0)
+    return fdata.gen_synthetic(P, N, g, fdata.SyntheticParams(seed=42, rho=0.003))
+
+
+def load_models(name):
+    from paper_2212_10733_b200 import AEModel
+    a = np.load(ROOT / "tests" / "golden" / f"{name}.npz")
+    return [AEModel(weights=a["model_W"][i], norm_mean=float(a["model_mean"][i]),
+                    norm_std=float(a["model_std"][i])) for i in range(a["model_W"].shape[0])]
+
+
+def pipeline_config(tau, shards=8):
+    from paper_2212_10733_b200 import PipelineConfig
+    return PipelineConfig(workers=8, shards=shards, seed=0, tau=tau, lambda_precision="f32",
+                          static_model=True)
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index),
+                                      f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits"],
+                                     capture_output=True, text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=6)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 2 + i and s[2 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def cpu_oracle_sample(ds_full, models, tau, threads):
+    """The oracle (oracle/port.py + C kernels) on plane 0 of the corpus with the
+    same 8 shards and models: a config-2-sized bounded sample."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from oracle import port
+    from paper_2212_10733_b200 import fdata as F  # noqa: F401
+    g = ds_full.grid
+    grid = port.Grid(g.v_perp, g.v_par, g.vol, g.mass)
+    data = ds_full.data[:1]
+    cfg = port.Cfg(shards=8, mode="col", tau=tau, seed=0)
+    members = port.shard_members(1, data.shape[1], 8, "col")
+    mods = [(m.weights, m.norm_mean, m.norm_std) for m in models]
+
+    def job(i):
+        pl, no = members[i]
+        return port.compress_shard(data[pl, no], grid, cfg, mods[i], i)
+
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(max_workers=threads) as ex:
+        list(ex.map(job, range(8)))
+    dt = time.perf_counter() - t0
+    n = data.shape[0] * data.shape[1]
+    return n / dt, n, dt
+
+
+def run_reference(args, rank, world):
+    """--impl reference: CPU oracle, rank 0 only."""
+    if rank != 0:
+        return
+    spec = CONFIGS[args.config]
+    ds = corpus(spec["P"], spec["N"])
+    models = load_models(spec["golden"])
+    threads = os.cpu_count() or 1
+    for _ in range(args.warmup):
+        cpu_oracle_sample(ds, models, args.tau, threads)
+    vals = []
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        v, n, dt = cpu_oracle_sample(ds, models, args.tau, threads)
+        vals.append(v)
+    total = time.perf_counter() - t0
+    value = args.steps * n / total
+    sample = (f"plane 0 of the {spec['desc']} corpus ({n} histograms, S=8 shards, "
+              f"tau={args.tau}), oracle/port.py + oracle/ckernels.c, {threads} threads")
+    line = {"metric": METRIC, "value": value, "unit": "hist/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "impl": "reference",
+            "config": {"workload": spec["desc"], "sample": "plane 0", "tau": args.tau},
+            "cpu_baseline": {"value": value, "unit": "hist/s", "cores": threads, "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": "hist/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2212_10733_b200 import _lib, engine, pipeline
+    from paper_2212_10733_b200.decomp import partition, rank_shards
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    spec = CONFIGS[args.config]
+    ds = corpus(spec["P"], spec["N"])
+    models = load_models(spec["golden"])
+    cfg = pipeline_config(args.tau)
+    shards = partition(ds.n_planes, ds.n_nodes, cfg.shards, cfg.mode)
+    mine = rank_shards(len(shards), rank, world)
+    my_shards = [shards[i] for i in mine]
+    lo, hi = my_shards[0].nodes_range[0], my_shards[-1].nodes_range[1]
+    D = ds.grid.rows * ds.grid.cols
+    f0 = pipeline.upload_f0(ds.data, dev, (lo, hi))
+    dgrid = engine.DeviceGrid(ds.grid, dev, cfg.latent_dim)
+    works = engine.shard_layout(my_shards, [models[i] for i in mine], hi - lo, D, node_lo=lo)
+    n_local = sum(w.n_img for w in works)
+    order = [np.fromiter((p * ds.n_nodes + x for p, x in sh.members), dtype=np.int64)
+             for sh in my_shards]
+
+    def one_step(timer=None):
+        out = engine.compress_device(f0, works, dgrid, cfg, timer)
+        blobs, off = [], 0
+        for s, sh in enumerate(my_shards):
+            pl = np.fromiter((p for p, _ in sh.members), dtype=np.intp)
+            no = np.fromiter((x for _, x in sh.members), dtype=np.intp)
+            blobs.append(pipeline.shard_blob(out, s, off, lambda i: ds.data[pl[i], no[i]], cfg))
+            off += sh.n_images
+        sizes = torch.tensor([len(b) for b in blobs], dtype=torch.int64, device=dev)
+        if world > 1:  # NCCL: blob sizes -> archive offsets (the only exchange)
+            allsz = [torch.zeros(8, dtype=torch.int64, device=dev) for _ in range(world)]
+            pad = torch.zeros(8, dtype=torch.int64, device=dev)
+            pad[:len(blobs)] = sizes
+            dist.all_gather(allsz, pad)
+        return out, blobs
+
+    for _ in range(args.warmup):
+        one_step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    _lib.LAUNCHES = 0
+    stage_sum = {}
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(local) as clk:
+        torch.cuda.synchronize()
+        start.record()
+        for _ in range(args.steps):
+            timer = engine.Timer(True)
+            out, blobs = one_step(timer)
+            timer.mark("end")
+            for k, v in timer.result().items():
+                stage_sum[k] = stage_sum.get(k, 0.0) + v
+        stop.record()
+        torch.cuda.synchronize()
+    launches = _lib.LAUNCHES
+    ms = start.elapsed_time(stop) / args.steps
+    t = torch.tensor([ms], device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    total_hist = ds.n_planes * ds.n_nodes
+    value = total_hist / (ms / 1e3)
+    stage_ms = {k: 1e3 * v / args.steps for k, v in stage_sum.items()}
+
+    # roofline of the pass-1 kernel (reads every histogram once: 12,168 B each)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    lat = torch.empty((n_local, 4), dtype=torch.float64, device=dev)
+    st = torch.empty((n_local, 4), dtype=torch.float64, device=dev)
+    qo = torch.empty((n_local, 4), dtype=torch.float64, device=dev)
+    table = engine._shard_table(works, D, cfg.latent_dim)
+    sh_d = engine._upload_shards(table, dev)
+    W = torch.from_numpy(np.stack([w.model.weights for w in works])).to(dev)
+    reps = 5
+    e0.record()
+    for _ in range(reps):
+        _lib.call("mlk_stage1", f0, sh_d, len(works), n_local, dgrid.addr, W, cfg.latent_dim,
+                  lat, st, qo)
+    e1.record()
+    torch.cuda.synchronize()
+    s1_ms = e0.elapsed_time(e1) / reps
+    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) \
+        if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    s1_bytes = n_local * HIST_BYTES
+    achieved = s1_bytes / (s1_ms / 1e3) / 1e9
+    roofline = {"bound": "hbm", "kernel": "k_stage1 (pass 1: encode + moments)",
+                "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": None, "algorithmic_bytes_per_launch": s1_bytes,
+                "launch_ms": s1_ms,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650"}
+
+    # end to end through the public API (N=1) and decompress
+    e2e = None
+    dec = None
+    if rank == 0 and world == 1 and not args.no_e2e:
+        from paper_2212_10733_b200 import TimestepState, compress, decompress
+        state = TimestepState(models=models, timestep_index=1)
+        compress(ds, cfg, state)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        reps = max(1, min(args.steps, 3))
+        for _ in range(reps):
+            arc, rep, _ = compress(ds, cfg, state)
+        torch.cuda.synchronize()
+        e2e_s = (time.perf_counter() - t0) / reps
+        d2h = len(arc)
+        e2e = {"value": total_hist / e2e_s, "unit": "hist/s", "h2d_bytes_per_step": ds.data.nbytes,
+               "d2h_bytes_per_step": d2h, "seconds_per_step": e2e_s,
+               "api": "paper_2212_10733_b200.compress(ds, config, state)"}
+        decompress(arc)
+        t0 = time.perf_counter()
+        back = decompress(arc)
+        dec_s = time.perf_counter() - t0
+        dec = {"value": total_hist / dec_s, "unit": "hist/s (e2e decompress via public API)",
+               "raw_gb_s": total_hist * HIST_BYTES / dec_s / 1e9,
+               "max_per_image_nrmse": rep.max_per_image_nrmse(),
+               "ratio": rep.compression_ratio, "exceptions": rep.exception_count}
+        del back
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        v, n, dt = cpu_oracle_sample(ds, models, args.tau, threads)
+        cpu = {"value": v, "unit": "hist/s", "cores": threads, "kind": "port",
+               "sample": f"plane 0 of the corpus ({n} histograms, 8 shards), oracle/port.py, "
+                         f"{threads} threads, {dt:.1f} s"}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "hist/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+                "dtype": "f64", "data": "synthetic (gen_synthetic seed 42, rho 0.003; "
+                                        "reference-trained static AE weights)",
+                "config": {"workload": spec["desc"], "histograms": total_hist, "shards": 8,
+                           "tau": args.tau, "lambda": "f32", "parallelism": f"shards/{world}",
+                           "l2": "inputs 1.6 GB > 126 MB L2 (no flush needed)"},
+                "raw_gb_s": value * HIST_BYTES / 1e9,
+                "stage_ms": stage_ms, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+                "decompress": dec, "gpu_launches": launches,
+                "clocks": clk.summary(),
+                "ratio": None if dec is None else dec["ratio"]}
+        print(json.dumps(line), flush=True)
+        if args.out:
+            Path(args.out).write_text(json.dumps(line, indent=1))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

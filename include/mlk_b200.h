@@ -138,12 +138,18 @@ int mlk_unpack_indices(const uint8_t* buf, int64_t count, int32_t bits, uint16_t
 /* zlib.compress(data, 6) (residual.py:70,77) for n streams: input s is
  * in_len[s] bytes at in + in_off[s]; output (2-byte zlib header, DEFLATE
  * stream reproducing zlib 1.3 deflate_slow level 6, Adler-32) goes to
- * out + out_off[s] with capacity out_cap each; out_len[s] = bytes written or
- * -1 if out_cap was too small.  `work` >= n * MLK_DEFLATE_WORK bytes. */
-#define MLK_DEFLATE_WORK (1u << 19)
+ * out + out_off[s] with capacity out_cap each; out_len[s] = bytes written,
+ * -1 if out_cap was too small, -2 if the input exceeds 32000 bytes.
+ * `work` = n_workers * MLK_DEFLATE_WORK bytes, zero-filled before first use
+ * (the kernel leaves it reusable). */
+#define MLK_DEFLATE_WORK (1u << 18)
 int mlk_zlib_compress6(const uint8_t* in, const int64_t* in_off, const int64_t* in_len,
                        int32_t n, uint8_t* out, const int64_t* out_off, int64_t out_cap,
-                       int64_t* out_len, uint8_t* work, cudaStream_t stream);
+                       int64_t* out_len, uint8_t* work, int32_t n_workers, cudaStream_t stream);
+
+/* dst[dst_off[i] .. + len[i]) = src[src_off[i] .. + len[i]) for n segments */
+int mlk_gather_segments(const uint8_t* src, const int64_t* src_off, const int64_t* len,
+                        int32_t n, uint8_t* dst, const int64_t* dst_off, cudaStream_t stream);
 
 /* zlib.decompress (residual.py:86) for n streams; out_len[s] = bytes produced,
  * or -1 (corrupt) / -2 (output capacity exceeded). */

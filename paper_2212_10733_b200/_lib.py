@@ -65,7 +65,8 @@ _SIGS = {
     "mlk_varint_decode_batch": [_P, _P, _P, _I32, _P, _P, _P, _P, _P],
     "mlk_pack_indices": [_P, _I64, _I32, _P, _P, _P],
     "mlk_unpack_indices": [_P, _I64, _I32, _P, _P],
-    "mlk_zlib_compress6": [_P, _P, _P, _I32, _P, _P, _I64, _P, _P, _P],
+    "mlk_zlib_compress6": [_P, _P, _P, _I32, _P, _P, _I64, _P, _P, _I32, _P],
+    "mlk_gather_segments": [_P, _P, _P, _I32, _P, _P, _P],
     "mlk_zlib_decompress": [_P, _P, _P, _I32, _P, _P, _I64, _P, _P],
     "mlk_stage1": [_P, _P, _I32, _I32, _P, _P, _I32, _P, _P, _P, _P],
     "mlk_kmeans": [_P, _P, _I32, _I32, _I32, _P, _P, _P, _P, _P, _P],
@@ -119,7 +120,12 @@ def ptr(t) -> int | None:
     return t
 
 
+LAUNCHES = 0  # C-ABI entry calls (each launches exactly one kernel)
+
+
 def call(name: str, *args, msg: str = "") -> None:
+    global LAUNCHES
+    LAUNCHES += 1
     fn = getattr(lib(), name)
     conv = [ptr(a) if isinstance(a, torch.Tensor) else a for a in args]
     rc = fn(*conv, stream_handle())

@@ -148,7 +148,30 @@ __global__ void k_unpack(const unsigned char* buf, long long count, int bits, un
     out[i] = (unsigned short)v;
 }
 
+// one warp per segment, byte copies (segments are short and unaligned)
+__global__ void k_gather(const unsigned char* __restrict__ src, const long long* __restrict__ soff,
+                         const long long* __restrict__ len, int n, unsigned char* __restrict__ dst,
+                         const long long* __restrict__ doff) {
+    const int seg = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (seg >= n) return;
+    const unsigned char* s = src + soff[seg];
+    unsigned char* d = dst + doff[seg];
+    const long long l = len[seg];
+    for (long long i = lane; i < l; i += 32) d[i] = s[i];
+}
+
 }  // namespace
+
+extern "C" int mlk_gather_segments(const uint8_t* src, const int64_t* src_off, const int64_t* len,
+                                   int32_t n, uint8_t* dst, const int64_t* dst_off,
+                                   cudaStream_t stream) {
+    if (n <= 0) return MLK_OK;
+    k_gather<<<(n + 7) / 8, 256, 0, stream>>>(src, reinterpret_cast<const long long*>(src_off),
+                                              reinterpret_cast<const long long*>(len), n, dst,
+                                              reinterpret_cast<const long long*>(dst_off));
+    return cudaGetLastError() == cudaSuccess ? MLK_OK : MLK_ERR_CUDA;
+}
 
 extern "C" int mlk_zigzag_map(const int64_t* q, uint64_t* z, int64_t n, cudaStream_t stream) {
     if (n <= 0) return MLK_OK;

@@ -16,7 +16,6 @@ import ctypes
 import functools
 import math
 import struct
-import zlib
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -395,20 +394,18 @@ def compress_device(f0: torch.Tensor, specs, dgrid: DeviceGrid, cfg, timer: Time
         raise ConfigError("error bound too small for this residual range")
     sel_h = sel.cpu().numpy()
     payloads = []
-    vlen_h = vlen.cpu().numpy()
-    var_h = varint.view(-1).cpu().numpy() if n_sel else None
     sel_lists = []
+    comp_h, zoff_h, zlen_h = deflate_slots(varint, vcap, vlen, n_sel, dev)
     for s, sp in enumerate(specs):
         off = table[s].img_off
-        idx = sel_h[off:off + cnt_h[s]].copy()
-        sel_lists.append(idx)
-        pl = []
+        sel_lists.append(sel_h[off:off + cnt_h[s]].copy())
         head = _PAYLOAD_HEAD.pack(1 if lossless[s] else 0, dgrid.struct.rows,
                                   dgrid.struct.cols, 0.0 if lossless[s] else eb[s])
+        pl = []
         for r in range(cnt_h[s]):
             slot = slot_base_h[s] + r
-            raw = var_h[slot * vcap: slot * vcap + vlen_h[slot]].tobytes()
-            pl.append(head + zlib.compress(raw, zlib_level))
+            a = zoff_h[slot]
+            pl.append(head + comp_h[a:a + zlen_h[slot]].tobytes())
         payloads.append(pl)
     packed = []
     codes16 = codes.to(torch.int16).view(torch.uint16) if hasattr(torch, "uint16") else None
@@ -433,6 +430,44 @@ def compress_device(f0: torch.Tensor, specs, dgrid: DeviceGrid, cfg, timer: Time
     return out
 
 
+
+
+# ---------------------------------------------------------------------------
+# DEFLATE on device (zlib.compress(x, 6) byte-exact, csrc/zlib6.h)
+
+_DEFLATE_POOLS = {}
+DEFLATE_WORK = 1 << 18
+
+
+def _deflate_pool(dev, n_workers):
+    key = (dev.index, n_workers)
+    if key not in _DEFLATE_POOLS:
+        _DEFLATE_POOLS.clear()
+        _DEFLATE_POOLS[key] = torch.zeros(n_workers * DEFLATE_WORK, dtype=torch.uint8, device=dev)
+    return _DEFLATE_POOLS[key]
+
+
+def deflate_slots(varint, vcap, vlen, n, dev, max_workers=8192):
+    """zlib-6 every varint slot on device; returns the packed bodies (host),
+    their offsets and lengths."""
+    if n == 0:
+        return np.zeros(0, np.uint8), np.zeros(0, np.int64), np.zeros(0, np.int64)
+    i64 = dict(dtype=torch.int64, device=dev)
+    zcap = vcap + 64
+    workers = min(n, max_workers)
+    zout = torch.empty(n * zcap, dtype=torch.uint8, device=dev)
+    zlen = torch.empty(n, **i64)
+    in_off = torch.arange(0, n * vcap, vcap, **i64)
+    out_off = torch.arange(0, n * zcap, zcap, **i64)
+    call("mlk_zlib_compress6", varint, in_off, vlen[:n], n, zout, out_off, zcap, zlen,
+         _deflate_pool(dev, workers), workers)
+    zlen_h = zlen.cpu().numpy()
+    if np.any(zlen_h < 0):
+        raise ConfigError("residual stream exceeds the device DEFLATE limits")
+    dst_h = np.concatenate([[0], np.cumsum(zlen_h)[:-1]]).astype(np.int64)
+    comp = torch.empty(max(1, int(zlen_h.sum())), dtype=torch.uint8, device=dev)
+    call("mlk_gather_segments", zout, out_off, zlen, n, comp, torch.from_numpy(dst_h).to(dev))
+    return comp.cpu().numpy(), dst_h, zlen_h
 
 
 # ---------------------------------------------------------------------------
@@ -497,10 +532,7 @@ def decompress_device(preamble, shards, blobs, dev) -> np.ndarray:
                 raise FormatError("residual payload dims do not match the shard")
             if mode not in (0, 1):
                 raise FormatError(f"unknown residual payload mode {mode}")
-            try:
-                raw = zlib.decompress(payload[_PAYLOAD_HEAD.size:])
-            except zlib.error as exc:
-                raise FormatError(f"corrupt residual stream: {exc}") from exc
+            raw = payload[_PAYLOAD_HEAD.size:]
             res_codes_l.append(raw)
             res_eb_l.append(eb)
             res_mode_l.append(mode)
@@ -513,25 +545,33 @@ def decompress_device(preamble, shards, blobs, dev) -> np.ndarray:
         n_exc += len(eidx)
         exc_slot_l.append(es)
         exc_img_l.append(eimg)
-    # varint streams -> device decode
+    # zlib bodies -> device inflate -> device varint decode
     i64 = dict(dtype=torch.int64, device=dev)
     if n_res:
         lens = np.array([len(r) for r in res_codes_l], dtype=np.int64)
         offs = np.concatenate([[0], np.cumsum(lens)[:-1]]).astype(np.int64)
         blob = np.frombuffer(b"".join(res_codes_l), dtype=np.uint8).copy()
-        raw_d = torch.from_numpy(blob if blob.size else np.zeros(1, np.uint8)).to(dev)
+        zin = torch.from_numpy(blob if blob.size else np.zeros(1, np.uint8)).to(dev)
+        icap = 10 * D + 64
+        raw_d = torch.empty(n_res * icap, dtype=torch.uint8, device=dev)
+        raw_off = torch.arange(0, n_res * icap, icap, **i64)
+        raw_len = torch.empty(n_res, **i64)
+        call("mlk_zlib_decompress", zin, torch.from_numpy(offs).to(dev),
+             torch.from_numpy(lens).to(dev), n_res, raw_d, raw_off, icap, raw_len)
+        rl = raw_len.cpu().numpy()
+        if np.any(rl < 0):
+            raise FormatError("corrupt residual stream")
         vals = torch.empty(n_res * D, dtype=torch.int64, device=dev)
         consumed = torch.empty(n_res, **i64)
-        call("mlk_varint_decode_batch", raw_d, torch.from_numpy(offs).to(dev),
-             torch.from_numpy(lens).to(dev), n_res,
-             torch.full((n_res,), D, **i64), vals,
-             torch.arange(0, n_res * D, D, **i64), consumed)
+        call("mlk_varint_decode_batch", raw_d, raw_off, raw_len, n_res,
+             torch.full((n_res,), D, **i64), vals, torch.arange(0, n_res * D, D, **i64),
+             consumed)
         con = consumed.cpu().numpy()
         if np.any(con == -1):
             raise FormatError("varint stream truncated")
         if np.any(con == -2):
             raise FormatError("varint value exceeds 64 bits")
-        if np.any(con != lens):
+        if np.any(con != rl):
             raise FormatError("residual stream has trailing bytes")
     else:
         vals = torch.zeros(1, dtype=torch.int64, device=dev)

@@ -165,3 +165,24 @@ def test_operator_api_newton_matches_compiled_reference():
         lam, s, i = kernels.newton_solve(fp, av, b, 1.0, 50, 1e-13)
         assert (s, i) == (st, it)
         np.testing.assert_allclose(lam, a[f"nw{t}_lam"], rtol=1e-9, atol=1e-12)
+
+
+def test_device_zlib_matches_host_zlib():
+    import zlib
+
+    from paper_2212_10733_b200 import engine
+    dev = torch.device("cuda", 0)
+    rng = np.random.default_rng(1)
+    streams = [rng.integers(0, k, n, dtype=np.uint8).tobytes()
+               for k, n in [(2, 1), (3, 500), (7, 1521), (256, 3000), (5, 15210), (1, 100)]]
+    streams += [zlib.decompress(G.load("units")[1][f"pl{t}_p"].tobytes()[13:])
+                for t in range(len(G.load("units")[0]["payload_ebs"]))]
+    vcap = 15216
+    var = torch.zeros(len(streams) * vcap, dtype=torch.uint8, device=dev)
+    vlen = torch.tensor([len(s) for s in streams], dtype=torch.int64, device=dev)
+    for i, s in enumerate(streams):
+        var[i * vcap:i * vcap + len(s)] = torch.frombuffer(bytearray(s), dtype=torch.uint8).to(dev)
+    comp, off, ln = engine.deflate_slots(var, vcap, vlen, len(streams), dev)
+    for i, s in enumerate(streams):
+        got = comp[off[i]:off[i] + ln[i]].tobytes()
+        assert got == zlib.compress(s, 6), i
