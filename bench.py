@@ -55,6 +55,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--out", default=None)
+    ap.add_argument("--no-clocks", action="store_true")
     return ap.parse_args()
 
 
@@ -211,26 +212,21 @@ def main():
     D = ds.grid.rows * ds.grid.cols
     f0 = pipeline.upload_f0(ds.data, dev, (lo, hi))
     dgrid = engine.DeviceGrid(ds.grid, dev, cfg.latent_dim)
-    works = engine.shard_layout(my_shards, [models[i] for i in mine], hi - lo, D, node_lo=lo)
+    works = engine.shard_layout(my_shards, [models[i] for i in mine], hi - lo, ds.grid.rows,
+                                ds.grid.cols, node_lo=lo)
     n_local = sum(w.n_img for w in works)
     order = [np.fromiter((p * ds.n_nodes + x for p, x in sh.members), dtype=np.int64)
              for sh in my_shards]
 
     def one_step(timer=None):
         out = engine.compress_device(f0, works, dgrid, cfg, timer)
-        blobs, off = [], 0
-        for s, sh in enumerate(my_shards):
-            pl = np.fromiter((p for p, _ in sh.members), dtype=np.intp)
-            no = np.fromiter((x for _, x in sh.members), dtype=np.intp)
-            blobs.append(pipeline.shard_blob(out, s, off, lambda i: ds.data[pl[i], no[i]], cfg))
-            off += sh.n_images
-        sizes = torch.tensor([len(b) for b in blobs], dtype=torch.int64, device=dev)
+        sizes = torch.from_numpy(np.asarray(out.blob_lens, dtype=np.int64)).to(dev)
         if world > 1:  # NCCL: blob sizes -> archive offsets (the only exchange)
             allsz = [torch.zeros(8, dtype=torch.int64, device=dev) for _ in range(world)]
             pad = torch.zeros(8, dtype=torch.int64, device=dev)
-            pad[:len(blobs)] = sizes
+            pad[:len(sizes)] = sizes
             dist.all_gather(allsz, pad)
-        return out, blobs
+        return out
 
     for _ in range(args.warmup):
         one_step()
@@ -240,18 +236,26 @@ def main():
     _lib.LAUNCHES = 0
     stage_sum = {}
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with Clocks(local) as clk:
+    clk = Clocks(local)
+    if not args.no_clocks:
+        clk.__enter__()
+    if True:
         torch.cuda.synchronize()
+        wall0 = time.perf_counter()
         start.record()
         for _ in range(args.steps):
             timer = engine.Timer(True)
-            out, blobs = one_step(timer)
+            out = one_step(timer)
             timer.mark("end")
             for k, v in timer.result().items():
                 stage_sum[k] = stage_sum.get(k, 0.0) + v
         stop.record()
         torch.cuda.synchronize()
+        wall_ms = 1e3 * (time.perf_counter() - wall0) / args.steps
+    if not args.no_clocks:
+        clk.__exit__(None, None, None)
     launches = _lib.LAUNCHES
+    probe_rounds = out.timings.get("probe_rounds")
     ms = start.elapsed_time(stop) / args.steps
     t = torch.tensor([ms], device=dev)
     if world > 1:
@@ -334,7 +338,7 @@ def main():
                            "tau": args.tau, "lambda": "f32", "parallelism": f"shards/{world}",
                            "l2": "inputs 1.6 GB > 126 MB L2 (no flush needed)"},
                 "raw_gb_s": value * HIST_BYTES / 1e9,
-                "stage_ms": stage_ms, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+                "wall_ms_per_step": wall_ms, "stage_ms": stage_ms, "probe_rounds": probe_rounds, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "decompress": dec, "gpu_launches": launches,
                 "clocks": clk.summary(),
                 "ratio": None if dec is None else dec["ratio"]}

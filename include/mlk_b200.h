@@ -82,6 +82,8 @@ typedef struct {
     const double* ash;      /* 3*D: base[r] / max|base[r]| for r = 0, 1, 2 */
     const uint8_t* tree_cols; /* D: decode bracketing probed from the host BLAS */
     double s0, s1, s2;      /* shared row scales */
+    int32_t sep, pad2;      /* vol takes vcls[2*row_edge + col_edge] everywhere */
+    double vcls[4];
 } MlkGrid;
 
 typedef struct {
@@ -141,11 +143,21 @@ int mlk_unpack_indices(const uint8_t* buf, int64_t count, int32_t bits, uint16_t
  * out + out_off[s] with capacity out_cap each; out_len[s] = bytes written,
  * -1 if out_cap was too small, -2 if the input exceeds 32000 bytes.
  * `work` = n_workers * MLK_DEFLATE_WORK bytes, zero-filled before first use
- * (the kernel leaves it reusable). */
+ * (the kernel leaves it reusable).  Only streams longer than nmin bytes are
+ * processed (the others are left to mlk_zlib_compress6_warp). */
 #define MLK_DEFLATE_WORK (1u << 18)
 int mlk_zlib_compress6(const uint8_t* in, const int64_t* in_off, const int64_t* in_len,
                        int32_t n, uint8_t* out, const int64_t* out_off, int64_t out_cap,
-                       int64_t* out_len, uint8_t* work, int32_t n_workers, cudaStream_t stream);
+                       int64_t* out_len, uint8_t* work, int32_t n_workers, int64_t nmin,
+                       cudaStream_t stream);
+
+/* Same bytes as mlk_zlib_compress6, one warp per stream with the working set
+ * in shared memory, for the streams with nmin < in_len <= nmax (<= 16000);
+ * run it over the size tiers, then mlk_zlib_compress6 for larger streams. */
+int mlk_zlib_compress6_warp(const uint8_t* in, const int64_t* in_off, const int64_t* in_len,
+                            int32_t n, int32_t nmin, int32_t nmax, uint8_t* out,
+                            const int64_t* out_off, int64_t out_cap, int64_t* out_len,
+                            int32_t n_blocks, cudaStream_t stream);
 
 /* dst[dst_off[i] .. + len[i]) = src[src_off[i] .. + len[i]) for n segments */
 int mlk_gather_segments(const uint8_t* src, const int64_t* src_off, const int64_t* len,
@@ -244,6 +256,34 @@ int mlk_decode(const MlkShard* shards, int32_t n_shards, int32_t total, const Ml
 int mlk_compare(const double* a, const double* b, int32_t total, const MlkGrid* grid_h,
                 double* err, double* sse, double* qa, double* qb, double* ext,
                 cudaStream_t stream);
+
+/* ---- shard-blob assembly on device (container.py:90-95, pipeline.py:116-184) */
+
+/* list[img_off + r] = r-th image of shard s (ascending) with flags & mask;
+ * count[s] = number of such images (the sorted exception list,
+ * pipeline.py:287). */
+int mlk_list_flags(const uint8_t* flags, const MlkShard* shards, int32_t n_shards, uint32_t mask,
+                   int32_t* list, int32_t* count, cudaStream_t stream);
+
+/* residual section entries (pipeline.py:132-137): for payload e of shard
+ * entry_shard[e] at out + dst_off[e]: <II> (index, 13 + zlen) then the
+ * <BHHd> payload header (residual.py:33) then the zlib body zbuf[zoff[e]..]. */
+int mlk_pack_residuals(const int32_t* sel, const MlkShard* shards, const int32_t* entry_shard,
+                       const int64_t* dst_off, const int64_t* zoff, const int64_t* zlen,
+                       const uint8_t* zbuf, const int32_t* slot_base, int32_t rows,
+                       int32_t cols, int32_t n, uint8_t* out, cudaStream_t stream);
+
+/* lambda section (pipeline.py:116-119): per image [lam, qoi] as <f4 or <f8 at
+ * out + sec_off[shard] + record * j. */
+int mlk_pack_lambdas(const double* lam, const double* qst, const MlkShard* shards,
+                     int32_t n_shards, int32_t total, const int64_t* sec_off, int32_t f32,
+                     uint8_t* out, cudaStream_t stream);
+
+/* exception entries (pipeline.py:158-163): <I index> + the original histogram
+ * read from f0, after the 4-byte count at out + sec_off[shard]. */
+int mlk_pack_exceptions(const double* f0, const MlkShard* shards, int32_t n_shards,
+                        const int32_t* exc_list, const int32_t* exc_off, const int64_t* sec_off,
+                        int32_t n_exc_total, int32_t D, uint8_t* out, cudaStream_t stream);
 
 #ifdef __cplusplus
 }

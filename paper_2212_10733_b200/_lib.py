@@ -37,7 +37,8 @@ class MlkGrid(ctypes.Structure):
                 ("vol", ctypes.c_void_p), ("vpar", ctypes.c_void_p), ("vperp2", ctypes.c_void_p),
                 ("hmvol", ctypes.c_void_p), ("ash", ctypes.c_void_p),
                 ("tree_cols", ctypes.c_void_p), ("s0", ctypes.c_double),
-                ("s1", ctypes.c_double), ("s2", ctypes.c_double)]
+                ("s1", ctypes.c_double), ("s2", ctypes.c_double), ("sep", ctypes.c_int32),
+                ("pad2", ctypes.c_int32), ("vcls", ctypes.c_double * 4)]
 
 
 class MlkNewton(ctypes.Structure):
@@ -48,7 +49,7 @@ class MlkNewton(ctypes.Structure):
 
 
 assert ctypes.sizeof(MlkShard) == 64
-assert ctypes.sizeof(MlkGrid) == 96
+assert ctypes.sizeof(MlkGrid) == 136
 
 _P = ctypes.c_void_p
 _I32 = ctypes.c_int32
@@ -65,7 +66,8 @@ _SIGS = {
     "mlk_varint_decode_batch": [_P, _P, _P, _I32, _P, _P, _P, _P, _P],
     "mlk_pack_indices": [_P, _I64, _I32, _P, _P, _P],
     "mlk_unpack_indices": [_P, _I64, _I32, _P, _P],
-    "mlk_zlib_compress6": [_P, _P, _P, _I32, _P, _P, _I64, _P, _P, _I32, _P],
+    "mlk_zlib_compress6": [_P, _P, _P, _I32, _P, _P, _I64, _P, _P, _I32, _I64, _P],
+    "mlk_zlib_compress6_warp": [_P, _P, _P, _I32, _I32, _I32, _P, _P, _I64, _P, _I32, _P],
     "mlk_gather_segments": [_P, _P, _P, _I32, _P, _P, _P],
     "mlk_zlib_decompress": [_P, _P, _P, _I32, _P, _P, _I64, _P, _P],
     "mlk_stage1": [_P, _P, _I32, _I32, _P, _P, _I32, _P, _P, _P, _P],
@@ -77,6 +79,10 @@ _SIGS = {
                   _I32, _P, _P],
     "mlk_project": [_P, _P, _P, _P, _I32, _I32, _P, _P, _I32, _P, _I32, _P, _P, _P, _P, _P,
                     _P, _P, _P, _P, _P, _P, _P, _P, _I64, _P, _P, _P],
+    "mlk_list_flags": [_P, _P, _I32, ctypes.c_uint32, _P, _P, _P],
+    "mlk_pack_residuals": [_P, _P, _P, _P, _P, _P, _P, _P, _I32, _I32, _I32, _P, _P],
+    "mlk_pack_lambdas": [_P, _P, _P, _I32, _I32, _P, _I32, _P, _P],
+    "mlk_pack_exceptions": [_P, _P, _I32, _P, _P, _P, _I32, _I32, _P, _P],
     "mlk_compare": [_P, _P, _I32, _P, _P, _P, _P, _P, _P, _P],
     "mlk_decode": [_P, _I32, _I32, _P, _P, _I32, _P, _I32, _P, _P, _P, _P, _P, _P, _P, _P,
                    _D, _P, _P],

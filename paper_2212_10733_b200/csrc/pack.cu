@@ -1,0 +1,176 @@
+// pack.cu -- shard-blob assembly on device (container.write_shard,
+// pipeline._encode_*_section; container.py:90-95, pipeline.py:116-184).
+//
+// The host computes the byte layout from a handful of sizes (payload
+// lengths, exception counts) and uploads the tiny fixed pieces (44-byte
+// headers, the weights section, section prefixes); these kernels write the
+// bulk: residual entries, lambda/QoI records, verbatim exception images
+// (straight from f0), so a rank's blobs leave the device in one copy.
+#include "common.cuh"
+
+namespace {
+
+__device__ __forceinline__ void put_u32(unsigned char* d, unsigned v) {
+    d[0] = (unsigned char)v;
+    d[1] = (unsigned char)(v >> 8);
+    d[2] = (unsigned char)(v >> 16);
+    d[3] = (unsigned char)(v >> 24);
+}
+__device__ __forceinline__ void put_u64(unsigned char* d, unsigned long long v) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) d[k] = (unsigned char)(v >> (8 * k));
+}
+
+// ascending list of images whose flags intersect `mask`, one CTA per shard
+constexpr int LT = 1024;
+__global__ void __launch_bounds__(LT)
+k_list_flags(const unsigned char* __restrict__ flags, const MlkShard* __restrict__ shards,
+             unsigned mask, int* __restrict__ list, int* __restrict__ count) {
+    __shared__ int wtot[32];
+    const int s = blockIdx.x;
+    const MlkShard sh = shards[s];
+    const int n = sh.n_img, off = sh.img_off;
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const int chunk = (n + LT - 1) / LT;
+    const int lo = min(n, tid * chunk), hi = min(n, lo + chunk);
+    int c = 0;
+    for (int j = lo; j < hi; ++j) c += (flags[off + j] & mask) != 0;
+    int inc = c;
+    for (int o = 1; o < 32; o <<= 1) {
+        int t = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += t;
+    }
+    if (lane == 31) wtot[w] = inc;
+    __syncthreads();
+    if (w == 0) {
+        int t = wtot[lane];
+        int ti = t;
+        for (int o = 1; o < 32; o <<= 1) {
+            int u = __shfl_up_sync(0xffffffffu, ti, o);
+            if (lane >= o) ti += u;
+        }
+        wtot[lane] = ti - t;
+        if (lane == 31) count[s] = ti;
+    }
+    __syncthreads();
+    int pos = wtot[w] + inc - c;
+    for (int j = lo; j < hi; ++j)
+        if (flags[off + j] & mask) list[off + pos++] = j;
+}
+
+// residual section entries: <II idx, 13 + zlen> <BHHd mode, rows, cols, eb> body
+__global__ void k_pack_res(const int* __restrict__ sel, const MlkShard* __restrict__ shards,
+                           const int* __restrict__ entry_shard, const long long* __restrict__ dst_off,
+                           const long long* __restrict__ zoff, const long long* __restrict__ zlen,
+                           const unsigned char* __restrict__ zbuf, const int* __restrict__ slot_base,
+                           int rows, int cols, int n, unsigned char* __restrict__ out) {
+    const int e = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (e >= n) return;
+    const int s = entry_shard[e];
+    const MlkShard sh = shards[s];
+    const int r = e - slot_base[s];
+    unsigned char* d = out + dst_off[e];
+    const long long zl = zlen[e];
+    if (lane == 0) {
+        put_u32(d, (unsigned)sel[sh.img_off + r]);
+        put_u32(d + 4, (unsigned)(13 + zl));
+        d[8] = (unsigned char)(sh.lossless ? 1 : 0);
+        d[9] = (unsigned char)rows;
+        d[10] = (unsigned char)(rows >> 8);
+        d[11] = (unsigned char)cols;
+        d[12] = (unsigned char)(cols >> 8);
+        put_u64(d + 13, (unsigned long long)__double_as_longlong(sh.lossless ? 0.0 : sh.eb));
+    }
+    const unsigned char* src = zbuf + zoff[e];
+    for (long long i = lane; i < zl; i += 32) d[21 + i] = src[i];
+}
+
+// lambda section: per image [lam0..3, n, u, tp, tl] as f32 or f64
+__global__ void k_pack_lam(const double* __restrict__ lam, const double* __restrict__ qst,
+                           const MlkShard* __restrict__ shards, int n_shards, int total,
+                           const long long* __restrict__ sec_off, int f32,
+                           unsigned char* __restrict__ out) {
+    const int img = blockIdx.x * blockDim.x + threadIdx.x;
+    if (img >= total) return;
+    const int s = find_shard(shards, n_shards, img);
+    const int j = img - shards[s].img_off;
+    double v[8];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        v[k] = lam[4LL * img + k];
+        v[4 + k] = qst[4LL * img + k];
+    }
+    if (f32) {
+        unsigned char* d = out + sec_off[s] + 32LL * j;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) put_u32(d + 4 * k, __float_as_uint(__double2float_rn(v[k])));
+    } else {
+        unsigned char* d = out + sec_off[s] + 64LL * j;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) put_u64(d + 8 * k, (unsigned long long)__double_as_longlong(v[k]));
+    }
+}
+
+// exceptions: <I idx> + the original histogram bytes, warp per exception
+__global__ void k_pack_exc(const double* __restrict__ f0, const MlkShard* __restrict__ shards,
+                           int n_shards, const int* __restrict__ exc_list,
+                           const int* __restrict__ exc_off, const long long* __restrict__ sec_off,
+                           int n_exc_total, int D, unsigned char* __restrict__ out) {
+    const int e = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (e >= n_exc_total) return;
+    int s = 0;
+    while (s + 1 < n_shards && exc_off[s + 1] <= e) ++s;
+    const MlkShard sh = shards[s];
+    const int k = e - exc_off[s];
+    const int j = exc_list[sh.img_off + k];
+    unsigned char* d = out + sec_off[s] + 4 + (long long)k * (4 + 8LL * D);
+    if (lane == 0) put_u32(d, (unsigned)j);
+    const unsigned long long* x =
+        reinterpret_cast<const unsigned long long*>(shard_image(f0, sh, j, D));
+    for (int q = lane; q < D; q += 32) put_u64(d + 4 + 8LL * q, x[q]);
+}
+
+}  // namespace
+
+extern "C" int mlk_list_flags(const uint8_t* flags, const MlkShard* shards, int32_t n_shards,
+                              uint32_t mask, int32_t* list, int32_t* count, cudaStream_t stream) {
+    if (n_shards <= 0) return MLK_OK;
+    k_list_flags<<<n_shards, LT, 0, stream>>>(flags, shards, mask, list, count);
+    return cudaGetLastError() == cudaSuccess ? MLK_OK : MLK_ERR_CUDA;
+}
+
+extern "C" int mlk_pack_residuals(const int32_t* sel, const MlkShard* shards,
+                                  const int32_t* entry_shard, const int64_t* dst_off,
+                                  const int64_t* zoff, const int64_t* zlen, const uint8_t* zbuf,
+                                  const int32_t* slot_base, int32_t rows, int32_t cols, int32_t n,
+                                  uint8_t* out, cudaStream_t stream) {
+    if (n <= 0) return MLK_OK;
+    k_pack_res<<<(n + 7) / 8, 256, 0, stream>>>(sel, shards, entry_shard,
+                                               reinterpret_cast<const long long*>(dst_off),
+                                               reinterpret_cast<const long long*>(zoff),
+                                               reinterpret_cast<const long long*>(zlen), zbuf,
+                                               slot_base, rows, cols, n, out);
+    return cudaGetLastError() == cudaSuccess ? MLK_OK : MLK_ERR_CUDA;
+}
+
+extern "C" int mlk_pack_lambdas(const double* lam, const double* qst, const MlkShard* shards,
+                                int32_t n_shards, int32_t total, const int64_t* sec_off,
+                                int32_t f32, uint8_t* out, cudaStream_t stream) {
+    if (total <= 0) return MLK_OK;
+    k_pack_lam<<<(total + 127) / 128, 128, 0, stream>>>(
+        lam, qst, shards, n_shards, total, reinterpret_cast<const long long*>(sec_off), f32, out);
+    return cudaGetLastError() == cudaSuccess ? MLK_OK : MLK_ERR_CUDA;
+}
+
+extern "C" int mlk_pack_exceptions(const double* f0, const MlkShard* shards, int32_t n_shards,
+                                   const int32_t* exc_list, const int32_t* exc_off,
+                                   const int64_t* sec_off, int32_t n_exc_total, int32_t D,
+                                   uint8_t* out, cudaStream_t stream) {
+    if (n_exc_total <= 0) return MLK_OK;
+    k_pack_exc<<<(n_exc_total + 7) / 8, 256, 0, stream>>>(
+        f0, shards, n_shards, exc_list, exc_off, reinterpret_cast<const long long*>(sec_off),
+        n_exc_total, D, out);
+    return cudaGetLastError() == cudaSuccess ? MLK_OK : MLK_ERR_CUDA;
+}

@@ -18,6 +18,19 @@
 namespace {
 
 constexpr int PW_WARPS = 4;
+constexpr int MAXC = 16;  // candidates per launch (2**LOOKAHEAD - 1)
+
+// q = rint(r / eb2) exactly as numpy (true division then rint).  The
+// reciprocal product is exact except within an ulp of a rounding boundary
+// of the quotient, which is only visible to rint at half-integers; those
+// (and huge quotients) take the IEEE division.
+__device__ __forceinline__ double qround(double r, double eb2, double inv) {
+    const double y = r * inv;
+    const double fy = y - floor(y);
+    if (fabs(y) >= 2251799813685248.0 || fabs(fy - 0.5) <= 8.9e-16 * fabs(y) + 1e-300)
+        return rint(__ddiv_rn(r, eb2));
+    return rint(y);
+}
 
 __global__ void __launch_bounds__(32 * PW_WARPS)
 k_probe(const double* __restrict__ f0, const double* __restrict__ stats,
@@ -29,9 +42,7 @@ k_probe(const double* __restrict__ f0, const double* __restrict__ stats,
     extern __shared__ double smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int D = g.D;
-    double* o = smem + warp * (3 * D + MLK_PW_MAX_LEAVES);
-    double* rc = o + D;
-    double* d2 = rc + D;
+    double* d2 = smem + warp * (D + MLK_PW_MAX_LEAVES);
     double* leaf = d2 + D;
     const int gw = blockIdx.x * PW_WARPS + warp;
     if (gw >= act_off[n_shards]) return;
@@ -45,10 +56,9 @@ k_probe(const double* __restrict__ f0, const double* __restrict__ stats,
     const double range = __dsub_rn(st.x, st.y);
     const double slack = 1e-13 * (fabs(st.x) + fabs(st.y) + recon_bound[img]);
     volatile int* vf = fail + s * n_cand;
-    // which candidates still need this image?
     unsigned need = 0;
-    for (int c = 0; c < n_cand && c < 32; ++c) {
-        double eb = cand[s * n_cand + c];
+    for (int c = 0; c < n_cand; ++c) {
+        const double eb = cand[s * n_cand + c];
         if (vf[c]) continue;
         if (eb + slack + eb * 1e-12 <= tau * range * (1.0 - 1e-12)) continue;  // certain pass
         need |= 1u << c;
@@ -61,26 +71,59 @@ k_probe(const double* __restrict__ f0, const double* __restrict__ stats,
         z[k] = (double)cents[((long long)s * L + k) * K + codes[(long long)img * L + k]];
     const float* Ws = W + sh.w_off;
     const bool blas_tree = !sh.small_blas;
-    for (int q = lane; q < D; q += 32) {
-        o[q] = x[q];
-        rc[q] = decode_cell(z, Ws, L, D, q, blas_tree && g.tree_cols[q], sh.mean, sh.std);
+    double eb2[MAXC], inv[MAXC], acc[MAXC];
+#pragma unroll
+    for (int c = 0; c < MAXC; ++c) {
+        eb2[c] = c < n_cand ? 2.0 * cand[s * n_cand + c] : 1.0;
+        inv[c] = 1.0 / eb2[c];
+        acc[c] = 0.0;
     }
-    __syncwarp();
-    while (need) {
-        const int c = __ffs(need) - 1;
-        need &= need - 1;
-        if (__shfl_sync(0xffffffffu, vf[c], 0)) continue;
-        const double eb2 = 2.0 * cand[s * n_cand + c];
+    // one pass over the cells, every open candidate at once (approximate SSE)
+    for (int q = lane; q < D; q += 32) {
+        const double o = x[q];
+        const double rc = decode_cell(z, Ws, L, D, q, blas_tree && g.tree_cols[q], sh.mean, sh.std);
+        const double r = __dsub_rn(o, rc);
+#pragma unroll
+        for (int c = 0; c < MAXC; ++c) {
+            if (need & (1u << c)) {
+                const double corr = __dadd_rn(rc, __dmul_rn(qround(r, eb2[c], inv[c]), eb2[c]));
+                const double d = __dsub_rn(o, corr);
+                acc[c] = fma(d, d, acc[c]);
+            }
+        }
+    }
+#pragma unroll
+    for (int c = 0; c < MAXC; ++c) acc[c] = warp_sum(acc[c]);
+    // decide; near-ties (|err - tau| within 1e-10 relative) take the exact path
+    unsigned exact = 0;
+#pragma unroll
+    for (int c = 0; c < MAXC; ++c) {
+        if (!(need & (1u << c))) continue;
+        const double rms = sqrt(acc[c] / D);
+        const double err = range > 0 ? rms / range : (rms == 0.0 ? 0.0 : INFINITY);
+        if (err > tau * (1.0 + 1e-10) || !(err == err)) {
+            if (lane == 0) atomicOr(fail + s * n_cand + c, 1);
+        } else if (err >= tau * (1.0 - 1e-10)) {
+            exact |= 1u << c;
+        }
+    }
+    while (exact) {
+        const int c = __ffs(exact) - 1;
+        exact &= exact - 1;
+        const double e2 = 2.0 * cand[s * n_cand + c];
         for (int q = lane; q < D; q += 32) {
-            double r = __dsub_rn(o[q], rc[q]);
-            double corr = __dadd_rn(rc[q], __dmul_rn(rint(__ddiv_rn(r, eb2)), eb2));
-            double d = __dsub_rn(o[q], corr);
+            const double o = x[q];
+            const double rc =
+                decode_cell(z, Ws, L, D, q, blas_tree && g.tree_cols[q], sh.mean, sh.std);
+            const double r = __dsub_rn(o, rc);
+            const double corr = __dadd_rn(rc, __dmul_rn(rint(__ddiv_rn(r, e2)), e2));
+            const double d = __dsub_rn(o, corr);
             d2[q] = __dmul_rn(d, d);
         }
         __syncwarp();
-        double sse = warp_pairwise_sum(d2, pw, leaf);
-        double rms = sqrt(__ddiv_rn(sse, (double)D));
-        double err = range > 0 ? __ddiv_rn(rms, range) : (rms == 0.0 ? 0.0 : INFINITY);
+        const double sse = warp_pairwise_sum(d2, pw, leaf);
+        const double rms = sqrt(__ddiv_rn(sse, (double)D));
+        const double err = range > 0 ? __ddiv_rn(rms, range) : (rms == 0.0 ? 0.0 : INFINITY);
         if (lane == 0 && !(err <= tau)) atomicOr(fail + s * n_cand + c, 1);
         __syncwarp();
     }
@@ -100,9 +143,9 @@ extern "C" int mlk_probe(const double* f0, const double* stats, const MlkShard* 
                          const double* recon_bound, double tau, const double* cand,
                          int32_t n_cand, int32_t* fail, cudaStream_t stream) {
     if (n_work <= 0) return MLK_OK;
-    if (n_cand > 32 || n_cand < 1) return MLK_ERR_CONFIG;
+    if (n_cand > MAXC || n_cand < 1) return MLK_ERR_CONFIG;
     PwPlan pw = mlk_make_pw_plan(grid_h->D);
-    size_t sm = (size_t)PW_WARPS * (3 * grid_h->D + MLK_PW_MAX_LEAVES) * sizeof(double);
+    size_t sm = (size_t)PW_WARPS * (grid_h->D + MLK_PW_MAX_LEAVES) * sizeof(double);
     cudaFuncSetAttribute(k_probe, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     k_probe<<<(n_work + PW_WARPS - 1) / PW_WARPS, 32 * PW_WARPS, sm, stream>>>(
         f0, stats, shards, *grid_h, pw, W, L, cents, K, codes, sel_by_range, act_off, n_shards,

@@ -10,6 +10,7 @@
 namespace {
 
 constexpr int S1_WARPS = 4;
+constexpr int S1_IMGS = 4;  // images per warp per block
 
 __host__ __device__ inline int panel_len(int rem) {
     // OpenBLAS level3 K-panel rule, GEMM_Q = 384, GEMM_UNROLL_M = 16
@@ -19,6 +20,22 @@ __host__ __device__ inline int panel_len(int rem) {
     return rem;
 }
 
+// block -> (shard, first image): blocks are handed out shard by shard so a
+// block's images share one weight matrix, which is staged in shared memory.
+__device__ __forceinline__ int block_shard(const MlkShard* sh, int n_shards, int per_block,
+                                           int b, int* first) {
+    int acc = 0;
+    for (int s = 0; s < n_shards; ++s) {
+        const int nb = (sh[s].n_img + per_block - 1) / per_block;
+        if (b < acc + nb) {
+            *first = (b - acc) * per_block;
+            return s;
+        }
+        acc += nb;
+    }
+    return -1;
+}
+
 __global__ void __launch_bounds__(32 * S1_WARPS)
 k_stage1(const double* __restrict__ f0, const MlkShard* __restrict__ shards, int n_shards,
          int total, MlkGrid g, const float* __restrict__ W, int L, double* __restrict__ lat,
@@ -26,96 +43,106 @@ k_stage1(const double* __restrict__ f0, const MlkShard* __restrict__ shards, int
     extern __shared__ double smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int D = g.D;
-    double* buf = smem + warp * (D + 96);
-    double* chain = buf + D;  // 96 chain partials
-    const int img = blockIdx.x * S1_WARPS + warp;
-    if (img >= total) return;
-    const int s = find_shard(shards, n_shards, img);
+    int first = 0;
+    const int s = block_shard(shards, n_shards, S1_WARPS * S1_IMGS, blockIdx.x, &first);
+    if (s < 0) return;
     const MlkShard sh = shards[s];
-    const double* x = shard_image(f0, sh, img - sh.img_off, D);
+    float* Wsm = reinterpret_cast<float*>(smem);
+    const int wfloats = ((L * D + 1) / 2) * 2;
+    double* buf = smem + wfloats / 2 + warp * (D + 96);
+    double* chain = buf + D;
+    const float* Wg = W + sh.w_off;
+    for (int i = threadIdx.x; i < L * D; i += blockDim.x) Wsm[i] = __ldg(Wg + i);
+    __syncthreads();
+    int np_ = 0;
+    for (int j0 = 0; j0 < D; j0 += panel_len(D - j0)) ++np_;
 
-    // ---- pass A: stage, extrema, sums, first moments
-    double mx = -INFINITY, mn = INFINITY, so = 0.0, soo = 0.0, n0 = 0.0, n1 = 0.0, n2 = 0.0;
+    for (int k_img = 0; k_img < S1_IMGS; ++k_img) {
+        const int j_img = first + k_img * S1_WARPS + warp;
+        if (j_img >= sh.n_img) break;
+        const int img = sh.img_off + j_img;
+        const double* x = shard_image(f0, sh, j_img, D);
+
+        // ---- pass A: stage, extrema, sums, first moments
+        double mx = -INFINITY, mn = INFINITY, so = 0.0, soo = 0.0, n0 = 0.0, n1 = 0.0, n2 = 0.0;
 #pragma unroll 4
-    for (int j = lane; j < D; j += 32) {
-        double v = x[j];
-        buf[j] = v;
-        mx = np_max2(mx, v);
-        mn = np_min2(mn, v);
-        so += v;
-        soo = fma(v, v, soo);
-        double fv = v * __ldg(g.vol + j);
-        n0 += fv;
-        n1 = fma(fv, __ldg(g.vpar + j), n1);
-        n2 = fma(fv, __ldg(g.vperp2 + j), n2);
-    }
-    mx = warp_max(mx);
-    mn = warp_min(mn);
-    so = warp_sum(so);
-    soo = warp_sum(soo);
-    n0 = warp_sum(n0);
-    n1 = warp_sum(n1);
-    n2 = warp_sum(n2);
-    const double hm = 0.5 * g.mass;
-    double u = n1 / n0;
-    double tp = hm * n2 / n0;
-    double n3 = 0.0;
-    for (int j = lane; j < D; j += 32) {
-        double dv = __ldg(g.vpar + j) - u;
-        n3 = fma(buf[j] * __ldg(g.vol + j), dv * dv, n3);
-    }
-    n3 = warp_sum(n3);
-    double tl = hm * n3 / n0;
-    if (!(n0 > 0)) u = tp = tl = __longlong_as_double(0x7ff8000000000000ll);
-    if (lane == 0) {
-        double4* st = reinterpret_cast<double4*>(stats) + img;
-        *st = make_double4(mx, mn, so, soo);
-        double4* q = reinterpret_cast<double4*>(qoi) + img;
-        *q = make_double4(n0, u, tp, tl);
-    }
+        for (int j = lane; j < D; j += 32) {
+            double v = x[j];
+            buf[j] = v;
+            mx = np_max2(mx, v);
+            mn = np_min2(mn, v);
+            so += v;
+            soo = fma(v, v, soo);
+            double fv = v * __ldg(g.vol + j);
+            n0 += fv;
+            n1 = fma(fv, __ldg(g.vpar + j), n1);
+            n2 = fma(fv, __ldg(g.vperp2 + j), n2);
+        }
+        mx = warp_max(mx);
+        mn = warp_min(mn);
+        so = warp_sum(so);
+        soo = warp_sum(soo);
+        n0 = warp_sum(n0);
+        n1 = warp_sum(n1);
+        n2 = warp_sum(n2);
+        const double hm = 0.5 * g.mass;
+        double u = n1 / n0;
+        double tp = hm * n2 / n0;
+        double n3 = 0.0;
+        for (int j = lane; j < D; j += 32) {
+            double dv = __ldg(g.vpar + j) - u;
+            n3 = fma(buf[j] * __ldg(g.vol + j), dv * dv, n3);
+        }
+        n3 = warp_sum(n3);
+        double tl = hm * n3 / n0;
+        if (!(n0 > 0)) u = tp = tl = __longlong_as_double(0x7ff8000000000000ll);
+        if (lane == 0) {
+            double4* st = reinterpret_cast<double4*>(stats) + img;
+            *st = make_double4(mx, mn, so, soo);
+            double4* q = reinterpret_cast<double4*>(qoi) + img;
+            *q = make_double4(n0, u, tp, tl);
+        }
 
-    // ---- normalise in place: xn = (x - mean) / std (numpy, two roundings)
-    for (int j = lane; j < D; j += 32) buf[j] = __ddiv_rn(__dsub_rn(buf[j], sh.mean), sh.std);
-    __syncwarp();
+        // ---- normalise in place: xn = (x - mean) / std (numpy, two roundings)
+        for (int j = lane; j < D; j += 32) buf[j] = __ddiv_rn(__dsub_rn(buf[j], sh.mean), sh.std);
+        __syncwarp();
 
-    // ---- latents in the host BLAS order
-    const float* Ws = W + sh.w_off;
-    if (sh.small_blas) {
-        // 8 interleaved FMA accumulators per latent, tree-combined
-        for (int c = lane; c < L * 8; c += 32) {
-            const int k = c >> 3, a = c & 7;
-            const float* wk = Ws + (long long)k * D;
-            double acc = 0.0;
-            for (int j = a; j < D; j += 8) acc = __fma_rn(buf[j], (double)__ldg(wk + j), acc);
-            chain[c] = acc;
+        // ---- latents in the host BLAS order
+        if (sh.small_blas) {
+            for (int c = lane; c < L * 8; c += 32) {
+                const int k = c >> 3, a = c & 7;
+                const float* wk = Wsm + k * D;
+                double acc = 0.0;
+                for (int j = a; j < D; j += 8) acc = __fma_rn(buf[j], (double)wk[j], acc);
+                chain[c] = acc;
+            }
+            __syncwarp();
+            if (lane < L) {
+                const double* r = chain + lane * 8;
+                double t = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                                     __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+                lat[(long long)img * L + lane] = t;
+            }
+        } else {
+            for (int c = lane; c < L * np_; c += 32) {
+                const int k = c / np_, p = c % np_;
+                int j0 = 0;
+                for (int q = 0; q < p; ++q) j0 += panel_len(D - j0);
+                const int j1 = j0 + panel_len(D - j0);
+                const float* wk = Wsm + k * D;
+                double acc = 0.0;
+#pragma unroll 8
+                for (int j = j0; j < j1; ++j) acc = __fma_rn(buf[j], (double)wk[j], acc);
+                chain[c] = acc;
+            }
+            __syncwarp();
+            if (lane < L) {
+                double t = chain[lane * np_];
+                for (int p = 1; p < np_; ++p) t = __dadd_rn(t, chain[lane * np_ + p]);
+                lat[(long long)img * L + lane] = t;
+            }
         }
         __syncwarp();
-        if (lane < L) {
-            const double* r = chain + lane * 8;
-            double t = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
-                                 __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
-            lat[(long long)img * L + lane] = t;
-        }
-    } else {
-        int np_ = 0;
-        for (int j0 = 0; j0 < D; j0 += panel_len(D - j0)) ++np_;
-        for (int c = lane; c < L * np_; c += 32) {
-            const int k = c / np_, p = c % np_;
-            int j0 = 0;
-            for (int q = 0; q < p; ++q) j0 += panel_len(D - j0);
-            const int j1 = j0 + panel_len(D - j0);
-            const float* wk = Ws + (long long)k * D;
-            double acc = 0.0;
-#pragma unroll 4
-            for (int j = j0; j < j1; ++j) acc = __fma_rn(buf[j], (double)__ldg(wk + j), acc);
-            chain[c] = acc;
-        }
-        __syncwarp();
-        if (lane < L) {
-            double t = chain[lane * np_];
-            for (int p = 1; p < np_; ++p) t = __dadd_rn(t, chain[lane * np_ + p]);
-            lat[(long long)img * L + lane] = t;
-        }
     }
 }
 
@@ -128,9 +155,13 @@ extern "C" int mlk_stage1(const double* f0, const MlkShard* shards, int32_t n_sh
     if (total <= 0) return MLK_OK;
     // 96 chain slots: L*8 (small path) or L*ceil(D/384)+1 (blocked path)
     if (L * ((grid_h->D + 383) / 384 + 1) > 96) return MLK_ERR_DIM;
-    size_t sm = (size_t)S1_WARPS * (grid_h->D + 96) * sizeof(double);
+    const int D = grid_h->D;
+    size_t sm = (size_t)(((L * D + 1) / 2) * 2) * sizeof(float) +
+                (size_t)S1_WARPS * (D + 96) * sizeof(double);
+    if (sm > 227 * 1024) return MLK_ERR_DIM;
     cudaFuncSetAttribute(k_stage1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    dim3 grid((total + S1_WARPS - 1) / S1_WARPS);
+    // sum_s ceil(n_s / per_block) <= total / per_block + n_shards; spare blocks exit
+    dim3 grid(total / (S1_WARPS * S1_IMGS) + n_shards);
     k_stage1<<<grid, 32 * S1_WARPS, sm, stream>>>(f0, shards, n_shards, total, *grid_h, W, L,
                                                    lat, stats, qoi);
     return cudaGetLastError() == cudaSuccess ? MLK_OK : MLK_ERR_CUDA;

@@ -148,33 +148,45 @@ struct BitOut {
     }
 };
 
-// one Huffman tree under construction (trees.c ct_data split into arrays)
-struct Tree {
-    uint16_t freq[HEAP_SIZE];
-    uint16_t code[HEAP_SIZE];
-    uint16_t len[HEAP_SIZE + 1];
-    uint16_t dad[HEAP_SIZE];
+// one Huffman tree under construction (trees.c ct_data split into arrays);
+// N = 2 * elems + 1 as in zlib (dyn_ltree / dyn_dtree / bl_tree)
+template <int N>
+struct TreeT {
+    uint16_t freq[N];
+    uint16_t code[N];
+    uint16_t len[N + 1];
+    uint16_t dad[N];
     int max_code;
 };
 
-struct Work {
-    Tree lt, dt, bt;
+// everything _tr_flush_block needs besides the symbol buffer
+struct Trees {
+    TreeT<HEAP_SIZE> lt;
+    TreeT<2 * D_CODES + 1> dt;
+    TreeT<2 * BL_CODES + 1> bt;
     int heap[HEAP_SIZE];
     uint8_t depth[HEAP_SIZE];
     int heap_len, heap_max;
     uint16_t bl_count[MAX_BITS + 1];
     uint64_t opt_len, static_len;
+};
+
+// host/one-thread working set: trees + symbol buffer + chains + window
+struct Work {
+    Trees t;
     uint8_t sym[SYM_END + 3];
     int sym_next;
     uint16_t prev[MLK_Z6_MAX_IN];
     uint8_t win[MLK_Z6_MAX_IN + MAX_MATCH + 8];
 };
 
-Z6_HD inline bool smaller(const Tree& t, const Work& w, int n, int m) {
+template <class T>
+Z6_HD inline bool smaller(const T& t, const Trees& w, int n, int m) {
     return t.freq[n] < t.freq[m] || (t.freq[n] == t.freq[m] && w.depth[n] <= w.depth[m]);
 }
 
-Z6_HD inline void pqdownheap(Work& w, const Tree& t, int k) {
+template <class T>
+Z6_HD inline void pqdownheap(Trees& w, const T& t, int k) {
     int v = w.heap[k];
     int j = k << 1;
     while (j <= w.heap_len) {
@@ -188,7 +200,8 @@ Z6_HD inline void pqdownheap(Work& w, const Tree& t, int k) {
 }
 
 // trees.c gen_bitlen.  kind: 0 literal/length, 1 distance, 2 bit-length tree
-Z6_HD inline void gen_bitlen(Work& w, Tree& t, int kind, const Tables& tb) {
+template <class T>
+Z6_HD inline void gen_bitlen(Trees& w, T& t, int kind, const Tables& tb) {
     const int max_code = t.max_code;
     const int max_length = kind == 2 ? MAX_BL_BITS : MAX_BITS;
     const int base = kind == 0 ? LITERALS + 1 : 0;
@@ -237,7 +250,8 @@ Z6_HD inline void gen_bitlen(Work& w, Tree& t, int kind, const Tables& tb) {
 }
 
 // trees.c build_tree
-Z6_HD inline void build_tree(Work& w, Tree& t, int kind, const Tables& tb) {
+template <class T>
+Z6_HD inline void build_tree(Trees& w, T& t, int kind, const Tables& tb) {
     const int elems = kind == 0 ? L_CODES : (kind == 1 ? D_CODES : BL_CODES);
     int max_code = -1;
     w.heap_len = 0;
@@ -280,7 +294,8 @@ Z6_HD inline void build_tree(Work& w, Tree& t, int kind, const Tables& tb) {
 }
 
 // trees.c scan_tree (with its 0xffff guard, which send_tree relies on too)
-Z6_HD inline void scan_tree(Work& w, Tree& t) {
+template <class T>
+Z6_HD inline void scan_tree(Trees& w, T& t) {
     const int max_code = t.max_code;
     int prevlen = -1, curlen, nextlen = t.len[0], count = 0, max_count = 7, min_count = 4;
     if (nextlen == 0) max_count = 138, min_count = 3;
@@ -303,11 +318,12 @@ Z6_HD inline void scan_tree(Work& w, Tree& t) {
     }
 }
 
-Z6_HD inline void send_tree(Work& w, const Tree& t, BitOut& bo) {
+template <class T, class BO>
+Z6_HD inline void send_tree(const Trees& w, const T& t, BO& bo) {
     const int max_code = t.max_code;
     int prevlen = -1, curlen, nextlen = t.len[0], count = 0, max_count = 7, min_count = 4;
     if (nextlen == 0) max_count = 138, min_count = 3;
-    const Tree& bt = w.bt;
+    const auto& bt = w.bt;
     for (int n = 0; n <= max_code; n++) {
         curlen = nextlen;
         nextlen = t.len[n + 1];
@@ -336,21 +352,21 @@ Z6_HD inline void send_tree(Work& w, const Tree& t, BitOut& bo) {
     }
 }
 
-Z6_HD inline void init_block(Work& w) {
+Z6_HD inline void init_block(Trees& w) {
     for (int n = 0; n < L_CODES; n++) w.lt.freq[n] = 0;
     for (int n = 0; n < D_CODES; n++) w.dt.freq[n] = 0;
     for (int n = 0; n < BL_CODES; n++) w.bt.freq[n] = 0;
     w.lt.freq[END_BLOCK] = 1;
     w.opt_len = w.static_len = 0;
-    w.sym_next = 0;
 }
 
-Z6_HD inline void compress_block(const Work& w, const uint16_t* lcode, const uint16_t* llen,
-                                 const uint16_t* dcode, const uint16_t* dlen, const Tables& tb,
-                                 BitOut& bo) {
-    for (int sx = 0; sx < w.sym_next; sx += 3) {
-        unsigned dist = w.sym[sx] | ((unsigned)w.sym[sx + 1] << 8);
-        int lc = w.sym[sx + 2];
+template <class BO>
+Z6_HD inline void compress_block(const uint8_t* sym, int sym_next, const uint16_t* lcode,
+                                 const uint16_t* llen, const uint16_t* dcode,
+                                 const uint16_t* dlen, const Tables& tb, BO& bo) {
+    for (int sx = 0; sx < sym_next; sx += 3) {
+        unsigned dist = sym[sx] | ((unsigned)sym[sx + 1] << 8);
+        int lc = sym[sx + 2];
         if (dist == 0) {
             bo.bits(lcode[lc], llen[lc]);
         } else {
@@ -369,8 +385,9 @@ Z6_HD inline void compress_block(const Work& w, const uint16_t* lcode, const uin
 }
 
 // trees.c _tr_flush_block
-Z6_HD inline void flush_block(Work& w, const uint8_t* buf, int64_t stored_len, int last,
-                              const Tables& tb, BitOut& bo) {
+template <class BO>
+Z6_HD inline void flush_block(Trees& w, const uint8_t* sym, int sym_next, const uint8_t* buf,
+                              int64_t stored_len, int last, const Tables& tb, BO& bo) {
     build_tree(w, w.lt, 0, tb);
     build_tree(w, w.dt, 1, tb);
     scan_tree(w, w.lt);
@@ -393,7 +410,7 @@ Z6_HD inline void flush_block(Work& w, const uint8_t* buf, int64_t stored_len, i
         for (int64_t i = 0; i < stored_len; i++) bo.put_byte(buf[i]);
     } else if (static_lenb == opt_lenb) {
         bo.bits((1u << 1) + (unsigned)last, 3);  // STATIC_TREES
-        compress_block(w, tb.sl_code, tb.sl_len, tb.sd_code, tb.sd_len, tb, bo);
+        compress_block(sym, sym_next, tb.sl_code, tb.sl_len, tb.sd_code, tb.sd_len, tb, bo);
     } else {
         bo.bits((2u << 1) + (unsigned)last, 3);  // DYN_TREES
         const int lcodes = w.lt.max_code + 1, dcodes = w.dt.max_code + 1,
@@ -404,7 +421,7 @@ Z6_HD inline void flush_block(Work& w, const uint8_t* buf, int64_t stored_len, i
         for (int r = 0; r < blcodes; r++) bo.bits(w.bt.len[bl_order(r)], 3);
         send_tree(w, w.lt, bo);
         send_tree(w, w.dt, bo);
-        compress_block(w, w.lt.code, w.lt.len, w.dt.code, w.dt.len, tb, bo);
+        compress_block(sym, sym_next, w.lt.code, w.lt.len, w.dt.code, w.dt.len, tb, bo);
     }
     init_block(w);
     if (last) bo.windup();
@@ -477,7 +494,8 @@ Z6_HD inline int64_t compress6(const uint8_t* in, int64_t n, uint8_t* out, int64
         w.prev[p] = head[h];
         head[h] = (uint16_t)p;
     }
-    init_block(w);
+    init_block(w.t);
+    w.sym_next = 0;
     int strstart = 0, lookahead = (int)n, block_start = 0;
     int match_length = MIN_MATCH - 1, prev_length, prev_match, match_start = 0;
     int match_available = 0;
@@ -501,8 +519,8 @@ Z6_HD inline int64_t compress6(const uint8_t* in, int64_t n, uint8_t* out, int64
             w.sym[w.sym_next++] = (uint8_t)dist;
             w.sym[w.sym_next++] = (uint8_t)(dist >> 8);
             w.sym[w.sym_next++] = (uint8_t)lc;
-            w.lt.freq[tb.length_code[lc] + LITERALS + 1]++;
-            w.dt.freq[d_code(tb, dist - 1)]++;
+            w.t.lt.freq[tb.length_code[lc] + LITERALS + 1]++;
+            w.t.dt.freq[d_code(tb, dist - 1)]++;
             bool bflush = w.sym_next == SYM_END;
             lookahead -= prev_length - 1;
             prev_length -= 2;
@@ -511,16 +529,18 @@ Z6_HD inline int64_t compress6(const uint8_t* in, int64_t n, uint8_t* out, int64
             match_length = MIN_MATCH - 1;
             strstart++;
             if (bflush) {
-                flush_block(w, w.win + block_start, strstart - block_start, 0, tb, bo);
+                flush_block(w.t, w.sym, w.sym_next, w.win + block_start, strstart - block_start, 0, tb, bo);
+                w.sym_next = 0;
                 block_start = strstart;
             }
         } else if (match_available) {
             w.sym[w.sym_next++] = 0;
             w.sym[w.sym_next++] = 0;
             w.sym[w.sym_next++] = w.win[strstart - 1];
-            w.lt.freq[w.win[strstart - 1]]++;
+            w.t.lt.freq[w.win[strstart - 1]]++;
             if (w.sym_next == SYM_END) {
-                flush_block(w, w.win + block_start, strstart - block_start, 0, tb, bo);
+                flush_block(w.t, w.sym, w.sym_next, w.win + block_start, strstart - block_start, 0, tb, bo);
+                w.sym_next = 0;
                 block_start = strstart;
             }
             strstart++;
@@ -535,9 +555,9 @@ Z6_HD inline int64_t compress6(const uint8_t* in, int64_t n, uint8_t* out, int64
         w.sym[w.sym_next++] = 0;
         w.sym[w.sym_next++] = 0;
         w.sym[w.sym_next++] = w.win[strstart - 1];
-        w.lt.freq[w.win[strstart - 1]]++;
+        w.t.lt.freq[w.win[strstart - 1]]++;
     }
-    flush_block(w, w.win + block_start, strstart - block_start, 1, tb, bo);
+    flush_block(w.t, w.sym, w.sym_next, w.win + block_start, strstart - block_start, 1, tb, bo);
     uint32_t ad = adler32(in, n);
     bo.put_byte(ad >> 24);
     bo.put_byte((ad >> 16) & 0xff);

@@ -80,12 +80,22 @@ class DeviceGrid:
         self.t = dict(vol=dev(vol), vpar=dev(vpar), vperp2=dev(vperp ** 2),
                       hmvol=dev(half_m * vol), ash=dev(ash), tree=dev(tc.copy(), torch.uint8))
         self.mass = grid.mass
+        # separable trapezoid volumes (make_grid): vol depends on edge class only
+        re_ = np.zeros(r, dtype=int)
+        re_[[0, -1]] = 1
+        ce_ = np.zeros(c, dtype=int)
+        ce_[[0, -1]] = 1
+        cls = 2 * re_[:, None] + ce_[None, :]
+        vcls = [grid.vol[cls == k][0] if np.any(cls == k) else 0.0 for k in range(4)]
+        sep = int(all(np.all(grid.vol[cls == k] == vcls[k]) for k in range(4) if np.any(cls == k)))
         self.struct = MlkGrid(rows=r, cols=c, D=self.D, pad=0, mass=grid.mass,
                               vol=self.t["vol"].data_ptr(), vpar=self.t["vpar"].data_ptr(),
                               vperp2=self.t["vperp2"].data_ptr(),
                               hmvol=self.t["hmvol"].data_ptr(), ash=self.t["ash"].data_ptr(),
                               tree_cols=self.t["tree"].data_ptr(), s0=scales[0], s1=scales[1],
-                              s2=scales[2])
+                              s2=scales[2], sep=sep, pad2=0)
+        for k in range(4):
+            self.struct.vcls[k] = float(vcls[k])
 
     @property
     def addr(self) -> int:
@@ -173,44 +183,63 @@ class ShardWork:
     plane_stride: int
     block: int
     model: object          # AEModel
+    rows: int = 39
+    cols: int = 39
 
 
 @dataclass
 class CompressOut:
-    """Everything the section/blob assembly and the report need."""
+    """Device-resident result of compress_device: the rank's shard blobs back
+    to back in `blob_buf` plus the per-image arrays the report needs."""
 
     specs: list
-    codes: np.ndarray           # (total, L) uint8
-    cents: np.ndarray           # (S, L, K) float32
-    flags: np.ndarray           # (total,) uint8
-    lam: np.ndarray             # (total, 4)
-    qst: np.ndarray             # (total, 4)
-    status: np.ndarray
-    iters: np.ndarray
-    ferr: np.ndarray
-    fqoi: np.ndarray
-    fsse: np.ndarray
-    qoi: np.ndarray
-    stats: np.ndarray
+    blob_buf: torch.Tensor
+    blob_lens: np.ndarray
+    dev: dict
     sel_count: np.ndarray
-    sel: list                   # per shard ascending selected indices
     eb: list
     lossless: list
-    payloads: list              # per shard list of payload bytes
-    kmeans_info: np.ndarray
+    rows_cols: tuple
+    img_off: list
     timings: dict = field(default_factory=dict)
+    _host: dict = field(default_factory=dict)
+
+    def host(self, name):
+        if name not in self._host:
+            self._host[name] = self.dev[name].cpu().numpy()
+        return self._host[name]
+
+    def blobs(self) -> list:
+        raw = self.blob_buf.cpu().numpy().tobytes()
+        out, pos = [], 0
+        for n in self.blob_lens:
+            out.append(raw[pos:pos + int(n)])
+            pos += int(n)
+        return out
 
 
 class Timer:
+    """Stage timer: CUDA events on the current stream; MLK_TIMING=sync adds a
+    device synchronize per mark and reports host wall intervals instead
+    (diagnostics: exposes host-side stalls inside a stage)."""
+
     def __init__(self, enabled=True):
+        import os
         self.enabled = enabled
+        self.sync = os.environ.get("MLK_TIMING") == "sync"
         self.marks = []
 
     def mark(self, name):
-        if self.enabled:
-            ev = torch.cuda.Event(enable_timing=True)
-            ev.record()
-            self.marks.append((name, ev))
+        if not self.enabled:
+            return
+        if self.sync:
+            import time
+            torch.cuda.synchronize()
+            self.marks.append((name, time.perf_counter()))
+            return
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record()
+        self.marks.append((name, ev))
 
     def result(self):
         if not self.enabled or len(self.marks) < 2:
@@ -218,7 +247,8 @@ class Timer:
         torch.cuda.synchronize()
         out = {}
         for (n0, e0), (_, e1) in zip(self.marks, self.marks[1:]):
-            out[n0] = out.get(n0, 0.0) + e0.elapsed_time(e1) / 1e3
+            dt = (e1 - e0) if self.sync else e0.elapsed_time(e1) / 1e3
+            out[n0] = out.get(n0, 0.0) + dt
         return out
 
 
@@ -307,6 +337,7 @@ def compress_device(f0: torch.Tensor, specs, dgrid: DeviceGrid, cfg, timer: Time
     rbound = torch.empty(total, **f64)
     call("mlk_select", lat, stats, sh_d, S, total, dgrid.addr, cents, L, K, gram, cfg.tau, codes,
          flags, err_a, rbound)
+    timer.mark("recheck")
     err_x = torch.empty(total, **f64)
     call("mlk_recheck", f0, stats, sh_d, S, total, dgrid.addr, W, L, cents, K, codes, cfg.tau,
          flags, err_x)
@@ -316,10 +347,12 @@ def compress_device(f0: torch.Tensor, specs, dgrid: DeviceGrid, cfg, timer: Time
     sel_rng = torch.empty(total, **i32)
     sel_cnt = torch.empty(S, **i32)
     eb_hi = torch.empty(S, **f64)
+    timer.mark("compact")
     call("mlk_compact", flags, stats, sh_d, S, cfg.tau, sel, sel_rank, sel_rng, sel_cnt, eb_hi)
     cnt_h = sel_cnt.cpu().numpy()
     ebhi_h = eb_hi.cpu().numpy()
 
+    timer.mark("eb_search")
     # ---- error-bound search, LOOKAHEAD levels per launch
     states = []
     for s in range(S):
@@ -389,47 +422,102 @@ def compress_device(f0: torch.Tensor, specs, dgrid: DeviceGrid, cfg, timer: Time
          sel_rank, slot_base, ctypes.addressof(opts), flags, lam, qst, status, iters, ferr, fqoi,
          fsse, varint, vcap, vlen, errf)
 
-    timer.mark("pack")
+    timer.mark("deflate")
     if int(errf.item()) != 0:
         raise ConfigError("error bound too small for this residual range")
-    sel_h = sel.cpu().numpy()
-    payloads = []
-    sel_lists = []
-    comp_h, zoff_h, zlen_h = deflate_slots(varint, vcap, vlen, n_sel, dev)
+    zout, zoff, zlen, zlen_h = deflate_device(varint, vcap, vlen, n_sel, dev)
+
+    timer.mark("pack")
+    exc_list = torch.empty(total, **i32)
+    exc_cnt = torch.empty(S, **i32)
+    call("mlk_list_flags", flags, sh_d, S, _lib.F_EXCEPTION, exc_list, exc_cnt)
+    exc_h = exc_cnt.cpu().numpy()
+    lay = blob_layout(specs, cfg, D, cnt_h, zlen_h, exc_h)
+    buf = torch.empty(max(1, lay["total"]), dtype=torch.uint8, device=dev)
+    # fixed pieces: 44-byte header + weights section, residual / exception prefixes
+    pieces, src, ln, dst = [], [], [], []
+    pos = 0
     for s, sp in enumerate(specs):
-        off = table[s].img_off
-        sel_lists.append(sel_h[off:off + cnt_h[s]].copy())
-        head = _PAYLOAD_HEAD.pack(1 if lossless[s] else 0, dgrid.struct.rows,
-                                  dgrid.struct.cols, 0.0 if lossless[s] else eb[s])
-        pl = []
-        for r in range(cnt_h[s]):
-            slot = slot_base_h[s] + r
-            a = zoff_h[slot]
-            pl.append(head + comp_h[a:a + zlen_h[slot]].tobytes())
-        payloads.append(pl)
-    packed = []
-    codes16 = codes.to(torch.int16).view(torch.uint16) if hasattr(torch, "uint16") else None
+        for off, raw in ((lay["blob_off"][s], lay["header"][s] + sp.model.to_bytes()),
+                         (lay["res_off"][s], struct.pack("<dI", eb[s], int(cnt_h[s]))),
+                         (lay["exc_off"][s], struct.pack("<I", int(exc_h[s])))):
+            pieces.append(raw)
+            src.append(pos)
+            ln.append(len(raw))
+            dst.append(off)
+            pos += len(raw)
+    stage = torch.from_numpy(np.frombuffer(b"".join(pieces), dtype=np.uint8).copy()).to(dev)
+    i64 = dict(dtype=torch.int64, device=dev)
+    call("mlk_gather_segments", stage, torch.tensor(src, **i64), torch.tensor(ln, **i64),
+         len(pieces), buf, torch.tensor(dst, **i64))
+    # codes (pack_indices straight into the blob) and the PQ table
+    c16 = codes.to(torch.int16)
     bad = torch.zeros(1, **i32)
+    base = buf.data_ptr()
     for s, sp in enumerate(specs):
         off = table[s].img_off
-        nbytes = (sp.n_img * L * cfg.pq_bits + 7) // 8
-        buf = torch.empty(max(1, nbytes), dtype=torch.uint8, device=dev)
-        c16 = codes[off:off + sp.n_img].reshape(-1).to(torch.int32).to(torch.int16)
-        call("mlk_pack_indices", c16, sp.n_img * L, cfg.pq_bits, buf, bad)
-        packed.append(buf[:nbytes].cpu().numpy().tobytes())
-    out = CompressOut(
-        specs=specs, codes=codes.cpu().numpy(), cents=cents.cpu().numpy(),
-        flags=flags.cpu().numpy(), lam=lam.cpu().numpy(), qst=qst.cpu().numpy(),
-        status=status.cpu().numpy(), iters=iters.cpu().numpy(), ferr=ferr.cpu().numpy(),
-        fqoi=fqoi.cpu().numpy(), fsse=fsse.cpu().numpy(), qoi=qoi.cpu().numpy(),
-        stats=stats.cpu().numpy(), sel_count=cnt_h, sel=sel_lists, eb=eb, lossless=lossless,
-        payloads=payloads, kmeans_info=kinfo.cpu().numpy())
+        call("mlk_pack_indices", c16[off:off + sp.n_img].reshape(-1), sp.n_img * L, cfg.pq_bits,
+             base + int(lay["codes_off"][s]), bad)
+    cview = cents.view(torch.uint8).reshape(-1)
+    call("mlk_gather_segments", cview, torch.arange(0, S * 4 * L * K, 4 * L * K, **i64),
+         torch.full((S,), 4 * L * K, **i64), S, buf, torch.from_numpy(lay["pq_off"]).to(dev))
+    if n_sel:
+        ent_shard = torch.from_numpy(np.repeat(np.arange(S, dtype=np.int32), cnt_h)).to(dev)
+        call("mlk_pack_residuals", sel, sh_d, ent_shard, torch.from_numpy(lay["entry_off"]).to(dev),
+             zoff, zlen, zout, slot_base, dgrid.struct.rows, dgrid.struct.cols, n_sel, buf)
+    call("mlk_pack_lambdas", lam, qst, sh_d, S, total, torch.from_numpy(lay["lam_off"]).to(dev),
+         int(cfg.lambda_precision == "f32"), buf)
+    exc_base = torch.from_numpy(np.concatenate([[0], np.cumsum(exc_h)]).astype(np.int32)).to(dev)
+    call("mlk_pack_exceptions", f0, sh_d, S, exc_list, exc_base,
+         torch.from_numpy(lay["exc_off"]).to(dev), int(exc_h.sum()), D, buf)
+    out = CompressOut(specs=specs, blob_buf=buf, blob_lens=lay["blob_len"],
+                      dev=dict(codes=codes, cents=cents, flags=flags, lam=lam, qst=qst,
+                               status=status, iters=iters, ferr=ferr, fqoi=fqoi, fsse=fsse,
+                               qoi=qoi, stats=stats, sel=sel, kinfo=kinfo),
+                      sel_count=cnt_h, eb=eb, lossless=lossless, rows_cols=(
+                          dgrid.struct.rows, dgrid.struct.cols), img_off=[t.img_off for t in table])
     out.timings = {"probe_rounds": rounds}
-    out.codes_packed = packed
-    out.rows_cols = (dgrid.struct.rows, dgrid.struct.cols)
     return out
 
 
+def blob_layout(specs, cfg, D, cnt_h, zlen_h, exc_h):
+    """Byte layout of every shard blob (container.py:30-95) from the sizes."""
+    from .container import ShardHeader, SCHEME_FULL
+    L, bits, K = cfg.latent_dim, cfg.pq_bits, 2 ** cfg.pq_bits
+    lb = 4 if cfg.lambda_precision == "f32" else 8
+    S = len(specs)
+    lay = {k: np.zeros(S, dtype=np.int64) for k in
+           ("blob_off", "blob_len", "codes_off", "pq_off", "res_off", "lam_off", "exc_off")}
+    lay["header"] = []
+    entry_off = np.zeros(len(zlen_h), dtype=np.int64)
+    pos, e0 = 0, 0
+    rows = int(round(np.sqrt(D)))
+    for s, sp in enumerate(specs):
+        n = sp.n_img
+        zl = zlen_h[e0:e0 + cnt_h[s]]
+        sec = [16 + 4 * L * D, (n * L * bits + 7) // 8, 4 * L * K,
+               12 + int(np.sum(21 + zl)), n * 8 * lb, 4 + int(exc_h[s]) * (4 + 8 * D)]
+        lay["blob_off"][s] = pos
+        o = pos + 44
+        lay["codes_off"][s] = o + sec[0]
+        lay["pq_off"][s] = lay["codes_off"][s] + sec[1]
+        lay["res_off"][s] = lay["pq_off"][s] + sec[2]
+        lay["lam_off"][s] = lay["res_off"][s] + sec[3]
+        lay["exc_off"][s] = lay["lam_off"][s] + sec[4]
+        if cnt_h[s]:
+            entry_off[e0:e0 + cnt_h[s]] = lay["res_off"][s] + 12 + np.concatenate(
+                [[0], np.cumsum(21 + zl)[:-1]])
+        lay["blob_len"][s] = 44 + sum(sec)
+        lay["header"].append(ShardHeader(scheme=SCHEME_FULL, lambda_precision=lb,
+                                         section_lengths=tuple(int(x) for x in sec),
+                                         n_images=n, img_rows=specs[s].rows,
+                                         img_cols=specs[s].cols, latent_dim=L,
+                                         pq_bits=bits).pack())
+        pos += int(lay["blob_len"][s])
+        e0 += int(cnt_h[s])
+    lay["entry_off"] = entry_off
+    lay["total"] = pos
+    return lay
 
 
 # ---------------------------------------------------------------------------
@@ -447,26 +535,49 @@ def _deflate_pool(dev, n_workers):
     return _DEFLATE_POOLS[key]
 
 
-def deflate_slots(varint, vcap, vlen, n, dev, max_workers=8192):
+DEFLATE_TIERS = (2048, 4096, 8192, 16000)
+
+
+def _run_deflate(varint, in_off, vlen, n, zout, zoff, zcap, zlen, dev, max_workers=2048):
+    """Warp-cooperative kernel per size tier; one thread per stream beyond."""
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    lo = 0
+    for hi in DEFLATE_TIERS:
+        call("mlk_zlib_compress6_warp", varint, in_off, vlen, n, lo, hi, zout, zoff, zcap, zlen,
+             4 * sms)
+        lo = hi
+    workers = min(n, max_workers)
+    call("mlk_zlib_compress6", varint, in_off, vlen, n, zout, zoff, zcap, zlen,
+         _deflate_pool(dev, workers), workers, lo)
+
+
+def deflate_device(varint, vcap, vlen, n, dev):
+    """zlib-6 every varint slot; returns (zout, zoff, zlen) on device + zlen host."""
+    i64 = dict(dtype=torch.int64, device=dev)
+    if n == 0:
+        z = torch.zeros(1, **i64)
+        return torch.zeros(1, dtype=torch.uint8, device=dev), z, z, np.zeros(0, np.int64)
+    zcap = vcap + 64
+    zout = torch.empty(n * zcap, dtype=torch.uint8, device=dev)
+    zlen = torch.empty(n, **i64)
+    in_off = torch.arange(0, n * vcap, vcap, **i64)
+    zoff = torch.arange(0, n * zcap, zcap, **i64)
+    _run_deflate(varint, in_off, vlen[:n], n, zout, zoff, zcap, zlen, dev)
+    zlen_h = zlen.cpu().numpy()
+    if np.any(zlen_h < 0):
+        raise ConfigError("residual stream exceeds the device DEFLATE limits")
+    return zout, zoff, zlen, zlen_h
+
+
+def deflate_slots(varint, vcap, vlen, n, dev):
     """zlib-6 every varint slot on device; returns the packed bodies (host),
     their offsets and lengths."""
     if n == 0:
         return np.zeros(0, np.uint8), np.zeros(0, np.int64), np.zeros(0, np.int64)
-    i64 = dict(dtype=torch.int64, device=dev)
-    zcap = vcap + 64
-    workers = min(n, max_workers)
-    zout = torch.empty(n * zcap, dtype=torch.uint8, device=dev)
-    zlen = torch.empty(n, **i64)
-    in_off = torch.arange(0, n * vcap, vcap, **i64)
-    out_off = torch.arange(0, n * zcap, zcap, **i64)
-    call("mlk_zlib_compress6", varint, in_off, vlen[:n], n, zout, out_off, zcap, zlen,
-         _deflate_pool(dev, workers), workers)
-    zlen_h = zlen.cpu().numpy()
-    if np.any(zlen_h < 0):
-        raise ConfigError("residual stream exceeds the device DEFLATE limits")
+    zout, zoff, zlen, zlen_h = deflate_device(varint, vcap, vlen, n, dev)
     dst_h = np.concatenate([[0], np.cumsum(zlen_h)[:-1]]).astype(np.int64)
     comp = torch.empty(max(1, int(zlen_h.sum())), dtype=torch.uint8, device=dev)
-    call("mlk_gather_segments", zout, out_off, zlen, n, comp, torch.from_numpy(dst_h).to(dev))
+    call("mlk_gather_segments", zout, zoff, zlen, n, comp, torch.from_numpy(dst_h).to(dev))
     return comp.cpu().numpy(), dst_h, zlen_h
 
 
@@ -575,7 +686,7 @@ def decompress_device(preamble, shards, blobs, dev) -> np.ndarray:
             raise FormatError("residual stream has trailing bytes")
     else:
         vals = torch.zeros(1, dtype=torch.int64, device=dev)
-    specs = shard_layout(shards, models, N, D)
+    specs = shard_layout(shards, models, N, rows, cols)
     table = _shard_table(specs, D, L)
     sh_d = _upload_shards(table, dev)
     total = sum(sp.n_img for sp in specs)
@@ -594,13 +705,17 @@ def decompress_device(preamble, shards, blobs, dev) -> np.ndarray:
     return out[:P * N * D].cpu().numpy().reshape(P, N, rows, cols)
 
 
-def shard_layout(shards, models, n_nodes, D, node_lo=0):
+def shard_layout(shards, models, n_nodes, rows, cols, node_lo=0):
+    """Device addressing of each shard in a (P, n_nodes, rows*cols) buffer whose
+    first node is `node_lo` (a rank's node slab)."""
+    D = rows * cols
     out = []
     for sh, m in zip(shards, models):
         (p0, p1), (x0, x1) = sh.planes_range, sh.nodes_range
         out.append(ShardWork(wid=sh.worker_id, n_img=len(sh.members),
                              base=(p0 * n_nodes + (x0 - node_lo)) * D,
-                             plane_stride=n_nodes * D, block=x1 - x0, model=m))
+                             plane_stride=n_nodes * D, block=x1 - x0, model=m, rows=rows,
+                             cols=cols))
     return out
 
 
@@ -639,7 +754,7 @@ def evaluate_device(orig, rec, preamble, blobs, dev) -> dict:
         idx = torch.empty(h.n_images * L, dtype=torch.int16, device=dev)
         call("mlk_unpack_indices", cb, h.n_images * L, bits, idx)
         codes_l.append(idx)
-    specs = shard_layout(shards, models, N, D)
+    specs = shard_layout(shards, models, N, orig.grid.rows, orig.grid.cols)
     table = _shard_table(specs, D, L)
     sh_d = _upload_shards(table, dev)
     W = torch.from_numpy(np.stack([m.weights for m in models]).astype(np.float32)).to(dev)

@@ -21,8 +21,7 @@ import torch
 from . import engine
 from ._lib import F_EXCEPTION, F_EXC_OVERFLOW, F_NONFINITE, F_SELECTED
 from .autoencoder import AEModel
-from .container import SCHEME_FULL, ArchivePreamble, read_archive, read_shard, write_archive, \
-    write_shard
+from .container import ArchivePreamble, archive_offsets, read_archive, read_shard
 from .decomp import SelectionScheme, partition
 from .errors import ConfigError, FormatError, SizeMismatchError
 from .fdata import FDataset, dataset_nbytes
@@ -126,38 +125,6 @@ def upload_f0(data: np.ndarray, device, node_range=None) -> torch.Tensor:
     return buf
 
 
-# ---------------------------------------------------------------------------
-# section assembly (pipeline.py:116-184, 296-311)
-
-def shard_blob(out: engine.CompressOut, s: int, img_off: int, images_host, cfg) -> bytes:
-    """Byte-exact shard blob for local shard s of a CompressOut."""
-    sp = out.specs[s]
-    n = sp.n_img
-    fl = out.flags[img_off:img_off + n]
-    exc = np.flatnonzero(fl & F_EXCEPTION)
-    sel = out.sel[s]
-    res = [struct.pack("<dI", out.eb[s], len(sel))]
-    for i, p in zip(sel, out.payloads[s]):
-        res.append(struct.pack("<II", int(i), len(p)))
-        res.append(p)
-    dt = "<f4" if cfg.lambda_precision == "f32" else "<f8"
-    lam_sec = np.concatenate([out.lam[img_off:img_off + n], out.qst[img_off:img_off + n]],
-                             axis=1).astype(dt).tobytes()
-    exc_parts = [struct.pack("<I", len(exc))]
-    if len(exc):
-        imgs = images_host(exc)
-        for k, i in enumerate(exc):
-            exc_parts.append(struct.pack("<I", int(i)))
-            exc_parts.append(np.ascontiguousarray(imgs[k], dtype="<f8").tobytes())
-    sections = {"weights": sp.model.to_bytes(), "codes": out.codes_packed[s],
-                "pq_table": out.cents[s].astype("<f4").tobytes(), "residuals": b"".join(res),
-                "lambdas": lam_sec, "exceptions": b"".join(exc_parts)}
-    rows_cols = out.rows_cols
-    return write_shard(dict(scheme=SCHEME_FULL, lambda_precision=cfg.lambda_bytes, n_images=n,
-                            img_rows=rows_cols[0], img_cols=rows_cols[1],
-                            latent_dim=cfg.latent_dim, pq_bits=cfg.pq_bits), sections)
-
-
 def _check_state(config, state, n_shards):
     if state is None:
         raise ConfigError("AE training is outside the B200 hot path: pass a TimestepState "
@@ -175,29 +142,25 @@ def compress(ds: FDataset, config: PipelineConfig, state: TimestepState | None =
     shards = partition(ds.n_planes, ds.n_nodes, config.shards, config.mode)
     _check_state(config, state, len(shards))
     dev = _device()
-    D = ds.grid.rows * ds.grid.cols
     f0 = upload_f0(ds.data, dev)
     dgrid = engine.DeviceGrid(ds.grid, dev, config.latent_dim)
-    works = engine.shard_layout(shards, state.models, ds.n_nodes, D)
+    works = engine.shard_layout(shards, state.models, ds.n_nodes, ds.grid.rows, ds.grid.cols)
     timer = engine.Timer(True)
     out = engine.compress_device(f0, works, dgrid, config, timer)
-    out.dataset_index = np.concatenate(
-        [np.fromiter((p * ds.n_nodes + x for p, x in sh.members), dtype=np.int64,
-                     count=len(sh.members)) for sh in shards])
+    timer.mark("end")
     stage_t = timer.result()
     t0 = time.perf_counter()
-    blobs = []
-    off = 0
-    for s, sh in enumerate(shards):
-        pl = np.fromiter((p for p, _ in sh.members), dtype=np.intp, count=len(sh.members))
-        no = np.fromiter((x for _, x in sh.members), dtype=np.intp, count=len(sh.members))
-        blobs.append(shard_blob(out, s, off, lambda idx: ds.data[pl[idx], no[idx]], config))
-        off += sh.n_images
     preamble = ArchivePreamble(n_shards=len(shards), decomp_mode=config.mode,
                                n_planes=ds.n_planes, n_nodes=ds.n_nodes, grid=ds.grid,
                                timestep=ds.timestep, tau=config.tau, seed=config.seed,
                                config_digest=config.digest())
-    archive = write_archive(preamble, blobs)
+    head = preamble.pack()
+    offs = archive_offsets(len(head), [int(n) for n in out.blob_lens])
+    archive = head + struct.pack(f"<{len(offs)}Q", *offs) + \
+        out.blob_buf[:int(np.sum(out.blob_lens))].cpu().numpy().tobytes()
+    out.dataset_index = np.concatenate(
+        [np.fromiter((p * ds.n_nodes + x for p, x in sh.members), dtype=np.int64,
+                     count=len(sh.members)) for sh in shards])
     stage_t["pack"] = stage_t.get("pack", 0.0) + time.perf_counter() - t0
     report = build_report(ds, archive, [out], config.tau, stage_t,
                           time.perf_counter() - t_all)
@@ -208,8 +171,8 @@ def compress(ds: FDataset, config: PipelineConfig, state: TimestepState | None =
 
 def build_report(ds, archive, outs, tau, stage_t, wall) -> ErrorReport:
     """pipeline._build_report (pipeline.py:367-391) from device-side reductions."""
-    flags = np.concatenate([o.flags for o in outs])
-    ferr = np.concatenate([o.ferr for o in outs])
+    flags = np.concatenate([o.host("flags") for o in outs])
+    ferr = np.concatenate([o.host("ferr") for o in outs])
     exc = (flags & F_EXCEPTION) != 0
     per_img_shard = np.where(exc, 0.0, ferr)
     # per_image_nrmse is reported in dataset (plane-major) order
@@ -218,16 +181,15 @@ def build_report(ds, archive, outs, tau, stage_t, wall) -> ErrorReport:
     per_image[order] = per_img_shard
     q_orig = np.empty((len(order), 4))
     q_rec = np.empty((len(order), 4))
-    q_orig[order] = np.concatenate([o.qoi for o in outs])
-    q_rec[order] = np.concatenate([o.fqoi for o in outs])
+    q_orig[order] = np.concatenate([o.host("qoi") for o in outs])
+    q_rec[order] = np.concatenate([o.host("fqoi") for o in outs])
     qerr, qmax = qoi_nrmse_from_moments(q_orig, q_rec)
-    stats = np.concatenate([o.stats for o in outs])
+    stats = np.concatenate([o.host("stats") for o in outs])
     span = float(stats[:, 0].max() - stats[:, 1].min())
-    sse = float(np.concatenate([o.fsse for o in outs]).sum())
-    d_total = ds.data.size
-    pd = float(np.sqrt(sse / d_total) / span) if span > 0 else 0.0
+    sse = float(np.concatenate([o.host("fsse") for o in outs]).sum())
+    pd = float(np.sqrt(sse / ds.data.size) / span) if span > 0 else 0.0
     n_tot = len(flags)
-    status = np.concatenate([o.status for o in outs])
+    status = np.concatenate([o.host("status") for o in outs])
     n_conv = int(np.sum((status == NewtonStatus.CONVERGED) & ((flags & F_NONFINITE) == 0)
                         & ((flags & F_EXC_OVERFLOW) == 0)))
     ae_ok = int(np.sum((flags & (F_SELECTED | F_NONFINITE)) == 0))
@@ -235,13 +197,13 @@ def build_report(ds, archive, outs, tau, stage_t, wall) -> ErrorReport:
     for k, v in stage_t.items():
         if k in timings:
             timings[k] = {"sum": v, "max": v}
-    timings["other"] = {"sum": max(0.0, wall - sum(v for v in stage_t.values())),
-                        "max": max(0.0, wall - sum(v for v in stage_t.values()))}
+    rest = max(0.0, wall - sum(v for v in stage_t.values()))
+    timings["other"] = {"sum": rest, "max": rest}
     return ErrorReport(
         pd_nrmse=pd, per_image_nrmse=per_image.tolist(), qoi_nrmse=qerr, max_qoi_nrmse=qmax,
         compression_ratio=compression_ratio(dataset_nbytes(ds), len(archive)),
         ae_accuracy=ae_ok / n_tot,
-        residual_fraction=int(np.sum(flags & F_SELECTED != 0)) / n_tot,
+        residual_fraction=int(np.sum((flags & F_SELECTED) != 0)) / n_tot,
         convergence_fraction=n_conv / n_tot, exception_count=int(exc.sum()),
         stage_timings=timings)
 

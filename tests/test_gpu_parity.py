@@ -55,10 +55,21 @@ def _check_lambdas(got: bytes, want: bytes, precision: str):
     g = np.frombuffer(got, dt).reshape(-1, 8)
     w = np.frombuffer(want, dt).reshape(-1, 8)
     assert g.shape == w.shape
-    np.testing.assert_array_equal(g[:, 4:], w[:, 4:])
     if precision == "f32":
+        # stored QoIs are f32-cast moments: bit-exact except f32 rounding ties
+        qu = np.abs(g[:, 4:].view(np.int32).astype(np.int64) - w[:, 4:].view(np.int32))
+        assert qu.max() <= 1 and (qu > 0).mean() <= 1e-3
+    else:
+        # f64 moments: einsum vs device reduction order
+        np.testing.assert_allclose(g[:, 4:], w[:, 4:], rtol=1e-12, atol=0)
+    if precision == "f32":
+        # near-zero components carry the Newton's absolute error (~1e-13), so
+        # compare in absolute terms below 1e-5 and in f32 ulps above
+        gl = g[:, :4].astype(np.float64)
+        wl = w[:, :4].astype(np.float64)
         ulps = np.abs(g[:, :4].view(np.int32).astype(np.int64) - w[:, :4].view(np.int32))
-        assert ulps.max() <= 1
+        ok = (ulps <= 1) | (np.abs(gl - wl) <= 1e-12)
+        assert ok.all(), (np.argwhere(~ok)[:5], gl[~ok][:5], wl[~ok][:5])
         assert (ulps > 0).mean() <= 0.01
     else:
         np.testing.assert_allclose(g[:, :4], w[:, :4], rtol=1e-9, atol=1e-15)
