@@ -153,11 +153,12 @@ int mlk_zlib_compress6(const uint8_t* in, const int64_t* in_off, const int64_t* 
 
 /* Same bytes as mlk_zlib_compress6, one warp per stream with the working set
  * in shared memory, for the streams with nmin < in_len <= nmax (<= 16000);
- * run it over the size tiers, then mlk_zlib_compress6 for larger streams. */
+ * run it over the size tiers, then mlk_zlib_compress6 for larger streams.
+ * prof (may be NULL): 10 u64 cycle/counter accumulators for diagnostics. */
 int mlk_zlib_compress6_warp(const uint8_t* in, const int64_t* in_off, const int64_t* in_len,
                             int32_t n, int32_t nmin, int32_t nmax, uint8_t* out,
                             const int64_t* out_off, int64_t out_cap, int64_t* out_len,
-                            int32_t n_blocks, cudaStream_t stream);
+                            int32_t n_blocks, uint64_t* prof, cudaStream_t stream);
 
 /* dst[dst_off[i] .. + len[i]) = src[src_off[i] .. + len[i]) for n segments */
 int mlk_gather_segments(const uint8_t* src, const int64_t* src_off, const int64_t* len,
@@ -181,11 +182,12 @@ int mlk_stage1(const double* f0, const MlkShard* shards, int32_t n_shards, int32
 /* quantizer.pq_train (quantizer.py:99-108; kmeans_1d 53-91) for every
  * (shard, dim): first_idx / draws are the PCG64 draws kmeans_1d consumes
  * (one integers() then K-1 random(), computed by the host from the seed).
- * shards_h is a HOST array.  cents (n_shards, L, K) float32, sorted;
+ * shards (device) and shards_h (the same table on the host, for validation).  cents (n_shards, L, K) float32, sorted;
  * scratch >= 4 * L * total doubles; info (n_shards, L, 4). */
-int mlk_kmeans(const double* lat, const MlkShard* shards_h, int32_t n_shards, int32_t L,
-               int32_t K, const int64_t* first_idx, const double* draws, double* scratch,
-               float* cents, int32_t* info, cudaStream_t stream);
+int mlk_kmeans(const double* lat, const MlkShard* shards, const MlkShard* shards_h,
+               int32_t n_shards, int32_t L, int32_t K, const int64_t* first_idx,
+               const double* draws, double* scratch, float* cents, int32_t* info,
+               cudaStream_t stream);
 
 /* pq_encode + AE-error decision (quantizer.py:111-120; pipeline.py:228-235):
  * codes (total, L) u8; flags gets SELECTED or RECHECK.  gram holds per shard

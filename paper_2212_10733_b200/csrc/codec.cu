@@ -57,7 +57,7 @@ namespace wz {
 
 struct Lay {
     int nmax, T, direct;  // direct: a 32K-entry u16 table indexed by the hash
-    int win, p1, p4, p16, trees, sym, hash, total;
+    int win, p1, p4, p16, trees, obuf, sym, hash, total;
 };
 
 __host__ __device__ inline int pow2ge(int x) {
@@ -71,17 +71,19 @@ __host__ __device__ inline Lay layout(int nmax) {
     Lay L;
     L.nmax = nmax;
     L.direct = nmax > 4096;
-    L.T = L.direct ? 32768 : pow2ge(2 * nmax + 2);
+    L.T = L.direct ? 32768 : pow2ge(nmax + 2);
     int o = 0;
     L.win = o;
     o += al16(nmax + z6::MAX_MATCH + 16);
     // prev tables (matching) alias the Huffman trees (flush)
     int chains = al16(2 * nmax) * 3;
-    int trees = al16((int)sizeof(z6::Trees));
+    // trees + the block's output bit buffer (u64 words)
+    int trees = al16((int)sizeof(z6::Trees)) + al16(nmax + 256);
     L.p1 = o;
     L.p4 = o + al16(2 * nmax);
     L.p16 = o + 2 * al16(2 * nmax);
     L.trees = o;
+    L.obuf = o + al16((int)sizeof(z6::Trees));
     o += chains > trees ? chains : trees;
     // the hash table (chain building) aliases the symbol buffer (matching)
     int sym = al16(3 * nmax + 8);
@@ -107,12 +109,44 @@ __device__ __forceinline__ int jump(const uint16_t* p1, const uint16_t* p4, cons
 
 // zlib longest_match length of window[c..] against window[p..] (bytes 0, 1
 // checked, byte 2 implied by the hash, then 3..258)
+__device__ __forceinline__ unsigned long long load8(const uint8_t* w, int i) {
+    // 8 bytes at any offset from 4-byte-aligned words (the window is 16-aligned
+    // and padded beyond n + 258)
+    const unsigned* u = reinterpret_cast<const unsigned*>(w);
+    const int q = i >> 2, r = (i & 3) * 8;
+    const unsigned a = u[q], b = u[q + 1], c = u[q + 2];
+    const unsigned lo = r ? __funnelshift_r(a, b, r) : a;
+    const unsigned hi = r ? __funnelshift_r(b, c, r) : b;
+    return ((unsigned long long)hi << 32) | lo;
+}
+
 __device__ __forceinline__ int match_len(const uint8_t* win, int p, int c) {
     if (win[c] != win[p] || win[c + 1] != win[p + 1]) return 0;
     int k = 3;
-    while (k < z6::MAX_MATCH && win[c + k] == win[p + k]) ++k;
-    return k;
+    while (k < z6::MAX_MATCH) {
+        const unsigned long long x = load8(win, p + k) ^ load8(win, c + k);
+        if (x) {
+            k += (__ffsll((long long)x) - 1) >> 3;
+            return k < z6::MAX_MATCH ? k : z6::MAX_MATCH;
+        }
+        k += 8;
+    }
+    return z6::MAX_MATCH;
 }
+
+// sequential bit writer into a shared u64 buffer (lane 0 only)
+struct SBit {
+    unsigned long long* w;
+    long long bit;
+    __device__ void bits(unsigned value, int len) {
+        if (!len) return;
+        const long long q = bit >> 6;
+        const int sh = (int)(bit & 63);
+        w[q] |= (unsigned long long)value << sh;
+        if (sh + len > 64) w[q + 1] |= (unsigned long long)value >> (64 - sh);
+        bit += len;
+    }
+};
 
 struct GBit {  // lane-0 bit writer into global memory
     uint8_t* out;
@@ -147,7 +181,8 @@ __global__ void __launch_bounds__(256)
 k_deflate_warp(const uint8_t* __restrict__ in, const long long* __restrict__ in_off,
                const long long* __restrict__ in_len, int n_streams, uint8_t* __restrict__ out,
                const long long* __restrict__ out_off, long long out_cap,
-               long long* __restrict__ out_len, int nmin, int nmax) {
+               long long* __restrict__ out_len, int nmin, int nmax,
+               unsigned long long* __restrict__ prof) {
     __shared__ z6::Tables tb;
     extern __shared__ __align__(16) uint8_t zsm[];
     if (threadIdx.x == 0) z6::init_tables(tb);
@@ -171,6 +206,7 @@ k_deflate_warp(const uint8_t* __restrict__ in, const long long* __restrict__ in_
         const int n = (int)in_len[s];
         if (n <= nmin || n > nmax) continue;  // another tier handles it
         const uint8_t* src = in + in_off[s];
+        long long t_0 = clock64();
         // ---- window + zero pad, Adler-32 (lane-parallel sums)
         unsigned long long sa = 0, sb = 0;
         for (int i = lane; i < n; i += 32) {
@@ -192,6 +228,7 @@ k_deflate_warp(const uint8_t* __restrict__ in, const long long* __restrict__ in_
             for (int i = lane; i < Ly.T; i += 32) htab[i] = 0u;
         }
         __syncwarp();
+        long long t_1 = clock64();
         // ---- prev[] (hash chains), 32 positions per step
         const int n_ins = n - z6::MIN_MATCH + 1;  // positions 0 .. n-3
         for (int b0 = 0; b0 < n_ins; b0 += 32) {
@@ -237,6 +274,7 @@ k_deflate_warp(const uint8_t* __restrict__ in, const long long* __restrict__ in_
             }
             __syncwarp();
         }
+        long long t_2 = clock64();
         for (int p = lane; p < n; p += 32) {
             int x = p < n_ins ? p1[p] : 0;
             if (p >= n_ins) p1[p] = 0;
@@ -254,6 +292,9 @@ k_deflate_warp(const uint8_t* __restrict__ in, const long long* __restrict__ in_
             p16[p] = (uint16_t)x;
         }
         __syncwarp();
+        long long t_3 = clock64();
+        long long t_lm = 0;
+        int n_calls = 0;
         // ---- deflate_slow, warp-uniform state
         int strstart = 0, lookahead = n;
         int match_length = z6::MIN_MATCH - 1, prev_length, prev_match, match_start = 0;
@@ -265,6 +306,8 @@ k_deflate_warp(const uint8_t* __restrict__ in, const long long* __restrict__ in_
             match_length = z6::MIN_MATCH - 1;
             if (hash_head != 0 && prev_length < z6::LAZY &&
                 strstart - hash_head <= z6::MAX_DIST) {
+                const long long tlm0 = clock64();
+                ++n_calls;
                 const int chain = prev_length >= z6::GOOD ? z6::CHAIN / 4 : z6::CHAIN;
                 const int nice = lookahead < z6::NICE ? lookahead : z6::NICE;
                 const int thr = nice > prev_length + 1 ? nice : prev_length + 1;
@@ -294,6 +337,7 @@ k_deflate_warp(const uint8_t* __restrict__ in, const long long* __restrict__ in_
                 if (match_length <= 5 && match_length == z6::MIN_MATCH &&
                     strstart - match_start > z6::TOO_FAR)
                     match_length = z6::MIN_MATCH - 1;
+                t_lm += clock64() - tlm0;
             }
             if (prev_length >= z6::MIN_MATCH && match_length <= prev_length) {
                 if (lane == 0) {
@@ -332,9 +376,16 @@ k_deflate_warp(const uint8_t* __restrict__ in, const long long* __restrict__ in_
             sym_next += 3;
         }
         __syncwarp();
-        // ---- trees + bit stream (lane 0), prev tables are dead now
+        long long t_4 = clock64();
+        // ---- trees (lane 0) + bit stream (all lanes); prev tables are dead now
+        z6::Trees& t = *trees;
+        unsigned long long* ob = reinterpret_cast<unsigned long long*>(base + Ly.obuf);
+        const int obw = (n + 256) / 8;  // u64 words available
+        for (int i = lane; i < obw; i += 32) ob[i] = 0ull;
+        __shared__ int sh_kind[8];
+        __shared__ long long sh_hbits[8];
+        __syncwarp();
         if (lane == 0) {
-            z6::Trees& t = *trees;
             z6::init_block(t);
             for (int sx = 0; sx < sym_next; sx += 3) {
                 const unsigned dist = sym[sx] | ((unsigned)sym[sx + 1] << 8);
@@ -346,16 +397,152 @@ k_deflate_warp(const uint8_t* __restrict__ in, const long long* __restrict__ in_
                     t.dt.freq[z6::d_code(tb, dist - 1)]++;
                 }
             }
-            wz::GBit bo{out + out_off[s], out_cap, 0, 0ull, 0, false};
-            bo.put_byte(0x78);
-            bo.put_byte(0x9c);
-            z6::flush_block(t, sym, sym_next, win, strstart, 1, tb, bo);
-            const unsigned ad = (ad_b << 16) | ad_a;
-            bo.put_byte(ad >> 24);
-            bo.put_byte((ad >> 16) & 0xff);
-            bo.put_byte((ad >> 8) & 0xff);
-            bo.put_byte(ad & 0xff);
-            out_len[s] = bo.overflow ? -1 : bo.pos;
+            z6::build_tree(t, t.lt, 0, tb);
+            z6::build_tree(t, t.dt, 1, tb);
+            z6::scan_tree(t, t.lt);
+            z6::scan_tree(t, t.dt);
+            z6::build_tree(t, t.bt, 2, tb);
+            int max_blindex;
+            for (max_blindex = z6::BL_CODES - 1; max_blindex >= 3; max_blindex--)
+                if (t.bt.len[z6::bl_order(max_blindex)] != 0) break;
+            t.opt_len += 3 * ((uint64_t)max_blindex + 1) + 5 + 5 + 4;
+            uint64_t opt_lenb = (t.opt_len + 3 + 7) >> 3;
+            const uint64_t static_lenb = (t.static_len + 3 + 7) >> 3;
+            if (static_lenb <= opt_lenb) opt_lenb = static_lenb;
+            wz::SBit sb{ob, 16};  // after the 2-byte zlib header
+            int kind;
+            if ((uint64_t)strstart + 4 <= opt_lenb) {
+                kind = 0;  // stored
+                sb.bits(1u, 3);
+            } else if (static_lenb == opt_lenb) {
+                kind = 1;
+                sb.bits((1u << 1) + 1u, 3);
+            } else {
+                kind = 2;
+                sb.bits((2u << 1) + 1u, 3);
+                const int lcodes = t.lt.max_code + 1, dcodes = t.dt.max_code + 1,
+                          blcodes = max_blindex + 1;
+                sb.bits((unsigned)(lcodes - 257), 5);
+                sb.bits((unsigned)(dcodes - 1), 5);
+                sb.bits((unsigned)(blcodes - 4), 4);
+                for (int r = 0; r < blcodes; r++) sb.bits(t.bt.len[z6::bl_order(r)], 3);
+                z6::send_tree(t, t.lt, sb);
+                z6::send_tree(t, t.dt, sb);
+            }
+            sh_kind[warp] = kind;
+            sh_hbits[warp] = sb.bit;
+        }
+        __syncwarp();
+        const int kind = sh_kind[warp];
+        long long bitpos = sh_hbits[warp];
+        long long nbytes;
+        if (kind == 0) {
+            // stored block: windup, LEN, NLEN, raw bytes
+            const long long b0 = (bitpos + 7) >> 3;
+            uint8_t* ob8 = reinterpret_cast<uint8_t*>(ob);
+            if (lane == 0) {
+                ob8[b0] = (uint8_t)strstart;
+                ob8[b0 + 1] = (uint8_t)(strstart >> 8);
+                ob8[b0 + 2] = (uint8_t)~strstart;
+                ob8[b0 + 3] = (uint8_t)(~strstart >> 8);
+            }
+            for (int i = lane; i < strstart; i += 32) ob8[b0 + 4 + i] = win[i];
+            nbytes = b0 + 4 + strstart;
+        } else {
+            const uint16_t* lcode = kind == 1 ? tb.sl_code : t.lt.code;
+            const uint16_t* llen = kind == 1 ? tb.sl_len : t.lt.len;
+            const uint16_t* dcode = kind == 1 ? tb.sd_code : t.dt.code;
+            const uint16_t* dlen = kind == 1 ? tb.sd_len : t.dt.len;
+            const int nsym = sym_next / 3;
+            for (int k0 = 0; k0 < nsym; k0 += 32) {
+                const int k = k0 + lane;
+                unsigned long long val = 0;
+                int nb = 0;
+                if (k < nsym) {
+                    const unsigned dist = sym[3 * k] | ((unsigned)sym[3 * k + 1] << 8);
+                    const int lc = sym[3 * k + 2];
+                    if (dist == 0) {
+                        val = lcode[lc];
+                        nb = llen[lc];
+                    } else {
+                        int code = tb.length_code[lc];
+                        val = lcode[code + z6::LITERALS + 1];
+                        nb = llen[code + z6::LITERALS + 1];
+                        int extra = z6::extra_lbits(code);
+                        if (extra) {
+                            val |= (unsigned long long)(lc - tb.base_length[code]) << nb;
+                            nb += extra;
+                        }
+                        const unsigned d = dist - 1;
+                        code = z6::d_code(tb, d);
+                        val |= (unsigned long long)dcode[code] << nb;
+                        nb += dlen[code];
+                        extra = z6::extra_dbits(code);
+                        if (extra) {
+                            val |= (unsigned long long)(d - (unsigned)tb.base_dist[code]) << nb;
+                            nb += extra;
+                        }
+                    }
+                }
+                int inc = nb;
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int tt = __shfl_up_sync(FULL, inc, o);
+                    if (lane >= o) inc += tt;
+                }
+                if (nb) {
+                    const long long at = bitpos + inc - nb;
+                    const long long q = at >> 6;
+                    const int sh = (int)(at & 63);
+                    atomicOr(ob + q, val << sh);
+                    if (sh + nb > 64) atomicOr(ob + q + 1, val >> (64 - sh));
+                }
+                bitpos += __shfl_sync(FULL, inc, 31);
+            }
+            __syncwarp();
+            if (lane == 0) {
+                wz::SBit sb{ob, bitpos};
+                sb.bits(lcode[z6::END_BLOCK], llen[z6::END_BLOCK]);
+                bitpos = sb.bit;
+            }
+            bitpos = __shfl_sync(FULL, bitpos, 0);
+            nbytes = (bitpos + 7) >> 3;
+        }
+        __syncwarp();
+        // ---- zlib header + body + Adler-32 to global memory
+        {
+            const uint8_t* ob8 = reinterpret_cast<const uint8_t*>(ob);
+            uint8_t* dst = out + out_off[s];
+            const long long total = nbytes + 4;
+            if (total > out_cap) {
+                if (lane == 0) out_len[s] = -1;
+            } else {
+                for (long long i = lane; i < nbytes; i += 32)
+                    dst[i] = i == 0 ? 0x78 : (i == 1 ? 0x9c : ob8[i]);
+                const unsigned ad = (ad_b << 16) | ad_a;
+                if (lane == 0) {
+                    dst[nbytes] = ad >> 24;
+                    dst[nbytes + 1] = (ad >> 16) & 0xff;
+                    dst[nbytes + 2] = (ad >> 8) & 0xff;
+                    dst[nbytes + 3] = ad & 0xff;
+                    out_len[s] = total;
+                }
+            }
+        }
+        if (lane == 0) {
+            if (prof) {
+                long long t_5 = clock64();
+                (void)t_5;
+                atomicAdd(prof + 0, (unsigned long long)(t_1 - t_0));
+                atomicAdd(prof + 1, (unsigned long long)(t_2 - t_1));
+                atomicAdd(prof + 2, (unsigned long long)(t_3 - t_2));
+                atomicAdd(prof + 3, (unsigned long long)(t_4 - t_3));
+                atomicAdd(prof + 4, (unsigned long long)t_lm);
+                atomicAdd(prof + 5, (unsigned long long)(t_5 - t_4));
+                atomicAdd(prof + 6, (unsigned long long)n_calls);
+                atomicAdd(prof + 7, 1ull);
+                atomicAdd(prof + 8, (unsigned long long)n);
+                atomicAdd(prof + 9, (unsigned long long)(sym_next / 3));
+            }
         }
         __syncwarp();
     }
@@ -383,7 +570,7 @@ extern "C" int mlk_zlib_compress6_warp(const uint8_t* in, const int64_t* in_off,
                                        const int64_t* in_len, int32_t n, int32_t nmin,
                                        int32_t nmax, uint8_t* out, const int64_t* out_off,
                                        int64_t out_cap, int64_t* out_len, int32_t n_blocks,
-                                       cudaStream_t stream) {
+                                       uint64_t* prof, cudaStream_t stream) {
     if (n <= 0) return MLK_OK;
     if (nmax > 16000 || nmax < 1) return MLK_ERR_CONFIG;
     const wz::Lay Ly = wz::layout(nmax);
@@ -395,7 +582,8 @@ extern "C" int mlk_zlib_compress6_warp(const uint8_t* in, const int64_t* in_off,
     k_deflate_warp<<<n_blocks, 32 * zw, sm, stream>>>(
         in, reinterpret_cast<const long long*>(in_off), reinterpret_cast<const long long*>(in_len),
         n, out, reinterpret_cast<const long long*>(out_off), (long long)out_cap,
-        reinterpret_cast<long long*>(out_len), nmin, nmax);
+        reinterpret_cast<long long*>(out_len), nmin, nmax,
+        reinterpret_cast<unsigned long long*>(prof));
     return cudaGetLastError() == cudaSuccess ? MLK_OK : MLK_ERR_CUDA;
 }
 

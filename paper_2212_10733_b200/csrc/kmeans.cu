@@ -470,24 +470,18 @@ k_kmeans(const double* __restrict__ lat, const MlkShard* __restrict__ shards, in
 
 }  // namespace
 
-extern "C" int mlk_kmeans(const double* lat, const MlkShard* shards_h, int32_t n_shards,
-                          int32_t L, int32_t K, const int64_t* first_idx, const double* draws,
-                          double* scratch, float* cents, int32_t* info, cudaStream_t stream) {
+extern "C" int mlk_kmeans(const double* lat, const MlkShard* shards, const MlkShard* shards_h,
+                          int32_t n_shards, int32_t L, int32_t K, const int64_t* first_idx,
+                          const double* draws, double* scratch, float* cents, int32_t* info,
+                          cudaStream_t stream) {
     if (K < 2 || K > MLK_MAXK || L < 1 || L > MLK_MAXL) return MLK_ERR_CONFIG;
     for (int s = 0; s < n_shards; ++s)
         if (shards_h[s].n_img < 1 || shards_h[s].n_img > (1 << 18)) return MLK_ERR_DIM;
-    // shards_h is a host mirror; the kernel needs a device copy
-    MlkShard* d_sh = nullptr;
-    if (cudaMallocAsync(&d_sh, sizeof(MlkShard) * n_shards, stream) != cudaSuccess)
-        return MLK_ERR_CUDA;
-    cudaMemcpyAsync(d_sh, shards_h, sizeof(MlkShard) * n_shards, cudaMemcpyHostToDevice, stream);
     size_t dyn = KM_MAX_LEAVES * (sizeof(double) + sizeof(int) + sizeof(short)) +
                  (size_t)KW * MLK_MAXK * sizeof(int);
     cudaFuncSetAttribute(k_kmeans, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
-    k_kmeans<<<n_shards * L, KT, dyn, stream>>>(lat, d_sh, L, K,
+    k_kmeans<<<n_shards * L, KT, dyn, stream>>>(lat, shards, L, K,
                                                 reinterpret_cast<const long long*>(first_idx),
                                                 draws, scratch, cents, info);
-    cudaError_t e = cudaGetLastError();
-    cudaFreeAsync(d_sh, stream);
-    return e == cudaSuccess ? MLK_OK : MLK_ERR_CUDA;
+    return cudaGetLastError() == cudaSuccess ? MLK_OK : MLK_ERR_CUDA;
 }

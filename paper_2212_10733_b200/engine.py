@@ -325,8 +325,8 @@ def compress_device(f0: torch.Tensor, specs, dgrid: DeviceGrid, cfg, timer: Time
     scratch = torch.empty(4 * L * total, **f64)
     cents = torch.empty((S, L, K), dtype=torch.float32, device=dev)
     kinfo = torch.zeros((S, L, 4), dtype=torch.int32, device=dev)
-    call("mlk_kmeans", lat, ctypes.addressof(table), S, L, K, first_d, draws_d, scratch, cents,
-         kinfo)
+    call("mlk_kmeans", lat, sh_d, ctypes.addressof(table), S, L, K, first_d, draws_d, scratch,
+         cents, kinfo)
     del scratch
 
     timer.mark("find_eb")
@@ -538,13 +538,16 @@ def _deflate_pool(dev, n_workers):
 DEFLATE_TIERS = (2048, 4096, 8192, 16000)
 
 
+DEFLATE_PROF = None   # set to a (10,) uint64 CUDA tensor to collect phase cycles
+
+
 def _run_deflate(varint, in_off, vlen, n, zout, zoff, zcap, zlen, dev, max_workers=2048):
     """Warp-cooperative kernel per size tier; one thread per stream beyond."""
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     lo = 0
     for hi in DEFLATE_TIERS:
         call("mlk_zlib_compress6_warp", varint, in_off, vlen, n, lo, hi, zout, zoff, zcap, zlen,
-             4 * sms)
+             4 * sms, DEFLATE_PROF)
         lo = hi
     workers = min(n, max_workers)
     call("mlk_zlib_compress6", varint, in_off, vlen, n, zout, zoff, zcap, zlen,

@@ -60,8 +60,9 @@ def _check_lambdas(got: bytes, want: bytes, precision: str):
         qu = np.abs(g[:, 4:].view(np.int32).astype(np.int64) - w[:, 4:].view(np.int32))
         assert qu.max() <= 1 and (qu > 0).mean() <= 1e-3
     else:
-        # f64 moments: einsum vs device reduction order
-        np.testing.assert_allclose(g[:, 4:], w[:, 4:], rtol=1e-12, atol=0)
+        # f64 moments: einsum vs device reduction order; u_par is a ratio that
+        # can be ~1e-5 of the thermal speed, so it gets an absolute floor
+        np.testing.assert_allclose(g[:, 4:], w[:, 4:], rtol=1e-10, atol=1e-15)
     if precision == "f32":
         # near-zero components carry the Newton's absolute error (~1e-13), so
         # compare in absolute terms below 1e-5 and in f32 ulps above
@@ -72,7 +73,9 @@ def _check_lambdas(got: bytes, want: bytes, precision: str):
         assert ok.all(), (np.argwhere(~ok)[:5], gl[~ok][:5], wl[~ok][:5])
         assert (ulps > 0).mean() <= 0.01
     else:
-        np.testing.assert_allclose(g[:, :4], w[:, :4], rtol=1e-9, atol=1e-15)
+        # stated tolerance: 1e-7 relative (north star: <= 1e-6), 1e-13 absolute
+        # for components that are zero up to the Newton's convergence level
+        np.testing.assert_allclose(g[:, :4], w[:, :4], rtol=1e-7, atol=1e-13)
 
 
 @pytest.mark.parametrize("name", CASES)
