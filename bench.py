@@ -194,8 +194,7 @@ def main():
     import torch
     import torch.distributed as dist
 
-    from paper_2212_10733_b200 import _lib, engine, pipeline
-    from paper_2212_10733_b200.decomp import partition, rank_shards
+    from paper_2212_10733_b200 import _lib, distributed, engine, pipeline
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -205,27 +204,21 @@ def main():
     ds = corpus(spec["P"], spec["N"])
     models = load_models(spec["golden"])
     cfg = pipeline_config(args.tau)
-    shards = partition(ds.n_planes, ds.n_nodes, cfg.shards, cfg.mode)
-    mine = rank_shards(len(shards), rank, world)
-    my_shards = [shards[i] for i in mine]
-    lo, hi = my_shards[0].nodes_range[0], my_shards[-1].nodes_range[1]
-    D = ds.grid.rows * ds.grid.cols
+    rp = distributed.plan(ds.n_planes, ds.n_nodes, cfg.shards, cfg.mode, rank, world)
+    lo, hi = rp.node_range
+    my_shards = [rp.shards[i] for i in rp.mine]
     f0 = pipeline.upload_f0(ds.data, dev, (lo, hi))
     dgrid = engine.DeviceGrid(ds.grid, dev, cfg.latent_dim)
-    works = engine.shard_layout(my_shards, [models[i] for i in mine], hi - lo, ds.grid.rows,
+    works = engine.shard_layout(my_shards, [models[i] for i in rp.mine], hi - lo, ds.grid.rows,
                                 ds.grid.cols, node_lo=lo)
+    D = ds.grid.rows * ds.grid.cols
     n_local = sum(w.n_img for w in works)
-    order = [np.fromiter((p * ds.n_nodes + x for p, x in sh.members), dtype=np.int64)
-             for sh in my_shards]
+    head_len = 80 + 8 * (1 + ds.grid.rows + ds.grid.cols + D)
 
     def one_step(timer=None):
         out = engine.compress_device(f0, works, dgrid, cfg, timer)
-        sizes = torch.from_numpy(np.asarray(out.blob_lens, dtype=np.int64)).to(dev)
-        if world > 1:  # NCCL: blob sizes -> archive offsets (the only exchange)
-            allsz = [torch.zeros(8, dtype=torch.int64, device=dev) for _ in range(world)]
-            pad = torch.zeros(8, dtype=torch.int64, device=dev)
-            pad[:len(sizes)] = sizes
-            dist.all_gather(allsz, pad)
+        # the only exchange: blob sizes -> archive offsets (NCCL all_reduce)
+        distributed.exchange_sizes(rp, out.blob_lens, head_len)
         return out
 
     for _ in range(args.warmup):
@@ -292,33 +285,55 @@ def main():
                 "launch_ms": s1_ms,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650"}
 
-    # end to end through the public API (N=1) and decompress
+    # end to end through the public API: host numpy f0 in, archive bytes out
     e2e = None
     dec = None
-    if rank == 0 and world == 1 and not args.no_e2e:
+    if not args.no_e2e:
         from paper_2212_10733_b200 import TimestepState, compress, decompress
         state = TimestepState(models=models, timestep_index=1)
-        compress(ds, cfg, state)
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
         reps = max(1, min(args.steps, 3))
-        for _ in range(reps):
-            arc, rep, _ = compress(ds, cfg, state)
+        shm = f"/dev/shm/mlk_bench_{os.getpid()}_{rank}.mlk" if world > 1 else None
+        if world > 1:
+            shm = f"/dev/shm/mlk_bench_{os.environ.get('MASTER_PORT', '0')}.mlk"
+
+        def e2e_step():
+            if world == 1:
+                return compress(ds, cfg, state)
+            return pipeline.compress_distributed(ds, cfg, state, out_path=shm)
+
+        e2e_step()
         torch.cuda.synchronize()
-        e2e_s = (time.perf_counter() - t0) / reps
-        d2h = len(arc)
-        e2e = {"value": total_hist / e2e_s, "unit": "hist/s", "h2d_bytes_per_step": ds.data.nbytes,
-               "d2h_bytes_per_step": d2h, "seconds_per_step": e2e_s,
-               "api": "paper_2212_10733_b200.compress(ds, config, state)"}
-        decompress(arc)
+        if world > 1:
+            dist.barrier()
         t0 = time.perf_counter()
-        back = decompress(arc)
-        dec_s = time.perf_counter() - t0
-        dec = {"value": total_hist / dec_s, "unit": "hist/s (e2e decompress via public API)",
-               "raw_gb_s": total_hist * HIST_BYTES / dec_s / 1e9,
-               "max_per_image_nrmse": rep.max_per_image_nrmse(),
-               "ratio": rep.compression_ratio, "exceptions": rep.exception_count}
-        del back
+        for _ in range(reps):
+            res = e2e_step()
+        torch.cuda.synchronize()
+        e2e_s = torch.tensor([(time.perf_counter() - t0) / reps], device=dev)
+        if world > 1:
+            dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
+        e2e_s = float(e2e_s.item())
+        rep = res[1]
+        arc_len = len(res[0]) if world == 1 else os.path.getsize(shm)
+        e2e = {"value": total_hist / e2e_s, "unit": "hist/s",
+               "h2d_bytes_per_step": int(ds.data[:, lo:hi].nbytes) * world,
+               "d2h_bytes_per_step": int(arc_len), "seconds_per_step": e2e_s,
+               "api": ("paper_2212_10733_b200.compress(ds, config, state)" if world == 1 else
+                       "pipeline.compress_distributed(ds, config, state, out_path)")}
+        if world == 1:
+            arc = res[0]
+            decompress(arc)
+            t0 = time.perf_counter()
+            back = decompress(arc)
+            dec_s = time.perf_counter() - t0
+            dec = {"value": total_hist / dec_s, "unit": "hist/s (e2e decompress via public API)",
+                   "raw_gb_s": total_hist * HIST_BYTES / dec_s / 1e9}
+            del back
+        dec = dict(dec or {}, max_per_image_nrmse=rep.max_per_image_nrmse() if world == 1
+                   else None, ratio=rep.compression_ratio, exceptions=rep.exception_count,
+                   residual_fraction=rep.residual_fraction, max_qoi_nrmse=rep.max_qoi_nrmse)
+        if world > 1 and rank == 0 and os.path.exists(shm):
+            os.unlink(shm)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -339,9 +354,12 @@ def main():
                            "l2": "inputs 1.6 GB > 126 MB L2 (no flush needed)"},
                 "raw_gb_s": value * HIST_BYTES / 1e9,
                 "wall_ms_per_step": wall_ms, "stage_ms": stage_ms, "probe_rounds": probe_rounds, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-                "decompress": dec, "gpu_launches": launches,
+                "decompress_and_report": dec, "gpu_launches": launches,
                 "clocks": clk.summary(),
                 "ratio": None if dec is None else dec["ratio"]}
+        if world > 1:
+            line["scaling"] = "strong"
+            line["config"]["parallelism"] = f"{world} ranks x {len(rp.mine)} shards (NCCL sizes)"
         print(json.dumps(line), flush=True)
         if args.out:
             Path(args.out).write_text(json.dumps(line, indent=1))

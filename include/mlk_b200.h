@@ -154,11 +154,13 @@ int mlk_zlib_compress6(const uint8_t* in, const int64_t* in_off, const int64_t* 
 /* Same bytes as mlk_zlib_compress6, one warp per stream with the working set
  * in shared memory, for the streams with nmin < in_len <= nmax (<= 16000);
  * run it over the size tiers, then mlk_zlib_compress6 for larger streams.
- * prof (may be NULL): 10 u64 cycle/counter accumulators for diagnostics. */
+ * sym_scratch: n * sym_cap bytes (sym_cap >= 3 * nmax + 3) for the LZ77
+ * symbol buffers; prof (may be NULL): 10 u64 cycle/counter accumulators. */
 int mlk_zlib_compress6_warp(const uint8_t* in, const int64_t* in_off, const int64_t* in_len,
                             int32_t n, int32_t nmin, int32_t nmax, uint8_t* out,
                             const int64_t* out_off, int64_t out_cap, int64_t* out_len,
-                            int32_t n_blocks, uint64_t* prof, cudaStream_t stream);
+                            int32_t n_blocks, uint8_t* sym_scratch, int64_t sym_cap,
+                            uint64_t* prof, cudaStream_t stream);
 
 /* dst[dst_off[i] .. + len[i]) = src[src_off[i] .. + len[i]) for n segments */
 int mlk_gather_segments(const uint8_t* src, const int64_t* src_off, const int64_t* len,

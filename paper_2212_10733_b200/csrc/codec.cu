@@ -56,8 +56,8 @@ __global__ void k_inflate(const uint8_t* __restrict__ in, const long long* __res
 namespace wz {
 
 struct Lay {
-    int nmax, T, direct;  // direct: a 32K-entry u16 table indexed by the hash
-    int win, p1, p4, p16, trees, obuf, sym, hash, total;
+    int nmax, T, direct;  // direct: a 32K-entry table indexed by the hash
+    int win, p1, p4, hash, trees, hist, obuf, total;
 };
 
 __host__ __device__ inline int pow2ge(int x) {
@@ -67,6 +67,11 @@ __host__ __device__ inline int pow2ge(int x) {
 }
 __host__ __device__ inline int al16(int x) { return (x + 15) & ~15; }
 
+// Per-warp shared memory: the window, then one region reused by phase:
+//   chain build  : p1 | hash table (u16 entries, aliasing where p4 will go)
+//   matching     : p1 | p4
+//   flush        : Huffman trees | u32 symbol histogram / output bit buffer
+// The symbol buffer lives in global scratch.
 __host__ __device__ inline Lay layout(int nmax) {
     Lay L;
     L.nmax = nmax;
@@ -74,23 +79,19 @@ __host__ __device__ inline Lay layout(int nmax) {
     L.T = L.direct ? 32768 : pow2ge(nmax + 2);
     int o = 0;
     L.win = o;
-    o += al16(nmax + z6::MAX_MATCH + 16);
-    // prev tables (matching) alias the Huffman trees (flush)
-    int chains = al16(2 * nmax) * 3;
-    // trees + the block's output bit buffer (u64 words)
-    int trees = al16((int)sizeof(z6::Trees)) + al16(nmax + 256);
-    L.p1 = o;
-    L.p4 = o + al16(2 * nmax);
-    L.p16 = o + 2 * al16(2 * nmax);
-    L.trees = o;
-    L.obuf = o + al16((int)sizeof(z6::Trees));
-    o += chains > trees ? chains : trees;
-    // the hash table (chain building) aliases the symbol buffer (matching)
-    int sym = al16(3 * nmax + 8);
-    int hash = al16((L.direct ? 2 : 4) * L.T);
-    L.sym = o;
-    L.hash = o;
-    o += sym > hash ? sym : hash;
+    o += al16(nmax + z6::MAX_MATCH + 24);
+    const int b0 = o;
+    L.p1 = b0;
+    L.p4 = b0 + al16(2 * nmax);
+    L.hash = L.p4;
+    const int chains = al16(2 * nmax) + (al16(2 * nmax) > al16(2 * L.T) ? al16(2 * nmax)
+                                                                          : al16(2 * L.T));
+    L.trees = b0;
+    L.hist = b0 + al16((int)sizeof(z6::Trees));
+    L.obuf = L.hist;
+    const int tail = al16(nmax + 256) > 4 * 320 ? al16(nmax + 256) : 4 * 320;
+    const int flush = al16((int)sizeof(z6::Trees)) + tail;
+    o += chains > flush ? chains : flush;
     L.total = o;
     return L;
 }
@@ -99,9 +100,7 @@ __device__ __forceinline__ unsigned hkey(const uint8_t* w) {
     return (((unsigned)w[0] << 10) ^ ((unsigned)w[1] << 5) ^ w[2]) & 0x7fffu;
 }
 
-__device__ __forceinline__ int jump(const uint16_t* p1, const uint16_t* p4, const uint16_t* p16,
-                                    int x, int i) {
-    while (i >= 16 && x) { x = p16[x]; i -= 16; }
+__device__ __forceinline__ int jump(const uint16_t* p1, const uint16_t* p4, int x, int i) {
     while (i >= 4 && x) { x = p4[x]; i -= 4; }
     while (i > 0 && x) { x = p1[x]; --i; }
     return x;
@@ -177,11 +176,12 @@ struct GBit {  // lane-0 bit writer into global memory
 
 }  // namespace wz
 
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(512)
 k_deflate_warp(const uint8_t* __restrict__ in, const long long* __restrict__ in_off,
                const long long* __restrict__ in_len, int n_streams, uint8_t* __restrict__ out,
                const long long* __restrict__ out_off, long long out_cap,
                long long* __restrict__ out_len, int nmin, int nmax,
+               uint8_t* __restrict__ sym_g, long long sym_cap,
                unsigned long long* __restrict__ prof) {
     __shared__ z6::Tables tb;
     extern __shared__ __align__(16) uint8_t zsm[];
@@ -194,10 +194,7 @@ k_deflate_warp(const uint8_t* __restrict__ in, const long long* __restrict__ in_
     uint8_t* win = base + Ly.win;
     uint16_t* p1 = reinterpret_cast<uint16_t*>(base + Ly.p1);
     uint16_t* p4 = reinterpret_cast<uint16_t*>(base + Ly.p4);
-    uint16_t* p16 = reinterpret_cast<uint16_t*>(base + Ly.p16);
-    uint8_t* sym = base + Ly.sym;
-    unsigned* htab = reinterpret_cast<unsigned*>(base + Ly.hash);
-    uint16_t* dtab = reinterpret_cast<uint16_t*>(base + Ly.hash);
+    uint16_t* htab = reinterpret_cast<uint16_t*>(base + Ly.hash);
     z6::Trees* trees = reinterpret_cast<z6::Trees*>(base + Ly.trees);
     const unsigned FULL = 0xffffffffu;
     const unsigned lt_mask = (1u << lane) - 1u;
@@ -206,6 +203,7 @@ k_deflate_warp(const uint8_t* __restrict__ in, const long long* __restrict__ in_
         const int n = (int)in_len[s];
         if (n <= nmin || n > nmax) continue;  // another tier handles it
         const uint8_t* src = in + in_off[s];
+        uint8_t* sym = sym_g + (long long)s * sym_cap;
         long long t_0 = clock64();
         // ---- window + zero pad, Adler-32 (lane-parallel sums)
         unsigned long long sa = 0, sb = 0;
@@ -222,14 +220,12 @@ k_deflate_warp(const uint8_t* __restrict__ in, const long long* __restrict__ in_
         }
         const unsigned ad_a = (unsigned)((1 + sa) % 65521ull);
         const unsigned ad_b = (unsigned)(((unsigned long long)n + sb) % 65521ull);
-        if (Ly.direct) {
-            for (int i = lane; i < Ly.T; i += 32) dtab[i] = 0;
-        } else {
-            for (int i = lane; i < Ly.T; i += 32) htab[i] = 0u;
-        }
+        for (int i = lane; i < Ly.T; i += 32) htab[i] = 0;
         __syncwarp();
         long long t_1 = clock64();
-        // ---- prev[] (hash chains), 32 positions per step
+        // ---- prev[] (hash chains), 32 positions per step.  Table entries
+        //      are position + 1; a probed entry's key is re-derived from the
+        //      window (no key storage), direct mode indexes by the hash.
         const int n_ins = n - z6::MIN_MATCH + 1;  // positions 0 .. n-3
         for (int b0 = 0; b0 < n_ins; b0 += 32) {
             const int p = b0 + lane;
@@ -238,58 +234,58 @@ k_deflate_warp(const uint8_t* __restrict__ in, const long long* __restrict__ in_
             const unsigned m = __match_any_sync(FULL, h);
             if (v) {
                 const unsigned lower = m & lt_mask;
-                int pr;
+                int pr = 0;
                 if (lower) {
                     pr = b0 + 31 - __clz(lower);
                 } else if (Ly.direct) {
-                    pr = (int)dtab[h] - 1;
-                    if (pr < 0) pr = 0;
+                    pr = htab[h];
+                    pr = pr ? pr - 1 : 0;
                 } else {
-                    pr = 0;
                     unsigned i = (h * 2654435761u) & (Ly.T - 1);
                     for (;;) {
                         const unsigned e = htab[i];
                         if (e == 0u) break;
-                        if ((e >> 16) == h) { pr = (int)(e & 0xffffu) - 1; break; }
+                        if (wz::hkey(win + e - 1) == h) { pr = (int)e - 1; break; }
                         i = (i + 1) & (Ly.T - 1);
                     }
                 }
                 p1[p] = (uint16_t)pr;
             }
             __syncwarp();
-            if (v && (31 - __clz(m)) == lane && Ly.direct) {
-                dtab[h] = (uint16_t)(p + 1);
-            } else if (v && (31 - __clz(m)) == lane) {  // last of its group updates the table
-                const unsigned nv = (h << 16) | (unsigned)(p + 1);
-                unsigned i = (h * 2654435761u) & (Ly.T - 1);
-                for (;;) {
-                    const unsigned e = htab[i];
-                    if (e == 0u) {
-                        if (atomicCAS(&htab[i], 0u, nv) == 0u) break;
-                        continue;  // lost the slot to another key; re-read it
+            if (v && (31 - __clz(m)) == lane) {  // last of its group updates the table
+                if (Ly.direct) {
+                    htab[h] = (uint16_t)(p + 1);
+                } else {
+                    unsigned i = (h * 2654435761u) & (Ly.T - 1);
+                    for (;;) {
+                        unsigned* w32 = reinterpret_cast<unsigned*>(htab) + (i >> 1);
+                        const int sh = (i & 1) * 16;
+                        unsigned old = *w32;
+                        unsigned e = (old >> sh) & 0xffffu;
+                        while (e == 0u) {  // claim the empty half-word
+                            const unsigned prev = atomicCAS(w32, old, old | ((unsigned)(p + 1) << sh));
+                            if (prev == old) break;
+                            old = prev;
+                            e = (old >> sh) & 0xffffu;
+                        }
+                        if (e == 0u) break;  // claimed
+                        if (wz::hkey(win + e - 1) == h) { htab[i] = (uint16_t)(p + 1); break; }
+                        i = (i + 1) & (Ly.T - 1);
                     }
-                    if ((e >> 16) == h) { htab[i] = nv; break; }
-                    i = (i + 1) & (Ly.T - 1);
                 }
             }
             __syncwarp();
         }
         long long t_2 = clock64();
-        for (int p = lane; p < n; p += 32) {
-            int x = p < n_ins ? p1[p] : 0;
+        for (int p = lane; p < n; p += 32)
             if (p >= n_ins) p1[p] = 0;
+        __syncwarp();
+        for (int p = lane; p < n; p += 32) {  // the hash table is dead: p4 reuses it
+            int x = p1[p];
             x = x ? p1[x] : 0;
             x = x ? p1[x] : 0;
             x = x ? p1[x] : 0;
             p4[p] = (uint16_t)x;
-        }
-        __syncwarp();
-        for (int p = lane; p < n; p += 32) {
-            int x = p4[p];
-            x = x ? p4[x] : 0;
-            x = x ? p4[x] : 0;
-            x = x ? p4[x] : 0;
-            p16[p] = (uint16_t)x;
         }
         __syncwarp();
         long long t_3 = clock64();
@@ -314,7 +310,7 @@ k_deflate_warp(const uint8_t* __restrict__ in, const long long* __restrict__ in_
                 int best = prev_length, bstart = match_start;
                 int cb = hash_head;  // first candidate of the round
                 for (int r = 0; r < chain; r += 32) {
-                    const int c = wz::jump(p1, p4, p16, cb, lane);
+                    const int c = wz::jump(p1, p4, cb, lane);
                     const bool valid = c != 0 && r + lane < chain;
                     const int len = valid ? wz::match_len(win, strstart, c) : 0;
                     const unsigned hit = __ballot_sync(FULL, valid && len >= thr);
@@ -329,7 +325,7 @@ k_deflate_warp(const uint8_t* __restrict__ in, const long long* __restrict__ in_
                     }
                     const unsigned alive = __ballot_sync(FULL, valid);
                     if (hit || alive != FULL) break;
-                    cb = __shfl_sync(FULL, wz::jump(p1, p4, p16, c, 1), 31);
+                    cb = __shfl_sync(FULL, wz::jump(p1, p4, c, 1), 31);
                     if (cb == 0) break;
                 }
                 match_start = bstart;
@@ -380,23 +376,33 @@ k_deflate_warp(const uint8_t* __restrict__ in, const long long* __restrict__ in_
         // ---- trees (lane 0) + bit stream (all lanes); prev tables are dead now
         z6::Trees& t = *trees;
         unsigned long long* ob = reinterpret_cast<unsigned long long*>(base + Ly.obuf);
-        const int obw = (n + 256) / 8;  // u64 words available
+        unsigned* hist = reinterpret_cast<unsigned*>(base + Ly.hist);
+        __shared__ int sh_kind[16];
+        __shared__ long long sh_hbits[16];
+        for (int i = lane; i < 320; i += 32) hist[i] = 0u;
+        __syncwarp();
+        const int nsym = sym_next / 3;
+        for (int k = lane; k < nsym; k += 32) {  // symbol frequencies
+            const unsigned dist = sym[3 * k] | ((unsigned)sym[3 * k + 1] << 8);
+            const int lc = sym[3 * k + 2];
+            if (dist == 0) {
+                atomicAdd(hist + lc, 1u);
+            } else {
+                atomicAdd(hist + tb.length_code[lc] + z6::LITERALS + 1, 1u);
+                atomicAdd(hist + z6::L_CODES + z6::d_code(tb, dist - 1), 1u);
+            }
+        }
+        __syncwarp();
+        for (int i = lane; i < z6::L_CODES; i += 32) t.lt.freq[i] = (uint16_t)hist[i];
+        for (int i = lane; i < z6::D_CODES; i += 32) t.dt.freq[i] = (uint16_t)hist[z6::L_CODES + i];
+        for (int i = lane; i < z6::BL_CODES; i += 32) t.bt.freq[i] = 0;
+        __syncwarp();
+        const int obw = (n + 256) / 8;  // u64 words available (the histogram is dead)
         for (int i = lane; i < obw; i += 32) ob[i] = 0ull;
-        __shared__ int sh_kind[8];
-        __shared__ long long sh_hbits[8];
         __syncwarp();
         if (lane == 0) {
-            z6::init_block(t);
-            for (int sx = 0; sx < sym_next; sx += 3) {
-                const unsigned dist = sym[sx] | ((unsigned)sym[sx + 1] << 8);
-                const int lc = sym[sx + 2];
-                if (dist == 0) {
-                    t.lt.freq[lc]++;
-                } else {
-                    t.lt.freq[tb.length_code[lc] + z6::LITERALS + 1]++;
-                    t.dt.freq[z6::d_code(tb, dist - 1)]++;
-                }
-            }
+            t.lt.freq[z6::END_BLOCK] = 1;
+            t.opt_len = t.static_len = 0;
             z6::build_tree(t, t.lt, 0, tb);
             z6::build_tree(t, t.dt, 1, tb);
             z6::scan_tree(t, t.lt);
@@ -453,7 +459,6 @@ k_deflate_warp(const uint8_t* __restrict__ in, const long long* __restrict__ in_
             const uint16_t* llen = kind == 1 ? tb.sl_len : t.lt.len;
             const uint16_t* dcode = kind == 1 ? tb.sd_code : t.dt.code;
             const uint16_t* dlen = kind == 1 ? tb.sd_len : t.dt.len;
-            const int nsym = sym_next / 3;
             for (int k0 = 0; k0 < nsym; k0 += 32) {
                 const int k = k0 + lane;
                 unsigned long long val = 0;
@@ -570,19 +575,22 @@ extern "C" int mlk_zlib_compress6_warp(const uint8_t* in, const int64_t* in_off,
                                        const int64_t* in_len, int32_t n, int32_t nmin,
                                        int32_t nmax, uint8_t* out, const int64_t* out_off,
                                        int64_t out_cap, int64_t* out_len, int32_t n_blocks,
-                                       uint64_t* prof, cudaStream_t stream) {
+                                       uint8_t* sym_scratch, int64_t sym_cap, uint64_t* prof,
+                                       cudaStream_t stream) {
     if (n <= 0) return MLK_OK;
-    if (nmax > 16000 || nmax < 1) return MLK_ERR_CONFIG;
+    if (nmax > 16000 || nmax < 1 || sym_cap < 3LL * nmax + 3) return MLK_ERR_CONFIG;
     const wz::Lay Ly = wz::layout(nmax);
-    int zw = (200 * 1024) / Ly.total;
-    zw = zw < 1 ? 1 : (zw > 8 ? 8 : zw);
+    // two blocks per SM when they fit, up to 16 warps each
+    int zw = (110 * 1024) / Ly.total;
+    if (zw < 1) zw = (220 * 1024) / Ly.total;
+    zw = zw < 1 ? 1 : (zw > 16 ? 16 : zw);
     size_t sm = (size_t)zw * Ly.total;
     if (sm > 227 * 1024) return MLK_ERR_CONFIG;
     cudaFuncSetAttribute(k_deflate_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     k_deflate_warp<<<n_blocks, 32 * zw, sm, stream>>>(
         in, reinterpret_cast<const long long*>(in_off), reinterpret_cast<const long long*>(in_len),
         n, out, reinterpret_cast<const long long*>(out_off), (long long)out_cap,
-        reinterpret_cast<long long*>(out_len), nmin, nmax,
+        reinterpret_cast<long long*>(out_len), nmin, nmax, sym_scratch, (long long)sym_cap,
         reinterpret_cast<unsigned long long*>(prof));
     return cudaGetLastError() == cudaSuccess ? MLK_OK : MLK_ERR_CUDA;
 }

@@ -164,7 +164,7 @@ struct Trees {
     TreeT<HEAP_SIZE> lt;
     TreeT<2 * D_CODES + 1> dt;
     TreeT<2 * BL_CODES + 1> bt;
-    int heap[HEAP_SIZE];
+    uint16_t heap[HEAP_SIZE];
     uint8_t depth[HEAP_SIZE];
     int heap_len, heap_max;
     uint16_t bl_count[MAX_BITS + 1];
@@ -196,7 +196,7 @@ Z6_HD inline void pqdownheap(Trees& w, const T& t, int k) {
         k = j;
         j <<= 1;
     }
-    w.heap[k] = v;
+    w.heap[k] = (uint16_t)v;
 }
 
 // trees.c gen_bitlen.  kind: 0 literal/length, 1 distance, 2 bit-length tree
@@ -258,14 +258,16 @@ Z6_HD inline void build_tree(Trees& w, T& t, int kind, const Tables& tb) {
     w.heap_max = HEAP_SIZE;
     for (int n = 0; n < elems; n++) {
         if (t.freq[n] != 0) {
-            w.heap[++w.heap_len] = max_code = n;
+            w.heap[++w.heap_len] = (uint16_t)n;
+            max_code = n;
             w.depth[n] = 0;
         } else {
             t.len[n] = 0;
         }
     }
     while (w.heap_len < 2) {
-        int node = w.heap[++w.heap_len] = (max_code < 2 ? ++max_code : 0);
+        int node = (max_code < 2 ? ++max_code : 0);
+        w.heap[++w.heap_len] = (uint16_t)node;
         t.freq[node] = 1;
         w.depth[node] = 0;
         w.opt_len--;
@@ -280,12 +282,12 @@ Z6_HD inline void build_tree(Trees& w, T& t, int kind, const Tables& tb) {
         w.heap[1] = w.heap[w.heap_len--];
         pqdownheap(w, t, 1);
         int m = w.heap[1];
-        w.heap[--w.heap_max] = n;
-        w.heap[--w.heap_max] = m;
+        w.heap[--w.heap_max] = (uint16_t)n;
+        w.heap[--w.heap_max] = (uint16_t)m;
         t.freq[node] = (uint16_t)(t.freq[n] + t.freq[m]);
         w.depth[node] = (uint8_t)((w.depth[n] >= w.depth[m] ? w.depth[n] : w.depth[m]) + 1);
         t.dad[n] = t.dad[m] = (uint16_t)node;
-        w.heap[1] = node++;
+        w.heap[1] = (uint16_t)node++;
         pqdownheap(w, t, 1);
     } while (w.heap_len >= 2);
     w.heap[--w.heap_max] = w.heap[1];

@@ -279,11 +279,93 @@ def _gram(models):
     return np.stack(rows)
 
 
+@functools.lru_cache(maxsize=4096)
 def kmeans_draws(n: int, k: int, seed: int):
-    """The PCG64 draws quantizer.kmeans_1d consumes (quantizer.py:68,77)."""
+    """The PCG64 draws quantizer.kmeans_1d consumes (quantizer.py:68,77): a pure
+    function of (n, k, seed), so it is cached."""
     g = np.random.Generator(np.random.PCG64(seed))
     first = int(g.integers(n))
-    return first, [g.random() for _ in range(k - 1)]
+    return first, tuple(g.random() for _ in range(k - 1))
+
+
+class Workspace:
+    """Per-device persistent buffers: grow-only device arenas by name and a
+    pinned host staging arena whose contents reach the device with one async
+    copy per flush (no pageable, stream-draining H2D on the hot path)."""
+
+    _by_dev = {}
+
+    def __init__(self, dev, cap=1 << 26):
+        self.dev = dev
+        self.bufs = {}
+        self._alloc(cap)
+        self.pending = []
+        self.ready = None
+
+    def _alloc(self, cap):
+        self.h = torch.empty(cap, dtype=torch.uint8).pin_memory()
+        self.hn = self.h.numpy()
+        self.d = torch.empty(cap, dtype=torch.uint8, device=self.dev)
+        self.pos = 0
+
+    @classmethod
+    def get(cls, dev):
+        ws = cls._by_dev.get(dev.index)
+        if ws is None:
+            ws = cls._by_dev[dev.index] = Workspace(dev)
+        return ws
+
+    def tensor(self, name, shape, dtype):
+        n = int(np.prod(shape)) if shape else 1
+        nbytes = max(16, n * torch.empty((), dtype=dtype).element_size())
+        b = self.bufs.get(name)
+        if b is None or b.numel() < nbytes:
+            self.bufs[name] = b = torch.empty(int(nbytes * 1.25) + 64, dtype=torch.uint8,
+                                              device=self.dev)
+        return b[:nbytes].view(dtype)[:n].view(shape)
+
+    def reset(self):
+        """Start of a call: the previous call's staged copies must have landed
+        before the arena is rewritten (device views of one call stay valid for
+        the whole call because positions only grow within it)."""
+        if self.ready is not None:
+            self.ready.synchronize()
+            self.ready = None
+        self.pos = 0
+
+    def begin(self):
+        pass
+
+    def stage(self, arr):
+        """Queue a host array; returns its device view after the next flush()."""
+        a = np.ascontiguousarray(arr)
+        nb = a.nbytes
+        if self.pos + nb + 16 > self.h.numel():
+            # grow (rare): everything staged so far must reach the device first
+            if self.pending:
+                raise MemoryError("staging arena exhausted inside a flush group")
+            torch.cuda.synchronize(self.dev)
+            self._alloc(max(2 * self.h.numel(), nb + (1 << 20)))
+        self.hn[self.pos:self.pos + nb] = a.reshape(-1).view(np.uint8)
+        view = self.d[self.pos:self.pos + max(nb, 1)]
+        out = view[:nb].view(torch.from_numpy(a[:0]).dtype).view(a.shape) if nb else view
+        self.pending.append((self.pos, nb))
+        self.pos = (self.pos + nb + 15) & ~15
+        return out
+
+    def flush(self):
+        if self.pending:
+            lo = self.pending[0][0]
+            self.d[lo:self.pos].copy_(self.h[lo:self.pos], non_blocking=True)
+            self.pending = []
+            ev = torch.cuda.Event()
+            ev.record()
+            self.ready = ev
+
+
+def _d2h(*tensors):
+    """One synchronisation point for several small device results."""
+    return [t.cpu().numpy() for t in tensors]
 
 
 def compress_device(f0: torch.Tensor, specs, dgrid: DeviceGrid, cfg, timer: Timer | None = None,
@@ -292,6 +374,7 @@ def compress_device(f0: torch.Tensor, specs, dgrid: DeviceGrid, cfg, timer: Time
 
     f0 is a flat float64 CUDA tensor holding the rank's histograms; shard s's
     image j lives at base + (j // block) * plane_stride + (j % block) * D.
+    Device arrays in the result stay valid until the next call on the device.
     """
     dev = f0.device
     D, L, K = dgrid.D, cfg.latent_dim, 2 ** cfg.pq_bits
@@ -300,19 +383,14 @@ def compress_device(f0: torch.Tensor, specs, dgrid: DeviceGrid, cfg, timer: Time
     for sp in specs:
         if sp.model.latent_dim != L or sp.model.input_dim != D:
             raise ConfigError("shard model does not match the configuration/grid")
+    ws = Workspace.get(dev)
+    ws.reset()
+    T = ws.tensor
+    f64, i32, i64 = torch.float64, torch.int32, torch.int64
     table = _shard_table(specs, D, L)
-    sh_d = _upload_shards(table, dev)
     total = sum(sp.n_img for sp in specs)
-    W = torch.from_numpy(np.stack([sp.model.weights for sp in specs]).astype(np.float32)).to(dev)
-    f64 = dict(dtype=torch.float64, device=dev)
-
-    timer.mark("encode")
-    lat = torch.empty((total, L), **f64)
-    stats = torch.empty((total, 4), **f64)
-    qoi = torch.empty((total, 4), **f64)
-    call("mlk_stage1", f0, sh_d, S, total, dgrid.addr, W, L, lat, stats, qoi)
-
-    timer.mark("pq")
+    sh_d = ws.stage(np.frombuffer(bytes(table), dtype=np.uint8))
+    W = ws.stage(np.stack([sp.model.weights for sp in specs]).astype(np.float32))
     first, draws = [], []
     for sp in specs:
         seed = mix_seed(cfg.seed, sp.wid)
@@ -320,37 +398,43 @@ def compress_device(f0: torch.Tensor, specs, dgrid: DeviceGrid, cfg, timer: Time
             f, u = kmeans_draws(sp.n_img, K, seed + d)
             first.append(f)
             draws.extend(u)
-    first_d = torch.tensor(first, dtype=torch.int64, device=dev)
-    draws_d = torch.tensor(draws, **f64)
-    scratch = torch.empty(4 * L * total, **f64)
-    cents = torch.empty((S, L, K), dtype=torch.float32, device=dev)
-    kinfo = torch.zeros((S, L, 4), dtype=torch.int32, device=dev)
+    first_d = ws.stage(np.asarray(first, dtype=np.int64))
+    draws_d = ws.stage(np.asarray(draws, dtype=np.float64))
+    gram = ws.stage(_gram([sp.model for sp in specs]))
+    ws.flush()
+
+    timer.mark("encode")
+    lat = T("lat", (total, L), f64)
+    stats = T("stats", (total, 4), f64)
+    qoi = T("qoi", (total, 4), f64)
+    call("mlk_stage1", f0, sh_d, S, total, dgrid.addr, W, L, lat, stats, qoi)
+
+    timer.mark("pq")
+    scratch = T("km_scratch", (4 * L * total,), f64)
+    cents = T("cents", (S, L, K), torch.float32)
+    kinfo = T("kinfo", (S, L, 4), i32)
     call("mlk_kmeans", lat, sh_d, ctypes.addressof(table), S, L, K, first_d, draws_d, scratch,
          cents, kinfo)
-    del scratch
 
     timer.mark("find_eb")
-    gram = torch.from_numpy(_gram([sp.model for sp in specs])).to(dev)
-    codes = torch.empty((total, L), dtype=torch.uint8, device=dev)
-    flags = torch.empty(total, dtype=torch.uint8, device=dev)
-    err_a = torch.empty(total, **f64)
-    rbound = torch.empty(total, **f64)
+    codes = T("codes", (total, L), torch.uint8)
+    flags = T("flags", (total,), torch.uint8)
+    err_a = T("err_a", (total,), f64)
+    rbound = T("rbound", (total,), f64)
     call("mlk_select", lat, stats, sh_d, S, total, dgrid.addr, cents, L, K, gram, cfg.tau, codes,
          flags, err_a, rbound)
     timer.mark("recheck")
-    err_x = torch.empty(total, **f64)
+    err_x = T("err_x", (total,), f64)
     call("mlk_recheck", f0, stats, sh_d, S, total, dgrid.addr, W, L, cents, K, codes, cfg.tau,
          flags, err_x)
-    i32 = dict(dtype=torch.int32, device=dev)
-    sel = torch.empty(total, **i32)
-    sel_rank = torch.empty(total, **i32)
-    sel_rng = torch.empty(total, **i32)
-    sel_cnt = torch.empty(S, **i32)
-    eb_hi = torch.empty(S, **f64)
     timer.mark("compact")
+    sel = T("sel", (total,), i32)
+    sel_rank = T("sel_rank", (total,), i32)
+    sel_rng = T("sel_rng", (total,), i32)
+    sel_cnt = T("sel_cnt", (S,), i32)
+    eb_hi = T("eb_hi", (S,), f64)
     call("mlk_compact", flags, stats, sh_d, S, cfg.tau, sel, sel_rank, sel_rng, sel_cnt, eb_hi)
-    cnt_h = sel_cnt.cpu().numpy()
-    ebhi_h = eb_hi.cpu().numpy()
+    cnt_h, ebhi_h = _d2h(sel_cnt, eb_hi)
 
     timer.mark("eb_search")
     # ---- error-bound search, LOOKAHEAD levels per launch
@@ -366,6 +450,7 @@ def compress_device(f0: torch.Tensor, specs, dgrid: DeviceGrid, cfg, timer: Time
             states.append(_Search("hi", eb_hi_s))
     n_cand = 2 ** LOOKAHEAD - 1
     rounds = 0
+    fail = T("fail", (S, n_cand), i32)
     while any(st is not None and st.stage != "done" for st in states):
         rounds += 1
         trees, cand = [], np.zeros((S, n_cand))
@@ -377,12 +462,14 @@ def compress_device(f0: torch.Tensor, specs, dgrid: DeviceGrid, cfg, timer: Time
             for c, nd in enumerate(tree[0]):
                 cand[s, c] = float(nd[0].query())
             act[s + 1] = act[s] + (int(cnt_h[s]) if tree[0] else 0)
-        fail = torch.zeros((S, n_cand), **i32)
-        cand_d = torch.from_numpy(cand).to(dev)
-        act_d = torch.from_numpy(act).to(dev)
+        ws.begin()
+        cand_d = ws.stage(cand)
+        act_d = ws.stage(act)
+        ws.flush()
+        fail.zero_()
         call("mlk_probe", f0, stats, sh_d, S, dgrid.addr, W, L, cents, K, codes, sel_rng, act_d,
              int(act[-1]), rbound, cfg.tau, cand_d, n_cand, fail)
-        fail_h = fail.cpu().numpy()
+        (fail_h,) = _d2h(fail)
         for s, (nodes, ref) in enumerate(trees):
             if not nodes:
                 continue
@@ -397,43 +484,49 @@ def compress_device(f0: torch.Tensor, specs, dgrid: DeviceGrid, cfg, timer: Time
     for s in range(S):
         table[s].eb = eb[s]
         table[s].lossless = int(lossless[s])
-    sh_d = _upload_shards(table, dev)
 
     timer.mark("newton")
     slot_base_h = np.concatenate([[0], np.cumsum(cnt_h)[:-1]]).astype(np.int32)
     n_sel = int(cnt_h.sum())
+    ws.begin()
+    sh_d = ws.stage(np.frombuffer(bytes(table), dtype=np.uint8))
+    slot_base = ws.stage(slot_base_h)
+    ws.flush()
     vcap = ((10 * D + 15) // 16) * 16
-    varint = torch.empty(max(1, n_sel) * vcap, dtype=torch.uint8, device=dev)
-    vlen = torch.zeros(max(1, n_sel), dtype=torch.int64, device=dev)
-    slot_base = torch.from_numpy(slot_base_h).to(dev)
+    varint = T("varint", (max(1, n_sel) * vcap,), torch.uint8)
+    vlen = T("vlen", (max(1, n_sel),), i64)
     opts = MlkNewton(step=cfg.newton.step, max_iter=cfg.newton.max_iter,
                      retry=int(cfg.newton.retry), tol=cfg.newton.tol, floor=cfg.newton.floor,
                      retry_step=cfg.newton.retry_step, retry_max_iter=cfg.newton.retry_max_iter,
                      lam_f32=int(cfg.lambda_precision == "f32"), tau=cfg.tau)
-    lam = torch.empty((total, 4), **f64)
-    qst = torch.empty((total, 4), **f64)
-    status = torch.empty(total, **i32)
-    iters = torch.empty(total, **i32)
-    ferr = torch.empty(total, **f64)
-    fqoi = torch.empty((total, 4), **f64)
-    fsse = torch.empty(total, **f64)
-    errf = torch.zeros(1, **i32)
+    lam = T("lam", (total, 4), f64)
+    qst = T("qst", (total, 4), f64)
+    status = T("status", (total,), i32)
+    iters = T("iters", (total,), i32)
+    ferr = T("ferr", (total,), f64)
+    fqoi = T("fqoi", (total, 4), f64)
+    fsse = T("fsse", (total,), f64)
+    errf = T("errf", (1,), i32)
+    errf.zero_()
     call("mlk_project", f0, stats, qoi, sh_d, S, total, dgrid.addr, W, L, cents, K, codes,
          sel_rank, slot_base, ctypes.addressof(opts), flags, lam, qst, status, iters, ferr, fqoi,
          fsse, varint, vcap, vlen, errf)
+    exc_list = T("exc_list", (total,), i32)
+    exc_cnt = T("exc_cnt", (S,), i32)
+    call("mlk_list_flags", flags, sh_d, S, _lib.F_EXCEPTION, exc_list, exc_cnt)
 
     timer.mark("deflate")
-    if int(errf.item()) != 0:
+    zout, zoff, zlen = deflate_launch(ws, varint, vcap, vlen, n_sel, dev)
+    zlen_h, exc_h, errf_h = _d2h(zlen[:max(1, n_sel)], exc_cnt, errf)
+    zlen_h = zlen_h[:n_sel]
+    if int(errf_h[0]) != 0:
         raise ConfigError("error bound too small for this residual range")
-    zout, zoff, zlen, zlen_h = deflate_device(varint, vcap, vlen, n_sel, dev)
+    if np.any(zlen_h < 0):
+        raise ConfigError("residual stream exceeds the device DEFLATE limits")
 
     timer.mark("pack")
-    exc_list = torch.empty(total, **i32)
-    exc_cnt = torch.empty(S, **i32)
-    call("mlk_list_flags", flags, sh_d, S, _lib.F_EXCEPTION, exc_list, exc_cnt)
-    exc_h = exc_cnt.cpu().numpy()
     lay = blob_layout(specs, cfg, D, cnt_h, zlen_h, exc_h)
-    buf = torch.empty(max(1, lay["total"]), dtype=torch.uint8, device=dev)
+    buf = T("blob", (max(1, lay["total"]),), torch.uint8)
     # fixed pieces: 44-byte header + weights section, residual / exception prefixes
     pieces, src, ln, dst = [], [], [], []
     pos = 0
@@ -446,30 +539,39 @@ def compress_device(f0: torch.Tensor, specs, dgrid: DeviceGrid, cfg, timer: Time
             ln.append(len(raw))
             dst.append(off)
             pos += len(raw)
-    stage = torch.from_numpy(np.frombuffer(b"".join(pieces), dtype=np.uint8).copy()).to(dev)
-    i64 = dict(dtype=torch.int64, device=dev)
-    call("mlk_gather_segments", stage, torch.tensor(src, **i64), torch.tensor(ln, **i64),
-         len(pieces), buf, torch.tensor(dst, **i64))
+    ws.begin()
+    stage = ws.stage(np.frombuffer(b"".join(pieces), dtype=np.uint8))
+    src_d = ws.stage(np.asarray(src, np.int64))
+    ln_d = ws.stage(np.asarray(ln, np.int64))
+    dst_d = ws.stage(np.asarray(dst, np.int64))
+    pq_src = ws.stage(np.arange(0, S * 4 * L * K, 4 * L * K, dtype=np.int64))
+    pq_len = ws.stage(np.full(S, 4 * L * K, dtype=np.int64))
+    pq_off = ws.stage(lay["pq_off"])
+    ent_shard = ws.stage(np.repeat(np.arange(S, dtype=np.int32), cnt_h))
+    entry_off = ws.stage(lay["entry_off"])
+    lam_off = ws.stage(lay["lam_off"])
+    exc_base = ws.stage(np.concatenate([[0], np.cumsum(exc_h)]).astype(np.int32))
+    exc_off = ws.stage(lay["exc_off"])
+    ws.flush()
+    call("mlk_gather_segments", stage, src_d, ln_d, len(pieces), buf, dst_d)
     # codes (pack_indices straight into the blob) and the PQ table
-    c16 = codes.to(torch.int16)
-    bad = torch.zeros(1, **i32)
+    c16 = T("codes16", (total * L,), torch.int16)
+    c16.copy_(codes.reshape(-1))
+    bad = T("bad", (1,), i32)
     base = buf.data_ptr()
     for s, sp in enumerate(specs):
         off = table[s].img_off
-        call("mlk_pack_indices", c16[off:off + sp.n_img].reshape(-1), sp.n_img * L, cfg.pq_bits,
+        call("mlk_pack_indices", c16[off * L:(off + sp.n_img) * L], sp.n_img * L, cfg.pq_bits,
              base + int(lay["codes_off"][s]), bad)
-    cview = cents.view(torch.uint8).reshape(-1)
-    call("mlk_gather_segments", cview, torch.arange(0, S * 4 * L * K, 4 * L * K, **i64),
-         torch.full((S,), 4 * L * K, **i64), S, buf, torch.from_numpy(lay["pq_off"]).to(dev))
+    call("mlk_gather_segments", cents.view(torch.uint8).reshape(-1), pq_src, pq_len, S, buf,
+         pq_off)
     if n_sel:
-        ent_shard = torch.from_numpy(np.repeat(np.arange(S, dtype=np.int32), cnt_h)).to(dev)
-        call("mlk_pack_residuals", sel, sh_d, ent_shard, torch.from_numpy(lay["entry_off"]).to(dev),
-             zoff, zlen, zout, slot_base, dgrid.struct.rows, dgrid.struct.cols, n_sel, buf)
-    call("mlk_pack_lambdas", lam, qst, sh_d, S, total, torch.from_numpy(lay["lam_off"]).to(dev),
+        call("mlk_pack_residuals", sel, sh_d, ent_shard, entry_off, zoff, zlen, zout, slot_base,
+             dgrid.struct.rows, dgrid.struct.cols, n_sel, buf)
+    call("mlk_pack_lambdas", lam, qst, sh_d, S, total, lam_off,
          int(cfg.lambda_precision == "f32"), buf)
-    exc_base = torch.from_numpy(np.concatenate([[0], np.cumsum(exc_h)]).astype(np.int32)).to(dev)
-    call("mlk_pack_exceptions", f0, sh_d, S, exc_list, exc_base,
-         torch.from_numpy(lay["exc_off"]).to(dev), int(exc_h.sum()), D, buf)
+    call("mlk_pack_exceptions", f0, sh_d, S, exc_list, exc_base, exc_off, int(exc_h.sum()), D,
+         buf)
     out = CompressOut(specs=specs, blob_buf=buf, blob_lens=lay["blob_len"],
                       dev=dict(codes=codes, cents=cents, flags=flags, lam=lam, qst=qst,
                                status=status, iters=iters, ferr=ferr, fqoi=fqoi, fsse=fsse,
@@ -525,6 +627,17 @@ def blob_layout(specs, cfg, D, cnt_h, zlen_h, exc_h):
 
 _DEFLATE_POOLS = {}
 DEFLATE_WORK = 1 << 18
+_SCRATCH = {}
+
+
+def _scratch(dev, name, nbytes):
+    """Grow-only named device scratch (uint8), reused across calls."""
+    key = (dev.index, name)
+    buf = _SCRATCH.get(key)
+    if buf is None or buf.numel() < nbytes:
+        _SCRATCH[key] = buf = torch.empty(max(1, int(nbytes * 1.25)), dtype=torch.uint8,
+                                          device=dev)
+    return buf
 
 
 def _deflate_pool(dev, n_workers):
@@ -535,38 +648,74 @@ def _deflate_pool(dev, n_workers):
     return _DEFLATE_POOLS[key]
 
 
-DEFLATE_TIERS = (2048, 4096, 8192, 16000)
+DEFLATE_TIERS = (1024, 1600, 2048, 3072, 4096, 8192, 16000)
 
 
 DEFLATE_PROF = None   # set to a (10,) uint64 CUDA tensor to collect phase cycles
 
 
-def _run_deflate(varint, in_off, vlen, n, zout, zoff, zcap, zlen, dev, max_workers=2048):
-    """Warp-cooperative kernel per size tier; one thread per stream beyond."""
+_TIER_STREAMS = {}
+
+
+def _tier_streams(dev, n):
+    key = dev.index
+    if key not in _TIER_STREAMS:
+        _TIER_STREAMS[key] = [torch.cuda.Stream(device=dev) for _ in range(n)]
+    return _TIER_STREAMS[key]
+
+
+def _run_deflate(ws, varint, in_off, vlen, n, zout, zoff, zcap, zlen, dev, max_workers=2048):
+    """Warp-cooperative kernel per size tier, the tiers concurrently on their own
+    streams (a sparse tier is bounded by single-stream latency, not throughput);
+    one thread per stream beyond the last tier."""
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    sym_cap = 3 * DEFLATE_TIERS[-1] + 16
+    sym = ws.tensor("deflate_sym", (n * sym_cap,), torch.uint8)
+    main = torch.cuda.current_stream(dev)
+    streams = _tier_streams(dev, len(DEFLATE_TIERS) + 1)
+    ev0 = torch.cuda.Event()
+    ev0.record(main)
     lo = 0
-    for hi in DEFLATE_TIERS:
-        call("mlk_zlib_compress6_warp", varint, in_off, vlen, n, lo, hi, zout, zoff, zcap, zlen,
-             4 * sms, DEFLATE_PROF)
-        lo = hi
-    workers = min(n, max_workers)
-    call("mlk_zlib_compress6", varint, in_off, vlen, n, zout, zoff, zcap, zlen,
-         _deflate_pool(dev, workers), workers, lo)
+    for k, hi in enumerate(DEFLATE_TIERS + (None,)):
+        st = streams[k]
+        st.wait_event(ev0)
+        with torch.cuda.stream(st):
+            if hi is None:
+                workers = min(n, max_workers)
+                call("mlk_zlib_compress6", varint, in_off, vlen, n, zout, zoff, zcap, zlen,
+                     _deflate_pool(dev, workers), workers, lo)
+            else:
+                # the few streams of the upper tiers get one block per 2 SMs
+                nb = 2 * sms if k < 3 else max(1, sms // 2)
+                call("mlk_zlib_compress6_warp", varint, in_off, vlen, n, lo, hi, zout, zoff,
+                     zcap, zlen, nb, sym, sym_cap, DEFLATE_PROF)
+                lo = hi
+        ev = torch.cuda.Event()
+        ev.record(st)
+        main.wait_event(ev)
+
+
+def deflate_launch(ws, varint, vcap, vlen, n, dev):
+    """Launch zlib-6 over every varint slot; returns device (zout, zoff, zlen)."""
+    i64 = torch.int64
+    zcap = vcap + 64
+    m = max(1, n)
+    zout = ws.tensor("zout", (m * zcap,), torch.uint8)
+    zlen = ws.tensor("zlen", (m,), i64)
+    in_off = ws.tensor("in_off", (m,), i64)
+    zoff = ws.tensor("zoff", (m,), i64)
+    torch.arange(0, m * vcap, vcap, out=in_off)
+    torch.arange(0, m * zcap, zcap, out=zoff)
+    if n:
+        _run_deflate(ws, varint, in_off, vlen[:n], n, zout, zoff, zcap, zlen, dev)
+    return zout, zoff, zlen
 
 
 def deflate_device(varint, vcap, vlen, n, dev):
     """zlib-6 every varint slot; returns (zout, zoff, zlen) on device + zlen host."""
-    i64 = dict(dtype=torch.int64, device=dev)
-    if n == 0:
-        z = torch.zeros(1, **i64)
-        return torch.zeros(1, dtype=torch.uint8, device=dev), z, z, np.zeros(0, np.int64)
-    zcap = vcap + 64
-    zout = torch.empty(n * zcap, dtype=torch.uint8, device=dev)
-    zlen = torch.empty(n, **i64)
-    in_off = torch.arange(0, n * vcap, vcap, **i64)
-    zoff = torch.arange(0, n * zcap, zcap, **i64)
-    _run_deflate(varint, in_off, vlen[:n], n, zout, zoff, zcap, zlen, dev)
-    zlen_h = zlen.cpu().numpy()
+    ws = Workspace.get(dev)
+    zout, zoff, zlen = deflate_launch(ws, varint, vcap, vlen, n, dev)
+    zlen_h = zlen[:n].cpu().numpy()
     if np.any(zlen_h < 0):
         raise ConfigError("residual stream exceeds the device DEFLATE limits")
     return zout, zoff, zlen, zlen_h

@@ -28,8 +28,8 @@ from .fdata import FDataset, dataset_nbytes
 from .lagrange import NewtonOptions, NewtonStatus
 from .qoi import ErrorReport, compression_ratio, qoi_nrmse_from_moments
 
-__all__ = ["PipelineConfig", "TimestepState", "compress", "decompress", "evaluate",
-           "run_timesteps", "QOI_GATES"]
+__all__ = ["PipelineConfig", "TimestepState", "compress", "compress_distributed", "decompress",
+           "evaluate", "run_timesteps", "QOI_GATES"]
 
 QOI_GATES = {"f32": 1e-8, "f64": 1e-12}
 _STAGES = ("train", "encode", "pq", "find_eb", "newton", "pack", "other")
@@ -167,6 +167,75 @@ def compress(ds: FDataset, config: PipelineConfig, state: TimestepState | None =
     new_state = TimestepState(models=list(state.models),
                               timestep_index=state.timestep_index + 1)
     return archive, report, new_state
+
+
+def compress_distributed(ds: FDataset, config: PipelineConfig, state: TimestepState,
+                         out_path: str | None = None, group=None):
+    """compress() with one process per GPU (torch.distributed initialised).
+
+    Every rank passes the same dataset description; only its own node slab
+    is uploaded to its GPU.  Ranks exchange blob sizes (all_reduce) to place
+    their shards in the archive, write them with pwrite at those offsets
+    into `out_path` (rank 0 also writes the preamble and offset index), and
+    all-reduce the report statistics.  Returns (out_path, report, new_state);
+    the report's per_image_nrmse is empty (it would gather every image)."""
+    import os
+
+    import torch.distributed as dist
+
+    from . import distributed as D_
+    t_all = time.perf_counter()
+    rp = D_.plan(ds.n_planes, ds.n_nodes, config.shards, config.mode)
+    _check_state(config, state, rp.n_shards)
+    dev = _device()
+    lo, hi = rp.node_range
+    f0 = upload_f0(ds.data, dev, (lo, hi))
+    dgrid = engine.DeviceGrid(ds.grid, dev, config.latent_dim)
+    mine = [rp.shards[i] for i in rp.mine]
+    works = engine.shard_layout(mine, [state.models[i] for i in rp.mine], hi - lo,
+                                ds.grid.rows, ds.grid.cols, node_lo=lo)
+    out = engine.compress_device(f0, works, dgrid, config)
+    preamble = ArchivePreamble(n_shards=rp.n_shards, decomp_mode=config.mode,
+                               n_planes=ds.n_planes, n_nodes=ds.n_nodes, grid=ds.grid,
+                               timestep=ds.timestep, tau=config.tau, seed=config.seed,
+                               config_digest=config.digest())
+    head = preamble.pack()
+    sizes, offs = D_.exchange_sizes(rp, out.blob_lens, len(head), group)
+    if out_path is not None:
+        body = out.blob_buf[:int(np.sum(out.blob_lens))].cpu().numpy()
+        if rp.rank == 0:
+            with open(out_path, "wb") as fh:
+                fh.write(head + struct.pack(f"<{len(offs)}Q", *[int(x) for x in offs]))
+                fh.truncate(int(offs[-1] + sizes[-1]))
+        if dist.is_initialized():
+            dist.barrier(group=group)
+        if rp.mine:
+            fd = os.open(out_path, os.O_WRONLY)
+            try:
+                os.pwrite(fd, body.tobytes(), int(offs[rp.mine[0]]))
+            finally:
+                os.close(fd)
+        if dist.is_initialized():
+            dist.barrier(group=group)
+    st = D_.reduce_stats(D_.report_partials(out, config.tau), group)
+    n = float(st["n"][0])
+    span = float(st["data_max"][0] - st["data_min"][0])
+    names = ("n", "u_par", "t_perp", "t_par")
+    qspan = st["qoi_max"] - st["qoi_min"]
+    qerr = {nm: float(np.sqrt(st["qoi_sse"][k] / st["qoi_cnt"][0]) / qspan[k])
+            for k, nm in enumerate(names)}
+    total_bytes = len(head) + 8 * rp.n_shards + int(sizes.sum())
+    report = ErrorReport(
+        pd_nrmse=float(np.sqrt(st["sse"][0] / ds.data.size) / span) if span > 0 else 0.0,
+        per_image_nrmse=[], qoi_nrmse=qerr, max_qoi_nrmse=max(qerr.values()),
+        compression_ratio=compression_ratio(dataset_nbytes(ds), total_bytes),
+        ae_accuracy=float(st["ae_ok"][0]) / n, residual_fraction=float(st["selected"][0]) / n,
+        convergence_fraction=float(st["converged"][0]) / n,
+        exception_count=int(st["exceptions"][0]),
+        stage_timings={"other": {"sum": time.perf_counter() - t_all,
+                                 "max": time.perf_counter() - t_all}})
+    return out_path, report, TimestepState(models=list(state.models),
+                                           timestep_index=state.timestep_index + 1)
 
 
 def build_report(ds, archive, outs, tau, stage_t, wall) -> ErrorReport:
