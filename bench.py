@@ -249,6 +249,10 @@ def main():
         clk.__exit__(None, None, None)
     launches = _lib.LAUNCHES
     probe_rounds = out.timings.get("probe_rounds")
+    it_h, st_h = out.host("iters"), out.host("status")
+    newton = {"mean_iters": float(it_h.mean()), "max_iters": int(it_h.max()),
+              "p50": float(np.percentile(it_h, 50)), "p99": float(np.percentile(it_h, 99)),
+              "status_counts": {int(k): int(v) for k, v in zip(*np.unique(st_h, return_counts=True))}}
     ms = start.elapsed_time(stop) / args.steps
     t = torch.tensor([ms], device=dev)
     if world > 1:
@@ -353,7 +357,8 @@ def main():
                            "tau": args.tau, "lambda": "f32", "parallelism": f"shards/{world}",
                            "l2": "inputs 1.6 GB > 126 MB L2 (no flush needed)"},
                 "raw_gb_s": value * HIST_BYTES / 1e9,
-                "wall_ms_per_step": wall_ms, "stage_ms": stage_ms, "probe_rounds": probe_rounds, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+                "wall_ms_per_step": wall_ms, "stage_ms": stage_ms, "probe_rounds": probe_rounds,
+                "newton": newton, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "decompress_and_report": dec, "gpu_launches": launches,
                 "clocks": clk.summary(),
                 "ratio": None if dec is None else dec["ratio"]}

@@ -217,12 +217,14 @@ int mlk_compact(const uint8_t* flags, const double* stats, const MlkShard* shard
 
 /* residual.find_error_bound's predicate (residual.py:149-155) for n_cand
  * candidate bounds per shard: fail[s*n_cand + c] becomes non-zero when a
- * selected image of shard s misses tau at cand[s*n_cand + c].  act_off
- * (n_shards + 1) enumerates the selected images visited per shard. */
+ * selected image of shard s misses tau at cand[s*n_cand + c].  The launch
+ * visits positions act_start[s] .. act_start[s] + (act_off[s+1] - act_off[s])
+ * of shard s's range-ordered selection (smallest ranges fail first). */
 int mlk_probe(const double* f0, const double* stats, const MlkShard* shards,
               int32_t n_shards, const MlkGrid* grid_h, const float* W, int32_t L,
               const float* cents, int32_t K, const uint8_t* codes,
-              const int32_t* sel_by_range, const int32_t* act_off, int32_t n_work,
+              const int32_t* sel_by_range, const int32_t* act_off, const int32_t* act_start,
+              int32_t n_work,
               const double* recon_bound, double tau, const double* cand, int32_t n_cand,
               int32_t* fail, cudaStream_t stream);
 

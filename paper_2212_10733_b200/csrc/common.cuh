@@ -160,10 +160,77 @@ __device__ __forceinline__ double decode_cell(const double* z, const float* W, i
         s = __dadd_rn(__dadd_rn(p0, p1), __dadd_rn(p2, p3));
     } else {
         s = __dmul_rn(z[0], (double)__ldg(W + j));
-        for (int k = 1; k < L; ++k)
-            s = __dadd_rn(s, __dmul_rn(z[k], (double)__ldg(W + (long long)k * D + j)));
+#pragma unroll
+        for (int k = 1; k < MLK_MAXL; ++k)  // unrolled + guarded: z stays in registers
+            if (k < L) s = __dadd_rn(s, __dmul_rn(z[k], (double)__ldg(W + (long long)k * D + j)));
     }
     return __dadd_rn(__dmul_rn(s, sd), mean);
 }
 
 __device__ __forceinline__ bool is_finite(double x) { return isfinite(x); }
+
+// ----------------------------------------------------------------------------
+// TMA bulk copies (cp.async.bulk, sm_90+) with an mbarrier, for staging one
+// histogram into shared memory with a single instruction.  A 39x39 fp64
+// histogram is 12,168 B = 8 mod 16, so odd histograms start 8 B off the
+// 16-B alignment the bulk copy needs: copy the 16-B-aligned superset and
+// return the offset of the first element inside it (callers allocate D + 2
+// doubles per buffer and the f0 buffer carries 16 B of tail padding).
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+                 : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes,
+                                         unsigned long long* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+            "r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phase) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
+
+// Issue (lane 0) the bulk copy of histogram `x` (D doubles) into `buf`
+// (D + 2 doubles, 16-B aligned); returns the element offset (0 or 1).
+__device__ __forceinline__ int stage_histogram(double* buf, const double* x, int D,
+                                               unsigned long long* bar) {
+    const unsigned long long a = reinterpret_cast<unsigned long long>(x);
+    const int shift = (int)((a & 15ull) >> 3);
+    const double* src = x - shift;
+    const unsigned bytes = (unsigned)(((D + shift) * 8 + 15) & ~15);
+    if ((threadIdx.x & 31) == 0) {
+        mbar_expect_tx(bar, bytes);
+        bulk_g2s(buf, src, bytes, bar);
+    }
+    return shift;
+}
+
+// rint(r / eb2) without a division per cell: y = r * (1 / eb2) is within a
+// few ulps of the quotient, so its nearest integer is the quotient's unless
+// y sits within that error of a .5 tie -- then divide exactly.
+__device__ __forceinline__ double qround(double r, double eb2, double inv) {
+    const double y = r * inv;
+    const double fy = y - floor(y);
+    if (fabs(y) >= 2251799813685248.0 || fabs(fy - 0.5) <= 8.9e-16 * fabs(y) + 1e-300)
+        return rint(__ddiv_rn(r, eb2));
+    return rint(y);
+}

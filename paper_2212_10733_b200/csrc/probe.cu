@@ -20,23 +20,14 @@ namespace {
 constexpr int PW_WARPS = 4;
 constexpr int MAXC = 16;  // candidates per launch (2**LOOKAHEAD - 1)
 
-// q = rint(r / eb2) exactly as numpy (true division then rint).  The
-// reciprocal product is exact except within an ulp of a rounding boundary
-// of the quotient, which is only visible to rint at half-integers; those
-// (and huge quotients) take the IEEE division.
-__device__ __forceinline__ double qround(double r, double eb2, double inv) {
-    const double y = r * inv;
-    const double fy = y - floor(y);
-    if (fabs(y) >= 2251799813685248.0 || fabs(fy - 0.5) <= 8.9e-16 * fabs(y) + 1e-300)
-        return rint(__ddiv_rn(r, eb2));
-    return rint(y);
-}
+// q = rint(r / eb2): qround() in common.cuh.
 
 __global__ void __launch_bounds__(32 * PW_WARPS)
 k_probe(const double* __restrict__ f0, const double* __restrict__ stats,
         const MlkShard* __restrict__ shards, MlkGrid g, PwPlan pw, const float* __restrict__ W,
         int L, const float* __restrict__ cents, int K, const unsigned char* __restrict__ codes,
-        const int* __restrict__ sel_by_range, const int* __restrict__ act_off, int n_shards,
+        const int* __restrict__ sel_by_range, const int* __restrict__ act_off,
+        const int* __restrict__ act_start, int n_shards,
         const double* __restrict__ recon_bound, double tau, const double* __restrict__ cand,
         int n_cand, int* fail) {
     extern __shared__ double smem[];
@@ -48,7 +39,7 @@ k_probe(const double* __restrict__ f0, const double* __restrict__ stats,
     if (gw >= act_off[n_shards]) return;
     int s = 0;
     while (act_off[s + 1] <= gw) ++s;
-    const int pos = gw - act_off[s];
+    const int pos = gw - act_off[s] + act_start[s];
     const MlkShard sh = shards[s];
     const int j = sel_by_range[sh.img_off + pos];
     const int img = sh.img_off + j;
@@ -134,12 +125,13 @@ k_probe(const double* __restrict__ f0, const double* __restrict__ stats,
 PwPlan mlk_make_pw_plan(int n);
 
 // act_off[s]..act_off[s+1] enumerates the selected images of shard s that
-// the launch visits (zero-length for shards whose search is over);
-// n_work = act_off[n_shards] (host copy).
+// the launch visits -- positions act_start[s] + k of its range-ordered list
+// (zero-length for shards whose search is over); n_work = act_off[n_shards].
 extern "C" int mlk_probe(const double* f0, const double* stats, const MlkShard* shards,
                          int32_t n_shards, const MlkGrid* grid_h, const float* W, int32_t L,
                          const float* cents, int32_t K, const uint8_t* codes,
-                         const int32_t* sel_by_range, const int32_t* act_off, int32_t n_work,
+                         const int32_t* sel_by_range, const int32_t* act_off,
+                         const int32_t* act_start, int32_t n_work,
                          const double* recon_bound, double tau, const double* cand,
                          int32_t n_cand, int32_t* fail, cudaStream_t stream) {
     if (n_work <= 0) return MLK_OK;
@@ -148,7 +140,7 @@ extern "C" int mlk_probe(const double* f0, const double* stats, const MlkShard* 
     size_t sm = (size_t)PW_WARPS * (grid_h->D + MLK_PW_MAX_LEAVES) * sizeof(double);
     cudaFuncSetAttribute(k_probe, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     k_probe<<<(n_work + PW_WARPS - 1) / PW_WARPS, 32 * PW_WARPS, sm, stream>>>(
-        f0, stats, shards, *grid_h, pw, W, L, cents, K, codes, sel_by_range, act_off, n_shards,
-        recon_bound, tau, cand, n_cand, fail);
+        f0, stats, shards, *grid_h, pw, W, L, cents, K, codes, sel_by_range, act_off, act_start,
+        n_shards, recon_bound, tau, cand, n_cand, fail);
     return cudaGetLastError() == cudaSuccess ? MLK_OK : MLK_ERR_CUDA;
 }

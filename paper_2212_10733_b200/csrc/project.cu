@@ -1,7 +1,7 @@
 // project.cu -- residual coding + Lagrange QoI projection + final PD gate.
 //
-// One CTA (128 threads) per histogram; each thread owns CELLS contiguous
-// cells in registers.  Replaces, per image, pipeline.py:239-292:
+// One CTA (128 threads) per histogram.  Replaces, per image,
+// pipeline.py:239-292:
 //   * residual q = rint(r / 2eb), zigzag, LEB128 (residual.py:60-79,
 //     _ckernels.pyx:143-171) for selected images -- the varint stream goes
 //     to a per-payload slot for the DEFLATE stage;
@@ -12,73 +12,118 @@
 //   * cast_lambda (lagrange.py:239-253), apply_lambda_batch (152-185) in the
 //     reference's exact elementwise order, the final per-image NRMSE in
 //     numpy's pairwise order and the tau gate (pipeline.py:284-292).
+//
+// Shared memory holds two histogram-sized buffers (the TMA-staged original,
+// later the squared errors; the working image) so 6-7 CTAs fit an SM.  The
+// Newton iteration is split: every thread accumulates its cells' 14 sums,
+// a warp reduce-scatter + one shared-memory pass combine them, and warp 0
+// alone solves the 4x4 system, updates lambda and (separable grids) the
+// exponent tables for the next iteration.  Two barriers per iteration.
 #include "common.cuh"
 
 namespace {
 
 constexpr int PJ_T = 128;
 constexpr int PJ_W = PJ_T / 32;
-constexpr int NRED = 16;
+constexpr unsigned FULL = 0xffffffffu;
 
-struct PjShared {
-    double red[2][PJ_W][NRED];
+struct PjCtl {
+    double part[PJ_W][16];  // per-warp Newton sums (index 14: clamp flag)
+    double red[2][PJ_W][16];
+    double lam[4];          // current iterate (read by the direct path)
+    double lu[4];           // lambdas applied to the image
+    double ea[2][64];       // exp(-vol * A_c) by row-edge class
+    double eb[2][64];       // exp(-vol * B_r) by column-edge class
+    double vp1[64];         // vpar_c / s1
+    double p3c[64];         // hm (vpar_c - u)^2 / s4        (per image)
+    double p2r[64];         // hm vperp2_r / s2
     double leaf[MLK_PW_MAX_LEAVES];
-    int iscan[PJ_W];
     double bval;
+    int iscan[PJ_W];
+    int go, direct, status, iters;
+    unsigned flags;
 };
 
 template <int NV>
-__device__ __forceinline__ void block_allsum(double (&v)[NV], PjShared& S, int& ph) {
+__device__ __forceinline__ void block_allsum(double (&v)[NV], PjCtl& C, int& ph) {
+    static_assert(NV <= 16, "PjCtl::red holds 16 values per warp");
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
 #pragma unroll
     for (int k = 0; k < NV; ++k) v[k] = warp_sum(v[k]);
     if (lane == 0) {
 #pragma unroll
-        for (int k = 0; k < NV; ++k) S.red[ph][w][k] = v[k];
+        for (int k = 0; k < NV; ++k) C.red[ph][w][k] = v[k];
     }
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < NV; ++k) {
-        double t = S.red[ph][0][k];
+        double t = C.red[ph][0][k];
 #pragma unroll
-        for (int q = 1; q < PJ_W; ++q) t += S.red[ph][q][k];
+        for (int q = 1; q < PJ_W; ++q) t += C.red[ph][q][k];
         v[k] = t;
     }
     ph ^= 1;
 }
 
-__device__ __forceinline__ double block_allmax(double v, PjShared& S, int& ph) {
+// NaN-propagating max of two values over the block
+__device__ __forceinline__ void block_allmax2(double& a, double& b, PjCtl& C, int& ph) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v = np_max2(v, __shfl_xor_sync(0xffffffffu, v, o));
-    if (lane == 0) S.red[ph][w][0] = v;
+    for (int o = 16; o > 0; o >>= 1) {
+        a = np_max2(a, __shfl_xor_sync(FULL, a, o));
+        b = np_max2(b, __shfl_xor_sync(FULL, b, o));
+    }
+    if (lane == 0) {
+        C.red[ph][w][0] = a;
+        C.red[ph][w][1] = b;
+    }
     __syncthreads();
-    double t = S.red[ph][0][0];
+    a = C.red[ph][0][0];
+    b = C.red[ph][0][1];
 #pragma unroll
-    for (int q = 1; q < PJ_W; ++q) t = np_max2(t, S.red[ph][q][0]);
+    for (int q = 1; q < PJ_W; ++q) {
+        a = np_max2(a, C.red[ph][q][0]);
+        b = np_max2(b, C.red[ph][q][1]);
+    }
     ph ^= 1;
-    return t;
 }
 
-__device__ __forceinline__ int block_exscan_int(int v, int* total, PjShared& S) {
+__device__ __forceinline__ int block_exscan_int(int v, int* total, PjCtl& C) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     int inc = v;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-        int t = __shfl_up_sync(0xffffffffu, inc, o);
+        int t = __shfl_up_sync(FULL, inc, o);
         if (lane >= o) inc += t;
     }
     __syncthreads();
-    if (lane == 31) S.iscan[w] = inc;
+    if (lane == 31) C.iscan[w] = inc;
     __syncthreads();
     int base = 0, tot = 0;
 #pragma unroll
     for (int q = 0; q < PJ_W; ++q) {
-        if (q < w) base += S.iscan[q];
-        tot += S.iscan[q];
+        if (q < w) base += C.iscan[q];
+        tot += C.iscan[q];
     }
     *total = tot;
     return base + inc - v;
+}
+
+// 16 per-lane values -> lane l holds the warp sum of value l >> 1
+// (reduce-scatter: 16 shuffles instead of 80).
+__device__ __forceinline__ double warp_rs16(double (&v)[16]) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int h = 8; h >= 1; h >>= 1) {
+        const bool up = (lane & (2 * h)) != 0;
+#pragma unroll
+        for (int i = 0; i < h; ++i) {
+            const double send = up ? v[i] : v[i + h];
+            const double keep = up ? v[i + h] : v[i];
+            v[i] = keep + __shfl_xor_sync(FULL, send, 2 * h);
+        }
+    }
+    return v[0] + __shfl_xor_sync(FULL, v[0], 1);
 }
 
 // _ckernels.pyx:25-59 (same pivot rule and failure tests), written so every
@@ -132,137 +177,263 @@ __device__ __forceinline__ int solve4(const double* m, const double* r, double* 
     return 0;
 }
 
-// Separable exponent (trapezoid make_grid grids, fdata.py:151-167): every
-// feature row carries vol, so t = vol_rc * (A_c + B_r) with
-//   A_c = l0/s0 + l1 vpar_c/s1 + l3 hm (vpar_c - u)^2/s3,  B_r = l2 hm vperp_r^2/s2,
-// and vol_rc takes one of 4 values set by (row edge, col edge).  exp(-t)
-// is then EA[row edge][c] * EB[col edge][r]: 4 * 39 exps per iteration instead
-// of 1521.  Only the Newton iterate uses it (tolerance-level, like the
-// reference's own summation order); the stored image uses the exact formula.
-struct SepCtx {
-    const double* vpar;    // per cell (row 0 holds the column values)
-    const double* vperp2;  // per cell (column 0 holds the row values)
-    int rows, cols;
-    double vcls[4];        // vol for (row edge, col edge) = 2 re + ce
-    double s0, s1, s2, s4, hm, u;
-};
+// The 14 Newton sums of one cell: v[0..3] += a_k f, v[4..13] += a_k a_l f.
+__device__ __forceinline__ void cell_sums(double (&v)[16], double a0, double a1, double a2,
+                                          double a3, double f) {
+    const double f0 = a0 * f, f1 = a1 * f, f2 = a2 * f, f3 = a3 * f;
+    v[0] += f0; v[1] += f1; v[2] += f2; v[3] += f3;
+    v[4] += a0 * f0; v[5] += a0 * f1; v[6] += a0 * f2; v[7] += a0 * f3;
+    v[8] += a1 * f1; v[9] += a1 * f2; v[10] += a1 * f3;
+    v[11] += a2 * f2; v[12] += a2 * f3; v[13] += a3 * f3;
+}
 
-struct SepSmem {
-    double ea[2][64];
-    double eb[2][64];
-    int too_big;
-};
-
-template <bool SEP>
-__device__ int newton(const double* fp, const double* __restrict__ ash, const double* a3n, int D,
-                      const double* b, double step, int max_iter, double tol, double* lam,
-                      int* iters, PjShared& S, int& ph, const SepCtx& sc, SepSmem& E) {
-    double bmax = 0.0;
+// One Newton step from the 15 reduced sums (warp-uniform); returns 1 while
+// the iteration continues.  Same tests and order as _ckernels.pyx:62-137.
+__device__ __forceinline__ int newton_step(const double* v, const double* b, double bmax,
+                                           double step, int max_iter, double tol, int it,
+                                           double (&lam)[4], bool& clamped, int& status,
+                                           int& iters) {
+    if (v[14] > 0.0) clamped = true;
+    double g[4] = {v[0] - b[0], v[1] - b[1], v[2] - b[2], v[3] - b[3]};
+    double m[16] = {v[4], v[5], v[6], v[7], v[5], v[8], v[9], v[10],
+                    v[6], v[9], v[11], v[12], v[7], v[10], v[12], v[13]};
+    double gmax = 0.0;
+    bool bad = false;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-        lam[k] = 0.0;
-        bmax = fmax(bmax, fabs(b[k]));
+        if (!isfinite(g[k])) bad = true;
+        gmax = fmax(gmax, fabs(g[k]));
     }
-    *iters = max_iter;
-    if (bmax <= 0.0 || !isfinite(bmax)) { *iters = 0; return MLK_NEWTON_DEGENERATE; }
+    if (bad) { iters = it; status = MLK_NEWTON_DEGENERATE; return 0; }
+    if (gmax <= tol * bmax) {
+        iters = it;
+        status = clamped ? MLK_NEWTON_MAX_ITER : MLK_NEWTON_CONVERGED;
+        return 0;
+    }
+    if (it == max_iter) { iters = max_iter; status = MLK_NEWTON_MAX_ITER; return 0; }
+    double d[4];
+    if (solve4(m, g, d) != 0) {
+        const double jit = 1e-14 * (m[0] + m[5] + m[10] + m[15]);
+        bool fail = true;
+        if (jit > 0.0 && isfinite(jit)) {
+            m[0] += jit; m[5] += jit; m[10] += jit; m[15] += jit;
+            fail = solve4(m, g, d) != 0;
+        }
+        if (fail) { iters = it; status = MLK_NEWTON_DEGENERATE; return 0; }
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) lam[k] += step * d[k];
+    return 1;
+}
+
+// Generic Newton over explicit constraint rows a (4, d) for the operator API
+// (kernels.newton_solve): every thread redundantly solves (one CTA/system).
+__device__ int newton_generic(const double* fp, const double* __restrict__ a, int D,
+                              const double* b, double step, int max_iter, double tol,
+                              double* lam_out, int* iters, PjCtl& C, int& ph) {
+    double lam[4] = {0.0, 0.0, 0.0, 0.0};
+    double bmax = 0.0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) bmax = fmax(bmax, fabs(b[k]));
+    *iters = 0;
+    int status = MLK_NEWTON_DEGENERATE;
+    if (bmax <= 0.0 || !isfinite(bmax)) {
+        for (int k = 0; k < 4; ++k) lam_out[k] = 0.0;
+        return status;
+    }
     bool clamped = false;
-    const int tid = threadIdx.x;
-    const int cstep = SEP ? PJ_T % sc.cols : 0, rstep = SEP ? PJ_T / sc.cols : 0;
-    const int r0 = SEP ? tid / sc.cols : 0, c0 = SEP ? tid % sc.cols : 0;
+    int it_out = max_iter;
+    status = MLK_NEWTON_MAX_ITER;
     for (int it = 0; it <= max_iter; ++it) {
-        bool direct = true;
-        if (SEP) {
-            if (tid == 0) E.too_big = 0;
-            __syncthreads();
-            if (tid < 2 * sc.cols) {
-                const int c = tid % sc.cols, re = tid / sc.cols;
-                const int ce = (c == 0 || c == sc.cols - 1);
-                const double dv = sc.vpar[c] - sc.u;
-                const double A = lam[0] / sc.s0 + lam[1] * sc.vpar[c] / sc.s1 +
-                                 lam[3] * sc.hm * dv * dv / sc.s4;
-                const double x = sc.vcls[2 * re + ce] * A;
-                if (fabs(x) > 349.0 || !isfinite(x)) E.too_big = 1;
-                E.ea[re][c] = exp(-x);
-            } else if (tid - 2 * sc.cols < 2 * sc.rows) {
-                const int q = tid - 2 * sc.cols;
-                const int r = q % sc.rows, ce = q / sc.rows;
-                const int re = (r == 0 || r == sc.rows - 1);
-                const double B = lam[2] * sc.hm * sc.vperp2[r * sc.cols] / sc.s2;
-                const double x = sc.vcls[2 * re + ce] * B;
-                if (fabs(x) > 349.0 || !isfinite(x)) E.too_big = 1;
-                E.eb[ce][r] = exp(-x);
-            }
-            __syncthreads();
-            direct = E.too_big != 0;
-        }
-        double v[15];
+        double v[16];
 #pragma unroll
-        for (int k = 0; k < 15; ++k) v[k] = 0.0;
-        int r = r0, c = c0;
-        for (int j = tid; j < D; j += PJ_T) {
-            const double a0 = __ldg(ash + j), a1 = __ldg(ash + D + j), a2 = __ldg(ash + 2 * D + j);
-            const double a3 = a3n[j];
-            double f;
-            if (SEP && !direct) {
-                const int re = (r == 0 || r == sc.rows - 1);
-                const int ce = (c == 0 || c == sc.cols - 1);
-                f = fp[j] * E.ea[re][c] * E.eb[ce][r];
-            } else {
-                double t = lam[0] * a0 + lam[1] * a1 + lam[2] * a2 + lam[3] * a3;
-                if (fabs(t) > 700.0) { v[14] = 1.0; t = t > 0 ? 700.0 : -700.0; }
-                f = fp[j] * exp(-t);
-            }
-            const double f0 = a0 * f, f1 = a1 * f, f2 = a2 * f, f3 = a3 * f;
-            v[0] += f0; v[1] += f1; v[2] += f2; v[3] += f3;
-            v[4] += a0 * f0; v[5] += a0 * f1; v[6] += a0 * f2; v[7] += a0 * f3;
-            v[8] += a1 * f1; v[9] += a1 * f2; v[10] += a1 * f3;
-            v[11] += a2 * f2; v[12] += a2 * f3; v[13] += a3 * f3;
-            if (SEP) {
-                c += cstep;
-                r += rstep;
-                if (c >= sc.cols) { c -= sc.cols; ++r; }
-            }
+        for (int k = 0; k < 16; ++k) v[k] = 0.0;
+        for (int j = threadIdx.x; j < D; j += PJ_T) {
+            const double a0 = __ldg(a + j), a1 = __ldg(a + D + j), a2 = __ldg(a + 2 * D + j),
+                         a3 = __ldg(a + 3 * D + j);
+            double t = lam[0] * a0 + lam[1] * a1 + lam[2] * a2 + lam[3] * a3;
+            if (fabs(t) > 700.0) { v[14] = 1.0; t = t > 0 ? 700.0 : -700.0; }
+            cell_sums(v, a0, a1, a2, a3, fp[j] * exp(-t));
         }
-        block_allsum(v, S, ph);
-        if (v[14] > 0.0) clamped = true;
-        double g[4] = {v[0] - b[0], v[1] - b[1], v[2] - b[2], v[3] - b[3]};
-        double m[16] = {v[4], v[5], v[6], v[7], v[5], v[8], v[9], v[10],
-                        v[6], v[9], v[11], v[12], v[7], v[10], v[12], v[13]};
-        double gmax = 0.0;
-        bool bad = false;
+        double r[15];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            if (!isfinite(g[k])) bad = true;
-            gmax = fmax(gmax, fabs(g[k]));
-        }
-        if (bad) { *iters = it; return MLK_NEWTON_DEGENERATE; }
-        if (gmax <= tol * bmax) {
-            *iters = it;
-            return clamped ? MLK_NEWTON_MAX_ITER : MLK_NEWTON_CONVERGED;
-        }
-        if (it == max_iter) break;
-        double d[4];
-        if (solve4(m, g, d) != 0) {
-            const double jit = 1e-14 * (m[0] + m[5] + m[10] + m[15]);
-            bool fail = true;
-            if (jit > 0.0 && isfinite(jit)) {
-                m[0] += jit; m[5] += jit; m[10] += jit; m[15] += jit;
-                fail = solve4(m, g, d) != 0;
-            }
-            if (fail) { *iters = it; return MLK_NEWTON_DEGENERATE; }
-        }
-#pragma unroll
-        for (int k = 0; k < 4; ++k) lam[k] += step * d[k];
+        for (int k = 0; k < 15; ++k) r[k] = v[k];
+        block_allsum(r, C, ph);
+        if (!newton_step(r, b, bmax, step, max_iter, tol, it, lam, clamped, status, it_out))
+            break;
     }
-    return MLK_NEWTON_MAX_ITER;
+    *iters = it_out;
+    for (int k = 0; k < 4; ++k) lam_out[k] = lam[k];
+    return status;
+}
+
+// ---------------------------------------------------------------------------
+// Separable exponent (trapezoid make_grid grids, fdata.py:151-167): every
+// feature row carries vol, so t = vol_rc * (A_c + B_r) with
+//   A_c = l0/s0 + l1 vpar_c/s1 + l3 hm (vpar_c - u)^2/s4,  B_r = l2 hm vperp_r^2/s2,
+// and vol_rc takes one of 4 values set by (row edge, col edge).  exp(-t)
+// is then ea[row edge][c] * eb[col edge][r]: 2 (rows + cols) exps per
+// iteration instead of rows * cols.  Only the Newton iterate uses it
+// (tolerance-level, like the reference's own summation order); the stored
+// image uses the exact per-cell formula.
+
+__device__ __forceinline__ double cls_val(const double (&w)[4], bool re, bool ce) {
+    return re ? (ce ? w[3] : w[2]) : (ce ? w[1] : w[0]);
+}
+
+struct NtCtx {
+    double w[4];  // vol by class (2 re + ce)
+    double is0, is4, u;
+    int rows, cols;
+};
+
+// warp 0: exponent tables for lam; returns true (warp-uniform) when some
+// |t| could exceed the reference's +-700 clamp (the caller then evaluates
+// that iteration cell by cell).
+__device__ __forceinline__ bool sep_tables(const double (&lam)[4], const NtCtx& X, PjCtl& C) {
+    const int lane = threadIdx.x & 31;
+    const int rows = X.rows, cols = X.cols;
+    bool big = false;
+    for (int q = lane; q < 2 * (rows + cols); q += 32) {
+        double x;
+        if (q < 2 * cols) {
+            const int re = q >= cols, c = q - re * cols;
+            const bool ce = (c == 0) | (c == cols - 1);
+            x = cls_val(X.w, re, ce) * (lam[0] * X.is0 + lam[1] * C.vp1[c] + lam[3] * C.p3c[c]);
+            C.ea[re][c] = exp(-x);
+        } else {
+            const int q2 = q - 2 * cols;
+            const int ce = q2 >= rows, r = q2 - ce * rows;
+            const bool re = (r == 0) | (r == rows - 1);
+            x = cls_val(X.w, re, ce) * (lam[2] * C.p2r[r]);
+            C.eb[ce][r] = exp(-x);
+        }
+        if (!(fabs(x) <= 349.0)) big = true;
+    }
+    return __any_sync(FULL, big);
+}
+
+// The block's Newton iteration for one image.  All threads call it; the
+// result (status, iters, lam) is valid in warp 0.
+template <bool SEP>
+__device__ void newton_block(const double* fp, const MlkGrid& g, const NtCtx& X, const double* b,
+                             double bmax, double step, int max_iter, double tol, PjCtl& C,
+                             double (&lam)[4], int& status, int& iters) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int D = g.D, rows = X.rows, cols = X.cols;
+    bool clamped = false;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) lam[k] = 0.0;
+    status = MLK_NEWTON_MAX_ITER;
+    iters = max_iter;
+    if (warp == 0) {
+        const bool big = SEP ? sep_tables(lam, X, C) : true;
+        if (lane == 0) {
+            C.direct = big;
+            C.go = 1;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) C.lam[k] = 0.0;
+        }
+    }
+    __syncthreads();
+    // (r, c) of this thread's first cell and the stride PJ_T in (rows, cols)
+    const int dr = PJ_T / cols, dc = PJ_T - dr * cols;
+    for (int it = 0;; ++it) {
+        if (!C.go) break;
+        double v[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) v[k] = 0.0;
+        if (SEP && !C.direct) {
+            int r = tid / cols, c = tid - (tid / cols) * cols;
+            for (int j = tid; j < D; j += PJ_T) {
+                const bool re = (r == 0) | (r == rows - 1), ce = (c == 0) | (c == cols - 1);
+                const double w = cls_val(X.w, re, ce);
+                const double f = fp[j] * C.ea[re][c] * C.eb[ce][r];
+                cell_sums(v, w * X.is0, w * C.vp1[c], w * C.p2r[r], w * C.p3c[c], f);
+                c += dc;
+                r += dr;
+                if (c >= cols) { c -= cols; ++r; }
+            }
+        } else {
+            const double l0 = C.lam[0], l1 = C.lam[1], l2 = C.lam[2], l3 = C.lam[3];
+            for (int j = tid; j < D; j += PJ_T) {
+                const double a0 = __ldg(g.ash + j), a1 = __ldg(g.ash + D + j),
+                             a2 = __ldg(g.ash + 2 * D + j);
+                const double dv = __ldg(g.vpar + j) - X.u;
+                const double a3 = __ldg(g.hmvol + j) * dv * dv * X.is4;
+                double t = l0 * a0 + l1 * a1 + l2 * a2 + l3 * a3;
+                if (fabs(t) > 700.0) { v[14] = 1.0; t = t > 0 ? 700.0 : -700.0; }
+                cell_sums(v, a0, a1, a2, a3, fp[j] * exp(-t));
+            }
+        }
+        const double part = warp_rs16(v);
+        if (!(lane & 1)) C.part[warp][lane >> 1] = part;
+        __syncthreads();
+        if (warp == 0) {
+            double tot = 0.0;
+            if (lane < 16) {
+                tot = C.part[0][lane];
+#pragma unroll
+                for (int q = 1; q < PJ_W; ++q) tot += C.part[q][lane];
+            }
+            double s[15];
+#pragma unroll
+            for (int k = 0; k < 15; ++k) s[k] = __shfl_sync(FULL, tot, k);
+            int go = newton_step(s, b, bmax, step, max_iter, tol, it, lam, clamped, status, iters);
+            bool big = true;
+            if (go && SEP) big = sep_tables(lam, X, C);
+            if (lane == 0) {
+                C.go = go;
+                C.direct = big;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) C.lam[k] = lam[k];
+            }
+        }
+        __syncthreads();
+    }
 }
 
 __device__ __forceinline__ int varint_len(unsigned long long z) {
     return z == 0ull ? 1 : (64 - __clzll(z) + 6) / 7;
 }
 
+// exact numpy pairwise sum of v[0..n) by the whole block: thread (leaf,
+// accumulator) pairs run the 8 strided accumulators, the ((r0+r1)+(r2+r3))+
+// ((r4+r5)+(r6+r7)) tree runs over 8-lane groups, thread 0 combines leaves.
+__device__ double block_pairwise(const double* v, const PwPlan& pw, PjCtl& C) {
+    const int tid = threadIdx.x, a = tid & 7;
+    for (int l0 = 0; l0 < pw.n_leaves; l0 += PJ_T / 8) {
+        const int l = l0 + (tid >> 3);
+        int st = 0, len = 0;
+        if (l < pw.n_leaves) { st = pw.start[l]; len = pw.len[l]; }
+        const int lim = len - (len % 8);
+        double r = 0.0;
+        if (len >= 8) {
+            r = v[st + a];
+            for (int i = a + 8; i < lim; i += 8) r = __dadd_rn(r, v[st + i]);
+        }
+        r = __dadd_rn(r, __shfl_down_sync(FULL, r, 1));
+        r = __dadd_rn(r, __shfl_down_sync(FULL, r, 2));
+        r = __dadd_rn(r, __shfl_down_sync(FULL, r, 4));
+        if (a == 0 && l < pw.n_leaves) {
+            double s = 0.0;
+            int i = 0;
+            if (len >= 8) { s = r; i = lim; }
+            for (; i < len; ++i) s = __dadd_rn(s, v[st + i]);
+            C.leaf[l] = s;
+        }
+    }
+    __syncthreads();
+    if (tid == 0) {
+        int next = 0;
+        C.bval = pw_combine(C.leaf, pw.n, next);
+    }
+    __syncthreads();
+    return C.bval;
+}
+
 template <bool SEP>
-__global__ void __launch_bounds__(PJ_T, 4)
+__global__ void __launch_bounds__(PJ_T, 6)
 k_project(const double* __restrict__ f0, const double* __restrict__ stats,
           const double* __restrict__ qoi, const MlkShard* __restrict__ shards, int n_shards,
           MlkGrid g, PwPlan pw, const float* __restrict__ W, int L, const float* __restrict__ cents,
@@ -273,30 +444,58 @@ k_project(const double* __restrict__ f0, const double* __restrict__ stats,
           double* __restrict__ ferr_out, double* __restrict__ fqoi_out,
           double* __restrict__ fsse_out, unsigned char* __restrict__ varint, long long vcap,
           long long* __restrict__ vlen, int* __restrict__ err_flag) {
-    __shared__ PjShared S;
-    __shared__ SepSmem E;
-    extern __shared__ double sm[];
+    __shared__ PjCtl C;
+    __shared__ unsigned long long bar;
+    extern __shared__ __align__(16) double sm[];
     const int D = g.D;
-    double* O = sm;          // the original histogram
-    double* F = sm + D;      // recon -> corrected -> f_plus -> final
-    double* A = sm + 2 * D;  // a3 / s4 -> d^2
     const int img = blockIdx.x;
-    const int tid = threadIdx.x, lane = tid & 31;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     int ph = 0;
     const int s = find_shard(shards, n_shards, img);
     const MlkShard sh = shards[s];
     const double* x = shard_image(f0, sh, img - sh.img_off, D);
+    double* Ob = sm;                     // TMA target: the original, later d^2
+    double* F = sm + ((D + 3) / 2) * 2;  // recon -> corrected -> f_plus -> final
 
-    // ---- stage the histogram, AE reconstruction (exact decode order)
+    // ---- one bulk copy of the original; the AE decode overlaps it
+    if (tid == 0) mbar_init(&bar, 1);
+    __syncthreads();
+    int shift;
+    if (warp == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        shift = stage_histogram(Ob, x, D, &bar);
+    } else {
+        shift = (int)((reinterpret_cast<unsigned long long>(x) & 15ull) >> 3);
+    }
+    double* O = Ob + shift;
     double z[MLK_MAXL];
-    for (int k = 0; k < L; ++k)
-        z[k] = (double)cents[((long long)s * L + k) * K + codes[(long long)img * L + k]];
+#pragma unroll
+    for (int k = 0; k < MLK_MAXL; ++k)
+        z[k] = k < L ? (double)cents[((long long)s * L + k) * K + codes[(long long)img * L + k]]
+                     : 0.0;
     const float* Ws = W + sh.w_off;
     const bool blas_tree = !sh.small_blas;
-    for (int j = tid; j < D; j += PJ_T) {
-        O[j] = x[j];
+    for (int j = tid; j < D; j += PJ_T)
         F[j] = decode_cell(z, Ws, L, D, j, blas_tree && g.tree_cols[j], sh.mean, sh.std);
+    // per-grid / per-image column and row tables of the separable Newton
+    const double4 q4 = reinterpret_cast<const double4*>(qoi)[img];
+    double qs[4] = {q4.x, q4.y, q4.z, q4.w};
+    if (opt.lam_f32) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) qs[k] = (double)__double2float_rn(qs[k]);
     }
+    const double hm = 0.5 * g.mass;
+    if (SEP) {
+        if (tid < g.cols) {
+            const double vp = g.vpar[tid];
+            C.vp1[tid] = vp / g.s1;
+            const double dv = vp - qs[1];
+            C.p3c[tid] = hm * dv * dv;  // / s4 once s4 is known
+        } else if (tid >= 64 && tid - 64 < g.rows) {
+            C.p2r[tid - 64] = hm * g.vperp2[(tid - 64) * g.cols] / g.s2;
+        }
+    }
+    mbar_wait(&bar, 0);
     __syncthreads();
 
     // ---- residual stage for selected images (contiguous cells per thread so
@@ -304,6 +503,7 @@ k_project(const double* __restrict__ f0, const double* __restrict__ stats,
     const int rank = sel_rank[img];
     if (rank >= 0) {  // block-uniform
         const double eb2 = 2.0 * sh.eb;
+        const double inv = 1.0 / eb2;
         const bool lossless = sh.lossless != 0;
         const int per = (D + PJ_T - 1) / PJ_T;
         const int c0 = min(D, tid * per), c1 = min(D, c0 + per);
@@ -315,7 +515,7 @@ k_project(const double* __restrict__ f0, const double* __restrict__ stats,
             if (lossless) {
                 zz = (unsigned long long)__double_as_longlong(r);
             } else {
-                const double q = rint(__ddiv_rn(r, eb2));
+                const double q = qround(r, eb2, inv);
                 if (!(fabs(q) < 4611686018427387904.0)) too_big = true;
                 const long long qi = (long long)q;
                 zz = ((unsigned long long)qi << 1) ^ (unsigned long long)(qi >> 63);
@@ -324,7 +524,7 @@ k_project(const double* __restrict__ f0, const double* __restrict__ stats,
         }
         if (too_big) atomicExch(err_flag, MLK_ERR_CONFIG);
         int tot = 0;
-        int pos = block_exscan_int(nb, &tot, S);
+        int pos = block_exscan_int(nb, &tot, C);
         const long long slot = slot_base[s] + rank;
         unsigned char* out = varint + slot * vcap;
         for (int j = c0; j < c1; ++j) {
@@ -334,7 +534,7 @@ k_project(const double* __restrict__ f0, const double* __restrict__ stats,
                 zz = (unsigned long long)__double_as_longlong(r);
                 F[j] = __dadd_rn(F[j], r);
             } else {
-                const double q = rint(__ddiv_rn(r, eb2));
+                const double q = qround(r, eb2, inv);
                 const long long qi = (long long)q;
                 zz = ((unsigned long long)qi << 1) ^ (unsigned long long)(qi >> 63);
                 F[j] = __dadd_rn(F[j], __dmul_rn(q, eb2));
@@ -349,30 +549,22 @@ k_project(const double* __restrict__ f0, const double* __restrict__ stats,
         __syncthreads();
     }
 
-    // ---- stored QoIs (pipeline.py:254-260) and the per-image system
-    const double4 q4 = reinterpret_cast<const double4*>(qoi)[img];
-    double qs[4] = {q4.x, q4.y, q4.z, q4.w};
-    if (opt.lam_f32) {
-#pragma unroll
-        for (int k = 0; k < 4; ++k) qs[k] = (double)__double2float_rn(qs[k]);
-    }
+    // ---- stored QoIs (pipeline.py:254-260) and the per-image system:
+    //      top = max(corrected), s4 = max |a3| (lagrange.py:199-204)
     double top = -INFINITY, amax = 0.0;
     for (int j = tid; j < D; j += PJ_T) {
         top = np_max2(top, F[j]);
-        const double dv = __dsub_rn(g.vpar[j], qs[1]);
-        const double a3 = __dmul_rn(g.hmvol[j], __dmul_rn(dv, dv));
-        A[j] = a3;
-        amax = np_max2(amax, fabs(a3));
+        const double dv = __dsub_rn(__ldg(g.vpar + j), qs[1]);
+        amax = np_max2(amax, fabs(__dmul_rn(__ldg(g.hmvol + j), __dmul_rn(dv, dv))));
     }
-    top = block_allmax(top, S, ph);
-    const double s4 = block_allmax(amax, S, ph);
+    block_allmax2(top, amax, C, ph);
+    const double s4 = amax;
     const double sc4 = s4 > 0 ? s4 : 1.0;
-    const double fl = __dmul_rn(opt.floor, top);
-    for (int j = tid; j < D; j += PJ_T) {
-        A[j] = __ddiv_rn(A[j], sc4);
-        if (top > 0) F[j] = np_max2(F[j], fl);  // f_plus (apply keeps the corrected image otherwise)
+    if (top > 0) {  // f_plus (apply keeps the corrected image otherwise)
+        const double fl = __dmul_rn(opt.floor, top);
+        for (int j = tid; j < D; j += PJ_T) F[j] = np_max2(F[j], fl);
     }
-    __syncthreads();
+    if (SEP && tid < g.cols) C.p3c[tid] /= sc4;
 
     double lam[4] = {0.0, 0.0, 0.0, 0.0};
     int status = MLK_NEWTON_DEGENERATE, iters = 0;
@@ -382,88 +574,102 @@ k_project(const double* __restrict__ f0, const double* __restrict__ stats,
         const double b[4] = {__ddiv_rn(qs[0], g.s0), __ddiv_rn(__dmul_rn(qs[0], qs[1]), g.s1),
                              __ddiv_rn(__dmul_rn(qs[0], qs[2]), g.s2),
                              __ddiv_rn(__dmul_rn(qs[0], qs[3]), s4)};
-        SepCtx sc;
-        sc.vpar = g.vpar;
-        sc.vperp2 = g.vperp2;
-        sc.rows = g.rows;
-        sc.cols = g.cols;
+        double bmax = 0.0;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) sc.vcls[k] = g.vcls[k];
-        sc.s0 = g.s0;
-        sc.s1 = g.s1;
-        sc.s2 = g.s2;
-        sc.s4 = s4;
-        sc.hm = 0.5 * g.mass;
-        sc.u = qs[1];
-        status = newton<SEP>(F, g.ash, A, D, b, opt.step, opt.max_iter, opt.tol, lam, &iters, S,
-                             ph, sc, E);
-        if (status == MLK_NEWTON_MAX_ITER && opt.retry) {
-            double lam2[4];
-            int it2 = 0;
-            int st2 = newton<SEP>(F, g.ash, A, D, b, opt.retry_step, opt.retry_max_iter, opt.tol,
-                                  lam2, &it2, S, ph, sc, E);
-            if (st2 == MLK_NEWTON_CONVERGED) {
+        for (int k = 0; k < 4; ++k) bmax = fmax(bmax, fabs(b[k]));
+        if (bmax > 0.0 && isfinite(bmax)) {
+            NtCtx X;
 #pragma unroll
-                for (int k = 0; k < 4; ++k) lam[k] = lam2[k];
-                status = st2;
-                iters += it2;
+            for (int k = 0; k < 4; ++k) X.w[k] = g.vcls[k];
+            X.is0 = 1.0 / g.s0;
+            X.is4 = 1.0 / s4;
+            X.u = qs[1];
+            X.rows = g.rows;
+            X.cols = g.cols;
+            __syncthreads();  // f_plus and the p3c tables
+            newton_block<SEP>(F, g, X, b, bmax, opt.step, opt.max_iter, opt.tol, C, lam, status,
+                              iters);
+            // warp 0 holds the result: publish its status so the retry
+            // decision is block-uniform
+            if (warp == 0 && lane == 0) C.status = status;
+            __syncthreads();
+            if (opt.retry && C.status == MLK_NEWTON_MAX_ITER) {
+                double lam2[4];
+                int st2 = 0, it2 = 0;
+                newton_block<SEP>(F, g, X, b, bmax, opt.retry_step, opt.retry_max_iter, opt.tol,
+                                  C, lam2, st2, it2);
+                if (warp == 0 && st2 == MLK_NEWTON_CONVERGED) {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) lam[k] = lam2[k];
+                    status = st2;
+                    iters += it2;
+                }
             }
         }
     }
 
-    // ---- exception bookkeeping (pipeline.py:263-277)
-    unsigned char fl8 = flags[img];
-    double lu[4] = {0.0, 0.0, 0.0, 0.0};
-    if (!(fl8 & MLK_F_NONFINITE)) {
-        if (status != MLK_NEWTON_CONVERGED) {
-            fl8 |= MLK_F_EXC_NEWTON;
-        } else if (opt.lam_f32) {
-            bool over = false;
+    // ---- exception bookkeeping (pipeline.py:263-277), warp 0
+    if (warp == 0) {
+        unsigned fl8 = flags[img];
+        double lu[4] = {0.0, 0.0, 0.0, 0.0};
+        if (!(fl8 & MLK_F_NONFINITE)) {
+            if (status != MLK_NEWTON_CONVERGED) {
+                fl8 |= MLK_F_EXC_NEWTON;
+            } else if (opt.lam_f32) {
+                bool over = false;
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                float f = __double2float_rn(lam[k]);
-                if (!isfinite(f)) over = true;
-                lu[k] = (double)f;
+                for (int k = 0; k < 4; ++k) {
+                    float f = __double2float_rn(lam[k]);
+                    if (!isfinite(f)) over = true;
+                    lu[k] = (double)f;
+                }
+                if (over) {
+                    fl8 |= MLK_F_EXC_OVERFLOW;
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) lu[k] = 0.0;
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) lu[k] = lam[k];
             }
-            if (over) {
-                fl8 |= MLK_F_EXC_OVERFLOW;
+        }
+        if (lane == 0) {
 #pragma unroll
-                for (int k = 0; k < 4; ++k) lu[k] = 0.0;
-            }
-        } else {
-#pragma unroll
-            for (int k = 0; k < 4; ++k) lu[k] = lam[k];
+            for (int k = 0; k < 4; ++k) C.lu[k] = lu[k];
+            C.flags = fl8;
+            C.status = status;
+            C.iters = iters;
         }
     }
+    __syncthreads();
 
     // ---- apply_lambda_batch (exact elementwise order) + final NRMSE
+    const double lu0 = C.lu[0], lu1 = C.lu[1], lu2 = C.lu[2], lu3 = C.lu[3];
     const double* ash = g.ash;
     double sv[3] = {0.0, 0.0, 0.0};
     for (int j = tid; j < D; j += PJ_T) {
         double outv = F[j];
         if (top > 0) {
-            double t = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(lu[0], __ldg(ash + j)),
-                                                     __dmul_rn(lu[1], __ldg(ash + D + j))),
-                                           __dmul_rn(lu[2], __ldg(ash + 2 * D + j))),
-                                 __dmul_rn(lu[3], A[j]));
+            const double dv = __dsub_rn(__ldg(g.vpar + j), qs[1]);
+            const double a3 = __ddiv_rn(__dmul_rn(__ldg(g.hmvol + j), __dmul_rn(dv, dv)), sc4);
+            double t = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(lu0, __ldg(ash + j)),
+                                                     __dmul_rn(lu1, __ldg(ash + D + j))),
+                                           __dmul_rn(lu2, __ldg(ash + 2 * D + j))),
+                                 __dmul_rn(lu3, a3));
             t = t < -700.0 ? -700.0 : (t > 700.0 ? 700.0 : t);
-            outv = __dmul_rn(F[j], exp(-t));
+            outv = __dmul_rn(outv, exp(-t));
         }
         F[j] = outv;
         const double d = __dsub_rn(O[j], outv);
-        A[j] = __dmul_rn(d, d);  // each thread only reads/writes its own cells here
+        O[j] = __dmul_rn(d, d);  // each thread only reads/writes its own cells here
         const double fv = outv * __ldg(g.vol + j);
         sv[0] += fv;
         sv[1] += fv * __ldg(g.vpar + j);
         sv[2] += fv * __ldg(g.vperp2 + j);
     }
-    __syncthreads();
-    if (tid < 32) {
-        double sse = warp_pairwise_sum(A, pw, S.leaf);
-        if (lane == 0) S.bval = sse;
-    }
-    block_allsum(sv, S, ph);  // contains __syncthreads: S.bval visible after it
-    const double sse = S.bval;
+    block_allsum(sv, C, ph);  // barrier: every d^2 is in O
+    const double sse = block_pairwise(O, pw, C);
+    unsigned fl8 = C.flags;
     const double4 st = reinterpret_cast<const double4*>(stats)[img];
     const double range = __dsub_rn(st.x, st.y);
     const double rms = sqrt(__ddiv_rn(sse, (double)D));
@@ -471,7 +677,6 @@ k_project(const double* __restrict__ f0, const double* __restrict__ stats,
     if (!(ferr <= opt.tau)) fl8 |= MLK_F_EXC_GATE;
     const bool exc = (fl8 & MLK_F_EXCEPTION) != 0;
 
-    const double hm = 0.5 * g.mass;
     const double n = sv[0];
     const double u = sv[1] / n;
     double tl = 0.0;
@@ -481,13 +686,13 @@ k_project(const double* __restrict__ f0, const double* __restrict__ stats,
             const double dv = __ldg(g.vpar + j) - u;
             t1[0] += F[j] * __ldg(g.vol + j) * dv * dv;
         }
-        block_allsum(t1, S, ph);
+        block_allsum(t1, C, ph);
         tl = t1[0];
     }
     if (tid == 0) {
-        flags[img] = fl8;
-        status_out[img] = status;
-        iters_out[img] = iters;
+        flags[img] = (unsigned char)fl8;
+        status_out[img] = C.status;
+        iters_out[img] = C.iters;
         ferr_out[img] = ferr;
         double4* lo = reinterpret_cast<double4*>(lam_out) + img;
         double4* qo = reinterpret_cast<double4*>(qst_out) + img;
@@ -498,7 +703,7 @@ k_project(const double* __restrict__ f0, const double* __restrict__ stats,
             *fo = q4;
             fsse_out[img] = 0.0;
         } else {
-            *lo = make_double4(lu[0], lu[1], lu[2], lu[3]);
+            *lo = make_double4(lu0, lu1, lu2, lu3);
             *qo = make_double4(qs[0], qs[1], qs[2], qs[3]);
             const double nan = __longlong_as_double(0x7ff8000000000000ll);
             *fo = n > 0 ? make_double4(n, u, hm * sv[2] / n, hm * tl / n)
@@ -514,17 +719,14 @@ __global__ void __launch_bounds__(PJ_T)
 k_newton_batch(const double* __restrict__ f_plus, const double* __restrict__ a,
                const double* __restrict__ b, int d, double step, int max_iter, double tol,
                double* __restrict__ lam, int* __restrict__ status, int* __restrict__ iters) {
-    __shared__ PjShared S;
-    __shared__ SepSmem E;
+    __shared__ PjCtl C;
     int ph = 0;
     const long long i = blockIdx.x;
-    const double* ai = a + i * 4 * (long long)d;
-    double bl[4] = {b[4 * i], b[4 * i + 1], b[4 * i + 2], b[4 * i + 3]};
+    const double bl[4] = {b[4 * i], b[4 * i + 1], b[4 * i + 2], b[4 * i + 3]};
     double l[4];
     int it = 0;
-    SepCtx sc{};
-    int st = newton<false>(f_plus + i * d, ai, ai + 3 * (long long)d, d, bl, step, max_iter, tol,
-                           l, &it, S, ph, sc, E);
+    const int st = newton_generic(f_plus + i * d, a + i * 4 * (long long)d, d, bl, step, max_iter,
+                                  tol, l, &it, C, ph);
     if (threadIdx.x == 0) {
         for (int k = 0; k < 4; ++k) lam[4 * i + k] = l[k];
         status[i] = st;
@@ -547,11 +749,10 @@ extern "C" int mlk_project(const double* f0, const double* stats, const double* 
                            cudaStream_t stream) {
     if (total <= 0) return MLK_OK;
     const int D = grid_h->D;
-    if (D > MLK_MAX_D) return MLK_ERR_DIM;
+    if (D > MLK_MAX_D || L < 1 || L > MLK_MAXL) return MLK_ERR_DIM;
     PwPlan pw = mlk_make_pw_plan(D);
-    const size_t sm = (size_t)3 * D * sizeof(double);
-    const bool sep = grid_h->sep && grid_h->rows <= 64 && grid_h->cols <= 64 &&
-                     2 * (grid_h->rows + grid_h->cols) <= PJ_T;
+    const size_t sm = (size_t)(((D + 3) / 2) * 2 + D) * sizeof(double);
+    const bool sep = grid_h->sep && grid_h->rows <= 64 && grid_h->cols <= 64 && grid_h->cols > 0;
     const MlkNewton opt = *opts_h;
 #define MLK_PJ_LAUNCH(SEP)                                                                     \
     cudaFuncSetAttribute(k_project<SEP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); \

@@ -9,7 +9,7 @@
 
 namespace {
 
-constexpr int S1_WARPS = 4;
+constexpr int S1_WARPS = 6;
 constexpr int S1_IMGS = 4;  // images per warp per block
 
 __host__ __device__ inline int panel_len(int rem) {
@@ -40,7 +40,8 @@ __global__ void __launch_bounds__(32 * S1_WARPS)
 k_stage1(const double* __restrict__ f0, const MlkShard* __restrict__ shards, int n_shards,
          int total, MlkGrid g, const float* __restrict__ W, int L, double* __restrict__ lat,
          double* __restrict__ stats, double* __restrict__ qoi) {
-    extern __shared__ double smem[];
+    extern __shared__ __align__(16) double smem[];
+    __shared__ unsigned long long bars[S1_WARPS];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int D = g.D;
     int first = 0;
@@ -48,27 +49,36 @@ k_stage1(const double* __restrict__ f0, const MlkShard* __restrict__ shards, int
     if (s < 0) return;
     const MlkShard sh = shards[s];
     float* Wsm = reinterpret_cast<float*>(smem);
-    const int wfloats = ((L * D + 1) / 2) * 2;
-    double* buf = smem + wfloats / 2 + warp * (D + 96);
-    double* chain = buf + D;
+    const int wdoubles = ((L * D + 3) / 4) * 2;  // 16-B aligned float region
+    const int per_warp = ((D + 2 + 1) / 2) * 2 + 96;
+    double* tbuf = smem + wdoubles + warp * per_warp;  // TMA target (D + 2 doubles)
+    double* chain = tbuf + ((D + 2 + 1) / 2) * 2;
+    unsigned long long* bar = &bars[warp];
+    if (lane == 0) mbar_init(bar, 1);
     const float* Wg = W + sh.w_off;
     for (int i = threadIdx.x; i < L * D; i += blockDim.x) Wsm[i] = __ldg(Wg + i);
     __syncthreads();
     int np_ = 0;
     for (int j0 = 0; j0 < D; j0 += panel_len(D - j0)) ++np_;
 
+    unsigned phase = 0;
     for (int k_img = 0; k_img < S1_IMGS; ++k_img) {
         const int j_img = first + k_img * S1_WARPS + warp;
         if (j_img >= sh.n_img) break;
         const int img = sh.img_off + j_img;
         const double* x = shard_image(f0, sh, j_img, D);
+        __syncwarp();
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        const int shift = stage_histogram(tbuf, x, D, bar);
+        mbar_wait(bar, phase);
+        phase ^= 1u;
+        double* buf = tbuf + shift;
 
-        // ---- pass A: stage, extrema, sums, first moments
+        // ---- pass A: extrema, sums, first moments from the staged copy
         double mx = -INFINITY, mn = INFINITY, so = 0.0, soo = 0.0, n0 = 0.0, n1 = 0.0, n2 = 0.0;
 #pragma unroll 4
         for (int j = lane; j < D; j += 32) {
-            double v = x[j];
-            buf[j] = v;
+            double v = buf[j];
             mx = np_max2(mx, v);
             mn = np_min2(mn, v);
             so += v;
@@ -156,8 +166,8 @@ extern "C" int mlk_stage1(const double* f0, const MlkShard* shards, int32_t n_sh
     // 96 chain slots: L*8 (small path) or L*ceil(D/384)+1 (blocked path)
     if (L * ((grid_h->D + 383) / 384 + 1) > 96) return MLK_ERR_DIM;
     const int D = grid_h->D;
-    size_t sm = (size_t)(((L * D + 1) / 2) * 2) * sizeof(float) +
-                (size_t)S1_WARPS * (D + 96) * sizeof(double);
+    size_t sm = (size_t)(((L * D + 3) / 4) * 2) * sizeof(double) +
+                (size_t)S1_WARPS * (((D + 3) / 2) * 2 + 96) * sizeof(double);
     if (sm > 227 * 1024) return MLK_ERR_DIM;
     cudaFuncSetAttribute(k_stage1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     // sum_s ceil(n_s / per_block) <= total / per_block + n_shards; spare blocks exit

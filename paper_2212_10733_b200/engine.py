@@ -59,6 +59,11 @@ def decode_tree_cols(d: int, l: int) -> bytes:
 # ---------------------------------------------------------------------------
 # grid tables
 
+# Separable grids take the exponent-table Newton (project.cu); tests switch it
+# off to exercise the per-cell path on the same fixtures.
+SEPARABLE_NEWTON = True
+
+
 class DeviceGrid:
     """Exact grid tables on device (lagrange.py:68-80, 163-173, 199-204)."""
 
@@ -88,6 +93,11 @@ class DeviceGrid:
         cls = 2 * re_[:, None] + ce_[None, :]
         vcls = [grid.vol[cls == k][0] if np.any(cls == k) else 0.0 for k in range(4)]
         sep = int(all(np.all(grid.vol[cls == k] == vcls[k]) for k in range(4) if np.any(cls == k)))
+        # the factorised Newton sums also need vol ~= dlt * w_r * w_c
+        if sep and vcls[0] > 0:
+            wc_, wr_ = vcls[1] / vcls[0], vcls[2] / vcls[0]
+            sep = int(abs(vcls[3] - vcls[0] * wr_ * wc_) <= 1e-12 * abs(vcls[3]))
+        sep = int(sep and SEPARABLE_NEWTON)
         self.struct = MlkGrid(rows=r, cols=c, D=self.D, pad=0, mass=grid.mass,
                               vol=self.t["vol"].data_ptr(), vpar=self.t["vpar"].data_ptr(),
                               vperp2=self.t["vperp2"].data_ptr(),
@@ -454,21 +464,30 @@ def compress_device(f0: torch.Tensor, specs, dgrid: DeviceGrid, cfg, timer: Time
     while any(st is not None and st.stage != "done" for st in states):
         rounds += 1
         trees, cand = [], np.zeros((S, n_cand))
-        act = np.zeros(S + 1, dtype=np.int32)
+        cnt_act = np.zeros(S, dtype=np.int32)
         for s, st in enumerate(states):
             tree = _search_tree(st, LOOKAHEAD) if (st is not None and st.stage != "done") \
                 else ([], st)
             trees.append(tree)
             for c, nd in enumerate(tree[0]):
                 cand[s, c] = float(nd[0].query())
-            act[s + 1] = act[s] + (int(cnt_h[s]) if tree[0] else 0)
-        ws.begin()
+            cnt_act[s] = int(cnt_h[s]) if tree[0] else 0
+        # two launches: the smallest-range images first (they fail the large
+        # bounds), then the rest against whatever bounds are still open
+        head = np.minimum(cnt_act, np.maximum(64, cnt_act // 16)).astype(np.int32)
+        off_a = np.concatenate([[0], np.cumsum(head)]).astype(np.int32)
+        off_b = np.concatenate([[0], np.cumsum(cnt_act - head)]).astype(np.int32)
         cand_d = ws.stage(cand)
-        act_d = ws.stage(act)
+        off_a_d = ws.stage(off_a)
+        off_b_d = ws.stage(off_b)
+        start_a = ws.stage(np.zeros(S, dtype=np.int32))
+        start_b = ws.stage(head)
         ws.flush()
         fail.zero_()
-        call("mlk_probe", f0, stats, sh_d, S, dgrid.addr, W, L, cents, K, codes, sel_rng, act_d,
-             int(act[-1]), rbound, cfg.tau, cand_d, n_cand, fail)
+        call("mlk_probe", f0, stats, sh_d, S, dgrid.addr, W, L, cents, K, codes, sel_rng, off_a_d,
+             start_a, int(off_a[-1]), rbound, cfg.tau, cand_d, n_cand, fail)
+        call("mlk_probe", f0, stats, sh_d, S, dgrid.addr, W, L, cents, K, codes, sel_rng, off_b_d,
+             start_b, int(off_b[-1]), rbound, cfg.tau, cand_d, n_cand, fail)
         (fail_h,) = _d2h(fail)
         for s, (nodes, ref) in enumerate(trees):
             if not nodes:
