@@ -4,30 +4,29 @@
 
 #include "common.cuh"
 
+static void pw_plan_rec(PwPlan& p, int b, int l) {
+    if (l <= 128) {
+        if (p.n_leaves < MLK_PW_MAX_LEAVES) {
+            p.start[p.n_leaves] = (short)b;
+            p.len[p.n_leaves] = (short)l;
+        }
+        ++p.n_leaves;
+        if (p.n_ops < 2 * MLK_PW_MAX_LEAVES) p.ops[p.n_ops >> 5] |= 1u << (p.n_ops & 31);
+        ++p.n_ops;
+        return;
+    }
+    const int l2 = pw_split(l);
+    pw_plan_rec(p, b, l2);
+    pw_plan_rec(p, b + l2, l - l2);
+    ++p.n_ops;  // add (bit 0)
+}
+
+// numpy's pairwise recursion as leaves (pre-order) plus the postfix program
+// that combines them.
 PwPlan mlk_make_pw_plan(int n) {
     PwPlan p{};
     p.n = n;
-    p.n_leaves = 0;
-    // iterative pre-order walk of numpy's pairwise recursion
-    int st_b[40], st_l[40], sp = 0;
-    st_b[sp] = 0;
-    st_l[sp] = n;
-    ++sp;
-    while (sp) {
-        --sp;
-        int b = st_b[sp], l = st_l[sp];
-        if (l <= 128) {
-            if (p.n_leaves < MLK_PW_MAX_LEAVES) {
-                p.start[p.n_leaves] = (short)b;
-                p.len[p.n_leaves] = (short)l;
-            }
-            ++p.n_leaves;
-            continue;
-        }
-        int l2 = pw_split(l);
-        st_b[sp] = b + l2; st_l[sp] = l - l2; ++sp;
-        st_b[sp] = b; st_l[sp] = l2; ++sp;
-    }
+    pw_plan_rec(p, 0, n);
     return p;
 }
 

@@ -30,6 +30,8 @@
 struct PwPlan {
     int n;
     int n_leaves;
+    int n_ops;                                  // postfix program of the combine:
+    unsigned ops[(2 * MLK_PW_MAX_LEAVES + 31) / 32];  // bit 1 = push next leaf, 0 = add
     short start[MLK_PW_MAX_LEAVES];
     short len[MLK_PW_MAX_LEAVES];
 };
@@ -77,6 +79,22 @@ __device__ inline double pw_combine(const double* leaf, int n, int& next) {
     return __dadd_rn(a, b);
 }
 
+// The same combine without recursion: run the plan's postfix program with
+// `leaf` itself as the stack (the stack never overtakes the next unread
+// leaf).  Returns the total; `leaf` is clobbered.
+__device__ inline double pw_combine_ops(double* leaf, const PwPlan& p) {
+    int sp = 0, next = 0;
+    for (int i = 0; i < p.n_ops; ++i) {
+        if ((p.ops[i >> 5] >> (i & 31)) & 1u) {
+            leaf[sp++] = leaf[next++];
+        } else {
+            --sp;
+            leaf[sp - 1] = __dadd_rn(leaf[sp - 1], leaf[sp]);
+        }
+    }
+    return leaf[0];
+}
+
 // Warp-cooperative exact pairwise sum of v[0..plan.n) held in shared memory.
 // All lanes return the same value.  `scratch` holds MLK_PW_MAX_LEAVES doubles.
 __device__ inline double warp_pairwise_sum(const double* v, const PwPlan& plan,
@@ -86,10 +104,7 @@ __device__ inline double warp_pairwise_sum(const double* v, const PwPlan& plan,
         scratch[l] = pw_leaf([&](int i) { return v[i]; }, plan.start[l], plan.len[l]);
     __syncwarp();
     double tot = 0.0;
-    if (lane == 0) {
-        int next = 0;
-        tot = pw_combine(scratch, plan.n, next);
-    }
+    if (lane == 0) tot = pw_combine_ops(scratch, plan);
     tot = __shfl_sync(0xffffffffu, tot, 0);
     __syncwarp();
     return tot;
@@ -151,18 +166,20 @@ __device__ __forceinline__ int find_shard(const MlkShard* sh, int n_shards, int 
 // * std + mean (two roundings, numpy `recon * std + mean`).
 __device__ __forceinline__ double decode_cell(const double* z, const float* W, int L, int D,
                                               int j, bool tree, double mean, double sd) {
+    const float* wp = W + j;
     double s;
-    if (L == 4 && tree) {
-        double p0 = __dmul_rn(z[0], (double)__ldg(W + j));
-        double p1 = __dmul_rn(z[1], (double)__ldg(W + D + j));
-        double p2 = __dmul_rn(z[2], (double)__ldg(W + 2 * D + j));
-        double p3 = __dmul_rn(z[3], (double)__ldg(W + 3 * D + j));
-        s = __dadd_rn(__dadd_rn(p0, p1), __dadd_rn(p2, p3));
+    if (L == 4) {
+        const double p0 = __dmul_rn(z[0], (double)__ldg(wp));
+        const double p1 = __dmul_rn(z[1], (double)__ldg(wp + D));
+        const double p2 = __dmul_rn(z[2], (double)__ldg(wp + 2 * D));
+        const double p3 = __dmul_rn(z[3], (double)__ldg(wp + 3 * D));
+        const double p01 = __dadd_rn(p0, p1);
+        s = tree ? __dadd_rn(p01, __dadd_rn(p2, p3)) : __dadd_rn(__dadd_rn(p01, p2), p3);
     } else {
-        s = __dmul_rn(z[0], (double)__ldg(W + j));
+        s = __dmul_rn(z[0], (double)__ldg(wp));
 #pragma unroll
         for (int k = 1; k < MLK_MAXL; ++k)  // unrolled + guarded: z stays in registers
-            if (k < L) s = __dadd_rn(s, __dmul_rn(z[k], (double)__ldg(W + (long long)k * D + j)));
+            if (k < L) s = __dadd_rn(s, __dmul_rn(z[k], (double)__ldg(wp + k * D)));
     }
     return __dadd_rn(__dmul_rn(s, sd), mean);
 }

@@ -321,6 +321,7 @@ __device__ void newton_block(const double* fp, const MlkGrid& g, const NtCtx& X,
                              double (&lam)[4], int& status, int& iters) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int D = g.D, rows = X.rows, cols = X.cols;
+    (void)rows;
     bool clamped = false;
 #pragma unroll
     for (int k = 0; k < 4; ++k) lam[k] = 0.0;
@@ -336,23 +337,39 @@ __device__ void newton_block(const double* fp, const MlkGrid& g, const NtCtx& X,
         }
     }
     __syncthreads();
-    // (r, c) of this thread's first cell and the stride PJ_T in (rows, cols)
-    const int dr = PJ_T / cols, dc = PJ_T - dr * cols;
     for (int it = 0;; ++it) {
         if (!C.go) break;
         double v[16];
 #pragma unroll
         for (int k = 0; k < 16; ++k) v[k] = 0.0;
         if (SEP && !C.direct) {
-            int r = tid / cols, c = tid - (tid / cols) * cols;
-            for (int j = tid; j < D; j += PJ_T) {
-                const bool re = (r == 0) | (r == rows - 1), ce = (c == 0) | (c == cols - 1);
-                const double w = cls_val(X.w, re, ce);
-                const double f = fp[j] * C.ea[re][c] * C.eb[ce][r];
-                cell_sums(v, w * X.is0, w * C.vp1[c], w * C.p2r[r], w * C.p3c[c], f);
-                c += dc;
-                r += dr;
-                if (c >= cols) { c -= cols; ++r; }
+            // thread = (row group, column): exp(-t) = ea[re][c] eb[ce][r] and
+            // a_k = w * p_k with w the class volume, so with the column fixed
+            // the 14 sums factor into 5 row accumulations per thread
+            const int ngrp = PJ_T / cols, c = tid % cols, g0 = tid / cols;
+            if (g0 < ngrp) {
+                const bool ce = (c == 0) | (c == cols - 1);
+                const double ea0 = C.ea[0][c], ea1 = C.ea[1][c];
+                const double w_in = cls_val(X.w, false, ce), w_ed = cls_val(X.w, true, ce);
+                const double* ebp = C.eb[ce];
+                double G1 = 0.0, G2 = 0.0, H1 = 0.0, H2 = 0.0, H3 = 0.0;
+                for (int r = g0; r < rows; r += ngrp) {
+                    const bool re = (r == 0) | (r == rows - 1);
+                    const double w = re ? w_ed : w_in;
+                    const double wf = w * (fp[r * cols + c] * (re ? ea1 : ea0) * ebp[r]);
+                    const double p2 = C.p2r[r];
+                    const double w2f = w * wf, t2 = p2 * w2f;
+                    G1 += wf;
+                    G2 = fma(p2, wf, G2);
+                    H1 += w2f;
+                    H2 += t2;
+                    H3 = fma(p2, t2, H3);
+                }
+                const double q0 = X.is0, q1 = C.vp1[c], q3 = C.p3c[c];
+                v[0] = q0 * G1; v[1] = q1 * G1; v[2] = G2; v[3] = q3 * G1;
+                v[4] = q0 * q0 * H1; v[5] = q0 * q1 * H1; v[6] = q0 * H2; v[7] = q0 * q3 * H1;
+                v[8] = q1 * q1 * H1; v[9] = q1 * H2; v[10] = q1 * q3 * H1;
+                v[11] = H3; v[12] = q3 * H2; v[13] = q3 * q3 * H1;
             }
         } else {
             const double l0 = C.lam[0], l1 = C.lam[1], l2 = C.lam[2], l3 = C.lam[3];
@@ -424,10 +441,7 @@ __device__ double block_pairwise(const double* v, const PwPlan& pw, PjCtl& C) {
         }
     }
     __syncthreads();
-    if (tid == 0) {
-        int next = 0;
-        C.bval = pw_combine(C.leaf, pw.n, next);
-    }
+    if (tid == 0) C.bval = pw_combine_ops(C.leaf, pw);
     __syncthreads();
     return C.bval;
 }
@@ -552,17 +566,24 @@ k_project(const double* __restrict__ f0, const double* __restrict__ stats,
     // ---- stored QoIs (pipeline.py:254-260) and the per-image system:
     //      top = max(corrected), s4 = max |a3| (lagrange.py:199-204)
     double top = -INFINITY, amax = 0.0;
+    bool nan_t = false, nan_a = false;  // numpy max propagates NaN
     for (int j = tid; j < D; j += PJ_T) {
-        top = np_max2(top, F[j]);
+        const double fj = F[j];
+        nan_t |= fj != fj;
+        top = fmax(top, fj);
         const double dv = __dsub_rn(__ldg(g.vpar + j), qs[1]);
-        amax = np_max2(amax, fabs(__dmul_rn(__ldg(g.hmvol + j), __dmul_rn(dv, dv))));
+        const double a3 = fabs(__dmul_rn(__ldg(g.hmvol + j), __dmul_rn(dv, dv)));
+        nan_a |= a3 != a3;
+        amax = fmax(amax, a3);
     }
+    if (nan_t) top = __longlong_as_double(0x7ff8000000000000ll);
+    if (nan_a) amax = __longlong_as_double(0x7ff8000000000000ll);
     block_allmax2(top, amax, C, ph);
     const double s4 = amax;
     const double sc4 = s4 > 0 ? s4 : 1.0;
-    if (top > 0) {  // f_plus (apply keeps the corrected image otherwise)
+    if (top > 0) {  // f_plus (apply keeps the corrected image otherwise); no NaN here
         const double fl = __dmul_rn(opt.floor, top);
-        for (int j = tid; j < D; j += PJ_T) F[j] = np_max2(F[j], fl);
+        for (int j = tid; j < D; j += PJ_T) F[j] = fmax(F[j], fl);
     }
     if (SEP && tid < g.cols) C.p3c[tid] /= sc4;
 
@@ -647,25 +668,66 @@ k_project(const double* __restrict__ f0, const double* __restrict__ stats,
     const double lu0 = C.lu[0], lu1 = C.lu[1], lu2 = C.lu[2], lu3 = C.lu[3];
     const double* ash = g.ash;
     double sv[3] = {0.0, 0.0, 0.0};
-    for (int j = tid; j < D; j += PJ_T) {
-        double outv = F[j];
-        if (top > 0) {
-            const double dv = __dsub_rn(__ldg(g.vpar + j), qs[1]);
-            const double a3 = __ddiv_rn(__dmul_rn(__ldg(g.hmvol + j), __dmul_rn(dv, dv)), sc4);
-            double t = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(lu0, __ldg(ash + j)),
-                                                     __dmul_rn(lu1, __ldg(ash + D + j))),
-                                           __dmul_rn(lu2, __ldg(ash + 2 * D + j))),
-                                 __dmul_rn(lu3, a3));
-            t = t < -700.0 ? -700.0 : (t > 700.0 ? 700.0 : t);
-            outv = __dmul_rn(outv, exp(-t));
+    if (SEP) {
+        // column-fixed threads: ash0, ash1, a3 and vol depend on (row edge,
+        // column) only, so the first two and the last product of t are two
+        // per-thread constants; the order of the additions is unchanged
+        const int cols = g.cols, rows = g.rows, ngrp = PJ_T / cols;
+        const int c = tid % cols, g0 = tid / cols;
+        if (g0 < ngrp) {
+            double P[2], Q[2], V[2];
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int jj = (e == 0 && rows > 2 ? cols : 0) + c;  // row 1: interior; row 0: edge
+                const double dv = __dsub_rn(__ldg(g.vpar + jj), qs[1]);
+                const double a3 = __ddiv_rn(__dmul_rn(__ldg(g.hmvol + jj), __dmul_rn(dv, dv)), sc4);
+                P[e] = __dadd_rn(__dmul_rn(lu0, __ldg(ash + jj)), __dmul_rn(lu1, __ldg(ash + D + jj)));
+                Q[e] = __dmul_rn(lu3, a3);
+                V[e] = __ldg(g.vol + jj);
+            }
+            const double vpc = __ldg(g.vpar + c);
+            for (int r = g0; r < rows; r += ngrp) {
+                const bool re = (r == 0) | (r == rows - 1);
+                const int j = r * cols + c;
+                double outv = F[j];
+                if (top > 0) {
+                    double t = __dadd_rn(__dadd_rn(re ? P[1] : P[0],
+                                                   __dmul_rn(lu2, __ldg(ash + 2 * D + j))),
+                                         re ? Q[1] : Q[0]);
+                    t = t < -700.0 ? -700.0 : (t > 700.0 ? 700.0 : t);
+                    outv = __dmul_rn(outv, exp(-t));
+                }
+                F[j] = outv;
+                const double d = __dsub_rn(O[j], outv);
+                O[j] = __dmul_rn(d, d);
+                const double fv = outv * (re ? V[1] : V[0]);
+                sv[0] += fv;
+                sv[1] += fv * vpc;
+                sv[2] += fv * __ldg(g.vperp2 + j);
+            }
         }
-        F[j] = outv;
-        const double d = __dsub_rn(O[j], outv);
-        O[j] = __dmul_rn(d, d);  // each thread only reads/writes its own cells here
-        const double fv = outv * __ldg(g.vol + j);
-        sv[0] += fv;
-        sv[1] += fv * __ldg(g.vpar + j);
-        sv[2] += fv * __ldg(g.vperp2 + j);
+    } else {
+        for (int j = tid; j < D; j += PJ_T) {
+            double outv = F[j];
+            if (top > 0) {
+                const double dv = __dsub_rn(__ldg(g.vpar + j), qs[1]);
+                const double a3 =
+                    __ddiv_rn(__dmul_rn(__ldg(g.hmvol + j), __dmul_rn(dv, dv)), sc4);
+                double t = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(lu0, __ldg(ash + j)),
+                                                         __dmul_rn(lu1, __ldg(ash + D + j))),
+                                               __dmul_rn(lu2, __ldg(ash + 2 * D + j))),
+                                     __dmul_rn(lu3, a3));
+                t = t < -700.0 ? -700.0 : (t > 700.0 ? 700.0 : t);
+                outv = __dmul_rn(outv, exp(-t));
+            }
+            F[j] = outv;
+            const double d = __dsub_rn(O[j], outv);
+            O[j] = __dmul_rn(d, d);  // each thread only reads/writes its own cells here
+            const double fv = outv * __ldg(g.vol + j);
+            sv[0] += fv;
+            sv[1] += fv * __ldg(g.vpar + j);
+            sv[2] += fv * __ldg(g.vperp2 + j);
+        }
     }
     block_allsum(sv, C, ph);  // barrier: every d^2 is in O
     const double sse = block_pairwise(O, pw, C);
