@@ -30,7 +30,6 @@ constexpr unsigned FULL = 0xffffffffu;
 struct PjCtl {
     double part[PJ_W][16];  // per-warp Newton sums (index 14: clamp flag)
     double red[2][PJ_W][16];
-    double lam[4];          // current iterate (read by the direct path)
     double lu[4];           // lambdas applied to the image
     double ea[2][64];       // exp(-vol * A_c) by row-edge class
     double eb[2][64];       // exp(-vol * B_r) by column-edge class
@@ -40,7 +39,8 @@ struct PjCtl {
     double leaf[MLK_PW_MAX_LEAVES];
     double bval;
     int iscan[PJ_W];
-    int go, direct, status, iters;
+    int big[PJ_W];          // per-warp "table exponent too large" flags
+    int status, iters;
     unsigned flags;
 };
 
@@ -142,8 +142,9 @@ __device__ __forceinline__ void swap_rows(double (&t)[4][5], int c, int p) {
     }
 }
 
+// (tolerance-level like the rest of the iterate: one reciprocal per pivot)
 __device__ __forceinline__ int solve4(const double* m, const double* r, double* x) {
-    double t[4][5];
+    double t[4][5], inv[4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
 #pragma unroll
@@ -159,9 +160,10 @@ __device__ __forceinline__ int solve4(const double* m, const double* r, double* 
             if (fabs(t[i][c]) > big) { big = fabs(t[i][c]); p = i; }
         if (big < 1e-300 || !isfinite(big)) return 1;
         swap_rows(t, c, p);
+        inv[c] = 1.0 / t[c][c];
 #pragma unroll
         for (int i = c + 1; i < 4; ++i) {
-            const double f = t[i][c] / t[c][c];
+            const double f = t[i][c] * inv[c];
 #pragma unroll
             for (int j = c; j < 5; ++j) t[i][j] -= f * t[c][j];
         }
@@ -171,7 +173,7 @@ __device__ __forceinline__ int solve4(const double* m, const double* r, double* 
         double acc = t[c][4];
 #pragma unroll
         for (int j = c + 1; j < 4; ++j) acc -= t[c][j] * x[j];
-        x[c] = acc / t[c][c];
+        x[c] = acc * inv[c];
         if (!isfinite(x[c])) return 1;
     }
     return 0;
@@ -287,14 +289,13 @@ struct NtCtx {
     int rows, cols;
 };
 
-// warp 0: exponent tables for lam; returns true (warp-uniform) when some
-// |t| could exceed the reference's +-700 clamp (the caller then evaluates
-// that iteration cell by cell).
+// Exponent tables for lam, entries spread over the block; returns true
+// (warp-uniform) when this warp saw some |t| that could exceed the
+// reference's +-700 clamp (that iteration is then evaluated cell by cell).
 __device__ __forceinline__ bool sep_tables(const double (&lam)[4], const NtCtx& X, PjCtl& C) {
-    const int lane = threadIdx.x & 31;
     const int rows = X.rows, cols = X.cols;
     bool big = false;
-    for (int q = lane; q < 2 * (rows + cols); q += 32) {
+    for (int q = threadIdx.x; q < 2 * (rows + cols); q += PJ_T) {
         double x;
         if (q < 2 * cols) {
             const int re = q >= cols, c = q - re * cols;
@@ -313,8 +314,10 @@ __device__ __forceinline__ bool sep_tables(const double (&lam)[4], const NtCtx& 
     return __any_sync(FULL, big);
 }
 
-// The block's Newton iteration for one image.  All threads call it; the
-// result (status, iters, lam) is valid in warp 0.
+// The block's Newton iteration for one image.  All threads call it.  Every
+// warp combines the per-warp partial sums and takes the (identical) Newton
+// step itself, so lambda never needs a broadcast; the next iteration's
+// exponent tables are computed by the whole block.  Two barriers per step.
 template <bool SEP>
 __device__ void newton_block(const double* fp, const MlkGrid& g, const NtCtx& X, const double* b,
                              double bmax, double step, int max_iter, double tol, PjCtl& C,
@@ -327,22 +330,21 @@ __device__ void newton_block(const double* fp, const MlkGrid& g, const NtCtx& X,
     for (int k = 0; k < 4; ++k) lam[k] = 0.0;
     status = MLK_NEWTON_MAX_ITER;
     iters = max_iter;
-    if (warp == 0) {
-        const bool big = SEP ? sep_tables(lam, X, C) : true;
-        if (lane == 0) {
-            C.direct = big;
-            C.go = 1;
-#pragma unroll
-            for (int k = 0; k < 4; ++k) C.lam[k] = 0.0;
-        }
+    if (SEP) {
+        const bool big = sep_tables(lam, X, C);
+        if (lane == 0) C.big[warp] = big;
     }
     __syncthreads();
     for (int it = 0;; ++it) {
-        if (!C.go) break;
+        bool direct = !SEP;
+        if (SEP) {
+#pragma unroll
+            for (int q = 0; q < PJ_W; ++q) direct |= C.big[q] != 0;
+        }
         double v[16];
 #pragma unroll
         for (int k = 0; k < 16; ++k) v[k] = 0.0;
-        if (SEP && !C.direct) {
+        if (SEP && !direct) {
             // thread = (row group, column): exp(-t) = ea[re][c] eb[ce][r] and
             // a_k = w * p_k with w the class volume, so with the column fixed
             // the 14 sums factor into 5 row accumulations per thread
@@ -372,7 +374,7 @@ __device__ void newton_block(const double* fp, const MlkGrid& g, const NtCtx& X,
                 v[11] = H3; v[12] = q3 * H2; v[13] = q3 * q3 * H1;
             }
         } else {
-            const double l0 = C.lam[0], l1 = C.lam[1], l2 = C.lam[2], l3 = C.lam[3];
+            const double l0 = lam[0], l1 = lam[1], l2 = lam[2], l3 = lam[3];
             for (int j = tid; j < D; j += PJ_T) {
                 const double a0 = __ldg(g.ash + j), a1 = __ldg(g.ash + D + j),
                              a2 = __ldg(g.ash + 2 * D + j);
@@ -386,25 +388,20 @@ __device__ void newton_block(const double* fp, const MlkGrid& g, const NtCtx& X,
         const double part = warp_rs16(v);
         if (!(lane & 1)) C.part[warp][lane >> 1] = part;
         __syncthreads();
-        if (warp == 0) {
-            double tot = 0.0;
-            if (lane < 16) {
-                tot = C.part[0][lane];
+        double tot = 0.0;
+        if (lane < 16) {
+            tot = C.part[0][lane];
 #pragma unroll
-                for (int q = 1; q < PJ_W; ++q) tot += C.part[q][lane];
-            }
-            double s[15];
+            for (int q = 1; q < PJ_W; ++q) tot += C.part[q][lane];
+        }
+        double sums[15];
 #pragma unroll
-            for (int k = 0; k < 15; ++k) s[k] = __shfl_sync(FULL, tot, k);
-            int go = newton_step(s, b, bmax, step, max_iter, tol, it, lam, clamped, status, iters);
-            bool big = true;
-            if (go && SEP) big = sep_tables(lam, X, C);
-            if (lane == 0) {
-                C.go = go;
-                C.direct = big;
-#pragma unroll
-                for (int k = 0; k < 4; ++k) C.lam[k] = lam[k];
-            }
+        for (int k = 0; k < 15; ++k) sums[k] = __shfl_sync(FULL, tot, k);
+        if (!newton_step(sums, b, bmax, step, max_iter, tol, it, lam, clamped, status, iters))
+            break;  // block-uniform: every warp saw the same sums
+        if (SEP) {
+            const bool big = sep_tables(lam, X, C);
+            if (lane == 0) C.big[warp] = big;
         }
         __syncthreads();
     }
