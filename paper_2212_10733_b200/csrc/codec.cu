@@ -67,35 +67,6 @@ __host__ __device__ inline int pow2ge(int x) {
 }
 __host__ __device__ inline int al16(int x) { return (x + 15) & ~15; }
 
-// Per-warp shared memory: the window, then one region reused by phase:
-//   chain build  : p1 | hash table (u16 entries, aliasing where p4 will go)
-//   matching     : p1 | p4
-//   flush        : Huffman trees | u32 symbol histogram / output bit buffer
-// The symbol buffer lives in global scratch.
-__host__ __device__ inline Lay layout(int nmax) {
-    Lay L;
-    L.nmax = nmax;
-    L.direct = nmax > 4096;
-    L.T = L.direct ? 32768 : pow2ge(nmax + 2);
-    int o = 0;
-    L.win = o;
-    o += al16(nmax + z6::MAX_MATCH + 24);
-    const int b0 = o;
-    L.p1 = b0;
-    L.p4 = b0 + al16(2 * nmax);
-    L.hash = L.p4;
-    const int chains = al16(2 * nmax) + (al16(2 * nmax) > al16(2 * L.T) ? al16(2 * nmax)
-                                                                          : al16(2 * L.T));
-    L.trees = b0;
-    L.hist = b0 + al16((int)sizeof(z6::Trees));
-    L.obuf = L.hist;
-    const int tail = al16(nmax + 256) > 4 * 320 ? al16(nmax + 256) : 4 * 320;
-    const int flush = al16((int)sizeof(z6::Trees)) + tail;
-    o += chains > flush ? chains : flush;
-    L.total = o;
-    return L;
-}
-
 __device__ __forceinline__ unsigned hkey(const uint8_t* w) {
     return (((unsigned)w[0] << 10) ^ ((unsigned)w[1] << 5) ^ w[2]) & 0x7fffu;
 }
@@ -174,6 +145,274 @@ struct GBit {  // lane-0 bit writer into global memory
     }
 };
 
+// ---- Huffman construction (trees.c build_tree / gen_bitlen / gen_codes),
+// warp-cooperative where the result does not depend on order.  The heap is
+// the serial part; its entries carry the comparison key with the node id
+// (freq << 16 | depth << 10 | node), so zlib's smaller() -- freq, then
+// depth, ties count as smaller -- is one integer compare and a sift step
+// reads one word instead of chasing node -> freq/depth.
+template <int NL>
+struct DTree {
+    uint16_t freq[NL];
+    uint16_t code[NL];
+    uint16_t len[2 * NL + 2];
+    uint16_t dad[2 * NL + 1];
+    int max_code;
+};
+
+struct DTrees {
+    DTree<z6::L_CODES> lt;
+    DTree<z6::D_CODES> dt;
+    DTree<z6::BL_CODES> bt;
+    uint32_t hk[z6::HEAP_SIZE];  // heap 1..heap_len | node order heap_max..HEAP_SIZE-1
+    unsigned bl_count[z6::MAX_BITS + 1];
+    unsigned next_code[z6::MAX_BITS + 1];
+    unsigned long long opt_len, static_len;
+    int heap_max, overflow;
+};
+
+__device__ __forceinline__ void hdown(uint32_t* hk, int heap_len, int k) {
+    const uint32_t v = hk[k];
+    int j = k << 1;
+    while (j <= heap_len) {
+        uint32_t hj = hk[j];
+        if (j < heap_len) {
+            const uint32_t hj1 = hk[j + 1];
+            if ((hj1 >> 10) <= (hj >> 10)) { ++j; hj = hj1; }
+        }
+        if ((v >> 10) <= (hj >> 10)) break;
+        hk[k] = hj;
+        k = j;
+        j <<= 1;
+    }
+    hk[k] = v;
+}
+
+// kind: 0 literal/length, 1 distance, 2 bit-length tree.  Whole warp.
+template <int NL>
+__device__ void build_tree_warp(DTrees& W, DTree<NL>& t, int kind, const z6::Tables& tb) {
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const unsigned lt_mask = (1u << lane) - 1u;
+    uint32_t* hk = W.hk;
+    // leaves with nonzero frequency enter the heap in symbol order
+    int cnt = 0, max_code = -1;
+    for (int n0 = 0; n0 < NL; n0 += 32) {
+        const int n = n0 + lane;
+        const unsigned f = n < NL ? t.freq[n] : 0u;
+        const unsigned b = __ballot_sync(FULL, f != 0u);
+        if (n < NL) {
+            if (f) hk[cnt + __popc(b & lt_mask) + 1] = (f << 16) | (unsigned)n;
+            else t.len[n] = 0;
+        }
+        if (b) max_code = n0 + 31 - __clz(b);
+        cnt += __popc(b);
+    }
+    for (int b = lane; b <= z6::MAX_BITS; b += 32) W.bl_count[b] = 0u;
+    __syncwarp();
+    const int max_length = kind == 2 ? z6::MAX_BL_BITS : z6::MAX_BITS;
+    if (lane == 0) {
+        int heap_len = cnt;
+        while (heap_len < 2) {  // at least two codes (pkzip compatibility)
+            const int node = max_code < 2 ? ++max_code : 0;
+            hk[++heap_len] = (1u << 16) | (unsigned)node;
+            t.freq[node] = 1;
+            W.opt_len--;
+            if (kind == 0) W.static_len -= tb.sl_len[node];
+            else if (kind == 1) W.static_len -= tb.sd_len[node];
+        }
+        t.max_code = max_code;
+        for (int k = heap_len / 2; k >= 1; --k) hdown(hk, heap_len, k);
+        int node = NL, heap_max = z6::HEAP_SIZE;
+        do {
+            const uint32_t n = hk[1];
+            hk[1] = hk[heap_len--];
+            hdown(hk, heap_len, 1);
+            const uint32_t m = hk[1];
+            hk[--heap_max] = n & 1023u;
+            hk[--heap_max] = m & 1023u;
+            const uint32_t dn = (n >> 10) & 63u, dm = (m >> 10) & 63u;
+            t.dad[n & 1023u] = (uint16_t)node;
+            t.dad[m & 1023u] = (uint16_t)node;
+            hk[1] = (((n >> 16) + (m >> 16)) << 16) | (((dn >= dm ? dn : dm) + 1u) << 10) |
+                    (uint32_t)node;
+            ++node;
+            hdown(hk, heap_len, 1);
+        } while (heap_len >= 2);
+        hk[--heap_max] = hk[1] & 1023u;
+        // gen_bitlen: lengths from the root down, clamped (overflow counted
+        // over every node, as zlib does)
+        int overflow = 0;
+        t.len[hk[heap_max]] = 0;
+        for (int h = heap_max + 1; h < z6::HEAP_SIZE; ++h) {
+            const int n = (int)hk[h];
+            int bits = t.len[t.dad[n]] + 1;
+            if (bits > max_length) { bits = max_length; ++overflow; }
+            t.len[n] = (uint16_t)bits;
+        }
+        W.heap_max = heap_max;
+        W.overflow = overflow;
+    }
+    __syncwarp();
+    max_code = __shfl_sync(FULL, max_code, 0);
+    // bit-length histogram over the leaves
+    for (int n = lane; n <= max_code; n += 32)
+        if (t.freq[n]) atomicAdd(&W.bl_count[t.len[n]], 1u);
+    __syncwarp();
+    if (lane == 0 && W.overflow) {  // trees.c overflow repair, verbatim order
+        int overflow = W.overflow;
+        do {
+            int bits = max_length - 1;
+            while (W.bl_count[bits] == 0) bits--;
+            W.bl_count[bits]--;
+            W.bl_count[bits + 1] += 2;
+            W.bl_count[max_length]--;
+            overflow -= 2;
+        } while (overflow > 0);
+        int h = z6::HEAP_SIZE;
+        for (int bits = max_length; bits != 0; bits--) {
+            int n = (int)W.bl_count[bits];
+            while (n != 0) {
+                const int m = (int)hk[--h];
+                if (m > max_code) continue;
+                t.len[m] = (uint16_t)bits;
+                n--;
+            }
+        }
+    }
+    __syncwarp();
+    // opt_len / static_len with the final lengths (the repair's increments
+    // telescope to exactly this), and gen_codes' next_code
+    unsigned long long o = 0, st = 0;
+    const int base = kind == 0 ? z6::LITERALS + 1 : 0;
+    for (int n = lane; n <= max_code; n += 32) {
+        const unsigned f = t.freq[n];
+        if (!f) continue;
+        int xbits = 0;
+        if (n >= base) {
+            const int e = n - base;
+            xbits = kind == 0 ? z6::extra_lbits(e)
+                              : (kind == 1 ? z6::extra_dbits(e) : z6::extra_blbits(e));
+        }
+        o += (unsigned long long)f * (unsigned)(t.len[n] + xbits);
+        if (kind == 0) st += (unsigned long long)f * (unsigned)(tb.sl_len[n] + xbits);
+        else if (kind == 1) st += (unsigned long long)f * (unsigned)(tb.sd_len[n] + xbits);
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+        o += __shfl_xor_sync(FULL, o, d);
+        st += __shfl_xor_sync(FULL, st, d);
+    }
+    if (lane == 0) {
+        W.opt_len += o;
+        W.static_len += st;
+        unsigned c = 0;
+        for (int bits = 1; bits <= z6::MAX_BITS; bits++) {
+            c = (c + W.bl_count[bits - 1]) << 1;
+            W.next_code[bits] = c;
+        }
+    }
+    __syncwarp();
+    // gen_codes: code = next_code[len]++ in symbol order, bit-reversed
+    for (int n0 = 0; n0 <= max_code; n0 += 32) {
+        const int n = n0 + lane;
+        const int l = n <= max_code ? t.len[n] : 0;
+        const unsigned grp = __match_any_sync(FULL, l);
+        if (l) t.code[n] = (uint16_t)(__brev(W.next_code[l] + __popc(grp & lt_mask)) >> (32 - l));
+        __syncwarp();
+        if (l && (31 - __clz(grp)) == lane) W.next_code[l] += __popc(grp);
+        __syncwarp();
+    }
+}
+
+// trees.c scan_tree / send_tree over a DTree (lane 0)
+template <int NL>
+__device__ void scan_tree_d(DTrees& W, DTree<NL>& t) {
+    const int max_code = t.max_code;
+    int prevlen = -1, curlen, nextlen = t.len[0], count = 0, max_count = 7, min_count = 4;
+    if (nextlen == 0) max_count = 138, min_count = 3;
+    t.len[max_code + 1] = 0xffff;
+    for (int n = 0; n <= max_code; n++) {
+        curlen = nextlen;
+        nextlen = t.len[n + 1];
+        if (++count < max_count && curlen == nextlen) continue;
+        if (count < min_count) W.bt.freq[curlen] += (uint16_t)count;
+        else if (curlen != 0) {
+            if (curlen != prevlen) W.bt.freq[curlen]++;
+            W.bt.freq[z6::REP_3_6]++;
+        } else if (count <= 10) W.bt.freq[z6::REPZ_3_10]++;
+        else W.bt.freq[z6::REPZ_11_138]++;
+        count = 0;
+        prevlen = curlen;
+        if (nextlen == 0) max_count = 138, min_count = 3;
+        else if (curlen == nextlen) max_count = 6, min_count = 3;
+        else max_count = 7, min_count = 4;
+    }
+}
+
+template <int NL, class BO>
+__device__ void send_tree_d(const DTrees& W, const DTree<NL>& t, BO& bo) {
+    const int max_code = t.max_code;
+    int prevlen = -1, curlen, nextlen = t.len[0], count = 0, max_count = 7, min_count = 4;
+    if (nextlen == 0) max_count = 138, min_count = 3;
+    const auto& bt = W.bt;
+    for (int n = 0; n <= max_code; n++) {
+        curlen = nextlen;
+        nextlen = t.len[n + 1];
+        if (++count < max_count && curlen == nextlen) continue;
+        if (count < min_count) {
+            do { bo.bits(bt.code[curlen], bt.len[curlen]); } while (--count != 0);
+        } else if (curlen != 0) {
+            if (curlen != prevlen) {
+                bo.bits(bt.code[curlen], bt.len[curlen]);
+                count--;
+            }
+            bo.bits(bt.code[z6::REP_3_6], bt.len[z6::REP_3_6]);
+            bo.bits((unsigned)(count - 3), 2);
+        } else if (count <= 10) {
+            bo.bits(bt.code[z6::REPZ_3_10], bt.len[z6::REPZ_3_10]);
+            bo.bits((unsigned)(count - 3), 3);
+        } else {
+            bo.bits(bt.code[z6::REPZ_11_138], bt.len[z6::REPZ_11_138]);
+            bo.bits((unsigned)(count - 11), 7);
+        }
+        count = 0;
+        prevlen = curlen;
+        if (nextlen == 0) max_count = 138, min_count = 3;
+        else if (curlen == nextlen) max_count = 6, min_count = 3;
+        else max_count = 7, min_count = 4;
+    }
+}
+
+// Per-warp shared memory: the window, then one region reused by phase:
+//   chain build  : p1 | hash table (u16 entries, aliasing where p4 will go)
+//   matching     : p1 | p4
+//   flush        : Huffman trees | u32 symbol histogram / output bit buffer
+// The symbol buffer lives in global scratch.
+__host__ __device__ inline Lay layout(int nmax) {
+    Lay L;
+    L.nmax = nmax;
+    L.direct = nmax > 4096;
+    L.T = L.direct ? 32768 : pow2ge(nmax + 2);
+    int o = 0;
+    L.win = o;
+    o += al16(nmax + z6::MAX_MATCH + 24);
+    const int b0 = o;
+    L.p1 = b0;
+    L.p4 = b0 + al16(2 * nmax);
+    L.hash = L.p4;
+    const int chains = al16(2 * nmax) + (al16(2 * nmax) > al16(2 * L.T) ? al16(2 * nmax)
+                                                                          : al16(2 * L.T));
+    L.trees = b0;
+    L.hist = b0 + al16((int)sizeof(DTrees));
+    L.obuf = L.hist;
+    const int tail = al16(nmax + 256) > 4 * 320 ? al16(nmax + 256) : 4 * 320;
+    const int flush = al16((int)sizeof(DTrees)) + tail;
+    o += chains > flush ? chains : flush;
+    L.total = o;
+    return L;
+}
+
 }  // namespace wz
 
 __global__ void __launch_bounds__(512)
@@ -195,7 +434,7 @@ k_deflate_warp(const uint8_t* __restrict__ in, const long long* __restrict__ in_
     uint16_t* p1 = reinterpret_cast<uint16_t*>(base + Ly.p1);
     uint16_t* p4 = reinterpret_cast<uint16_t*>(base + Ly.p4);
     uint16_t* htab = reinterpret_cast<uint16_t*>(base + Ly.hash);
-    z6::Trees* trees = reinterpret_cast<z6::Trees*>(base + Ly.trees);
+    wz::DTrees* trees = reinterpret_cast<wz::DTrees*>(base + Ly.trees);
     const unsigned FULL = 0xffffffffu;
     const unsigned lt_mask = (1u << lane) - 1u;
     const int gw = blockIdx.x * ZW + warp, nw = gridDim.x * ZW;
@@ -290,7 +529,7 @@ k_deflate_warp(const uint8_t* __restrict__ in, const long long* __restrict__ in_
         __syncwarp();
         long long t_3 = clock64();
         long long t_lm = 0;
-        int n_calls = 0;
+        int n_calls = 0, n_rounds = 0, n_cands = 0;
         // ---- deflate_slow, warp-uniform state
         int strstart = 0, lookahead = n;
         int match_length = z6::MIN_MATCH - 1, prev_length, prev_match, match_start = 0;
@@ -324,6 +563,8 @@ k_deflate_warp(const uint8_t* __restrict__ in, const long long* __restrict__ in_
                         best = mx;
                     }
                     const unsigned alive = __ballot_sync(FULL, valid);
+                    ++n_rounds;
+                    n_cands += __popc(hit ? (alive & (0xffffffffu >> (31 - upto))) : alive);
                     if (hit || alive != FULL) break;
                     cb = __shfl_sync(FULL, wz::jump(p1, p4, c, 1), 31);
                     if (cb == 0) break;
@@ -374,7 +615,7 @@ k_deflate_warp(const uint8_t* __restrict__ in, const long long* __restrict__ in_
         __syncwarp();
         long long t_4 = clock64();
         // ---- trees (lane 0) + bit stream (all lanes); prev tables are dead now
-        z6::Trees& t = *trees;
+        wz::DTrees& t = *trees;
         unsigned long long* ob = reinterpret_cast<unsigned long long*>(base + Ly.obuf);
         unsigned* hist = reinterpret_cast<unsigned*>(base + Ly.hist);
         __shared__ int sh_kind[16];
@@ -393,21 +634,24 @@ k_deflate_warp(const uint8_t* __restrict__ in, const long long* __restrict__ in_
             }
         }
         __syncwarp();
-        for (int i = lane; i < z6::L_CODES; i += 32) t.lt.freq[i] = (uint16_t)hist[i];
+        for (int i = lane; i < z6::L_CODES; i += 32)
+            t.lt.freq[i] = (uint16_t)(i == z6::END_BLOCK ? 1u : hist[i]);
         for (int i = lane; i < z6::D_CODES; i += 32) t.dt.freq[i] = (uint16_t)hist[z6::L_CODES + i];
         for (int i = lane; i < z6::BL_CODES; i += 32) t.bt.freq[i] = 0;
+        if (lane == 0) t.opt_len = t.static_len = 0;
         __syncwarp();
-        const int obw = (n + 256) / 8;  // u64 words available (the histogram is dead)
+        wz::build_tree_warp(t, t.lt, 0, tb);
+        wz::build_tree_warp(t, t.dt, 1, tb);
+        if (lane == 0) {
+            wz::scan_tree_d(t, t.lt);
+            wz::scan_tree_d(t, t.dt);
+        }
+        __syncwarp();
+        wz::build_tree_warp(t, t.bt, 2, tb);
+        const int obw = (n + 256) / 8;  // u64 words available (histogram + heap are dead)
         for (int i = lane; i < obw; i += 32) ob[i] = 0ull;
         __syncwarp();
         if (lane == 0) {
-            t.lt.freq[z6::END_BLOCK] = 1;
-            t.opt_len = t.static_len = 0;
-            z6::build_tree(t, t.lt, 0, tb);
-            z6::build_tree(t, t.dt, 1, tb);
-            z6::scan_tree(t, t.lt);
-            z6::scan_tree(t, t.dt);
-            z6::build_tree(t, t.bt, 2, tb);
             int max_blindex;
             for (max_blindex = z6::BL_CODES - 1; max_blindex >= 3; max_blindex--)
                 if (t.bt.len[z6::bl_order(max_blindex)] != 0) break;
@@ -432,8 +676,8 @@ k_deflate_warp(const uint8_t* __restrict__ in, const long long* __restrict__ in_
                 sb.bits((unsigned)(dcodes - 1), 5);
                 sb.bits((unsigned)(blcodes - 4), 4);
                 for (int r = 0; r < blcodes; r++) sb.bits(t.bt.len[z6::bl_order(r)], 3);
-                z6::send_tree(t, t.lt, sb);
-                z6::send_tree(t, t.dt, sb);
+                wz::send_tree_d(t, t.lt, sb);
+                wz::send_tree_d(t, t.dt, sb);
             }
             sh_kind[warp] = kind;
             sh_hbits[warp] = sb.bit;
@@ -547,6 +791,8 @@ k_deflate_warp(const uint8_t* __restrict__ in, const long long* __restrict__ in_
                 atomicAdd(prof + 7, 1ull);
                 atomicAdd(prof + 8, (unsigned long long)n);
                 atomicAdd(prof + 9, (unsigned long long)(sym_next / 3));
+                atomicAdd(prof + 10, (unsigned long long)n_rounds);
+                atomicAdd(prof + 11, (unsigned long long)n_cands);
             }
         }
         __syncwarp();

@@ -670,7 +670,7 @@ def _deflate_pool(dev, n_workers):
 DEFLATE_TIERS = (1024, 1600, 2048, 3072, 4096, 8192, 16000)
 
 
-DEFLATE_PROF = None   # set to a (10,) uint64 CUDA tensor to collect phase cycles
+DEFLATE_PROF = None   # set to a (12,) uint64 CUDA tensor to collect phase cycles
 
 
 _TIER_STREAMS = {}

@@ -194,6 +194,19 @@ def test_device_zlib_matches_host_zlib():
                for k, n in [(2, 1), (3, 500), (7, 1521), (256, 3000), (5, 15210), (1, 100)]]
     streams += [zlib.decompress(G.load("units")[1][f"pl{t}_p"].tobytes()[13:])
                 for t in range(len(G.load("units")[0]["payload_ebs"]))]
+    # varint-like streams (geometric magnitudes) across the size tiers
+    for n in [2, 3, 17, 700, 1100, 1521, 1700, 2500, 3500, 5000, 9000]:
+        z = rng.geometric(rng.uniform(0.05, 0.6), n)
+        streams.append(np.minimum(z, 255).astype(np.uint8).tobytes())
+    # skewed (Fibonacci) symbol counts: Huffman lengths overflow MAX_BITS /
+    # MAX_BL_BITS and take the repair path
+    fib = [1, 1]
+    while len(fib) < 20:
+        fib.append(fib[-1] + fib[-2])
+    sym = np.concatenate([np.full(f, k, np.uint8) for k, f in enumerate(fib[:17])])
+    streams.append(rng.permutation(sym)[:15000].tobytes())
+    sym = np.concatenate([np.full(f, 3 * k + 1, np.uint8) for k, f in enumerate(fib[:12])])
+    streams.append(rng.permutation(sym).tobytes())
     vcap = 15216
     var = torch.zeros(len(streams) * vcap, dtype=torch.uint8, device=dev)
     vlen = torch.tensor([len(s) for s in streams], dtype=torch.int64, device=dev)
