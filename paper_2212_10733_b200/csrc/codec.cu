@@ -71,14 +71,21 @@ __device__ __forceinline__ unsigned hkey(const uint8_t* w) {
     return (((unsigned)w[0] << 10) ^ ((unsigned)w[1] << 5) ^ w[2]) & 0x7fffu;
 }
 
+// the i-th chain successor of x: p4^(i/4) o p1^(i%4), as predicated steps
+// (no divergent loop; 0 ends a chain and stays 0)
 __device__ __forceinline__ int jump(const uint16_t* p1, const uint16_t* p4, int x, int i) {
-    while (i >= 4 && x) { x = p4[x]; i -= 4; }
-    while (i > 0 && x) { x = p1[x]; --i; }
+    const int a = i & 3, b = i >> 2;
+#pragma unroll
+    for (int k = 1; k <= 3; ++k)
+        if (a >= k && x) x = p1[x];
+#pragma unroll
+    for (int k = 1; k <= 7; ++k)
+        if (b >= k && x) x = p4[x];
     return x;
 }
 
-// zlib longest_match length of window[c..] against window[p..] (bytes 0, 1
-// checked, byte 2 implied by the hash, then 3..258)
+// zlib longest_match length of window[c..] against window[p..], 8 bytes at
+// a time
 __device__ __forceinline__ unsigned long long load8(const uint8_t* w, int i) {
     // 8 bytes at any offset from 4-byte-aligned words (the window is 16-aligned
     // and padded beyond n + 258)
@@ -90,9 +97,11 @@ __device__ __forceinline__ unsigned long long load8(const uint8_t* w, int i) {
     return ((unsigned long long)hi << 32) | lo;
 }
 
+// (leading equal bytes, capped at MAX_MATCH; zlib rejects a candidate whose
+// first two bytes differ -- such lengths are < 2 here and never win, since
+// every search starts from best >= MIN_MATCH - 1)
 __device__ __forceinline__ int match_len(const uint8_t* win, int p, int c) {
-    if (win[c] != win[p] || win[c + 1] != win[p + 1]) return 0;
-    int k = 3;
+    int k = 0;
     while (k < z6::MAX_MATCH) {
         const unsigned long long x = load8(win, p + k) ^ load8(win, c + k);
         if (x) {
@@ -535,6 +544,29 @@ k_deflate_warp(const uint8_t* __restrict__ in, const long long* __restrict__ in_
         int match_length = z6::MIN_MATCH - 1, prev_length, prev_match, match_start = 0;
         int match_available = 0, sym_next = 0;
         while (lookahead > 0) {
+            if (match_length < z6::MIN_MATCH) {
+                // no pending match: a run of positions with an empty hash head
+                // (or < 3 bytes left) only emits the previous byte as a
+                // literal -- take up to 32 of them in one step
+                const int q = strstart + lane;
+                const bool skip = q < n && (lookahead - lane < z6::MIN_MATCH || p1[q] == 0);
+                const unsigned sk = __ballot_sync(FULL, skip);
+                const int f = sk == FULL ? 32 : __ffs(~sk) - 1;
+                if (f > 0) {
+                    const int first = match_available ? strstart - 1 : strstart;
+                    const int cnt = strstart + f - 1 - first;
+                    if (lane < cnt) {
+                        sym[sym_next + 3 * lane] = 0;
+                        sym[sym_next + 3 * lane + 1] = 0;
+                        sym[sym_next + 3 * lane + 2] = win[first + lane];
+                    }
+                    sym_next += 3 * cnt;
+                    strstart += f;
+                    lookahead -= f;
+                    match_available = 1;
+                    continue;
+                }
+            }
             const int hash_head = lookahead >= z6::MIN_MATCH ? p1[strstart] : 0;
             prev_length = match_length;
             prev_match = match_start;
@@ -554,9 +586,7 @@ k_deflate_warp(const uint8_t* __restrict__ in, const long long* __restrict__ in_
                     const int len = valid ? wz::match_len(win, strstart, c) : 0;
                     const unsigned hit = __ballot_sync(FULL, valid && len >= thr);
                     const int upto = hit ? __ffs(hit) - 1 : 31;
-                    int v = lane <= upto ? len : 0;
-                    int mx = v;
-                    for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(FULL, mx, o));
+                    const int mx = (int)__reduce_max_sync(FULL, lane <= upto ? (unsigned)len : 0u);
                     if (mx > best) {
                         const unsigned at = __ballot_sync(FULL, lane <= upto && len == mx);
                         bstart = __shfl_sync(FULL, c, __ffs(at) - 1);
@@ -566,7 +596,7 @@ k_deflate_warp(const uint8_t* __restrict__ in, const long long* __restrict__ in_
                     ++n_rounds;
                     n_cands += __popc(hit ? (alive & (0xffffffffu >> (31 - upto))) : alive);
                     if (hit || alive != FULL) break;
-                    cb = __shfl_sync(FULL, wz::jump(p1, p4, c, 1), 31);
+                    cb = __shfl_sync(FULL, c ? (int)p1[c] : 0, 31);
                     if (cb == 0) break;
                 }
                 match_start = bstart;
