@@ -1,0 +1,140 @@
+"""Host <-> device staging for the public API (compress / decompress).
+
+The end-to-end path moves the whole timestep over PCIe: 1.6 GB of f0 in,
+the archive (~1/7 of that) out.  Pageable copies run at a fraction of the
+link rate and a fresh `bytes` object costs a page fault per 4 KiB, so:
+
+  * uploads go through a persistent pinned staging buffer, filled in 64 MiB
+    chunks by a thread pool (numpy copies release the GIL) with each chunk's
+    async H2D issued on a copy stream as soon as it lands -- host copy and
+    PCIe transfer overlap;
+  * downloads land in a persistent pinned buffer with one async copy; the
+    archive `bytes` is allocated uninitialised and filled by the same pool.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import sys
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+import torch
+
+__all__ = ["upload_planes", "download_bytes", "download_view", "pinned"]
+
+CHUNK = 64 << 20
+_POOL = None
+_PINNED = {}
+_COPY_STREAMS = {}
+_LAST_UPLOAD = {}
+
+
+def _pool():
+    global _POOL
+    if _POOL is None:
+        _POOL = ThreadPoolExecutor(max_workers=max(2, min(16, os.cpu_count() or 2)),
+                                   thread_name_prefix="mlk-hostio")
+    return _POOL
+
+
+def pinned(name: str, nbytes: int) -> torch.Tensor:
+    """Grow-only pinned uint8 buffer by name."""
+    b = _PINNED.get(name)
+    if b is None or b.numel() < nbytes:
+        b = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, pin_memory=True)
+        _PINNED[name] = b
+    return b
+
+
+def _copy_stream(dev):
+    s = _COPY_STREAMS.get(dev.index)
+    if s is None:
+        s = _COPY_STREAMS[dev.index] = torch.cuda.Stream(device=dev)
+    return s
+
+
+def upload_planes(data: np.ndarray, dev, node_range=None, pad_elems: int = 2) -> torch.Tensor:
+    """data[:, lo:hi] of a (P, N, ...) float64 array -> flat device buffer
+    (+pad_elems zeros of tail padding), on the current stream's timeline."""
+    P, N = data.shape[:2]
+    lo, hi = node_range or (0, N)
+    per_node = int(np.prod(data.shape[2:])) * data.itemsize
+    slab = (hi - lo) * per_node
+    total = P * slab
+    buf = torch.empty(total // data.itemsize + pad_elems, dtype=torch.float64, device=dev)
+    if pad_elems:
+        buf[total // data.itemsize:].zero_()
+    if total == 0:
+        return buf
+    stage = pinned(f"up{dev.index}", total)
+    last = _LAST_UPLOAD.get(dev.index)
+    if last is not None:
+        last.synchronize()  # the previous upload has left the staging buffer
+    st_np = stage.numpy()
+    dst = buf.view(torch.uint8)
+    # (plane, byte range within the slab) pieces of <= CHUNK bytes
+    pieces = []
+    for p in range(P):
+        for a in range(0, slab, CHUNK):
+            pieces.append((p, a, min(slab, a + CHUNK)))
+    src2d = data.reshape(P, N * per_node // data.itemsize)
+
+    def fill(piece):
+        p, a, b = piece
+        row = src2d[p].view(np.uint8)[lo * per_node:hi * per_node]
+        st_np[p * slab + a:p * slab + b] = row[a:b]
+        return piece
+
+    cs = _copy_stream(dev)
+    cs.wait_stream(torch.cuda.current_stream(dev))  # buf allocation is ordered first
+    with torch.cuda.stream(cs):
+        for p, a, b in _pool().map(fill, pieces):
+            o = p * slab
+            dst[o + a:o + b].copy_(stage[o + a:o + b], non_blocking=True)
+    ev = torch.cuda.Event()
+    ev.record(cs)
+    _LAST_UPLOAD[dev.index] = ev
+    torch.cuda.current_stream(dev).wait_event(ev)
+    buf.record_stream(cs)
+    return buf
+
+
+_BYTES_OFF = sys.getsizeof(b"") - 1  # offset of ob_sval in a CPython bytes object
+_new_bytes = ctypes.pythonapi.PyBytes_FromStringAndSize
+_new_bytes.restype = ctypes.py_object
+_new_bytes.argtypes = [ctypes.c_void_p, ctypes.c_ssize_t]
+
+
+def download_bytes(src: torch.Tensor, nbytes: int, prefix: bytes = b"") -> bytes:
+    """prefix + the first nbytes of a device uint8 tensor, as one bytes object."""
+    dev = src.device
+    stage = pinned(f"down{dev.index}", nbytes)
+    if nbytes:
+        stage[:nbytes].copy_(src[:nbytes], non_blocking=True)
+        torch.cuda.current_stream(dev).synchronize()
+    total = len(prefix) + nbytes
+    out = _new_bytes(None, total)  # uninitialised; filled before anyone sees it
+    view = np.ctypeslib.as_array((ctypes.c_uint8 * total).from_address(id(out) + _BYTES_OFF))
+    view[:len(prefix)] = np.frombuffer(prefix, dtype=np.uint8)
+    body = view[len(prefix):]
+    st_np = stage.numpy()
+    spans = [(a, min(nbytes, a + CHUNK)) for a in range(0, nbytes, CHUNK)]
+
+    def cp(span):
+        a, b = span
+        body[a:b] = st_np[a:b]
+
+    list(_pool().map(cp, spans))
+    return out
+
+
+def download_view(src: torch.Tensor, nbytes: int) -> np.ndarray:
+    """The first nbytes of a device uint8 tensor in the pinned download buffer
+    (a view: valid until the next download on this device)."""
+    stage = pinned(f"down{src.device.index}", nbytes)
+    if nbytes:
+        stage[:nbytes].copy_(src[:nbytes], non_blocking=True)
+        torch.cuda.current_stream(src.device).synchronize()
+    return stage.numpy()[:nbytes]

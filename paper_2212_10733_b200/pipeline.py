@@ -18,11 +18,11 @@ from dataclasses import asdict, dataclass, field
 import numpy as np
 import torch
 
-from . import engine
+from . import engine, hostio
 from ._lib import F_EXCEPTION, F_EXC_OVERFLOW, F_NONFINITE, F_SELECTED
 from .autoencoder import AEModel
 from .container import ArchivePreamble, archive_offsets, read_archive, read_shard
-from .decomp import SelectionScheme, partition
+from .decomp import SelectionScheme, partition, shard_dataset_index
 from .errors import ConfigError, FormatError, SizeMismatchError
 from .fdata import FDataset, dataset_nbytes
 from .lagrange import NewtonOptions, NewtonStatus
@@ -112,17 +112,11 @@ def upload_f0(data: np.ndarray, device, node_range=None) -> torch.Tensor:
     """(P, N, R, C) float64 host array -> flat device buffer (+16 B pad).
 
     node_range=(lo, hi) uploads only that node slab of every plane (the
-    rank-local part of a column decomposition)."""
-    P, N, R, C = data.shape
-    lo, hi = node_range or (0, N)
-    n_el = P * (hi - lo) * R * C
-    buf = torch.empty(n_el + 2, dtype=torch.float64, device=device)
-    src = np.ascontiguousarray(data[:, lo:hi]) if (lo, hi) != (0, N) else \
-        np.ascontiguousarray(data)
-    host = torch.from_numpy(src.reshape(-1))
-    if host.numel():
-        buf[:n_el].copy_(host.pin_memory() if not host.is_pinned() else host, non_blocking=True)
-    return buf
+    rank-local part of a column decomposition).  Pinned, chunked and
+    overlapped with the host-side copy (hostio.upload_planes)."""
+    if data.dtype != np.float64:
+        data = data.astype(np.float64)
+    return hostio.upload_planes(data, device, node_range)
 
 
 def _check_state(config, state, n_shards):
@@ -156,11 +150,9 @@ def compress(ds: FDataset, config: PipelineConfig, state: TimestepState | None =
                                config_digest=config.digest())
     head = preamble.pack()
     offs = archive_offsets(len(head), [int(n) for n in out.blob_lens])
-    archive = head + struct.pack(f"<{len(offs)}Q", *offs) + \
-        out.blob_buf[:int(np.sum(out.blob_lens))].cpu().numpy().tobytes()
-    out.dataset_index = np.concatenate(
-        [np.fromiter((p * ds.n_nodes + x for p, x in sh.members), dtype=np.int64,
-                     count=len(sh.members)) for sh in shards])
+    archive = hostio.download_bytes(out.blob_buf, int(np.sum(out.blob_lens)),
+                                    head + struct.pack(f"<{len(offs)}Q", *offs))
+    out.dataset_index = np.concatenate([shard_dataset_index(sh, ds.n_nodes) for sh in shards])
     stage_t["pack"] = stage_t.get("pack", 0.0) + time.perf_counter() - t0
     report = build_report(ds, archive, [out], config.tau, stage_t,
                           time.perf_counter() - t_all)
@@ -202,7 +194,7 @@ def compress_distributed(ds: FDataset, config: PipelineConfig, state: TimestepSt
     head = preamble.pack()
     sizes, offs = D_.exchange_sizes(rp, out.blob_lens, len(head), group)
     if out_path is not None:
-        body = out.blob_buf[:int(np.sum(out.blob_lens))].cpu().numpy()
+        body = hostio.download_view(out.blob_buf, int(np.sum(out.blob_lens)))
         if rp.rank == 0:
             with open(out_path, "wb") as fh:
                 fh.write(head + struct.pack(f"<{len(offs)}Q", *[int(x) for x in offs]))
@@ -212,7 +204,7 @@ def compress_distributed(ds: FDataset, config: PipelineConfig, state: TimestepSt
         if rp.mine:
             fd = os.open(out_path, os.O_WRONLY)
             try:
-                os.pwrite(fd, body.tobytes(), int(offs[rp.mine[0]]))
+                os.pwrite(fd, memoryview(body), int(offs[rp.mine[0]]))
             finally:
                 os.close(fd)
         if dist.is_initialized():

@@ -56,9 +56,15 @@ def _check_lambdas(got: bytes, want: bytes, precision: str):
     w = np.frombuffer(want, dt).reshape(-1, 8)
     assert g.shape == w.shape
     if precision == "f32":
-        # stored QoIs are f32-cast moments: bit-exact except f32 rounding ties
+        # stored QoIs are f32-cast moments: bit-exact except f32 rounding ties.
+        # u_par = sum(f vol v_par) / n cancels to ~1e-8 of the thermal speed on
+        # symmetric histograms, where both sides carry ~1e-16 * sum|f vol v_par|
+        # of summation-order noise: absolute 1e-12 there
         qu = np.abs(g[:, 4:].view(np.int32).astype(np.int64) - w[:, 4:].view(np.int32))
-        assert qu.max() <= 1 and (qu > 0).mean() <= 1e-3
+        dq = np.abs(g[:, 4:].astype(np.float64) - w[:, 4:].astype(np.float64))
+        ok = (qu <= 1) | (dq <= 1e-12)
+        assert ok.all(), (np.argwhere(~ok)[:5], g[:, 4:][~ok][:5], w[:, 4:][~ok][:5])
+        assert (qu > 0).mean() <= 1e-3
     else:
         # f64 moments: einsum vs device reduction order; u_par is a ratio that
         # can be ~1e-5 of the thermal speed, so it gets an absolute floor
@@ -123,6 +129,62 @@ def test_compress_matches_reference(name, newton, monkeypatch):
             assert rep.max_qoi_nrmse <= 1e-8
         else:
             assert rep.max_qoi_nrmse <= 1e-12
+
+
+def _oracle_lambdas(ds, run, models):
+    """Lambda sections of the oracle's shards (threads over shards)."""
+    from concurrent.futures import ThreadPoolExecutor
+    cfg = G.oracle_cfg(run)
+    members = port.shard_members(ds.n_planes, ds.n_nodes, cfg.shards, cfg.mode)
+
+    def job(i):
+        pl, no = members[i]
+        blob = port.compress_shard(ds.data[pl, no], G.oracle_grid(), cfg, models[i], i).blob
+        return container.read_shard(blob).sections["lambdas"]
+
+    with ThreadPoolExecutor(max_workers=8) as ex:
+        return list(ex.map(job, range(len(members))))
+
+
+@pytest.mark.parametrize("name", ["cfg2", "cfg3"])
+def test_benchmark_configs_match_reference(name):
+    """BASELINE configs[1] (tau sweep 1e-3 / 1e-2 / 1e-4) and configs[2] (the
+    bench workload): every section hash, eb, selection count, exception list,
+    archive length and ratio as the reference produced them; lambda sections
+    bit-exact or, where an f32 rounding tie flips, within the tie tolerance of
+    the oracle's (pinned to the reference on the smaller corpora)."""
+    meta, _ = G.load(name)
+    ds, same = G.corpus(name)
+    if not same:
+        pytest.skip("host generates a different corpus")
+    models = _models(name)
+    for vi, run in enumerate(meta["runs"]):
+        cfg = _cfg(run)
+        arc, rep, _ = mb.compress(ds, cfg, mb.TimestepState(models=models, timestep_index=1))
+        _, blobs = container.read_archive(arc)
+        lam_mismatch = []
+        for si, b in enumerate(blobs):
+            h, sec = _sections(b)
+            ref = run["shards"][si]
+            assert G.sha(sec["codes"]) == ref["codes_sha"], (name, vi, si, "codes")
+            assert G.sha(sec["pq_table"]) == ref["ptab_sha"], (name, vi, si, "pq_table")
+            eb, cnt = struct.unpack_from("<dI", sec["residuals"], 0)
+            assert eb == ref["eb"] and cnt == ref["n_sel"], (name, vi, si, "eb/n_sel")
+            assert G.sha(sec["residuals"]) == ref["res_sha"], (name, vi, si, "residuals")
+            assert G.sha(sec["exceptions"]) == ref["exc_sha"], (name, vi, si, "exceptions")
+            assert list(h.section_lengths) == ref["sec_len"]
+            if G.sha(sec["lambdas"]) != ref["lam_sha"]:
+                lam_mismatch.append((si, sec["lambdas"]))
+        if lam_mismatch:
+            want = _oracle_lambdas(ds, run, G.models(name))
+            for si, got in lam_mismatch:
+                _check_lambdas(got, want[si], cfg.lambda_precision)
+        assert len(arc) == run["archive_len"]
+        assert rep.compression_ratio == run["ratio"]
+        assert rep.exception_count == run["exceptions"]
+        assert rep.residual_fraction == run["residual_fraction"]
+        assert rep.convergence_fraction == run["convergence_fraction"]
+        assert rep.max_per_image_nrmse() <= cfg.tau
 
 
 @pytest.mark.parametrize("name", CASES)
