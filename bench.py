@@ -182,6 +182,67 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def _peak():
+    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) \
+        if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    if "hbm_gbs" in peaks:
+        return float(peaks["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs"
+    return 6650.0, "B200_PROFILING.md fallback"
+
+
+def _traffic(kernel, launches_per_step):
+    """DRAM bytes per step of `kernel` from the committed ncu --set full
+    capture (profiles/r1_kernels.json), when every launch of a step is in it."""
+    path = ROOT / "profiles" / "r1_kernels.json"
+    if not path.exists():
+        return None
+    ks = [k for k in json.loads(path.read_text()) if k["kernel"].startswith(kernel)]
+    if len(ks) != launches_per_step:
+        return None
+    return sum(k.get("dram_read_bytes", 0) + k.get("dram_write_bytes", 0) for k in ks)
+
+
+def rooflines(out, stage_ms, n, dev):
+    """Per-kernel achieved GB/s = algorithmic bytes per step / stage time."""
+    import torch
+
+    from paper_2212_10733_b200 import engine
+    ws = engine.Workspace.get(dev)
+    n_sel = int(np.sum(out.sel_count))
+    vlen = ws.bufs["vlen"][:8 * n_sel].view(torch.int64).sum().item() if n_sel else 0
+    zlen = ws.bufs["zlen"][:8 * n_sel].view(torch.int64).sum().item() if n_sel else 0
+    peak, src = _peak()
+    rows = [
+        ("k_stage1", "encode", n * (HIST_BYTES + 96), 1,
+         "reads every histogram once (TMA) + 96 B of latents/stats/moments"),
+        ("k_project", "newton", n * (HIST_BYTES + 185) + vlen, 1,
+         "reads every histogram again + per-image outputs + varint streams"),
+        ("k_deflate_warp", "deflate", vlen + zlen, 7,
+         "varint bytes in + zlib bytes out; serial LZ77/Huffman per stream (latency-bound)"),
+        ("k_probe", "eb_search", None, None, "re-reads selected histograms per round; L2/latency"),
+        ("k_kmeans", "pq", None, None, "32 B of latents per histogram; barrier/latency-bound"),
+    ]
+    table = []
+    for kern, stage, nbytes, launches, note in rows:
+        ms = stage_ms.get(stage)
+        if ms is None:
+            continue
+        e = {"kernel": kern, "stage": stage, "ms_per_step": ms, "note": note}
+        if nbytes is not None:
+            ach = nbytes / (ms / 1e3) / 1e9
+            e.update(achieved=ach, peak=peak, unit="GB/s", frac=ach / peak,
+                     algorithmic_bytes_per_step=int(nbytes),
+                     traffic=_traffic(kern, launches) if launches else None)
+        table.append(e)
+    dom = max((e for e in table if "achieved" in e), key=lambda e: e["ms_per_step"])
+    roofline = {"bound": "hbm", "kernel": dom["kernel"], "achieved": dom["achieved"],
+                "peak": peak, "unit": "GB/s", "frac": dom["frac"], "traffic": dom["traffic"],
+                "algorithmic_bytes_per_step": dom["algorithmic_bytes_per_step"],
+                "ms_per_step": dom["ms_per_step"], "peak_source": src,
+                "note": dom["note"] + "; per-kernel table in 'kernels'"}
+    return roofline, table
+
+
 def main():
     args = parse()
     rank = int(os.environ.get("RANK", "0"))
@@ -262,32 +323,9 @@ def main():
     value = total_hist / (ms / 1e3)
     stage_ms = {k: 1e3 * v / args.steps for k, v in stage_sum.items()}
 
-    # roofline of the pass-1 kernel (reads every histogram once: 12,168 B each)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    lat = torch.empty((n_local, 4), dtype=torch.float64, device=dev)
-    st = torch.empty((n_local, 4), dtype=torch.float64, device=dev)
-    qo = torch.empty((n_local, 4), dtype=torch.float64, device=dev)
-    table = engine._shard_table(works, D, cfg.latent_dim)
-    sh_d = engine._upload_shards(table, dev)
-    W = torch.from_numpy(np.stack([w.model.weights for w in works])).to(dev)
-    reps = 5
-    e0.record()
-    for _ in range(reps):
-        _lib.call("mlk_stage1", f0, sh_d, len(works), n_local, dgrid.addr, W, cfg.latent_dim,
-                  lat, st, qo)
-    e1.record()
-    torch.cuda.synchronize()
-    s1_ms = e0.elapsed_time(e1) / reps
-    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) \
-        if (ROOT / "MEASURED_PEAKS.json").exists() else {}
-    peak = float(peaks.get("hbm_gbs", 6650.0))
-    s1_bytes = n_local * HIST_BYTES
-    achieved = s1_bytes / (s1_ms / 1e3) / 1e9
-    roofline = {"bound": "hbm", "kernel": "k_stage1 (pass 1: encode + moments)",
-                "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": None, "algorithmic_bytes_per_launch": s1_bytes,
-                "launch_ms": s1_ms,
-                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650"}
+    # rooflines from the stage intervals of the timed loop (CUDA events on the
+    # launching stream) and each kernel's algorithmic bytes per step
+    roofline, kernels = rooflines(out, stage_ms, n_local, dev)
 
     # end to end through the public API: host numpy f0 in, archive bytes out
     e2e = None
@@ -358,7 +396,7 @@ def main():
                            "l2": "inputs 1.6 GB > 126 MB L2 (no flush needed)"},
                 "raw_gb_s": value * HIST_BYTES / 1e9,
                 "wall_ms_per_step": wall_ms, "stage_ms": stage_ms, "probe_rounds": probe_rounds,
-                "newton": newton, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+                "newton": newton, "roofline": roofline, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e,
                 "decompress_and_report": dec, "gpu_launches": launches,
                 "clocks": clk.summary(),
                 "ratio": None if dec is None else dec["ratio"]}
