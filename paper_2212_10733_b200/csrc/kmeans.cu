@@ -21,7 +21,9 @@ namespace {
 
 constexpr int KT = 1024;           // threads per CTA
 constexpr int KW = KT / 32;        // warps
-constexpr int KM_MAX_LEAVES = 6144;  // pairwise leaves (n <= 2^18 per shard)
+constexpr int KM_MAX_N = 1 << 18;   // members per shard
+// heap slots of the pairwise trees: 2^(depth+1) < m / 28 per segment, + 2 per segment
+constexpr int KM_MAX_SLOTS = KM_MAX_N / 28 + 2 * MLK_MAXK + 64;
 
 struct KmSmem {
     double red[KW];
@@ -32,10 +34,11 @@ struct KmSmem {
     double distinct[MLK_MAXK + 1];
     int seg_start[MLK_MAXK];
     int seg_cnt[MLK_MAXK];
-    int first_leaf[MLK_MAXK + 1];
+    int seg_base[MLK_MAXK + 1];
+    int one_start, one_len;
     int bcast_i;
     double bcast_d;
-    int n_leaves;
+    double sums[MLK_MAXK];
 };
 
 // ---------------------------------------------------------------- block helpers
@@ -154,60 +157,96 @@ __device__ __forceinline__ int nearest(double v, const double* c, int K) {
     return best;
 }
 
-// enumerate pairwise leaves of a segment (single thread)
-__device__ void enum_leaves(int base, int len, int* lstart, short* llen, int& cnt) {
-    int st_b[40], st_l[40];
-    int sp = 0;
-    st_b[sp] = base;
-    st_l[sp] = len;
-    ++sp;
-    while (sp) {
-        --sp;
-        int b = st_b[sp], l = st_l[sp];
-        if (l <= 128) {
-            lstart[cnt] = b;
-            llen[cnt] = (short)l;
-            ++cnt;
-            continue;
-        }
-        int l2 = pw_split(l);
-        // push right first so the left half is enumerated first
-        st_b[sp] = b + l2; st_l[sp] = l - l2; ++sp;
-        st_b[sp] = b; st_l[sp] = l2; ++sp;
+// ---- numpy pairwise sums of many segments at once.  The recursion of
+// segment length m (pw_split) is laid out as a binary heap: slot i's path is
+// the bits of i below its leading one (0 = left, 1 = right).  Leaves
+// (len <= 128) are summed in parallel; internal slots are combined deepest
+// level first, one barrier per level -- no serial combine.
+__device__ __forceinline__ int pw_depth(int m) {
+    int d = 0;
+    while (m > 128) {
+        m -= pw_split(m);  // the right child is the longer one
+        ++d;
     }
+    return d;
 }
 
-__device__ double combine_leaves(const double* leaf, int n, int& next) {
-    // iterative post-order over the same recursion as pw_combine
-    int st_n[40];
-    unsigned char st_state[40];
-    double vals[40];
-    int sp = 0, vp = 0;
-    st_n[0] = n;
-    st_state[0] = 0;
-    sp = 1;
-    while (sp) {
-        int m = st_n[sp - 1];
-        if (m <= 128) {
-            vals[vp++] = leaf[next++];
-            --sp;
-            continue;
+// (start, len) of heap slot i of a length-m segment; kind 0 = absent (below
+// a leaf), 1 = leaf, 2 = internal
+__device__ __forceinline__ int pw_slot(int m, unsigned i, int& st, int& len) {
+    const int depth = 31 - __clz(i);
+    st = 0;
+    len = m;
+    for (int b = depth - 1; b >= 0; --b) {
+        if (len <= 128) return 0;
+        const int l2 = pw_split(len);
+        if ((i >> b) & 1u) { st += l2; len -= l2; } else { len = l2; }
+    }
+    return len <= 128 ? 1 : 2;
+}
+
+// seg k = x[seg_start[k] .. + seg_len[k]), k < nseg (nseg <= 32 * 8);
+// out[k] = its numpy pairwise sum (0 for empty segments).  Whole CTA.
+__device__ void block_pw_sums(const double* x, const int* seg_start, const int* seg_len,
+                              int nseg, double* val, unsigned char* kind, int* base,
+                              double* out, KmSmem& S) {
+    const int tid = threadIdx.x, lane = tid & 31;
+    if (tid < 32) {
+        int run = 0, dmax = 0;
+        for (int k0 = 0; k0 < nseg; k0 += 32) {
+            const int k = k0 + lane;
+            const int len = k < nseg ? seg_len[k] : 0;
+            const int d = len > 0 ? pw_depth(len) : -1;
+            const int sz = len > 0 ? (2 << d) : 0;
+            int inc = sz;
+            for (int o = 1; o < 32; o <<= 1) {
+                const int t = __shfl_up_sync(0xffffffffu, inc, o);
+                if (lane >= o) inc += t;
+            }
+            if (k < nseg) base[k] = run + inc - sz;
+            run += __shfl_sync(0xffffffffu, inc, 31);
+            dmax = max(dmax, d);
         }
-        int m2 = pw_split(m);
-        if (st_state[sp - 1] == 0) {
-            st_state[sp - 1] = 1;
-            st_n[sp] = m2; st_state[sp] = 0; ++sp;
-        } else if (st_state[sp - 1] == 1) {
-            st_state[sp - 1] = 2;
-            st_n[sp] = m - m2; st_state[sp] = 0; ++sp;
-        } else {
-            double b = vals[--vp];
-            double a = vals[--vp];
-            vals[vp++] = __dadd_rn(a, b);
-            --sp;
+        for (int o = 16; o > 0; o >>= 1) dmax = max(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+        if (lane == 0) {
+            base[nseg] = run;
+            S.bcast_i = dmax;
         }
     }
-    return vals[0];
+    __syncthreads();
+    const int total = base[nseg], dmax = S.bcast_i;
+    for (int t = tid; t < total; t += KT) {
+        int lo = 0, hi = nseg - 1;  // segment of slot t: last k with base[k] <= t
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (base[mid] <= t) lo = mid; else hi = mid - 1;
+        }
+        const unsigned i = (unsigned)(t - base[lo]);
+        int st = 0, len = 0;
+        const int kd = i ? pw_slot(seg_len[lo], i, st, len) : 0;
+        kind[t] = (unsigned char)(kd | ((i ? 31 - __clz(i) : 0) << 2));
+        if (kd == 1) {
+            const double* xs = x + seg_start[lo] + st;
+            val[t] = pw_leaf([&](int q) { return xs[q]; }, 0, len);
+        }
+    }
+    __syncthreads();
+    for (int d = dmax - 1; d >= 0; --d) {
+        for (int t = tid; t < total; t += KT) {
+            const unsigned char kd = kind[t];
+            if ((kd & 3) != 2 || (kd >> 2) != d) continue;
+            int lo = 0, hi = nseg - 1;
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if (base[mid] <= t) lo = mid; else hi = mid - 1;
+            }
+            const int i = t - base[lo];
+            val[t] = __dadd_rn(val[base[lo] + 2 * i], val[base[lo] + 2 * i + 1]);
+        }
+        __syncthreads();
+    }
+    for (int k = tid; k < nseg; k += KT) out[k] = seg_len[k] > 0 ? val[base[k] + 1] : 0.0;
+    __syncthreads();
 }
 
 __global__ void __launch_bounds__(KT, 1)
@@ -215,11 +254,10 @@ k_kmeans(const double* __restrict__ lat, const MlkShard* __restrict__ shards, in
          const long long* __restrict__ first_idx, const double* __restrict__ draws,
          double* __restrict__ scratch, float* __restrict__ cents, int* __restrict__ info) {
     __shared__ KmSmem S;
-    extern __shared__ double dyn[];  // leaf sums, leaf starts/lengths, warp counters
-    double* leafsum = dyn;
-    int* lstart = reinterpret_cast<int*>(dyn + KM_MAX_LEAVES);
-    int* wcnt = lstart + KM_MAX_LEAVES;                          // [KW][K]
-    short* llen = reinterpret_cast<short*>(wcnt + KW * MLK_MAXK);
+    extern __shared__ double dyn[];  // pairwise heap slots, slot kinds, warp counters
+    double* val = dyn;
+    int* wcnt = reinterpret_cast<int*>(dyn + KM_MAX_SLOTS);   // [KW][K]
+    unsigned char* kind = reinterpret_cast<unsigned char*>(wcnt + KW * MLK_MAXK);
 
     const int s = blockIdx.x / L, dim = blockIdx.x % L;
     const MlkShard sh = shards[s];
@@ -264,12 +302,10 @@ k_kmeans(const double* __restrict__ lat, const MlkShard* __restrict__ shards, in
 
     // ---- pairwise plan for length-n sums (leaves reused for every d2.sum())
     if (tid == 0) {
-        int c = 0;
-        enum_leaves(0, n, lstart, llen, c);
-        S.n_leaves = c;
+        S.one_start = 0;
+        S.one_len = n;
     }
     __syncthreads();
-    const int nl_full = S.n_leaves;
 
     // ---- k-means++ seeding (quantizer.py:66-76)
     const long long f_idx = first_idx[s * L + dim];
@@ -289,15 +325,8 @@ k_kmeans(const double* __restrict__ lat, const MlkShard* __restrict__ shards, in
     const int j_lo = min(n, tid * chunk), j_hi = min(n, j_lo + chunk);
     const double delta = (16.0 * (n + 8)) * 1.1102230246251565e-16;
     for (int i = 1; i < K; ++i) {
-        for (int l = tid; l < nl_full; l += KT)
-            leafsum[l] = pw_leaf([&](int q) { return d2[q]; }, lstart[l], llen[l]);
-        __syncthreads();
-        if (tid == 0) {
-            int nx = 0;
-            S.bcast_d = combine_leaves(leafsum, n, nx);
-        }
-        __syncthreads();
-        const double tot = S.bcast_d;
+        block_pw_sums(d2, &S.one_start, &S.one_len, 1, val, kind, S.seg_base, S.sums, S);
+        const double tot = S.sums[0];
         if (tot <= 0) {
             if (tid == 0)
                 for (int q = i; q < K; ++q) S.cent[q] = S.cent[0];
@@ -400,29 +429,11 @@ k_kmeans(const double* __restrict__ lat, const MlkShard* __restrict__ shards, in
         }
         __syncthreads();
         // pairwise means of every live cluster
-        if (tid == 0) {
-            int c = 0;
-            for (int k = 0; k < K; ++k) {
-                S.first_leaf[k] = c;
-                if (S.seg_cnt[k] > 0) enum_leaves(S.seg_start[k], S.seg_cnt[k], lstart, llen, c);
-            }
-            S.first_leaf[K] = c;
-            S.n_leaves = c;
-        }
-        __syncthreads();
-        for (int l = tid; l < S.n_leaves; l += KT)
-            leafsum[l] = pw_leaf([&](int q) { return srt[q]; }, lstart[l], llen[l]);
         if (tid < K) S.oldc[tid] = S.cent[tid];
-        __syncthreads();
+        block_pw_sums(srt, S.seg_start, S.seg_cnt, K, val, kind, S.seg_base, S.sums, S);
         if (tid < K) {
-            int c = S.seg_cnt[tid];
-            if (c > 0) {
-                int nx = 0;
-                double sm = combine_leaves(leafsum + S.first_leaf[tid], c, nx);
-                S.newc[tid] = __ddiv_rn(sm, (double)c);
-            } else {
-                S.newc[tid] = S.oldc[tid];
-            }
+            const int c = S.seg_cnt[tid];
+            S.newc[tid] = c > 0 ? __ddiv_rn(S.sums[tid], (double)c) : S.oldc[tid];
         }
         __syncthreads();
         // dead clusters, in index order, against the partially updated table
@@ -477,8 +488,7 @@ extern "C" int mlk_kmeans(const double* lat, const MlkShard* shards, const MlkSh
     if (K < 2 || K > MLK_MAXK || L < 1 || L > MLK_MAXL) return MLK_ERR_CONFIG;
     for (int s = 0; s < n_shards; ++s)
         if (shards_h[s].n_img < 1 || shards_h[s].n_img > (1 << 18)) return MLK_ERR_DIM;
-    size_t dyn = KM_MAX_LEAVES * (sizeof(double) + sizeof(int) + sizeof(short)) +
-                 (size_t)KW * MLK_MAXK * sizeof(int);
+    size_t dyn = (size_t)KM_MAX_SLOTS * (sizeof(double) + 1) + (size_t)KW * MLK_MAXK * sizeof(int);
     cudaFuncSetAttribute(k_kmeans, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
     k_kmeans<<<n_shards * L, KT, dyn, stream>>>(lat, shards, L, K,
                                                 reinterpret_cast<const long long*>(first_idx),
