@@ -77,7 +77,7 @@ _SIGS = {
     "mlk_recheck": [_P, _P, _P, _I32, _I32, _P, _P, _I32, _P, _I32, _P, _D, _P, _P, _P],
     "mlk_compact": [_P, _P, _P, _I32, _D, _P, _P, _P, _P, _P, _P],
     "mlk_probe": [_P, _P, _P, _I32, _P, _P, _I32, _P, _I32, _P, _P, _P, _P, _I32, _P, _D, _P,
-                  _I32, _P, _P],
+                  _I32, _I32, _P, _I32, _P],
     "mlk_project": [_P, _P, _P, _P, _I32, _I32, _P, _P, _I32, _P, _I32, _P, _P, _P, _P, _P,
                     _P, _P, _P, _P, _P, _P, _P, _P, _I64, _P, _P, _P],
     "mlk_list_flags": [_P, _P, _I32, ctypes.c_uint32, _P, _P, _P],

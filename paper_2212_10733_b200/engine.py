@@ -28,7 +28,7 @@ from .errors import ConfigError, FormatError, SizeMismatchError
 
 SPAN = 2.0 ** -20
 STEPS = 20
-LOOKAHEAD = 4          # bisection levels answered per probe launch (2**4 - 1 bounds)
+LOOKAHEAD = 6          # bisection levels per host round trip (one probe launch each)
 _PAYLOAD_HEAD = struct.Struct("<BHHd")
 
 
@@ -161,23 +161,34 @@ class _Search:
         return self
 
 
-def _search_tree(root: _Search, depth: int):
-    """Pre-order list of the states queried in the next `depth` decisions.
-
-    Each entry is [state, child_if_accepted, child_if_rejected] where a child
-    is an int (another entry) or a _Search left for the next round."""
-    nodes = []
-
-    def build(st, d):
-        if st.stage == "done" or d == depth:
-            return st
-        i = len(nodes)
-        nodes.append([st, None, None])
-        nodes[i][1] = build(st.advance(True), d + 1)
-        nodes[i][2] = build(st.advance(False), d + 1)
-        return i
-
-    return nodes, build(root, 0)
+def _search_heap(st: _Search, depth: int) -> np.ndarray:
+    """Candidate bounds of the next `depth` decisions in heap order: index 1
+    is st's query, 2i / 2i+1 the next query after node i is accepted /
+    rejected; NaN where the search has ended.  Full bisection subtrees are
+    built with vectorised numpy (the same float ops and the same numpy exp as
+    the scalar state machine -- bit-identical); other shapes step the state
+    machine node by node."""
+    n = 1 << depth
+    cand = np.full(n, np.nan)
+    if st.stage == "bis" and st.step + depth <= STEPS:
+        lo = np.array([st.lo], dtype=np.float64)
+        hi = np.array([st.hi], dtype=np.float64)
+        for lvl in range(depth):
+            mid = 0.5 * (lo + hi)
+            cand[1 << lvl:2 << lvl] = np.exp(mid)
+            lo, hi = np.stack([mid, lo], axis=1).reshape(-1), np.stack([hi, mid], axis=1).reshape(-1)
+        return cand
+    nodes = [None] * n
+    nodes[1] = st
+    for i in range(1, n):
+        q = nodes[i]
+        if q is None or q.stage == "done":
+            continue
+        cand[i] = float(q.query())
+        if 2 * i < n:
+            nodes[2 * i] = q.advance(True)
+            nodes[2 * i + 1] = q.advance(False)
+    return cand
 
 
 # ---------------------------------------------------------------------------
@@ -458,43 +469,43 @@ def compress_device(f0: torch.Tensor, specs, dgrid: DeviceGrid, cfg, timer: Time
             states.append(_Search("done", eb_hi_s, result=(eb_hi_s, True)))
         else:
             states.append(_Search("hi", eb_hi_s))
-    n_cand = 2 ** LOOKAHEAD - 1
+    n_nodes = 1 << LOOKAHEAD
     rounds = 0
-    fail = T("fail", (S, n_cand), i32)
+    fail = T("fail", (S, LOOKAHEAD), i32)
+    zero_start = None
     while any(st is not None and st.stage != "done" for st in states):
         rounds += 1
-        trees, cand = [], np.zeros((S, n_cand))
+        cand = np.full((S, n_nodes), np.nan)
         cnt_act = np.zeros(S, dtype=np.int32)
         for s, st in enumerate(states):
-            tree = _search_tree(st, LOOKAHEAD) if (st is not None and st.stage != "done") \
-                else ([], st)
-            trees.append(tree)
-            for c, nd in enumerate(tree[0]):
-                cand[s, c] = float(nd[0].query())
-            cnt_act[s] = int(cnt_h[s]) if tree[0] else 0
-        # two launches: the smallest-range images first (they fail the large
-        # bounds), then the rest against whatever bounds are still open
-        head = np.minimum(cnt_act, np.maximum(64, cnt_act // 16)).astype(np.int32)
-        off_a = np.concatenate([[0], np.cumsum(head)]).astype(np.int32)
-        off_b = np.concatenate([[0], np.cumsum(cnt_act - head)]).astype(np.int32)
+            if st is not None and st.stage != "done":
+                cand[s] = _search_heap(st, LOOKAHEAD)
+                cnt_act[s] = int(cnt_h[s])
+        off = np.concatenate([[0], np.cumsum(cnt_act)]).astype(np.int32)
         cand_d = ws.stage(cand)
-        off_a_d = ws.stage(off_a)
-        off_b_d = ws.stage(off_b)
-        start_a = ws.stage(np.zeros(S, dtype=np.int32))
-        start_b = ws.stage(head)
+        off_d = ws.stage(off)
+        if zero_start is None:
+            zero_start = ws.stage(np.zeros(S, dtype=np.int32))
         ws.flush()
         fail.zero_()
-        call("mlk_probe", f0, stats, sh_d, S, dgrid.addr, W, L, cents, K, codes, sel_rng, off_a_d,
-             start_a, int(off_a[-1]), rbound, cfg.tau, cand_d, n_cand, fail)
-        call("mlk_probe", f0, stats, sh_d, S, dgrid.addr, W, L, cents, K, codes, sel_rng, off_b_d,
-             start_b, int(off_b[-1]), rbound, cfg.tau, cand_d, n_cand, fail)
+        for level in range(LOOKAHEAD):
+            call("mlk_probe", f0, stats, sh_d, S, dgrid.addr, W, L, cents, K, codes, sel_rng,
+                 off_d, zero_start, int(off[-1]), rbound, cfg.tau, cand_d, n_nodes, level, fail,
+                 LOOKAHEAD)
         (fail_h,) = _d2h(fail)
-        for s, (nodes, ref) in enumerate(trees):
-            if not nodes:
+        for s, st in enumerate(states):
+            if st is None or st.stage == "done":
                 continue
-            while isinstance(ref, int):
-                ref = nodes[ref][1] if fail_h[s, ref] == 0 else nodes[ref][2]
-            states[s] = ref
+            node = 1
+            for level in range(LOOKAHEAD):
+                if st.stage == "done":
+                    break
+                if st.query() != cand[s, node]:
+                    raise AssertionError("lookahead tree out of step with the search")
+                ok = fail_h[s, level] == 0
+                st = st.advance(ok)
+                node = 2 * node + (0 if ok else 1)
+            states[s] = st
     eb = [0.0] * S
     lossless = [False] * S
     for s, st in enumerate(states):
