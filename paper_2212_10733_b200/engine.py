@@ -28,7 +28,7 @@ from .errors import ConfigError, FormatError, SizeMismatchError
 
 SPAN = 2.0 ** -20
 STEPS = 20
-LOOKAHEAD = 6          # bisection levels per host round trip (one probe launch each)
+LOOKAHEAD = 8         # bisection levels per host round trip (one probe launch each)
 _PAYLOAD_HEAD = struct.Struct("<BHHd")
 
 
@@ -161,34 +161,86 @@ class _Search:
         return self
 
 
-def _search_heap(st: _Search, depth: int) -> np.ndarray:
-    """Candidate bounds of the next `depth` decisions in heap order: index 1
-    is st's query, 2i / 2i+1 the next query after node i is accepted /
-    rejected; NaN where the search has ended.  Full bisection subtrees are
-    built with vectorised numpy (the same float ops and the same numpy exp as
-    the scalar state machine -- bit-identical); other shapes step the state
-    machine node by node."""
+@functools.lru_cache(maxsize=64)
+def _heap_shape(code: int, step: int, has_best: bool, depth: int):
+    """Tree shape of the next `depth` search decisions from a root of the
+    given (stage code, bisection step, best-found): per level the node kinds
+    and, for the level below, where each child's (lo, hi) comes from in
+    [parent lo | parent mid | parent hi | log(eb_hi 2^-20) | log(eb_hi)]."""
+    NONE, HI, BIS, LOW = 0, 1, 2, 3
+    kind = np.array([code], dtype=np.int8)
+    best = np.array([has_best])
+    levels = []
+    for lvl in range(depth):
+        m = kind.size
+        if lvl + 1 == depth:
+            levels.append((kind, None, None))
+            break
+        k2, best2 = np.repeat(kind, 2), np.repeat(best, 2)
+        par = np.repeat(np.arange(m), 2)
+        acc = np.zeros(2 * m, dtype=bool)
+        acc[0::2] = True
+        lo_src, hi_src = par.copy(), 2 * m + par  # default: inherit (lo, hi)
+        nk = np.full(2 * m, NONE, dtype=np.int8)
+        hrej = (k2 == HI) & ~acc                 # hi rejected -> bisection over [lo0, hi0]
+        nk[hrej] = BIS
+        lo_src[hrej], hi_src[hrej], best2[hrej] = 3 * m, 3 * m + 1, False
+        bis = k2 == BIS                          # accepted -> (mid, hi); rejected -> (lo, mid)
+        ba, br = bis & acc, bis & ~acc
+        lo_src[ba], best2[ba] = m + par[ba], True
+        hi_src[br] = m + par[br]
+        nk[bis] = BIS
+        if (kind == BIS).any():                  # low: either outcome ends the search
+            step += 1
+            if step == STEPS:                    # settle: done with the best bound, else low
+                nk[bis & best2] = NONE
+                nk[bis & ~best2] = LOW
+        elif (kind == HI).any():
+            step = 0
+        levels.append((kind, lo_src, hi_src))
+        kind, best = nk, best2
+    return tuple(levels)
+
+
+def _search_heap(states, depth: int) -> np.ndarray:
+    """Candidate bounds of the next `depth` decisions of each search, in heap
+    order: column 1 is the state's query, 2i / 2i+1 the next query after node
+    i is accepted / rejected; NaN where the search has ended.  Built level by
+    level with vectorised numpy over all searches that share a tree shape --
+    the same float operations and the same numpy exp/log as the scalar state
+    machine, hence bit-identical values (compress_device re-checks every
+    node it walks against _Search.query)."""
     n = 1 << depth
-    cand = np.full(n, np.nan)
-    if st.stage == "bis" and st.step + depth <= STEPS:
-        lo = np.array([st.lo], dtype=np.float64)
-        hi = np.array([st.hi], dtype=np.float64)
-        for lvl in range(depth):
-            mid = 0.5 * (lo + hi)
-            cand[1 << lvl:2 << lvl] = np.exp(mid)
-            lo, hi = np.stack([mid, lo], axis=1).reshape(-1), np.stack([hi, mid], axis=1).reshape(-1)
-        return cand
-    nodes = [None] * n
-    nodes[1] = st
-    for i in range(1, n):
-        q = nodes[i]
-        if q is None or q.stage == "done":
+    out = np.full((len(states), n), np.nan)
+    codes = {"done": 0, "hi": 1, "bis": 2, "low": 3}
+    groups = {}
+    for i, st in enumerate(states):
+        sig = (codes[st.stage], st.step if st.stage == "bis" else 0, st.best is not None)
+        groups.setdefault(sig, []).append(i)
+    for (code, step, has_best), rows in groups.items():
+        if code == 0:
             continue
-        cand[i] = float(q.query())
-        if 2 * i < n:
-            nodes[2 * i] = q.advance(True)
-            nodes[2 * i + 1] = q.advance(False)
-    return cand
+        sts = [states[i] for i in rows]
+        eb_hi = np.array([st.eb_hi for st in sts], dtype=np.float64)[:, None]
+        ends = np.concatenate([np.log(eb_hi * SPAN), np.log(eb_hi)], axis=1)
+        low_q = eb_hi * SPAN
+        lo = np.array([[st.lo if code == 2 else 0.0] for st in sts], dtype=np.float64)
+        hi = np.array([[st.hi if code == 2 else 0.0] for st in sts], dtype=np.float64)
+        cand = np.full((len(rows), n), np.nan)
+        for lvl, (kind, lo_src, hi_src) in enumerate(_heap_shape(code, step, has_best, depth)):
+            mid = 0.5 * (lo + hi)
+            q = cand[:, 1 << lvl:2 << lvl]
+            b = kind == 2
+            if b.any():
+                q[:, b] = np.exp(mid[:, b])
+            q[:, kind == 1] = eb_hi
+            q[:, kind == 3] = low_q
+            if lo_src is None:
+                break
+            src = np.concatenate([lo, mid, hi, ends], axis=1)
+            lo, hi = src[:, lo_src], src[:, hi_src]
+        out[rows] = cand
+    return out
 
 
 # ---------------------------------------------------------------------------
@@ -475,12 +527,14 @@ def compress_device(f0: torch.Tensor, specs, dgrid: DeviceGrid, cfg, timer: Time
     zero_start = None
     while any(st is not None and st.stage != "done" for st in states):
         rounds += 1
-        cand = np.full((S, n_nodes), np.nan)
         cnt_act = np.zeros(S, dtype=np.int32)
+        live = []
         for s, st in enumerate(states):
             if st is not None and st.stage != "done":
-                cand[s] = _search_heap(st, LOOKAHEAD)
+                live.append(s)
                 cnt_act[s] = int(cnt_h[s])
+        cand = np.full((S, n_nodes), np.nan)
+        cand[live] = _search_heap([states[s] for s in live], LOOKAHEAD)
         off = np.concatenate([[0], np.cumsum(cnt_act)]).astype(np.int32)
         cand_d = ws.stage(cand)
         off_d = ws.stage(off)

@@ -1,0 +1,87 @@
+"""Host-side logic of the device pipeline (no GPU needed)."""
+
+from __future__ import annotations
+
+import numpy as np
+
+from paper_2212_10733_b200 import engine as E
+
+
+def _scalar_heap(st, depth):
+    n = 1 << depth
+    cand = np.full(n, np.nan)
+    nodes = [None] * n
+    nodes[1] = st
+    for i in range(1, n):
+        q = nodes[i]
+        if q is None or q.stage == "done":
+            continue
+        cand[i] = float(q.query())
+        if 2 * i < n:
+            nodes[2 * i] = q.advance(True)
+            nodes[2 * i + 1] = q.advance(False)
+    return cand
+
+
+def test_search_heap_matches_the_scalar_bisection():
+    """The vectorised lookahead tree equals residual.find_error_bound's
+    sequence of candidate bounds (residual.py:129-173) on every path."""
+    rng = np.random.default_rng(0)
+    seen = set()
+    roots = []
+    for _ in range(60):
+        st = E._Search("hi", float(rng.uniform(1e-3, 1e15)))
+        for _ in range(int(rng.integers(0, 24))):
+            if st.stage == "done":
+                break
+            st = st.advance(bool(rng.integers(0, 2)))
+        roots.append(st)
+    low = E._Search("hi", 3.0)
+    while low.stage != "low":
+        low = low.advance(False)  # every bound rejected: the final lossless probe
+    roots.append(low)
+    for st in roots:
+        if st.stage == "done":
+            continue
+        seen.add(st.stage)
+        for depth in (1, 2, 5, 8):
+            a, b = E._search_heap([st], depth)[0], _scalar_heap(st, depth)
+            assert np.array_equal(np.isnan(a), np.isnan(b))
+            assert np.array_equal(a[~np.isnan(a)], b[~np.isnan(b)])
+    assert {"hi", "bis", "low"} <= seen
+
+
+def test_search_walk_reaches_the_reference_bound():
+    """Walking the heap with a monotone pass predicate gives the bound the
+    sequential bisection returns."""
+    for eb_hi, thr in [(1.0, 0.3), (5e9, 1e3), (1.0, 2.0), (1.0, 1e-9)]:
+        st = E._Search("hi", eb_hi)
+        seq = st
+        while seq.stage != "done":
+            seq = seq.advance(float(seq.query()) <= thr)
+        while st.stage != "done":
+            cand = E._search_heap([st], E.LOOKAHEAD)[0]
+            node = 1
+            for _ in range(E.LOOKAHEAD):
+                if st.stage == "done":
+                    break
+                assert st.query() == cand[node]
+                ok = cand[node] <= thr
+                st = st.advance(ok)
+                node = 2 * node + (0 if ok else 1)
+        assert st.result == seq.result
+
+
+def test_search_heap_groups_many_searches():
+    rng = np.random.default_rng(1)
+    sts = []
+    for _ in range(12):
+        st = E._Search("hi", float(rng.uniform(1e-3, 1e15)))
+        for _ in range(int(rng.integers(0, 3))):
+            st = st.advance(False)
+        sts.append(st)
+    got = E._search_heap(sts, 7)
+    for row, st in zip(got, sts):
+        want = _scalar_heap(st, 7)
+        assert np.array_equal(np.isnan(row), np.isnan(want))
+        assert np.array_equal(row[~np.isnan(row)], want[~np.isnan(want)])
