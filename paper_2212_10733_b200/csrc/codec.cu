@@ -57,7 +57,7 @@ namespace wz {
 
 struct Lay {
     int nmax, T, direct;  // direct: a 32K-entry table indexed by the hash
-    int win, p1, p4, hash, trees, hist, obuf, total;
+    int win, p1, p4, hash, trees, hist, total;
 };
 
 __host__ __device__ inline int pow2ge(int x) {
@@ -113,46 +113,6 @@ __device__ __forceinline__ int match_len(const uint8_t* win, int p, int c) {
     return z6::MAX_MATCH;
 }
 
-// sequential bit writer into a shared u64 buffer (lane 0 only)
-struct SBit {
-    unsigned long long* w;
-    long long bit;
-    __device__ void bits(unsigned value, int len) {
-        if (!len) return;
-        const long long q = bit >> 6;
-        const int sh = (int)(bit & 63);
-        w[q] |= (unsigned long long)value << sh;
-        if (sh + len > 64) w[q + 1] |= (unsigned long long)value >> (64 - sh);
-        bit += len;
-    }
-};
-
-struct GBit {  // lane-0 bit writer into global memory
-    uint8_t* out;
-    long long cap, pos;
-    unsigned long long acc;
-    int nacc;
-    bool overflow;
-    __device__ void put_byte(unsigned b) {
-        if (pos < cap) out[pos] = (uint8_t)b;
-        else overflow = true;
-        ++pos;
-    }
-    __device__ void bits(unsigned value, int len) {
-        acc |= (unsigned long long)value << nacc;
-        nacc += len;
-        while (nacc >= 8) {
-            put_byte((unsigned)(acc & 0xff));
-            acc >>= 8;
-            nacc -= 8;
-        }
-    }
-    __device__ void windup() {
-        if (nacc > 0) put_byte((unsigned)(acc & 0xff));
-        acc = 0;
-        nacc = 0;
-    }
-};
 
 // ---- Huffman construction (trees.c build_tree / gen_bitlen / gen_codes),
 // warp-cooperative where the result does not depend on order.  The heap is
@@ -393,11 +353,28 @@ __device__ void send_tree_d(const DTrees& W, const DTree<NL>& t, BO& bo) {
     }
 }
 
+// bit writers straight into the (zeroed) global output: `bit` counts from
+// the 8-byte-aligned word at or below the stream's first byte, so only OR
+// operations touch words shared with a neighbouring stream's bytes
+struct GBits {
+    unsigned long long* w;
+    long long bit;
+    __device__ void bits(unsigned value, int len) {  // single lane
+        if (!len) return;
+        const long long q = bit >> 6;
+        const int sh = (int)(bit & 63);
+        atomicOr(w + q, (unsigned long long)value << sh);
+        if (sh + len > 64) atomicOr(w + q + 1, (unsigned long long)value >> (64 - sh));
+        bit += len;
+    }
+};
+
 // Per-warp shared memory: the window, then one region reused by phase:
 //   chain build  : p1 | hash table (u16 entries, aliasing where p4 will go)
 //   matching     : p1 | p4
-//   flush        : Huffman trees | u32 symbol histogram / output bit buffer
-// The symbol buffer lives in global scratch.
+//   flush        : Huffman trees | u32 symbol histogram
+// The symbol buffer lives in global scratch; the bit stream is OR-ed into
+// the zeroed global output.
 __host__ __device__ inline Lay layout(int nmax) {
     Lay L;
     L.nmax = nmax;
@@ -414,9 +391,7 @@ __host__ __device__ inline Lay layout(int nmax) {
                                                                           : al16(2 * L.T));
     L.trees = b0;
     L.hist = b0 + al16((int)sizeof(DTrees));
-    L.obuf = L.hist;
-    const int tail = al16(nmax + 256) > 4 * 320 ? al16(nmax + 256) : 4 * 320;
-    const int flush = al16((int)sizeof(DTrees)) + tail;
+    const int flush = al16((int)sizeof(DTrees)) + 4 * 320;
     o += chains > flush ? chains : flush;
     L.total = o;
     return L;
@@ -424,6 +399,7 @@ __host__ __device__ inline Lay layout(int nmax) {
 
 }  // namespace wz
 
+template <bool PROF>
 __global__ void __launch_bounds__(512)
 k_deflate_warp(const uint8_t* __restrict__ in, const long long* __restrict__ in_off,
                const long long* __restrict__ in_len, int n_streams, uint8_t* __restrict__ out,
@@ -452,7 +428,7 @@ k_deflate_warp(const uint8_t* __restrict__ in, const long long* __restrict__ in_
         if (n <= nmin || n > nmax) continue;  // another tier handles it
         const uint8_t* src = in + in_off[s];
         uint8_t* sym = sym_g + (long long)s * sym_cap;
-        long long t_0 = clock64();
+        long long t_0 = PROF ? clock64() : 0;
         // ---- window + zero pad, Adler-32 (lane-parallel sums)
         unsigned long long sa = 0, sb = 0;
         for (int i = lane; i < n; i += 32) {
@@ -470,7 +446,7 @@ k_deflate_warp(const uint8_t* __restrict__ in, const long long* __restrict__ in_
         const unsigned ad_b = (unsigned)(((unsigned long long)n + sb) % 65521ull);
         for (int i = lane; i < Ly.T; i += 32) htab[i] = 0;
         __syncwarp();
-        long long t_1 = clock64();
+        long long t_1 = PROF ? clock64() : 0;
         // ---- prev[] (hash chains), 32 positions per step.  Table entries
         //      are position + 1; a probed entry's key is re-derived from the
         //      window (no key storage), direct mode indexes by the hash.
@@ -524,7 +500,7 @@ k_deflate_warp(const uint8_t* __restrict__ in, const long long* __restrict__ in_
             }
             __syncwarp();
         }
-        long long t_2 = clock64();
+        long long t_2 = PROF ? clock64() : 0;
         for (int p = lane; p < n; p += 32)
             if (p >= n_ins) p1[p] = 0;
         __syncwarp();
@@ -536,7 +512,7 @@ k_deflate_warp(const uint8_t* __restrict__ in, const long long* __restrict__ in_
             p4[p] = (uint16_t)x;
         }
         __syncwarp();
-        long long t_3 = clock64();
+        long long t_3 = PROF ? clock64() : 0;
         long long t_lm = 0;
         int n_calls = 0, n_rounds = 0, n_cands = 0;
         // ---- deflate_slow, warp-uniform state
@@ -573,8 +549,8 @@ k_deflate_warp(const uint8_t* __restrict__ in, const long long* __restrict__ in_
             match_length = z6::MIN_MATCH - 1;
             if (hash_head != 0 && prev_length < z6::LAZY &&
                 strstart - hash_head <= z6::MAX_DIST) {
-                const long long tlm0 = clock64();
-                ++n_calls;
+                const long long tlm0 = PROF ? clock64() : 0;
+                if (PROF) ++n_calls;
                 const int chain = prev_length >= z6::GOOD ? z6::CHAIN / 4 : z6::CHAIN;
                 const int nice = lookahead < z6::NICE ? lookahead : z6::NICE;
                 const int thr = nice > prev_length + 1 ? nice : prev_length + 1;
@@ -593,8 +569,10 @@ k_deflate_warp(const uint8_t* __restrict__ in, const long long* __restrict__ in_
                         best = mx;
                     }
                     const unsigned alive = __ballot_sync(FULL, valid);
-                    ++n_rounds;
-                    n_cands += __popc(hit ? (alive & (0xffffffffu >> (31 - upto))) : alive);
+                    if (PROF) {
+                        ++n_rounds;
+                        n_cands += __popc(hit ? (alive & (0xffffffffu >> (31 - upto))) : alive);
+                    }
                     if (hit || alive != FULL) break;
                     cb = __shfl_sync(FULL, c ? (int)p1[c] : 0, 31);
                     if (cb == 0) break;
@@ -604,7 +582,7 @@ k_deflate_warp(const uint8_t* __restrict__ in, const long long* __restrict__ in_
                 if (match_length <= 5 && match_length == z6::MIN_MATCH &&
                     strstart - match_start > z6::TOO_FAR)
                     match_length = z6::MIN_MATCH - 1;
-                t_lm += clock64() - tlm0;
+                if (PROF) t_lm += clock64() - tlm0;
             }
             if (prev_length >= z6::MIN_MATCH && match_length <= prev_length) {
                 if (lane == 0) {
@@ -643,10 +621,9 @@ k_deflate_warp(const uint8_t* __restrict__ in, const long long* __restrict__ in_
             sym_next += 3;
         }
         __syncwarp();
-        long long t_4 = clock64();
+        long long t_4 = PROF ? clock64() : 0;
         // ---- trees (lane 0) + bit stream (all lanes); prev tables are dead now
         wz::DTrees& t = *trees;
-        unsigned long long* ob = reinterpret_cast<unsigned long long*>(base + Ly.obuf);
         unsigned* hist = reinterpret_cast<unsigned*>(base + Ly.hist);
         __shared__ int sh_kind[16];
         __shared__ long long sh_hbits[16];
@@ -678,9 +655,15 @@ k_deflate_warp(const uint8_t* __restrict__ in, const long long* __restrict__ in_
         }
         __syncwarp();
         wz::build_tree_warp(t, t.bt, 2, tb);
-        const int obw = (n + 256) / 8;  // u64 words available (histogram + heap are dead)
-        for (int i = lane; i < obw; i += 32) ob[i] = 0ull;
+        // ---- output: zero the stream's bytes (it is at most n + 11 long),
+        //      then OR the bit stream into them
+        uint8_t* dst = out + out_off[s];
+        const long long zlim = (long long)n + 16 < out_cap ? (long long)n + 16 : out_cap;
+        for (long long i = lane; i < zlim; i += 32) dst[i] = 0;
         __syncwarp();
+        unsigned long long* gw =
+            reinterpret_cast<unsigned long long*>(reinterpret_cast<uintptr_t>(dst) & ~(uintptr_t)7);
+        const long long bit0 = (long long)(reinterpret_cast<uintptr_t>(dst) & 7) * 8;
         if (lane == 0) {
             int max_blindex;
             for (max_blindex = z6::BL_CODES - 1; max_blindex >= 3; max_blindex--)
@@ -689,7 +672,8 @@ k_deflate_warp(const uint8_t* __restrict__ in, const long long* __restrict__ in_
             uint64_t opt_lenb = (t.opt_len + 3 + 7) >> 3;
             const uint64_t static_lenb = (t.static_len + 3 + 7) >> 3;
             if (static_lenb <= opt_lenb) opt_lenb = static_lenb;
-            wz::SBit sb{ob, 16};  // after the 2-byte zlib header
+            wz::GBits sb{gw, bit0};
+            sb.bits(0x9c78u, 16);  // zlib header: deflate, 32K window, level 6
             int kind;
             if ((uint64_t)strstart + 4 <= opt_lenb) {
                 kind = 0;  // stored
@@ -715,18 +699,17 @@ k_deflate_warp(const uint8_t* __restrict__ in, const long long* __restrict__ in_
         __syncwarp();
         const int kind = sh_kind[warp];
         long long bitpos = sh_hbits[warp];
-        long long nbytes;
+        long long nbytes;  // from dst, header included
         if (kind == 0) {
             // stored block: windup, LEN, NLEN, raw bytes
-            const long long b0 = (bitpos + 7) >> 3;
-            uint8_t* ob8 = reinterpret_cast<uint8_t*>(ob);
+            const long long b0 = (bitpos - bit0 + 7) >> 3;
             if (lane == 0) {
-                ob8[b0] = (uint8_t)strstart;
-                ob8[b0 + 1] = (uint8_t)(strstart >> 8);
-                ob8[b0 + 2] = (uint8_t)~strstart;
-                ob8[b0 + 3] = (uint8_t)(~strstart >> 8);
+                dst[b0] = (uint8_t)strstart;
+                dst[b0 + 1] = (uint8_t)(strstart >> 8);
+                dst[b0 + 2] = (uint8_t)~strstart;
+                dst[b0 + 3] = (uint8_t)(~strstart >> 8);
             }
-            for (int i = lane; i < strstart; i += 32) ob8[b0 + 4 + i] = win[i];
+            for (int i = lane; i < strstart; i += 32) dst[b0 + 4 + i] = win[i];
             nbytes = b0 + 4 + strstart;
         } else {
             const uint16_t* lcode = kind == 1 ? tb.sl_code : t.lt.code;
@@ -772,43 +755,37 @@ k_deflate_warp(const uint8_t* __restrict__ in, const long long* __restrict__ in_
                     const long long at = bitpos + inc - nb;
                     const long long q = at >> 6;
                     const int sh = (int)(at & 63);
-                    atomicOr(ob + q, val << sh);
-                    if (sh + nb > 64) atomicOr(ob + q + 1, val >> (64 - sh));
+                    atomicOr(gw + q, val << sh);
+                    if (sh + nb > 64) atomicOr(gw + q + 1, val >> (64 - sh));
                 }
                 bitpos += __shfl_sync(FULL, inc, 31);
             }
             __syncwarp();
             if (lane == 0) {
-                wz::SBit sb{ob, bitpos};
+                wz::GBits sb{gw, bitpos};
                 sb.bits(lcode[z6::END_BLOCK], llen[z6::END_BLOCK]);
                 bitpos = sb.bit;
             }
             bitpos = __shfl_sync(FULL, bitpos, 0);
-            nbytes = (bitpos + 7) >> 3;
+            nbytes = (bitpos - bit0 + 7) >> 3;
         }
         __syncwarp();
-        // ---- zlib header + body + Adler-32 to global memory
-        {
-            const uint8_t* ob8 = reinterpret_cast<const uint8_t*>(ob);
-            uint8_t* dst = out + out_off[s];
+        // ---- Adler-32 trailer
+        if (lane == 0) {
             const long long total = nbytes + 4;
             if (total > out_cap) {
-                if (lane == 0) out_len[s] = -1;
+                out_len[s] = -1;
             } else {
-                for (long long i = lane; i < nbytes; i += 32)
-                    dst[i] = i == 0 ? 0x78 : (i == 1 ? 0x9c : ob8[i]);
                 const unsigned ad = (ad_b << 16) | ad_a;
-                if (lane == 0) {
-                    dst[nbytes] = ad >> 24;
-                    dst[nbytes + 1] = (ad >> 16) & 0xff;
-                    dst[nbytes + 2] = (ad >> 8) & 0xff;
-                    dst[nbytes + 3] = ad & 0xff;
-                    out_len[s] = total;
-                }
+                dst[nbytes] = ad >> 24;
+                dst[nbytes + 1] = (ad >> 16) & 0xff;
+                dst[nbytes + 2] = (ad >> 8) & 0xff;
+                dst[nbytes + 3] = ad & 0xff;
+                out_len[s] = total;
             }
         }
-        if (lane == 0) {
-            if (prof) {
+        if (PROF && lane == 0) {
+            {
                 long long t_5 = clock64();
                 (void)t_5;
                 atomicAdd(prof + 0, (unsigned long long)(t_1 - t_0));
@@ -862,12 +839,19 @@ extern "C" int mlk_zlib_compress6_warp(const uint8_t* in, const int64_t* in_off,
     zw = zw < 1 ? 1 : (zw > 16 ? 16 : zw);
     size_t sm = (size_t)zw * Ly.total;
     if (sm > 227 * 1024) return MLK_ERR_CONFIG;
-    cudaFuncSetAttribute(k_deflate_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    k_deflate_warp<<<n_blocks, 32 * zw, sm, stream>>>(
-        in, reinterpret_cast<const long long*>(in_off), reinterpret_cast<const long long*>(in_len),
-        n, out, reinterpret_cast<const long long*>(out_off), (long long)out_cap,
-        reinterpret_cast<long long*>(out_len), nmin, nmax, sym_scratch, (long long)sym_cap,
-        reinterpret_cast<unsigned long long*>(prof));
+#define MLK_DW_LAUNCH(P)                                                                        \
+    cudaFuncSetAttribute(k_deflate_warp<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); \
+    k_deflate_warp<P><<<n_blocks, 32 * zw, sm, stream>>>(                                        \
+        in, reinterpret_cast<const long long*>(in_off), reinterpret_cast<const long long*>(in_len), \
+        n, out, reinterpret_cast<const long long*>(out_off), (long long)out_cap,                  \
+        reinterpret_cast<long long*>(out_len), nmin, nmax, sym_scratch, (long long)sym_cap,        \
+        reinterpret_cast<unsigned long long*>(prof))
+    if (prof) {
+        MLK_DW_LAUNCH(true);
+    } else {
+        MLK_DW_LAUNCH(false);
+    }
+#undef MLK_DW_LAUNCH
     return cudaGetLastError() == cudaSuccess ? MLK_OK : MLK_ERR_CUDA;
 }
 
