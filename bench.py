@@ -322,6 +322,11 @@ def main():
     total_hist = ds.n_planes * ds.n_nodes
     value = total_hist / (ms / 1e3)
     stage_ms = {k: 1e3 * v / args.steps for k, v in stage_sum.items()}
+    stage_by_rank = None
+    if world > 1:
+        gathered = [None] * world
+        dist.all_gather_object(gathered, {k: round(v, 3) for k, v in stage_ms.items()})
+        stage_by_rank = gathered
 
     # rooflines from the stage intervals of the timed loop (CUDA events on the
     # launching stream) and each kernel's algorithmic bytes per step
@@ -395,7 +400,8 @@ def main():
                            "tau": args.tau, "lambda": "f32", "parallelism": f"shards/{world}",
                            "l2": "inputs 1.6 GB > 126 MB L2 (no flush needed)"},
                 "raw_gb_s": value * HIST_BYTES / 1e9,
-                "wall_ms_per_step": wall_ms, "stage_ms": stage_ms, "probe_rounds": probe_rounds,
+                "wall_ms_per_step": wall_ms, "stage_ms": stage_ms,
+                "stage_ms_by_rank": stage_by_rank, "probe_rounds": probe_rounds,
                 "newton": newton, "roofline": roofline, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e,
                 "decompress_and_report": dec, "gpu_launches": launches,
                 "clocks": clk.summary(),

@@ -268,6 +268,18 @@ int mlk_compare(const double* a, const double* b, int32_t total, const MlkGrid* 
                 double* err, double* sse, double* qa, double* qb, double* ext,
                 cudaStream_t stream);
 
+/* HOST function: walk one shard's residual section (pipeline.py:140-156 and
+ * the payload header of residual.py:81-98) over host memory `sec` (len
+ * bytes).  For entry k: idx (image index), body_off = base + offset of its
+ * zlib stream within sec, body_len, eb and mode from the payload header.
+ * Returns MLK_ERR_FORMAT with *why = 1 truncated, 2 trailing bytes,
+ * 3 payload shorter than its header, 4 payload dims != (rows, cols),
+ * 5 unknown mode, 6 image index >= n_images, 7 more than cap entries. */
+int mlk_parse_residual_section(const uint8_t* sec, int64_t len, int32_t n_images, int32_t rows,
+                               int32_t cols, int64_t base, int32_t cap, int32_t* idx,
+                               int64_t* body_off, int64_t* body_len, double* eb, uint8_t* mode,
+                               int32_t* count_out, int32_t* why);
+
 /* ---- shard-blob assembly on device (container.py:90-95, pipeline.py:116-184) */
 
 /* list[img_off + r] = r-th image of shard s (ascending) with flags & mask;

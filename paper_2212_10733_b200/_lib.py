@@ -76,6 +76,8 @@ _SIGS = {
     "mlk_select": [_P, _P, _P, _I32, _I32, _P, _P, _I32, _I32, _P, _D, _P, _P, _P, _P, _P],
     "mlk_recheck": [_P, _P, _P, _I32, _I32, _P, _P, _I32, _P, _I32, _P, _D, _P, _P, _P],
     "mlk_compact": [_P, _P, _P, _I32, _D, _P, _P, _P, _P, _P, _P],
+    "mlk_parse_residual_section": [_P, _I64, _I32, _I32, _I32, _I64, _I32, _P, _P, _P, _P, _P,
+                                   _P, _P],
     "mlk_probe": [_P, _P, _P, _I32, _P, _P, _I32, _P, _I32, _P, _P, _P, _P, _I32, _P, _D, _P,
                   _I32, _I32, _P, _I32, _P],
     "mlk_project": [_P, _P, _P, _P, _I32, _I32, _P, _P, _I32, _P, _I32, _P, _P, _P, _P, _P,

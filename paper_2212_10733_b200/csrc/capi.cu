@@ -1,6 +1,7 @@
 // capi.cu -- library info, the pairwise plan, and the reference operator API
 // (mlk/kernels.py:20-32) as batched device entry points.
 #include <cstdio>
+#include <cstring>
 
 #include "common.cuh"
 
@@ -225,4 +226,55 @@ extern "C" int mlk_unpack_indices(const uint8_t* buf, int64_t count, int32_t bit
     if (count <= 0) return MLK_OK;
     k_unpack<<<(unsigned)((count + 255) / 256), 256, 0, stream>>>(buf, count, bits, out);
     return cudaGetLastError() == cudaSuccess ? MLK_OK : MLK_ERR_CUDA;
+}
+
+// ---------------------------------------------------------------------------
+// Host-side walk of one shard's residual section (pipeline.py:140-156 +
+// the BuiltinCodec payload header, residual.py:81-98): `<dI` (eb, count),
+// then per entry `<II` (image index, payload length) + payload, where a
+// payload is `<BHHd` (mode, rows, cols, eb) + the zlib stream.  The entries
+// are a length-linked chain, so this walk is sequential; it runs on the
+// host over the archive bytes (no copies) and hands the device the zlib
+// body offsets.  Offsets are returned relative to `sec` + base.
+// why: 1 truncated, 2 trailing bytes, 3 payload shorter than its header,
+// 4 payload dims, 5 unknown mode, 6 image index out of range, 7 > cap.
+extern "C" int mlk_parse_residual_section(const uint8_t* sec, int64_t len, int32_t n_images,
+                                          int32_t rows, int32_t cols, int64_t base,
+                                          int32_t cap, int32_t* idx, int64_t* body_off,
+                                          int64_t* body_len, double* eb, uint8_t* mode,
+                                          int32_t* count_out, int32_t* why) {
+    auto rd32 = [&](int64_t o) {
+        uint32_t v;
+        memcpy(&v, sec + o, 4);
+        return v;
+    };
+    *why = 0;
+    *count_out = 0;
+    if (len < 12) { *why = 1; return MLK_ERR_FORMAT; }
+    const uint32_t count = rd32(8);
+    int64_t off = 12;
+    for (uint32_t k = 0; k < count; ++k) {
+        if (off + 8 > len) { *why = 1; return MLK_ERR_FORMAT; }
+        const uint32_t i = rd32(off), ln = rd32(off + 4);
+        off += 8;
+        if ((int64_t)ln > len - off) { *why = 1; return MLK_ERR_FORMAT; }
+        if (ln < 13) { *why = 3; return MLK_ERR_FORMAT; }
+        if ((int64_t)k >= cap) { *why = 7; return MLK_ERR_FORMAT; }
+        const uint8_t m = sec[off];
+        uint16_t r, c;
+        memcpy(&r, sec + off + 1, 2);
+        memcpy(&c, sec + off + 3, 2);
+        if (r != rows || c != cols) { *why = 4; return MLK_ERR_FORMAT; }
+        if (m > 1) { *why = 5; return MLK_ERR_FORMAT; }
+        if (i >= (uint32_t)n_images) { *why = 6; return MLK_ERR_FORMAT; }
+        idx[k] = (int32_t)i;
+        mode[k] = m;
+        memcpy(eb + k, sec + off + 5, 8);
+        body_off[k] = base + off + 13;
+        body_len[k] = (int64_t)ln - 13;
+        off += ln;
+    }
+    if (off != len) { *why = 2; return MLK_ERR_FORMAT; }
+    *count_out = (int32_t)count;
+    return MLK_OK;
 }

@@ -21,7 +21,7 @@ from dataclasses import dataclass, field
 import numpy as np
 import torch
 
-from . import _lib
+from . import _lib, hostio
 from ._lib import MlkGrid, MlkNewton, MlkShard, call
 from .decomp import mix_seed
 from .errors import ConfigError, FormatError, SizeMismatchError
@@ -824,96 +824,205 @@ def _unzigzag_host(z):
     return ((z >> np.uint64(1)) ^ (np.uint64(0) - (z & np.uint64(1)))).astype(np.int64)
 
 
-def decompress_device(preamble, shards, blobs, dev) -> np.ndarray:
-    """Decode every shard blob on `dev`; returns the (P, N, R, C) array."""
+_WHY = {1: "residual section truncated", 2: "residual section has trailing bytes",
+        3: "residual payload shorter than its header",
+        4: "residual payload dims do not match the shard",
+        5: "unknown residual payload mode", 6: "residual entry image index out of range",
+        7: "residual section lists more entries than images"}
+
+
+@dataclass
+class DecodedArchive:
+    """An archive decoded on the device (pipeline.py:397-440)."""
+
+    preamble: object
+    shards: list
+    out: torch.Tensor          # (P*N*D) float64 on the device, dataset order
+    specs: list
+    table: object
+    sh_d: torch.Tensor
+    W: torch.Tensor
+    cents: torch.Tensor
+    codes: torch.Tensor
+    L: int
+    K: int
+    lam_bytes: int
+    dgrid: "DeviceGrid"
+
+
+def decode_archive(archive, dev) -> DecodedArchive:
+    """Parse and decode a whole archive on `dev`.
+
+    The host reads only the preamble, the shard index, the 44-byte shard
+    headers, the small weight / codebook sections and the residual entry
+    chain (mlk_parse_residual_section, in place over the archive bytes);
+    the archive goes to the device in one pinned copy and every per-image
+    byte -- codes, lambdas, zlib bodies, exception images -- is read there."""
     from .autoencoder import AEModel
-    from .container import read_shard
+    from .container import HEADER_SIZE, SECTIONS, ArchivePreamble, ShardHeader
+    from .decomp import partition
     from .quantizer import PQCodebook
 
-    P, N = preamble.n_planes, preamble.n_nodes
-    rows, cols = preamble.grid.rows, preamble.grid.cols
+    raw = memoryview(archive).cast("B")
+    pre, off = ArchivePreamble.unpack(archive)
+    n_sh = pre.n_shards
+    if len(raw) < off + 8 * n_sh:
+        raise FormatError("archive shard index truncated")
+    offs = list(struct.unpack_from(f"<{n_sh}Q", raw, off)) + [len(raw)]
+    shards = partition(pre.n_planes, pre.n_nodes, n_sh, pre.decomp_mode)
+    if len(shards) != n_sh:
+        raise FormatError("archive shard count disagrees with the partition")
+    P, N = pre.n_planes, pre.n_nodes
+    rows, cols = pre.grid.rows, pre.grid.cols
     D = rows * cols
-    metas = []
-    for shard, blob in zip(shards, blobs):
-        sb = read_shard(blob)
-        h = sb.header
-        if h.n_images != len(shard.members):
+    heads, secs = [], []
+    for i in range(n_sh):
+        a_, b_ = offs[i], offs[i + 1]
+        if not (off + 8 * n_sh <= a_ < b_ <= len(raw)):
+            raise FormatError(f"corrupt shard offset index at entry {i}")
+        h = ShardHeader.unpack(raw[a_:a_ + HEADER_SIZE])
+        if b_ - a_ != HEADER_SIZE + sum(h.section_lengths):
+            raise FormatError(f"shard {i} length disagrees with its header")
+        if h.n_images != len(shards[i].members):
             raise FormatError("shard image count disagrees with the partition")
         if (h.img_rows, h.img_cols) != (rows, cols):
             raise FormatError("shard image dims disagree with the archive grid")
-        metas.append((shard, sb))
-    L = metas[0][1].header.latent_dim
-    bits = metas[0][1].header.pq_bits
+        o, d = a_ + HEADER_SIZE, {}
+        for name, ln in zip(SECTIONS, h.section_lengths):
+            d[name] = (o, ln)
+            o += ln
+        heads.append(h)
+        secs.append(d)
+    L, bits = heads[0].latent_dim, heads[0].pq_bits
     K = 1 << bits
-    if any(sb.header.latent_dim != L or sb.header.pq_bits != bits for _, sb in metas):
+    if any(h.latent_dim != L or h.pq_bits != bits for h in heads):
         raise FormatError("mixed latent/codebook shapes across shards are not supported")
-    dgrid = DeviceGrid(preamble.grid, dev, L)
-    models, cents, codes_l, lamq_l = [], [], [], []
-    res_slot_l, res_codes_l, res_eb_l, res_mode_l = [], [], [], []
-    exc_slot_l, exc_img_l = [], []
-    n_res = n_exc = 0
-    for shard, sb in metas:
-        h, sec = sb.header, sb.sections
+    lam_bytes = heads[-1].lambda_precision
+    if any(h.lambda_precision != lam_bytes for h in heads):
+        raise FormatError("mixed lambda precisions across shards are not supported")
+    so = _lib.lib()
+    arr = np.frombuffer(archive, dtype=np.uint8)
+    base_ptr = arr.ctypes.data
+    models, cents = [], []
+    res_idx, res_off, res_len, res_eb, res_mode, res_shard = [], [], [], [], [], []
+    exc_idx, exc_src, exc_cnt = [], [], []
+    cnt = ctypes.c_int32()
+    why = ctypes.c_int32()
+    for s, (h, d) in enumerate(zip(heads, secs)):
         n = h.n_images
-        models.append(AEModel.from_bytes(sec["weights"], L, D))
-        cents.append(PQCodebook.from_bytes(sec["pq_table"], L, K).centroids)
-        total_codes = n * L
-        if len(sec["codes"]) != (total_codes * bits + 7) // 8:
-            raise SizeMismatchError(f"code stream is {len(sec['codes'])} bytes, expected "
-                                    f"{(total_codes * bits + 7) // 8}")
-        cbuf = torch.from_numpy(np.frombuffer(sec["codes"], dtype=np.uint8).copy()).to(dev)
-        idx = torch.empty(total_codes, dtype=torch.int16, device=dev)
-        call("mlk_unpack_indices", cbuf, total_codes, bits, idx)
-        codes_l.append(idx)
-        dt = "<f4" if h.lambda_precision == 4 else "<f8"
-        if len(sec["lambdas"]) != n * 8 * h.lambda_precision:
+        wo, wl = d["weights"]
+        models.append(AEModel.from_bytes(bytes(raw[wo:wo + wl]), L, D))
+        po, pl = d["pq_table"]
+        cents.append(PQCodebook.from_bytes(bytes(raw[po:po + pl]), L, K).centroids)
+        if d["codes"][1] != (n * L * bits + 7) // 8:
+            raise SizeMismatchError(f"code stream is {d['codes'][1]} bytes, expected "
+                                    f"{(n * L * bits + 7) // 8}")
+        if d["lambdas"][1] != n * 8 * h.lambda_precision:
             raise FormatError("lambda section length mismatch")
-        lamq_l.append(np.frombuffer(sec["lambdas"], dtype=dt).reshape(n, 8).astype(np.float64))
-        slot = np.full(n, -1, dtype=np.int32)
-        from .pipeline import _parse_exceptions, _parse_residuals
-        for i, payload in _parse_residuals(sec["residuals"], n, rows, cols):
-            if len(payload) < _PAYLOAD_HEAD.size:
-                raise FormatError("residual payload shorter than its header")
-            mode, r, c, eb = _PAYLOAD_HEAD.unpack_from(payload, 0)
-            if (r, c) != (rows, cols):
-                raise FormatError("residual payload dims do not match the shard")
-            if mode not in (0, 1):
-                raise FormatError(f"unknown residual payload mode {mode}")
-            raw = payload[_PAYLOAD_HEAD.size:]
-            res_codes_l.append(raw)
-            res_eb_l.append(eb)
-            res_mode_l.append(mode)
-            slot[i] = n_res
-            n_res += 1
-        res_slot_l.append(slot)
-        eidx, eimg = _parse_exceptions(sec["exceptions"], D)
-        es = np.full(n, -1, dtype=np.int32)
-        es[eidx] = np.arange(n_exc, n_exc + len(eidx), dtype=np.int32)
-        n_exc += len(eidx)
-        exc_slot_l.append(es)
-        exc_img_l.append(eimg)
-    # zlib bodies -> device inflate -> device varint decode
+        ro, rl = d["residuals"]
+        cap = n
+        idx = np.empty(cap, np.int32)
+        bo = np.empty(cap, np.int64)
+        bl = np.empty(cap, np.int64)
+        eb = np.empty(cap, np.float64)
+        md = np.empty(cap, np.uint8)
+        rc = so.mlk_parse_residual_section(
+            ctypes.c_void_p(base_ptr + ro), rl, n, rows, cols, ro, cap,
+            idx.ctypes.data, bo.ctypes.data, bl.ctypes.data, eb.ctypes.data, md.ctypes.data,
+            ctypes.byref(cnt), ctypes.byref(why))
+        if rc != 0:
+            raise FormatError(_WHY.get(why.value, "corrupt residual section"))
+        k = cnt.value
+        res_idx.append(idx[:k])
+        res_off.append(bo[:k])
+        res_len.append(bl[:k])
+        res_eb.append(eb[:k])
+        res_mode.append(md[:k])
+        res_shard.append(np.full(k, s, np.int32))
+        eo, el = d["exceptions"]
+        if el < 4:
+            raise FormatError("exceptions section truncated")
+        ne = struct.unpack_from("<I", raw, eo)[0]
+        rec = 4 + 8 * D
+        if el != 4 + ne * rec:
+            raise FormatError("exceptions section truncated" if el < 4 + ne * rec
+                              else "exceptions section has trailing bytes")
+        if ne:
+            starts = eo + 4 + rec * np.arange(ne, dtype=np.int64)
+            ei = np.frombuffer(archive, np.uint8, ne * rec, eo + 4).reshape(ne, rec)[:, :4]
+            exc_idx.append(np.ascontiguousarray(ei).view("<u4").reshape(-1).astype(np.int64))
+            exc_src.append(starts + 4)
+        exc_cnt.append(ne)
+    n_res = sum(len(x) for x in res_idx)
+    n_exc = int(sum(exc_cnt))
+    arc_d = hostio.upload_bytes(archive, dev)
     i64 = dict(dtype=torch.int64, device=dev)
+    specs = shard_layout(shards, models, N, rows, cols)
+    table = _shard_table(specs, D, L)
+    img_off = np.array([t.img_off for t in table], dtype=np.int64)
+    total = sum(sp.n_img for sp in specs)
+    ws = Workspace.get(dev)
+    ws.reset()
+    # per-image slots and the small host-built tables, one staged copy
+    res_slot = np.full(total, -1, np.int32)
     if n_res:
-        lens = np.array([len(r) for r in res_codes_l], dtype=np.int64)
-        offs = np.concatenate([[0], np.cumsum(lens)[:-1]]).astype(np.int64)
-        blob = np.frombuffer(b"".join(res_codes_l), dtype=np.uint8).copy()
-        zin = torch.from_numpy(blob if blob.size else np.zeros(1, np.uint8)).to(dev)
+        gi = np.concatenate([img_off[s] + res_idx[s] for s in range(n_sh)])
+        res_slot[gi] = np.arange(n_res, dtype=np.int32)
+    exc_slot = np.full(total, -1, np.int32)
+    if n_exc:
+        shard_of = np.repeat(np.arange(n_sh), exc_cnt)
+        gi = img_off[shard_of] + np.concatenate(exc_idx)
+        if np.any(np.concatenate(exc_idx) >= np.repeat([h.n_images for h in heads], exc_cnt)):
+            raise FormatError("exception index out of range")
+        exc_slot[gi] = np.arange(n_exc, dtype=np.int32)
+    sh_d = ws.stage(np.frombuffer(bytes(table), dtype=np.uint8))
+    W = ws.stage(np.stack([m.weights for m in models]).astype(np.float32))
+    cents_d = ws.stage(np.stack(cents))
+    res_slot_d = ws.stage(res_slot)
+    exc_slot_d = ws.stage(exc_slot)
+    lam_seg = ws.stage(np.array([d["lambdas"][0] for d in secs], np.int64))
+    lam_len = ws.stage(np.array([d["lambdas"][1] for d in secs], np.int64))
+    lam_dst = ws.stage(np.concatenate([[0], np.cumsum([d["lambdas"][1] for d in secs])[:-1]])
+                       .astype(np.int64))
+    if n_res:
+        body_off = ws.stage(np.concatenate(res_off))
+        body_len = ws.stage(np.concatenate(res_len))
+        res_eb_d = ws.stage(np.concatenate(res_eb))
+        res_mode_d = ws.stage(np.concatenate(res_mode))
+    if n_exc:
+        ex_src = ws.stage(np.concatenate(exc_src))
+        ex_len = ws.stage(np.full(n_exc, 8 * D, np.int64))
+        ex_dst = ws.stage(8 * D * np.arange(n_exc, dtype=np.int64))
+    ws.flush()
+    # codes straight from the archive
+    codes16 = ws.tensor("dec_codes16", (total * L,), torch.int16)
+    for s, (h, d) in enumerate(zip(heads, secs)):
+        co = d["codes"][0]
+        o = int(img_off[s]) * L
+        call("mlk_unpack_indices", arc_d.data_ptr() + co, h.n_images * L, bits,
+             codes16.data_ptr() + 2 * o)
+    codes = ws.tensor("dec_codes", (total * L,), torch.uint8)
+    codes.copy_(codes16)
+    # lambda section -> aligned -> float64
+    lam_raw = ws.tensor("dec_lamraw", (total * 8 * lam_bytes,), torch.uint8)
+    call("mlk_gather_segments", arc_d, lam_seg, lam_len, n_sh, lam_raw, lam_dst)
+    lamq = lam_raw.view(torch.float32 if lam_bytes == 4 else torch.float64).to(torch.float64)
+    # zlib bodies -> device inflate -> device varint decode
+    if n_res:
         icap = 10 * D + 64
-        raw_d = torch.empty(n_res * icap, dtype=torch.uint8, device=dev)
+        raw_d = ws.tensor("dec_inflate", (n_res * icap,), torch.uint8)
         raw_off = torch.arange(0, n_res * icap, icap, **i64)
-        raw_len = torch.empty(n_res, **i64)
-        call("mlk_zlib_decompress", zin, torch.from_numpy(offs).to(dev),
-             torch.from_numpy(lens).to(dev), n_res, raw_d, raw_off, icap, raw_len)
-        rl = raw_len.cpu().numpy()
-        if np.any(rl < 0):
-            raise FormatError("corrupt residual stream")
-        vals = torch.empty(n_res * D, dtype=torch.int64, device=dev)
-        consumed = torch.empty(n_res, **i64)
+        raw_len = ws.tensor("dec_rawlen", (n_res,), torch.int64)
+        call("mlk_zlib_decompress", arc_d, body_off, body_len, n_res, raw_d, raw_off, icap,
+             raw_len)
+        vals = ws.tensor("dec_vals", (n_res * D,), torch.int64)
+        consumed = ws.tensor("dec_consumed", (n_res,), torch.int64)
         call("mlk_varint_decode_batch", raw_d, raw_off, raw_len, n_res,
              torch.full((n_res,), D, **i64), vals, torch.arange(0, n_res * D, D, **i64),
              consumed)
-        con = consumed.cpu().numpy()
+        rl, con = _d2h(raw_len, consumed)
+        if np.any(rl < 0):
+            raise FormatError("corrupt residual stream")
         if np.any(con == -1):
             raise FormatError("varint stream truncated")
         if np.any(con == -2):
@@ -921,24 +1030,29 @@ def decompress_device(preamble, shards, blobs, dev) -> np.ndarray:
         if np.any(con != rl):
             raise FormatError("residual stream has trailing bytes")
     else:
-        vals = torch.zeros(1, dtype=torch.int64, device=dev)
-    specs = shard_layout(shards, models, N, rows, cols)
-    table = _shard_table(specs, D, L)
-    sh_d = _upload_shards(table, dev)
-    total = sum(sp.n_img for sp in specs)
-    W = torch.from_numpy(np.stack([m.weights for m in models]).astype(np.float32)).to(dev)
-    cents_d = torch.from_numpy(np.stack(cents)).to(dev)
-    codes_d = torch.cat(codes_l).to(torch.uint8)
-    lamq = torch.from_numpy(np.concatenate(lamq_l)).to(dev)
-    res_slot = torch.from_numpy(np.concatenate(res_slot_l)).to(dev)
-    res_eb = torch.tensor(res_eb_l or [0.0], dtype=torch.float64, device=dev)
-    res_mode = torch.tensor(res_mode_l or [0], dtype=torch.uint8, device=dev)
-    exc_slot = torch.from_numpy(np.concatenate(exc_slot_l)).to(dev)
-    exc_img = torch.from_numpy(np.concatenate(exc_img_l) if n_exc else np.zeros((1, D))).to(dev)
+        vals = torch.zeros(1, **i64)
+        res_eb_d = torch.zeros(1, dtype=torch.float64, device=dev)
+        res_mode_d = torch.zeros(1, dtype=torch.uint8, device=dev)
+    exc_img = ws.tensor("dec_exc", (max(1, n_exc) * D,), torch.float64)
+    if n_exc:
+        call("mlk_gather_segments", arc_d, ex_src, ex_len, n_exc, exc_img.view(torch.uint8),
+             ex_dst)
+    dgrid = DeviceGrid(pre.grid, dev, L)
     out = torch.empty(P * N * D + 2, dtype=torch.float64, device=dev)
-    call("mlk_decode", sh_d, len(specs), total, dgrid.addr, W, L, cents_d, K, codes_d, res_slot,
-         vals, res_eb, res_mode, lamq, exc_slot, exc_img, 1e-12, out)
-    return out[:P * N * D].cpu().numpy().reshape(P, N, rows, cols)
+    call("mlk_decode", sh_d, len(specs), total, dgrid.addr, W, L, cents_d, K, codes, res_slot_d,
+         vals, res_eb_d, res_mode_d, lamq, exc_slot_d, exc_img, 1e-12, out)
+    return DecodedArchive(preamble=pre, shards=shards, out=out, specs=specs, table=table,
+                          sh_d=sh_d, W=W, cents=cents_d, codes=codes, L=L, K=K,
+                          lam_bytes=lam_bytes, dgrid=dgrid)
+
+
+def decompress_device(archive, dev) -> np.ndarray:
+    """Decode an archive on `dev`; returns the (P, N, R, C) array."""
+    dec = decode_archive(archive, dev)
+    pre = dec.preamble
+    g = pre.grid
+    return hostio.download_array(dec.out[:pre.n_planes * pre.n_nodes * g.rows * g.cols],
+                                 (pre.n_planes, pre.n_nodes, g.rows, g.cols))
 
 
 def shard_layout(shards, models, n_nodes, rows, cols, node_lo=0):
@@ -955,19 +1069,15 @@ def shard_layout(shards, models, n_nodes, rows, cols, node_lo=0):
     return out
 
 
-def evaluate_device(orig, rec, preamble, blobs, dev) -> dict:
-    """Per-image AE errors, final errors and moments for evaluate()."""
-    from .autoencoder import AEModel
-    from .container import read_shard
-    from .decomp import partition
-    from .quantizer import PQCodebook
-
+def evaluate_device(orig, dec: DecodedArchive, dev) -> dict:
+    """Per-image final errors, AE-only errors and moments for evaluate(),
+    against the archive decoded on the device (no host round trip)."""
     P, N = orig.n_planes, orig.n_nodes
     D = orig.grid.rows * orig.grid.cols
     total = P * N
-    dgrid = DeviceGrid(orig.grid, dev)
-    a = upload_flat(orig.data, dev)
-    b = upload_flat(rec.data, dev)
+    dgrid = dec.dgrid
+    a = hostio.upload_planes(np.ascontiguousarray(orig.data, dtype=np.float64), dev)
+    b = dec.out
     f64 = dict(dtype=torch.float64, device=dev)
     err = torch.empty(total, **f64)
     sse = torch.empty(total, **f64)
@@ -975,37 +1085,17 @@ def evaluate_device(orig, rec, preamble, blobs, dev) -> dict:
     qb = torch.empty((total, 4), **f64)
     ext = torch.empty((total, 2), **f64)
     call("mlk_compare", a, b, total, dgrid.addr, err, sse, qa, qb, ext)
-    # AE-only errors through the exact recheck kernel
-    shards = partition(P, N, preamble.n_shards, preamble.decomp_mode)
-    models, cents, codes_l = [], [], []
-    L = K = bits = None
-    for blob in blobs:
-        sb = read_shard(blob)
-        h = sb.header
-        L, bits = h.latent_dim, h.pq_bits
-        K = 1 << bits
-        models.append(AEModel.from_bytes(sb.sections["weights"], L, D))
-        cents.append(PQCodebook.from_bytes(sb.sections["pq_table"], L, K).centroids)
-        cb = torch.from_numpy(np.frombuffer(sb.sections["codes"], np.uint8).copy()).to(dev)
-        idx = torch.empty(h.n_images * L, dtype=torch.int16, device=dev)
-        call("mlk_unpack_indices", cb, h.n_images * L, bits, idx)
-        codes_l.append(idx)
-    specs = shard_layout(shards, models, N, orig.grid.rows, orig.grid.cols)
-    table = _shard_table(specs, D, L)
-    sh_d = _upload_shards(table, dev)
-    W = torch.from_numpy(np.stack([m.weights for m in models]).astype(np.float32)).to(dev)
-    cents_d = torch.from_numpy(np.stack(cents)).to(dev)
-    codes_d = torch.cat(codes_l).to(torch.uint8)
-    stats = torch.zeros((total, 4), **f64)
-    order = np.concatenate([np.fromiter((p * N + x for p, x in sh.members), dtype=np.int64)
-                            for sh in shards])
+    # AE-only errors through the exact recheck kernel (shard order)
+    from .decomp import shard_dataset_index
+    order = np.concatenate([shard_dataset_index(sh, N) for sh in dec.shards])
     order_d = torch.from_numpy(order).to(dev)
+    stats = torch.zeros((total, 4), **f64)
     stats[:, 0] = ext[order_d, 0]
     stats[:, 1] = ext[order_d, 1]
     flags = torch.full((total,), 4, dtype=torch.uint8, device=dev)
     ae = torch.empty(total, **f64)
-    call("mlk_recheck", a, stats, sh_d, len(specs), total, dgrid.addr, W, L, cents_d, K,
-         codes_d, preamble.tau, flags, ae)
+    call("mlk_recheck", a, stats, dec.sh_d, len(dec.specs), total, dgrid.addr, dec.W, dec.L,
+         dec.cents, dec.K, dec.codes, dec.preamble.tau, flags, ae)
     span = float(ext[:, 0].max() - ext[:, 1].min())
     pd = float(np.sqrt(float(sse.sum()) / orig.data.size) / span) if span > 0 else 0.0
     ae_h = np.empty(total)
@@ -1014,8 +1104,3 @@ def evaluate_device(orig, rec, preamble, blobs, dev) -> dict:
             "q_rec": qb.cpu().numpy(), "pd_nrmse": pd, "ae_err": ae_h}
 
 
-def upload_flat(data: np.ndarray, dev) -> torch.Tensor:
-    n = data.size
-    buf = torch.empty(n + 2, dtype=torch.float64, device=dev)
-    buf[:n].copy_(torch.from_numpy(np.ascontiguousarray(data).reshape(-1)))
-    return buf

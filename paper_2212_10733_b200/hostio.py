@@ -22,7 +22,8 @@ from concurrent.futures import ThreadPoolExecutor
 import numpy as np
 import torch
 
-__all__ = ["upload_planes", "download_bytes", "download_view", "pinned"]
+__all__ = ["upload_planes", "upload_bytes", "download_bytes", "download_view", "download_array",
+           "pinned"]
 
 CHUNK = 64 << 20
 _POOL = None
@@ -138,3 +139,87 @@ def download_view(src: torch.Tensor, nbytes: int) -> np.ndarray:
         stage[:nbytes].copy_(src[:nbytes], non_blocking=True)
         torch.cuda.current_stream(src.device).synchronize()
     return stage.numpy()[:nbytes]
+
+
+def upload_bytes(raw, dev) -> torch.Tensor:
+    """A bytes-like object -> device uint8 tensor (pinned staging, chunked)."""
+    src = np.frombuffer(raw, dtype=np.uint8)
+    n = src.size
+    buf = torch.empty(max(n, 1), dtype=torch.uint8, device=dev)
+    if n == 0:
+        return buf
+    stage = pinned(f"upb{dev.index}", n)
+    last = _LAST_UPLOAD.get(("b", dev.index))
+    if last is not None:
+        last.synchronize()
+    st_np = stage.numpy()
+    spans = [(a, min(n, a + CHUNK)) for a in range(0, n, CHUNK)]
+
+    def fill(span):
+        a, b = span
+        st_np[a:b] = src[a:b]
+        return span
+
+    cs = _copy_stream(dev)
+    cs.wait_stream(torch.cuda.current_stream(dev))
+    with torch.cuda.stream(cs):
+        for a, b in _pool().map(fill, spans):
+            buf[a:b].copy_(stage[a:b], non_blocking=True)
+    ev = torch.cuda.Event()
+    ev.record(cs)
+    _LAST_UPLOAD[("b", dev.index)] = ev
+    torch.cuda.current_stream(dev).wait_event(ev)
+    buf.record_stream(cs)
+    return buf
+
+
+_MADV_HUGEPAGE = 14
+_libc = None
+
+
+def _advise_huge(arr: np.ndarray):
+    """Ask for transparent huge pages on a fresh large array (fewer faults)."""
+    global _libc
+    try:
+        if _libc is None:
+            _libc = ctypes.CDLL(None, use_errno=True)
+        a = arr.ctypes.data
+        lo = (a + (2 << 20) - 1) & ~((2 << 20) - 1)
+        hi = (a + arr.nbytes) & ~((2 << 20) - 1)
+        if hi > lo:
+            _libc.madvise(ctypes.c_void_p(lo), ctypes.c_size_t(hi - lo), _MADV_HUGEPAGE)
+    except Exception:
+        pass
+
+
+def download_array(src: torch.Tensor, shape, dtype=np.float64) -> np.ndarray:
+    """Device tensor -> a fresh numpy array: chunked async D2H into pinned
+    memory overlapped with thread-parallel copies into the result."""
+    dev = src.device
+    out = np.empty(shape, dtype=dtype)
+    nbytes = out.nbytes
+    if nbytes == 0:
+        return out
+    _advise_huge(out)
+    flat = out.reshape(-1).view(np.uint8)
+    s8 = src.reshape(-1).view(torch.uint8)[:nbytes]
+    stage = pinned(f"dla{dev.index}", nbytes)
+    st_np = stage.numpy()
+    cs = _copy_stream(dev)
+    cs.wait_stream(torch.cuda.current_stream(dev))
+    spans = [(a, min(nbytes, a + CHUNK)) for a in range(0, nbytes, CHUNK)]
+    events = []
+    with torch.cuda.stream(cs):
+        for a, b in spans:
+            stage[a:b].copy_(s8[a:b], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(cs)
+            events.append(ev)
+
+    def cp(k):
+        a, b = spans[k]
+        events[k].synchronize()
+        flat[a:b] = st_np[a:b]
+
+    list(_pool().map(cp, range(len(spans))))
+    return out

@@ -21,7 +21,7 @@ import torch
 from . import engine, hostio
 from ._lib import F_EXCEPTION, F_EXC_OVERFLOW, F_NONFINITE, F_SELECTED
 from .autoencoder import AEModel
-from .container import ArchivePreamble, archive_offsets, read_archive, read_shard
+from .container import ArchivePreamble, archive_offsets
 from .decomp import SelectionScheme, partition, shard_dataset_index
 from .errors import ConfigError, FormatError, SizeMismatchError
 from .fdata import FDataset, dataset_nbytes
@@ -272,62 +272,29 @@ def build_report(ds, archive, outs, tau, stage_t, wall) -> ErrorReport:
 # ---------------------------------------------------------------------------
 # decompress (pipeline.py:397-440)
 
-def _parse_residuals(raw: bytes, n_img: int, rows: int, cols: int):
-    if len(raw) < 12:
-        raise FormatError("residual section truncated")
-    _, count = struct.unpack_from("<dI", raw, 0)
-    off, entries = 12, []
-    for _ in range(count):
-        if off + 8 > len(raw):
-            raise FormatError("residual section truncated")
-        idx, ln = struct.unpack_from("<II", raw, off)
-        off += 8
-        entries.append((idx, raw[off:off + ln]))
-        off += ln
-    if off != len(raw):
-        raise FormatError("residual section has trailing bytes")
-    return entries
-
-
-def _parse_exceptions(raw: bytes, D: int):
-    if len(raw) < 4:
-        raise FormatError("exceptions section truncated")
-    count = struct.unpack_from("<I", raw, 0)[0]
-    if len(raw) != 4 + count * (4 + 8 * D):
-        if len(raw) < 4 + count * (4 + 8 * D):
-            raise FormatError("exceptions section truncated")
-        raise FormatError("exceptions section has trailing bytes")
-    rec = np.frombuffer(raw, dtype=np.uint8, offset=4).reshape(count, 4 + 8 * D)
-    idx = rec[:, :4].copy().view("<u4").reshape(-1).astype(np.int64)
-    imgs = rec[:, 4:].copy().view("<f8").reshape(count, D)
-    return idx, imgs
-
-
 def decompress(archive: bytes) -> FDataset:
     """Invert compress(); exception images are reproduced verbatim."""
-    preamble, blobs = read_archive(archive)
-    shards = partition(preamble.n_planes, preamble.n_nodes, preamble.n_shards,
-                       preamble.decomp_mode)
-    dev = _device()
-    data = engine.decompress_device(preamble, shards, blobs, dev)
-    return FDataset(grid=preamble.grid, data=data, timestep=preamble.timestep)
+    pre, _ = ArchivePreamble.unpack(archive)
+    data = engine.decompress_device(archive, _device())
+    return FDataset(grid=pre.grid, data=data, timestep=pre.timestep)
 
 
 def evaluate(orig: FDataset, archive: bytes) -> ErrorReport:
     """Decompress and fill a full error report with gate verdicts (pipeline.py:443-491)."""
     t0 = time.perf_counter()
-    preamble, blobs = read_archive(archive)
+    preamble, _ = ArchivePreamble.unpack(archive)
     if (preamble.n_planes, preamble.n_nodes) != (orig.n_planes, orig.n_nodes) or \
             (preamble.grid.rows, preamble.grid.cols) != (orig.grid.rows, orig.grid.cols):
         raise ConfigError("archive dimensions do not match the dataset")
-    rec = decompress(archive)
+    dev = _device()
+    dec = engine.decode_archive(archive, dev)
+    torch.cuda.synchronize(dev)
     decode_time = time.perf_counter() - t0
     t1 = time.perf_counter()
-    ev = engine.evaluate_device(orig, rec, preamble, blobs, _device())
-    lam_bytes = read_shard(blobs[-1]).header.lambda_precision
+    ev = engine.evaluate_device(orig, dec, dev)
     qerr, qmax = qoi_nrmse_from_moments(ev["q_orig"], ev["q_rec"])
     tau = preamble.tau
-    gate = QOI_GATES["f32" if lam_bytes == 4 else "f64"]
+    gate = QOI_GATES["f32" if dec.lam_bytes == 4 else "f64"]
     per_image = ev["per_image"]
     ae = ev["ae_err"]
     fin = np.where(np.isfinite(ae), ae, np.inf)

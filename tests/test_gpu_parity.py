@@ -278,3 +278,37 @@ def test_device_zlib_matches_host_zlib():
     for i, s in enumerate(streams):
         got = comp[off[i]:off[i] + ln[i]].tobytes()
         assert got == zlib.compress(s, 6), i
+
+
+def test_evaluate_agrees_with_the_compress_report():
+    meta, _ = G.load("small")
+    ds, same = G.corpus("small")
+    if not same:
+        pytest.skip("host generates a different corpus")
+    cfg = _cfg(meta["runs"][0])
+    arc, rep, _ = mb.compress(ds, cfg, mb.TimestepState(models=_models("small"),
+                                                        timestep_index=1))
+    ev = mb.evaluate(ds, arc)
+    np.testing.assert_allclose(ev.per_image_nrmse, rep.per_image_nrmse, rtol=1e-12, atol=0)
+    assert ev.compression_ratio == rep.compression_ratio
+    assert ev.gates["pd_per_image"] and ev.gates["qoi"]
+    assert abs(ev.pd_nrmse - rep.pd_nrmse) <= 1e-9 * rep.pd_nrmse
+    for k, v in rep.qoi_nrmse.items():
+        assert abs(ev.qoi_nrmse[k] - v) <= 1e-6 * max(v, 1e-30)
+
+
+def test_decompress_rejects_corrupt_archives():
+    from paper_2212_10733_b200.errors import FormatError
+    meta, _ = G.load("tiny")
+    ds, same = G.corpus("tiny")
+    if not same:
+        pytest.skip("host generates a different corpus")
+    cfg = _cfg(meta["runs"][0])
+    arc, _, _ = mb.compress(ds, cfg, mb.TimestepState(models=_models("tiny"), timestep_index=1))
+    with pytest.raises(FormatError):
+        mb.decompress(arc[:-7])
+    pre, off = container.ArchivePreamble.unpack(arc)
+    bad = bytearray(arc)
+    bad[off:off + 8] = (len(arc) + 5).to_bytes(8, "little")  # shard offset past the end
+    with pytest.raises(FormatError):
+        mb.decompress(bytes(bad))
