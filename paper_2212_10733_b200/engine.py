@@ -279,8 +279,23 @@ class CompressOut:
 
     def host(self, name):
         if name not in self._host:
-            self._host[name] = self.dev[name].cpu().numpy()
+            self.fetch(name)
         return self._host[name]
+
+    def fetch(self, *names):
+        """Bring several per-image arrays to the host with one copy."""
+        need = [n for n in names if n not in self._host]
+        if not need:
+            return
+        ts = [self.dev[n].contiguous() for n in need]
+        flat = torch.cat([t.reshape(-1).view(torch.uint8) for t in ts])
+        raw = hostio.download_view(flat, flat.numel())
+        pos = 0
+        for n, t in zip(need, ts):
+            nb = t.numel() * t.element_size()
+            dt = torch.empty((), dtype=t.dtype).numpy().dtype
+            self._host[n] = raw[pos:pos + nb].view(dt).reshape(tuple(t.shape)).copy()
+            pos += nb
 
     def blobs(self) -> list:
         raw = self.blob_buf.cpu().numpy().tobytes()
@@ -1047,12 +1062,16 @@ def decode_archive(archive, dev) -> DecodedArchive:
 
 
 def decompress_device(archive, dev) -> np.ndarray:
-    """Decode an archive on `dev`; returns the (P, N, R, C) array."""
+    """Decode an archive on `dev`; returns the (P, N, R, C) array.  Raises
+    ConfigError, like FDataset (fdata.py:70-103), if a value is negative --
+    checked on the device, so the host never rescans the array."""
     dec = decode_archive(archive, dev)
     pre = dec.preamble
     g = pre.grid
-    return hostio.download_array(dec.out[:pre.n_planes * pre.n_nodes * g.rows * g.cols],
-                                 (pre.n_planes, pre.n_nodes, g.rows, g.cols))
+    vals = dec.out[:pre.n_planes * pre.n_nodes * g.rows * g.cols]
+    if bool((vals < 0).any()):
+        raise ConfigError("histogram values must be non-negative")
+    return hostio.download_array(vals, (pre.n_planes, pre.n_nodes, g.rows, g.cols))
 
 
 def shard_layout(shards, models, n_nodes, rows, cols, node_lo=0):

@@ -102,6 +102,25 @@ def upload_planes(data: np.ndarray, dev, node_range=None, pad_elems: int = 2) ->
     return buf
 
 
+_MADV_HUGEPAGE = 14
+_libc = None
+
+
+def _advise_huge(arr: np.ndarray):
+    """Ask for transparent huge pages on a fresh large array (fewer faults)."""
+    global _libc
+    try:
+        if _libc is None:
+            _libc = ctypes.CDLL(None, use_errno=True)
+        a = arr.ctypes.data
+        lo = (a + (2 << 20) - 1) & ~((2 << 20) - 1)
+        hi = (a + arr.nbytes) & ~((2 << 20) - 1)
+        if hi > lo:
+            _libc.madvise(ctypes.c_void_p(lo), ctypes.c_size_t(hi - lo), _MADV_HUGEPAGE)
+    except Exception:
+        pass
+
+
 _BYTES_OFF = sys.getsizeof(b"") - 1  # offset of ob_sval in a CPython bytes object
 _new_bytes = ctypes.pythonapi.PyBytes_FromStringAndSize
 _new_bytes.restype = ctypes.py_object
@@ -118,6 +137,7 @@ def download_bytes(src: torch.Tensor, nbytes: int, prefix: bytes = b"") -> bytes
     total = len(prefix) + nbytes
     out = _new_bytes(None, total)  # uninitialised; filled before anyone sees it
     view = np.ctypeslib.as_array((ctypes.c_uint8 * total).from_address(id(out) + _BYTES_OFF))
+    _advise_huge(view)
     view[:len(prefix)] = np.frombuffer(prefix, dtype=np.uint8)
     body = view[len(prefix):]
     st_np = stage.numpy()
@@ -171,25 +191,6 @@ def upload_bytes(raw, dev) -> torch.Tensor:
     torch.cuda.current_stream(dev).wait_event(ev)
     buf.record_stream(cs)
     return buf
-
-
-_MADV_HUGEPAGE = 14
-_libc = None
-
-
-def _advise_huge(arr: np.ndarray):
-    """Ask for transparent huge pages on a fresh large array (fewer faults)."""
-    global _libc
-    try:
-        if _libc is None:
-            _libc = ctypes.CDLL(None, use_errno=True)
-        a = arr.ctypes.data
-        lo = (a + (2 << 20) - 1) & ~((2 << 20) - 1)
-        hi = (a + arr.nbytes) & ~((2 << 20) - 1)
-        if hi > lo:
-            _libc.madvise(ctypes.c_void_p(lo), ctypes.c_size_t(hi - lo), _MADV_HUGEPAGE)
-    except Exception:
-        pass
 
 
 def download_array(src: torch.Tensor, shape, dtype=np.float64) -> np.ndarray:

@@ -232,6 +232,8 @@ def compress_distributed(ds: FDataset, config: PipelineConfig, state: TimestepSt
 
 def build_report(ds, archive, outs, tau, stage_t, wall) -> ErrorReport:
     """pipeline._build_report (pipeline.py:367-391) from device-side reductions."""
+    for o in outs:
+        o.fetch("flags", "ferr", "qoi", "fqoi", "stats", "fsse", "status")
     flags = np.concatenate([o.host("flags") for o in outs])
     ferr = np.concatenate([o.host("ferr") for o in outs])
     exc = (flags & F_EXCEPTION) != 0
@@ -276,7 +278,7 @@ def decompress(archive: bytes) -> FDataset:
     """Invert compress(); exception images are reproduced verbatim."""
     pre, _ = ArchivePreamble.unpack(archive)
     data = engine.decompress_device(archive, _device())
-    return FDataset(grid=pre.grid, data=data, timestep=pre.timestep)
+    return FDataset._trusted(pre.grid, data, pre.timestep)
 
 
 def evaluate(orig: FDataset, archive: bytes) -> ErrorReport:
