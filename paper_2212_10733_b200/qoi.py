@@ -35,7 +35,9 @@ def qoi_nrmse_from_moments(q_orig: np.ndarray, q_rec: np.ndarray):
     """qoi.qoi_error_report (qoi.py:122-133) from (N, 4) moment tables."""
     mask = q_orig[:, 0] > 0
     names = ("n", "u_par", "t_perp", "t_par")
-    errs = {nm: nrmse(q_orig[mask, k], q_rec[mask, k]) for k, nm in enumerate(names)}
+    qo = np.ascontiguousarray(q_orig[mask].T)  # one gather, then contiguous columns
+    qr = np.ascontiguousarray(q_rec[mask].T)
+    errs = {nm: nrmse(qo[k], qr[k]) for k, nm in enumerate(names)}
     return errs, max(errs.values())
 
 
