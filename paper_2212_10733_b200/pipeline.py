@@ -23,7 +23,8 @@ from ._lib import F_EXCEPTION, F_EXC_OVERFLOW, F_NONFINITE, F_SELECTED
 from .autoencoder import AEModel
 from .container import ArchivePreamble, archive_offsets
 from .decomp import SelectionScheme, partition, shard_dataset_index
-from .errors import ConfigError, FormatError, SizeMismatchError
+from .errors import (ConfigError, DegenerateRangeError, DimensionError, FormatError,
+                     SizeMismatchError)
 from .fdata import FDataset, dataset_nbytes
 from .lagrange import NewtonOptions, NewtonStatus
 from .qoi import ErrorReport, compression_ratio, qoi_nrmse_from_moments
@@ -231,31 +232,48 @@ def compress_distributed(ds: FDataset, config: PipelineConfig, state: TimestepSt
 
 
 def build_report(ds, archive, outs, tau, stage_t, wall) -> ErrorReport:
-    """pipeline._build_report (pipeline.py:367-391) from device-side reductions."""
-    for o in outs:
-        o.fetch("flags", "ferr", "qoi", "fqoi", "stats", "fsse", "status")
-    flags = np.concatenate([o.host("flags") for o in outs])
-    ferr = np.concatenate([o.host("ferr") for o in outs])
+    """pipeline._build_report (pipeline.py:367-391): every statistic reduced on
+    the device, one small D2H of scalars plus the per-image list (dataset
+    order, as the reference reports it)."""
+    dev = outs[0].dev["flags"].device
+    cat = lambda k: torch.cat([o.dev[k] for o in outs]) if len(outs) > 1 else outs[0].dev[k]
+    flags, ferr = cat("flags"), cat("ferr")
+    qoi, fqoi, stats = cat("qoi"), cat("fqoi"), cat("stats")
+    fsse, status = cat("fsse"), cat("status")
+    n_tot = flags.numel()
     exc = (flags & F_EXCEPTION) != 0
-    per_img_shard = np.where(exc, 0.0, ferr)
-    # per_image_nrmse is reported in dataset (plane-major) order
-    order = np.concatenate([o.dataset_index for o in outs])
-    per_image = np.empty_like(per_img_shard)
-    per_image[order] = per_img_shard
-    q_orig = np.empty((len(order), 4))
-    q_rec = np.empty((len(order), 4))
-    q_orig[order] = np.concatenate([o.host("qoi") for o in outs])
-    q_rec[order] = np.concatenate([o.host("fqoi") for o in outs])
-    qerr, qmax = qoi_nrmse_from_moments(q_orig, q_rec)
-    stats = np.concatenate([o.host("stats") for o in outs])
-    span = float(stats[:, 0].max() - stats[:, 1].min())
-    sse = float(np.concatenate([o.host("fsse") for o in outs]).sum())
+    order = torch.from_numpy(np.concatenate([o.dataset_index for o in outs])).to(dev)
+    per_image = torch.empty(n_tot, dtype=torch.float64, device=dev)
+    per_image[order] = torch.where(exc, torch.zeros_like(ferr), ferr)
+    # QoI errors over the nodes with positive density (qoi.py:122-133)
+    mask = (qoi[:, 0] > 0).unsqueeze(1)
+    d2 = torch.where(mask, (qoi - fqoi) ** 2, torch.zeros_like(qoi)).sum(0)
+    qhi = torch.where(mask, qoi, torch.full_like(qoi, -np.inf)).amax(0)
+    qlo = torch.where(mask, qoi, torch.full_like(qoi, np.inf)).amin(0)
+    scal = torch.stack([
+        stats[:, 0].max(), stats[:, 1].min(), fsse.sum(), mask.sum().to(torch.float64),
+        ((status == NewtonStatus.CONVERGED) & ((flags & F_NONFINITE) == 0)
+         & ((flags & F_EXC_OVERFLOW) == 0)).sum().to(torch.float64),
+        ((flags & (F_SELECTED | F_NONFINITE)) == 0).sum().to(torch.float64),
+        ((flags & F_SELECTED) != 0).sum().to(torch.float64),
+        exc.sum().to(torch.float64)])
+    host = torch.cat([scal, d2, qhi, qlo, per_image]).cpu().numpy()
+    dmax, dmin, sse, cnt, n_conv, ae_ok, n_sel, n_exc = host[:8]
+    d2_h, qhi_h, qlo_h = host[8:12], host[12:16], host[16:20]
+    span = float(dmax - dmin)
     pd = float(np.sqrt(sse / ds.data.size) / span) if span > 0 else 0.0
-    n_tot = len(flags)
-    status = np.concatenate([o.host("status") for o in outs])
-    n_conv = int(np.sum((status == NewtonStatus.CONVERGED) & ((flags & F_NONFINITE) == 0)
-                        & ((flags & F_EXC_OVERFLOW) == 0)))
-    ae_ok = int(np.sum((flags & (F_SELECTED | F_NONFINITE)) == 0))
+    names = ("n", "u_par", "t_perp", "t_par")
+    qerr = {}
+    for k, nm in enumerate(names):
+        rng_k = float(qhi_h[k] - qlo_h[k])
+        if cnt == 0:
+            raise DimensionError("nrmse needs two equal-length, non-empty arrays")
+        if rng_k == 0.0:
+            if d2_h[k] != 0.0:
+                raise DegenerateRangeError("reference range is zero but arrays differ")
+            qerr[nm] = 0.0
+        else:
+            qerr[nm] = float(np.sqrt(d2_h[k] / cnt) / rng_k)
     timings = {s: {"sum": 0.0, "max": 0.0} for s in _STAGES}
     for k, v in stage_t.items():
         if k in timings:
@@ -263,11 +281,11 @@ def build_report(ds, archive, outs, tau, stage_t, wall) -> ErrorReport:
     rest = max(0.0, wall - sum(v for v in stage_t.values()))
     timings["other"] = {"sum": rest, "max": rest}
     return ErrorReport(
-        pd_nrmse=pd, per_image_nrmse=per_image.tolist(), qoi_nrmse=qerr, max_qoi_nrmse=qmax,
+        pd_nrmse=pd, per_image_nrmse=host[20:].tolist(), qoi_nrmse=qerr,
+        max_qoi_nrmse=max(qerr.values()),
         compression_ratio=compression_ratio(dataset_nbytes(ds), len(archive)),
-        ae_accuracy=ae_ok / n_tot,
-        residual_fraction=int(np.sum((flags & F_SELECTED) != 0)) / n_tot,
-        convergence_fraction=n_conv / n_tot, exception_count=int(exc.sum()),
+        ae_accuracy=float(ae_ok) / n_tot, residual_fraction=float(n_sel) / n_tot,
+        convergence_fraction=float(n_conv) / n_tot, exception_count=int(n_exc),
         stage_timings=timings)
 
 
