@@ -319,7 +319,8 @@ __device__ __forceinline__ bool sep_tables(const double (&lam)[4], const NtCtx& 
 // step itself, so lambda never needs a broadcast; the next iteration's
 // exponent tables are computed by the whole block.  Two barriers per step.
 template <bool SEP>
-__device__ void newton_block(const double* fp, const MlkGrid& g, const NtCtx& X, const double* b,
+__device__ void newton_block(const double* fp, double fl, const MlkGrid& g, const NtCtx& X,
+                             const double* b,
                              double bmax, double step, int max_iter, double tol, PjCtl& C,
                              double (&lam)[4], int& status, int& iters) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -358,7 +359,7 @@ __device__ void newton_block(const double* fp, const MlkGrid& g, const NtCtx& X,
                 for (int r = g0; r < rows; r += ngrp) {
                     const bool re = (r == 0) | (r == rows - 1);
                     const double w = re ? w_ed : w_in;
-                    const double wf = w * (fp[r * cols + c] * (re ? ea1 : ea0) * ebp[r]);
+                    const double wf = w * (fmax(fp[r * cols + c], fl) * (re ? ea1 : ea0) * ebp[r]);
                     const double p2 = C.p2r[r];
                     const double w2f = w * wf, t2 = p2 * w2f;
                     G1 += wf;
@@ -382,7 +383,7 @@ __device__ void newton_block(const double* fp, const MlkGrid& g, const NtCtx& X,
                 const double a3 = __ldg(g.hmvol + j) * dv * dv * X.is4;
                 double t = l0 * a0 + l1 * a1 + l2 * a2 + l3 * a3;
                 if (fabs(t) > 700.0) { v[14] = 1.0; t = t > 0 ? 700.0 : -700.0; }
-                cell_sums(v, a0, a1, a2, a3, fp[j] * exp(-t));
+                cell_sums(v, a0, a1, a2, a3, fmax(fp[j], fl) * exp(-t));
             }
         }
         const double part = warp_rs16(v);
@@ -568,20 +569,37 @@ k_project(const double* __restrict__ f0, const double* __restrict__ stats,
         const double fj = F[j];
         nan_t |= fj != fj;
         top = fmax(top, fj);
-        const double dv = __dsub_rn(__ldg(g.vpar + j), qs[1]);
-        const double a3 = fabs(__dmul_rn(__ldg(g.hmvol + j), __dmul_rn(dv, dv)));
-        nan_a |= a3 != a3;
-        amax = fmax(amax, a3);
+    }
+    if (SEP) {
+        // a3 = hmvol * (vpar - u)^2 takes one value per (row edge, column)
+        if (tid < g.cols) {
+            const double dv = __dsub_rn(__ldg(g.vpar + tid), qs[1]);
+            const double dv2 = __dmul_rn(dv, dv);
+            const int r_in = g.rows > 2 ? 1 : 0;
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const double a3 = fabs(__dmul_rn(__ldg(g.hmvol + (e ? 0 : r_in) * g.cols + tid),
+                                                 dv2));
+                nan_a |= a3 != a3;
+                amax = fmax(amax, a3);
+            }
+        }
+    } else {
+        for (int j = tid; j < D; j += PJ_T) {
+            const double dv = __dsub_rn(__ldg(g.vpar + j), qs[1]);
+            const double a3 = fabs(__dmul_rn(__ldg(g.hmvol + j), __dmul_rn(dv, dv)));
+            nan_a |= a3 != a3;
+            amax = fmax(amax, a3);
+        }
     }
     if (nan_t) top = __longlong_as_double(0x7ff8000000000000ll);
     if (nan_a) amax = __longlong_as_double(0x7ff8000000000000ll);
     block_allmax2(top, amax, C, ph);
     const double s4 = amax;
     const double sc4 = s4 > 0 ? s4 : 1.0;
-    if (top > 0) {  // f_plus (apply keeps the corrected image otherwise); no NaN here
-        const double fl = __dmul_rn(opt.floor, top);
-        for (int j = tid; j < D; j += PJ_T) F[j] = fmax(F[j], fl);
-    }
+    // f_plus = max(corrected, floor * top) (lagrange.py:103-107) is applied on
+    // every read below when top > 0 (no NaN then); F keeps the corrected image
+    const double fl = top > 0 ? __dmul_rn(opt.floor, top) : 0.0;
     if (SEP && tid < g.cols) C.p3c[tid] /= sc4;
 
     double lam[4] = {0.0, 0.0, 0.0, 0.0};
@@ -604,8 +622,8 @@ k_project(const double* __restrict__ f0, const double* __restrict__ stats,
             X.u = qs[1];
             X.rows = g.rows;
             X.cols = g.cols;
-            __syncthreads();  // f_plus and the p3c tables
-            newton_block<SEP>(F, g, X, b, bmax, opt.step, opt.max_iter, opt.tol, C, lam, status,
+            __syncthreads();  // the p3c tables
+            newton_block<SEP>(F, fl, g, X, b, bmax, opt.step, opt.max_iter, opt.tol, C, lam, status,
                               iters);
             // warp 0 holds the result: publish its status so the retry
             // decision is block-uniform
@@ -614,7 +632,7 @@ k_project(const double* __restrict__ f0, const double* __restrict__ stats,
             if (opt.retry && C.status == MLK_NEWTON_MAX_ITER) {
                 double lam2[4];
                 int st2 = 0, it2 = 0;
-                newton_block<SEP>(F, g, X, b, bmax, opt.retry_step, opt.retry_max_iter, opt.tol,
+                newton_block<SEP>(F, fl, g, X, b, bmax, opt.retry_step, opt.retry_max_iter, opt.tol,
                                   C, lam2, st2, it2);
                 if (warp == 0 && st2 == MLK_NEWTON_CONVERGED) {
 #pragma unroll
@@ -692,7 +710,7 @@ k_project(const double* __restrict__ f0, const double* __restrict__ stats,
                                                    __dmul_rn(lu2, __ldg(ash + 2 * D + j))),
                                          re ? Q[1] : Q[0]);
                     t = t < -700.0 ? -700.0 : (t > 700.0 ? 700.0 : t);
-                    outv = __dmul_rn(outv, exp(-t));
+                    outv = __dmul_rn(fmax(outv, fl), exp(-t));
                 }
                 F[j] = outv;
                 const double d = __dsub_rn(O[j], outv);
@@ -715,7 +733,7 @@ k_project(const double* __restrict__ f0, const double* __restrict__ stats,
                                                __dmul_rn(lu2, __ldg(ash + 2 * D + j))),
                                      __dmul_rn(lu3, a3));
                 t = t < -700.0 ? -700.0 : (t > 700.0 ? 700.0 : t);
-                outv = __dmul_rn(outv, exp(-t));
+                outv = __dmul_rn(fmax(outv, fl), exp(-t));
             }
             F[j] = outv;
             const double d = __dsub_rn(O[j], outv);
