@@ -56,6 +56,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--out", default=None)
     ap.add_argument("--no-clocks", action="store_true")
+    ap.add_argument("--emulate-rank", default=None,
+                    help="R/W: run rank R of W alone on one GPU (diagnostics; no NCCL)")
     return ap.parse_args()
 
 
@@ -247,6 +249,9 @@ def main():
     args = parse()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    emu = None
+    if args.emulate_rank:
+        emu = tuple(int(x) for x in args.emulate_rank.split("/"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         run_reference(args, rank, world)
@@ -265,7 +270,8 @@ def main():
     ds = corpus(spec["P"], spec["N"])
     models = load_models(spec["golden"])
     cfg = pipeline_config(args.tau)
-    rp = distributed.plan(ds.n_planes, ds.n_nodes, cfg.shards, cfg.mode, rank, world)
+    rp = distributed.plan(ds.n_planes, ds.n_nodes, cfg.shards, cfg.mode,
+                          *(emu if emu else (rank, world)))
     lo, hi = rp.node_range
     my_shards = [rp.shards[i] for i in rp.mine]
     f0 = pipeline.upload_f0(ds.data, dev, (lo, hi))

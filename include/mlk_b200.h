@@ -215,23 +215,36 @@ int mlk_compact(const uint8_t* flags, const double* stats, const MlkShard* shard
                 int32_t n_shards, double tau, int32_t* sel, int32_t* sel_rank,
                 int32_t* sel_by_range, int32_t* sel_count, double* eb_hi, cudaStream_t stream);
 
-/* residual.find_error_bound's predicate (residual.py:149-155), one bisection
- * level of a lookahead tree per launch: cand (n_shards, n_nodes) holds each
- * shard's candidate bounds in heap order (node 1 = the current query,
- * 2i = next query if node i is accepted, 2i+1 if rejected; <= 0 / NaN = no
- * query).  The launch evaluates, for every shard, the node its levels
- * 0 .. level-1 reached and sets fail[s*max_levels + level] when a selected
- * image of shard s misses tau there.  Levels are launched in order on one
- * stream, so the walk down the tree needs no host round trip.  The launch
- * visits positions act_start[s] .. act_start[s] + (act_off[s+1] - act_off[s])
- * of shard s's range-ordered selection (smallest ranges fail first). */
+/* residual.find_error_bound's predicate (residual.py:149-155) for `span`
+ * (1 or 2) bisection levels of a lookahead tree per launch: cand
+ * (n_shards, n_nodes) holds each shard's candidate bounds in heap order
+ * (node 1 = the current query, 2i = next query if node i is accepted, 2i+1
+ * if rejected; <= 0 / NaN = no query).  For every shard the launch walks
+ * levels 0 .. level-1 through the flags of earlier launches, then evaluates
+ * the node reached and, for span 2, both its children, in one pass over the
+ * images; fail[s*n_nodes + i] becomes non-zero when a selected image of
+ * shard s misses tau at node i.  Launches queue on one stream, so walking
+ * the tree needs no host round trip.  The launch visits positions
+ * act_start[s] .. act_start[s] + (act_off[s+1] - act_off[s]) of shard s's
+ * range-ordered selection (smallest ranges fail first). */
 int mlk_probe(const double* f0, const double* stats, const MlkShard* shards,
               int32_t n_shards, const MlkGrid* grid_h, const float* W, int32_t L,
               const float* cents, int32_t K, const uint8_t* codes,
               const int32_t* sel_by_range, const int32_t* act_off, const int32_t* act_start,
               int32_t n_work,
               const double* recon_bound, double tau, const double* cand, int32_t n_nodes,
-              int32_t level, int32_t* fail, int32_t max_levels, cudaStream_t stream);
+              int32_t level, int32_t span, int32_t* fail, const double* bins,
+              const double* eb_hi, cudaStream_t stream);
+
+/* Residual-magnitude profile of every selected image (34 counts + 34 sums of
+ * r^2 over log2 bins anchored at eb_hi[s]) at bins[(img_off + pos) * 68],
+ * pos = the image's place in the range-ordered selection; mlk_probe uses it
+ * (bins may be NULL) to certify passes without re-reading the image. */
+int mlk_probe_bins(const double* f0, const MlkShard* shards, int32_t n_shards,
+                   const MlkGrid* grid_h, const float* W, int32_t L, const float* cents,
+                   int32_t K, const uint8_t* codes, const int32_t* sel_by_range,
+                   const int32_t* sel_count, int32_t n_sel, const double* eb_hi, double* bins,
+                   cudaStream_t stream);
 
 /* Stage 4 encode + stage 5 (pipeline.py:239-292): residual q / zigzag /
  * varint for selected images into varint + (slot_base[s] + sel_rank) *

@@ -79,7 +79,8 @@ _SIGS = {
     "mlk_parse_residual_section": [_P, _I64, _I32, _I32, _I32, _I64, _I32, _P, _P, _P, _P, _P,
                                    _P, _P],
     "mlk_probe": [_P, _P, _P, _I32, _P, _P, _I32, _P, _I32, _P, _P, _P, _P, _I32, _P, _D, _P,
-                  _I32, _I32, _P, _I32, _P],
+                  _I32, _I32, _I32, _P, _P, _P, _P],
+    "mlk_probe_bins": [_P, _P, _I32, _P, _P, _I32, _P, _I32, _P, _P, _P, _I32, _P, _P, _P],
     "mlk_project": [_P, _P, _P, _P, _I32, _I32, _P, _P, _I32, _P, _I32, _P, _P, _P, _P, _P,
                     _P, _P, _P, _P, _P, _P, _P, _P, _I64, _P, _P, _P],
     "mlk_list_flags": [_P, _P, _I32, ctypes.c_uint32, _P, _P, _P],

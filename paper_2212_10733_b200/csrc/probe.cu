@@ -21,42 +21,47 @@ constexpr int PW_WARPS = 4;
 
 // q = rint(r / eb2): qround() in common.cuh.
 
-// One bisection level for every active shard: the shard's candidate is the
-// node of its heap-ordered lookahead tree reached by the previous levels'
-// outcomes (node 1 = root, 2i = accepted, 2i + 1 = rejected; fail[s*max_lev
-// + l] != 0 means level l rejected).  One warp per selected image, images in
-// ascending range order so failures surface first; a warp leaves as soon as
-// its shard's level flag is set or the bound passes for certain.
-__global__ void __launch_bounds__(32 * PW_WARPS, 8)
-k_probe_level(const double* __restrict__ f0, const double* __restrict__ stats,
-              const MlkShard* __restrict__ shards, MlkGrid g, PwPlan pw,
-              const float* __restrict__ W, int L, const float* __restrict__ cents, int K,
-              const unsigned char* __restrict__ codes, const int* __restrict__ sel_by_range,
-              const int* __restrict__ act_off, const int* __restrict__ act_start, int n_shards,
-              const double* __restrict__ recon_bound, double tau,
-              const double* __restrict__ cand, int n_nodes, int level, int* fail, int max_lev) {
-    __shared__ double sh_leaf[PW_WARPS][MLK_PW_MAX_LEAVES];
+// `span` (1 or 2) bisection levels for every active shard in one pass over
+// the images: the shard's candidates are the node of its heap-ordered
+// lookahead tree that the earlier levels' outcomes reach (node 1 = root,
+// 2i = accepted, 2i + 1 = rejected; fail[s*n_nodes + i] != 0 means node i
+// was rejected) and, for span 2, both of that node's children -- one read
+// of each histogram serves both levels.  One warp per selected image,
+// images in ascending range order so failures surface first; a candidate is
+// skipped once its flag is set or when it passes for certain.
+// Residual-magnitude profile of every selected image, for a certified pass
+// test per candidate bound: bin b in 1..32 holds count and sum of r^2 of the
+// cells with floor(log2|r|) = E0 + b - 1, E0 = ilogb(eb_hi) - 28; bin 0 sums
+// r^2 below the window (|r| < every candidate bound), bin 33 counts cells
+// above it (|r| > every candidate).  A cell with |r| < eb is not quantised
+// (rint(r / 2eb) = 0) and keeps its error r exactly; any other cell errs by
+// at most eb (+ rounding slack), so
+//   SSE(eb) <= sum(bins entirely below eb) + (other cells) * eb'^2.
+constexpr int PB_NB = 34;
+
+__device__ __forceinline__ int pb_e0(double eb_hi) { return ilogb(eb_hi) - 28; }
+
+__global__ void __launch_bounds__(32 * PW_WARPS)
+k_probe_bins(const double* __restrict__ f0, const MlkShard* __restrict__ shards, MlkGrid g,
+             const float* __restrict__ W, int L, const float* __restrict__ cents, int K,
+             const unsigned char* __restrict__ codes, const int* __restrict__ sel_by_range,
+             const int* __restrict__ sel_count, int n_shards, const double* __restrict__ eb_hi,
+             double* __restrict__ bins) {
+    __shared__ double sb[PW_WARPS][2 * PB_NB];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int D = g.D;
-    const int gw = blockIdx.x * PW_WARPS + warp;
-    if (gw >= act_off[n_shards]) return;
+    int gw = blockIdx.x * PW_WARPS + warp;
     int s = 0;
-    while (act_off[s + 1] <= gw) ++s;
-    int node = 1;
-    for (int l = 0; l < level; ++l) node = 2 * node + (fail[s * max_lev + l] ? 1 : 0);
-    if (node >= n_nodes) return;
-    const double eb = cand[(long long)s * n_nodes + node];
-    if (!(eb > 0.0)) return;  // no query at this node (search finished on this path)
-    volatile int* flag = fail + s * max_lev + level;
-    if (*flag) return;
-    const int pos = gw - act_off[s] + act_start[s];
+    while (s < n_shards && gw >= sel_count[s]) gw -= sel_count[s++];
+    if (s >= n_shards) return;
     const MlkShard sh = shards[s];
+    const int pos = gw;
     const int j = sel_by_range[sh.img_off + pos];
     const int img = sh.img_off + j;
-    const double4 st = reinterpret_cast<const double4*>(stats)[img];
-    const double range = __dsub_rn(st.x, st.y);
-    const double slack = 1e-13 * (fabs(st.x) + fabs(st.y) + recon_bound[img]);
-    if (eb + slack + eb * 1e-12 <= tau * range * (1.0 - 1e-12)) return;  // certain pass
+    double* b = sb[warp];
+    for (int k = lane; k < 2 * PB_NB; k += 32) b[k] = 0.0;
+    __syncwarp();
+    const int e0 = pb_e0(eb_hi[s]);
     const double* x = shard_image(f0, sh, j, D);
     double z[MLK_MAXL];
 #pragma unroll
@@ -65,50 +70,167 @@ k_probe_level(const double* __restrict__ f0, const double* __restrict__ stats,
                      : 0.0;
     const float* Ws = W + sh.w_off;
     const bool blas_tree = !sh.small_blas;
-    const double eb2 = 2.0 * eb, inv = 1.0 / eb2;
-    // approximate SSE (any order), exact only near the threshold
+    for (int q = lane; q < D; q += 32) {
+        const double rc = decode_cell(z, Ws, L, D, q, blas_tree && g.tree_cols[q], sh.mean, sh.std);
+        const double r = __dsub_rn(x[q], rc);
+        const double ar = fabs(r);
+        int bin;
+        if (!(ar > 0.0)) bin = 0;  // zero (NaN images are never selected)
+        else {
+            const int e = ilogb(ar);
+            bin = e < e0 ? 0 : (e >= e0 + 32 ? PB_NB - 1 : e - e0 + 1);
+        }
+        atomicAdd(&b[bin], 1.0);
+        atomicAdd(&b[PB_NB + bin], r * r);
+    }
+    __syncwarp();
+    double* out = bins + (long long)(sh.img_off + pos) * 2 * PB_NB;
+    for (int k = lane; k < 2 * PB_NB; k += 32) out[k] = b[k];
+}
+
+// upper bound of the SSE at bound eb from an image's profile (whole warp)
+__device__ __forceinline__ double pb_bound(const double* pb, int e0, double eb, double ebp) {
+    const int lane = threadIdx.x & 31;
     double acc = 0.0;
+    for (int k = lane; k < PB_NB; k += 32) {
+        const double cnt = pb[k], sum = pb[PB_NB + k];
+        bool below;
+        if (k == 0) below = true;
+        else if (k == PB_NB - 1) below = false;
+        else below = ldexp(1.0, e0 + k) <= eb;  // bin k covers [2^(e0+k-1), 2^(e0+k))
+        acc += below ? sum : cnt * ebp * ebp;
+    }
+    return warp_sum(acc);
+}
+
+constexpr int PB_MAXC = 3;
+
+__global__ void __launch_bounds__(32 * PW_WARPS, 6)
+k_probe_level(const double* __restrict__ f0, const double* __restrict__ stats,
+              const MlkShard* __restrict__ shards, MlkGrid g, PwPlan pw,
+              const float* __restrict__ W, int L, const float* __restrict__ cents, int K,
+              const unsigned char* __restrict__ codes, const int* __restrict__ sel_by_range,
+              const int* __restrict__ act_off, const int* __restrict__ act_start, int n_shards,
+              const double* __restrict__ recon_bound, double tau,
+              const double* __restrict__ cand, int n_nodes, int level, int span, int* fail,
+              const double* __restrict__ bins, const double* __restrict__ eb_hi) {
+    __shared__ double sh_leaf[PW_WARPS][MLK_PW_MAX_LEAVES];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int D = g.D;
+    const int gw = blockIdx.x * PW_WARPS + warp;
+    if (gw >= act_off[n_shards]) return;
+    int s = 0;
+    while (act_off[s + 1] <= gw) ++s;
+    int* fl = fail + (long long)s * n_nodes;
+    int node = 1;
+    for (int l = 0; l < level; ++l) node = 2 * node + (fl[node] ? 1 : 0);
+    if (node >= n_nodes) return;
+    // the candidate nodes of this launch
+    int nodes[PB_MAXC];
+    int nc = 0;
+    nodes[nc++] = node;
+    if (span > 1 && 2 * node + 1 < n_nodes) {
+        nodes[nc++] = 2 * node;
+        nodes[nc++] = 2 * node + 1;
+    }
+    const int pos = gw - act_off[s] + act_start[s];
+    const MlkShard sh = shards[s];
+    const int j = sel_by_range[sh.img_off + pos];
+    const int img = sh.img_off + j;
+    const double4 st = reinterpret_cast<const double4*>(stats)[img];
+    const double range = __dsub_rn(st.x, st.y);
+    const double slack = 1e-13 * (fabs(st.x) + fabs(st.y) + recon_bound[img]);
+    double eb2[PB_MAXC], inv[PB_MAXC], acc[PB_MAXC];
+    unsigned need = 0;
+#pragma unroll
+    for (int c = 0; c < PB_MAXC; ++c) {
+        eb2[c] = 1.0;
+        inv[c] = 1.0;
+        acc[c] = 0.0;
+        if (c < nc) {
+            const double eb = cand[(long long)s * n_nodes + nodes[c]];
+            if (!(eb > 0.0)) continue;  // no query at this node
+            if (*(volatile int*)(fl + nodes[c])) continue;
+            if (eb + slack + eb * 1e-12 <= tau * range * (1.0 - 1e-12)) continue;  // certain pass
+            eb2[c] = 2.0 * eb;
+            inv[c] = 1.0 / eb2[c];
+            need |= 1u << c;
+        }
+    }
+    if (need && bins) {  // certified pass from the residual profile
+        const double* pb = bins + (long long)(sh.img_off + pos) * 2 * PB_NB;
+        const int e0 = pb_e0(eb_hi[s]);
+#pragma unroll
+        for (int c = 0; c < PB_MAXC; ++c) {
+            if (!(need & (1u << c))) continue;
+            const double eb = 0.5 * eb2[c];
+            const double ebp = eb + slack + eb * 1e-12;
+            const double bound = pb_bound(pb, e0, eb, ebp);
+            if (sqrt(bound / D) <= tau * range * (1.0 - 1e-9)) need &= ~(1u << c);
+        }
+    }
+    if (!need) return;
+    const double* x = shard_image(f0, sh, j, D);
+    double z[MLK_MAXL];
+#pragma unroll
+    for (int k = 0; k < MLK_MAXL; ++k)
+        z[k] = k < L ? (double)cents[((long long)s * L + k) * K + codes[(long long)img * L + k]]
+                     : 0.0;
+    const float* Ws = W + sh.w_off;
+    const bool blas_tree = !sh.small_blas;
+    // approximate SSEs (any order), exact only near the threshold
     for (int q = lane; q < D; q += 32) {
         const double o = x[q];
         const double rc = decode_cell(z, Ws, L, D, q, blas_tree && g.tree_cols[q], sh.mean, sh.std);
         const double r = __dsub_rn(o, rc);
-        const double corr = __dadd_rn(rc, __dmul_rn(qround(r, eb2, inv), eb2));
-        const double d = __dsub_rn(o, corr);
-        acc = fma(d, d, acc);
-    }
-    acc = warp_sum(acc);
-    const double rms = sqrt(acc / D);
-    const double err = range > 0 ? rms / range : (rms == 0.0 ? 0.0 : INFINITY);
-    bool failed;
-    if (err > tau * (1.0 + 1e-10) || !(err == err)) {
-        failed = true;
-    } else if (err < tau * (1.0 - 1e-10)) {
-        failed = false;
-    } else {  // near tie: the reference's exact evaluation (pairwise leaves per lane)
-        double* leaf = sh_leaf[warp];
-        for (int l = lane; l < pw.n_leaves; l += 32) {
-            leaf[l] = pw_leaf(
-                [&](int q) {
-                    const double o = x[q];
-                    const double rc = decode_cell(z, Ws, L, D, q, blas_tree && g.tree_cols[q],
-                                                  sh.mean, sh.std);
-                    const double r = __dsub_rn(o, rc);
-                    const double d = __dsub_rn(o, __dadd_rn(rc, __dmul_rn(rint(__ddiv_rn(r, eb2)),
-                                                                          eb2)));
-                    return __dmul_rn(d, d);
-                },
-                pw.start[l], pw.len[l]);
+#pragma unroll
+        for (int c = 0; c < PB_MAXC; ++c) {
+            if (need & (1u << c)) {
+                const double corr = __dadd_rn(rc, __dmul_rn(qround(r, eb2[c], inv[c]), eb2[c]));
+                const double d = __dsub_rn(o, corr);
+                acc[c] = fma(d, d, acc[c]);
+            }
         }
-        __syncwarp();
-        double sse = 0.0;
-        if (lane == 0) sse = pw_combine_ops(leaf, pw);
-        sse = __shfl_sync(0xffffffffu, sse, 0);
-        const double rms_x = sqrt(__ddiv_rn(sse, (double)D));
-        const double err_x =
-            range > 0 ? __ddiv_rn(rms_x, range) : (rms_x == 0.0 ? 0.0 : INFINITY);
-        failed = !(err_x <= tau);
     }
-    if (failed && lane == 0) atomicOr(fail + s * max_lev + level, 1);
+#pragma unroll
+    for (int c = 0; c < PB_MAXC; ++c) {
+        if (!(need & (1u << c))) continue;
+        const double a = warp_sum(acc[c]);
+        const double rms = sqrt(a / D);
+        const double err = range > 0 ? rms / range : (rms == 0.0 ? 0.0 : INFINITY);
+        bool failed;
+        if (err > tau * (1.0 + 1e-10) || !(err == err)) {
+            failed = true;
+        } else if (err < tau * (1.0 - 1e-10)) {
+            failed = false;
+        } else {  // near tie: the reference's exact evaluation (pairwise leaves per lane)
+            double* leaf = sh_leaf[warp];
+            const double e2 = eb2[c];
+            for (int l = lane; l < pw.n_leaves; l += 32) {
+                leaf[l] = pw_leaf(
+                    [&](int q) {
+                        const double o = x[q];
+                        const double rc = decode_cell(z, Ws, L, D, q,
+                                                      blas_tree && g.tree_cols[q], sh.mean, sh.std);
+                        const double r = __dsub_rn(o, rc);
+                        const double d =
+                            __dsub_rn(o, __dadd_rn(rc, __dmul_rn(rint(__ddiv_rn(r, e2)), e2)));
+                        return __dmul_rn(d, d);
+                    },
+                    pw.start[l], pw.len[l]);
+            }
+            __syncwarp();
+            double sse = 0.0;
+            if (lane == 0) sse = pw_combine_ops(leaf, pw);
+            sse = __shfl_sync(0xffffffffu, sse, 0);
+            __syncwarp();
+            const double rms_x = sqrt(__ddiv_rn(sse, (double)D));
+            const double err_x =
+                range > 0 ? __ddiv_rn(rms_x, range) : (rms_x == 0.0 ? 0.0 : INFINITY);
+            failed = !(err_x <= tau);
+        }
+        if (failed && lane == 0) atomicOr(fl + nodes[c], 1);
+    }
 }
 
 }  // namespace
@@ -124,14 +246,26 @@ extern "C" int mlk_probe(const double* f0, const double* stats, const MlkShard* 
                          const int32_t* sel_by_range, const int32_t* act_off,
                          const int32_t* act_start, int32_t n_work,
                          const double* recon_bound, double tau, const double* cand,
-                         int32_t n_nodes, int32_t level, int32_t* fail, int32_t max_levels,
-                         cudaStream_t stream) {
+                         int32_t n_nodes, int32_t level, int32_t span, int32_t* fail,
+                         const double* bins, const double* eb_hi, cudaStream_t stream) {
     if (n_work <= 0) return MLK_OK;
-    if (n_nodes < 2 || level < 0 || level >= max_levels || (1 << level) >= n_nodes)
+    if (n_nodes < 2 || level < 0 || span < 1 || span > 2 || (1 << level) >= n_nodes)
         return MLK_ERR_CONFIG;
     PwPlan pw = mlk_make_pw_plan(grid_h->D);
     k_probe_level<<<(n_work + PW_WARPS - 1) / PW_WARPS, 32 * PW_WARPS, 0, stream>>>(
         f0, stats, shards, *grid_h, pw, W, L, cents, K, codes, sel_by_range, act_off, act_start,
-        n_shards, recon_bound, tau, cand, n_nodes, level, fail, max_levels);
+        n_shards, recon_bound, tau, cand, n_nodes, level, span, fail, bins, eb_hi);
+    return cudaGetLastError() == cudaSuccess ? MLK_OK : MLK_ERR_CUDA;
+}
+
+extern "C" int mlk_probe_bins(const double* f0, const MlkShard* shards, int32_t n_shards,
+                              const MlkGrid* grid_h, const float* W, int32_t L, const float* cents,
+                              int32_t K, const uint8_t* codes, const int32_t* sel_by_range,
+                              const int32_t* sel_count, int32_t n_sel, const double* eb_hi,
+                              double* bins, cudaStream_t stream) {
+    if (n_sel <= 0) return MLK_OK;
+    k_probe_bins<<<(n_sel + PW_WARPS - 1) / PW_WARPS, 32 * PW_WARPS, 0, stream>>>(
+        f0, shards, *grid_h, W, L, cents, K, codes, sel_by_range, sel_count, n_shards, eb_hi,
+        bins);
     return cudaGetLastError() == cudaSuccess ? MLK_OK : MLK_ERR_CUDA;
 }

@@ -536,9 +536,13 @@ def compress_device(f0: torch.Tensor, specs, dgrid: DeviceGrid, cfg, timer: Time
             states.append(_Search("done", eb_hi_s, result=(eb_hi_s, True)))
         else:
             states.append(_Search("hi", eb_hi_s))
+    n_sel_all = int(cnt_h.sum())
+    bins = T("probe_bins", (max(1, total) * 68,), f64)
+    call("mlk_probe_bins", f0, sh_d, S, dgrid.addr, W, L, cents, K, codes, sel_rng, sel_cnt,
+         n_sel_all, eb_hi, bins)
     n_nodes = 1 << LOOKAHEAD
     rounds = 0
-    fail = T("fail", (S, LOOKAHEAD), i32)
+    fail = T("fail", (S, n_nodes), i32)
     zero_start = None
     while any(st is not None and st.stage != "done" for st in states):
         rounds += 1
@@ -557,10 +561,10 @@ def compress_device(f0: torch.Tensor, specs, dgrid: DeviceGrid, cfg, timer: Time
             zero_start = ws.stage(np.zeros(S, dtype=np.int32))
         ws.flush()
         fail.zero_()
-        for level in range(LOOKAHEAD):
+        for level in range(0, LOOKAHEAD, 2):  # two levels per pass over the images
             call("mlk_probe", f0, stats, sh_d, S, dgrid.addr, W, L, cents, K, codes, sel_rng,
-                 off_d, zero_start, int(off[-1]), rbound, cfg.tau, cand_d, n_nodes, level, fail,
-                 LOOKAHEAD)
+                 off_d, zero_start, int(off[-1]), rbound, cfg.tau, cand_d, n_nodes, level,
+                 min(2, LOOKAHEAD - level), fail, bins, eb_hi)
         (fail_h,) = _d2h(fail)
         for s, st in enumerate(states):
             if st is None or st.stage == "done":
@@ -571,7 +575,7 @@ def compress_device(f0: torch.Tensor, specs, dgrid: DeviceGrid, cfg, timer: Time
                     break
                 if st.query() != cand[s, node]:
                     raise AssertionError("lookahead tree out of step with the search")
-                ok = fail_h[s, level] == 0
+                ok = fail_h[s, node] == 0
                 st = st.advance(ok)
                 node = 2 * node + (0 if ok else 1)
             states[s] = st
