@@ -334,20 +334,24 @@ k_kmeans(const double* __restrict__ lat, const MlkShard* __restrict__ shards, in
             break;
         }
         const double u = u_draw[i - 1];
-        // parallel scan of p = d2 / tot
+        // parallel scan of d2: cdf_j ~ run_j / ctot to within delta (the
+        // division by tot only rescales; its roundings are inside the bound)
         double loc = 0.0;
-        for (int j = j_lo; j < j_hi; ++j) loc += __ddiv_rn(d2[j], tot);
+        for (int j = j_lo; j < j_hi; ++j) loc += d2[j];
         double ctot;
         double run = block_exscan(loc, &ctot, S);
+        const double thr_a = u * ctot * (1.0 - 2.0 * delta), thr_b = u * ctot * (1.0 + 2.0 * delta);
         int a_cnt = 0, b_cnt = 0;
         for (int j = j_lo; j < j_hi; ++j) {
-            run += __ddiv_rn(d2[j], tot);
-            double rho = run / ctot;
-            if (rho * (1.0 + delta) <= u) ++a_cnt;
-            else if (rho * (1.0 - delta) > u) ++b_cnt;
+            run += d2[j];
+            if (run <= thr_a) ++a_cnt;        // cdf_j <= u for certain
+            else if (run > thr_b) ++b_cnt;    // cdf_j > u for certain
         }
-        a_cnt = block_sum_int(a_cnt, S);
-        b_cnt = block_sum_int(b_cnt, S);
+        {   // both counts in one exact reduction (each < 2^20)
+            const long long ab = (long long)block_sum((double)a_cnt + 1048576.0 * b_cnt, S);
+            a_cnt = (int)(ab & 1048575ll);
+            b_cnt = (int)(ab >> 20);
+        }
         if (tid == 0) {
             int idx = a_cnt;
             if (a_cnt + b_cnt != n) {
