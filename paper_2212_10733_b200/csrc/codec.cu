@@ -11,6 +11,16 @@ namespace {
 
 constexpr int Z_THREADS = 64;
 
+__constant__ short c_lbase[29] = {3,  4,  5,  6,  7,  8,  9,  10, 11,  13,  15,  17,  19,  23, 27,
+                                  31, 35, 43, 51, 59, 67, 83, 99, 115, 131, 163, 195, 227, 258};
+__constant__ short c_lext[29] = {0, 0, 0, 0, 0, 0, 0, 0, 1, 1, 1, 1, 2, 2, 2,
+                                 2, 3, 3, 3, 3, 4, 4, 4, 4, 5, 5, 5, 5, 0};
+__constant__ short c_dbase[30] = {1,    2,    3,    4,    5,    7,     9,     13,    17,  25,
+                                  33,   49,   65,   97,   129,  193,   257,   385,   513, 769,
+                                  1025, 1537, 2049, 3073, 4097, 6145, 8193, 12289, 16385, 24577};
+__constant__ short c_dext[30] = {0, 0, 0, 0, 1, 1, 2, 2, 3, 3, 4, 4, 5, 5, 6,
+                                 6, 7, 7, 8, 8, 9, 9, 10, 10, 11, 11, 12, 12, 13, 13};
+
 __global__ void __launch_bounds__(Z_THREADS)
 k_deflate6(const uint8_t* __restrict__ in, const long long* __restrict__ in_off,
            const long long* __restrict__ in_len, int n, uint8_t* __restrict__ out,
@@ -31,13 +41,311 @@ k_deflate6(const uint8_t* __restrict__ in, const long long* __restrict__ in_off,
                                    head, tb);
 }
 
-__global__ void k_inflate(const uint8_t* __restrict__ in, const long long* __restrict__ in_off,
-                          const long long* __restrict__ in_len, int n, uint8_t* __restrict__ out,
-                          const long long* __restrict__ out_off, long long out_cap,
-                          long long* __restrict__ out_len) {
-    const int s = blockIdx.x * blockDim.x + threadIdx.x;
-    if (s >= n) return;
-    out_len[s] = z6::inflate_zlib(in + in_off[s], in_len[s], out + out_off[s], out_cap);
+
+// ---------------------------------------------------------------------------
+// Warp-per-stream inflate (zlib.decompress, residual.py:86), same results and
+// error codes as z6::inflate_zlib.  Every lane runs the identical decode
+// (broadcast loads, no shuffles); Huffman symbols come from 10-bit (literal/
+// length) and 8-bit (distance) lookup tables built warp-parallel in shared
+// memory, longer codes from the canonical count/symbol walk; literals are
+// stored by lane 0, back-references copied by the whole warp (position i of
+// a copy reads out[o - dist + i % dist], always already written).
+namespace zi {
+
+constexpr int LB = 10, DB = 8;
+
+struct Tab {
+    uint16_t lit[1 << LB];  // (len << 9) | symbol, 0 = walk the canonical code
+    uint16_t dst[1 << DB];
+    uint16_t lcount[16], dcount[16];
+    uint16_t lsym[320], dsym[32];
+    uint8_t lens[320];
+    int tmp[16];
+};
+
+// canonical tables for n code lengths: count, symbol (sorted by (len, sym)),
+// and the direct lookup table of width `tb`; returns zlib's `left` (< 0 over-
+// subscribed, > 0 incomplete).  Whole warp.
+__device__ int build(const uint8_t* len, int n, uint16_t* count, uint16_t* sym, uint16_t* tab,
+                     int tb, int* tmp) {
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u;
+    if (lane < 16) tmp[lane] = 0;
+    __syncwarp();
+    for (int i = lane; i < n; i += 32) atomicAdd(&tmp[len[i]], 1);
+    __syncwarp();
+    if (lane < 16) count[lane] = (uint16_t)tmp[lane];
+    for (int i = lane; i < (1 << tb); i += 32) tab[i] = 0;
+    __syncwarp();
+    int left = 1;
+    int offs[16], base[16];
+    offs[0] = 0;
+    offs[1] = 0;
+    for (int l = 1; l <= 15; ++l) {
+        left <<= 1;
+        left -= count[l];
+        if (l < 15) offs[l + 1] = offs[l] + count[l];
+    }
+    if (count[0] == n) return 0;
+    if (left < 0) return left;
+    // code of length l starts at first[l] (canonical), symbols in order
+    int first[16];
+    int c = 0;
+    first[0] = 0;
+    for (int l = 1; l <= 15; ++l) {
+        c = (c + (l > 1 ? count[l - 1] : 0)) << 1;
+        first[l] = c;
+    }
+    // first[] above is zlib's next_code with bl_count[0] = 0
+    for (int l = 0; l <= 15; ++l) base[l] = offs[l];
+    for (int i0 = 0; i0 < n; i0 += 32) {
+        const int i = i0 + lane;
+        const int l = i < n ? len[i] : 0;
+        const unsigned grp = __match_any_sync(FULL, l);
+        const int rank = __popc(grp & lt);
+        if (l) {
+            const int pos = offs[l] + rank;
+            sym[pos] = (uint16_t)i;
+            const unsigned code = (unsigned)(first[l] + pos - base[l]);
+            if (l <= tb) {
+                const unsigned rev = __brev(code) >> (32 - l);
+                const uint16_t e = (uint16_t)((l << 9) | i);
+                for (unsigned k = rev; k < (1u << tb); k += 1u << l) tab[k] = e;
+            }
+        }
+        __syncwarp();
+        // advance the per-length offsets by this chunk's counts
+        for (int ll = 1; ll <= 15; ++ll) offs[ll] += __popc(__ballot_sync(FULL, l == ll));
+    }
+    __syncwarp();
+    return left;
+}
+
+struct Bits {
+    const uint8_t* in;
+    long long n, pos;
+    unsigned long long bb;
+    int nb;
+    __device__ void fill() {
+        while (nb <= 56 && pos < n) {
+            bb |= (unsigned long long)in[pos++] << nb;
+            nb += 8;
+        }
+    }
+    __device__ int take(int k, bool& err) {  // k <= 32
+        if (k == 0) return 0;
+        fill();
+        if (nb < k) { err = true; return 0; }
+        const int v = (int)(bb & ((1ull << k) - 1ull));
+        bb >>= k;
+        nb -= k;
+        return v;
+    }
+};
+
+__device__ __forceinline__ int decode(Bits& b, const uint16_t* tab, int tb, const uint16_t* count,
+                                      const uint16_t* sym, bool& err) {
+    b.fill();
+    const uint16_t e = tab[b.bb & ((1u << tb) - 1u)];
+    if (e) {
+        const int l = e >> 9;
+        if (l > b.nb) { err = true; return -1; }
+        b.bb >>= l;
+        b.nb -= l;
+        return e & 511;
+    }
+    int code = 0, first = 0, index = 0;  // canonical walk (long or invalid codes)
+    for (int len = 1; len <= 15; ++len) {
+        if (len > b.nb) { err = true; return -1; }
+        code |= (int)((b.bb >> (len - 1)) & 1ull);
+        const int cnt = count[len];
+        if (code - cnt < first) {
+            b.bb >>= len;
+            b.nb -= len;
+            return sym[index + (code - first)];
+        }
+        index += cnt;
+        first += cnt;
+        first <<= 1;
+        code <<= 1;
+    }
+    err = true;
+    return -1;
+}
+
+}  // namespace zi
+
+__global__ void __launch_bounds__(256)
+k_inflate_warp(const uint8_t* __restrict__ in, const long long* __restrict__ in_off,
+               const long long* __restrict__ in_len, int n_streams, uint8_t* __restrict__ out,
+               const long long* __restrict__ out_off, long long cap,
+               long long* __restrict__ out_len) {
+    __shared__ zi::Tab tabs[8];
+    const unsigned FULL = 0xffffffffu;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int s = blockIdx.x * 8 + warp;
+    if (s >= n_streams) return;
+    zi::Tab& T = tabs[warp];
+    const uint8_t* src = in + in_off[s];
+    const long long n = in_len[s];
+    uint8_t* dst = out + out_off[s];
+    long long res = -1;
+    do {
+        if (n < 6) break;
+        const unsigned cmf = src[0], flg = src[1];
+        if ((cmf & 0x0f) != 8 || (cmf >> 4) > 7 || ((cmf << 8) | flg) % 31 != 0 || (flg & 0x20))
+            break;
+        zi::Bits b{src + 2, n - 2, 0, 0ull, 0};
+        bool err = false;
+        long long o = 0;
+        int last = 0;
+        int rc = 0;
+        do {
+            last = b.take(1, err);
+            const int type = b.take(2, err);
+            if (err) { rc = -1; break; }
+            if (type == 0) {
+                // stored: drop to the byte boundary (the bit buffer holds whole bytes)
+                const int drop = b.nb & 7;
+                b.bb >>= drop;
+                b.nb -= drop;
+                const long long p = b.pos - b.nb / 8;
+                b.bb = 0;
+                b.nb = 0;
+                b.pos = p;
+                if (b.pos + 4 > b.n) { rc = -1; break; }
+                const unsigned len = b.in[b.pos] | ((unsigned)b.in[b.pos + 1] << 8);
+                const unsigned nlen = b.in[b.pos + 2] | ((unsigned)b.in[b.pos + 3] << 8);
+                b.pos += 4;
+                if (len != (~nlen & 0xffffu)) { rc = -1; break; }
+                if (b.pos + len > b.n) { rc = -1; break; }
+                if (o + len > cap) { rc = -2; break; }
+                for (unsigned i = lane; i < len; i += 32) dst[o + i] = b.in[b.pos + i];
+                __syncwarp();
+                b.pos += len;
+                o += len;
+                continue;
+            }
+            if (type == 3) { rc = -1; break; }
+            int nlen = 288, ndist = 30;
+            if (type == 1) {
+                for (int i = lane; i < 320; i += 32)
+                    T.lens[i] = (uint8_t)(i < 144 ? 8 : (i < 256 ? 9 : (i < 280 ? 7 : (i < 288 ? 8 : 5))));
+                __syncwarp();
+                zi::build(T.lens, 288, T.lcount, T.lsym, T.lit, zi::LB, T.tmp);
+                zi::build(T.lens + 288, 30, T.dcount, T.dsym, T.dst, zi::DB, T.tmp);
+            } else {
+                nlen = b.take(5, err) + 257;
+                ndist = b.take(5, err) + 1;
+                const int ncode = b.take(4, err) + 4;
+                if (err || nlen > 286 || ndist > 30) { rc = -1; break; }
+                uint8_t cl[z6::BL_CODES];
+                for (int i = 0; i < z6::BL_CODES; ++i) cl[i] = 0;
+                for (int i = 0; i < ncode; ++i) cl[z6::bl_order(i)] = (uint8_t)b.take(3, err);
+                if (err) { rc = -1; break; }
+                if (lane < z6::BL_CODES) T.lens[lane] = cl[lane];
+                __syncwarp();
+                // the code-length code, decoded through the distance table slots
+                if (zi::build(T.lens, z6::BL_CODES, T.dcount, T.dsym, T.dst, 7, T.tmp) != 0) {
+                    rc = -1;
+                    break;
+                }
+                uint8_t* L = T.lens;  // overwritten below (all lanes hold cl[] in registers)
+                __syncwarp();
+                int idx = 0;
+                bool bad = false;
+                while (idx < nlen + ndist) {
+                    const int sym = zi::decode(b, T.dst, 7, T.dcount, T.dsym, err);
+                    if (err || sym < 0) { bad = true; break; }
+                    if (sym < 16) {
+                        if (lane == 0) L[idx] = (uint8_t)sym;
+                        ++idx;
+                    } else {
+                        uint8_t len = 0;
+                        int rep;
+                        if (sym == 16) {
+                            if (idx == 0) { bad = true; break; }
+                            __syncwarp();
+                            len = L[idx - 1];
+                            rep = 3 + b.take(2, err);
+                        } else if (sym == 17) {
+                            rep = 3 + b.take(3, err);
+                        } else {
+                            rep = 11 + b.take(7, err);
+                        }
+                        if (err || idx + rep > nlen + ndist) { bad = true; break; }
+                        for (int q = lane; q < rep; q += 32) L[idx + q] = len;
+                        idx += rep;
+                    }
+                    __syncwarp();
+                }
+                __syncwarp();
+                if (bad) { rc = -1; break; }
+                if (L[256] == 0) { rc = -1; break; }
+                // distance lengths move after the literal/length ones (lens[288..])
+                uint8_t dl = 0;
+                if (lane < ndist) dl = L[nlen + lane];
+                __syncwarp();
+                for (int i = nlen + lane; i < 320; i += 32) L[i] = 0;
+                __syncwarp();
+                if (lane < 32) L[288 + lane] = lane < ndist ? dl : 0;
+                __syncwarp();
+                const int e1 = zi::build(L, nlen, T.lcount, T.lsym, T.lit, zi::LB, T.tmp);
+                if (e1 < 0 || (e1 > 0 && nlen - T.lcount[0] != 1)) { rc = -1; break; }
+                const int e2 = zi::build(L + 288, ndist, T.dcount, T.dsym, T.dst, zi::DB, T.tmp);
+                if (e2 < 0 || (e2 > 0 && ndist - T.dcount[0] != 1)) { rc = -1; break; }
+            }
+            // ---- symbols
+            for (;;) {
+                int sym = zi::decode(b, T.lit, zi::LB, T.lcount, T.lsym, err);
+                if (err || sym < 0) { rc = -1; break; }
+                if (sym < 256) {
+                    if (o >= cap) { rc = -2; break; }
+                    if (lane == 0) dst[o] = (uint8_t)sym;
+                    ++o;
+                } else if (sym == 256) {
+                    break;
+                } else {
+                    sym -= 257;
+                    if (sym >= 29) { rc = -1; break; }
+                    const int len = c_lbase[sym] + b.take(c_lext[sym], err);
+                    const int ds = zi::decode(b, T.dst, zi::DB, T.dcount, T.dsym, err);
+                    if (err || ds < 0 || ds >= 30) { rc = -1; break; }
+                    const long long dist = c_dbase[ds] + b.take(c_dext[ds], err);
+                    if (err || dist > o) { rc = -1; break; }
+                    if (o + len > cap) { rc = -2; break; }
+                    __syncwarp();
+                    for (int i = lane; i < len; i += 32) dst[o + i] = dst[o - dist + i % dist];
+                    __syncwarp();
+                    o += len;
+                }
+            }
+            __syncwarp();
+            if (rc) break;
+        } while (!last);
+        if (rc) { res = rc; break; }
+        // Adler-32 trailer (big-endian) after byte alignment
+        const long long p = b.pos - b.nb / 8;
+        if (p + 4 > b.n) break;
+        const unsigned want = ((unsigned)b.in[p] << 24) | ((unsigned)b.in[p + 1] << 16) |
+                              ((unsigned)b.in[p + 2] << 8) | b.in[p + 3];
+        unsigned long long sa = 0, sb = 0;
+        for (long long i = lane; i < o; i += 32) {
+            const unsigned v = dst[i];
+            sa += v;
+            sb += (unsigned long long)(o - i) * v;
+        }
+        for (int k = 16; k > 0; k >>= 1) {
+            sa += __shfl_xor_sync(FULL, sa, k);
+            sb += __shfl_xor_sync(FULL, sb, k);
+        }
+        const unsigned a = (unsigned)((1 + sa) % 65521ull);
+        const unsigned bsum = (unsigned)(((unsigned long long)o + sb) % 65521ull);
+        if (((bsum << 16) | a) != want) break;
+        res = o;
+    } while (false);
+    if (lane == 0) out_len[s] = res;
 }
 
 // ---------------------------------------------------------------------------
@@ -860,7 +1168,7 @@ extern "C" int mlk_zlib_decompress(const uint8_t* in, const int64_t* in_off,
                                    const int64_t* out_off, int64_t out_cap, int64_t* out_len,
                                    cudaStream_t stream) {
     if (n <= 0) return MLK_OK;
-    k_inflate<<<(n + 63) / 64, 64, 0, stream>>>(
+    k_inflate_warp<<<(n + 7) / 8, 256, 0, stream>>>(
         in, reinterpret_cast<const long long*>(in_off), reinterpret_cast<const long long*>(in_len),
         n, out, reinterpret_cast<const long long*>(out_off), (long long)out_cap,
         reinterpret_cast<long long*>(out_len));

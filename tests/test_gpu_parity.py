@@ -312,3 +312,44 @@ def test_decompress_rejects_corrupt_archives():
     bad[off:off + 8] = (len(arc) + 5).to_bytes(8, "little")  # shard offset past the end
     with pytest.raises(FormatError):
         mb.decompress(bytes(bad))
+
+
+def test_device_inflate_matches_host_zlib():
+    """mlk_zlib_decompress on streams host zlib produced at several levels
+    (stored, fixed and dynamic blocks, long codes), and corrupt input."""
+    import zlib
+
+    from paper_2212_10733_b200._lib import call
+    dev = torch.device("cuda", 0)
+    rng = np.random.default_rng(7)
+    raws = [b"", b"a", bytes(range(256)) * 3, rng.integers(0, 256, 5000, dtype=np.uint8).tobytes()]
+    for n in [10, 700, 1521, 4000, 15000]:
+        z = rng.geometric(rng.uniform(0.05, 0.6), n)
+        raws.append(np.minimum(z, 255).astype(np.uint8).tobytes())
+    fib = [1, 1]
+    while len(fib) < 20:
+        fib.append(fib[-1] + fib[-2])
+    raws.append(rng.permutation(np.concatenate(
+        [np.full(f, k, np.uint8) for k, f in enumerate(fib[:17])])).tobytes())
+    comp = [zlib.compress(r, lvl) for r in raws for lvl in (0, 1, 6, 9)]
+    want = [r for r in raws for _ in (0, 1, 6, 9)]
+    bad = bytearray(comp[-1])
+    bad[len(bad) // 2] ^= 0x5A
+    comp.append(bytes(bad))
+    comp.append(comp[5][:-3])
+    n = len(comp)
+    cap = 16384
+    in_off = np.concatenate([[0], np.cumsum([len(c) for c in comp])[:-1]]).astype(np.int64)
+    blob = torch.from_numpy(np.frombuffer(b"".join(comp), np.uint8).copy()).to(dev)
+    i64 = dict(dtype=torch.int64, device=dev)
+    out = torch.zeros(n * cap, dtype=torch.uint8, device=dev)
+    out_len = torch.empty(n, **i64)
+    call("mlk_zlib_decompress", blob, torch.from_numpy(in_off).to(dev),
+         torch.tensor([len(c) for c in comp], **i64), n, out,
+         torch.arange(0, n * cap, cap, **i64), cap, out_len)
+    ol = out_len.cpu().numpy()
+    host = out.cpu().numpy()
+    for k, w in enumerate(want):
+        assert ol[k] == len(w), k
+        assert host[k * cap:k * cap + len(w)].tobytes() == w, k
+    assert ol[-2] < 0 and ol[-1] < 0
