@@ -1075,7 +1075,7 @@ def decompress_device(archive, dev) -> np.ndarray:
     vals = dec.out[:pre.n_planes * pre.n_nodes * g.rows * g.cols]
     if bool((vals < 0).any()):
         raise ConfigError("histogram values must be non-negative")
-    return hostio.download_array(vals, (pre.n_planes, pre.n_nodes, g.rows, g.cols))
+    return hostio.download_pinned_array(vals, (pre.n_planes, pre.n_nodes, g.rows, g.cols))
 
 
 def shard_layout(shards, models, n_nodes, rows, cols, node_lo=0):

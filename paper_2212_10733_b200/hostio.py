@@ -23,7 +23,7 @@ import numpy as np
 import torch
 
 __all__ = ["upload_planes", "upload_bytes", "download_bytes", "download_view", "download_array",
-           "pinned"]
+           "download_pinned_array", "pinned"]
 
 CHUNK = 64 << 20
 _POOL = None
@@ -224,3 +224,15 @@ def download_array(src: torch.Tensor, shape, dtype=np.float64) -> np.ndarray:
 
     list(_pool().map(cp, range(len(spans))))
     return out
+
+
+def download_pinned_array(src: torch.Tensor, shape, dtype=np.float64) -> np.ndarray:
+    """Device tensor -> numpy array backed by page-locked memory from torch's
+    caching host allocator: one DMA at full PCIe rate, no staging copy and
+    no page faults (freed results are recycled for the next call)."""
+    nbytes = int(np.prod(shape)) * np.dtype(dtype).itemsize
+    host = torch.empty(max(nbytes, 1), dtype=torch.uint8, pin_memory=True)
+    if nbytes:
+        host[:nbytes].copy_(src.reshape(-1).view(torch.uint8)[:nbytes], non_blocking=True)
+        torch.cuda.current_stream(src.device).synchronize()
+    return host.numpy()[:nbytes].view(dtype).reshape(shape)
