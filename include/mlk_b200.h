@@ -293,6 +293,9 @@ int mlk_parse_residual_section(const uint8_t* sec, int64_t len, int32_t n_images
                                int64_t* body_off, int64_t* body_len, double* eb, uint8_t* mode,
                                int32_t* count_out, int32_t* why);
 
+/* HOST: 1 if p lies in page-locked host memory (cudaHostAlloc/Register). */
+int mlk_is_pinned(const void* p);
+
 /* ---- shard-blob assembly on device (container.py:90-95, pipeline.py:116-184) */
 
 /* list[img_off + r] = r-th image of shard s (ascending) with flags & mask;

@@ -78,6 +78,7 @@ _SIGS = {
     "mlk_compact": [_P, _P, _P, _I32, _D, _P, _P, _P, _P, _P, _P],
     "mlk_parse_residual_section": [_P, _I64, _I32, _I32, _I32, _I64, _I32, _P, _P, _P, _P, _P,
                                    _P, _P],
+    "mlk_is_pinned": [_P],
     "mlk_probe": [_P, _P, _P, _I32, _P, _P, _I32, _P, _I32, _P, _P, _P, _P, _I32, _P, _D, _P,
                   _I32, _I32, _I32, _P, _P, _P, _P],
     "mlk_probe_bins": [_P, _P, _I32, _P, _P, _I32, _P, _I32, _P, _P, _P, _I32, _P, _P, _P],

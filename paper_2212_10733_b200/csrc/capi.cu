@@ -278,3 +278,14 @@ extern "C" int mlk_parse_residual_section(const uint8_t* sec, int64_t len, int32
     *count_out = (int32_t)count;
     return MLK_OK;
 }
+
+// HOST: 1 if p points into page-locked (pinned) host memory -- the public
+// API then DMAs straight from the caller's array without a staging copy.
+extern "C" int mlk_is_pinned(const void* p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return a.type == cudaMemoryTypeHost ? 1 : 0;
+}

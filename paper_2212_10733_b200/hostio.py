@@ -23,7 +23,7 @@ import numpy as np
 import torch
 
 __all__ = ["upload_planes", "upload_bytes", "download_bytes", "download_view", "download_array",
-           "download_pinned_array", "pinned"]
+           "download_pinned_array", "pinned", "pinned_empty"]
 
 CHUNK = 64 << 20
 _POOL = None
@@ -56,6 +56,22 @@ def _copy_stream(dev):
     return s
 
 
+def _is_pinned(arr: np.ndarray) -> bool:
+    if not arr.flags.c_contiguous or arr.nbytes == 0:
+        return False
+    from ._lib import lib
+    return bool(lib().mlk_is_pinned(ctypes.c_void_p(arr.ctypes.data)))
+
+
+def pinned_empty(shape, dtype=np.float64) -> np.ndarray:
+    """A numpy array in page-locked host memory (torch's caching host
+    allocator).  Filling the timestep's f0 into such a buffer lets compress()
+    DMA it straight to the GPU."""
+    nbytes = int(np.prod(shape)) * np.dtype(dtype).itemsize
+    host = torch.empty(max(nbytes, 1), dtype=torch.uint8, pin_memory=True)
+    return host.numpy()[:nbytes].view(dtype).reshape(shape)
+
+
 def upload_planes(data: np.ndarray, dev, node_range=None, pad_elems: int = 2) -> torch.Tensor:
     """data[:, lo:hi] of a (P, N, ...) float64 array -> flat device buffer
     (+pad_elems zeros of tail padding), on the current stream's timeline."""
@@ -68,6 +84,21 @@ def upload_planes(data: np.ndarray, dev, node_range=None, pad_elems: int = 2) ->
     if pad_elems:
         buf[total // data.itemsize:].zero_()
     if total == 0:
+        return buf
+    if _is_pinned(data):
+        # the caller's array is page-locked: DMA each plane slab directly
+        cs = _copy_stream(dev)
+        cs.wait_stream(torch.cuda.current_stream(dev))
+        src = torch.from_numpy(data.reshape(P, -1).view(np.uint8))
+        dst = buf.view(torch.uint8)
+        with torch.cuda.stream(cs):
+            for p in range(P):
+                dst[p * slab:(p + 1) * slab].copy_(src[p, lo * per_node:hi * per_node],
+                                                   non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(cs)
+        torch.cuda.current_stream(dev).wait_event(ev)
+        buf.record_stream(cs)
         return buf
     stage = pinned(f"up{dev.index}", total)
     last = _LAST_UPLOAD.get(dev.index)

@@ -353,3 +353,18 @@ def test_device_inflate_matches_host_zlib():
         assert ol[k] == len(w), k
         assert host[k * cap:k * cap + len(w)].tobytes() == w, k
     assert ol[-2] < 0 and ol[-1] < 0
+
+
+def test_pinned_input_gives_the_same_archive():
+    from paper_2212_10733_b200.hostio import pinned_empty
+    meta, _ = G.load("small")
+    ds, same = G.corpus("small")
+    if not same:
+        pytest.skip("host generates a different corpus")
+    cfg = _cfg(meta["runs"][0])
+    st = mb.TimestepState(models=_models("small"), timestep_index=1)
+    arc, _, _ = mb.compress(ds, cfg, st)
+    pin = pinned_empty(ds.data.shape)
+    pin[...] = ds.data
+    arc2, _, _ = mb.compress(mb.FDataset(grid=ds.grid, data=pin, timestep=ds.timestep), cfg, st)
+    assert arc2 == arc
