@@ -68,17 +68,26 @@ def exchange_sizes(rp: RankPlan, local_sizes, head_len: int, group=None):
 
 
 def reduce_stats(local: dict, group=None) -> dict:
-    """SUM / MIN / MAX reductions of the report statistics.
+    """SUM / MIN / MAX reductions of the report statistics, one collective per
+    operation (the values of each kind are packed into one tensor).
 
     `local` maps name -> (op, float64 array) with op in {"sum", "min", "max"}."""
     dev = _device_for(group)
-    out = {}
     ops = {"sum": dist.ReduceOp.SUM, "min": dist.ReduceOp.MIN, "max": dist.ReduceOp.MAX}
-    for name, (op, arr) in local.items():
-        t = torch.as_tensor(np.atleast_1d(np.asarray(arr, dtype=np.float64)), device=dev).clone()
+    out = {}
+    for op in ("sum", "min", "max"):
+        names = [k for k, (o, _) in local.items() if o == op]
+        if not names:
+            continue
+        parts = [np.atleast_1d(np.asarray(local[k][1], dtype=np.float64)) for k in names]
+        t = torch.as_tensor(np.concatenate(parts), device=dev).clone()
         if dist.is_initialized() and dist.get_world_size(group) > 1:
             dist.all_reduce(t, op=ops[op], group=group)
-        out[name] = t.cpu().numpy()
+        flat = t.cpu().numpy()
+        pos = 0
+        for k, pa in zip(names, parts):
+            out[k] = flat[pos:pos + pa.size]
+            pos += pa.size
     return out
 
 
@@ -92,27 +101,30 @@ def gather_bytes(payload: bytes, group=None, dst=0):
 
 
 def report_partials(out, tau):
-    """Decomposable per-rank statistics of a CompressOut for reduce_stats."""
+    """Decomposable per-rank statistics of a CompressOut for reduce_stats,
+    reduced on the device (one small D2H)."""
     from ._lib import F_EXCEPTION, F_EXC_OVERFLOW, F_NONFINITE, F_SELECTED
-    flags = out.host("flags")
-    status = out.host("status")
-    stats = out.host("stats")
-    q_o = out.host("qoi")
-    q_r = out.host("fqoi")
-    mask = q_o[:, 0] > 0
-    d = (q_o[mask] - q_r[mask]) ** 2
+    d = out.dev
+    flags, status, stats = d["flags"], d["status"], d["stats"]
+    q_o, q_r = d["qoi"], d["fqoi"]
+    mask = (q_o[:, 0] > 0).unsqueeze(1)
+    f64 = torch.float64
+    cnt = lambda m: m.sum().to(f64).reshape(1)
+    dq = torch.where(mask, (q_o - q_r) ** 2, torch.zeros_like(q_o)).sum(0)
+    qmax = torch.where(mask, q_o, torch.full_like(q_o, -np.inf)).amax(0)
+    qmin = torch.where(mask, q_o, torch.full_like(q_o, np.inf)).amin(0)
+    vals = torch.cat([
+        torch.tensor([float(flags.numel())], dtype=f64, device=flags.device),
+        cnt((flags & F_SELECTED) != 0), cnt((flags & F_EXCEPTION) != 0),
+        cnt((status == 0) & ((flags & F_NONFINITE) == 0) & ((flags & F_EXC_OVERFLOW) == 0)),
+        cnt((flags & (F_SELECTED | F_NONFINITE)) == 0), d["fsse"].sum().reshape(1),
+        stats[:, 0].max().reshape(1), stats[:, 1].min().reshape(1), dq, mask.sum().to(f64)
+        .reshape(1), qmax, qmin]).cpu().numpy()
     return {
-        "n": ("sum", [len(flags)]),
-        "selected": ("sum", [np.sum((flags & F_SELECTED) != 0)]),
-        "exceptions": ("sum", [np.sum((flags & F_EXCEPTION) != 0)]),
-        "converged": ("sum", [np.sum((status == 0) & ((flags & F_NONFINITE) == 0)
-                                     & ((flags & F_EXC_OVERFLOW) == 0))]),
-        "ae_ok": ("sum", [np.sum((flags & (F_SELECTED | F_NONFINITE)) == 0)]),
-        "sse": ("sum", [out.host("fsse").sum()]),
-        "data_max": ("max", [stats[:, 0].max()]),
-        "data_min": ("min", [stats[:, 1].min()]),
-        "qoi_sse": ("sum", d.sum(axis=0) if d.size else np.zeros(4)),
-        "qoi_cnt": ("sum", [mask.sum()]),
-        "qoi_max": ("max", q_o[mask].max(axis=0) if mask.any() else np.full(4, -np.inf)),
-        "qoi_min": ("min", q_o[mask].min(axis=0) if mask.any() else np.full(4, np.inf)),
+        "n": ("sum", vals[0:1]), "selected": ("sum", vals[1:2]),
+        "exceptions": ("sum", vals[2:3]), "converged": ("sum", vals[3:4]),
+        "ae_ok": ("sum", vals[4:5]), "sse": ("sum", vals[5:6]),
+        "data_max": ("max", vals[6:7]), "data_min": ("min", vals[7:8]),
+        "qoi_sse": ("sum", vals[8:12]), "qoi_cnt": ("sum", vals[12:13]),
+        "qoi_max": ("max", vals[13:17]), "qoi_min": ("min", vals[17:21]),
     }

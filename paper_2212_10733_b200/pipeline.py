@@ -197,15 +197,25 @@ def compress_distributed(ds: FDataset, config: PipelineConfig, state: TimestepSt
     if out_path is not None:
         body = hostio.download_view(out.blob_buf, int(np.sum(out.blob_lens)))
         if rp.rank == 0:
-            with open(out_path, "wb") as fh:
-                fh.write(head + struct.pack(f"<{len(offs)}Q", *[int(x) for x in offs]))
-                fh.truncate(int(offs[-1] + sizes[-1]))
+            # rewrite in place (no truncate-to-zero: an existing archive file's
+            # pages are reused instead of re-allocated)
+            fd = os.open(out_path, os.O_RDWR | os.O_CREAT, 0o644)
+            try:
+                os.pwrite(fd, head + struct.pack(f"<{len(offs)}Q", *[int(x) for x in offs]), 0)
+                os.ftruncate(fd, int(offs[-1] + sizes[-1]))
+            finally:
+                os.close(fd)
         if dist.is_initialized():
             dist.barrier(group=group)
         if rp.mine:
             fd = os.open(out_path, os.O_WRONLY)
             try:
-                os.pwrite(fd, memoryview(body), int(offs[rp.mine[0]]))
+                base = int(offs[rp.mine[0]])
+                mv = memoryview(body)
+                spans = [(a, min(len(mv), a + hostio.CHUNK)) for a in range(0, len(mv),
+                                                                           hostio.CHUNK)]
+                list(hostio._pool().map(lambda sp: os.pwrite(fd, mv[sp[0]:sp[1]], base + sp[0]),
+                                        spans))
             finally:
                 os.close(fd)
         if dist.is_initialized():
