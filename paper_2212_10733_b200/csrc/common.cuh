@@ -251,3 +251,16 @@ __device__ __forceinline__ double qround(double r, double eb2, double inv) {
         return rint(__ddiv_rn(r, eb2));
     return rint(y);
 }
+
+// a / b correctly rounded from y = RN(1/b) (b fixed across many a): Markstein's
+// correction q' = RN(q + RN(a - q b) y), q = RN(a y), is the IEEE quotient
+// for normal-range results (checked against a / b on 2e8 random pairs);
+// zero, tiny, huge or non-finite quotients take the IEEE division.
+__device__ __forceinline__ double div_by_recip(double a, double b, double y) {
+    const double q = __dmul_rn(a, y);
+    const double r = __fma_rn(-q, b, a);
+    const double q2 = __fma_rn(r, y, q);
+    const double m = fabs(q2);
+    if (a == 0.0 || (m >= 0x1p-1000 && m <= 0x1p+1000)) return q2;
+    return __ddiv_rn(a, b);
+}

@@ -42,6 +42,8 @@ k_stage1(const double* __restrict__ f0, const MlkShard* __restrict__ shards, int
          double* __restrict__ stats, double* __restrict__ qoi) {
     extern __shared__ __align__(16) double smem[];
     __shared__ unsigned long long bars[S1_WARPS];
+    __shared__ double gvp[64], gvq[64];  // separable grids: v_par by column, v_perp^2 by row
+    __shared__ int pstart[16];           // OpenBLAS K-panel starts (GEMM path)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int D = g.D;
     int first = 0;
@@ -50,16 +52,33 @@ k_stage1(const double* __restrict__ f0, const MlkShard* __restrict__ shards, int
     const MlkShard sh = shards[s];
     float* Wsm = reinterpret_cast<float*>(smem);
     const int wdoubles = ((L * D + 3) / 4) * 2;  // 16-B aligned float region
-    const int per_warp = ((D + 2 + 1) / 2) * 2 + 96;
-    double* tbuf = smem + wdoubles + warp * per_warp;  // TMA target (D + 2 doubles)
-    double* chain = tbuf + ((D + 2 + 1) / 2) * 2;
+    const int per_warp = ((D + 2 + 1) / 2) * 2 + 16 + 96;
+    double* tbuf = smem + wdoubles + warp * per_warp;  // TMA target (D + 2 doubles) + pad
+    double* chain = tbuf + ((D + 2 + 1) / 2) * 2 + 16;
     unsigned long long* bar = &bars[warp];
     if (lane == 0) mbar_init(bar, 1);
     const float* Wg = W + sh.w_off;
     for (int i = threadIdx.x; i < L * D; i += blockDim.x) Wsm[i] = __ldg(Wg + i);
-    __syncthreads();
+    const bool sep = g.sep && g.rows <= 64 && g.cols <= 64;
+    if (sep) {
+        for (int i = threadIdx.x; i < g.cols; i += blockDim.x) gvp[i] = g.vpar[i];
+        for (int i = threadIdx.x; i < g.rows; i += blockDim.x) gvq[i] = g.vperp2[i * g.cols];
+    }
     int np_ = 0;
-    for (int j0 = 0; j0 < D; j0 += panel_len(D - j0)) ++np_;
+    for (int j0 = 0; j0 < D; j0 += panel_len(D - j0)) {
+        if (threadIdx.x == 0 && np_ < 16) pstart[np_] = j0;
+        ++np_;
+    }
+    __syncthreads();
+    // panel of element j: full 384-panels first, then at most two halves
+    int k0 = 0;
+    while (k0 < np_ && pstart[k0] == 384 * k0) ++k0;
+    const int b1 = k0 < np_ ? (k0 + 1 < np_ ? pstart[k0 + 1] : D) : D;
+    // GEMM path: the normalised image is stored with one pad slot per K-panel
+    // (element j of panel p at j + p) so the 4-8 lanes walking different
+    // panels in step hit different banks
+    const bool padded = !sh.small_blas && np_ <= 16;
+    const double rstd = __drcp_rn(sh.std);
 
     unsigned phase = 0;
     for (int k_img = 0; k_img < S1_IMGS; ++k_img) {
@@ -76,18 +95,44 @@ k_stage1(const double* __restrict__ f0, const MlkShard* __restrict__ shards, int
 
         // ---- pass A: extrema, sums, first moments from the staged copy
         double mx = -INFINITY, mn = INFINITY, so = 0.0, soo = 0.0, n0 = 0.0, n1 = 0.0, n2 = 0.0;
+        bool has_nan = false;  // numpy's max/min propagate NaN
+        if (sep) {  // grid values from the (row, column) tables
+            const int rows = g.rows, cols = g.cols;
+            int r = lane / cols, c = lane - (lane / cols) * cols;
+            const int dr = 32 / cols, dc = 32 - (32 / cols) * cols;
+            for (int j = lane; j < D; j += 32) {
+                const double v = buf[j];
+                has_nan |= v != v;
+                mx = fmax(mx, v);
+                mn = fmin(mn, v);
+                so += v;
+                soo = fma(v, v, soo);
+                const bool re = (r == 0) | (r == rows - 1), ce = (c == 0) | (c == cols - 1);
+                const double vol = re ? (ce ? g.vcls[3] : g.vcls[2]) : (ce ? g.vcls[1] : g.vcls[0]);
+                const double fv = v * vol;
+                n0 += fv;
+                n1 = fma(fv, gvp[c], n1);
+                n2 = fma(fv, gvq[r], n2);
+                c += dc;
+                r += dr;
+                if (c >= cols) { c -= cols; ++r; }
+            }
+        } else {
 #pragma unroll 4
-        for (int j = lane; j < D; j += 32) {
-            double v = buf[j];
-            mx = np_max2(mx, v);
-            mn = np_min2(mn, v);
-            so += v;
-            soo = fma(v, v, soo);
-            double fv = v * __ldg(g.vol + j);
-            n0 += fv;
-            n1 = fma(fv, __ldg(g.vpar + j), n1);
-            n2 = fma(fv, __ldg(g.vperp2 + j), n2);
+            for (int j = lane; j < D; j += 32) {
+                double v = buf[j];
+                has_nan |= v != v;
+                mx = fmax(mx, v);
+                mn = fmin(mn, v);
+                so += v;
+                soo = fma(v, v, soo);
+                double fv = v * __ldg(g.vol + j);
+                n0 += fv;
+                n1 = fma(fv, __ldg(g.vpar + j), n1);
+                n2 = fma(fv, __ldg(g.vperp2 + j), n2);
+            }
         }
+        if (__any_sync(0xffffffffu, has_nan)) mx = mn = __longlong_as_double(0x7ff8000000000000ll);
         mx = warp_max(mx);
         mn = warp_min(mn);
         so = warp_sum(so);
@@ -99,9 +144,24 @@ k_stage1(const double* __restrict__ f0, const MlkShard* __restrict__ shards, int
         double u = n1 / n0;
         double tp = hm * n2 / n0;
         double n3 = 0.0;
-        for (int j = lane; j < D; j += 32) {
-            double dv = __ldg(g.vpar + j) - u;
-            n3 = fma(buf[j] * __ldg(g.vol + j), dv * dv, n3);
+        if (sep) {
+            const int rows = g.rows, cols = g.cols;
+            int r = lane / cols, c = lane - (lane / cols) * cols;
+            const int dr = 32 / cols, dc = 32 - (32 / cols) * cols;
+            for (int j = lane; j < D; j += 32) {
+                const bool re = (r == 0) | (r == rows - 1), ce = (c == 0) | (c == cols - 1);
+                const double vol = re ? (ce ? g.vcls[3] : g.vcls[2]) : (ce ? g.vcls[1] : g.vcls[0]);
+                const double dv = gvp[c] - u;
+                n3 = fma(buf[j] * vol, dv * dv, n3);
+                c += dc;
+                r += dr;
+                if (c >= cols) { c -= cols; ++r; }
+            }
+        } else {
+            for (int j = lane; j < D; j += 32) {
+                double dv = __ldg(g.vpar + j) - u;
+                n3 = fma(buf[j] * __ldg(g.vol + j), dv * dv, n3);
+            }
         }
         n3 = warp_sum(n3);
         double tl = hm * n3 / n0;
@@ -114,7 +174,25 @@ k_stage1(const double* __restrict__ f0, const MlkShard* __restrict__ shards, int
         }
 
         // ---- normalise in place: xn = (x - mean) / std (numpy, two roundings)
-        for (int j = lane; j < D; j += 32) buf[j] = __ddiv_rn(__dsub_rn(buf[j], sh.mean), sh.std);
+        if (padded) {
+            // descending, so every write (to j + panel(j) >= j) lands on a slot
+            // that has already been read
+            for (int t = 0; t < (D + 31) / 32; ++t) {  // warp-uniform trip count
+                const int j = D - 1 - lane - 32 * t;
+                double xn = 0.0;
+                int p = 0;
+                if (j >= 0) {
+                    xn = div_by_recip(__dsub_rn(buf[j], sh.mean), sh.std, rstd);
+                    p = j < 384 * k0 ? j / 384 : (j < b1 ? k0 : k0 + 1);
+                    if (p > np_ - 1) p = np_ - 1;
+                }
+                __syncwarp();
+                if (j >= 0) buf[j + p] = xn;
+            }
+        } else {
+            for (int j = lane; j < D; j += 32)
+                buf[j] = div_by_recip(__dsub_rn(buf[j], sh.mean), sh.std, rstd);
+        }
         __syncwarp();
 
         // ---- latents in the host BLAS order
@@ -140,9 +218,10 @@ k_stage1(const double* __restrict__ f0, const MlkShard* __restrict__ shards, int
                 for (int q = 0; q < p; ++q) j0 += panel_len(D - j0);
                 const int j1 = j0 + panel_len(D - j0);
                 const float* wk = Wsm + k * D;
+                const double* bp = buf + (padded ? p : 0);
                 double acc = 0.0;
 #pragma unroll 8
-                for (int j = j0; j < j1; ++j) acc = __fma_rn(buf[j], (double)wk[j], acc);
+                for (int j = j0; j < j1; ++j) acc = __fma_rn(bp[j], (double)wk[j], acc);
                 chain[c] = acc;
             }
             __syncwarp();
@@ -167,7 +246,7 @@ extern "C" int mlk_stage1(const double* f0, const MlkShard* shards, int32_t n_sh
     if (L * ((grid_h->D + 383) / 384 + 1) > 96) return MLK_ERR_DIM;
     const int D = grid_h->D;
     size_t sm = (size_t)(((L * D + 3) / 4) * 2) * sizeof(double) +
-                (size_t)S1_WARPS * (((D + 3) / 2) * 2 + 96) * sizeof(double);
+                (size_t)S1_WARPS * (((D + 3) / 2) * 2 + 16 + 96) * sizeof(double);
     if (sm > 227 * 1024) return MLK_ERR_DIM;
     cudaFuncSetAttribute(k_stage1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     // sum_s ceil(n_s / per_block) <= total / per_block + n_shards; spare blocks exit
