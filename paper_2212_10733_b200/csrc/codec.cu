@@ -11,6 +11,31 @@ namespace {
 
 constexpr int Z_THREADS = 64;
 
+// trees.c's static tables, computed once on the host per device and copied
+// into each block's shared memory by all threads (instead of one thread
+// rebuilding them per block)
+__device__ z6::Tables g_ztables;
+
+__device__ __forceinline__ void load_tables(z6::Tables& tb) {
+    static_assert(sizeof(z6::Tables) % 4 == 0, "table words");
+    const unsigned* src = reinterpret_cast<const unsigned*>(&g_ztables);
+    unsigned* dst = reinterpret_cast<unsigned*>(&tb);
+    for (int i = threadIdx.x; i < (int)(sizeof(z6::Tables) / 4); i += blockDim.x) dst[i] = src[i];
+}
+
+int ensure_tables() {
+    static bool ready[64] = {false};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return MLK_ERR_CUDA;
+    if (!ready[dev]) {
+        z6::Tables h;
+        z6::init_tables(h);
+        if (cudaMemcpyToSymbol(g_ztables, &h, sizeof(h)) != cudaSuccess) return MLK_ERR_CUDA;
+        ready[dev] = true;
+    }
+    return MLK_OK;
+}
+
 __constant__ short c_lbase[29] = {3,  4,  5,  6,  7,  8,  9,  10, 11,  13,  15,  17,  19,  23, 27,
                                   31, 35, 43, 51, 59, 67, 83, 99, 115, 131, 163, 195, 227, 258};
 __constant__ short c_lext[29] = {0, 0, 0, 0, 0, 0, 0, 0, 1, 1, 1, 1, 2, 2, 2,
@@ -28,7 +53,7 @@ k_deflate6(const uint8_t* __restrict__ in, const long long* __restrict__ in_off,
            long long* __restrict__ out_len, uint8_t* __restrict__ work, int n_workers,
            long long nmin) {
     __shared__ z6::Tables tb;
-    if (threadIdx.x == 0) z6::init_tables(tb);
+    load_tables(tb);
     __syncthreads();
     const int wid = blockIdx.x * blockDim.x + threadIdx.x;
     if (wid >= n_workers) return;
@@ -717,7 +742,7 @@ k_deflate_warp(const uint8_t* __restrict__ in, const long long* __restrict__ in_
                unsigned long long* __restrict__ prof) {
     __shared__ z6::Tables tb;
     extern __shared__ __align__(16) uint8_t zsm[];
-    if (threadIdx.x == 0) z6::init_tables(tb);
+    load_tables(tb);
     __syncthreads();
     const wz::Lay Ly = wz::layout(nmax);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1124,6 +1149,7 @@ extern "C" int mlk_zlib_compress6(const uint8_t* in, const int64_t* in_off, cons
                                   int32_t n_workers, int64_t nmin, cudaStream_t stream) {
     if (n <= 0) return MLK_OK;
     if (n_workers <= 0) return MLK_ERR_CONFIG;
+    if (ensure_tables() != MLK_OK) return MLK_ERR_CUDA;
     cudaFuncSetAttribute(k_deflate6, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
     k_deflate6<<<(n_workers + Z_THREADS - 1) / Z_THREADS, Z_THREADS, 0, stream>>>(
         in, reinterpret_cast<const long long*>(in_off), reinterpret_cast<const long long*>(in_len),
@@ -1140,6 +1166,7 @@ extern "C" int mlk_zlib_compress6_warp(const uint8_t* in, const int64_t* in_off,
                                        cudaStream_t stream) {
     if (n <= 0) return MLK_OK;
     if (nmax > 16000 || nmax < 1 || sym_cap < 3LL * nmax + 3) return MLK_ERR_CONFIG;
+    if (ensure_tables() != MLK_OK) return MLK_ERR_CUDA;
     const wz::Lay Ly = wz::layout(nmax);
     // two blocks per SM when they fit, up to 16 warps each
     int zw = (110 * 1024) / Ly.total;
