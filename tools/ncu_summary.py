@@ -80,9 +80,9 @@ def launches(path: Path):
         name = d["Kernel Name"].split("(")[0].replace("<unnamed>::", "").replace("void ", "")
         seq.append((name, _num(d["Metric Value"]) / 1e6))
     starts = [i for i, (n, _) in enumerate(seq) if n.startswith("k_stage1")]
-    # one step = between the last two stage-1 launches of the timed loop
-    # (bench.py's roofline reps follow the loop and are excluded)
-    step = seq[starts[-7]:starts[-6]] if len(starts) >= 7 else seq
+    # one step = from the last stage-1 launch to the end (the last timed step
+    # of a `bench.py --no-e2e` run; nothing launches after the loop)
+    step = seq[starts[-1]:] if starts else seq
     agg = collections.defaultdict(lambda: [0, 0.0])
     for n, t in step:
         agg[n][0] += 1
