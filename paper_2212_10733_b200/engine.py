@@ -778,8 +778,11 @@ def _run_deflate(ws, varint, in_off, vlen, n, zout, zoff, zcap, zlen, dev, max_w
     streams = _tier_streams(dev, len(DEFLATE_TIERS) + 1)
     ev0 = torch.cuda.Event()
     ev0.record(main)
-    lo = 0
-    for k, hi in enumerate(DEFLATE_TIERS + (None,)):
+    bounds = list(zip((0,) + DEFLATE_TIERS, DEFLATE_TIERS + (None,)))
+    # largest streams first: the few long, latency-bound streams of the upper
+    # tiers start at once and overlap the bulk tier instead of trailing it
+    for k in reversed(range(len(bounds))):
+        lo, hi = bounds[k]
         st = streams[k]
         st.wait_event(ev0)
         with torch.cuda.stream(st):
@@ -788,11 +791,9 @@ def _run_deflate(ws, varint, in_off, vlen, n, zout, zoff, zcap, zlen, dev, max_w
                 call("mlk_zlib_compress6", varint, in_off, vlen, n, zout, zoff, zcap, zlen,
                      _deflate_pool(dev, workers), workers, lo)
             else:
-                # the few streams of the upper tiers get one block per 2 SMs
-                nb = 2 * sms if k < 3 else max(1, sms // 2)
+                nb = 2 * sms if k < 3 else sms
                 call("mlk_zlib_compress6_warp", varint, in_off, vlen, n, lo, hi, zout, zoff,
                      zcap, zlen, nb, sym, sym_cap, DEFLATE_PROF)
-                lo = hi
         ev = torch.cuda.Event()
         ev.record(st)
         main.wait_event(ev)
