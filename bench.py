@@ -56,8 +56,6 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--out", default=None)
     ap.add_argument("--no-clocks", action="store_true")
-    ap.add_argument("--emulate-rank", default=None,
-                    help="R/W: run rank R of W alone on one GPU (diagnostics; no NCCL)")
     return ap.parse_args()
 
 
@@ -249,9 +247,6 @@ def main():
     args = parse()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
-    emu = None
-    if args.emulate_rank:
-        emu = tuple(int(x) for x in args.emulate_rank.split("/"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         run_reference(args, rank, world)
@@ -270,23 +265,18 @@ def main():
     ds = corpus(spec["P"], spec["N"])
     models = load_models(spec["golden"])
     cfg = pipeline_config(args.tau)
-    rp = distributed.plan(ds.n_planes, ds.n_nodes, cfg.shards, cfg.mode,
-                          *(emu if emu else (rank, world)))
-    lo, hi = rp.node_range
-    my_shards = [rp.shards[i] for i in rp.mine]
-    f0 = pipeline.upload_f0(ds.data, dev, (lo, hi))
+    sp = distributed.split_plan(ds.n_planes, ds.n_nodes, cfg.shards, cfg.mode, rank, world,
+                                cfg.latent_dim, cfg.pq_bits)
+    f0 = pipeline.upload_f0(ds.data[sp.plane_lo:sp.plane_hi], dev)
     dgrid = engine.DeviceGrid(ds.grid, dev, cfg.latent_dim)
-    works = engine.shard_layout(my_shards, [models[i] for i in rp.mine], hi - lo, ds.grid.rows,
-                                ds.grid.cols, node_lo=lo)
-    D = ds.grid.rows * ds.grid.cols
+    works = engine.split_layout(sp, models, ds.grid.rows, ds.grid.cols)
     n_local = sum(w.n_img for w in works)
-    head_len = 80 + 8 * (1 + ds.grid.rows + ds.grid.cols + D)
+    comm = distributed.Comm(sp) if world > 1 else None
 
     def one_step(timer=None):
-        out = engine.compress_device(f0, works, dgrid, cfg, timer)
-        # the only exchange: blob sizes -> archive offsets (NCCL all_reduce)
-        distributed.exchange_sizes(rp, out.blob_lens, head_len)
-        return out
+        # at N > 1 the step includes every collective of the split (latents
+        # all_gather, selection / probe all_reduces, section-size all_gather)
+        return engine.compress_device(f0, works, dgrid, cfg, timer, comm=comm)
 
     for _ in range(args.warmup):
         one_step()
@@ -375,7 +365,7 @@ def main():
         rep = res[1]
         arc_len = len(res[0]) if world == 1 else os.path.getsize(shm)
         e2e = {"value": total_hist / e2e_s, "unit": "hist/s",
-               "h2d_bytes_per_step": int(ds.data[:, lo:hi].nbytes) * world,
+               "h2d_bytes_per_step": int(ds.data[sp.plane_lo:sp.plane_hi].nbytes) * world,
                "d2h_bytes_per_step": int(arc_len), "seconds_per_step": e2e_s,
                "api": ("paper_2212_10733_b200.compress(ds, config, state)" if world == 1 else
                        "pipeline.compress_distributed(ds, config, state, out_path)"),
@@ -421,7 +411,8 @@ def main():
                 "ratio": None if dec is None else dec["ratio"]}
         if world > 1:
             line["scaling"] = "strong"
-            line["config"]["parallelism"] = f"{world} ranks x {len(rp.mine)} shards (NCCL sizes)"
+            line["config"]["parallelism"] = (f"{world} ranks x members [n_s r/{world}, "
+                                             f"n_s (r+1)/{world}) of all 8 shards (NCCL)")
         print(json.dumps(line), flush=True)
         if args.out:
             Path(args.out).write_text(json.dumps(line, indent=1))

@@ -52,10 +52,11 @@ extern "C" {
 #define MLK_F_EXC_GATE 32u    /* final PD gate (pipeline.py:285) */
 #define MLK_F_EXCEPTION (MLK_F_NONFINITE | MLK_F_EXC_NEWTON | MLK_F_EXC_OVERFLOW | MLK_F_EXC_GATE)
 
-/* One shard of the node-range decomposition (decomp.py:73-105).  Image j of
- * the shard is the D doubles at f0 + base + (j / block) * plane_stride
- * + (j % block) * D, i.e. plane-major members exactly as partition() lists
- * them (decomp.py:102). */
+/* One shard of the node-range decomposition (decomp.py:73-105), or the
+ * contiguous index range [j0, j0 + n_img) of it that one rank processes.
+ * Image j of the table entry is shard member g = j0 + j, the D doubles at
+ * f0 + base + (g / block) * plane_stride + (g % block) * D, i.e. plane-major
+ * members exactly as partition() lists them (decomp.py:102). */
 typedef struct {
     int64_t base;
     int64_t plane_stride;
@@ -67,6 +68,8 @@ typedef struct {
     double eb;          /* error bound chosen by the search (residual.py:129) */
     int32_t lossless;   /* search fell back to lossless payloads */
     int32_t w_off;      /* float offset of this shard's W (L x D) */
+    int32_t j0;         /* member index of image 0 (0 unless the shard is split) */
+    int32_t pad;
 } MlkShard;
 
 /* Grid tables, all DEVICE arrays of D = rows*cols doubles computed on the

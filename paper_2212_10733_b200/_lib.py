@@ -28,7 +28,8 @@ class MlkShard(ctypes.Structure):
                 ("block", ctypes.c_int32), ("n_img", ctypes.c_int32),
                 ("img_off", ctypes.c_int32), ("small_blas", ctypes.c_int32),
                 ("mean", ctypes.c_double), ("std", ctypes.c_double), ("eb", ctypes.c_double),
-                ("lossless", ctypes.c_int32), ("w_off", ctypes.c_int32)]
+                ("lossless", ctypes.c_int32), ("w_off", ctypes.c_int32),
+                ("j0", ctypes.c_int32), ("pad", ctypes.c_int32)]
 
 
 class MlkGrid(ctypes.Structure):
@@ -48,7 +49,7 @@ class MlkNewton(ctypes.Structure):
                 ("lam_f32", ctypes.c_int32), ("tau", ctypes.c_double)]
 
 
-assert ctypes.sizeof(MlkShard) == 64
+assert ctypes.sizeof(MlkShard) == 72
 assert ctypes.sizeof(MlkGrid) == 136
 
 _P = ctypes.c_void_p

@@ -143,11 +143,12 @@ __device__ __forceinline__ double np_min2(double a, double b) {
 }
 
 // ----------------------------------------------------------------------------
-// shard addressing: image j of shard s lives at
-//   f0 + base + (j / block) * plane_stride + (j % block) * D
+// shard addressing: image j of table entry s is member g = j0 + j, at
+//   f0 + base + (g / block) * plane_stride + (g % block) * D
 __device__ __forceinline__ const double* shard_image(const double* f0, const MlkShard& s,
                                                     int j, int D) {
-    long long p = j / s.block, x = j % s.block;
+    const int g = s.j0 + j;
+    long long p = g / s.block, x = g % s.block;
     return f0 + s.base + p * s.plane_stride + x * (long long)D;
 }
 

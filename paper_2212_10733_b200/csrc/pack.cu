@@ -73,7 +73,7 @@ __global__ void k_pack_res(const int* __restrict__ sel, const MlkShard* __restri
     unsigned char* d = out + dst_off[e];
     const long long zl = zlen[e];
     if (lane == 0) {
-        put_u32(d, (unsigned)sel[sh.img_off + r]);
+        put_u32(d, (unsigned)(sh.j0 + sel[sh.img_off + r]));
         put_u32(d + 4, (unsigned)(13 + zl));
         d[8] = (unsigned char)(sh.lossless ? 1 : 0);
         d[9] = (unsigned char)rows;
@@ -126,7 +126,7 @@ __global__ void k_pack_exc(const double* __restrict__ f0, const MlkShard* __rest
     const int k = e - exc_off[s];
     const int j = exc_list[sh.img_off + k];
     unsigned char* d = out + sec_off[s] + 4 + (long long)k * (4 + 8LL * D);
-    if (lane == 0) put_u32(d, (unsigned)j);
+    if (lane == 0) put_u32(d, (unsigned)(sh.j0 + j));
     const unsigned long long* x =
         reinterpret_cast<const unsigned long long*>(shard_image(f0, sh, j, D));
     for (int q = lane; q < D; q += 32) put_u64(d + 4 + 8LL * q, x[q]);

@@ -258,6 +258,12 @@ class ShardWork:
     model: object          # AEModel
     rows: int = 39
     cols: int = 39
+    j0: int = 0            # member index of image 0 (split shards, distributed.SplitPlan)
+    n_full: int = -1       # images of the whole shard (-1: n_img)
+
+    @property
+    def n_total(self) -> int:
+        return self.n_img if self.n_full < 0 else self.n_full
 
 
 @dataclass
@@ -267,13 +273,14 @@ class CompressOut:
 
     specs: list
     blob_buf: torch.Tensor
-    blob_lens: np.ndarray
+    blob_lens: np.ndarray  # whole shard blobs (every rank's pieces)
     dev: dict
     sel_count: np.ndarray
     eb: list
     lossless: list
     rows_cols: tuple
     img_off: list
+    segments: list = field(default_factory=list)  # (buf offset, blob-region offset, length)
     timings: dict = field(default_factory=dict)
     _host: dict = field(default_factory=dict)
 
@@ -340,16 +347,20 @@ class Timer:
         return out
 
 
-def _shard_table(specs, D, L):
+def _shard_table(specs, D, L, full=False):
+    """MlkShard table of a rank's (pieces of) shards; full=True describes the
+    whole shards instead (the k-means input after the latents all_gather)."""
     arr = (MlkShard * len(specs))()
     off = 0
     for i, sp in enumerate(specs):
-        small = sp.n_img * L * D <= 1e6
+        n = sp.n_total if full else sp.n_img
+        # the encode order is the one numpy picks for the whole shard's matmul
+        small = sp.n_total * L * D <= 1e6
         arr[i] = MlkShard(base=sp.base, plane_stride=sp.plane_stride, block=sp.block,
-                          n_img=sp.n_img, img_off=off, small_blas=int(small),
+                          n_img=n, img_off=off, small_blas=int(small),
                           mean=float(sp.model.norm_mean), std=float(sp.model.norm_std), eb=0.0,
-                          lossless=0, w_off=i * L * D)
-        off += sp.n_img
+                          lossless=0, w_off=i * L * D, j0=0 if full else sp.j0, pad=0)
+        off += n
     return arr
 
 
@@ -457,11 +468,16 @@ def _d2h(*tensors):
 
 
 def compress_device(f0: torch.Tensor, specs, dgrid: DeviceGrid, cfg, timer: Timer | None = None,
-                    zlib_level: int = 6) -> CompressOut:
+                    zlib_level: int = 6, comm=None) -> CompressOut:
     """Run stages 2-5 of pipeline._compress_shard for every shard in `specs`.
 
-    f0 is a flat float64 CUDA tensor holding the rank's histograms; shard s's
-    image j lives at base + (j // block) * plane_stride + (j % block) * D.
+    f0 is a flat float64 CUDA tensor holding the rank's histograms; image j
+    of spec s is member g = j0 + j of its shard, at
+    base + (g // block) * plane_stride + (g % block) * D.
+    comm (distributed.Comm): the specs are this rank's member ranges of every
+    shard (distributed.SplitPlan); the per-shard decisions are made on
+    collectively reduced inputs, so every rank's pieces are exactly those of
+    the single-process blobs.
     Device arrays in the result stay valid until the next call on the device.
     """
     dev = f0.device
@@ -483,12 +499,17 @@ def compress_device(f0: torch.Tensor, specs, dgrid: DeviceGrid, cfg, timer: Time
     for sp in specs:
         seed = mix_seed(cfg.seed, sp.wid)
         for d in range(L):
-            f, u = kmeans_draws(sp.n_img, K, seed + d)
+            f, u = kmeans_draws(sp.n_total, K, seed + d)
             first.append(f)
             draws.extend(u)
     first_d = ws.stage(np.asarray(first, dtype=np.int64))
     draws_d = ws.stage(np.asarray(draws, dtype=np.float64))
     gram = ws.stage(_gram([sp.model for sp in specs]))
+    if comm is not None:
+        table_full = _shard_table(specs, D, L, full=True)
+        shf_d = ws.stage(np.frombuffer(bytes(table_full), dtype=np.uint8))
+    else:
+        table_full, shf_d = table, sh_d
     ws.flush()
 
     timer.mark("encode")
@@ -498,11 +519,19 @@ def compress_device(f0: torch.Tensor, specs, dgrid: DeviceGrid, cfg, timer: Time
     call("mlk_stage1", f0, sh_d, S, total, dgrid.addr, W, L, lat, stats, qoi)
 
     timer.mark("pq")
-    scratch = T("km_scratch", (4 * L * total,), f64)
+    lat_km, total_km = lat, total
+    if comm is not None:
+        # every rank's latents, rearranged into whole shards (32 B per image)
+        gidx, m = comm.gather_index(dev)
+        lat_pad = T("lat_pad", (m, L), f64)
+        lat_pad[:total].copy_(lat)
+        lat_km = comm.all_gather(lat_pad).reshape(-1, L).index_select(0, gidx)
+        total_km = lat_km.shape[0]
+    scratch = T("km_scratch", (4 * L * total_km,), f64)
     cents = T("cents", (S, L, K), torch.float32)
     kinfo = T("kinfo", (S, L, 4), i32)
-    call("mlk_kmeans", lat, sh_d, ctypes.addressof(table), S, L, K, first_d, draws_d, scratch,
-         cents, kinfo)
+    call("mlk_kmeans", lat_km, shf_d, ctypes.addressof(table_full), S, L, K, first_d, draws_d,
+         scratch, cents, kinfo)
 
     timer.mark("find_eb")
     codes = T("codes", (total, L), torch.uint8)
@@ -522,13 +551,21 @@ def compress_device(f0: torch.Tensor, specs, dgrid: DeviceGrid, cfg, timer: Time
     sel_cnt = T("sel_cnt", (S,), i32)
     eb_hi = T("eb_hi", (S,), f64)
     call("mlk_compact", flags, stats, sh_d, S, cfg.tau, sel, sel_rank, sel_rng, sel_cnt, eb_hi)
-    cnt_h, ebhi_h = _d2h(sel_cnt, eb_hi)
+    if comm is not None:
+        # eb_hi = tau * max range over the whole shard's selection (residual.py:143)
+        cnt_g = sel_cnt.clone()
+        comm.all_reduce_(cnt_g, "sum")
+        comm.all_reduce_(eb_hi, "max")
+        cnt_h, cntg_h, ebhi_h = _d2h(sel_cnt, cnt_g, eb_hi)
+    else:
+        cnt_h, ebhi_h = _d2h(sel_cnt, eb_hi)
+        cntg_h = cnt_h
 
     timer.mark("eb_search")
     # ---- error-bound search, LOOKAHEAD levels per launch
     states = []
     for s in range(S):
-        if cnt_h[s] == 0:
+        if cntg_h[s] == 0:
             states.append(None)
             continue
         eb_hi_s = float(ebhi_h[s])
@@ -565,6 +602,8 @@ def compress_device(f0: torch.Tensor, specs, dgrid: DeviceGrid, cfg, timer: Time
             call("mlk_probe", f0, stats, sh_d, S, dgrid.addr, W, L, cents, K, codes, sel_rng,
                  off_d, zero_start, int(off[-1]), rbound, cfg.tau, cand_d, n_nodes, level,
                  min(2, LOOKAHEAD - level), fail, bins, eb_hi)
+        if comm is not None:
+            comm.all_reduce_(fail, "max")
         (fail_h,) = _d2h(fail)
         for s, st in enumerate(states):
             if st is None or st.stage == "done":
@@ -622,52 +661,72 @@ def compress_device(f0: torch.Tensor, specs, dgrid: DeviceGrid, cfg, timer: Time
     zout, zoff, zlen = deflate_launch(ws, varint, vcap, vlen, n_sel, dev)
     zlen_h, exc_h, errf_h = _d2h(zlen[:max(1, n_sel)], exc_cnt, errf)
     zlen_h = zlen_h[:n_sel]
-    if int(errf_h[0]) != 0:
+    bad = [int(errf_h[0]), int(np.any(zlen_h < 0))]
+    ranks = None
+    if comm is not None:
+        # every rank's section sizes: where its pieces go in each shard blob
+        res_h = np.array([int(np.sum(21 + zlen_h[a:b])) for a, b in
+                          zip(slot_base_h, slot_base_h + cnt_h)], dtype=np.int64)
+        mine = np.concatenate([[sp.n_img for sp in specs], cnt_h, res_h, exc_h, bad]).astype(
+            np.int64)
+        allr = comm.all_gather(torch.from_numpy(mine).to(dev)).cpu().numpy()
+        ranks = dict(rank=comm.sp.rank, n=allr[:, :S], cnt=allr[:, S:2 * S],
+                     res=allr[:, 2 * S:3 * S], exc=allr[:, 3 * S:4 * S])
+        bad = allr[:, 4 * S:].max(axis=0).tolist()
+    if bad[0]:
         raise ConfigError("error bound too small for this residual range")
-    if np.any(zlen_h < 0):
+    if bad[1]:
         raise ConfigError("residual stream exceeds the device DEFLATE limits")
 
     timer.mark("pack")
-    lay = blob_layout(specs, cfg, D, cnt_h, zlen_h, exc_h)
+    lay = blob_layout(specs, cfg, D, cnt_h, zlen_h, exc_h, ranks)
     buf = T("blob", (max(1, lay["total"]),), torch.uint8)
-    # fixed pieces: 44-byte header + weights section, residual / exception prefixes
+    # fixed pieces (rank 0 of a split): 44-byte header + weights section,
+    # residual / exception section prefixes
     pieces, src, ln, dst = [], [], [], []
     pos = 0
     for s, sp in enumerate(specs):
-        for off, raw in ((lay["blob_off"][s], lay["header"][s] + sp.model.to_bytes()),
-                         (lay["res_off"][s], struct.pack("<dI", eb[s], int(cnt_h[s]))),
-                         (lay["exc_off"][s], struct.pack("<I", int(exc_h[s])))):
+        if lay["hdr_off"][s] < 0:
+            continue
+        for off, raw in ((lay["hdr_off"][s], lay["header"][s] + sp.model.to_bytes()),
+                         (lay["res_pre_off"][s], struct.pack("<dI", eb[s], int(cntg_h[s]))),
+                         (lay["exc_pre_off"][s], struct.pack("<I", int(lay["exc_total"][s])))):
             pieces.append(raw)
             src.append(pos)
             ln.append(len(raw))
             dst.append(off)
             pos += len(raw)
+    pq_s = [s for s in range(S) if lay["pq_off"][s] >= 0]
     ws.begin()
-    stage = ws.stage(np.frombuffer(b"".join(pieces), dtype=np.uint8))
-    src_d = ws.stage(np.asarray(src, np.int64))
-    ln_d = ws.stage(np.asarray(ln, np.int64))
-    dst_d = ws.stage(np.asarray(dst, np.int64))
-    pq_src = ws.stage(np.arange(0, S * 4 * L * K, 4 * L * K, dtype=np.int64))
-    pq_len = ws.stage(np.full(S, 4 * L * K, dtype=np.int64))
-    pq_off = ws.stage(lay["pq_off"])
+    if pieces:
+        stage = ws.stage(np.frombuffer(b"".join(pieces), dtype=np.uint8))
+        src_d = ws.stage(np.asarray(src, np.int64))
+        ln_d = ws.stage(np.asarray(ln, np.int64))
+        dst_d = ws.stage(np.asarray(dst, np.int64))
+        pq_src = ws.stage(np.asarray([4 * L * K * s for s in pq_s], dtype=np.int64))
+        pq_len = ws.stage(np.full(len(pq_s), 4 * L * K, dtype=np.int64))
+        pq_off = ws.stage(lay["pq_off"][pq_s])
     ent_shard = ws.stage(np.repeat(np.arange(S, dtype=np.int32), cnt_h))
     entry_off = ws.stage(lay["entry_off"])
     lam_off = ws.stage(lay["lam_off"])
     exc_base = ws.stage(np.concatenate([[0], np.cumsum(exc_h)]).astype(np.int32))
-    exc_off = ws.stage(lay["exc_off"])
+    exc_off = ws.stage(lay["exc_base"])
     ws.flush()
-    call("mlk_gather_segments", stage, src_d, ln_d, len(pieces), buf, dst_d)
-    # codes (pack_indices straight into the blob) and the PQ table
+    if pieces:
+        call("mlk_gather_segments", stage, src_d, ln_d, len(pieces), buf, dst_d)
+        call("mlk_gather_segments", cents.view(torch.uint8).reshape(-1), pq_src, pq_len,
+             len(pq_s), buf, pq_off)
+    # codes: pack_indices straight into the blob (each piece starts on a byte)
     c16 = T("codes16", (total * L,), torch.int16)
     c16.copy_(codes.reshape(-1))
-    bad = T("bad", (1,), i32)
+    bad_d = T("bad", (1,), i32)
     base = buf.data_ptr()
     for s, sp in enumerate(specs):
+        if sp.n_img == 0:
+            continue
         off = table[s].img_off
         call("mlk_pack_indices", c16[off * L:(off + sp.n_img) * L], sp.n_img * L, cfg.pq_bits,
-             base + int(lay["codes_off"][s]), bad)
-    call("mlk_gather_segments", cents.view(torch.uint8).reshape(-1), pq_src, pq_len, S, buf,
-         pq_off)
+             base + int(lay["codes_off"][s]), bad_d)
     if n_sel:
         call("mlk_pack_residuals", sel, sh_d, ent_shard, entry_off, zoff, zlen, zout, slot_base,
              dgrid.struct.rows, dgrid.struct.cols, n_sel, buf)
@@ -680,48 +739,102 @@ def compress_device(f0: torch.Tensor, specs, dgrid: DeviceGrid, cfg, timer: Time
                                status=status, iters=iters, ferr=ferr, fqoi=fqoi, fsse=fsse,
                                qoi=qoi, stats=stats, sel=sel, kinfo=kinfo),
                       sel_count=cnt_h, eb=eb, lossless=lossless, rows_cols=(
-                          dgrid.struct.rows, dgrid.struct.cols), img_off=[t.img_off for t in table])
+                          dgrid.struct.rows, dgrid.struct.cols), img_off=[t.img_off for t in table],
+                      segments=lay["segments"])
     out.timings = {"probe_rounds": rounds}
     return out
 
 
-def blob_layout(specs, cfg, D, cnt_h, zlen_h, exc_h):
-    """Byte layout of every shard blob (container.py:30-95) from the sizes."""
+def blob_layout(specs, cfg, D, cnt_h, zlen_h, exc_h, ranks=None):
+    """Byte layout of every shard blob (container.py:30-95, pipeline.py:116-184)
+    and of the pieces of it this rank writes.
+
+    ranks=None: the rank holds whole shards.  Otherwise a dict of (G, S)
+    arrays over every rank -- n (images), cnt (residual entries), res (entry
+    bytes), exc (exceptions) -- and `rank`: the blob sizes are those of the
+    whole shards, and this rank writes its member range of the codes, lambda,
+    residual-entry and exception sections (rank 0 also the header, weights,
+    PQ table and section prefixes).  Pieces are laid out in the rank's buffer
+    in blob order; `segments` maps (buffer offset, blob-region offset, length).
+    With one rank the buffer IS the blob region (a single segment)."""
     from .container import ShardHeader, SCHEME_FULL
     L, bits, K = cfg.latent_dim, cfg.pq_bits, 2 ** cfg.pq_bits
     lb = 4 if cfg.lambda_precision == "f32" else 8
     S = len(specs)
-    lay = {k: np.zeros(S, dtype=np.int64) for k in
-           ("blob_off", "blob_len", "codes_off", "pq_off", "res_off", "lam_off", "exc_off")}
+    zl_sum = np.array([int(np.sum(21 + zlen_h[a:a + c])) for a, c in
+                       zip(np.concatenate([[0], np.cumsum(cnt_h)[:-1]]).astype(np.int64), cnt_h)],
+                      dtype=np.int64)
+    if ranks is None:
+        ranks = dict(rank=0, n=np.array([[sp.n_img for sp in specs]], dtype=np.int64),
+                     cnt=np.asarray(cnt_h, np.int64)[None], res=zl_sum[None],
+                     exc=np.asarray(exc_h, np.int64)[None])
+    r = ranks["rank"]
+    n_all, res_all, exc_all = ranks["n"], ranks["res"], ranks["exc"]
+    keys = ("blob_off", "blob_len", "hdr_off", "codes_off", "pq_off", "res_pre_off", "lam_off",
+            "exc_pre_off", "exc_base", "exc_total")
+    lay = {k: np.full(S, -1, dtype=np.int64) for k in keys}
     lay["header"] = []
     entry_off = np.zeros(len(zlen_h), dtype=np.int64)
-    pos, e0 = 0, 0
-    rows = int(round(np.sqrt(D)))
+    segs = []
+    cur = [0]
+
+    def put(goff, n):
+        """Reserve n buffer bytes for blob-region bytes [goff, goff + n)."""
+        o = cur[0]
+        if n <= 0:
+            return o
+        if segs and segs[-1][0] + segs[-1][2] == o and segs[-1][1] + segs[-1][2] == goff:
+            segs[-1][2] += n
+        else:
+            segs.append([o, goff, n])
+        cur[0] += n
+        return o
+
+    gpos, e0 = 0, 0
     for s, sp in enumerate(specs):
-        n = sp.n_img
-        zl = zlen_h[e0:e0 + cnt_h[s]]
+        n = int(n_all[:, s].sum())
+        a = int(n_all[:r, s].sum())          # first member of this rank's range
+        m = int(n_all[r, s])
+        n_exc = int(exc_all[:, s].sum())
         sec = [16 + 4 * L * D, (n * L * bits + 7) // 8, 4 * L * K,
-               12 + int(np.sum(21 + zl)), n * 8 * lb, 4 + int(exc_h[s]) * (4 + 8 * D)]
-        lay["blob_off"][s] = pos
-        o = pos + 44
-        lay["codes_off"][s] = o + sec[0]
-        lay["pq_off"][s] = lay["codes_off"][s] + sec[1]
-        lay["res_off"][s] = lay["pq_off"][s] + sec[2]
-        lay["lam_off"][s] = lay["res_off"][s] + sec[3]
-        lay["exc_off"][s] = lay["lam_off"][s] + sec[4]
-        if cnt_h[s]:
-            entry_off[e0:e0 + cnt_h[s]] = lay["res_off"][s] + 12 + np.concatenate(
-                [[0], np.cumsum(21 + zl)[:-1]])
+               12 + int(res_all[:, s].sum()), n * 8 * lb, 4 + n_exc * (4 + 8 * D)]
+        g_codes = gpos + 44 + sec[0]
+        g_pq = g_codes + sec[1]
+        g_res = g_pq + sec[2]
+        g_lam = g_res + sec[3]
+        g_exc = g_lam + sec[4]
+        own0 = r == 0
+        if own0:
+            lay["hdr_off"][s] = put(gpos, 44 + sec[0])
+        c_lo = a * L * bits // 8
+        c_hi = sec[1] if a + m == n else (a + m) * L * bits // 8
+        lay["codes_off"][s] = put(g_codes + c_lo, c_hi - c_lo)
+        if own0:
+            lay["pq_off"][s] = put(g_pq, sec[2])
+            lay["res_pre_off"][s] = put(g_res, 12)
+        ent = put(g_res + 12 + int(res_all[:r, s].sum()), int(res_all[r, s]))
+        c = int(cnt_h[s])
+        if c:
+            zl = zlen_h[e0:e0 + c]
+            entry_off[e0:e0 + c] = ent + np.concatenate([[0], np.cumsum(21 + zl)[:-1]])
+        lay["lam_off"][s] = put(g_lam + a * 8 * lb, m * 8 * lb)
+        if own0:
+            lay["exc_pre_off"][s] = put(g_exc, 4)
+        lay["exc_base"][s] = put(g_exc + 4 + int(exc_all[:r, s].sum()) * (4 + 8 * D),
+                                 int(exc_all[r, s]) * (4 + 8 * D)) - 4
+        lay["exc_total"][s] = n_exc
+        lay["blob_off"][s] = gpos
         lay["blob_len"][s] = 44 + sum(sec)
         lay["header"].append(ShardHeader(scheme=SCHEME_FULL, lambda_precision=lb,
                                          section_lengths=tuple(int(x) for x in sec),
                                          n_images=n, img_rows=specs[s].rows,
                                          img_cols=specs[s].cols, latent_dim=L,
                                          pq_bits=bits).pack())
-        pos += int(lay["blob_len"][s])
-        e0 += int(cnt_h[s])
+        gpos += int(lay["blob_len"][s])
+        e0 += c
     lay["entry_off"] = entry_off
-    lay["total"] = pos
+    lay["total"] = cur[0]
+    lay["segments"] = [tuple(x) for x in segs]
     return lay
 
 
@@ -1090,6 +1203,23 @@ def shard_layout(shards, models, n_nodes, rows, cols, node_lo=0):
                              base=(p0 * n_nodes + (x0 - node_lo)) * D,
                              plane_stride=n_nodes * D, block=x1 - x0, model=m, rows=rows,
                              cols=cols))
+    return out
+
+
+def split_layout(sp, models, rows, cols):
+    """ShardWork of rank sp.rank's member range of every shard
+    (distributed.SplitPlan) in an f0 buffer holding planes
+    [sp.plane_lo, sp.plane_hi) x all nodes."""
+    D = rows * cols
+    N = sp.n_nodes
+    out = []
+    for s, sh in enumerate(sp.shards):
+        a, e = sp.range(s)
+        (p0, _), (x0, x1) = sh.planes_range, sh.nodes_range
+        out.append(ShardWork(wid=sh.worker_id, n_img=e - a,
+                             base=((p0 - sp.plane_lo) * N + x0) * D, plane_stride=N * D,
+                             block=x1 - x0, model=models[s], rows=rows, cols=cols, j0=a,
+                             n_full=len(sh.members)))
     return out
 
 

@@ -166,37 +166,41 @@ def compress_distributed(ds: FDataset, config: PipelineConfig, state: TimestepSt
                          out_path: str | None = None, group=None):
     """compress() with one process per GPU (torch.distributed initialised).
 
-    Every rank passes the same dataset description; only its own node slab
-    is uploaded to its GPU.  Ranks exchange blob sizes (all_reduce) to place
-    their shards in the archive, write them with pwrite at those offsets
-    into `out_path` (rank 0 also writes the preamble and offset index), and
-    all-reduce the report statistics.  Returns (out_path, report, new_state);
-    the report's per_image_nrmse is empty (it would gather every image)."""
+    Every rank passes the same dataset description and uploads only its
+    slab: under distributed.SplitPlan rank r processes members
+    [n_s r / G, n_s (r + 1) / G) of every shard s (whole planes when G
+    divides the plane count).  The per-shard decisions are reduced across
+    ranks inside compress_device, every rank learns the full blob sizes,
+    and each writes its pieces of every shard blob with pwrite at their
+    archive offsets into `out_path` (rank 0 also writes the preamble and the
+    offset index); the report statistics are all-reduced.  Returns
+    (out_path, report, new_state); the report's per_image_nrmse is empty
+    (it would gather every image)."""
     import os
 
     import torch.distributed as dist
 
     from . import distributed as D_
     t_all = time.perf_counter()
-    rp = D_.plan(ds.n_planes, ds.n_nodes, config.shards, config.mode)
-    _check_state(config, state, rp.n_shards)
+    sp = D_.split_plan(ds.n_planes, ds.n_nodes, config.shards, config.mode,
+                       latent_dim=config.latent_dim, pq_bits=config.pq_bits)
+    _check_state(config, state, sp.n_shards)
     dev = _device()
-    lo, hi = rp.node_range
-    f0 = upload_f0(ds.data, dev, (lo, hi))
+    f0 = upload_f0(ds.data[sp.plane_lo:sp.plane_hi], dev)
     dgrid = engine.DeviceGrid(ds.grid, dev, config.latent_dim)
-    mine = [rp.shards[i] for i in rp.mine]
-    works = engine.shard_layout(mine, [state.models[i] for i in rp.mine], hi - lo,
-                                ds.grid.rows, ds.grid.cols, node_lo=lo)
-    out = engine.compress_device(f0, works, dgrid, config)
-    preamble = ArchivePreamble(n_shards=rp.n_shards, decomp_mode=config.mode,
+    works = engine.split_layout(sp, state.models, ds.grid.rows, ds.grid.cols)
+    out = engine.compress_device(f0, works, dgrid, config, comm=D_.Comm(sp, group))
+    preamble = ArchivePreamble(n_shards=sp.n_shards, decomp_mode=config.mode,
                                n_planes=ds.n_planes, n_nodes=ds.n_nodes, grid=ds.grid,
                                timestep=ds.timestep, tau=config.tau, seed=config.seed,
                                config_digest=config.digest())
     head = preamble.pack()
-    sizes, offs = D_.exchange_sizes(rp, out.blob_lens, len(head), group)
+    sizes = np.asarray(out.blob_lens, dtype=np.int64)
+    offs = np.asarray(archive_offsets(len(head), [int(x) for x in sizes]), dtype=np.int64)
     if out_path is not None:
-        body = hostio.download_view(out.blob_buf, int(np.sum(out.blob_lens)))
-        if rp.rank == 0:
+        nbytes = max([o + n for o, _, n in out.segments], default=0)
+        body = hostio.download_view(out.blob_buf, nbytes)
+        if sp.rank == 0:
             # rewrite in place (no truncate-to-zero: an existing archive file's
             # pages are reused instead of re-allocated)
             fd = os.open(out_path, os.O_RDWR | os.O_CREAT, 0o644)
@@ -207,17 +211,17 @@ def compress_distributed(ds: FDataset, config: PipelineConfig, state: TimestepSt
                 os.close(fd)
         if dist.is_initialized():
             dist.barrier(group=group)
-        if rp.mine:
-            fd = os.open(out_path, os.O_WRONLY)
-            try:
-                base = int(offs[rp.mine[0]])
-                mv = memoryview(body)
-                spans = [(a, min(len(mv), a + hostio.CHUNK)) for a in range(0, len(mv),
-                                                                           hostio.CHUNK)]
-                list(hostio._pool().map(lambda sp: os.pwrite(fd, mv[sp[0]:sp[1]], base + sp[0]),
-                                        spans))
-            finally:
-                os.close(fd)
+        fd = os.open(out_path, os.O_WRONLY)
+        try:
+            base = int(offs[0])
+            mv = memoryview(body)
+            spans = []
+            for lo, goff, n in out.segments:
+                spans += [(lo + a, base + goff + a, min(n, a + hostio.CHUNK) - a)
+                          for a in range(0, n, hostio.CHUNK)]
+            list(hostio._pool().map(lambda x: os.pwrite(fd, mv[x[0]:x[0] + x[2]], x[1]), spans))
+        finally:
+            os.close(fd)
         if dist.is_initialized():
             dist.barrier(group=group)
     st = D_.reduce_stats(D_.report_partials(out, config.tau), group)
@@ -227,7 +231,7 @@ def compress_distributed(ds: FDataset, config: PipelineConfig, state: TimestepSt
     qspan = st["qoi_max"] - st["qoi_min"]
     qerr = {nm: float(np.sqrt(st["qoi_sse"][k] / st["qoi_cnt"][0]) / qspan[k])
             for k, nm in enumerate(names)}
-    total_bytes = len(head) + 8 * rp.n_shards + int(sizes.sum())
+    total_bytes = len(head) + 8 * sp.n_shards + int(sizes.sum())
     report = ErrorReport(
         pd_nrmse=float(np.sqrt(st["sse"][0] / ds.data.size) / span) if span > 0 else 0.0,
         per_image_nrmse=[], qoi_nrmse=qerr, max_qoi_nrmse=max(qerr.values()),
