@@ -408,10 +408,12 @@ class Workspace:
         self.pos = 0
 
     @classmethod
-    def get(cls, dev):
-        ws = cls._by_dev.get(dev.index)
+    def get(cls, dev, tag=0):
+        """The workspace `tag` of a device (compress() pipelines shard groups
+        through separate workspaces so a group's results outlive the next)."""
+        ws = cls._by_dev.get((dev.index, tag))
         if ws is None:
-            ws = cls._by_dev[dev.index] = Workspace(dev)
+            ws = cls._by_dev[(dev.index, tag)] = Workspace(dev)
         return ws
 
     def tensor(self, name, shape, dtype):
@@ -468,7 +470,7 @@ def _d2h(*tensors):
 
 
 def compress_device(f0: torch.Tensor, specs, dgrid: DeviceGrid, cfg, timer: Timer | None = None,
-                    zlib_level: int = 6, comm=None) -> CompressOut:
+                    zlib_level: int = 6, comm=None, ws_tag=0) -> CompressOut:
     """Run stages 2-5 of pipeline._compress_shard for every shard in `specs`.
 
     f0 is a flat float64 CUDA tensor holding the rank's histograms; image j
@@ -478,7 +480,8 @@ def compress_device(f0: torch.Tensor, specs, dgrid: DeviceGrid, cfg, timer: Time
     shard (distributed.SplitPlan); the per-shard decisions are made on
     collectively reduced inputs, so every rank's pieces are exactly those of
     the single-process blobs.
-    Device arrays in the result stay valid until the next call on the device.
+    Device arrays in the result stay valid until the next call on the device
+    with the same ws_tag.
     """
     dev = f0.device
     D, L, K = dgrid.D, cfg.latent_dim, 2 ** cfg.pq_bits
@@ -487,7 +490,7 @@ def compress_device(f0: torch.Tensor, specs, dgrid: DeviceGrid, cfg, timer: Time
     for sp in specs:
         if sp.model.latent_dim != L or sp.model.input_dim != D:
             raise ConfigError("shard model does not match the configuration/grid")
-    ws = Workspace.get(dev)
+    ws = Workspace.get(dev, ws_tag)
     ws.reset()
     T = ws.tensor
     f64, i32, i64 = torch.float64, torch.int32, torch.int64

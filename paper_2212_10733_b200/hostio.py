@@ -14,18 +14,24 @@ link rate and a fresh `bytes` object costs a page fault per 4 KiB, so:
 
 from __future__ import annotations
 
+import collections
 import ctypes
 import os
 import sys
+import threading
 from concurrent.futures import ThreadPoolExecutor
 
 import numpy as np
 import torch
 
-__all__ = ["upload_planes", "upload_bytes", "download_bytes", "download_view", "download_array",
-           "download_pinned_array", "pinned", "pinned_empty"]
+__all__ = ["upload_planes", "upload_pieces", "upload_bytes", "download_bytes", "download_view",
+           "download_array", "download_pinned_array", "pinned", "pinned_empty", "ArchiveWriter"]
 
 CHUNK = 64 << 20
+UP_CHUNK = 2 << 20    # upload_pieces copy granularity
+UP_DEPTH = 2          # upload_pieces copies queued on the copy engine at once
+DOWN_CHUNK = 16 << 20 # ArchiveWriter D2H granularity
+PREFAULT = os.environ.get("MLK_PREFAULT", "1") != "0"
 _POOL = None
 _PINNED = {}
 _COPY_STREAMS = {}
@@ -133,6 +139,217 @@ def upload_planes(data: np.ndarray, dev, node_range=None, pad_elems: int = 2) ->
     return buf
 
 
+class PieceUpload:
+    """Handle of upload_pieces: wait(g) orders the current stream after group
+    g's copies (blocking the host only until they have been issued)."""
+
+    def __init__(self, buf, n_groups):
+        self.buf = buf
+        self.issued = [threading.Event() for _ in range(n_groups)]
+        self.events = [None] * n_groups
+        self.error = None
+        self.thread = None
+
+    def wait(self, g):
+        self.issued[g].wait()
+        if self.error is not None:
+            raise self.error
+        torch.cuda.current_stream(self.buf.device).wait_event(self.events[g])
+
+    def join(self):
+        if self.thread is not None:
+            self.thread.join()
+        if self.error is not None:
+            raise self.error
+
+
+class UploadDone(PieceUpload):
+    """PieceUpload of a buffer whose copies are already ordered on the
+    current stream (upload_planes)."""
+
+    def __init__(self, buf):
+        super().__init__(buf, 1)
+        self.issued[0].set()
+
+    def wait(self, g):
+        pass
+
+
+def upload_pieces(data: np.ndarray, dev, groups, pad_elems: int = 2) -> PieceUpload:
+    """(P, N, ...) float64 host array -> flat device buffer of the same layout
+    (+pad_elems zeros), copied group by group: `groups` is a list of lists of
+    (plane, node_lo, node_hi) pieces.  A background thread issues the copies
+    in order on the copy stream (DMA straight from page-locked caller memory,
+    otherwise through the pinned staging buffer filled by the pool), so the
+    caller can start on group 0 while later groups are still in flight."""
+    P, N = data.shape[:2]
+    per_node = int(np.prod(data.shape[2:])) * data.itemsize
+    total = P * N * per_node
+    buf = torch.empty(total // data.itemsize + pad_elems, dtype=torch.float64, device=dev)
+    if pad_elems:
+        buf[total // data.itemsize:].zero_()
+    h = PieceUpload(buf, len(groups))
+    cs = _copy_stream(dev)
+    cs.wait_stream(torch.cuda.current_stream(dev))  # buf allocation is ordered first
+    buf.record_stream(cs)
+    flat = data.reshape(P, N * per_node // data.itemsize)
+    pinned_src = _is_pinned(data)
+    if not pinned_src:
+        stage = pinned(f"up{dev.index}", total)
+        last = _LAST_UPLOAD.get(dev.index)
+        if last is not None:
+            last.synchronize()  # the previous upload has left the staging buffer
+        st_np = stage.numpy()
+    dst = buf.view(torch.uint8)
+
+    def spans(group):
+        out = []
+        for p, lo, hi in group:
+            a0, a1 = (p * N + lo) * per_node, (p * N + hi) * per_node
+            out += [(p, lo * per_node + a - a0, min(a1, a + UP_CHUNK) - a0 + lo * per_node, a)
+                    for a in range(a0, a1, UP_CHUNK)]
+        return out
+
+    def fill(sp):
+        p, b0, b1, a = sp
+        st_np[a:a + b1 - b0] = flat[p].view(np.uint8)[b0:b1]
+        return sp
+
+    def run():
+        try:
+            torch.cuda.set_device(dev)
+            inflight = collections.deque()
+            with torch.cuda.stream(cs):
+                for g, group in enumerate(groups):
+                    sps = spans(group)
+                    it = iter(sps) if pinned_src else _pool().map(fill, sps)
+                    for p, b0, b1, a in it:
+                        # the copy engine serves copies in issue order: keep only
+                        # UP_DEPTH chunks queued so the compute stream's small
+                        # D2H reads do not wait behind the whole upload
+                        if len(inflight) >= UP_DEPTH:
+                            inflight.popleft().synchronize()
+                        src = (torch.from_numpy(flat[p].view(np.uint8)[b0:b1]) if pinned_src
+                               else stage[a:a + b1 - b0])
+                        dst[a:a + b1 - b0].copy_(src, non_blocking=True)
+                        e = torch.cuda.Event()
+                        e.record(cs)
+                        inflight.append(e)
+                    ev = torch.cuda.Event()
+                    ev.record(cs)
+                    h.events[g] = ev
+                    h.issued[g].set()
+                if not pinned_src:
+                    _LAST_UPLOAD[dev.index] = h.events[-1]
+        except BaseException as e:  # surfaced by wait()
+            h.error = e
+            for x in h.issued:
+                x.set()
+
+    h.thread = threading.Thread(target=run, daemon=True, name="mlk-upload")
+    h.thread.start()
+    return h
+
+
+class ArchiveWriter:
+    """Builds the archive `bytes` while the device is still working: each
+    shard group's blobs are copied D2H on their own stream as soon as they are
+    packed and copied into the (uninitialised, upper-bound sized) bytes object
+    by the pool; pages ahead of the write position are pre-faulted in the
+    background; finish() writes the preamble + offset index and shrinks the
+    object to its length (realloc of an mmap'd block: no copy)."""
+
+    _HINT = {}
+
+    def __init__(self, dev, cap: int, head_len: int):
+        self.dev = dev
+        self.cap = cap
+        self.head_len = head_len
+        self.obj = _new_bytes(None, cap)
+        self.addr = id(self.obj) + _BYTES_OFF
+        self.view = np.ctypeslib.as_array((ctypes.c_uint8 * cap).from_address(self.addr))
+        _advise_huge(self.view)
+        self.pos = head_len
+        self.jobs = []
+        self.d2h = _d2h_stream(dev)
+        self.n_groups = 0
+        hint = min(cap, self._HINT.get(dev.index, 0)) if PREFAULT else 0
+        self._prefault(head_len, hint)
+
+    def _prefault(self, lo, hi):
+        """Touch one byte per page of [lo, hi) in the pool (first-touch faults
+        off the critical path; the bytes are overwritten later)."""
+        step = 4096
+        spans = [(a, min(hi, a + CHUNK)) for a in range(lo, hi, CHUNK)]
+        v = self.view
+
+        def touch(sp):
+            v[sp[0]:sp[1]:step] = 0
+
+        self.prefault_jobs = [_pool().submit(touch, sp) for sp in spans]
+        self.jobs += self.prefault_jobs
+
+    def prefaulted(self):
+        """Block until the pre-faulting is done (page faults take the address
+        space lock, which the driver's host-side calls contend for)."""
+        for j in self.prefault_jobs:
+            j.result()
+
+    def add(self, src: torch.Tensor, nbytes: int):
+        """Append the first nbytes of a device uint8 tensor (enqueued after the
+        current stream's work)."""
+        if nbytes == 0:
+            return
+        if self.pos + nbytes > self.cap:
+            raise MemoryError("archive larger than its bound")
+        stage = pinned(f"arc{self.dev.index}_{self.n_groups}", nbytes)
+        self.n_groups += 1
+        self.d2h.wait_stream(torch.cuda.current_stream(self.dev))
+        st_np = stage.numpy()
+        body = self.view[self.pos:self.pos + nbytes]
+
+        def cp(job):
+            ev, a, b = job
+            ev.synchronize()
+            body[a:b] = st_np[a:b]
+
+        # chunked D2H: each chunk is copied into the bytes object as it lands
+        with torch.cuda.stream(self.d2h):
+            for a in range(0, nbytes, DOWN_CHUNK):
+                b = min(nbytes, a + DOWN_CHUNK)
+                stage[a:b].copy_(src[a:b], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(self.d2h)
+                self.jobs.append(_pool().submit(cp, (ev, a, b)))
+        src.record_stream(self.d2h)
+        self.pos += nbytes
+
+    def finish(self, head: bytes) -> bytes:
+        if len(head) != self.head_len:
+            raise ValueError("archive head length changed")
+        for j in self.jobs:
+            j.result()
+        self.view[:len(head)] = np.frombuffer(head, dtype=np.uint8)
+        n = self.pos
+        self._HINT[self.dev.index] = n
+        self.view = None
+        ref = ctypes.py_object(self.obj)
+        self.obj = None
+        if n != self.cap and _resize_bytes(ctypes.byref(ref), n) != 0:
+            raise MemoryError("could not shrink the archive")
+        return ref.value
+
+
+_D2H_STREAMS = {}
+
+
+def _d2h_stream(dev):
+    s = _D2H_STREAMS.get(dev.index)
+    if s is None:
+        s = _D2H_STREAMS[dev.index] = torch.cuda.Stream(device=dev)
+    return s
+
+
 _MADV_HUGEPAGE = 14
 _libc = None
 
@@ -156,6 +373,9 @@ _BYTES_OFF = sys.getsizeof(b"") - 1  # offset of ob_sval in a CPython bytes obje
 _new_bytes = ctypes.pythonapi.PyBytes_FromStringAndSize
 _new_bytes.restype = ctypes.py_object
 _new_bytes.argtypes = [ctypes.c_void_p, ctypes.c_ssize_t]
+_resize_bytes = ctypes.pythonapi._PyBytes_Resize
+_resize_bytes.restype = ctypes.c_int
+_resize_bytes.argtypes = [ctypes.POINTER(ctypes.py_object), ctypes.c_ssize_t]
 
 
 def download_bytes(src: torch.Tensor, nbytes: int, prefix: bytes = b"") -> bytes:

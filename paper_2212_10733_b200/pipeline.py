@@ -131,32 +131,111 @@ def _check_state(config, state, n_shards):
                           "PipelineConfig(static_model=True)")
 
 
+# compress() can pipeline shard groups: group g's node blocks are uploaded
+# while group g-1 runs on the device, and each group's blobs go D2H / into
+# the archive bytes while the next group computes.  The archive does not
+# depend on the grouping (shards are independent, pipeline.py:4-7).  Measured
+# on the B200 box (tools/e2e_groups.py, config 3, pinned f0): 1 group 63 ms,
+# 2 groups 65 ms, 4 groups 70 ms -- every group repeats the latency-bound
+# k-means / bisection / DEFLATE tails and the device step slows while the
+# upload streams in, so the default is one group (upload, then compute, with
+# the archive bytes pre-faulted and filled by the pool as chunks land).
+PIPELINE_GROUPS = 1
+_GRIDS = {}
+
+
+def _device_grid(grid, dev, latent_dim):
+    """DeviceGrid per (device, grid values, L): built once, reused by every call."""
+    key = (dev.index, latent_dim, grid.rows, grid.cols, float(grid.mass),
+           hashlib.sha1(np.ascontiguousarray(grid.vol).tobytes() + grid.v_par.tobytes()
+                        + grid.v_perp.tobytes()).digest())
+    g = _GRIDS.get(key)
+    if g is None:
+        if len(_GRIDS) > 16:
+            _GRIDS.clear()
+        g = _GRIDS[key] = engine.DeviceGrid(grid, dev, latent_dim)
+    return g
+
+
+def _groups(S, spec):
+    """Shard groups: spec = a count (even split) or a tuple of group sizes."""
+    if isinstance(spec, int):
+        G = max(1, min(spec, S))
+        return [list(range(S * g // G, S * (g + 1) // G)) for g in range(G)]
+    out, lo = [], 0
+    for n in spec:
+        if lo < S:
+            out.append(list(range(lo, min(S, lo + n))))
+            lo += n
+    if lo < S:
+        out.append(list(range(lo, S)))
+    return out
+
+
+def _archive_bound(ds, config, n_shards, head_len):
+    """Upper bound of the archive length: every image an exception AND a
+    residual payload of maximal length (section codecs, pipeline.py:116-184)."""
+    D = ds.grid.rows * ds.grid.cols
+    n = ds.n_planes * ds.n_nodes
+    per_img = (4 + 8 * D) + (21 + 10 * D + 64 + 16) + 64 + config.latent_dim * 2
+    per_shard = 44 + 16 + 4 * config.latent_dim * D + 4 * config.latent_dim * 256 + 16
+    return head_len + 8 * n_shards + n * per_img + n_shards * per_shard
+
+
 def compress(ds: FDataset, config: PipelineConfig, state: TimestepState | None = None):
     """Run the five stages on the GPU; returns (archive bytes, report, new state)."""
     t_all = time.perf_counter()
     shards = partition(ds.n_planes, ds.n_nodes, config.shards, config.mode)
     _check_state(config, state, len(shards))
     dev = _device()
-    f0 = upload_f0(ds.data, dev)
-    dgrid = engine.DeviceGrid(ds.grid, dev, config.latent_dim)
+    data = ds.data if ds.data.dtype == np.float64 else ds.data.astype(np.float64)
+    S = len(shards)
+    groups = _groups(S, PIPELINE_GROUPS)
+    pieces = [[(p, sh.nodes_range[0], sh.nodes_range[1]) for i in grp for sh in [shards[i]]
+               for p in range(*sh.planes_range)] for grp in groups]
+    if len(groups) == 1:
+        up = hostio.UploadDone(upload_f0(data, dev))
+    else:
+        up = hostio.upload_pieces(data, dev, pieces)
+    f0 = up.buf
+    dgrid = _device_grid(ds.grid, dev, config.latent_dim)
     works = engine.shard_layout(shards, state.models, ds.n_nodes, ds.grid.rows, ds.grid.cols)
-    timer = engine.Timer(True)
-    out = engine.compress_device(f0, works, dgrid, config, timer)
-    timer.mark("end")
-    stage_t = timer.result()
-    t0 = time.perf_counter()
-    preamble = ArchivePreamble(n_shards=len(shards), decomp_mode=config.mode,
+    preamble = ArchivePreamble(n_shards=S, decomp_mode=config.mode,
                                n_planes=ds.n_planes, n_nodes=ds.n_nodes, grid=ds.grid,
                                timestep=ds.timestep, tau=config.tau, seed=config.seed,
                                config_digest=config.digest())
     head = preamble.pack()
-    offs = archive_offsets(len(head), [int(n) for n in out.blob_lens])
-    archive = hostio.download_bytes(out.blob_buf, int(np.sum(out.blob_lens)),
-                                    head + struct.pack(f"<{len(offs)}Q", *offs))
-    out.dataset_index = np.concatenate([shard_dataset_index(sh, ds.n_nodes) for sh in shards])
+    head_len = len(head) + 8 * S
+    writer = hostio.ArchiveWriter(dev, _archive_bound(ds, config, S, len(head)), head_len)
+    outs, lens, timers, stage_t = [], [], [], {}
+    try:
+        for g, grp in enumerate(groups):
+            if g == 0:
+                writer.prefaulted()
+            up.wait(g)
+            timer = engine.Timer(True)
+            out = engine.compress_device(f0, [works[i] for i in grp], dgrid, config, timer,
+                                         ws_tag=g)
+            timer.mark("end")
+            timers.append(timer)
+            writer.add(out.blob_buf, int(np.sum(out.blob_lens)))
+            out.dataset_index = np.concatenate([shard_dataset_index(shards[i], ds.n_nodes)
+                                                for i in grp])
+            outs.append(out)
+            lens += [int(x) for x in out.blob_lens]
+    finally:
+        up.join()
+    t0 = time.perf_counter()
+    offs = archive_offsets(len(head), lens)
+    # the report needs only the archive length: reduce it on the device while
+    # the pool is still filling the archive bytes
+    report = build_report(ds, offs[-1] + lens[-1], outs, config.tau, stage_t, 0.0)
+    archive = writer.finish(head + struct.pack(f"<{len(offs)}Q", *offs))
+    for timer in timers:
+        for k, v in timer.result().items():
+            stage_t[k] = stage_t.get(k, 0.0) + v
     stage_t["pack"] = stage_t.get("pack", 0.0) + time.perf_counter() - t0
-    report = build_report(ds, archive, [out], config.tau, stage_t,
-                          time.perf_counter() - t_all)
+    report.stage_timings = _timings(stage_t, time.perf_counter() - t_all)
     new_state = TimestepState(models=list(state.models),
                               timestep_index=state.timestep_index + 1)
     return archive, report, new_state
@@ -245,10 +324,13 @@ def compress_distributed(ds: FDataset, config: PipelineConfig, state: TimestepSt
                                            timestep_index=state.timestep_index + 1)
 
 
-def build_report(ds, archive, outs, tau, stage_t, wall) -> ErrorReport:
+def build_report(ds, archive_len, outs, tau, stage_t, wall) -> ErrorReport:
     """pipeline._build_report (pipeline.py:367-391): every statistic reduced on
     the device, one small D2H of scalars plus the per-image list (dataset
-    order, as the reference reports it)."""
+    order, as the reference reports it).  archive_len: the archive's length
+    (or the archive itself)."""
+    if not isinstance(archive_len, (int, np.integer)):
+        archive_len = len(archive_len)
     dev = outs[0].dev["flags"].device
     cat = lambda k: torch.cat([o.dev[k] for o in outs]) if len(outs) > 1 else outs[0].dev[k]
     flags, ferr = cat("flags"), cat("ferr")
@@ -288,19 +370,23 @@ def build_report(ds, archive, outs, tau, stage_t, wall) -> ErrorReport:
             qerr[nm] = 0.0
         else:
             qerr[nm] = float(np.sqrt(d2_h[k] / cnt) / rng_k)
+    return ErrorReport(
+        pd_nrmse=pd, per_image_nrmse=host[20:].tolist(), qoi_nrmse=qerr,
+        max_qoi_nrmse=max(qerr.values()),
+        compression_ratio=compression_ratio(dataset_nbytes(ds), archive_len),
+        ae_accuracy=float(ae_ok) / n_tot, residual_fraction=float(n_sel) / n_tot,
+        convergence_fraction=float(n_conv) / n_tot, exception_count=int(n_exc),
+        stage_timings=_timings(stage_t, wall))
+
+
+def _timings(stage_t, wall):
     timings = {s: {"sum": 0.0, "max": 0.0} for s in _STAGES}
     for k, v in stage_t.items():
         if k in timings:
             timings[k] = {"sum": v, "max": v}
     rest = max(0.0, wall - sum(v for v in stage_t.values()))
     timings["other"] = {"sum": rest, "max": rest}
-    return ErrorReport(
-        pd_nrmse=pd, per_image_nrmse=host[20:].tolist(), qoi_nrmse=qerr,
-        max_qoi_nrmse=max(qerr.values()),
-        compression_ratio=compression_ratio(dataset_nbytes(ds), len(archive)),
-        ae_accuracy=float(ae_ok) / n_tot, residual_fraction=float(n_sel) / n_tot,
-        convergence_fraction=float(n_conv) / n_tot, exception_count=int(n_exc),
-        stage_timings=timings)
+    return timings
 
 
 # ---------------------------------------------------------------------------
