@@ -3,15 +3,21 @@
 Workload (default): BASELINE.json configs[2] -- D3D-scale synthetic f0,
 8 planes x 16,395 nodes x 39x39 fp64 (131,160 histograms, 1.596 GB),
 S = 8 column shards, tau = 1e-3, f32 lambdas, static AE weights trained
-once by the reference (tests/golden/cfg3.npz).  At N GPUs rank r owns shards
-[8r/N, 8(r+1)/N) and only its node slab of f0 (strong scaling of one fixed
-archive; shard count never depends on N, so the archive is identical).
+once by the reference (tests/golden/cfg3.npz).  At N GPUs rank r processes
+members [n_s r/N, n_s (r+1)/N) of every shard s (distributed.SplitPlan: plane
+r of every node block at N = 8) and holds only those planes of f0; the
+per-shard decisions are reduced over NCCL inside the step (latents
+all_gather, selection / probe all_reduces, section sizes all_gather), so the
+archive is identical for every N (strong scaling of one fixed archive).
 
   value : histograms/s of the device pipeline (f0 resident in HBM; step =
-          every stage of pipeline._compress_shard for the rank's shards,
-          shard blobs assembled, blob sizes exchanged over NCCL).
-  e2e   : the same metric through the public API (compress(ds, cfg, state)
-          at N=1: host f0 -> H2D -> device -> D2H -> archive bytes + report).
+          every stage of pipeline._compress_shard for the rank's member
+          ranges, every collective of the split, the rank's pieces of every
+          shard blob assembled at their archive offsets).
+  e2e   : the same metric through the public API: compress(ds, cfg, state)
+          at N=1 (host f0 -> H2D -> device -> D2H -> archive bytes + report),
+          compress_distributed(..., out_path) at N>1 (each rank uploads its
+          planes and pwrites its pieces into one archive file).
 Timing: CUDA events on the launching stream, barrier + synchronize on both
 sides, max over ranks.  Every step reads 1.6 GB of f0 (> 126 MB L2).
 

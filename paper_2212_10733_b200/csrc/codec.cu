@@ -432,18 +432,28 @@ __device__ __forceinline__ unsigned long long load8(const uint8_t* w, int i) {
 
 // (leading equal bytes, capped at MAX_MATCH; zlib rejects a candidate whose
 // first two bytes differ -- such lengths are < 2 here and never win, since
-// every search starts from best >= MIN_MATCH - 1)
-__device__ __forceinline__ int match_len(const uint8_t* win, int p, int c) {
-    int k = 0;
-    while (k < z6::MAX_MATCH) {
+// every search starts from best >= MIN_MATCH - 1).  Starts at k (window[p..
+// p+k) == window[c..c+k) already known) and compares 16 bytes per step; the
+// result is exact when it is < cap, otherwise it is some length >= cap that
+// is matched (a lane only needs its exact length past `cap` if it is the
+// candidate that ends the search).  Reads up to 19 bytes past p + cap: the
+// window's zero pad covers MAX_MATCH + 8, the rest of the over-read lands in
+// the warp's own chain tables and only affects bytes past MAX_MATCH.
+__device__ __forceinline__ int match_len_upto(const uint8_t* win, int p, int c, int k, int cap) {
+    while (k < cap) {
         const unsigned long long x = load8(win, p + k) ^ load8(win, c + k);
+        const unsigned long long y = load8(win, p + k + 8) ^ load8(win, c + k + 8);
         if (x) {
             k += (__ffsll((long long)x) - 1) >> 3;
             return k < z6::MAX_MATCH ? k : z6::MAX_MATCH;
         }
-        k += 8;
+        if (y) {
+            k += 8 + ((__ffsll((long long)y) - 1) >> 3);
+            return k < z6::MAX_MATCH ? k : z6::MAX_MATCH;
+        }
+        k += 16;
     }
-    return z6::MAX_MATCH;
+    return k < z6::MAX_MATCH ? k : z6::MAX_MATCH;
 }
 
 
@@ -892,9 +902,14 @@ k_deflate_warp(const uint8_t* __restrict__ in, const long long* __restrict__ in_
                 for (int r = 0; r < chain; r += 32) {
                     const int c = wz::jump(p1, p4, cb, lane);
                     const bool valid = c != 0 && r + lane < chain;
-                    const int len = valid ? wz::match_len(win, strstart, c) : 0;
+                    // lengths up to thr (exact below it), then the exact length of
+                    // the first candidate reaching thr -- the one that ends the search
+                    int len = valid ? wz::match_len_upto(win, strstart, c, 0, thr) : 0;
                     const unsigned hit = __ballot_sync(FULL, valid && len >= thr);
                     const int upto = hit ? __ffs(hit) - 1 : 31;
+                    if (hit && lane == upto)
+                        len = wz::match_len_upto(win, strstart, c, len, z6::MAX_MATCH);
+                    __syncwarp();
                     const int mx = (int)__reduce_max_sync(FULL, lane <= upto ? (unsigned)len : 0u);
                     if (mx > best) {
                         const unsigned at = __ballot_sync(FULL, lane <= upto && len == mx);

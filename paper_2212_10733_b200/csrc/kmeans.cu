@@ -185,6 +185,33 @@ __device__ __forceinline__ int pw_slot(int m, unsigned i, int& st, int& len) {
     return len <= 128 ? 1 : 2;
 }
 
+// pw_leaf (numpy's pairwise block of <= 128 values) by 8 lanes: lane `sub`
+// of an aligned 8-lane group runs accumulator r[sub] (its loads are
+// independent of the other accumulators', so they overlap), the fixed
+// ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) bracket is three xor-shuffles (fp
+// addition is commutative, so every lane forms the same sums), then the
+// len % 8 tail in order.  len < 0: no leaf (the lanes still shuffle).
+// Called by every lane of the warp.
+__device__ __forceinline__ double pw_leaf8(const double* xs, int len, int sub) {
+    const int nb = len >= 8 ? len - len % 8 : 0;
+    double r = 0.0;
+    if (nb) {
+        r = xs[sub];
+        for (int i = 8 + sub; i < nb; i += 8) r = __dadd_rn(r, xs[i]);
+    }
+    double t = __dadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 1));
+    t = __dadd_rn(t, __shfl_xor_sync(0xffffffffu, t, 2));
+    t = __dadd_rn(t, __shfl_xor_sync(0xffffffffu, t, 4));
+    double s = 0.0;
+    int i = 0;
+    if (len >= 8) {
+        s = t;
+        i = nb;
+    }
+    for (; i < len; ++i) s = __dadd_rn(s, xs[i]);
+    return s;
+}
+
 // seg k = x[seg_start[k] .. + seg_len[k]), k < nseg (nseg <= 32 * 8);
 // out[k] = its numpy pairwise sum (0 for empty segments).  Whole CTA.
 __device__ void block_pw_sums(const double* x, const int* seg_start, const int* seg_len,
@@ -215,20 +242,23 @@ __device__ void block_pw_sums(const double* x, const int* seg_start, const int* 
     }
     __syncthreads();
     const int total = base[nseg], dmax = S.bcast_i;
-    for (int t = tid; t < total; t += KT) {
-        int lo = 0, hi = nseg - 1;  // segment of slot t: last k with base[k] <= t
-        while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (base[mid] <= t) lo = mid; else hi = mid - 1;
+    // one slot per group of 8 lanes (uniform trip count: the leaf sums shuffle)
+    const int sub = tid & 7;
+    for (int t0 = 0; t0 < total; t0 += KT / 8) {
+        const int t = t0 + (tid >> 3);
+        int kd = 0, st = 0, len = -1, lo = 0;
+        if (t < total) {
+            int hi = nseg - 1;  // segment of slot t: last k with base[k] <= t
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if (base[mid] <= t) lo = mid; else hi = mid - 1;
+            }
+            const unsigned i = (unsigned)(t - base[lo]);
+            kd = i ? pw_slot(seg_len[lo], i, st, len) : 0;
+            if (sub == 0) kind[t] = (unsigned char)(kd | ((i ? 31 - __clz(i) : 0) << 2));
         }
-        const unsigned i = (unsigned)(t - base[lo]);
-        int st = 0, len = 0;
-        const int kd = i ? pw_slot(seg_len[lo], i, st, len) : 0;
-        kind[t] = (unsigned char)(kd | ((i ? 31 - __clz(i) : 0) << 2));
-        if (kd == 1) {
-            const double* xs = x + seg_start[lo] + st;
-            val[t] = pw_leaf([&](int q) { return xs[q]; }, 0, len);
-        }
+        const double r = pw_leaf8(x + seg_start[lo] + st, kd == 1 ? len : -1, sub);
+        if (kd == 1 && sub == 0) val[t] = r;
     }
     __syncthreads();
     for (int d = dmax - 1; d >= 0; --d) {

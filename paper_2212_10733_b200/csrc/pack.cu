@@ -129,7 +129,24 @@ __global__ void k_pack_exc(const double* __restrict__ f0, const MlkShard* __rest
     if (lane == 0) put_u32(d, (unsigned)(sh.j0 + j));
     const unsigned long long* x =
         reinterpret_cast<const unsigned long long*>(shard_image(f0, sh, j, D));
-    for (int q = lane; q < D; q += 32) put_u64(d + 4 + 8LL * q, x[q]);
+    // the 8D raw bytes land at any alignment: bytes up to the first 8-byte
+    // boundary and after the last one one by one (neighbouring entries own
+    // the rest of those words), whole aligned words in between, each
+    // funnel-shifted out of two source words (f0 carries a 16-byte tail pad)
+    unsigned char* r = d + 4;
+    const long long nb = 8LL * D;
+    const int head = (int)((8 - ((unsigned long long)r & 7)) & 7);
+    const long long nw = (nb - head) >> 3;
+    const long long tail0 = head + 8 * nw;
+    const unsigned char* xb = reinterpret_cast<const unsigned char*>(x);
+    if (lane < head) r[lane] = xb[lane];
+    if (lane < nb - tail0) r[tail0 + lane] = xb[tail0 + lane];
+    unsigned long long* rw = reinterpret_cast<unsigned long long*>(r + head);
+    const int sh8 = head * 8;
+    for (long long w = lane; w < nw; w += 32) {
+        const unsigned long long lo = x[w], hi = x[w + 1];
+        rw[w] = sh8 ? (lo >> sh8) | (hi << (64 - sh8)) : lo;
+    }
 }
 
 }  // namespace

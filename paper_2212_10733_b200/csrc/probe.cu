@@ -21,12 +21,12 @@ constexpr int PW_WARPS = 4;
 
 // q = rint(r / eb2): qround() in common.cuh.
 
-// `span` (1 or 2) bisection levels for every active shard in one pass over
-// the images: the shard's candidates are the node of its heap-ordered
+// `span` (1, 2 or 3) bisection levels for every active shard in one pass
+// over the images: the shard's candidates are the node of its heap-ordered
 // lookahead tree that the earlier levels' outcomes reach (node 1 = root,
 // 2i = accepted, 2i + 1 = rejected; fail[s*n_nodes + i] != 0 means node i
-// was rejected) and, for span 2, both of that node's children -- one read
-// of each histogram serves both levels.  One warp per selected image,
+// was rejected) and, for span 2 / 3, that node's children / grandchildren
+// -- one read of each histogram serves all the levels.  One warp per selected image,
 // images in ascending range order so failures surface first; a candidate is
 // skipped once its flag is set or when it passes for certain.
 // Residual-magnitude profile of every selected image, for a certified pass
@@ -41,13 +41,18 @@ constexpr int PB_NB = 34;
 
 __device__ __forceinline__ int pb_e0(double eb_hi) { return ilogb(eb_hi) - 28; }
 
+// Lane-private bins in shared memory ([bin][lane], conflict-free, no
+// atomics: an fp64 shared-memory atomicAdd is a CAS loop and the 32 lanes of
+// a warp mostly hit the same few bins), summed across lanes at the end.  The
+// order of the r^2 sums is free: the certification keeps a 1e-9 margin.
 __global__ void __launch_bounds__(32 * PW_WARPS)
 k_probe_bins(const double* __restrict__ f0, const MlkShard* __restrict__ shards, MlkGrid g,
              const float* __restrict__ W, int L, const float* __restrict__ cents, int K,
              const unsigned char* __restrict__ codes, const int* __restrict__ sel_by_range,
              const int* __restrict__ sel_count, int n_shards, const double* __restrict__ eb_hi,
              double* __restrict__ bins) {
-    __shared__ double sb[PW_WARPS][2 * PB_NB];
+    __shared__ double ssum[PW_WARPS][PB_NB][32];
+    __shared__ unsigned short scnt[PW_WARPS][PB_NB][32];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int D = g.D;
     int gw = blockIdx.x * PW_WARPS + warp;
@@ -58,9 +63,13 @@ k_probe_bins(const double* __restrict__ f0, const MlkShard* __restrict__ shards,
     const int pos = gw;
     const int j = sel_by_range[sh.img_off + pos];
     const int img = sh.img_off + j;
-    double* b = sb[warp];
-    for (int k = lane; k < 2 * PB_NB; k += 32) b[k] = 0.0;
-    __syncwarp();
+    double (*bs)[32] = ssum[warp];
+    unsigned short (*bc)[32] = scnt[warp];
+#pragma unroll
+    for (int k = 0; k < PB_NB; ++k) {
+        bs[k][lane] = 0.0;
+        bc[k][lane] = 0;
+    }
     const int e0 = pb_e0(eb_hi[s]);
     const double* x = shard_image(f0, sh, j, D);
     double z[MLK_MAXL];
@@ -80,12 +89,21 @@ k_probe_bins(const double* __restrict__ f0, const MlkShard* __restrict__ shards,
             const int e = ilogb(ar);
             bin = e < e0 ? 0 : (e >= e0 + 32 ? PB_NB - 1 : e - e0 + 1);
         }
-        atomicAdd(&b[bin], 1.0);
-        atomicAdd(&b[PB_NB + bin], r * r);
+        bc[bin][lane] += 1;
+        bs[bin][lane] += r * r;
     }
     __syncwarp();
     double* out = bins + (long long)(sh.img_off + pos) * 2 * PB_NB;
-    for (int k = lane; k < 2 * PB_NB; k += 32) out[k] = b[k];
+    for (int k = lane; k < PB_NB; k += 32) {
+        double c = 0.0, t = 0.0;
+#pragma unroll 8
+        for (int l = 0; l < 32; ++l) {
+            c += (double)bc[k][l];
+            t += bs[k][l];
+        }
+        out[k] = c;
+        out[PB_NB + k] = t;
+    }
 }
 
 // upper bound of the SSE at bound eb from an image's profile (whole warp)
@@ -103,9 +121,11 @@ __device__ __forceinline__ double pb_bound(const double* pb, int e0, double eb, 
     return warp_sum(acc);
 }
 
-constexpr int PB_MAXC = 3;
 
-__global__ void __launch_bounds__(32 * PW_WARPS, 6)
+// PB_MAXC candidates per image: 3 (span <= 2) or 7 (span 3: a node, its
+// children and grandchildren), each with its own register budget
+template <int PB_MAXC>
+__global__ void __launch_bounds__(32 * PW_WARPS, PB_MAXC == 3 ? 6 : 3)
 k_probe_level(const double* __restrict__ f0, const double* __restrict__ stats,
               const MlkShard* __restrict__ shards, MlkGrid g, PwPlan pw,
               const float* __restrict__ W, int L, const float* __restrict__ cents, int K,
@@ -132,6 +152,10 @@ k_probe_level(const double* __restrict__ f0, const double* __restrict__ stats,
     if (span > 1 && 2 * node + 1 < n_nodes) {
         nodes[nc++] = 2 * node;
         nodes[nc++] = 2 * node + 1;
+        if (span > 2 && 4 * node + 3 < n_nodes) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) nodes[nc++] = 4 * node + k;
+        }
     }
     const int pos = gw - act_off[s] + act_start[s];
     const MlkShard sh = shards[s];
@@ -249,10 +273,11 @@ extern "C" int mlk_probe(const double* f0, const double* stats, const MlkShard* 
                          int32_t n_nodes, int32_t level, int32_t span, int32_t* fail,
                          const double* bins, const double* eb_hi, cudaStream_t stream) {
     if (n_work <= 0) return MLK_OK;
-    if (n_nodes < 2 || level < 0 || span < 1 || span > 2 || (1 << level) >= n_nodes)
+    if (n_nodes < 2 || level < 0 || span < 1 || span > 3 || (1 << level) >= n_nodes)
         return MLK_ERR_CONFIG;
     PwPlan pw = mlk_make_pw_plan(grid_h->D);
-    k_probe_level<<<(n_work + PW_WARPS - 1) / PW_WARPS, 32 * PW_WARPS, 0, stream>>>(
+    auto kern = span > 2 ? k_probe_level<7> : k_probe_level<3>;
+    kern<<<(n_work + PW_WARPS - 1) / PW_WARPS, 32 * PW_WARPS, 0, stream>>>(
         f0, stats, shards, *grid_h, pw, W, L, cents, K, codes, sel_by_range, act_off, act_start,
         n_shards, recon_bound, tau, cand, n_nodes, level, span, fail, bins, eb_hi);
     return cudaGetLastError() == cudaSuccess ? MLK_OK : MLK_ERR_CUDA;

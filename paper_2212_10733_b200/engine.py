@@ -14,6 +14,7 @@ from __future__ import annotations
 
 import ctypes
 import functools
+import os
 import math
 import struct
 from dataclasses import dataclass, field
@@ -28,7 +29,8 @@ from .errors import ConfigError, FormatError, SizeMismatchError
 
 SPAN = 2.0 ** -20
 STEPS = 20
-LOOKAHEAD = 8         # bisection levels per host round trip (one probe launch each)
+LOOKAHEAD = int(os.environ.get("MLK_LOOKAHEAD", 12))  # levels per host round trip
+PASS_LEVELS = int(os.environ.get("MLK_PASS_LEVELS", 2))  # levels per probe launch
 _PAYLOAD_HEAD = struct.Struct("<BHHd")
 
 
@@ -601,10 +603,10 @@ def compress_device(f0: torch.Tensor, specs, dgrid: DeviceGrid, cfg, timer: Time
             zero_start = ws.stage(np.zeros(S, dtype=np.int32))
         ws.flush()
         fail.zero_()
-        for level in range(0, LOOKAHEAD, 2):  # two levels per pass over the images
+        for level in range(0, LOOKAHEAD, PASS_LEVELS):  # several levels per pass
             call("mlk_probe", f0, stats, sh_d, S, dgrid.addr, W, L, cents, K, codes, sel_rng,
                  off_d, zero_start, int(off[-1]), rbound, cfg.tau, cand_d, n_nodes, level,
-                 min(2, LOOKAHEAD - level), fail, bins, eb_hi)
+                 min(PASS_LEVELS, LOOKAHEAD - level), fail, bins, eb_hi)
         if comm is not None:
             comm.all_reduce_(fail, "max")
         (fail_h,) = _d2h(fail)
