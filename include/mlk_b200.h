@@ -175,6 +175,16 @@ int mlk_zlib_decompress(const uint8_t* in, const int64_t* in_off, const int64_t*
                         int32_t n, uint8_t* out, const int64_t* out_off, int64_t out_cap,
                         int64_t* out_len, cudaStream_t stream);
 
+/* fdata.gen_synthetic (fdata.py:322-347) on device, bit-identical: planes
+ * plane0 .. plane0 + n_planes - 1 of the corpus, each nd = n_nodes * D
+ * doubles, out[p * nd + e] = the numpy value.  base (nd doubles, device) is
+ * the per-node image before the per-plane rho term; pcg_h (HOST, 8 x u64):
+ * the Generator's PCG64 state and increment after seeding (hi, lo each),
+ * then the affine map of 32 steps (A^32, c_32).  Only noise == 0 corpora. */
+int mlk_synth_planes(const double* base, int64_t nd, int64_t plane0, int32_t n_planes,
+                     const uint64_t* pcg_h, double rho, double value_min, double* out,
+                     cudaStream_t stream);
+
 /* ======================= (2) stage API (one launch covers all shards) ====== */
 
 /* Pass 1 over f0 (autoencoder.encode_batch autoencoder.py:99-103 in OpenBLAS
@@ -193,6 +203,11 @@ int mlk_kmeans(const double* lat, const MlkShard* shards, const MlkShard* shards
                int32_t n_shards, int32_t L, int32_t K, const int64_t* first_idx,
                const double* draws, double* scratch, float* cents, int32_t* info,
                cudaStream_t stream);
+
+/* diagnostics: cycles of CTA 0 of the last mlk_kmeans launch in its phases
+ * (load + distinct test, k-means++ seeding, Lloyd) and its Lloyd sweeps;
+ * out_h is a HOST array of 4. */
+int mlk_kmeans_prof(int64_t* out_h, cudaStream_t stream);
 
 /* pq_encode + AE-error decision (quantizer.py:111-120; pipeline.py:228-235):
  * codes (total, L) u8; flags gets SELECTED or RECHECK.  gram holds per shard

@@ -74,6 +74,8 @@ _SIGS = {
     "mlk_zlib_decompress": [_P, _P, _P, _I32, _P, _P, _I64, _P, _P],
     "mlk_stage1": [_P, _P, _I32, _I32, _P, _P, _I32, _P, _P, _P, _P],
     "mlk_kmeans": [_P, _P, _P, _I32, _I32, _I32, _P, _P, _P, _P, _P, _P],
+    "mlk_kmeans_prof": [_P, _P],
+    "mlk_synth_planes": [_P, _I64, _I64, _I32, _P, _D, _D, _P, _P],
     "mlk_select": [_P, _P, _P, _I32, _I32, _P, _P, _I32, _I32, _P, _D, _P, _P, _P, _P, _P],
     "mlk_recheck": [_P, _P, _P, _I32, _I32, _P, _P, _I32, _P, _I32, _P, _D, _P, _P, _P],
     "mlk_compact": [_P, _P, _P, _I32, _D, _P, _P, _P, _P, _P, _P],

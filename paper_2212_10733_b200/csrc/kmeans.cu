@@ -17,6 +17,10 @@
 // One 1024-thread CTA per (shard, dim); members live in L2-resident scratch.
 #include "common.cuh"
 
+// phase clocks of the last launch's CTA 0: load + distinct test, seeding,
+// Lloyd, sweeps (read by mlk_kmeans_prof; diagnostics only)
+__device__ long long g_km_prof[4];
+
 namespace {
 
 constexpr int KT = 1024;           // threads per CTA
@@ -302,6 +306,7 @@ k_kmeans(const double* __restrict__ lat, const MlkShard* __restrict__ shards, in
     float* out = cents + ((long long)s * L + dim) * K;
     int* inf = info + (s * L + dim) * 4;
 
+    const long long kp_t0 = clock64();
     for (int j = tid; j < n; j += KT) v[j] = lat[(long long)(sh.img_off + j) * L + dim];
     __syncthreads();
 
@@ -330,6 +335,7 @@ k_kmeans(const double* __restrict__ lat, const MlkShard* __restrict__ shards, in
         }
     }
 
+    const long long kp_t1 = clock64();
     // ---- pairwise plan for length-n sums (leaves reused for every d2.sum())
     if (tid == 0) {
         S.one_start = 0;
@@ -409,6 +415,7 @@ k_kmeans(const double* __restrict__ lat, const MlkShard* __restrict__ shards, in
         __syncthreads();
     }
 
+    const long long kp_t2 = clock64();
     // ---- Lloyd (quantizer.py:78-90)
     for (int j = tid; j < n; j += KT) lab[j] = (unsigned short)nearest(v[j], S.cent, K);
     __syncthreads();
@@ -499,6 +506,12 @@ k_kmeans(const double* __restrict__ lat, const MlkShard* __restrict__ shards, in
         __syncthreads();
     }
 
+    if (tid == 0 && blockIdx.x == 0) {  // phase clocks of CTA 0 (mlk_kmeans_prof)
+        g_km_prof[0] = kp_t1 - kp_t0;
+        g_km_prof[1] = kp_t2 - kp_t1;
+        g_km_prof[2] = clock64() - kp_t2;
+        g_km_prof[3] = sweeps;
+    }
     // ---- sorted float32 codebook row
     if (tid == 0) {
         for (int a = 1; a < K; ++a) {
@@ -528,4 +541,11 @@ extern "C" int mlk_kmeans(const double* lat, const MlkShard* shards, const MlkSh
                                                 reinterpret_cast<const long long*>(first_idx),
                                                 draws, scratch, cents, info);
     return cudaGetLastError() == cudaSuccess ? MLK_OK : MLK_ERR_CUDA;
+}
+
+// diagnostics: phase clocks of the last mlk_kmeans launch's CTA 0
+extern "C" int mlk_kmeans_prof(int64_t* out_h, cudaStream_t stream) {
+    if (cudaStreamSynchronize(stream) != cudaSuccess) return MLK_ERR_CUDA;
+    return cudaMemcpyFromSymbol(out_h, g_km_prof, sizeof(long long) * 4) == cudaSuccess
+               ? MLK_OK : MLK_ERR_CUDA;
 }

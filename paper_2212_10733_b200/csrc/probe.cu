@@ -106,19 +106,25 @@ k_probe_bins(const double* __restrict__ f0, const MlkShard* __restrict__ shards,
     }
 }
 
-// upper bound of the SSE at bound eb from an image's profile (whole warp)
-__device__ __forceinline__ double pb_bound(const double* pb, int e0, double eb, double ebp) {
+// bounds of the SSE at bound eb from an image's profile (whole warp): the
+// cells of the bins entirely below eb are not quantised (rint(r / 2eb) = 0)
+// and err by exactly r, every other cell by at most ebp, so
+//   lower = sum(bins below eb) <= SSE(eb) <= lower + (other cells) ebp^2 = upper
+__device__ __forceinline__ void pb_bounds(const double* pb, int e0, double eb, double ebp,
+                                          double& lower, double& upper) {
     const int lane = threadIdx.x & 31;
-    double acc = 0.0;
+    double lo = 0.0, hi = 0.0;
     for (int k = lane; k < PB_NB; k += 32) {
         const double cnt = pb[k], sum = pb[PB_NB + k];
         bool below;
         if (k == 0) below = true;
         else if (k == PB_NB - 1) below = false;
         else below = ldexp(1.0, e0 + k) <= eb;  // bin k covers [2^(e0+k-1), 2^(e0+k))
-        acc += below ? sum : cnt * ebp * ebp;
+        lo += below ? sum : 0.0;
+        hi += below ? 0.0 : cnt * ebp * ebp;
     }
-    return warp_sum(acc);
+    lower = warp_sum(lo);
+    upper = lower + warp_sum(hi);
 }
 
 
@@ -189,8 +195,15 @@ k_probe_level(const double* __restrict__ f0, const double* __restrict__ stats,
             if (!(need & (1u << c))) continue;
             const double eb = 0.5 * eb2[c];
             const double ebp = eb + slack + eb * 1e-12;
-            const double bound = pb_bound(pb, e0, eb, ebp);
-            if (sqrt(bound / D) <= tau * range * (1.0 - 1e-9)) need &= ~(1u << c);
+            double lower, upper;
+            pb_bounds(pb, e0, eb, ebp, lower, upper);
+            if (sqrt(upper / D) <= tau * range * (1.0 - 1e-9)) {
+                need &= ~(1u << c);  // passes for certain
+            } else if (lower > 0.0 &&
+                       (range == 0.0 || sqrt(lower / D) > tau * range * (1.0 + 1e-9))) {
+                need &= ~(1u << c);  // fails for certain: no read of the image
+                if (lane == 0) atomicOr(fl + nodes[c], 1);
+            }
         }
     }
     if (!need) return;
