@@ -417,8 +417,10 @@ def main():
         dec = dict(dec or {}, max_per_image_nrmse=rep.max_per_image_nrmse() if world == 1
                    else None, ratio=rep.compression_ratio, exceptions=rep.exception_count,
                    residual_fraction=rep.residual_fraction, max_qoi_nrmse=rep.max_qoi_nrmse)
-        if world > 1 and rank == 0 and os.path.exists(shm):
-            os.unlink(shm)
+        if world > 1:
+            dist.barrier()  # every rank has read the archive size
+            if rank == 0 and os.path.exists(shm):
+                os.unlink(shm)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -29,7 +29,7 @@ from .errors import ConfigError, FormatError, SizeMismatchError
 
 SPAN = 2.0 ** -20
 STEPS = 20
-LOOKAHEAD = int(os.environ.get("MLK_LOOKAHEAD", 12))  # levels per host round trip
+LOOKAHEAD = int(os.environ.get("MLK_LOOKAHEAD", 8))  # levels per host round trip
 PASS_LEVELS = int(os.environ.get("MLK_PASS_LEVELS", 2))  # levels per probe launch
 _PAYLOAD_HEAD = struct.Struct("<BHHd")
 

@@ -11,6 +11,7 @@ from __future__ import annotations
 
 import hashlib
 import json
+import mmap
 import struct
 import time
 from dataclasses import asdict, dataclass, field
@@ -241,6 +242,26 @@ def compress(ds: FDataset, config: PipelineConfig, state: TimestepState | None =
     return archive, report, new_state
 
 
+class _Trace:
+    """MLK_TRACE=1: print the wall time of each phase (synchronised)."""
+
+    def __init__(self, tag):
+        import os
+        self.on = os.environ.get("MLK_TRACE") == "1"
+        self.tag, self.t, self.parts = tag, time.perf_counter(), []
+
+    def mark(self, name):
+        if self.on:
+            torch.cuda.synchronize()
+            t = time.perf_counter()
+            self.parts.append(f"{name} {1e3 * (t - self.t):.2f}")
+            self.t = t
+
+    def done(self):
+        if self.on:
+            print(f"[trace {self.tag}] " + " | ".join(self.parts), flush=True)
+
+
 def compress_distributed(ds: FDataset, config: PipelineConfig, state: TimestepState,
                          out_path: str | None = None, group=None):
     """compress() with one process per GPU (torch.distributed initialised).
@@ -265,10 +286,13 @@ def compress_distributed(ds: FDataset, config: PipelineConfig, state: TimestepSt
                        latent_dim=config.latent_dim, pq_bits=config.pq_bits)
     _check_state(config, state, sp.n_shards)
     dev = _device()
+    trace = _Trace(f"rank {sp.rank}")
     f0 = upload_f0(ds.data[sp.plane_lo:sp.plane_hi], dev)
-    dgrid = engine.DeviceGrid(ds.grid, dev, config.latent_dim)
+    dgrid = _device_grid(ds.grid, dev, config.latent_dim)
+    trace.mark("upload issued")
     works = engine.split_layout(sp, state.models, ds.grid.rows, ds.grid.cols)
     out = engine.compress_device(f0, works, dgrid, config, comm=D_.Comm(sp, group))
+    trace.mark("device")
     preamble = ArchivePreamble(n_shards=sp.n_shards, decomp_mode=config.mode,
                                n_planes=ds.n_planes, n_nodes=ds.n_nodes, grid=ds.grid,
                                timestep=ds.timestep, tau=config.tau, seed=config.seed,
@@ -288,22 +312,40 @@ def compress_distributed(ds: FDataset, config: PipelineConfig, state: TimestepSt
                 os.ftruncate(fd, int(offs[-1] + sizes[-1]))
             finally:
                 os.close(fd)
+        trace.mark("d2h + head")
         if dist.is_initialized():
             dist.barrier(group=group)
-        fd = os.open(out_path, os.O_WRONLY)
+        trace.mark("barrier")
+        # every rank copies its pieces into a shared mapping of the file from the
+        # pool: pwrite()s to one file serialise on its inode lock across ranks
+        fd = os.open(out_path, os.O_RDWR)
         try:
-            base = int(offs[0])
-            mv = memoryview(body)
-            spans = []
-            for lo, goff, n in out.segments:
-                spans += [(lo + a, base + goff + a, min(n, a + hostio.CHUNK) - a)
-                          for a in range(0, n, hostio.CHUNK)]
-            list(hostio._pool().map(lambda x: os.pwrite(fd, mv[x[0]:x[0] + x[2]], x[1]), spans))
+            total = int(offs[-1] + sizes[-1])
+            mm = mmap.mmap(fd, total, mmap.MAP_SHARED, mmap.PROT_WRITE | mmap.PROT_READ)
+            try:
+                dst = np.frombuffer(mm, dtype=np.uint8)
+                base = int(offs[0])
+                spans = []
+                for lo, goff, n in out.segments:
+                    spans += [(lo + a, base + goff + a, min(n, a + (8 << 20)) - a)
+                              for a in range(0, n, 8 << 20)]
+
+                def put(x):
+                    dst[x[1]:x[1] + x[2]] = body[x[0]:x[0] + x[2]]
+
+                list(hostio._pool().map(put, spans))
+                del dst
+            finally:
+                mm.close()
         finally:
             os.close(fd)
+        trace.mark("pwrite")
         if dist.is_initialized():
             dist.barrier(group=group)
+        trace.mark("barrier")
     st = D_.reduce_stats(D_.report_partials(out, config.tau), group)
+    trace.mark("report")
+    trace.done()
     n = float(st["n"][0])
     span = float(st["data_max"][0] - st["data_min"][0])
     names = ("n", "u_par", "t_perp", "t_par")
