@@ -262,6 +262,7 @@ class ShardWork:
     cols: int = 39
     j0: int = 0            # member index of image 0 (split shards, distributed.SplitPlan)
     n_full: int = -1       # images of the whole shard (-1: n_img)
+    plane0: int = 0        # plane of member 0 (plane-wise stage 1)
 
     @property
     def n_total(self) -> int:
@@ -472,7 +473,7 @@ def _d2h(*tensors):
 
 
 def compress_device(f0: torch.Tensor, specs, dgrid: DeviceGrid, cfg, timer: Timer | None = None,
-                    zlib_level: int = 6, comm=None, ws_tag=0) -> CompressOut:
+                    zlib_level: int = 6, comm=None, ws_tag=0, plane_events=None) -> CompressOut:
     """Run stages 2-5 of pipeline._compress_shard for every shard in `specs`.
 
     f0 is a flat float64 CUDA tensor holding the rank's histograms; image j
@@ -482,6 +483,9 @@ def compress_device(f0: torch.Tensor, specs, dgrid: DeviceGrid, cfg, timer: Time
     shard (distributed.SplitPlan); the per-shard decisions are made on
     collectively reduced inputs, so every rank's pieces are exactly those of
     the single-process blobs.
+    plane_events: [(plane, cuda event)] of an upload still in flight
+    (hostio.upload_planes(..., plane_events=True)): stage 1 runs plane by
+    plane as each lands, everything after it in stream order behind them all.
     Device arrays in the result stay valid until the next call on the device
     with the same ws_tag.
     """
@@ -515,13 +519,36 @@ def compress_device(f0: torch.Tensor, specs, dgrid: DeviceGrid, cfg, timer: Time
         shf_d = ws.stage(np.frombuffer(bytes(table_full), dtype=np.uint8))
     else:
         table_full, shf_d = table, sh_d
+    plane_tabs = []
+    for p, ev in plane_events or ():
+        # the members of every shard that lie on plane p (plane-major order)
+        ents = []
+        for si, sp in enumerate(specs):
+            q = p - sp.plane0
+            if sp.n_img % sp.block or sp.j0 % sp.block or not 0 <= q < sp.n_img // sp.block:
+                continue
+            e = MlkShard.from_buffer_copy(table[si])
+            e.n_img, e.img_off, e.j0 = sp.block, e.img_off + q * sp.block, e.j0 + q * sp.block
+            ents.append(e)
+        arr = (MlkShard * max(1, len(ents)))(*ents)
+        plane_tabs.append((ev, ws.stage(np.frombuffer(bytes(arr), dtype=np.uint8)), len(ents),
+                           sum(e.n_img for e in ents)))
+    if plane_tabs and sum(t[3] for t in plane_tabs) != total:
+        raise ConfigError("plane-wise stage 1 needs shards made of whole planes")
     ws.flush()
 
     timer.mark("encode")
     lat = T("lat", (total, L), f64)
     stats = T("stats", (total, 4), f64)
     qoi = T("qoi", (total, 4), f64)
-    call("mlk_stage1", f0, sh_d, S, total, dgrid.addr, W, L, lat, stats, qoi)
+    if plane_tabs:
+        main = torch.cuda.current_stream(dev)
+        for ev, tab_d, n_ent, n_pl in plane_tabs:
+            main.wait_event(ev)
+            if n_ent:
+                call("mlk_stage1", f0, tab_d, n_ent, n_pl, dgrid.addr, W, L, lat, stats, qoi)
+    else:
+        call("mlk_stage1", f0, sh_d, S, total, dgrid.addr, W, L, lat, stats, qoi)
 
     timer.mark("pq")
     lat_km, total_km = lat, total
@@ -1207,7 +1234,7 @@ def shard_layout(shards, models, n_nodes, rows, cols, node_lo=0):
         out.append(ShardWork(wid=sh.worker_id, n_img=len(sh.members),
                              base=(p0 * n_nodes + (x0 - node_lo)) * D,
                              plane_stride=n_nodes * D, block=x1 - x0, model=m, rows=rows,
-                             cols=cols))
+                             cols=cols, plane0=p0))
     return out
 
 

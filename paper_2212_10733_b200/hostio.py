@@ -78,9 +78,14 @@ def pinned_empty(shape, dtype=np.float64) -> np.ndarray:
     return host.numpy()[:nbytes].view(dtype).reshape(shape)
 
 
-def upload_planes(data: np.ndarray, dev, node_range=None, pad_elems: int = 2) -> torch.Tensor:
+def upload_planes(data: np.ndarray, dev, node_range=None, pad_elems: int = 2,
+                  plane_events: bool = False):
     """data[:, lo:hi] of a (P, N, ...) float64 array -> flat device buffer
-    (+pad_elems zeros of tail padding), on the current stream's timeline."""
+    (+pad_elems zeros of tail padding), on the current stream's timeline.
+
+    plane_events=True returns (buf, [event per plane]) and leaves the ordering
+    to the caller: the current stream must wait on plane p's event before it
+    reads plane p (compress_device runs stage 1 plane by plane as they land)."""
     P, N = data.shape[:2]
     lo, hi = node_range or (0, N)
     per_node = int(np.prod(data.shape[2:])) * data.itemsize
@@ -89,55 +94,60 @@ def upload_planes(data: np.ndarray, dev, node_range=None, pad_elems: int = 2) ->
     buf = torch.empty(total // data.itemsize + pad_elems, dtype=torch.float64, device=dev)
     if pad_elems:
         buf[total // data.itemsize:].zero_()
+    events = []
     if total == 0:
-        return buf
+        return (buf, events) if plane_events else buf
+    cs = _copy_stream(dev)
+    cs.wait_stream(torch.cuda.current_stream(dev))  # buf allocation is ordered first
+    dst = buf.view(torch.uint8)
     if _is_pinned(data):
         # the caller's array is page-locked: DMA each plane slab directly
-        cs = _copy_stream(dev)
-        cs.wait_stream(torch.cuda.current_stream(dev))
         src = torch.from_numpy(data.reshape(P, -1).view(np.uint8))
-        dst = buf.view(torch.uint8)
         with torch.cuda.stream(cs):
             for p in range(P):
                 dst[p * slab:(p + 1) * slab].copy_(src[p, lo * per_node:hi * per_node],
                                                    non_blocking=True)
+                if plane_events:
+                    e = torch.cuda.Event()
+                    e.record(cs)
+                    events.append(e)
         ev = torch.cuda.Event()
         ev.record(cs)
-        torch.cuda.current_stream(dev).wait_event(ev)
-        buf.record_stream(cs)
-        return buf
-    stage = pinned(f"up{dev.index}", total)
-    last = _LAST_UPLOAD.get(dev.index)
-    if last is not None:
-        last.synchronize()  # the previous upload has left the staging buffer
-    st_np = stage.numpy()
-    dst = buf.view(torch.uint8)
-    # (plane, byte range within the slab) pieces of <= CHUNK bytes
-    pieces = []
-    for p in range(P):
-        for a in range(0, slab, CHUNK):
-            pieces.append((p, a, min(slab, a + CHUNK)))
-    src2d = data.reshape(P, N * per_node // data.itemsize)
+    else:
+        stage = pinned(f"up{dev.index}", total)
+        last = _LAST_UPLOAD.get(dev.index)
+        if last is not None:
+            last.synchronize()  # the previous upload has left the staging buffer
+        st_np = stage.numpy()
+        # (plane, byte range within the slab) pieces of <= CHUNK bytes
+        pieces = []
+        for p in range(P):
+            for a in range(0, slab, CHUNK):
+                pieces.append((p, a, min(slab, a + CHUNK)))
+        src2d = data.reshape(P, N * per_node // data.itemsize)
 
-    def fill(piece):
-        p, a, b = piece
-        row = src2d[p].view(np.uint8)[lo * per_node:hi * per_node]
-        st_np[p * slab + a:p * slab + b] = row[a:b]
-        return piece
+        def fill(piece):
+            p, a, b = piece
+            row = src2d[p].view(np.uint8)[lo * per_node:hi * per_node]
+            st_np[p * slab + a:p * slab + b] = row[a:b]
+            return piece
 
-    cs = _copy_stream(dev)
-    cs.wait_stream(torch.cuda.current_stream(dev))  # buf allocation is ordered first
-    with torch.cuda.stream(cs):
-        for p, a, b in _pool().map(fill, pieces):
-            o = p * slab
-            dst[o + a:o + b].copy_(stage[o + a:o + b], non_blocking=True)
-    ev = torch.cuda.Event()
-    ev.record(cs)
-    _LAST_UPLOAD[dev.index] = ev
-    torch.cuda.current_stream(dev).wait_event(ev)
+        with torch.cuda.stream(cs):
+            for p, a, b in _pool().map(fill, pieces):
+                o = p * slab
+                dst[o + a:o + b].copy_(stage[o + a:o + b], non_blocking=True)
+                if plane_events and b == slab:
+                    e = torch.cuda.Event()
+                    e.record(cs)
+                    events.append(e)
+        ev = torch.cuda.Event()
+        ev.record(cs)
+        _LAST_UPLOAD[dev.index] = ev
     buf.record_stream(cs)
+    if plane_events:
+        return buf, events
+    torch.cuda.current_stream(dev).wait_event(ev)
     return buf
-
 
 class PieceUpload:
     """Handle of upload_pieces: wait(g) orders the current stream after group

@@ -194,8 +194,12 @@ def compress(ds: FDataset, config: PipelineConfig, state: TimestepState | None =
     groups = _groups(S, PIPELINE_GROUPS)
     pieces = [[(p, sh.nodes_range[0], sh.nodes_range[1]) for i in grp for sh in [shards[i]]
                for p in range(*sh.planes_range)] for grp in groups]
+    plane_events = None
     if len(groups) == 1:
-        up = hostio.UploadDone(upload_f0(data, dev))
+        # stage 1 of plane p starts as soon as plane p has landed
+        buf, evs = hostio.upload_planes(data, dev, plane_events=True)
+        up = hostio.UploadDone(buf)
+        plane_events = list(enumerate(evs))
     else:
         up = hostio.upload_pieces(data, dev, pieces)
     f0 = up.buf
@@ -216,7 +220,7 @@ def compress(ds: FDataset, config: PipelineConfig, state: TimestepState | None =
             up.wait(g)
             timer = engine.Timer(True)
             out = engine.compress_device(f0, [works[i] for i in grp], dgrid, config, timer,
-                                         ws_tag=g)
+                                         ws_tag=g, plane_events=plane_events)
             timer.mark("end")
             timers.append(timer)
             writer.add(out.blob_buf, int(np.sum(out.blob_lens)))

@@ -16,3 +16,11 @@ timeout 900 ncu --set full --import-source on --clock-control none -k regex:'k_d
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:'k_probe_level' \
   --launch-skip 12 --launch-count 12 -f -o gpurun_out/full_c $B > gpurun_out/ncu_c.log 2>&1; echo full_c=$?
 ls -la gpurun_out/*.ncu-rep
+# summaries on the box (the .ncu-rep files would exceed gpurun_out's 64 MiB)
+python tools/ncu_summary.py gpurun_out/full_a.ncu-rep gpurun_out/full_b.ncu-rep \
+  gpurun_out/full_c.ncu-rep --launches gpurun_out/launches.csv --out gpurun_out/prof; echo summary=$?
+ncu -i gpurun_out/full_a.ncu-rep --page source --csv --print-units base > gpurun_out/src_a.csv 2>/dev/null
+gzip -f gpurun_out/src_a.csv
+[ $(stat -c %s gpurun_out/src_a.csv.gz) -gt 30000000 ] && rm -f gpurun_out/src_a.csv.gz
+rm -f gpurun_out/full_*.ncu-rep
+du -sh gpurun_out
