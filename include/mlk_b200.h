@@ -314,6 +314,13 @@ int mlk_parse_residual_section(const uint8_t* sec, int64_t len, int32_t n_images
 /* HOST: 1 if p lies in page-locked host memory (cudaHostAlloc/Register). */
 int mlk_is_pinned(const void* p);
 
+/* HOST memory only: exception entries <I idx[k]> + 8 D bytes of the host
+ * histogram at src + src_off[k] (elements), back to back at dst
+ * (pipeline.py:116-184, 281-292).  compress() fills the archive's exception
+ * sections from its own input with it instead of a device -> host copy. */
+int mlk_host_exception_entries(uint8_t* dst, const double* src, const int64_t* src_off,
+                               const uint32_t* idx, int64_t n, int32_t D);
+
 /* ---- shard-blob assembly on device (container.py:90-95, pipeline.py:116-184) */
 
 /* list[img_off + r] = r-th image of shard s (ascending) with flags & mask;

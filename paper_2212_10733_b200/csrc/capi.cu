@@ -289,3 +289,25 @@ extern "C" int mlk_is_pinned(const void* p) {
     }
     return a.type == cudaMemoryTypeHost ? 1 : 0;
 }
+
+// Host side of the exceptions section (pipeline.py:281-292, 116-184): entry k
+// is <I idx[k]> + the D doubles of the original histogram at
+// src + src_off[k] (element offsets into the caller's host f0).  compress()
+// writes these straight from its input into the archive instead of copying
+// them back from the device (they are the input's own bytes).
+extern "C" int mlk_host_exception_entries(uint8_t* dst, const double* src,
+                                          const int64_t* src_off, const uint32_t* idx,
+                                          int64_t n, int32_t D) {
+    if (n < 0 || D <= 0) return MLK_ERR_DIM;
+    const size_t row = 8u * (size_t)D;
+    for (int64_t k = 0; k < n; ++k) {
+        uint8_t* d = dst + (size_t)k * (4 + row);
+        const uint32_t v = idx[k];
+        d[0] = (uint8_t)v;
+        d[1] = (uint8_t)(v >> 8);
+        d[2] = (uint8_t)(v >> 16);
+        d[3] = (uint8_t)(v >> 24);
+        memcpy(d + 4, src + src_off[k], row);
+    }
+    return MLK_OK;
+}

@@ -79,6 +79,7 @@ k_probe_bins(const double* __restrict__ f0, const MlkShard* __restrict__ shards,
                      : 0.0;
     const float* Ws = W + sh.w_off;
     const bool blas_tree = !sh.small_blas;
+    #pragma unroll 2  // two cells' loads in flight per lane
     for (int q = lane; q < D; q += 32) {
         const double rc = decode_cell(z, Ws, L, D, q, blas_tree && g.tree_cols[q], sh.mean, sh.std);
         const double r = __dsub_rn(x[q], rc);
@@ -216,6 +217,7 @@ k_probe_level(const double* __restrict__ f0, const double* __restrict__ stats,
     const float* Ws = W + sh.w_off;
     const bool blas_tree = !sh.small_blas;
     // approximate SSEs (any order), exact only near the threshold
+    #pragma unroll 2  // two cells' loads in flight per lane
     for (int q = lane; q < D; q += 32) {
         const double o = x[q];
         const double rc = decode_cell(z, Ws, L, D, q, blas_tree && g.tree_cols[q], sh.mean, sh.std);

@@ -284,6 +284,7 @@ class CompressOut:
     rows_cols: tuple
     img_off: list
     segments: list = field(default_factory=list)  # (buf offset, blob-region offset, length)
+    exceptions: list = None  # per shard (buf offset of its entries, member indices)
     timings: dict = field(default_factory=dict)
     _host: dict = field(default_factory=dict)
 
@@ -483,9 +484,12 @@ def compress_device(f0: torch.Tensor, specs, dgrid: DeviceGrid, cfg, timer: Time
     shard (distributed.SplitPlan); the per-shard decisions are made on
     collectively reduced inputs, so every rank's pieces are exactly those of
     the single-process blobs.
-    plane_events: [(plane, cuda event)] of an upload still in flight
-    (hostio.upload_planes(..., plane_events=True)): stage 1 runs plane by
-    plane as each lands, everything after it in stream order behind them all.
+    plane_events: a callable that starts the upload of f0 and returns
+    [(plane, cuda event)] (hostio.upload_planes(..., plane_events=True)): it
+    is called once this call's own small host->device copies are queued (the
+    copy engine serves copies in order, so they must not wait behind the
+    upload), and stage 1 then runs plane by plane as each lands, everything
+    after it in stream order behind them all.
     Device arrays in the result stay valid until the next call on the device
     with the same ws_tag.
     """
@@ -520,7 +524,9 @@ def compress_device(f0: torch.Tensor, specs, dgrid: DeviceGrid, cfg, timer: Time
     else:
         table_full, shf_d = table, sh_d
     plane_tabs = []
-    for p, ev in plane_events or ():
+    planes = list(range(max((sp.plane0 + sp.n_img // max(1, sp.block) for sp in specs),
+                            default=0))) if plane_events is not None else []
+    for p in planes:
         # the members of every shard that lie on plane p (plane-major order)
         ents = []
         for si, sp in enumerate(specs):
@@ -531,11 +537,14 @@ def compress_device(f0: torch.Tensor, specs, dgrid: DeviceGrid, cfg, timer: Time
             e.n_img, e.img_off, e.j0 = sp.block, e.img_off + q * sp.block, e.j0 + q * sp.block
             ents.append(e)
         arr = (MlkShard * max(1, len(ents)))(*ents)
-        plane_tabs.append((ev, ws.stage(np.frombuffer(bytes(arr), dtype=np.uint8)), len(ents),
+        plane_tabs.append((p, ws.stage(np.frombuffer(bytes(arr), dtype=np.uint8)), len(ents),
                            sum(e.n_img for e in ents)))
     if plane_tabs and sum(t[3] for t in plane_tabs) != total:
         raise ConfigError("plane-wise stage 1 needs shards made of whole planes")
     ws.flush()
+    if plane_events is not None:
+        evs = dict(plane_events())
+        plane_tabs = [(evs[p], tab_d, n_ent, n_pl) for p, tab_d, n_ent, n_pl in plane_tabs]
 
     timer.mark("encode")
     lat = T("lat", (total, L), f64)
@@ -691,7 +700,11 @@ def compress_device(f0: torch.Tensor, specs, dgrid: DeviceGrid, cfg, timer: Time
 
     timer.mark("deflate")
     zout, zoff, zlen = deflate_launch(ws, varint, vcap, vlen, n_sel, dev)
-    zlen_h, exc_h, errf_h = _d2h(zlen[:max(1, n_sel)], exc_cnt, errf)
+    if comm is None:
+        zlen_h, exc_h, errf_h, excl_h = _d2h(zlen[:max(1, n_sel)], exc_cnt, errf, exc_list)
+    else:
+        zlen_h, exc_h, errf_h = _d2h(zlen[:max(1, n_sel)], exc_cnt, errf)
+        excl_h = None
     zlen_h = zlen_h[:n_sel]
     bad = [int(errf_h[0]), int(np.any(zlen_h < 0))]
     ranks = None
@@ -773,6 +786,12 @@ def compress_device(f0: torch.Tensor, specs, dgrid: DeviceGrid, cfg, timer: Time
                       sel_count=cnt_h, eb=eb, lossless=lossless, rows_cols=(
                           dgrid.struct.rows, dgrid.struct.cols), img_off=[t.img_off for t in table],
                       segments=lay["segments"])
+    if excl_h is not None:
+        # where each shard's exception entries sit in blob_buf, and whose they
+        # are (member indices), for callers that fill them from host f0
+        out.exceptions = [(int(lay["exc_base"][s]) + 4,
+                           excl_h[table[s].img_off:table[s].img_off + int(exc_h[s])].astype(np.int64)
+                           + table[s].j0) for s in range(S)]
     out.timings = {"probe_rounds": rounds}
     return out
 

@@ -78,22 +78,32 @@ def pinned_empty(shape, dtype=np.float64) -> np.ndarray:
     return host.numpy()[:nbytes].view(dtype).reshape(shape)
 
 
+def device_planes_buffer(data: np.ndarray, dev, node_range=None, pad_elems: int = 2):
+    """The (uninitialised) device buffer upload_planes fills, tail pad zeroed."""
+    P, N = data.shape[:2]
+    lo, hi = node_range or (0, N)
+    n = P * (hi - lo) * int(np.prod(data.shape[2:]))
+    buf = torch.empty(n + pad_elems, dtype=torch.float64, device=dev)
+    if pad_elems:
+        buf[n:].zero_()
+    return buf
+
+
 def upload_planes(data: np.ndarray, dev, node_range=None, pad_elems: int = 2,
-                  plane_events: bool = False):
+                  plane_events: bool = False, into: torch.Tensor | None = None):
     """data[:, lo:hi] of a (P, N, ...) float64 array -> flat device buffer
     (+pad_elems zeros of tail padding), on the current stream's timeline.
 
     plane_events=True returns (buf, [event per plane]) and leaves the ordering
     to the caller: the current stream must wait on plane p's event before it
-    reads plane p (compress_device runs stage 1 plane by plane as they land)."""
+    reads plane p (compress_device runs stage 1 plane by plane as they land).
+    into: a buffer from device_planes_buffer to fill instead of a new one."""
     P, N = data.shape[:2]
     lo, hi = node_range or (0, N)
     per_node = int(np.prod(data.shape[2:])) * data.itemsize
     slab = (hi - lo) * per_node
     total = P * slab
-    buf = torch.empty(total // data.itemsize + pad_elems, dtype=torch.float64, device=dev)
-    if pad_elems:
-        buf[total // data.itemsize:].zero_()
+    buf = into if into is not None else device_planes_buffer(data, dev, node_range, pad_elems)
     events = []
     if total == 0:
         return (buf, events) if plane_events else buf
@@ -280,6 +290,7 @@ class ArchiveWriter:
         self.view = np.ctypeslib.as_array((ctypes.c_uint8 * cap).from_address(self.addr))
         _advise_huge(self.view)
         self.pos = head_len
+        self.d2h_bytes = 0
         self.jobs = []
         self.d2h = _d2h_stream(dev)
         self.n_groups = 0
@@ -332,6 +343,49 @@ class ArchiveWriter:
                 ev.record(self.d2h)
                 self.jobs.append(_pool().submit(cp, (ev, a, b)))
         src.record_stream(self.d2h)
+        self.pos += nbytes
+        self.d2h_bytes += nbytes
+
+    def add_with_host_rows(self, src: torch.Tensor, nbytes: int, holes, fill):
+        """add() for a buffer whose byte ranges `holes` [(offset, length)] are
+        written from host memory by fill(view, offset, length) jobs instead
+        of being copied back from the device."""
+        if not holes:
+            return self.add(src, nbytes)
+        base = self.pos
+        if base + nbytes > self.cap:
+            raise MemoryError("archive larger than its bound")
+        holes = sorted((int(o), int(n)) for o, n in holes if n > 0)
+        stage = pinned(f"arc{self.dev.index}_{self.n_groups}", nbytes)
+        self.n_groups += 1
+        self.d2h.wait_stream(torch.cuda.current_stream(self.dev))
+        st_np = stage.numpy()
+        body = self.view[base:base + nbytes]
+
+        def cp(job):
+            ev, a, b = job
+            ev.synchronize()
+            body[a:b] = st_np[a:b]
+
+        spans, pos = [], 0
+        for o, n in holes:
+            if o > pos:
+                spans.append((pos, o))
+            pos = o + n
+        if pos < nbytes:
+            spans.append((pos, nbytes))
+        with torch.cuda.stream(self.d2h):
+            for lo, hi in spans:
+                for a in range(lo, hi, DOWN_CHUNK):
+                    b = min(hi, a + DOWN_CHUNK)
+                    stage[a:b].copy_(src[a:b], non_blocking=True)
+                    ev = torch.cuda.Event()
+                    ev.record(self.d2h)
+                    self.jobs.append(_pool().submit(cp, (ev, a, b)))
+                self.d2h_bytes += hi - lo
+        src.record_stream(self.d2h)
+        for o, n in holes:
+            self.jobs += fill(body, o, n)
         self.pos += nbytes
 
     def finish(self, head: bytes) -> bytes:

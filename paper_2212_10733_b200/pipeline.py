@@ -9,6 +9,7 @@ archives are identical for any worker or GPU count (pipeline.py:4-7).
 
 from __future__ import annotations
 
+import ctypes
 import hashlib
 import json
 import mmap
@@ -143,6 +144,8 @@ def _check_state(config, state, n_shards):
 # the archive bytes pre-faulted and filled by the pool as chunks land).
 PIPELINE_GROUPS = 1
 _GRIDS = {}
+# bytes the last compress() moved over PCIe (diagnostics; bench.py's e2e)
+LAST_CALL = {}
 
 
 def _device_grid(grid, dev, latent_dim):
@@ -173,6 +176,44 @@ def _groups(S, spec):
     return out
 
 
+def _exception_fills(out, shards, data, ds):
+    """Holes (buffer offset, length) of the exception entries of `out`'s
+    shards and a fill(view, offset, length) that writes them from the host
+    f0 with mlk_host_exception_entries in pool-sized chunks."""
+    from ._lib import lib
+    D = ds.grid.rows * ds.grid.cols
+    row = 4 + 8 * D
+    src = np.ascontiguousarray(data)
+    holes, srcs = [], {}
+    for (off, members), sh in zip(out.exceptions, shards):
+        if members.size == 0:
+            continue
+        (p0, _), (x0, x1) = sh.planes_range, sh.nodes_range
+        b = x1 - x0
+        elem = ((p0 + members // b) * ds.n_nodes + x0 + members % b) * D
+        holes.append((off, members.size * row))
+        srcs[off] = (np.ascontiguousarray(elem, dtype=np.int64),
+                     np.ascontiguousarray(members, dtype=np.uint32))
+
+    def fill(view, off, length):
+        elem, idx = srcs[off]
+        n = idx.size
+        per = max(1, (8 << 20) // row)
+
+        def job(a):
+            k = min(n, a + per) - a
+            rc = lib().mlk_host_exception_entries(
+                ctypes.c_void_p(view[off + a * row:].ctypes.data),
+                ctypes.c_void_p(src.ctypes.data), ctypes.c_void_p(elem[a:].ctypes.data),
+                ctypes.c_void_p(idx[a:].ctypes.data), k, D)
+            if rc != 0:
+                raise RuntimeError("mlk_host_exception_entries failed")
+
+        return [hostio._pool().submit(job, a) for a in range(0, n, per)]
+
+    return holes, fill
+
+
 def _archive_bound(ds, config, n_shards, head_len):
     """Upper bound of the archive length: every image an exception AND a
     residual payload of maximal length (section codecs, pipeline.py:116-184)."""
@@ -196,13 +237,17 @@ def compress(ds: FDataset, config: PipelineConfig, state: TimestepState | None =
                for p in range(*sh.planes_range)] for grp in groups]
     plane_events = None
     if len(groups) == 1:
-        # stage 1 of plane p starts as soon as plane p has landed
-        buf, evs = hostio.upload_planes(data, dev, plane_events=True)
-        up = hostio.UploadDone(buf)
-        plane_events = list(enumerate(evs))
+        # stage 1 of plane p starts as soon as plane p has landed; the upload
+        # is started by compress_device once its own small copies are queued
+        f0 = hostio.device_planes_buffer(data, dev)
+        up = hostio.UploadDone(f0)
+
+        def plane_events():
+            return list(enumerate(hostio.upload_planes(data, dev, plane_events=True,
+                                                       into=f0)[1]))
     else:
         up = hostio.upload_pieces(data, dev, pieces)
-    f0 = up.buf
+        f0 = up.buf
     dgrid = _device_grid(ds.grid, dev, config.latent_dim)
     works = engine.shard_layout(shards, state.models, ds.n_nodes, ds.grid.rows, ds.grid.cols)
     preamble = ArchivePreamble(n_shards=S, decomp_mode=config.mode,
@@ -215,27 +260,36 @@ def compress(ds: FDataset, config: PipelineConfig, state: TimestepState | None =
     outs, lens, timers, stage_t = [], [], [], {}
     try:
         for g, grp in enumerate(groups):
-            if g == 0:
-                writer.prefaulted()
             up.wait(g)
             timer = engine.Timer(True)
             out = engine.compress_device(f0, [works[i] for i in grp], dgrid, config, timer,
                                          ws_tag=g, plane_events=plane_events)
             timer.mark("end")
             timers.append(timer)
-            writer.add(out.blob_buf, int(np.sum(out.blob_lens)))
             out.dataset_index = np.concatenate([shard_dataset_index(shards[i], ds.n_nodes)
                                                 for i in grp])
             outs.append(out)
+            if g == len(groups) - 1:
+                # the report needs only the archive length: its reductions and
+                # small D2H go ahead of the last blob download
+                rep_h = report_launch(outs)
+            if out.exceptions is not None:
+                # exception entries are the input's own bytes: written from
+                # the host f0 by the pool, only the rest comes back over PCIe
+                holes, fills = _exception_fills(out, [shards[i] for i in grp], data, ds)
+                writer.add_with_host_rows(out.blob_buf, int(np.sum(out.blob_lens)), holes,
+                                          fills)
+            else:
+                writer.add(out.blob_buf, int(np.sum(out.blob_lens)))
             lens += [int(x) for x in out.blob_lens]
     finally:
         up.join()
     t0 = time.perf_counter()
     offs = archive_offsets(len(head), lens)
-    # the report needs only the archive length: reduce it on the device while
-    # the pool is still filling the archive bytes
-    report = build_report(ds, offs[-1] + lens[-1], outs, config.tau, stage_t, 0.0)
+    report = report_finish(rep_h, ds, offs[-1] + lens[-1], config.tau, stage_t, 0.0)
     archive = writer.finish(head + struct.pack(f"<{len(offs)}Q", *offs))
+    LAST_CALL.update(h2d_bytes=int(data.nbytes), d2h_bytes=int(writer.d2h_bytes),
+                     host_filled_bytes=len(archive) - int(writer.d2h_bytes))
     for timer in timers:
         for k, v in timer.result().items():
             stage_t[k] = stage_t.get(k, 0.0) + v
@@ -375,8 +429,13 @@ def build_report(ds, archive_len, outs, tau, stage_t, wall) -> ErrorReport:
     the device, one small D2H of scalars plus the per-image list (dataset
     order, as the reference reports it).  archive_len: the archive's length
     (or the archive itself)."""
-    if not isinstance(archive_len, (int, np.integer)):
-        archive_len = len(archive_len)
+    return report_finish(report_launch(outs), ds, archive_len, tau, stage_t, wall)
+
+
+def report_launch(outs):
+    """The device half of build_report: reductions and one async D2H into
+    page-locked memory, queued ahead of the archive download (the copy
+    engine serves copies in order)."""
     dev = outs[0].dev["flags"].device
     cat = lambda k: torch.cat([o.dev[k] for o in outs]) if len(outs) > 1 else outs[0].dev[k]
     flags, ferr = cat("flags"), cat("ferr")
@@ -384,7 +443,8 @@ def build_report(ds, archive_len, outs, tau, stage_t, wall) -> ErrorReport:
     fsse, status = cat("fsse"), cat("status")
     n_tot = flags.numel()
     exc = (flags & F_EXCEPTION) != 0
-    order = torch.from_numpy(np.concatenate([o.dataset_index for o in outs])).to(dev)
+    order = torch.from_numpy(np.concatenate([o.dataset_index for o in outs])).pin_memory().to(
+        dev, non_blocking=True)
     per_image = torch.empty(n_tot, dtype=torch.float64, device=dev)
     per_image[order] = torch.where(exc, torch.zeros_like(ferr), ferr)
     # QoI errors over the nodes with positive density (qoi.py:122-133)
@@ -399,7 +459,21 @@ def build_report(ds, archive_len, outs, tau, stage_t, wall) -> ErrorReport:
         ((flags & (F_SELECTED | F_NONFINITE)) == 0).sum().to(torch.float64),
         ((flags & F_SELECTED) != 0).sum().to(torch.float64),
         exc.sum().to(torch.float64)])
-    host = torch.cat([scal, d2, qhi, qlo, per_image]).cpu().numpy()
+    flat = torch.cat([scal, d2, qhi, qlo, per_image])
+    host = torch.empty(flat.shape, dtype=flat.dtype, pin_memory=True)
+    host.copy_(flat, non_blocking=True)
+    ev = torch.cuda.Event()
+    ev.record()
+    return host, ev, n_tot
+
+
+def report_finish(handle, ds, archive_len, tau, stage_t, wall) -> ErrorReport:
+    """The host half of build_report (waits for report_launch's copy)."""
+    if not isinstance(archive_len, (int, np.integer)):
+        archive_len = len(archive_len)
+    host_t, ev, n_tot = handle
+    ev.synchronize()
+    host = host_t.numpy()
     dmax, dmin, sse, cnt, n_conv, ae_ok, n_sel, n_exc = host[:8]
     d2_h, qhi_h, qlo_h = host[8:12], host[12:16], host[16:20]
     span = float(dmax - dmin)
