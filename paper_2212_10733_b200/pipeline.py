@@ -13,6 +13,7 @@ import ctypes
 import hashlib
 import json
 import mmap
+import os
 import struct
 import time
 from dataclasses import asdict, dataclass, field
@@ -146,6 +147,12 @@ PIPELINE_GROUPS = 1
 _GRIDS = {}
 # bytes the last compress() moved over PCIe (diagnostics; bench.py's e2e)
 LAST_CALL = {}
+# stage 1 plane by plane under the upload (measured: 62.4 ms vs 61.5 ms without
+# -- the upload then starts only after compress_device's own staging, which
+# costs what the overlap gains; tools/e2e_ab.py); exception entries from the
+# host f0 (61.5 vs 62.5 ms)
+PLANE_STAGE1 = os.environ.get("MLK_PLANE_STAGE1", "0") == "1"
+HOST_EXCEPTIONS = os.environ.get("MLK_HOST_EXCEPTIONS", "1") != "0"
 
 
 def _device_grid(grid, dev, latent_dim):
@@ -236,7 +243,10 @@ def compress(ds: FDataset, config: PipelineConfig, state: TimestepState | None =
     pieces = [[(p, sh.nodes_range[0], sh.nodes_range[1]) for i in grp for sh in [shards[i]]
                for p in range(*sh.planes_range)] for grp in groups]
     plane_events = None
-    if len(groups) == 1:
+    if len(groups) == 1 and not PLANE_STAGE1:
+        f0 = upload_f0(data, dev)
+        up = hostio.UploadDone(f0)
+    elif len(groups) == 1:
         # stage 1 of plane p starts as soon as plane p has landed; the upload
         # is started by compress_device once its own small copies are queued
         f0 = hostio.device_planes_buffer(data, dev)
@@ -273,7 +283,7 @@ def compress(ds: FDataset, config: PipelineConfig, state: TimestepState | None =
                 # the report needs only the archive length: its reductions and
                 # small D2H go ahead of the last blob download
                 rep_h = report_launch(outs)
-            if out.exceptions is not None:
+            if out.exceptions is not None and HOST_EXCEPTIONS:
                 # exception entries are the input's own bytes: written from
                 # the host f0 by the pool, only the rest comes back over PCIe
                 holes, fills = _exception_fills(out, [shards[i] for i in grp], data, ds)
@@ -334,8 +344,6 @@ def compress_distributed(ds: FDataset, config: PipelineConfig, state: TimestepSt
     offset index); the report statistics are all-reduced.  Returns
     (out_path, report, new_state); the report's per_image_nrmse is empty
     (it would gather every image)."""
-    import os
-
     import torch.distributed as dist
 
     from . import distributed as D_
