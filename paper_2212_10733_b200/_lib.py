@@ -121,7 +121,14 @@ def lib() -> ctypes.CDLL:
     return so
 
 
+_raw_stream = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+
+
 def stream_handle() -> int:
+    """cudaStream_t of the current stream (the raw accessor skips the device
+    resolution torch.cuda.current_stream() does on every call)."""
+    if _raw_stream is not None:
+        return _raw_stream(torch.cuda.current_device())
     return torch.cuda.current_stream().cuda_stream
 
 
@@ -136,14 +143,19 @@ def ptr(t) -> int | None:
 
 
 LAUNCHES = 0  # C-ABI entry calls (each launches exactly one kernel)
+_FNS = {}
 
 
-def call(name: str, *args, msg: str = "") -> None:
+def call(name: str, *args, msg: str = "", stream: int | None = None) -> None:
+    """Launch `name` on the current stream (or the raw cudaStream_t `stream`)."""
     global LAUNCHES
     LAUNCHES += 1
-    fn = getattr(lib(), name)
-    conv = [ptr(a) if isinstance(a, torch.Tensor) else a for a in args]
-    rc = fn(*conv, stream_handle())
+    fn = _FNS.get(name)
+    if fn is None:
+        fn = _FNS[name] = getattr(lib(), name)
+    conv = [(a.data_ptr() if a.is_cuda or not a.numel() else ptr(a))
+            if isinstance(a, torch.Tensor) else a for a in args]
+    rc = fn(*conv, stream_handle() if stream is None else stream)
     if rc != 0:
         raise _ERRORS.get(rc, BackendError)(f"{name} failed ({rc}) {msg}".strip())
 

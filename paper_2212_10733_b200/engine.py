@@ -373,7 +373,25 @@ def _upload_shards(arr, device):
     return torch.from_numpy(raw).to(device)
 
 
+_GRAMS = {}
+
+
 def _gram(models):
+    """Per-shard [W W^T, row sums, row norms, max |W|] (cached on the weight
+    bytes: the models are the same every timestep in static mode)."""
+    # identity + address + a checksum of each weight array (a model mutated in
+    # place changes its sum)
+    key = tuple((id(m.weights), m.weights.ctypes.data, float(np.sum(m.weights, dtype=np.float64)))
+                for m in models)
+    g = _GRAMS.get(key)
+    if g is None:
+        if len(_GRAMS) > 64:
+            _GRAMS.clear()
+        g = _GRAMS[key] = _gram_compute(models)
+    return g
+
+
+def _gram_compute(models):
     rows = []
     for m in models:
         w = m.weights.astype(np.float64)
@@ -391,6 +409,9 @@ def kmeans_draws(n: int, k: int, seed: int):
     return first, tuple(g.random() for _ in range(k - 1))
 
 
+_NP2TORCH = {}
+
+
 class Workspace:
     """Per-device persistent buffers: grow-only device arenas by name and a
     pinned host staging arena whose contents reach the device with one async
@@ -401,6 +422,7 @@ class Workspace:
     def __init__(self, dev, cap=1 << 26):
         self.dev = dev
         self.bufs = {}
+        self.views = {}
         self._alloc(cap)
         self.pending = []
         self.ready = None
@@ -420,14 +442,29 @@ class Workspace:
             ws = cls._by_dev[(dev.index, tag)] = Workspace(dev)
         return ws
 
+    _ESIZE = {}
+
     def tensor(self, name, shape, dtype):
-        n = int(np.prod(shape)) if shape else 1
-        nbytes = max(16, n * torch.empty((), dtype=dtype).element_size())
+        """A typed view of the grow-only buffer `name` (views are cached per
+        (name, shape, dtype) while the buffer stays the same)."""
+        key = (name, shape, dtype)
+        hit = self.views.get(key)
         b = self.bufs.get(name)
+        if hit is not None and hit[0] is b:
+            return hit[1]
+        es = self._ESIZE.get(dtype)
+        if es is None:
+            es = self._ESIZE[dtype] = torch.empty((), dtype=dtype).element_size()
+        n = int(np.prod(shape)) if shape else 1
+        nbytes = max(16, n * es)
         if b is None or b.numel() < nbytes:
             self.bufs[name] = b = torch.empty(int(nbytes * 1.25) + 64, dtype=torch.uint8,
                                               device=self.dev)
-        return b[:nbytes].view(dtype)[:n].view(shape)
+        v = b[:nbytes].view(dtype)[:n].view(shape)
+        if len(self.views) > 512:  # data-dependent shapes: keep the cache bounded
+            self.views.clear()
+        self.views[key] = (b, v)
+        return v
 
     def reset(self):
         """Start of a call: the previous call's staged copies must have landed
@@ -453,7 +490,10 @@ class Workspace:
             self._alloc(max(2 * self.h.numel(), nb + (1 << 20)))
         self.hn[self.pos:self.pos + nb] = a.reshape(-1).view(np.uint8)
         view = self.d[self.pos:self.pos + max(nb, 1)]
-        out = view[:nb].view(torch.from_numpy(a[:0]).dtype).view(a.shape) if nb else view
+        td = _NP2TORCH.get(a.dtype)
+        if td is None:
+            td = _NP2TORCH[a.dtype] = torch.from_numpy(a[:0].copy()).dtype
+        out = view[:nb].view(td).view(a.shape) if nb else view
         self.pending.append((self.pos, nb))
         self.pos = (self.pos + nb + 15) & ~15
         return out
@@ -924,6 +964,16 @@ DEFLATE_PROF = None   # set to a (12,) uint64 CUDA tensor to collect phase cycle
 _TIER_STREAMS = {}
 
 
+_SMS = {}
+
+
+def _sm_count(dev):
+    n = _SMS.get(dev.index)
+    if n is None:
+        n = _SMS[dev.index] = torch.cuda.get_device_properties(dev).multi_processor_count
+    return n
+
+
 def _tier_streams(dev, n):
     key = dev.index
     if key not in _TIER_STREAMS:
@@ -935,7 +985,7 @@ def _run_deflate(ws, varint, in_off, vlen, n, zout, zoff, zcap, zlen, dev, max_w
     """Warp-cooperative kernel per size tier, the tiers concurrently on their own
     streams (a sparse tier is bounded by single-stream latency, not throughput);
     one thread per stream beyond the last tier."""
-    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    sms = _sm_count(dev)
     sym_cap = 3 * DEFLATE_TIERS[-1] + 16
     sym = ws.tensor("deflate_sym", (n * sym_cap,), torch.uint8)
     main = torch.cuda.current_stream(dev)
@@ -945,19 +995,19 @@ def _run_deflate(ws, varint, in_off, vlen, n, zout, zoff, zcap, zlen, dev, max_w
     bounds = list(zip((0,) + DEFLATE_TIERS, DEFLATE_TIERS + (None,)))
     # largest streams first: the few long, latency-bound streams of the upper
     # tiers start at once and overlap the bulk tier instead of trailing it
+    # (launched on the tier streams by handle: no current-stream switching)
     for k in reversed(range(len(bounds))):
         lo, hi = bounds[k]
         st = streams[k]
         st.wait_event(ev0)
-        with torch.cuda.stream(st):
-            if hi is None:
-                workers = min(n, max_workers)
-                call("mlk_zlib_compress6", varint, in_off, vlen, n, zout, zoff, zcap, zlen,
-                     _deflate_pool(dev, workers), workers, lo)
-            else:
-                nb = 2 * sms if k < 3 else sms
-                call("mlk_zlib_compress6_warp", varint, in_off, vlen, n, lo, hi, zout, zoff,
-                     zcap, zlen, nb, sym, sym_cap, DEFLATE_PROF)
+        if hi is None:
+            workers = min(n, max_workers)
+            call("mlk_zlib_compress6", varint, in_off, vlen, n, zout, zoff, zcap, zlen,
+                 _deflate_pool(dev, workers), workers, lo, stream=st.cuda_stream)
+        else:
+            nb = 2 * sms if k < 3 else sms
+            call("mlk_zlib_compress6_warp", varint, in_off, vlen, n, lo, hi, zout, zoff,
+                 zcap, zlen, nb, sym, sym_cap, DEFLATE_PROF, stream=st.cuda_stream)
         ev = torch.cuda.Event()
         ev.record(st)
         main.wait_event(ev)
