@@ -169,6 +169,15 @@ int mlk_zlib_compress6_warp(const uint8_t* in, const int64_t* in_off, const int6
 int mlk_gather_segments(const uint8_t* src, const int64_t* src_off, const int64_t* len,
                         int32_t n, uint8_t* dst, const int64_t* dst_off, cudaStream_t stream);
 
+/* mlk_zlib_compress6_warp with dynamic balance: the warps claim streams one
+ * at a time from *counter (device int, zero before the launch; one counter
+ * per concurrently running tier). */
+int mlk_zlib_compress6_warp_dyn(const uint8_t* in, const int64_t* in_off, const int64_t* in_len,
+                                int32_t n, int32_t nmin, int32_t nmax, uint8_t* out,
+                                const int64_t* out_off, int64_t out_cap, int64_t* out_len,
+                                int32_t n_blocks, uint8_t* sym_scratch, int64_t sym_cap,
+                                uint64_t* prof, int32_t* counter, cudaStream_t stream);
+
 /* zlib.decompress (residual.py:86) for n streams; out_len[s] = bytes produced,
  * or -1 (corrupt) / -2 (output capacity exceeded). */
 int mlk_zlib_decompress(const uint8_t* in, const int64_t* in_off, const int64_t* in_len,

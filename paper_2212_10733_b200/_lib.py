@@ -70,6 +70,8 @@ _SIGS = {
     "mlk_zlib_compress6": [_P, _P, _P, _I32, _P, _P, _I64, _P, _P, _I32, _I64, _P],
     "mlk_zlib_compress6_warp": [_P, _P, _P, _I32, _I32, _I32, _P, _P, _I64, _P, _I32, _P, _I64,
                                 _P, _P],
+    "mlk_zlib_compress6_warp_dyn": [_P, _P, _P, _I32, _I32, _I32, _P, _P, _I64, _P, _I32, _P,
+                                    _I64, _P, _P, _P],
     "mlk_gather_segments": [_P, _P, _P, _I32, _P, _P, _P],
     "mlk_zlib_decompress": [_P, _P, _P, _I32, _P, _P, _I64, _P, _P],
     "mlk_stage1": [_P, _P, _I32, _I32, _P, _P, _I32, _P, _P, _P, _P],

@@ -749,7 +749,7 @@ k_deflate_warp(const uint8_t* __restrict__ in, const long long* __restrict__ in_
                const long long* __restrict__ out_off, long long out_cap,
                long long* __restrict__ out_len, int nmin, int nmax,
                uint8_t* __restrict__ sym_g, long long sym_cap,
-               unsigned long long* __restrict__ prof) {
+               unsigned long long* __restrict__ prof, int* __restrict__ counter) {
     __shared__ z6::Tables tb;
     extern __shared__ __align__(16) uint8_t zsm[];
     load_tables(tb);
@@ -766,7 +766,20 @@ k_deflate_warp(const uint8_t* __restrict__ in, const long long* __restrict__ in_
     const unsigned FULL = 0xffffffffu;
     const unsigned lt_mask = (1u << lane) - 1u;
     const int gw = blockIdx.x * ZW + warp, nw = gridDim.x * ZW;
-    for (int s = gw; s < n_streams; s += nw) {
+    // streams are claimed one at a time from `counter` when given (dynamic
+    // balance: a tier's streams are scattered over the index range and their
+    // cost varies), else taken with a static stride
+    int s_next = gw;
+    for (;;) {
+        int s;
+        if (counter) {
+            if (lane == 0) s = atomicAdd(counter, 1);
+            s = __shfl_sync(FULL, s, 0);
+        } else {
+            s = s_next;
+            s_next += nw;
+        }
+        if (s >= n_streams) break;
         const int n = (int)in_len[s];
         if (n <= nmin || n > nmax) continue;  // another tier handles it
         const uint8_t* src = in + in_off[s];
@@ -1173,12 +1186,11 @@ extern "C" int mlk_zlib_compress6(const uint8_t* in, const int64_t* in_off, cons
     return cudaGetLastError() == cudaSuccess ? MLK_OK : MLK_ERR_CUDA;
 }
 
-extern "C" int mlk_zlib_compress6_warp(const uint8_t* in, const int64_t* in_off,
-                                       const int64_t* in_len, int32_t n, int32_t nmin,
-                                       int32_t nmax, uint8_t* out, const int64_t* out_off,
-                                       int64_t out_cap, int64_t* out_len, int32_t n_blocks,
-                                       uint8_t* sym_scratch, int64_t sym_cap, uint64_t* prof,
-                                       cudaStream_t stream) {
+static int launch_deflate_warp(const uint8_t* in, const int64_t* in_off, const int64_t* in_len,
+                               int32_t n, int32_t nmin, int32_t nmax, uint8_t* out,
+                               const int64_t* out_off, int64_t out_cap, int64_t* out_len,
+                               int32_t n_blocks, uint8_t* sym_scratch, int64_t sym_cap,
+                               uint64_t* prof, int32_t* counter, cudaStream_t stream) {
     if (n <= 0) return MLK_OK;
     if (nmax > 16000 || nmax < 1 || sym_cap < 3LL * nmax + 3) return MLK_ERR_CONFIG;
     if (ensure_tables() != MLK_OK) return MLK_ERR_CUDA;
@@ -1195,7 +1207,7 @@ extern "C" int mlk_zlib_compress6_warp(const uint8_t* in, const int64_t* in_off,
         in, reinterpret_cast<const long long*>(in_off), reinterpret_cast<const long long*>(in_len), \
         n, out, reinterpret_cast<const long long*>(out_off), (long long)out_cap,                  \
         reinterpret_cast<long long*>(out_len), nmin, nmax, sym_scratch, (long long)sym_cap,        \
-        reinterpret_cast<unsigned long long*>(prof))
+        reinterpret_cast<unsigned long long*>(prof), counter)
     if (prof) {
         MLK_DW_LAUNCH(true);
     } else {
@@ -1203,6 +1215,27 @@ extern "C" int mlk_zlib_compress6_warp(const uint8_t* in, const int64_t* in_off,
     }
 #undef MLK_DW_LAUNCH
     return cudaGetLastError() == cudaSuccess ? MLK_OK : MLK_ERR_CUDA;
+}
+
+extern "C" int mlk_zlib_compress6_warp(const uint8_t* in, const int64_t* in_off,
+                                       const int64_t* in_len, int32_t n, int32_t nmin,
+                                       int32_t nmax, uint8_t* out, const int64_t* out_off,
+                                       int64_t out_cap, int64_t* out_len, int32_t n_blocks,
+                                       uint8_t* sym_scratch, int64_t sym_cap, uint64_t* prof,
+                                       cudaStream_t stream) {
+    return launch_deflate_warp(in, in_off, in_len, n, nmin, nmax, out, out_off, out_cap, out_len,
+                               n_blocks, sym_scratch, sym_cap, prof, nullptr, stream);
+}
+
+extern "C" int mlk_zlib_compress6_warp_dyn(const uint8_t* in, const int64_t* in_off,
+                                           const int64_t* in_len, int32_t n, int32_t nmin,
+                                           int32_t nmax, uint8_t* out, const int64_t* out_off,
+                                           int64_t out_cap, int64_t* out_len, int32_t n_blocks,
+                                           uint8_t* sym_scratch, int64_t sym_cap, uint64_t* prof,
+                                           int32_t* counter, cudaStream_t stream) {
+    if (!counter) return MLK_ERR_CONFIG;
+    return launch_deflate_warp(in, in_off, in_len, n, nmin, nmax, out, out_off, out_cap, out_len,
+                               n_blocks, sym_scratch, sym_cap, prof, counter, stream);
 }
 
 extern "C" int mlk_zlib_decompress(const uint8_t* in, const int64_t* in_off,

@@ -959,6 +959,8 @@ DEFLATE_TIERS = (1024, 1600, 2048, 3072, 4096, 8192, 16000)
 
 
 DEFLATE_PROF = None   # set to a (12,) uint64 CUDA tensor to collect phase cycles
+# tier warps claim streams from an atomic counter (dynamic balance)
+DEFLATE_DYNAMIC = os.environ.get("MLK_DEFLATE_DYNAMIC", "1") != "0"
 
 
 _TIER_STREAMS = {}
@@ -990,6 +992,8 @@ def _run_deflate(ws, varint, in_off, vlen, n, zout, zoff, zcap, zlen, dev, max_w
     sym = ws.tensor("deflate_sym", (n * sym_cap,), torch.uint8)
     main = torch.cuda.current_stream(dev)
     streams = _tier_streams(dev, len(DEFLATE_TIERS) + 1)
+    ctr = ws.tensor("deflate_ctr", (len(DEFLATE_TIERS) + 1,), torch.int32)
+    ctr.zero_()
     ev0 = torch.cuda.Event()
     ev0.record(main)
     bounds = list(zip((0,) + DEFLATE_TIERS, DEFLATE_TIERS + (None,)))
@@ -1006,8 +1010,13 @@ def _run_deflate(ws, varint, in_off, vlen, n, zout, zoff, zcap, zlen, dev, max_w
                  _deflate_pool(dev, workers), workers, lo, stream=st.cuda_stream)
         else:
             nb = 2 * sms if k < 3 else sms
-            call("mlk_zlib_compress6_warp", varint, in_off, vlen, n, lo, hi, zout, zoff,
-                 zcap, zlen, nb, sym, sym_cap, DEFLATE_PROF, stream=st.cuda_stream)
+            if DEFLATE_DYNAMIC:
+                call("mlk_zlib_compress6_warp_dyn", varint, in_off, vlen, n, lo, hi, zout, zoff,
+                     zcap, zlen, nb, sym, sym_cap, DEFLATE_PROF, ctr[k:k + 1],
+                     stream=st.cuda_stream)
+            else:
+                call("mlk_zlib_compress6_warp", varint, in_off, vlen, n, lo, hi, zout, zoff,
+                     zcap, zlen, nb, sym, sym_cap, DEFLATE_PROF, stream=st.cuda_stream)
         ev = torch.cuda.Event()
         ev.record(st)
         main.wait_event(ev)
