@@ -214,8 +214,8 @@ int mlk_kmeans(const double* lat, const MlkShard* shards, const MlkShard* shards
                cudaStream_t stream);
 
 /* diagnostics: cycles of CTA 0 of the last mlk_kmeans launch in its phases
- * (load + distinct test, k-means++ seeding, Lloyd) and its Lloyd sweeps;
- * out_h is a HOST array of 4. */
+ * (load + distinct test, k-means++ seeding, Lloyd), its Lloyd sweeps and six
+ * sub-phase totals; out_h is a HOST array of 12. */
 int mlk_kmeans_prof(int64_t* out_h, cudaStream_t stream);
 
 /* pq_encode + AE-error decision (quantizer.py:111-120; pipeline.py:228-235):

@@ -19,7 +19,7 @@
 
 // phase clocks of the last launch's CTA 0: load + distinct test, seeding,
 // Lloyd, sweeps (read by mlk_kmeans_prof; diagnostics only)
-__device__ long long g_km_prof[4];
+__device__ long long g_km_prof[12];
 
 namespace {
 
@@ -307,6 +307,7 @@ k_kmeans(const double* __restrict__ lat, const MlkShard* __restrict__ shards, in
     int* inf = info + (s * L + dim) * 4;
 
     const long long kp_t0 = clock64();
+    long long kp_acc[6] = {0, 0, 0, 0, 0, 0};  // sub-phase clocks (thread 0 of CTA 0 reports)
     for (int j = tid; j < n; j += KT) v[j] = lat[(long long)(sh.img_off + j) * L + dim];
     __syncthreads();
 
@@ -361,7 +362,9 @@ k_kmeans(const double* __restrict__ lat, const MlkShard* __restrict__ shards, in
     const int j_lo = min(n, tid * chunk), j_hi = min(n, j_lo + chunk);
     const double delta = (16.0 * (n + 8)) * 1.1102230246251565e-16;
     for (int i = 1; i < K; ++i) {
+        const long long kq0 = clock64();
         block_pw_sums(d2, &S.one_start, &S.one_len, 1, val, kind, S.seg_base, S.sums, S);
+        kp_acc[0] += clock64() - kq0;
         const double tot = S.sums[0];
         if (tot <= 0) {
             if (tid == 0)
@@ -375,6 +378,7 @@ k_kmeans(const double* __restrict__ lat, const MlkShard* __restrict__ shards, in
         double loc = 0.0;
         for (int j = j_lo; j < j_hi; ++j) loc += d2[j];
         double ctot;
+        const long long kq1 = clock64();
         double run = block_exscan(loc, &ctot, S);
         const double thr_a = u * ctot * (1.0 - 2.0 * delta), thr_b = u * ctot * (1.0 + 2.0 * delta);
         int a_cnt = 0, b_cnt = 0;
@@ -404,9 +408,11 @@ k_kmeans(const double* __restrict__ lat, const MlkShard* __restrict__ shards, in
                 ++fallbacks;
             }
             S.cent[i] = v[idx];
+            kp_acc[1] += clock64() - kq1;
         }
         __syncthreads();
         const double ci = S.cent[i];
+#pragma unroll 4  // independent members: keep several L2 round trips in flight
         for (int j = tid; j < n; j += KT) {
             double t = __dsub_rn(v[j], ci);
             double q = __dmul_rn(t, t);
@@ -424,6 +430,7 @@ k_kmeans(const double* __restrict__ lat, const MlkShard* __restrict__ shards, in
     const int w_lo = min(n, w * wchunk), w_hi = min(n, w_lo + wchunk);
     for (int it = 0; it < 25; ++it) {
         ++sweeps;
+        const long long kl0 = clock64();
         // stable partition of members by label into srt
         for (int q = tid; q < KW * K; q += KT) wcnt[q] = 0;
         __syncthreads();
@@ -455,6 +462,8 @@ k_kmeans(const double* __restrict__ lat, const MlkShard* __restrict__ shards, in
             }
         }
         __syncthreads();
+        const long long kl1 = clock64();
+        kp_acc[2] += kl1 - kl0;
         const unsigned lt = (1u << lane) - 1u;
         for (int j0 = w_lo; j0 < w_hi; j0 += 32) {
             int j = j0 + lane;
@@ -469,6 +478,8 @@ k_kmeans(const double* __restrict__ lat, const MlkShard* __restrict__ shards, in
             __syncwarp();
         }
         __syncthreads();
+        const long long kl2 = clock64();
+        kp_acc[3] += kl2 - kl1;
         // pairwise means of every live cluster
         if (tid < K) S.oldc[tid] = S.cent[tid];
         block_pw_sums(srt, S.seg_start, S.seg_cnt, K, val, kind, S.seg_base, S.sums, S);
@@ -477,6 +488,8 @@ k_kmeans(const double* __restrict__ lat, const MlkShard* __restrict__ shards, in
             S.newc[tid] = c > 0 ? __ddiv_rn(S.sums[tid], (double)c) : S.oldc[tid];
         }
         __syncthreads();
+        const long long kl3 = clock64();
+        kp_acc[4] += kl3 - kl2;
         // dead clusters, in index order, against the partially updated table
         for (int k = 0; k < K; ++k) {
             if (S.seg_cnt[k] != 0) continue;
@@ -495,14 +508,18 @@ k_kmeans(const double* __restrict__ lat, const MlkShard* __restrict__ shards, in
         if (tid < K) S.cent[tid] = S.newc[tid];
         __syncthreads();
         int changed = 0;
+#pragma unroll 2
         for (int j = tid; j < n; j += KT) {
             unsigned short nl = (unsigned short)nearest(v[j], S.cent, K);
             lab2[j] = nl;
             changed |= (nl != lab[j]);
         }
         changed = block_sum_int(changed, S);
+        kp_acc[5] += clock64() - kl3;
         if (!changed) break;
-        for (int j = tid; j < n; j += KT) lab[j] = lab2[j];
+        unsigned short* t = lab;  // the new labels become the current ones
+        lab = lab2;
+        lab2 = t;
         __syncthreads();
     }
 
@@ -511,6 +528,7 @@ k_kmeans(const double* __restrict__ lat, const MlkShard* __restrict__ shards, in
         g_km_prof[1] = kp_t2 - kp_t1;
         g_km_prof[2] = clock64() - kp_t2;
         g_km_prof[3] = sweeps;
+        for (int q = 0; q < 6; ++q) g_km_prof[4 + q] = kp_acc[q];
     }
     // ---- sorted float32 codebook row
     if (tid == 0) {
@@ -546,6 +564,6 @@ extern "C" int mlk_kmeans(const double* lat, const MlkShard* shards, const MlkSh
 // diagnostics: phase clocks of the last mlk_kmeans launch's CTA 0
 extern "C" int mlk_kmeans_prof(int64_t* out_h, cudaStream_t stream) {
     if (cudaStreamSynchronize(stream) != cudaSuccess) return MLK_ERR_CUDA;
-    return cudaMemcpyFromSymbol(out_h, g_km_prof, sizeof(long long) * 4) == cudaSuccess
+    return cudaMemcpyFromSymbol(out_h, g_km_prof, sizeof(long long) * 12) == cudaSuccess
                ? MLK_OK : MLK_ERR_CUDA;
 }

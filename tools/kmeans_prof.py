@@ -16,9 +16,15 @@ dg = engine.DeviceGrid(ds.grid, dev)
 works = engine.shard_layout(shards, models, ds.n_nodes, 39, 39)
 for _ in range(2):
     out = engine.compress_device(f0, works, dg, cfg)
-buf = (ctypes.c_int64 * 4)()
+buf = (ctypes.c_int64 * 12)()
 _lib.call("mlk_kmeans_prof", ctypes.addressof(buf))
 ghz = 1.965
 print("kmeans CTA0 cycles: load+distinct %d (%.1f us)  seeding %d (%.1f us)  lloyd %d (%.1f us)  sweeps %d"
       % (buf[0], buf[0] / ghz / 1e3, buf[1], buf[1] / ghz / 1e3, buf[2], buf[2] / ghz / 1e3, buf[3]))
-print("kinfo (per shard, dim: exact, k, sweeps, fallbacks):", out.host("kinfo").reshape(-1, 4)[:, 2].tolist())
+names = ["seed: pairwise d2 sum", "seed: scan + choice", "lloyd: count + offsets",
+         "lloyd: scatter", "lloyd: pairwise means", "lloyd: reseed + nearest"]
+for k, nm in enumerate(names):
+    print(f"  {nm:26s} {buf[4 + k] / ghz / 1e3:8.1f} us")
+ki = out.host("kinfo").reshape(-1, 4)
+print("sweeps per (shard, dim):", ki[:, 2].tolist())
+print("choice(p) fallbacks per (shard, dim):", ki[:, 3].tolist())
