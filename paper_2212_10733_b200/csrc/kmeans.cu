@@ -43,9 +43,6 @@ struct KmSmem {
     int bcast_i;
     double bcast_d;
     double sums[MLK_MAXK];
-    double sc[MLK_MAXK];  // centroids in ascending order (nearest_sorted)
-    int si[MLK_MAXK];     // their indices
-    int sorted_ok;        // every centroid finite
 };
 
 // ---------------------------------------------------------------- block helpers
@@ -152,50 +149,6 @@ __device__ double block_exscan(double v, double* total, KmSmem& S) {
     double r = S.red[w] + exc;
     __syncthreads();
     return r;
-}
-
-// the centroids sorted (thread 0; K <= 256, insertion sort) for nearest_sorted
-__device__ void sort_centroids(KmSmem& S, int K) {
-    if (threadIdx.x == 0) {
-        int ok = 1;
-        for (int a = 0; a < K; ++a) {
-            const double x = S.cent[a];
-            ok &= isfinite(x) ? 1 : 0;
-            int b = a - 1;
-            while (b >= 0 && S.sc[b] > x) {
-                S.sc[b + 1] = S.sc[b];
-                S.si[b + 1] = S.si[b];
-                --b;
-            }
-            S.sc[b + 1] = x;
-            S.si[b + 1] = a;
-        }
-        S.sorted_ok = ok;
-    }
-    __syncthreads();
-}
-
-__device__ __forceinline__ int nearest(double v, const double* c, int K);
-
-// nearest() from the sorted centroids: |v - c| rounded is monotone in c on
-// each side of v, so the minimum lies next to v's position and every centroid
-// at that distance is in one contiguous run around it; the lowest index of
-// the run is the first minimum nearest() returns.  Only when every centroid
-// and v are finite (else the linear scan's NaN behaviour applies).
-__device__ __forceinline__ int nearest_sorted(double v, const KmSmem& S, int K) {
-    if (!S.sorted_ok || !isfinite(v)) return nearest(v, S.cent, K);
-    int lo = 0, hi = K;  // first sorted position with sc > v
-    while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (S.sc[mid] <= v) lo = mid + 1; else hi = mid;
-    }
-    const double dl = lo > 0 ? __dsub_rn(v, S.sc[lo - 1]) : INFINITY;
-    const double dr = lo < K ? __dsub_rn(S.sc[lo], v) : INFINITY;
-    const double d = dl < dr ? dl : dr;
-    int best = 0x7fffffff;
-    for (int a = lo - 1; a >= 0 && __dsub_rn(v, S.sc[a]) == d; --a) best = min(best, S.si[a]);
-    for (int a = lo; a < K && __dsub_rn(S.sc[a], v) == d; ++a) best = min(best, S.si[a]);
-    return best;
 }
 
 __device__ __forceinline__ int nearest(double v, const double* c, int K) {
@@ -470,8 +423,7 @@ k_kmeans(const double* __restrict__ lat, const MlkShard* __restrict__ shards, in
 
     const long long kp_t2 = clock64();
     // ---- Lloyd (quantizer.py:78-90)
-    sort_centroids(S, K);
-    for (int j = tid; j < n; j += KT) lab[j] = (unsigned short)nearest_sorted(v[j], S, K);
+    for (int j = tid; j < n; j += KT) lab[j] = (unsigned short)nearest(v[j], S.cent, K);
     __syncthreads();
     int sweeps = 0;
     const int wchunk = (n + KW - 1) / KW;
@@ -556,10 +508,9 @@ k_kmeans(const double* __restrict__ lat, const MlkShard* __restrict__ shards, in
         if (tid < K) S.cent[tid] = S.newc[tid];
         __syncthreads();
         int changed = 0;
-        sort_centroids(S, K);
 #pragma unroll 2
         for (int j = tid; j < n; j += KT) {
-            unsigned short nl = (unsigned short)nearest_sorted(v[j], S, K);
+            unsigned short nl = (unsigned short)nearest(v[j], S.cent, K);
             lab2[j] = nl;
             changed |= (nl != lab[j]);
         }
