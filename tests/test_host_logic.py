@@ -85,3 +85,31 @@ def test_search_heap_groups_many_searches():
         want = _scalar_heap(st, 7)
         assert np.array_equal(np.isnan(row), np.isnan(want))
         assert np.array_equal(row[~np.isnan(row)], want[~np.isnan(want)])
+
+
+def test_archive_bound_covers_every_fixture_archive():
+    """compress() sizes the archive bytes object by _archive_bound and shrinks
+    it in place: the bound must hold for every reference archive."""
+    import json
+    from types import SimpleNamespace
+
+    from paper_2212_10733_b200 import PipelineConfig, fdata, pipeline
+    from paper_2212_10733_b200.container import ArchivePreamble
+    from tests.golden_util import GOLDEN
+
+    grid = fdata.make_grid(39, 39, 5.0, 5.0, 1.0)
+    for path in sorted(GOLDEN.glob("*.json")):
+        meta = json.loads(path.read_text())
+        if "runs" not in meta:
+            continue
+        ds = SimpleNamespace(grid=grid, n_planes=meta["P"], n_nodes=meta["N"])
+        for run in meta["runs"]:
+            c = dict(run["cfg"])
+            c.pop("newton", None)
+            cfg = PipelineConfig(**c)
+            head = ArchivePreamble(n_shards=cfg.shards, decomp_mode=cfg.mode,
+                                   n_planes=ds.n_planes, n_nodes=ds.n_nodes, grid=grid,
+                                   timestep=0, tau=cfg.tau, seed=cfg.seed,
+                                   config_digest=cfg.digest()).pack()
+            bound = pipeline._archive_bound(ds, cfg, cfg.shards, len(head))
+            assert run["archive_len"] <= bound, (path.name, run["archive_len"], bound)
