@@ -9,7 +9,7 @@
 
 namespace {
 
-constexpr int S1_WARPS = 6;
+constexpr int S1_WARPS = 15;  // one CTA per SM: W once + 15 staged histograms in 221 KB
 constexpr int S1_IMGS = 4;  // images per warp per block
 
 __host__ __device__ inline int panel_len(int rem) {
