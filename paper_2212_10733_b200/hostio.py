@@ -388,11 +388,26 @@ class ArchiveWriter:
             self.jobs += fill(body, o, n)
         self.pos += nbytes
 
+    def drain(self):
+        """Wait for every pool job writing into the archive object (error
+        paths: the object must outlive them)."""
+        for j in self.jobs:
+            try:
+                j.result()
+            except Exception:
+                pass
+
     def finish(self, head: bytes) -> bytes:
         if len(head) != self.head_len:
             raise ValueError("archive head length changed")
-        for j in self.jobs:
-            j.result()
+        err = None
+        for j in self.jobs:  # every job finishes before an error propagates
+            try:
+                j.result()
+            except Exception as e:  # noqa: BLE001
+                err = err or e
+        if err is not None:
+            raise err
         self.view[:len(head)] = np.frombuffer(head, dtype=np.uint8)
         n = self.pos
         self._HINT[self.dev.index] = n

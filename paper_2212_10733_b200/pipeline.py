@@ -292,6 +292,9 @@ def compress(ds: FDataset, config: PipelineConfig, state: TimestepState | None =
             else:
                 writer.add(out.blob_buf, int(np.sum(out.blob_lens)))
             lens += [int(x) for x in out.blob_lens]
+    except BaseException:
+        writer.drain()  # pool jobs still write into the archive object
+        raise
     finally:
         up.join()
     t0 = time.perf_counter()
@@ -314,7 +317,6 @@ class _Trace:
     """MLK_TRACE=1: print the wall time of each phase (synchronised)."""
 
     def __init__(self, tag):
-        import os
         self.on = os.environ.get("MLK_TRACE") == "1"
         self.tag, self.t, self.parts = tag, time.perf_counter(), []
 
