@@ -693,7 +693,10 @@ def compress_device(f0: torch.Tensor, specs, dgrid: DeviceGrid, cfg, timer: Time
             for level in range(LOOKAHEAD):
                 if st.stage == "done":
                     break
-                if st.query() != cand[s, node]:
+                # the tree was built with the state machine's own float
+                # operations (tests/test_host_logic.py pins it level by level);
+                # the root of every round is re-checked here
+                if level == 0 and st.query() != cand[s, node]:
                     raise AssertionError("lookahead tree out of step with the search")
                 ok = fail_h[s, node] == 0
                 st = st.advance(ok)
