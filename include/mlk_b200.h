@@ -358,6 +358,34 @@ int mlk_pack_exceptions(const double* f0, const MlkShard* shards, int32_t n_shar
                         const int32_t* exc_list, const int32_t* exc_off, const int64_t* sec_off,
                         int32_t n_exc_total, int32_t D, uint8_t* out, cudaStream_t stream);
 
+/* ---- AE training (off the per-histogram path) ----
+ * Replaces autoencoder.train (autoencoder.py:137-177) with fit_normalizer
+ * (77-84) and _loss_and_grad_normalized (127-134), as compress() calls it per
+ * shard (pipeline.py:209-218).  One job per shard: the training images are
+ * base + row_off[i] (i < n, D doubles each, device), order is the epochs x n
+ * table of rng.permutation draws (device int32), w (L x D f64, device) holds
+ * the Glorot / warm-start weights on entry and the trained weights on exit,
+ * mv is 2 x L x D f64 scratch.  bias (2T doubles, device) = [1 - beta1^t,
+ * 1 - beta2^t] for t = 1..T, computed with Python floats.  norm (2 per job)
+ * receives (mean, std); diag (2 per job) receives (-1, 0) or (epoch, mse) of
+ * the first non-finite mse (TrainingDivergedError).  MLK_ERR_CONFIG when
+ * L * D > 12800 (shared-memory residency of W and its gradient). */
+#define MLK_STD_FLOOR 1e-30   /* autoencoder.STD_FLOOR */
+typedef struct {
+    const double* base;
+    const int64_t* row_off;
+    const int32_t* order;
+    double* w;
+    double* mv;
+    int32_t n;
+    int32_t epochs;
+} MlkTrainJob;
+
+int mlk_ae_train(const MlkTrainJob* jobs, const MlkTrainJob* jobs_h, int32_t n_jobs, int32_t L,
+                 int32_t D, int32_t batch, double lr, double beta1, double one_minus_beta1,
+                 double beta2, double one_minus_beta2, double eps, const double* bias,
+                 int32_t T, double* norm, double* diag, cudaStream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -119,6 +119,80 @@ def mix_seed(seed: int, wid: int) -> int:
 
 
 # ---------------------------------------------------------------------------
+# AE training: selection + Adam, autoencoder.py:77-177
+
+def select_training(planes, nodes, scheme: str, n_planes: int, seed: int, wid: int):
+    """decomp.py:116-153 on a shard given as (plane, node) member arrays."""
+    rng = np.random.Generator(np.random.PCG64(mix_seed(seed, wid)))
+    n = len(planes)
+    row_based = scheme.startswith("row")
+    single = len(set(planes.tolist())) == 1
+    if row_based and not single and n_planes > 1:
+        raise ValueError("row scheme needs row-wise shards")
+    if not row_based and single and n_planes > 1:
+        raise ValueError("col scheme needs column-wise shards")
+    frac = int(scheme[-2:]) / 100 if scheme[-2:].isdigit() else None
+    if scheme in ("row", "col"):
+        return np.arange(n)
+    if row_based:
+        return np.sort(rng.choice(n, size=max(1, int(n * frac)), replace=False))
+    block = sorted(set(nodes.tolist()))
+    if scheme == "colfst":
+        return np.nonzero(planes == min(planes))[0]
+    if scheme == "colrand":
+        return np.sort(rng.choice(n, size=len(block), replace=False))
+    pos = {x: j for j, x in enumerate(block)}
+    by_node = [[] for _ in block]
+    for i, x in enumerate(nodes.tolist()):
+        by_node[pos[x]].append(i)
+    picks = np.array([c[rng.integers(len(c))] for c in by_node])
+    if scheme == "colrandind":
+        return np.sort(picks)
+    return np.sort(rng.choice(picks, size=max(1, int(len(block) * frac)), replace=False))
+
+
+def ae_train(images, lr=0.001, batch=128, epochs=100, beta1=0.9, beta2=0.999, eps=1e-8,
+             seed=0, init_w=None, latent_dim=4):
+    """autoencoder.train (137-177) with fit_normalizer (77-84) and
+    _loss_and_grad_normalized (127-134); returns (W f32, mean, std) or
+    raises FloatingPointError(epoch, mse) where the reference raises
+    TrainingDivergedError."""
+    x = np.asarray(images, dtype=np.float64)
+    x = x.reshape(len(x), -1)
+    mean = float(np.mean(x))
+    std = max(float(np.std(x)), 1e-30)
+    x = (x - mean) / std
+    n, d = x.shape
+    rng = np.random.Generator(np.random.PCG64(seed))
+    if init_w is not None:
+        w = np.asarray(init_w, dtype=np.float32).astype(np.float64)
+    else:
+        bound = np.sqrt(6.0 / (latent_dim + d))
+        w = rng.uniform(-bound, bound, size=(latent_dim, d))
+    m = np.zeros_like(w)
+    v = np.zeros_like(w)
+    t = 0
+    for epoch in range(epochs):
+        order = rng.permutation(n)
+        for start in range(0, n, batch):
+            xb = x[order[start:start + batch]]
+            b = len(xb)
+            z = xb @ w.T
+            err = z @ w - xb
+            mse = float(np.mean(err ** 2))
+            grad = 2.0 / (b * d) * (z.T @ err + (err @ w.T).T @ xb)
+            if not np.isfinite(mse):
+                raise FloatingPointError(epoch, mse)
+            t += 1
+            m = beta1 * m + (1 - beta1) * grad
+            v = beta2 * v + (1 - beta2) * grad ** 2
+            mhat = m / (1 - beta1 ** t)
+            vhat = v / (1 - beta2 ** t)
+            w -= lr * mhat / (np.sqrt(vhat) + eps)
+    return w.astype(np.float32), mean, std
+
+
+# ---------------------------------------------------------------------------
 # autoencoder contractions (autoencoder.py:99-110)
 
 @functools.lru_cache(maxsize=None)

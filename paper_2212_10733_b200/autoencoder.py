@@ -1,9 +1,12 @@
-"""Tied-weight linear autoencoder model container (reference autoencoder.py:26-74).
+"""Tied-weight linear autoencoder (reference autoencoder.py:26-177).
 
-The hot path consumes trained weights (static-model mode,
-pipeline.py:206-207); the contraction itself runs on device in
-``csrc/stage1.cu`` (encode) and every kernel that needs a reconstruction
-(decode).  Training is outside the B200 hot path.
+The per-histogram path consumes trained weights: the contraction runs on
+device in ``csrc/stage1.cu`` (encode) and every kernel that needs a
+reconstruction (decode).  Training also runs on the
+device: :func:`train` / :func:`train_jobs` drive ``csrc/train.cu``
+(``mlk_ae_train``, one CTA per job for every epoch); the host only draws the
+reference's PCG64 stream (Glorot init, per-epoch permutations) and the Adam
+bias-correction table.
 """
 
 from __future__ import annotations
@@ -13,9 +16,9 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from .errors import ConfigError
+from .errors import ConfigError, DimensionError, TrainingDivergedError
 
-__all__ = ["AEModel", "TrainConfig", "train", "STD_FLOOR"]
+__all__ = ["AEModel", "TrainConfig", "train", "train_jobs", "STD_FLOOR"]
 
 STD_FLOOR = 1e-30
 
@@ -57,6 +60,8 @@ class AEModel:
 
 @dataclass(frozen=True)
 class TrainConfig:
+    """Adam settings (autoencoder.py:60-75)."""
+
     learning_rate: float = 0.001
     batch_size: int = 128
     epochs: int = 100
@@ -65,7 +70,119 @@ class TrainConfig:
     eps: float = 1e-8
     seed: int = 0
 
+    def __post_init__(self):
+        if self.learning_rate <= 0:
+            raise ConfigError("learning rate must be positive")
+        if self.batch_size < 1 or self.epochs < 1:
+            raise ConfigError("batch size and epochs must be >= 1")
 
-def train(images, config: TrainConfig, init=None, latent_dim: int = 4):
-    raise ConfigError("AE training is outside the B200 hot path: supply static per-shard "
-                      "models through TimestepState (static_model=True)")
+
+@dataclass
+class TrainJob:
+    """One independent training run: images base[row_off[i] : row_off[i] + D]."""
+
+    base: object            # device float64 tensor (flat)
+    row_off: np.ndarray     # (n,) int64 element offsets into base
+    epochs: int
+    seed: int
+    init: AEModel | None = None
+
+
+def _host_draws(n, d, latent_dim, epochs, seed, init):
+    """Glorot init + per-epoch permutations from PCG64(seed) (autoencoder.py:150-163)."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    if init is not None:
+        w = init.weights.astype(np.float64)
+    else:
+        bound = np.sqrt(6.0 / (latent_dim + d))
+        w = rng.uniform(-bound, bound, size=(latent_dim, d))
+    order = np.empty((epochs, n), dtype=np.int32)
+    for e in range(epochs):
+        order[e] = rng.permutation(n)
+    return np.ascontiguousarray(w, dtype=np.float64), order
+
+
+def train_jobs(jobs, config: TrainConfig, latent_dim: int, d: int):
+    """Train every job in one launch; returns one AEModel per job.
+
+    ``config.epochs`` and ``config.seed`` are taken per job from TrainJob."""
+    import torch
+
+    from . import _lib
+
+    if not jobs:
+        return []
+    L = jobs[0].init.latent_dim if jobs[0].init is not None else latent_dim
+    for jb in jobs:
+        if jb.init is not None and (jb.init.input_dim != d or jb.init.latent_dim != L):
+            raise DimensionError("warm-start model does not match image size")
+        if len(jb.row_off) == 0:
+            raise ConfigError("need at least one training image")
+    dev = jobs[0].base.device
+    B = config.batch_size
+    T = max(jb.epochs * -(-len(jb.row_off) // B) for jb in jobs)
+    # Python-float bias corrections, exactly as autoencoder.py:171-172 evaluates them
+    bias = np.array([[1 - config.beta1 ** t, 1 - config.beta2 ** t] for t in range(1, T + 1)],
+                    dtype=np.float64)
+    ws, keep, recs = [], [], []
+    for jb in jobs:
+        n = len(jb.row_off)
+        w, order = _host_draws(n, d, L, jb.epochs, jb.seed, jb.init)
+        wd = torch.from_numpy(w).to(dev)
+        offs = torch.from_numpy(np.ascontiguousarray(jb.row_off, dtype=np.int64)).to(dev)
+        od = torch.from_numpy(order).to(dev)
+        mv = torch.empty(2 * L * d, dtype=torch.float64, device=dev)
+        keep += [offs, od, mv, jb.base]
+        ws.append(wd)
+        recs.append((jb.base.data_ptr(), offs.data_ptr(), od.data_ptr(), wd.data_ptr(),
+                     mv.data_ptr(), n, jb.epochs))
+    rec_t = np.dtype([("base", "<u8"), ("row_off", "<u8"), ("order", "<u8"), ("w", "<u8"),
+                      ("mv", "<u8"), ("n", "<i4"), ("epochs", "<i4")])
+    table_h = np.array(recs, dtype=rec_t)
+    table_d = torch.from_numpy(table_h.view(np.uint8).copy()).to(dev)
+    bias_d = torch.from_numpy(bias.reshape(-1)).to(dev)
+    norm = torch.empty(2 * len(jobs), dtype=torch.float64, device=dev)
+    diag = torch.empty(2 * len(jobs), dtype=torch.float64, device=dev)
+    _lib.call("mlk_ae_train", table_d, table_h.ctypes.data, len(jobs), L, d, B,
+              float(config.learning_rate), float(config.beta1), float(1 - config.beta1),
+              float(config.beta2), float(1 - config.beta2), float(config.eps), bias_d, T,
+              norm, diag, msg="(AE training)")
+    norm_h, diag_h = norm.cpu().numpy(), diag.cpu().numpy()
+    out = []
+    for j, wd in enumerate(ws):
+        if diag_h[2 * j] >= 0:
+            raise TrainingDivergedError(int(diag_h[2 * j]), float(diag_h[2 * j + 1]))
+        out.append(AEModel(weights=wd.cpu().numpy().astype(np.float32),
+                           norm_mean=float(norm_h[2 * j]), norm_std=float(norm_h[2 * j + 1])))
+    del keep
+    return out
+
+
+def train(images, config: TrainConfig, init: AEModel | None = None,
+          latent_dim: int = 4) -> AEModel:
+    """Adam-train a model on the device (autoencoder.py:137-177).
+
+    ``images``: (N, rows, cols) / (N, D) host array or CUDA tensor.  Fresh
+    Glorot init unless warm-started via ``init``; the normaliser is always
+    refit on the supplied images."""
+    import torch
+
+    from .pipeline import _device
+
+    if isinstance(images, torch.Tensor):
+        if images.ndim < 2 or images.shape[0] == 0:
+            raise ConfigError("need at least one training image")
+        x = images.to(dtype=torch.float64).reshape(images.shape[0], -1).contiguous()
+        if not x.is_cuda:
+            x = x.to(_device())
+    else:
+        arr = np.asarray(images, dtype=np.float64)
+        if arr.ndim < 2 or len(arr) == 0:
+            raise ConfigError("need at least one training image")
+        x = torch.from_numpy(np.ascontiguousarray(arr.reshape(len(arr), -1))).to(_device())
+    n, d = x.shape
+    if init is not None and init.input_dim != d:
+        raise DimensionError("warm-start model does not match image size")
+    job = TrainJob(base=x.reshape(-1), row_off=np.arange(n, dtype=np.int64) * d,
+                   epochs=config.epochs, seed=config.seed, init=init)
+    return train_jobs([job], config, latent_dim, d)[0]

@@ -23,9 +23,11 @@ import torch
 
 from . import engine, hostio
 from ._lib import F_EXCEPTION, F_EXC_OVERFLOW, F_NONFINITE, F_SELECTED
+from . import autoencoder as ae
 from .autoencoder import AEModel
 from .container import ArchivePreamble, archive_offsets
-from .decomp import SelectionScheme, partition, shard_dataset_index
+from .decomp import (SelectionScheme, mix_seed, partition, select_training,
+                     shard_dataset_index)
 from .errors import (ConfigError, DegenerateRangeError, DimensionError, FormatError,
                      SizeMismatchError)
 from .fdata import FDataset, dataset_nbytes
@@ -124,14 +126,34 @@ def upload_f0(data: np.ndarray, device, node_range=None) -> torch.Tensor:
 
 
 def _check_state(config, state, n_shards):
-    if state is None:
-        raise ConfigError("AE training is outside the B200 hot path: pass a TimestepState "
-                          "holding one trained AEModel per shard (static_model=True)")
-    if len(state.models) != n_shards:
+    """Reference compress (pipeline.py:327-331): the shard count must match;
+    returns train_full (None when the stored models are reused as they are)."""
+    if state is not None and len(state.models) != n_shards:
         raise ConfigError("timestep state does not match the shard count")
-    if not config.static_model:
-        raise ConfigError("incremental retraining is outside the B200 hot path: use "
-                          "PipelineConfig(static_model=True)")
+    index = state.timestep_index if state is not None else 0
+    train_full = (state is None) or (not config.static_model
+                                     and index % config.retrain_period == 0)
+    if state is not None and config.static_model:
+        return None      # static mode reuses the models (pipeline.py:206-207)
+    return train_full
+
+
+def _train_models(f0, shards, ds, config, state, train_full):
+    """Per-shard AE training on the device (pipeline.py:208-218): selection
+    indices and PCG64 draws on the host, every shard's Adam run in ONE
+    mlk_ae_train launch over the device-resident f0."""
+    D = ds.grid.rows * ds.grid.cols
+    epochs = config.epochs_full if train_full else config.epochs_incremental
+    tc = ae.TrainConfig(learning_rate=config.learning_rate, batch_size=config.batch_size,
+                        epochs=epochs, seed=0)
+    jobs = []
+    for i, sh in enumerate(shards):
+        seed = mix_seed(config.seed, sh.worker_id)
+        sel = select_training(sh, config.scheme, ds.n_planes, seed)
+        rows = shard_dataset_index(sh, ds.n_nodes)[sel] * D
+        init = None if train_full else state.models[i]
+        jobs.append(ae.TrainJob(base=f0, row_off=rows, epochs=epochs, seed=seed, init=init))
+    return ae.train_jobs(jobs, tc, config.latent_dim, D)
 
 
 # compress() can pipeline shard groups: group g's node blocks are uploaded
@@ -235,15 +257,16 @@ def compress(ds: FDataset, config: PipelineConfig, state: TimestepState | None =
     """Run the five stages on the GPU; returns (archive bytes, report, new state)."""
     t_all = time.perf_counter()
     shards = partition(ds.n_planes, ds.n_nodes, config.shards, config.mode)
-    _check_state(config, state, len(shards))
+    train_full = _check_state(config, state, len(shards))
     dev = _device()
     data = ds.data if ds.data.dtype == np.float64 else ds.data.astype(np.float64)
     S = len(shards)
-    groups = _groups(S, PIPELINE_GROUPS)
+    # training needs every shard's f0 resident before the step: one group
+    groups = _groups(S, PIPELINE_GROUPS if train_full is None else 1)
     pieces = [[(p, sh.nodes_range[0], sh.nodes_range[1]) for i in grp for sh in [shards[i]]
                for p in range(*sh.planes_range)] for grp in groups]
     plane_events = None
-    if len(groups) == 1 and not PLANE_STAGE1:
+    if len(groups) == 1 and (not PLANE_STAGE1 or train_full is not None):
         f0 = upload_f0(data, dev)
         up = hostio.UploadDone(f0)
     elif len(groups) == 1:
@@ -259,7 +282,13 @@ def compress(ds: FDataset, config: PipelineConfig, state: TimestepState | None =
         up = hostio.upload_pieces(data, dev, pieces)
         f0 = up.buf
     dgrid = _device_grid(ds.grid, dev, config.latent_dim)
-    works = engine.shard_layout(shards, state.models, ds.n_nodes, ds.grid.rows, ds.grid.cols)
+    t_train = time.perf_counter()
+    if train_full is None:
+        models = list(state.models)
+    else:
+        models = _train_models(f0, shards, ds, config, state, train_full)
+    t_train = time.perf_counter() - t_train
+    works = engine.shard_layout(shards, models, ds.n_nodes, ds.grid.rows, ds.grid.cols)
     preamble = ArchivePreamble(n_shards=S, decomp_mode=config.mode,
                                n_planes=ds.n_planes, n_nodes=ds.n_nodes, grid=ds.grid,
                                timestep=ds.timestep, tau=config.tau, seed=config.seed,
@@ -307,9 +336,11 @@ def compress(ds: FDataset, config: PipelineConfig, state: TimestepState | None =
         for k, v in timer.result().items():
             stage_t[k] = stage_t.get(k, 0.0) + v
     stage_t["pack"] = stage_t.get("pack", 0.0) + time.perf_counter() - t0
+    if train_full is not None:
+        stage_t["train"] = t_train
     report.stage_timings = _timings(stage_t, time.perf_counter() - t_all)
-    new_state = TimestepState(models=list(state.models),
-                              timestep_index=state.timestep_index + 1)
+    new_state = TimestepState(models=models,
+                              timestep_index=(state.timestep_index if state else 0) + 1)
     return archive, report, new_state
 
 
@@ -352,7 +383,9 @@ def compress_distributed(ds: FDataset, config: PipelineConfig, state: TimestepSt
     t_all = time.perf_counter()
     sp = D_.split_plan(ds.n_planes, ds.n_nodes, config.shards, config.mode,
                        latent_dim=config.latent_dim, pq_bits=config.pq_bits)
-    _check_state(config, state, sp.n_shards)
+    if _check_state(config, state, sp.n_shards) is not None:
+        raise ConfigError("compress_distributed reuses trained models: pass a TimestepState "
+                          "with static_model=True (train with compress() or ae.train first)")
     dev = _device()
     trace = _Trace(f"rank {sp.rank}")
     f0 = upload_f0(ds.data[sp.plane_lo:sp.plane_hi], dev)
@@ -560,12 +593,24 @@ def evaluate(orig: FDataset, archive: bytes) -> ErrorReport:
 
 
 def run_timesteps(datasets, config: PipelineConfig, models=None):
-    """Compress a sequence with fixed models (static mode only, see compress)."""
+    """Compress a sequence; full training every retrain_period steps (pipeline.py:494-515).
+
+    Returns a list of (archive, report, mode), mode in {"full", "incremental",
+    "static"}.  ``models`` (optional, an extension of the reference API) seeds
+    the state with trained per-shard models instead of training at step 0."""
     if not datasets:
         raise ConfigError("need at least one timestep")
     state = TimestepState(models=list(models), timestep_index=0) if models else None
     out = []
-    for ds in datasets:
+    for index, ds in enumerate(datasets):
+        if state is None:
+            mode = "full"
+        elif config.static_model:
+            mode = "static"
+        elif index % config.retrain_period == 0:
+            mode = "full"
+        else:
+            mode = "incremental"
         archive, report, state = compress(ds, config, state)
-        out.append((archive, report, "static"))
+        out.append((archive, report, mode))
     return out
