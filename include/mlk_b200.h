@@ -365,7 +365,8 @@ int mlk_pack_exceptions(const double* f0, const MlkShard* shards, int32_t n_shar
  * base + row_off[i] (i < n, D doubles each, device), order is the epochs x n
  * table of rng.permutation draws (device int32), w (L x D f64, device) holds
  * the Glorot / warm-start weights on entry and the trained weights on exit,
- * mv is 2 x L x D f64 scratch.  bias (2T doubles, device) = [1 - beta1^t,
+ * mv is 2 x L x D f64 scratch, xn n x D f64 scratch (the normalised
+ * training images, written once per call).  bias (2T doubles, device) = [1 - beta1^t,
  * 1 - beta2^t] for t = 1..T, computed with Python floats.  norm (2 per job)
  * receives (mean, std); diag (2 per job) receives (-1, 0) or (epoch, mse) of
  * the first non-finite mse (TrainingDivergedError).  MLK_ERR_CONFIG when
@@ -377,6 +378,7 @@ typedef struct {
     const int32_t* order;
     double* w;
     double* mv;
+    double* xn;
     int32_t n;
     int32_t epochs;
 } MlkTrainJob;
@@ -385,6 +387,10 @@ int mlk_ae_train(const MlkTrainJob* jobs, const MlkTrainJob* jobs_h, int32_t n_j
                  int32_t D, int32_t batch, double lr, double beta1, double one_minus_beta1,
                  double beta2, double one_minus_beta2, double eps, const double* bias,
                  int32_t T, double* norm, double* diag, cudaStream_t stream);
+
+/* diagnostics: {cluster size, rows per chunk, columns per CTA, shared-memory
+ * bytes} of the last mlk_ae_train launch; out_h is a HOST array of 4. */
+int mlk_ae_train_config(int32_t* out_h, cudaStream_t stream);
 
 #ifdef __cplusplus
 }

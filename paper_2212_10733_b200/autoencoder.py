@@ -132,12 +132,13 @@ def train_jobs(jobs, config: TrainConfig, latent_dim: int, d: int):
         offs = torch.from_numpy(np.ascontiguousarray(jb.row_off, dtype=np.int64)).to(dev)
         od = torch.from_numpy(order).to(dev)
         mv = torch.empty(2 * L * d, dtype=torch.float64, device=dev)
-        keep += [offs, od, mv, jb.base]
+        xn = torch.empty(n * d, dtype=torch.float64, device=dev)
+        keep += [offs, od, mv, xn, jb.base]
         ws.append(wd)
         recs.append((jb.base.data_ptr(), offs.data_ptr(), od.data_ptr(), wd.data_ptr(),
-                     mv.data_ptr(), n, jb.epochs))
+                     mv.data_ptr(), xn.data_ptr(), n, jb.epochs))
     rec_t = np.dtype([("base", "<u8"), ("row_off", "<u8"), ("order", "<u8"), ("w", "<u8"),
-                      ("mv", "<u8"), ("n", "<i4"), ("epochs", "<i4")])
+                      ("mv", "<u8"), ("xn", "<u8"), ("n", "<i4"), ("epochs", "<i4")])
     table_h = np.array(recs, dtype=rec_t)
     table_d = torch.from_numpy(table_h.view(np.uint8).copy()).to(dev)
     bias_d = torch.from_numpy(bias.reshape(-1)).to(dev)

@@ -27,12 +27,15 @@
 // the three passes of a step.
 #include "common.cuh"
 
+#include <cooperative_groups.h>
+
+// launch configuration of the last mlk_ae_train call (diagnostics)
+static int g_train_cfg[4];
+
 namespace {
 
 constexpr int TT = 1024;        // threads per CTA
 constexpr int TW = TT / 32;     // warps
-constexpr int TCH = 128;        // batch rows per chunk (z / e staged in shared memory)
-constexpr int TMAX_LD = 12800;  // L * D limit: 2 * 8 * L * D + chunk tables <= 227 KB
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -51,25 +54,14 @@ __device__ double block_sum(double v, double* red) {
     return warp_sum(t);
 }
 
+// fit_normalizer (autoencoder.py:77-84): one CTA per job
 __global__ void __launch_bounds__(TT, 1)
-k_ae_train(const MlkTrainJob* __restrict__ jobs, int L, int D, int batch, double lr,
-           double b1, double omb1, double b2, double omb2, double eps,
-           const double* __restrict__ bias, int T, double* __restrict__ norm_out,
-           double* __restrict__ diag_out) {
-    extern __shared__ double sm[];
-    double* W = sm;                          // L * D
-    double* G = W + (size_t)L * D;           // L * D
-    double* Z = G + (size_t)L * D;           // TCH * L
-    double* E = Z + TCH * L;                 // TCH * L
-    double* red = E + TCH * L;               // TW
-    __shared__ const double* rowp[TCH];
-
+k_ae_norm(const MlkTrainJob* __restrict__ jobs, int D, double* __restrict__ norm_out,
+          double* __restrict__ diag_out) {
+    __shared__ double red[TW];
     const MlkTrainJob job = jobs[blockIdx.x];
     const int n = job.n;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const long long LD = (long long)L * D;
-
-    // ---- fit_normalizer (autoencoder.py:77-84) ----
     double s = 0.0;
     for (int i = warp; i < n; i += TW) {
         const double* r = job.base + job.row_off[i];
@@ -93,125 +85,222 @@ k_ae_train(const MlkTrainJob* __restrict__ jobs, int L, int D, int batch, double
         diag_out[2 * blockIdx.x] = -1.0;
         diag_out[2 * blockIdx.x + 1] = 0.0;
     }
+}
 
-    double* M = job.mv;
-    double* V = job.mv + LD;
-    for (long long k = tid; k < LD; k += TT) {
-        W[k] = job.w[k];
-        G[k] = 0.0;
-        M[k] = 0.0;
-        V[k] = 0.0;
+// x = (flat - mean) / std once per training image (autoencoder.py:150-151),
+// the same IEEE quotient the reference stores; grid (jobs, row blocks)
+__global__ void __launch_bounds__(256)
+k_ae_normalize(const MlkTrainJob* __restrict__ jobs, int D, const double* __restrict__ norm) {
+    const MlkTrainJob job = jobs[blockIdx.x];
+    const double mean = norm[2 * blockIdx.x], stdv = norm[2 * blockIdx.x + 1];
+    for (int i = blockIdx.y; i < job.n; i += gridDim.y) {
+        const double* r = job.base + job.row_off[i];
+        double* o = job.xn + (long long)i * D;
+        for (int d = threadIdx.x; d < D; d += blockDim.x) o[d] = (r[d] - mean) / stdv;
+    }
+}
+
+// One thread-block CLUSTER of C CTAs per job; CTA c owns columns
+// [c*DC, c*DC + nd) of W, its gradient and the Adam moments (all in shared
+// memory) and stages its column slice of TCH batch rows in shared memory.
+// Per chunk: partial z over the slice -> cluster barrier -> every CTA sums the
+// C partials in rank order from distributed shared memory (deterministic) ->
+// partial e = err W^T and err^2 -> barrier -> sum -> the gradient of the own
+// columns from the staged rows.  Adam is column-local.
+template <int LT>
+__global__ void __launch_bounds__(TT, 1)
+k_ae_train(const MlkTrainJob* __restrict__ jobs, int L_, int D, int DC, int TCH_, int batch,
+           double lr, double b1, double omb1, double b2, double omb2, double eps,
+           const double* __restrict__ bias, double* __restrict__ diag_out) {
+    namespace cg = cooperative_groups;
+    constexpr int LM = LT ? LT : MLK_MAXL;   // unrolled latent loop bound
+    const int L = LT ? LT : L_;
+    cg::cluster_group cluster = cg::this_cluster();
+    const int C = (int)cluster.num_blocks();
+    const int rank = (int)cluster.block_rank();
+    const int jid = blockIdx.x / C;
+    extern __shared__ double sm[];
+    double* W = sm;                      // L * DC
+    double* G = W + L * DC;              // L * DC
+    double* M = G + L * DC;              // L * DC
+    double* V = M + L * DC;              // L * DC
+    double* X = V + L * DC;              // TCH * DC
+    double* PZ = X + (size_t)TCH_ * DC;  // TCH * L  (partials, read remotely)
+    double* PE = PZ + TCH_ * L;          // TCH * L + 1 (partials + err^2, read remotely)
+    double* Z = PE + TCH_ * L + 1;       // TCH * L
+    double* E = Z + TCH_ * L;            // TCH * L
+    double* red = E + TCH_ * L;          // TW
+    double* P = red + TW;                // NG * L * DC gradient partials
+    __shared__ const double* rowp[128];
+
+    const MlkTrainJob job = jobs[jid];
+    const int n = job.n;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int d0 = rank * DC;
+    const int nd = max(0, min(DC, D - d0));
+
+    for (int o = tid; o < L * DC; o += TT) {
+        const int l = o / DC, k = o % DC;
+        W[o] = k < nd ? job.w[(long long)l * D + d0 + k] : 0.0;
+        G[o] = 0.0;
+        M[o] = 0.0;
+        V[o] = 0.0;
     }
     __syncthreads();
 
     int t = 0;
-    for (int e = 0; e < job.epochs; ++e) {
+    bool diverged = false;
+    for (int e = 0; e < job.epochs && !diverged; ++e) {
         const int32_t* ord = job.order + (long long)e * n;
         for (int start = 0; start < n; start += batch) {
             const int b = min(batch, n - start);
-            double sq = 0.0;
-            for (int c0 = 0; c0 < b; c0 += TCH) {
-                const int cb = min(TCH, b - c0);
-                if (tid < cb) rowp[tid] = job.base + job.row_off[ord[start + c0 + tid]];
+            double sq = 0.0;       // cluster total of err^2 (identical in every CTA)
+            for (int c0 = 0; c0 < b; c0 += TCH_) {
+                const int cb = min(TCH_, b - c0);
+                if (tid < cb) rowp[tid] = job.xn + (long long)ord[start + c0 + tid] * D + d0;
                 __syncthreads();
-                // phase A: one warp per row -> z (L), e = err W^T (L), err^2
+#pragma unroll 4
+                for (int r = warp; r < cb; r += TW)
+                    for (int k = lane; k < nd; k += 32) X[r * DC + k] = __ldg(rowp[r] + k);
+                __syncthreads();
+                // partial z over the own columns: one warp per row
                 for (int r = warp; r < cb; r += TW) {
-                    const double* x = rowp[r];
-                    double za[MLK_MAXL];
+                    double za[LM];
 #pragma unroll
-                    for (int l = 0; l < MLK_MAXL; ++l) za[l] = 0.0;
-                    for (int d = lane; d < D; d += 32) {
-                        const double xn = (x[d] - mean) / stdv;
+                    for (int l = 0; l < LM; ++l) za[l] = 0.0;
+                    for (int k = lane; k < nd; k += 32) {
+                        const double x = X[r * DC + k];
 #pragma unroll
-                        for (int l = 0; l < MLK_MAXL; ++l)
-                            if (l < L) za[l] = fma(xn, W[l * D + d], za[l]);
+                        for (int l = 0; l < LM; ++l)
+                            if (l < L) za[l] = fma(x, W[l * DC + k], za[l]);
                     }
 #pragma unroll
-                    for (int l = 0; l < MLK_MAXL; ++l)
-                        if (l < L) za[l] = warp_sum(za[l]);
-                    double ea[MLK_MAXL];
-#pragma unroll
-                    for (int l = 0; l < MLK_MAXL; ++l) ea[l] = 0.0;
-                    for (int d = lane; d < D; d += 32) {
-                        const double xn = (x[d] - mean) / stdv;
-                        double rec = 0.0;
-#pragma unroll
-                        for (int l = 0; l < MLK_MAXL; ++l)
-                            if (l < L) rec = fma(za[l], W[l * D + d], rec);
-                        const double er = rec - xn;
-                        sq = fma(er, er, sq);
-#pragma unroll
-                        for (int l = 0; l < MLK_MAXL; ++l)
-                            if (l < L) ea[l] = fma(er, W[l * D + d], ea[l]);
-                    }
-#pragma unroll
-                    for (int l = 0; l < MLK_MAXL; ++l)
-                        if (l < L) ea[l] = warp_sum(ea[l]);
-                    if (lane < L) {
-                        double zv = 0.0, ev = 0.0;
-#pragma unroll
-                        for (int l = 0; l < MLK_MAXL; ++l)
-                            if (l == lane) { zv = za[l]; ev = ea[l]; }
-                        Z[r * L + lane] = zv;
-                        E[r * L + lane] = ev;
-                    }
+                    for (int l = 0; l < LM; ++l)
+                        if (l < L) {
+                            const double v = warp_sum(za[l]);
+                            if (lane == 0) PZ[r * L + l] = v;
+                        }
+                }
+                cluster.sync();
+                for (int o = tid; o < cb * L; o += TT) {
+                    double v = 0.0;
+                    for (int c = 0; c < C; ++c) v += cluster.map_shared_rank(PZ, c)[o];
+                    Z[o] = v;
                 }
                 __syncthreads();
-                // phase B: one thread per column: G += z_r err_r + e_r x_r
-                for (int d = tid; d < D; d += TT) {
-                    double g[MLK_MAXL];
+                // err = z W - x; partial e = err W^T and err^2
+                double sql = 0.0;
+                for (int r = warp; r < cb; r += TW) {
+                    double ea[LM];
 #pragma unroll
-                    for (int l = 0; l < MLK_MAXL; ++l) g[l] = 0.0;
-                    double w[MLK_MAXL];
-#pragma unroll
-                    for (int l = 0; l < MLK_MAXL; ++l) w[l] = l < L ? W[l * D + d] : 0.0;
-                    for (int r = 0; r < cb; ++r) {
-                        const double xn = (rowp[r][d] - mean) / stdv;
+                    for (int l = 0; l < LM; ++l) ea[l] = 0.0;
+                    for (int k = lane; k < nd; k += 32) {
                         double rec = 0.0;
 #pragma unroll
-                        for (int l = 0; l < MLK_MAXL; ++l)
-                            if (l < L) rec = fma(Z[r * L + l], w[l], rec);
-                        const double er = rec - xn;
+                        for (int l = 0; l < LM; ++l)
+                            if (l < L) rec = fma(Z[r * L + l], W[l * DC + k], rec);
+                        const double er = rec - X[r * DC + k];
+                        sql = fma(er, er, sql);
 #pragma unroll
-                        for (int l = 0; l < MLK_MAXL; ++l)
-                            if (l < L) g[l] = fma(Z[r * L + l], er, fma(E[r * L + l], xn, g[l]));
+                        for (int l = 0; l < LM; ++l)
+                            if (l < L) ea[l] = fma(er, W[l * DC + k], ea[l]);
                     }
 #pragma unroll
-                    for (int l = 0; l < MLK_MAXL; ++l)
-                        if (l < L) G[l * D + d] += g[l];
+                    for (int l = 0; l < LM; ++l)
+                        if (l < L) {
+                            const double v = warp_sum(ea[l]);
+                            if (lane == 0) PE[r * L + l] = v;
+                        }
+                }
+                sql = warp_sum(sql);
+                if (lane == 0) red[warp] = sql;
+                __syncthreads();
+                if (tid == 0) {
+                    double v = 0.0;
+                    for (int w = 0; w < TW; ++w) v += red[w];
+                    PE[TCH_ * L] = v;
+                }
+                cluster.sync();
+                for (int o = tid; o < cb * L; o += TT) {
+                    double v = 0.0;
+                    for (int c = 0; c < C; ++c) v += cluster.map_shared_rank(PE, c)[o];
+                    E[o] = v;
+                }
+                for (int c = 0; c < C; ++c) sq += cluster.map_shared_rank(PE, c)[TCH_ * L];
+                __syncthreads();
+                // gradient of the own columns: G += z_r err_r + e_r x_r.  Thread
+                // (k, grp) sums rows grp, grp + NG, ... for every l; the NG
+                // partials are then added in group order (deterministic)
+                {
+                    const int NG = max(1, min(8, TT / max(nd, 1)));
+                    if (tid < NG * nd) {
+                        const int k = tid % nd, grp = tid / nd;
+                        double w[LM], g[LM];
+#pragma unroll
+                        for (int l = 0; l < LM; ++l) {
+                            w[l] = l < L ? W[l * DC + k] : 0.0;
+                            g[l] = 0.0;
+                        }
+                        for (int r = grp; r < cb; r += NG) {
+                            const double x = X[r * DC + k];
+                            double rec = 0.0;
+#pragma unroll
+                            for (int l = 0; l < LM; ++l)
+                                if (l < L) rec = fma(Z[r * L + l], w[l], rec);
+                            const double er = rec - x;
+#pragma unroll
+                            for (int l = 0; l < LM; ++l)
+                                if (l < L) g[l] = fma(Z[r * L + l], er, fma(E[r * L + l], x, g[l]));
+                        }
+#pragma unroll
+                        for (int l = 0; l < LM; ++l)
+                            if (l < L) P[(grp * L + l) * DC + k] = g[l];
+                    }
+                    __syncthreads();
+                    for (int o = tid; o < L * nd; o += TT) {
+                        const int l = o / nd, k = o - l * nd;
+                        double v = 0.0;
+                        for (int q = 0; q < NG; ++q) v += P[(q * L + l) * DC + k];
+                        G[l * DC + k] += v;
+                    }
                 }
                 __syncthreads();
             }
             // mse = mean(err ** 2); non-finite -> TrainingDivergedError(epoch, mse)
-            const double mse = block_sum(sq, red) / ((double)b * (double)D);
+            const double mse = sq / ((double)b * (double)D);
             if (!isfinite(mse)) {
-                if (tid == 0) {
-                    diag_out[2 * blockIdx.x] = (double)e;
-                    diag_out[2 * blockIdx.x + 1] = mse;
+                if (tid == 0 && rank == 0) {
+                    diag_out[2 * jid] = (double)e;
+                    diag_out[2 * jid + 1] = mse;
                 }
-                return;
+                diverged = true;
+                break;
             }
             ++t;
             const double bc1 = bias[2 * (t - 1)], bc2 = bias[2 * (t - 1) + 1];
             const double scale = 2.0 / ((double)b * (double)D);
             // Adam (autoencoder.py:168-173), numpy's elementwise rounding order
-            for (long long k = tid; k < LD; k += TT) {
-                const double gr = __dmul_rn(scale, G[k]);
-                const double m = __dadd_rn(__dmul_rn(b1, M[k]), __dmul_rn(omb1, gr));
-                const double v = __dadd_rn(__dmul_rn(b2, V[k]), __dmul_rn(omb2, __dmul_rn(gr, gr)));
-                M[k] = m;
-                V[k] = v;
+            for (int o = tid; o < L * DC; o += TT) {
+                const double gr = __dmul_rn(scale, G[o]);
+                const double m = __dadd_rn(__dmul_rn(b1, M[o]), __dmul_rn(omb1, gr));
+                const double v = __dadd_rn(__dmul_rn(b2, V[o]), __dmul_rn(omb2, __dmul_rn(gr, gr)));
+                M[o] = m;
+                V[o] = v;
                 const double mhat = __ddiv_rn(m, bc1);
                 const double vhat = __ddiv_rn(v, bc2);
                 const double up = __ddiv_rn(__dmul_rn(lr, mhat), __dadd_rn(__dsqrt_rn(vhat), eps));
-                W[k] = __dsub_rn(W[k], up);
-                G[k] = 0.0;
+                W[o] = __dsub_rn(W[o], up);
+                G[o] = 0.0;
             }
             __syncthreads();
         }
     }
-    for (long long k = tid; k < LD; k += TT) job.w[k] = W[k];
-    (void)T;
+    if (!diverged)
+        for (int o = tid; o < L * DC; o += TT) {
+            const int l = o / DC, k = o % DC;
+            if (k < nd) job.w[(long long)l * D + d0 + k] = W[o];
+        }
+    cluster.sync();   // no CTA leaves while a peer may still read its partials
 }
 
 }  // namespace
@@ -223,18 +312,78 @@ extern "C" int mlk_ae_train(const MlkTrainJob* jobs, const MlkTrainJob* jobs_h, 
                             double* diag, cudaStream_t stream) {
     if (n_jobs < 1 || L < 1 || L > MLK_MAXL || D < 1 || D > MLK_MAX_D || batch < 1)
         return MLK_ERR_CONFIG;
-    if ((long long)L * D > TMAX_LD) return MLK_ERR_CONFIG;
     for (int j = 0; j < n_jobs; ++j) {
         const MlkTrainJob& jb = jobs_h[j];
         if (jb.n < 1 || jb.epochs < 1) return MLK_ERR_CONFIG;
         const long long steps = (long long)jb.epochs * ((jb.n + batch - 1) / batch);
         if (steps > T) return MLK_ERR_SIZE;
     }
-    const size_t dyn = sizeof(double) * ((size_t)2 * L * D + 2 * TCH * L + TW);
-    if (cudaFuncSetAttribute(k_ae_train, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)dyn) != cudaSuccess)
-        return MLK_ERR_CUDA;
-    k_ae_train<<<n_jobs, TT, dyn, stream>>>(jobs, L, D, batch, lr, beta1, one_minus_beta1, beta2,
-                                            one_minus_beta2, eps, bias, T, norm, diag);
+    int max_n = 0;
+    for (int j = 0; j < n_jobs; ++j) max_n = max(max_n, jobs_h[j].n);
+    // cluster size: 16 CTAs per job when the device can co-schedule them, else 8
+    int C = 16;
+    auto kern = L == 4 ? k_ae_train<4> : k_ae_train<0>;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
+        cudaSuccess)
+        C = 8;
+    size_t dyn = 0;
+    int tch = 0;
+    for (;; C /= 2) {
+        const int DC = (D + C - 1) / C;
+        const size_t fixed = sizeof(double) * ((size_t)12 * L * DC + 1 + TW);
+        const size_t per_row = sizeof(double) * ((size_t)DC + 4 * L);
+        const size_t budget = 220 * 1024;
+        tch = 0;
+        if (fixed < budget) {
+            const size_t rows = (budget - fixed) / per_row;
+            tch = rows > 128 ? 128 : (int)rows;
+        }
+        if (tch < 1) {
+            if (C == 1) return MLK_ERR_CONFIG;
+            continue;
+        }
+        dyn = fixed + per_row * tch;
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)dyn) != cudaSuccess)
+            return MLK_ERR_CUDA;
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(n_jobs * C);
+        cfg.blockDim = dim3(TT);
+        cfg.dynamicSmemBytes = dyn;
+        cfg.stream = stream;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = C;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        int ok = 0;
+        if (cudaOccupancyMaxActiveClusters(&ok, kern, &cfg) != cudaSuccess) {
+            cudaGetLastError();
+            ok = 0;
+        }
+        if (ok < 1 && C > 1) continue;
+        k_ae_norm<<<n_jobs, TT, 0, stream>>>(jobs, D, norm, diag);
+        k_ae_normalize<<<dim3(n_jobs, min(max_n, 1184)), 256, 0, stream>>>(jobs, D, norm);
+        const int DCv = (D + C - 1) / C;
+        g_train_cfg[0] = C;
+        g_train_cfg[1] = tch;
+        g_train_cfg[2] = DCv;
+        g_train_cfg[3] = (int)dyn;
+        if (cudaLaunchKernelEx(&cfg, kern, (const MlkTrainJob*)jobs, (int)L, (int)D, DCv,
+                               tch, (int)batch, lr, beta1, one_minus_beta1, beta2,
+                               one_minus_beta2, eps, bias, diag) != cudaSuccess)
+            return MLK_ERR_CUDA;
+        break;
+    }
     return cudaGetLastError() == cudaSuccess ? MLK_OK : MLK_ERR_CUDA;
+}
+
+// diagnostics: {cluster size, rows per chunk, columns per CTA, shared bytes}
+// of the last mlk_ae_train launch; out_h is a HOST array of 4
+extern "C" int mlk_ae_train_config(int32_t* out_h, cudaStream_t stream) {
+    (void)stream;
+    for (int i = 0; i < 4; ++i) out_h[i] = g_train_cfg[i];
+    return MLK_OK;
 }
