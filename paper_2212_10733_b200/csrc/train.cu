@@ -100,6 +100,22 @@ k_ae_normalize(const MlkTrainJob* __restrict__ jobs, int D, const double* __rest
     }
 }
 
+// sum of p[o] over the cluster's CTAs in rank order; every remote load is
+// issued before the first add
+__device__ __forceinline__ double cluster_sum(cooperative_groups::cluster_group& cl,
+                                              double* p, int o, int C) {
+    double s = 0.0;
+    for (int c0 = 0; c0 < C; c0 += 8) {
+        double v[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) v[c] = c0 + c < C ? cl.map_shared_rank(p, c0 + c)[o] : 0.0;
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+            if (c0 + c < C) s += v[c];
+    }
+    return s;
+}
+
 // One thread-block CLUSTER of C CTAs per job; CTA c owns columns
 // [c*DC, c*DC + nd) of W, its gradient and the Adam moments (all in shared
 // memory) and stages its column slice of TCH batch rows in shared memory.
@@ -182,11 +198,7 @@ k_ae_train(const MlkTrainJob* __restrict__ jobs, int L_, int D, int DC, int TCH_
                         }
                 }
                 cluster.sync();
-                for (int o = tid; o < cb * L; o += TT) {
-                    double v = 0.0;
-                    for (int c = 0; c < C; ++c) v += cluster.map_shared_rank(PZ, c)[o];
-                    Z[o] = v;
-                }
+                for (int o = tid; o < cb * L; o += TT) Z[o] = cluster_sum(cluster, PZ, o, C);
                 __syncthreads();
                 // err = z W - x; partial e = err W^T and err^2
                 double sql = 0.0;
@@ -221,12 +233,8 @@ k_ae_train(const MlkTrainJob* __restrict__ jobs, int L_, int D, int DC, int TCH_
                     PE[TCH_ * L] = v;
                 }
                 cluster.sync();
-                for (int o = tid; o < cb * L; o += TT) {
-                    double v = 0.0;
-                    for (int c = 0; c < C; ++c) v += cluster.map_shared_rank(PE, c)[o];
-                    E[o] = v;
-                }
-                for (int c = 0; c < C; ++c) sq += cluster.map_shared_rank(PE, c)[TCH_ * L];
+                for (int o = tid; o < cb * L; o += TT) E[o] = cluster_sum(cluster, PE, o, C);
+                sq += cluster_sum(cluster, PE, TCH_ * L, C);
                 __syncthreads();
                 // gradient of the own columns: G += z_r err_r + e_r x_r.  Thread
                 // (k, grp) sums rows grp, grp + NG, ... for every l; the NG
