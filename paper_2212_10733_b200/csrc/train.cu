@@ -65,15 +65,17 @@ k_ae_norm(const MlkTrainJob* __restrict__ jobs, int D, double* __restrict__ norm
     double s = 0.0;
     for (int i = warp; i < n; i += TW) {
         const double* r = job.base + job.row_off[i];
-        for (int d = lane; d < D; d += 32) s += r[d];
+#pragma unroll 8
+        for (int d = lane; d < D; d += 32) s += __ldg(r + d);
     }
     const double cnt = (double)n * (double)D;
     const double mean = block_sum(s, red) / cnt;
     double q = 0.0;
     for (int i = warp; i < n; i += TW) {
         const double* r = job.base + job.row_off[i];
+#pragma unroll 8
         for (int d = lane; d < D; d += 32) {
-            const double t = r[d] - mean;
+            const double t = __ldg(r + d) - mean;
             q += t * t;
         }
     }
