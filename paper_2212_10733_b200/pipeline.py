@@ -141,18 +141,32 @@ def _check_state(config, state, n_shards):
 def _train_models(f0, shards, ds, config, state, train_full):
     """Per-shard AE training on the device (pipeline.py:208-218): selection
     indices and PCG64 draws on the host, every shard's Adam run in ONE
-    mlk_ae_train launch over the device-resident f0."""
+    mlk_ae_train launch.  f0 = the device-resident dataset (flat, the
+    dataset's own layout), or None: then only the selected training rows are
+    gathered on the host and uploaded (compress_distributed, where a rank
+    holds just its slab of planes; every rank trains every shard with the
+    same deterministic kernel, so all ranks hold identical models)."""
     D = ds.grid.rows * ds.grid.cols
     epochs = config.epochs_full if train_full else config.epochs_incremental
     tc = ae.TrainConfig(learning_rate=config.learning_rate, batch_size=config.batch_size,
                         epochs=epochs, seed=0)
-    jobs = []
-    for i, sh in enumerate(shards):
+    sels = []
+    for sh in shards:
         seed = mix_seed(config.seed, sh.worker_id)
-        sel = select_training(sh, config.scheme, ds.n_planes, seed)
-        rows = shard_dataset_index(sh, ds.n_nodes)[sel] * D
-        init = None if train_full else state.models[i]
-        jobs.append(ae.TrainJob(base=f0, row_off=rows, epochs=epochs, seed=seed, init=init))
+        sels.append((seed, shard_dataset_index(sh, ds.n_nodes)[
+            select_training(sh, config.scheme, ds.n_planes, seed)]))
+    if f0 is None:
+        idx = np.concatenate([ix for _, ix in sels])
+        rows = np.ascontiguousarray(ds.data.reshape(-1, D)[idx], dtype=np.float64)
+        f0 = torch.from_numpy(rows.reshape(-1)).to(_device())
+        starts = np.cumsum([0] + [len(ix) for _, ix in sels])
+        offs = [(starts[i] + np.arange(len(ix), dtype=np.int64)) * D
+                for i, (_, ix) in enumerate(sels)]
+    else:
+        offs = [ix * D for _, ix in sels]
+    jobs = [ae.TrainJob(base=f0, row_off=o, epochs=epochs, seed=seed,
+                        init=None if train_full else state.models[i])
+            for i, ((seed, _), o) in enumerate(zip(sels, offs))]
     return ae.train_jobs(jobs, tc, config.latent_dim, D)
 
 
@@ -363,7 +377,7 @@ class _Trace:
             print(f"[trace {self.tag}] " + " | ".join(self.parts), flush=True)
 
 
-def compress_distributed(ds: FDataset, config: PipelineConfig, state: TimestepState,
+def compress_distributed(ds: FDataset, config: PipelineConfig, state: TimestepState | None,
                          out_path: str | None = None, group=None):
     """compress() with one process per GPU (torch.distributed initialised).
 
@@ -383,15 +397,19 @@ def compress_distributed(ds: FDataset, config: PipelineConfig, state: TimestepSt
     t_all = time.perf_counter()
     sp = D_.split_plan(ds.n_planes, ds.n_nodes, config.shards, config.mode,
                        latent_dim=config.latent_dim, pq_bits=config.pq_bits)
-    if _check_state(config, state, sp.n_shards) is not None:
-        raise ConfigError("compress_distributed reuses trained models: pass a TimestepState "
-                          "with static_model=True (train with compress() or ae.train first)")
+    train_full = _check_state(config, state, sp.n_shards)
     dev = _device()
     trace = _Trace(f"rank {sp.rank}")
     f0 = upload_f0(ds.data[sp.plane_lo:sp.plane_hi], dev)
     dgrid = _device_grid(ds.grid, dev, config.latent_dim)
     trace.mark("upload issued")
-    works = engine.split_layout(sp, state.models, ds.grid.rows, ds.grid.cols)
+    if train_full is None:
+        models = list(state.models)
+    else:
+        models = _train_models(None, partition(ds.n_planes, ds.n_nodes, config.shards,
+                                               config.mode), ds, config, state, train_full)
+        trace.mark("train")
+    works = engine.split_layout(sp, models, ds.grid.rows, ds.grid.cols)
     out = engine.compress_device(f0, works, dgrid, config, comm=D_.Comm(sp, group))
     trace.mark("device")
     preamble = ArchivePreamble(n_shards=sp.n_shards, decomp_mode=config.mode,
@@ -463,8 +481,9 @@ def compress_distributed(ds: FDataset, config: PipelineConfig, state: TimestepSt
         exception_count=int(st["exceptions"][0]),
         stage_timings={"other": {"sum": time.perf_counter() - t_all,
                                  "max": time.perf_counter() - t_all}})
-    return out_path, report, TimestepState(models=list(state.models),
-                                           timestep_index=state.timestep_index + 1)
+    return out_path, report, TimestepState(models=models,
+                                           timestep_index=(state.timestep_index if state
+                                                           else 0) + 1)
 
 
 def build_report(ds, archive_len, outs, tau, stage_t, wall) -> ErrorReport:
