@@ -67,6 +67,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--out", default=None)
     ap.add_argument("--no-clocks", action="store_true")
+    ap.add_argument("--no-train", action="store_true")
     return ap.parse_args()
 
 
@@ -435,6 +436,31 @@ def main():
                "sample": f"plane 0 of the corpus ({n} histograms, 8 shards), oracle/port.py, "
                          f"{threads} threads, {dt:.1f} s"}
 
+    train = None
+    if rank == 0 and world == 1 and not devgen and not args.no_train:
+        # SURVEY §8f rank 4, not part of the compress step above: the device
+        # AE training compress(ds, cfg, None) runs (8 shards x epochs_full),
+        # event-timed on the resident f0, compared with the golden models
+        try:
+            from paper_2212_10733_b200.decomp import partition
+            shards_all = partition(ds.n_planes, ds.n_nodes, cfg.shards, cfg.mode)
+            tms = []
+            for _ in range(2):
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record()
+                tmodels = pipeline._train_models(f0, shards_all, ds, cfg, None, True)
+                e1.record()
+                torch.cuda.synchronize()
+                tms.append(e0.elapsed_time(e1))
+            same = sum(int(np.array_equal(a.weights, b.weights)) for a, b in zip(tmodels, models))
+            train = {"ms": tms[-1], "shards": len(shards_all), "epochs": cfg.epochs_full,
+                     "batch": cfg.batch_size,
+                     "f32_weights_identical_to_reference_models": f"{same}/{len(models)}",
+                     "api": "pipeline._train_models (= compress(ds, cfg, None)'s training)"}
+        except Exception as exc:  # reported, never fatal to the bench line
+            train = {"error": repr(exc)[:200]}
+
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "hist/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
@@ -450,7 +476,7 @@ def main():
                 "stage_ms_by_rank": stage_by_rank, "probe_rounds": probe_rounds,
                 "newton": newton, "roofline": roofline, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e,
                 "decompress_and_report": dec, "gpu_launches": launches,
-                "clocks": clk.summary(),
+                "train": train, "clocks": clk.summary(),
                 "ratio": None if dec is None else dec["ratio"]}
         if world > 1:
             line["scaling"] = "strong"
