@@ -43,6 +43,23 @@ __device__ __forceinline__ double warp_sum(double v) {
     return v;
 }
 
+// four warp sums in 6 shuffle rounds instead of 20 (reduce-scatter over lane
+// bits 4 and 3, then a 3-level tree); lane 8*i (i = 0..3) writes sum i to out[i]
+__device__ __forceinline__ void warp_sum4(const double* v, int lane, double* out) {
+    const bool h16 = lane & 16, h8 = lane & 8;
+    double k0 = h16 ? v[2] : v[0], k1 = h16 ? v[3] : v[1];
+    const double s0 = h16 ? v[0] : v[2], s1 = h16 ? v[1] : v[3];
+    k0 += __shfl_xor_sync(0xffffffffu, s0, 16);
+    k1 += __shfl_xor_sync(0xffffffffu, s1, 16);
+    double k = h8 ? k1 : k0;
+    const double s = h8 ? k0 : k1;
+    k += __shfl_xor_sync(0xffffffffu, s, 8);
+    k += __shfl_xor_sync(0xffffffffu, k, 4);
+    k += __shfl_xor_sync(0xffffffffu, k, 2);
+    k += __shfl_xor_sync(0xffffffffu, k, 1);
+    if ((lane & 7) == 0) out[(h16 ? 2 : 0) + (h8 ? 1 : 0)] = k;
+}
+
 // block sum; every thread gets the total (red holds TW doubles)
 __device__ double block_sum(double v, double* red) {
     v = warp_sum(v);
@@ -192,12 +209,16 @@ k_ae_train(const MlkTrainJob* __restrict__ jobs, int L_, int D, int DC, int TCH_
                         for (int l = 0; l < LM; ++l)
                             if (l < L) za[l] = fma(x, W[l * DC + k], za[l]);
                     }
+                    if constexpr (LT == 4) {
+                        warp_sum4(za, lane, PZ + r * 4);
+                    } else {
 #pragma unroll
-                    for (int l = 0; l < LM; ++l)
-                        if (l < L) {
-                            const double v = warp_sum(za[l]);
-                            if (lane == 0) PZ[r * L + l] = v;
-                        }
+                        for (int l = 0; l < LM; ++l)
+                            if (l < L) {
+                                const double v = warp_sum(za[l]);
+                                if (lane == 0) PZ[r * L + l] = v;
+                            }
+                    }
                 }
                 cluster.sync();
                 for (int o = tid; o < cb * L; o += TT) Z[o] = cluster_sum(cluster, PZ, o, C);
@@ -219,12 +240,16 @@ k_ae_train(const MlkTrainJob* __restrict__ jobs, int L_, int D, int DC, int TCH_
                         for (int l = 0; l < LM; ++l)
                             if (l < L) ea[l] = fma(er, W[l * DC + k], ea[l]);
                     }
+                    if constexpr (LT == 4) {
+                        warp_sum4(ea, lane, PE + r * 4);
+                    } else {
 #pragma unroll
-                    for (int l = 0; l < LM; ++l)
-                        if (l < L) {
-                            const double v = warp_sum(ea[l]);
-                            if (lane == 0) PE[r * L + l] = v;
-                        }
+                        for (int l = 0; l < LM; ++l)
+                            if (l < L) {
+                                const double v = warp_sum(ea[l]);
+                                if (lane == 0) PE[r * L + l] = v;
+                            }
+                    }
                 }
                 sql = warp_sum(sql);
                 if (lane == 0) red[warp] = sql;
