@@ -119,15 +119,15 @@ k_ae_normalize(const MlkTrainJob* __restrict__ jobs, int D, const double* __rest
     }
 }
 
-// sum of p[o] over the cluster's CTAs in rank order; every remote load is
-// issued before the first add
-__device__ __forceinline__ double cluster_sum(cooperative_groups::cluster_group& cl,
-                                              double* p, int o, int C) {
+// sum of p[o] over the cluster's CTAs in rank order (rp = the peers' mapped
+// addresses of p, computed once); every remote load of a batch is issued
+// before the first add
+__device__ __forceinline__ double cluster_sum(double* const* rp, int o, int C) {
     double s = 0.0;
     for (int c0 = 0; c0 < C; c0 += 8) {
         double v[8];
 #pragma unroll
-        for (int c = 0; c < 8; ++c) v[c] = c0 + c < C ? cl.map_shared_rank(p, c0 + c)[o] : 0.0;
+        for (int c = 0; c < 8; ++c) v[c] = c0 + c < C ? rp[c0 + c][o] : 0.0;
 #pragma unroll
         for (int c = 0; c < 8; ++c)
             if (c0 + c < C) s += v[c];
@@ -167,11 +167,17 @@ k_ae_train(const MlkTrainJob* __restrict__ jobs, int L_, int D, int DC, int TCH_
     double* red = E + TCH_ * L;          // TW
     double* P = red + TW;                // NG * L * DC gradient partials
     __shared__ const double* rowp[128];
+    __shared__ double* rPZ[16];
+    __shared__ double* rPE[16];
 
     const MlkTrainJob job = jobs[jid];
     const int n = job.n;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int d0 = rank * DC;
+    if (tid < C) {
+        rPZ[tid] = cluster.map_shared_rank(PZ, tid);
+        rPE[tid] = cluster.map_shared_rank(PE, tid);
+    }
     const int nd = max(0, min(DC, D - d0));
 
     for (int o = tid; o < L * DC; o += TT) {
@@ -221,7 +227,7 @@ k_ae_train(const MlkTrainJob* __restrict__ jobs, int L_, int D, int DC, int TCH_
                     }
                 }
                 cluster.sync();
-                for (int o = tid; o < cb * L; o += TT) Z[o] = cluster_sum(cluster, PZ, o, C);
+                for (int o = tid; o < cb * L; o += TT) Z[o] = cluster_sum(rPZ, o, C);
                 __syncthreads();
                 // err = z W - x; partial e = err W^T and err^2
                 double sql = 0.0;
@@ -260,8 +266,8 @@ k_ae_train(const MlkTrainJob* __restrict__ jobs, int L_, int D, int DC, int TCH_
                     PE[TCH_ * L] = v;
                 }
                 cluster.sync();
-                for (int o = tid; o < cb * L; o += TT) E[o] = cluster_sum(cluster, PE, o, C);
-                sq += cluster_sum(cluster, PE, TCH_ * L, C);
+                for (int o = tid; o < cb * L; o += TT) E[o] = cluster_sum(rPE, o, C);
+                sq += cluster_sum(rPE, TCH_ * L, C);
                 __syncthreads();
                 // gradient of the own columns: G += z_r err_r + e_r x_r.  Thread
                 // (k, grp) sums rows grp, grp + NG, ... for every l; the NG
