@@ -150,3 +150,23 @@ def test_run_timesteps_modes():
                                                        static_model=True))
     assert [m for _, _, m in out] == ["full", "static"]
     assert out[0][0][:100] == out[1][0][:100]
+
+
+def test_train_config_validation_and_no_cpu_fallback():
+    """TrainConfig rejects what the reference rejects (autoencoder.py:70-75);
+    without a CUDA device train() raises BackendError -- there is no host
+    fallback for the trainer."""
+    import torch
+
+    import paper_2212_10733_b200 as mb
+    with pytest.raises(mb.ConfigError):
+        mb.TrainConfig(learning_rate=0.0)
+    with pytest.raises(mb.ConfigError):
+        mb.TrainConfig(batch_size=0)
+    with pytest.raises(mb.ConfigError):
+        mb.TrainConfig(epochs=0)
+    if torch.cuda.is_available():
+        pytest.skip("a CUDA device is present")
+    imgs = np.ones((4, 39, 39))
+    with pytest.raises(mb.BackendError):
+        mb.train(imgs, mb.TrainConfig(epochs=1))
