@@ -308,6 +308,31 @@ int mlk_compare(const double* a, const double* b, int32_t total, const MlkGrid* 
                 double* err, double* sse, double* qa, double* qb, double* ext,
                 cudaStream_t stream);
 
+/* The report's reductions (pipeline._build_report, pipeline.py:367-391;
+ * qoi.py:122-133) over the per-image arrays mlk_project leaves in HBM.  One
+ * segment per CompressOut (DEVICE arrays of n images); order (device int64,
+ * may be NULL) is each image's dataset index.  out (MLK_REPORT_NVALS doubles,
+ * device) = [data max, data min, sum fsse, defined-QoI count, converged,
+ * ae_ok, selected, exceptions, qoi d2 (4), qoi max (4), qoi min (4)] with
+ * identities (-inf / +inf / 0) for empty input; per_image (may be NULL)
+ * receives ferr in dataset order, 0 for exceptions.  scratch >= 20 * 296 *
+ * n_segs doubles. */
+#define MLK_REPORT_NVALS 20
+typedef struct {
+    const uint8_t* flags;
+    const int32_t* status;
+    const double* stats;   /* (n, 4) */
+    const double* qoi;     /* (n, 4) */
+    const double* fqoi;    /* (n, 4) */
+    const double* fsse;    /* (n) */
+    const double* ferr;    /* (n) */
+    const int64_t* order;  /* (n) or NULL */
+    int64_t n;
+} MlkReportSeg;
+
+int mlk_report(const MlkReportSeg* segs_h, int32_t n_segs, double* scratch,
+               int64_t scratch_doubles, double* out, double* per_image, cudaStream_t stream);
+
 /* HOST function: walk one shard's residual section (pipeline.py:140-156 and
  * the payload header of residual.py:81-98) over host memory `sec` (len
  * bytes).  For entry k: idx (image index), body_off = base + offset of its
@@ -365,12 +390,13 @@ int mlk_pack_exceptions(const double* f0, const MlkShard* shards, int32_t n_shar
  * base + row_off[i] (i < n, D doubles each, device), order is the epochs x n
  * table of rng.permutation draws (device int32), w (L x D f64, device) holds
  * the Glorot / warm-start weights on entry and the trained weights on exit,
- * mv is 2 x L x D f64 scratch, xn n x D f64 scratch (the normalised
+ * mv is reserved (unused; NULL), xn n x D f64 scratch (the normalised
  * training images, written once per call).  bias (2T doubles, device) = [1 - beta1^t,
  * 1 - beta2^t] for t = 1..T, computed with Python floats.  norm (2 per job)
  * receives (mean, std); diag (2 per job) receives (-1, 0) or (epoch, mse) of
- * the first non-finite mse (TrainingDivergedError).  MLK_ERR_CONFIG when
- * L * D > 12800 (shared-memory residency of W and its gradient). */
+ * the first non-finite mse (TrainingDivergedError).  MLK_ERR_CONFIG when the
+ * per-CTA column slice of W, its gradient and both Adam moments does not fit
+ * shared memory even at the largest cluster size. */
 #define MLK_STD_FLOOR 1e-30   /* autoencoder.STD_FLOOR */
 typedef struct {
     const double* base;
@@ -383,7 +409,25 @@ typedef struct {
     int32_t epochs;
 } MlkTrainJob;
 
-int mlk_ae_train(const MlkTrainJob* jobs, const MlkTrainJob* jobs_h, int32_t n_jobs, int32_t L,
+/* numpy's pairwise summation of a job's n*D training entries laid out as a
+ * tree (autoencoder.pairwise_tree): leaves [leaf_start, +leaf_len) of <= 128
+ * entries, then internal nodes level by level, deepest first (node
+ * n_leaves + k = node child[2k] + node child[2k+1] for k in level_off[lv] ..
+ * level_off[lv+1]); nodes is scratch for n_leaves + level_off[n_levels]
+ * doubles.  fit_normalizer's mean and std are computed through it. */
+typedef struct {
+    const int64_t* leaf_start;
+    const int32_t* leaf_len;
+    const int32_t* child;
+    const int32_t* level_off;
+    double* nodes;
+    int64_t n_total;
+    int32_t n_leaves;
+    int32_t n_levels;
+} MlkPwTree;
+
+int mlk_ae_train(const MlkTrainJob* jobs, const MlkTrainJob* jobs_h, const MlkPwTree* trees,
+                 const MlkPwTree* trees_h, int32_t n_jobs, int32_t L,
                  int32_t D, int32_t batch, double lr, double beta1, double one_minus_beta1,
                  double beta2, double one_minus_beta2, double eps, const double* bias,
                  int32_t T, double* norm, double* diag, cudaStream_t stream);

@@ -636,14 +636,24 @@ def manifest_nbytes(data, grid: Grid, timestep=0) -> int:
     return data.size * 8 + len(json.dumps(man, indent=1))
 
 
-def compress(data, grid: Grid, cfg: Cfg, models, timestep=0):
-    """pipeline.py:323-391 with every shard run serially (results do not depend
-    on the worker count, pipeline.py:4-7).  Returns (archive, report, shards)."""
+def compress(data, grid: Grid, cfg: Cfg, models, timestep=0, threads=1):
+    """pipeline.py:323-391: shards on a thread pool like the reference's
+    workers (pipeline.py:338-342; results do not depend on the worker count,
+    pipeline.py:4-7), then the archive and the report.  Returns (archive,
+    report, shards)."""
     P, N = data.shape[:2]
     members = shard_members(P, N, cfg.shards, cfg.mode)
-    outs = []
-    for wid, (pl, no) in enumerate(members):
-        outs.append(compress_shard(data[pl, no], grid, cfg, models[wid], wid))
+
+    def job(wid):
+        pl, no = members[wid]
+        return compress_shard(data[pl, no], grid, cfg, models[wid], wid)
+
+    if threads > 1:
+        from concurrent.futures import ThreadPoolExecutor
+        with ThreadPoolExecutor(max_workers=threads) as ex:
+            outs = list(ex.map(job, range(len(members))))
+    else:
+        outs = [job(w) for w in range(len(members))]
     arc = archive(grid, cfg, P, N, timestep, [o.blob for o in outs])
     recon = np.empty_like(data)
     for (pl, no), o in zip(members, outs):
@@ -709,13 +719,25 @@ def decode_shard(blob, grid: Grid):
     return rec, corrected, final
 
 
-def decompress(arc):
+def decompress(arc, threads=1):
+    """pipeline.py:430-440 (shards decoded independently, on a thread pool)."""
     grid, meta, blobs = unarchive(arc)
     P, N = meta["n_planes"], meta["n_nodes"]
     r, c = grid.vol.shape
     out = np.empty((P, N, r, c))
-    for (pl, no), b in zip(shard_members(P, N, len(blobs), meta["mode"]), blobs):
-        out[pl, no] = decode_shard(b, grid)[2]
+    members = shard_members(P, N, len(blobs), meta["mode"])
+
+    def job(k):
+        pl, no = members[k]
+        out[pl, no] = decode_shard(blobs[k], grid)[2]
+
+    if threads > 1:
+        from concurrent.futures import ThreadPoolExecutor
+        with ThreadPoolExecutor(max_workers=threads) as ex:
+            list(ex.map(job, range(len(blobs))))
+    else:
+        for k in range(len(blobs)):
+            job(k)
     return out, grid, meta
 
 

@@ -49,6 +49,15 @@ class MlkNewton(ctypes.Structure):
                 ("lam_f32", ctypes.c_int32), ("tau", ctypes.c_double)]
 
 
+class MlkReportSeg(ctypes.Structure):
+    _fields_ = [("flags", ctypes.c_void_p), ("status", ctypes.c_void_p),
+                ("stats", ctypes.c_void_p), ("qoi", ctypes.c_void_p), ("fqoi", ctypes.c_void_p),
+                ("fsse", ctypes.c_void_p), ("ferr", ctypes.c_void_p), ("order", ctypes.c_void_p),
+                ("n", ctypes.c_int64)]
+
+
+REPORT_NVALS = 20
+
 assert ctypes.sizeof(MlkShard) == 72
 assert ctypes.sizeof(MlkGrid) == 136
 
@@ -95,7 +104,8 @@ _SIGS = {
     "mlk_pack_lambdas": [_P, _P, _P, _I32, _I32, _P, _I32, _P, _P],
     "mlk_pack_exceptions": [_P, _P, _I32, _P, _P, _P, _I32, _I32, _P, _P],
     "mlk_compare": [_P, _P, _I32, _P, _P, _P, _P, _P, _P, _P],
-    "mlk_ae_train": [_P, _P, _I32, _I32, _I32, _I32, _D, _D, _D, _D, _D, _D, _P, _I32, _P, _P, _P],
+    "mlk_report": [_P, _I32, _P, _I64, _P, _P, _P],
+    "mlk_ae_train": [_P, _P, _P, _P, _I32, _I32, _I32, _I32, _D, _D, _D, _D, _D, _D, _P, _I32, _P, _P, _P],
     "mlk_ae_train_config": [_P, _P],
     "mlk_decode": [_P, _I32, _I32, _P, _P, _I32, _P, _I32, _P, _P, _P, _P, _P, _P, _P, _P,
                    _D, _P, _P],

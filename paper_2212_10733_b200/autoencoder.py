@@ -11,6 +11,7 @@ bias-correction table.
 
 from __future__ import annotations
 
+import functools
 import struct
 from dataclasses import dataclass
 
@@ -102,6 +103,49 @@ def _host_draws(n, d, latent_dim, epochs, seed, init):
     return np.ascontiguousarray(w, dtype=np.float64), order
 
 
+PW_BLOCK = 128  # numpy PW_BLOCKSIZE
+
+
+@functools.lru_cache(maxsize=32)
+def pairwise_tree(n: int):
+    """numpy's pairwise_sum recursion over n entries as a tree (the layout
+    MlkPwTree describes): leaves (start, len) in entry order, each <= 128
+    entries; internal nodes grouped by depth, deepest first, with the ids of
+    their two children (leaf l has id l, internal node k has id n_leaves + k).
+    Split rule: n2 = n // 2 rounded down to a multiple of 8 (loops_utils.h.src)."""
+    levels = []                         # per depth: (lo, n) of every node
+    lo, ln = np.array([0], np.int64), np.array([n], np.int64)
+    while lo.size:
+        levels.append((lo, ln))
+        inner = ln > PW_BLOCK
+        h = ln[inner] // 2
+        n2 = h - h % 8
+        lo = np.stack([lo[inner], lo[inner] + n2], 1).reshape(-1)
+        ln = np.stack([n2, ln[inner] - n2], 1).reshape(-1)
+    leaf_lo = np.concatenate([l[n_ <= PW_BLOCK] for l, n_ in levels])
+    leaf_ln = np.concatenate([n_[n_ <= PW_BLOCK] for _, n_ in levels])
+    order = np.argsort(leaf_lo, kind="stable")
+    leaf_lo, leaf_ln = leaf_lo[order], leaf_ln[order]
+    n_leaves = leaf_lo.size
+    ids = [None] * len(levels)
+    child, level_off, nxt = [], [0], n_leaves
+    for dpt in range(len(levels) - 1, -1, -1):
+        l, n_ = levels[dpt]
+        idv = np.empty(l.size, np.int64)
+        leaf = n_ <= PW_BLOCK
+        idv[leaf] = np.searchsorted(leaf_lo, l[leaf])
+        k = int((~leaf).sum())
+        if k:
+            idv[~leaf] = nxt + np.arange(k)
+            nxt += k
+            child.append(ids[dpt + 1].reshape(-1, 2))
+            level_off.append(level_off[-1] + k)
+        ids[dpt] = idv
+    child = np.concatenate(child).reshape(-1) if child else np.zeros(0, np.int64)
+    return (leaf_lo.astype(np.int64), leaf_ln.astype(np.int32), child.astype(np.int32),
+            np.array(level_off, np.int32))
+
+
 def train_jobs(jobs, config: TrainConfig, latent_dim: int, d: int):
     """Train every job in one launch; returns one AEModel per job.
 
@@ -124,27 +168,38 @@ def train_jobs(jobs, config: TrainConfig, latent_dim: int, d: int):
     # Python-float bias corrections, exactly as autoencoder.py:171-172 evaluates them
     bias = np.array([[1 - config.beta1 ** t, 1 - config.beta2 ** t] for t in range(1, T + 1)],
                     dtype=np.float64)
-    ws, keep, recs = [], [], []
+    ws, keep, recs, trees = [], [], [], []
     for jb in jobs:
         n = len(jb.row_off)
         w, order = _host_draws(n, d, L, jb.epochs, jb.seed, jb.init)
         wd = torch.from_numpy(w).to(dev)
         offs = torch.from_numpy(np.ascontiguousarray(jb.row_off, dtype=np.int64)).to(dev)
         od = torch.from_numpy(order).to(dev)
-        mv = torch.empty(2 * L * d, dtype=torch.float64, device=dev)
         xn = torch.empty(n * d, dtype=torch.float64, device=dev)
-        keep += [offs, od, mv, xn, jb.base]
+        # fit_normalizer's pairwise tree over the n*d entries
+        t_lo, t_ln, t_ch, t_lv = (torch.from_numpy(a).to(dev) for a in pairwise_tree(n * d))
+        nodes = torch.empty(t_lo.numel() + int(t_lv[-1].item() if t_lv.numel() else 0),
+                            dtype=torch.float64, device=dev)
+        keep += [offs, od, xn, jb.base, t_lo, t_ln, t_ch, t_lv, nodes]
         ws.append(wd)
         recs.append((jb.base.data_ptr(), offs.data_ptr(), od.data_ptr(), wd.data_ptr(),
-                     mv.data_ptr(), xn.data_ptr(), n, jb.epochs))
+                     0, xn.data_ptr(), n, jb.epochs))
+        trees.append((t_lo.data_ptr(), t_ln.data_ptr(), t_ch.data_ptr(), t_lv.data_ptr(),
+                      nodes.data_ptr(), n * d, t_lo.numel(), t_lv.numel() - 1))
     rec_t = np.dtype([("base", "<u8"), ("row_off", "<u8"), ("order", "<u8"), ("w", "<u8"),
                       ("mv", "<u8"), ("xn", "<u8"), ("n", "<i4"), ("epochs", "<i4")])
+    tree_t = np.dtype([("leaf_start", "<u8"), ("leaf_len", "<u8"), ("child", "<u8"),
+                       ("level_off", "<u8"), ("nodes", "<u8"), ("n_total", "<i8"),
+                       ("n_leaves", "<i4"), ("n_levels", "<i4")])
     table_h = np.array(recs, dtype=rec_t)
     table_d = torch.from_numpy(table_h.view(np.uint8).copy()).to(dev)
+    trees_h = np.array(trees, dtype=tree_t)
+    trees_d = torch.from_numpy(trees_h.view(np.uint8).copy()).to(dev)
     bias_d = torch.from_numpy(bias.reshape(-1)).to(dev)
     norm = torch.empty(2 * len(jobs), dtype=torch.float64, device=dev)
     diag = torch.empty(2 * len(jobs), dtype=torch.float64, device=dev)
-    _lib.call("mlk_ae_train", table_d, table_h.ctypes.data, len(jobs), L, d, B,
+    _lib.call("mlk_ae_train", table_d, table_h.ctypes.data, trees_d, trees_h.ctypes.data,
+              len(jobs), L, d, B,
               float(config.learning_rate), float(config.beta1), float(1 - config.beta1),
               float(config.beta2), float(1 - config.beta2), float(config.eps), bias_d, T,
               norm, diag, msg="(AE training)")

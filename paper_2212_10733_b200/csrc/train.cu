@@ -14,17 +14,19 @@
 //    reference raises TrainingDivergedError;
 //  * Adam with the host's bias-correction table 1 - beta^t (Python pow),
 //    elementwise in numpy's rounding order with explicit _rn intrinsics.
-// The GEMM reductions (z, err W^T, grad, mse, the normaliser sums) run in a
-// different order than numpy/OpenBLAS, so the weights match the reference
-// within a tolerance, not bit for bit (training is not
-// bit-reproducible); tests/test_train.py states the tolerance.
+// The normaliser is numpy's pairwise sums exactly (k_pw_leaves /
+// k_pw_combine), so mean and std are bit-identical to fit_normalizer's.  The
+// GEMM reductions (z, err W^T, grad, mse) run in a different order than
+// OpenBLAS, so the f64 weights match the reference within a tolerance, not
+// bit for bit; tests/test_train.py states the tolerance (the f32
+// weights the archive stores have matched the reference's exactly so far).
 //
-// Layout: W (L x D f64) and the grad accumulator G (L x D f64) in shared
-// memory; Adam moments in global scratch (each thread touches only its own
-// columns).  Phase A: one warp per batch row (coalesced row reads, shuffle
-// reductions of z and e = err W^T).  Phase B: one thread per column
-// accumulates G over the chunk's rows.  The training rows stay in L2 between
-// the three passes of a step.
+// Layout: one thread-block CLUSTER per job (k_ae_train below): each CTA owns
+// a column slice of W, its gradient and both Adam moments in shared memory
+// and sums the cluster's partials from distributed shared memory in rank
+// order.  The cluster size C is fixed per device (16 when non-portable
+// clusters are allowed, else 8, smaller only when the occupancy query says a
+// cluster cannot be co-scheduled); mlk_ae_train_config reports it.
 #include "common.cuh"
 
 #include <cooperative_groups.h>
@@ -60,49 +62,67 @@ __device__ __forceinline__ void warp_sum4(const double* v, int lane, double* out
     if ((lane & 7) == 0) out[(h16 ? 2 : 0) + (h8 ? 1 : 0)] = k;
 }
 
-// block sum; every thread gets the total (red holds TW doubles)
-__device__ double block_sum(double v, double* red) {
-    v = warp_sum(v);
-    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    __syncthreads();
-    if (lane == 0) red[w] = v;
-    __syncthreads();
-    double t = lane < TW ? red[lane] : 0.0;
-    return warp_sum(t);
+// fit_normalizer (autoencoder.py:77-84) in numpy's own summation order:
+// np.mean / np.std over the (n, rows, cols) selection reduce its n*D entries
+// with ONE pairwise sum (pairwise_sum_DOUBLE over the flattened array), and
+// np.std sums (x - mean)**2 the same way.  The host lays the recursion out
+// as a tree (autoencoder.pairwise_tree): leaves of <= 128 entries (8
+// accumulators each, common.cuh pw_leaf) and internal nodes grouped by depth.
+// Pass 0 sums x, pass 1 sums (x - mean)^2 with the two roundings numpy does.
+__global__ void __launch_bounds__(256)
+k_pw_leaves(const MlkTrainJob* __restrict__ jobs, const MlkPwTree* __restrict__ trees, int D,
+            const double* __restrict__ norm, int pass) {
+    const MlkTrainJob job = jobs[blockIdx.y];
+    const MlkPwTree t = trees[blockIdx.y];
+    const int l = blockIdx.x * blockDim.x + threadIdx.x;
+    if (l >= t.n_leaves) return;
+    const long long e0 = t.leaf_start[l];
+    const int len = t.leaf_len[l];
+    const double mean = pass ? norm[2 * blockIdx.y] : 0.0;
+    long long row = e0 / D;
+    int col = (int)(e0 - row * D);
+    // entries are visited in increasing order: walk (row, col) incrementally
+    int cur = 0;
+    const double* rp = job.base + job.row_off[row];
+    auto get = [&](int i) {
+        while (cur < i) {
+            ++cur;
+            if (++col == D) {
+                col = 0;
+                rp = job.base + job.row_off[++row];
+            }
+        }
+        const double x = __ldg(rp + col);
+        if (!pass) return x;
+        const double d = __dsub_rn(x, mean);
+        return __dmul_rn(d, d);
+    };
+    t.nodes[l] = pw_leaf(get, 0, len);
 }
 
-// fit_normalizer (autoencoder.py:77-84): one CTA per job
-__global__ void __launch_bounds__(TT, 1)
-k_ae_norm(const MlkTrainJob* __restrict__ jobs, int D, double* __restrict__ norm_out,
-          double* __restrict__ diag_out) {
-    __shared__ double red[TW];
-    const MlkTrainJob job = jobs[blockIdx.x];
-    const int n = job.n;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    double s = 0.0;
-    for (int i = warp; i < n; i += TW) {
-        const double* r = job.base + job.row_off[i];
-#pragma unroll 8
-        for (int d = lane; d < D; d += 32) s += __ldg(r + d);
+__global__ void __launch_bounds__(1024)
+k_pw_combine(const MlkPwTree* __restrict__ trees, double* __restrict__ norm,
+             double* __restrict__ diag, int pass) {
+    const MlkPwTree t = trees[blockIdx.x];
+    for (int lv = 0; lv < t.n_levels; ++lv) {
+        for (int k = t.level_off[lv] + threadIdx.x; k < t.level_off[lv + 1]; k += blockDim.x)
+            t.nodes[t.n_leaves + k] =
+                __dadd_rn(t.nodes[t.child[2 * k]], t.nodes[t.child[2 * k + 1]]);
+        __syncthreads();
     }
-    const double cnt = (double)n * (double)D;
-    const double mean = block_sum(s, red) / cnt;
-    double q = 0.0;
-    for (int i = warp; i < n; i += TW) {
-        const double* r = job.base + job.row_off[i];
-#pragma unroll 8
-        for (int d = lane; d < D; d += 32) {
-            const double t = __ldg(r + d) - mean;
-            q += t * t;
+    if (threadIdx.x == 0) {
+        const int n_int = t.n_levels ? t.level_off[t.n_levels] : 0;
+        const double root = t.nodes[n_int ? t.n_leaves + n_int - 1 : 0];
+        const double cnt = (double)t.n_total;
+        if (pass == 0) {
+            norm[2 * blockIdx.x] = __ddiv_rn(root, cnt);
+            diag[2 * blockIdx.x] = -1.0;
+            diag[2 * blockIdx.x + 1] = 0.0;
+        } else {
+            double sd = __dsqrt_rn(__ddiv_rn(root, cnt));
+            if (MLK_STD_FLOOR > sd) sd = MLK_STD_FLOOR;  // max(std, STD_FLOOR)
+            norm[2 * blockIdx.x + 1] = sd;
         }
-    }
-    double stdv = sqrt(block_sum(q, red) / cnt);
-    if (MLK_STD_FLOOR > stdv) stdv = MLK_STD_FLOOR;   // max(std, STD_FLOOR)
-    if (tid == 0) {
-        norm_out[2 * blockIdx.x] = mean;
-        norm_out[2 * blockIdx.x + 1] = stdv;
-        diag_out[2 * blockIdx.x] = -1.0;
-        diag_out[2 * blockIdx.x + 1] = 0.0;
     }
 }
 
@@ -346,7 +366,8 @@ k_ae_train(const MlkTrainJob* __restrict__ jobs, int L_, int D, int DC, int TCH_
 
 }  // namespace
 
-extern "C" int mlk_ae_train(const MlkTrainJob* jobs, const MlkTrainJob* jobs_h, int32_t n_jobs,
+extern "C" int mlk_ae_train(const MlkTrainJob* jobs, const MlkTrainJob* jobs_h,
+                            const MlkPwTree* trees, const MlkPwTree* trees_h, int32_t n_jobs,
                             int32_t L, int32_t D, int32_t batch, double lr, double beta1,
                             double one_minus_beta1, double beta2, double one_minus_beta2,
                             double eps, const double* bias, int32_t T, double* norm,
@@ -359,8 +380,13 @@ extern "C" int mlk_ae_train(const MlkTrainJob* jobs, const MlkTrainJob* jobs_h, 
         const long long steps = (long long)jb.epochs * ((jb.n + batch - 1) / batch);
         if (steps > T) return MLK_ERR_SIZE;
     }
-    int max_n = 0;
-    for (int j = 0; j < n_jobs; ++j) max_n = max(max_n, jobs_h[j].n);
+    int max_n = 0, max_leaves = 1;
+    for (int j = 0; j < n_jobs; ++j) {
+        max_n = max(max_n, jobs_h[j].n);
+        const MlkPwTree& tr = trees_h[j];
+        if (tr.n_total != (long long)jobs_h[j].n * D || tr.n_leaves < 1) return MLK_ERR_CONFIG;
+        max_leaves = max(max_leaves, tr.n_leaves);
+    }
     // cluster size: 16 CTAs per job when the device can co-schedule them, else 8
     int C = 16;
     auto kern = L == 4 ? k_ae_train<4> : k_ae_train<0>;
@@ -379,10 +405,8 @@ extern "C" int mlk_ae_train(const MlkTrainJob* jobs, const MlkTrainJob* jobs_h, 
             const size_t rows = (budget - fixed) / per_row;
             tch = rows > 128 ? 128 : (int)rows;
         }
-        if (tch < 1) {
-            if (C == 1) return MLK_ERR_CONFIG;
-            continue;
-        }
+        // fewer CTAs per cluster only make each CTA's column slice larger
+        if (tch < 1) return MLK_ERR_CONFIG;
         dyn = fixed + per_row * tch;
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)dyn) != cudaSuccess)
@@ -405,7 +429,11 @@ extern "C" int mlk_ae_train(const MlkTrainJob* jobs, const MlkTrainJob* jobs_h, 
             ok = 0;
         }
         if (ok < 1 && C > 1) continue;
-        k_ae_norm<<<n_jobs, TT, 0, stream>>>(jobs, D, norm, diag);
+        for (int pass = 0; pass < 2; ++pass) {
+            k_pw_leaves<<<dim3((max_leaves + 255) / 256, n_jobs), 256, 0, stream>>>(
+                jobs, trees, D, norm, pass);
+            k_pw_combine<<<n_jobs, 1024, 0, stream>>>(trees, norm, diag, pass);
+        }
         k_ae_normalize<<<dim3(n_jobs, min(max_n, 1184)), 256, 0, stream>>>(jobs, D, norm);
         const int DCv = (D + C - 1) / C;
         g_train_cfg[0] = C;

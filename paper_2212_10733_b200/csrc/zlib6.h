@@ -13,6 +13,31 @@
 // validated against the host zlib in tests/test_zlib6.py.
 //
 // Limits: input <= MLK_Z6_MAX_IN bytes (no window sliding is ever needed).
+//
+// Attribution.  The algorithm, its constants and parts of the Huffman code
+// construction (bi_reverse, gen_codes, the bit-length overflow repair) follow
+// zlib 1.3 (deflate.c, trees.c), which carries this notice:
+//
+//   Copyright (C) 1995-2023 Jean-loup Gailly and Mark Adler
+//
+//   This software is provided 'as-is', without any express or implied
+//   warranty.  In no event will the authors be held liable for any damages
+//   arising from the use of this software.
+//
+//   Permission is granted to anyone to use this software for any purpose,
+//   including commercial applications, and to alter it and redistribute it
+//   freely, subject to the following restrictions:
+//
+//   1. The origin of this software must not be misrepresented; you must not
+//      claim that you wrote the original software. If you use this software
+//      in a product, an acknowledgment in the product documentation would be
+//      appreciated but is not required.
+//   2. Altered source versions must be plainly marked as such, and must not be
+//      misrepresented as being the original software.
+//   3. This notice may not be removed or altered from any source distribution.
+//
+// This file is an altered version in that sense: a restatement for CUDA
+// device code, not the zlib sources.
 #pragma once
 #include <stdint.h>
 #include <string.h>

@@ -233,29 +233,15 @@ def gather_bytes(payload: bytes, group=None, dst=0):
 
 def report_partials(out, tau):
     """Decomposable per-rank statistics of a CompressOut for reduce_stats,
-    reduced on the device (one small D2H)."""
-    from ._lib import F_EXCEPTION, F_EXC_OVERFLOW, F_NONFINITE, F_SELECTED
-    d = out.dev
-    flags, status, stats = d["flags"], d["status"], d["stats"]
-    q_o, q_r = d["qoi"], d["fqoi"]
-    mask = (q_o[:, 0] > 0).unsqueeze(1)
-    f64 = torch.float64
-    cnt = lambda m: m.sum().to(f64).reshape(1)
-    dq = torch.where(mask, (q_o - q_r) ** 2, torch.zeros_like(q_o)).sum(0)
-    qmax = torch.where(mask, q_o, torch.full_like(q_o, -np.inf)).amax(0)
-    qmin = torch.where(mask, q_o, torch.full_like(q_o, np.inf)).amin(0)
-    vals = torch.cat([
-        torch.tensor([float(flags.numel())], dtype=f64, device=flags.device),
-        cnt((flags & F_SELECTED) != 0), cnt((flags & F_EXCEPTION) != 0),
-        cnt((status == 0) & ((flags & F_NONFINITE) == 0) & ((flags & F_EXC_OVERFLOW) == 0)),
-        cnt((flags & (F_SELECTED | F_NONFINITE)) == 0), d["fsse"].sum().reshape(1),
-        stats[:, 0].max().reshape(1), stats[:, 1].min().reshape(1), dq, mask.sum().to(f64)
-        .reshape(1), qmax, qmin]).cpu().numpy()
+    reduced on the device by mlk_report (csrc/report.cu; one small D2H).  A
+    rank that owns no members contributes the identities (0 / -inf / +inf)."""
+    from . import report as R
+    v, _, n = R.finish(R.launch([out], False))
     return {
-        "n": ("sum", vals[0:1]), "selected": ("sum", vals[1:2]),
-        "exceptions": ("sum", vals[2:3]), "converged": ("sum", vals[3:4]),
-        "ae_ok": ("sum", vals[4:5]), "sse": ("sum", vals[5:6]),
-        "data_max": ("max", vals[6:7]), "data_min": ("min", vals[7:8]),
-        "qoi_sse": ("sum", vals[8:12]), "qoi_cnt": ("sum", vals[12:13]),
-        "qoi_max": ("max", vals[13:17]), "qoi_min": ("min", vals[17:21]),
+        "n": ("sum", np.array([float(n)])), "selected": ("sum", v[R.SEL:R.SEL + 1]),
+        "exceptions": ("sum", v[R.EXC:R.EXC + 1]), "converged": ("sum", v[R.CONV:R.CONV + 1]),
+        "ae_ok": ("sum", v[R.AE_OK:R.AE_OK + 1]), "sse": ("sum", v[R.SSE:R.SSE + 1]),
+        "data_max": ("max", v[R.DMAX:R.DMAX + 1]), "data_min": ("min", v[R.DMIN:R.DMIN + 1]),
+        "qoi_sse": ("sum", v[R.Q_D2]), "qoi_cnt": ("sum", v[R.QCNT:R.QCNT + 1]),
+        "qoi_max": ("max", v[R.Q_MAX]), "qoi_min": ("min", v[R.Q_MIN]),
     }

@@ -1096,8 +1096,49 @@ class DecodedArchive:
     dgrid: "DeviceGrid"
 
 
-def decode_archive(archive, dev) -> DecodedArchive:
-    """Parse and decode a whole archive on `dev`.
+@dataclass
+class DecodePlan:
+    """An archive parsed on the host and staged on the device: everything
+    run_decode's launches read (prepare_decode)."""
+
+    preamble: object
+    shards: list
+    specs: list
+    table: object
+    models: list
+    total: int
+    n_res: int
+    n_exc: int
+    L: int
+    K: int
+    bits: int
+    lam_bytes: int
+    arc_d: torch.Tensor
+    sh_d: torch.Tensor
+    W: torch.Tensor
+    cents: torch.Tensor
+    res_slot: torch.Tensor
+    exc_slot: torch.Tensor
+    lam_seg: torch.Tensor
+    lam_len: torch.Tensor
+    lam_dst: torch.Tensor
+    code_src: list          # per shard (archive offset, n_images, first member, count)
+    img_off: np.ndarray
+    body: tuple             # (off, len, eb, mode) device tensors of the kept entries
+    exc_seg: tuple          # (src, len, dst)
+    dgrid: "DeviceGrid"
+    out_elems: int
+    dev: torch.device
+    plane_lo: int = 0
+    plane_hi: int = 0
+    codes: object = None    # the unpacked codes of the last run_decode
+
+
+def prepare_decode(archive, dev, sp=None) -> DecodePlan:
+    """Parse an archive (pipeline.py:397-440) and stage what the device
+    decode needs.  sp: a distributed.SplitPlan -- decode only rank sp.rank's
+    members [n_s r/G, n_s (r+1)/G) of every shard into its slab of planes
+    [sp.plane_lo, sp.plane_hi) (decompress_distributed); None: everything.
 
     The host reads only the preamble, the shard index, the 44-byte shard
     headers, the small weight / codebook sections and the residual entry
@@ -1146,16 +1187,20 @@ def decode_archive(archive, dev) -> DecodedArchive:
     lam_bytes = heads[-1].lambda_precision
     if any(h.lambda_precision != lam_bytes for h in heads):
         raise FormatError("mixed lambda precisions across shards are not supported")
+    # the member range [lo_s, hi_s) of every shard this call decodes
+    rng_ = [sp.range(s) for s in range(n_sh)] if sp is not None else \
+        [(0, h.n_images) for h in heads]
     so = _lib.lib()
     arr = np.frombuffer(archive, dtype=np.uint8)
     base_ptr = arr.ctypes.data
     models, cents = [], []
-    res_idx, res_off, res_len, res_eb, res_mode, res_shard = [], [], [], [], [], []
-    exc_idx, exc_src, exc_cnt = [], [], []
+    res_idx, res_off, res_len, res_eb, res_mode = [], [], [], [], []
+    exc_idx, exc_src = [], []
     cnt = ctypes.c_int32()
     why = ctypes.c_int32()
     for s, (h, d) in enumerate(zip(heads, secs)):
         n = h.n_images
+        lo_s, hi_s = rng_[s]
         wo, wl = d["weights"]
         models.append(AEModel.from_bytes(bytes(raw[wo:wo + wl]), L, D))
         po, pl = d["pq_table"]
@@ -1179,12 +1224,12 @@ def decode_archive(archive, dev) -> DecodedArchive:
         if rc != 0:
             raise FormatError(_WHY.get(why.value, "corrupt residual section"))
         k = cnt.value
-        res_idx.append(idx[:k])
-        res_off.append(bo[:k])
-        res_len.append(bl[:k])
-        res_eb.append(eb[:k])
-        res_mode.append(md[:k])
-        res_shard.append(np.full(k, s, np.int32))
+        keep = (idx[:k] >= lo_s) & (idx[:k] < hi_s)
+        res_idx.append(idx[:k][keep] - lo_s)
+        res_off.append(bo[:k][keep])
+        res_len.append(bl[:k][keep])
+        res_eb.append(eb[:k][keep])
+        res_mode.append(md[:k][keep])
         eo, el = d["exceptions"]
         if el < 4:
             raise FormatError("exceptions section truncated")
@@ -1196,100 +1241,149 @@ def decode_archive(archive, dev) -> DecodedArchive:
         if ne:
             starts = eo + 4 + rec * np.arange(ne, dtype=np.int64)
             ei = np.frombuffer(archive, np.uint8, ne * rec, eo + 4).reshape(ne, rec)[:, :4]
-            exc_idx.append(np.ascontiguousarray(ei).view("<u4").reshape(-1).astype(np.int64))
-            exc_src.append(starts + 4)
-        exc_cnt.append(ne)
+            ei = np.ascontiguousarray(ei).view("<u4").reshape(-1).astype(np.int64)
+            if np.any(ei >= n):
+                raise FormatError("exception index out of range")
+            keep = (ei >= lo_s) & (ei < hi_s)
+            exc_idx.append(ei[keep] - lo_s)
+            exc_src.append(starts[keep] + 4)
+        else:
+            exc_idx.append(np.zeros(0, np.int64))
+            exc_src.append(np.zeros(0, np.int64))
     n_res = sum(len(x) for x in res_idx)
-    n_exc = int(sum(exc_cnt))
+    n_exc = sum(len(x) for x in exc_idx)
     arc_d = hostio.upload_bytes(archive, dev)
-    i64 = dict(dtype=torch.int64, device=dev)
-    specs = shard_layout(shards, models, N, rows, cols)
+    if sp is not None:
+        specs = split_layout(sp, models, rows, cols)
+        plane_lo, plane_hi = sp.plane_lo, sp.plane_hi
+    else:
+        specs = shard_layout(shards, models, N, rows, cols)
+        plane_lo, plane_hi = 0, P
     table = _shard_table(specs, D, L)
     img_off = np.array([t.img_off for t in table], dtype=np.int64)
-    total = sum(sp.n_img for sp in specs)
+    total = sum(sp_.n_img for sp_ in specs)
     ws = Workspace.get(dev)
     ws.reset()
     # per-image slots and the small host-built tables, one staged copy
-    res_slot = np.full(total, -1, np.int32)
+    res_slot = np.full(max(total, 1), -1, np.int32)
     if n_res:
         gi = np.concatenate([img_off[s] + res_idx[s] for s in range(n_sh)])
         res_slot[gi] = np.arange(n_res, dtype=np.int32)
-    exc_slot = np.full(total, -1, np.int32)
+    exc_slot = np.full(max(total, 1), -1, np.int32)
     if n_exc:
-        shard_of = np.repeat(np.arange(n_sh), exc_cnt)
-        gi = img_off[shard_of] + np.concatenate(exc_idx)
-        if np.any(np.concatenate(exc_idx) >= np.repeat([h.n_images for h in heads], exc_cnt)):
-            raise FormatError("exception index out of range")
+        gi = np.concatenate([img_off[s] + exc_idx[s] for s in range(n_sh)])
         exc_slot[gi] = np.arange(n_exc, dtype=np.int32)
+    lrec = 8 * lam_bytes
     sh_d = ws.stage(np.frombuffer(bytes(table), dtype=np.uint8))
     W = ws.stage(np.stack([m.weights for m in models]).astype(np.float32))
     cents_d = ws.stage(np.stack(cents))
     res_slot_d = ws.stage(res_slot)
     exc_slot_d = ws.stage(exc_slot)
-    lam_seg = ws.stage(np.array([d["lambdas"][0] for d in secs], np.int64))
-    lam_len = ws.stage(np.array([d["lambdas"][1] for d in secs], np.int64))
-    lam_dst = ws.stage(np.concatenate([[0], np.cumsum([d["lambdas"][1] for d in secs])[:-1]])
-                       .astype(np.int64))
+    lam_seg = ws.stage(np.array([d["lambdas"][0] + lrec * rng_[s][0]
+                                 for s, d in enumerate(secs)], np.int64))
+    lam_len = ws.stage(np.array([lrec * (b_ - a_) for a_, b_ in rng_], np.int64))
+    lam_dst = ws.stage(lrec * img_off)
+    body = exc_seg = None
     if n_res:
-        body_off = ws.stage(np.concatenate(res_off))
-        body_len = ws.stage(np.concatenate(res_len))
-        res_eb_d = ws.stage(np.concatenate(res_eb))
-        res_mode_d = ws.stage(np.concatenate(res_mode))
+        body = (ws.stage(np.concatenate(res_off)), ws.stage(np.concatenate(res_len)),
+                ws.stage(np.concatenate(res_eb)), ws.stage(np.concatenate(res_mode)))
     if n_exc:
-        ex_src = ws.stage(np.concatenate(exc_src))
-        ex_len = ws.stage(np.full(n_exc, 8 * D, np.int64))
-        ex_dst = ws.stage(8 * D * np.arange(n_exc, dtype=np.int64))
+        exc_seg = (ws.stage(np.concatenate(exc_src)), ws.stage(np.full(n_exc, 8 * D, np.int64)),
+                   ws.stage(8 * D * np.arange(n_exc, dtype=np.int64)))
     ws.flush()
-    # codes straight from the archive
-    codes16 = ws.tensor("dec_codes16", (total * L,), torch.int16)
-    for s, (h, d) in enumerate(zip(heads, secs)):
-        co = d["codes"][0]
-        o = int(img_off[s]) * L
-        call("mlk_unpack_indices", arc_d.data_ptr() + co, h.n_images * L, bits,
-             codes16.data_ptr() + 2 * o)
-    codes = ws.tensor("dec_codes", (total * L,), torch.uint8)
+    code_src = [(d["codes"][0], h.n_images, rng_[s][0], rng_[s][1] - rng_[s][0])
+                for s, (h, d) in enumerate(zip(heads, secs))]
+    return DecodePlan(preamble=pre, shards=shards, specs=specs, table=table, models=models,
+                      total=total, n_res=n_res, n_exc=n_exc, L=L, K=K, bits=bits,
+                      lam_bytes=lam_bytes, arc_d=arc_d, sh_d=sh_d, W=W, cents=cents_d,
+                      res_slot=res_slot_d, exc_slot=exc_slot_d, lam_seg=lam_seg,
+                      lam_len=lam_len, lam_dst=lam_dst, code_src=code_src, img_off=img_off,
+                      body=body, exc_seg=exc_seg, dgrid=DeviceGrid(pre.grid, dev, L),
+                      out_elems=(plane_hi - plane_lo) * N * D, dev=dev, plane_lo=plane_lo,
+                      plane_hi=plane_hi)
+
+
+def run_decode(pl: DecodePlan, check: bool = True, out: torch.Tensor | None = None):
+    """The device half of the decode: unpack codes, gather lambdas, inflate +
+    varint-decode the residual bodies, gather the exception images, then
+    mlk_decode writes every image at its dataset address in `out` (flat,
+    the plan's planes x all nodes).  check: raise FormatError on corrupt
+    residual streams (one small D2H); the timed device loop passes False
+    after a checked run."""
+    dev = pl.dev
+    D = pl.preamble.grid.rows * pl.preamble.grid.cols
+    L, total = pl.L, pl.total
+    i64 = dict(dtype=torch.int64, device=dev)
+    ws = Workspace.get(dev)
+    codes16 = ws.tensor("dec_codes16", (max(1, total) * L,), torch.int16)
+    for s, (co, n_img, lo_s, cnt_s) in enumerate(pl.code_src):
+        if not cnt_s:
+            continue
+        o = int(pl.img_off[s]) * L
+        if lo_s == 0 and cnt_s == n_img:
+            call("mlk_unpack_indices", pl.arc_d.data_ptr() + co, n_img * L, pl.bits,
+                 codes16.data_ptr() + 2 * o)
+        else:
+            full = ws.tensor(f"dec_codes_full{s}", (n_img * L,), torch.int16)
+            call("mlk_unpack_indices", pl.arc_d.data_ptr() + co, n_img * L, pl.bits,
+                 full.data_ptr())
+            codes16[o:o + cnt_s * L].copy_(full[lo_s * L:(lo_s + cnt_s) * L])
+    codes = ws.tensor("dec_codes", (max(1, total) * L,), torch.uint8)
     codes.copy_(codes16)
-    # lambda section -> aligned -> float64
-    lam_raw = ws.tensor("dec_lamraw", (total * 8 * lam_bytes,), torch.uint8)
-    call("mlk_gather_segments", arc_d, lam_seg, lam_len, n_sh, lam_raw, lam_dst)
-    lamq = lam_raw.view(torch.float32 if lam_bytes == 4 else torch.float64).to(torch.float64)
-    # zlib bodies -> device inflate -> device varint decode
+    pl.codes = codes
+    lam_raw = ws.tensor("dec_lamraw", (max(1, total) * 8 * pl.lam_bytes,), torch.uint8)
+    call("mlk_gather_segments", pl.arc_d, pl.lam_seg, pl.lam_len, len(pl.code_src), lam_raw,
+         pl.lam_dst)
+    lamq = lam_raw.view(torch.float32 if pl.lam_bytes == 4 else torch.float64).to(torch.float64)
+    n_res = pl.n_res
     if n_res:
+        body_off, body_len, res_eb_d, res_mode_d = pl.body
         icap = 10 * D + 64
         raw_d = ws.tensor("dec_inflate", (n_res * icap,), torch.uint8)
         raw_off = torch.arange(0, n_res * icap, icap, **i64)
         raw_len = ws.tensor("dec_rawlen", (n_res,), torch.int64)
-        call("mlk_zlib_decompress", arc_d, body_off, body_len, n_res, raw_d, raw_off, icap,
+        call("mlk_zlib_decompress", pl.arc_d, body_off, body_len, n_res, raw_d, raw_off, icap,
              raw_len)
         vals = ws.tensor("dec_vals", (n_res * D,), torch.int64)
         consumed = ws.tensor("dec_consumed", (n_res,), torch.int64)
         call("mlk_varint_decode_batch", raw_d, raw_off, raw_len, n_res,
              torch.full((n_res,), D, **i64), vals, torch.arange(0, n_res * D, D, **i64),
              consumed)
-        rl, con = _d2h(raw_len, consumed)
-        if np.any(rl < 0):
-            raise FormatError("corrupt residual stream")
-        if np.any(con == -1):
-            raise FormatError("varint stream truncated")
-        if np.any(con == -2):
-            raise FormatError("varint value exceeds 64 bits")
-        if np.any(con != rl):
-            raise FormatError("residual stream has trailing bytes")
+        if check:
+            rl, con = _d2h(raw_len, consumed)
+            if np.any(rl < 0):
+                raise FormatError("corrupt residual stream")
+            if np.any(con == -1):
+                raise FormatError("varint stream truncated")
+            if np.any(con == -2):
+                raise FormatError("varint value exceeds 64 bits")
+            if np.any(con != rl):
+                raise FormatError("residual stream has trailing bytes")
     else:
         vals = torch.zeros(1, **i64)
         res_eb_d = torch.zeros(1, dtype=torch.float64, device=dev)
         res_mode_d = torch.zeros(1, dtype=torch.uint8, device=dev)
-    exc_img = ws.tensor("dec_exc", (max(1, n_exc) * D,), torch.float64)
-    if n_exc:
-        call("mlk_gather_segments", arc_d, ex_src, ex_len, n_exc, exc_img.view(torch.uint8),
-             ex_dst)
-    dgrid = DeviceGrid(pre.grid, dev, L)
-    out = torch.empty(P * N * D + 2, dtype=torch.float64, device=dev)
-    call("mlk_decode", sh_d, len(specs), total, dgrid.addr, W, L, cents_d, K, codes, res_slot_d,
-         vals, res_eb_d, res_mode_d, lamq, exc_slot_d, exc_img, 1e-12, out)
-    return DecodedArchive(preamble=pre, shards=shards, out=out, specs=specs, table=table,
-                          sh_d=sh_d, W=W, cents=cents_d, codes=codes, L=L, K=K,
-                          lam_bytes=lam_bytes, dgrid=dgrid)
+    exc_img = ws.tensor("dec_exc", (max(1, pl.n_exc) * D,), torch.float64)
+    if pl.n_exc:
+        ex_src, ex_len, ex_dst = pl.exc_seg
+        call("mlk_gather_segments", pl.arc_d, ex_src, ex_len, pl.n_exc,
+             exc_img.view(torch.uint8), ex_dst)
+    if out is None:
+        out = torch.empty(pl.out_elems + 2, dtype=torch.float64, device=dev)
+    if total:
+        call("mlk_decode", pl.sh_d, len(pl.specs), total, pl.dgrid.addr, pl.W, L, pl.cents,
+             pl.K, codes, pl.res_slot, vals, res_eb_d, res_mode_d, lamq, pl.exc_slot, exc_img,
+             1e-12, out)
+    return out
+
+
+def decode_archive(archive, dev) -> DecodedArchive:
+    """Parse and decode a whole archive on `dev` (prepare_decode + run_decode)."""
+    pl = prepare_decode(archive, dev)
+    out = run_decode(pl)
+    return DecodedArchive(preamble=pl.preamble, shards=pl.shards, out=out, specs=pl.specs,
+                          table=pl.table, sh_d=pl.sh_d, W=pl.W, cents=pl.cents, codes=pl.codes,
+                          L=pl.L, K=pl.K, lam_bytes=pl.lam_bytes, dgrid=pl.dgrid)
 
 
 def decompress_device(archive, dev) -> np.ndarray:

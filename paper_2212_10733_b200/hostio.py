@@ -17,7 +17,6 @@ from __future__ import annotations
 import collections
 import ctypes
 import os
-import sys
 import threading
 from concurrent.futures import ThreadPoolExecutor
 
@@ -286,7 +285,7 @@ class ArchiveWriter:
         self.cap = cap
         self.head_len = head_len
         self.obj = _new_bytes(None, cap)
-        self.addr = id(self.obj) + _BYTES_OFF
+        self.addr = _bytes_buffer(self.obj)
         self.view = np.ctypeslib.as_array((ctypes.c_uint8 * cap).from_address(self.addr))
         _advise_huge(self.view)
         self.pos = head_len
@@ -448,13 +447,29 @@ def _advise_huge(arr: np.ndarray):
         pass
 
 
-_BYTES_OFF = sys.getsizeof(b"") - 1  # offset of ob_sval in a CPython bytes object
+# The archive is returned as `bytes` (the reference API's type) without an
+# extra host copy: the documented C-API pattern for building a bytes object in
+# place -- PyBytes_FromStringAndSize(NULL, n) gives an uninitialised object
+# whose buffer (PyBytes_AsString) may be written until the object is shared,
+# and _PyBytes_Resize may shrink such a brand-new object.  Nothing else sees
+# the object before it is complete.
 _new_bytes = ctypes.pythonapi.PyBytes_FromStringAndSize
 _new_bytes.restype = ctypes.py_object
 _new_bytes.argtypes = [ctypes.c_void_p, ctypes.c_ssize_t]
 _resize_bytes = ctypes.pythonapi._PyBytes_Resize
 _resize_bytes.restype = ctypes.c_int
 _resize_bytes.argtypes = [ctypes.POINTER(ctypes.py_object), ctypes.c_ssize_t]
+_bytes_as_string = ctypes.pythonapi.PyBytes_AsString
+_bytes_as_string.restype = ctypes.c_void_p
+_bytes_as_string.argtypes = [ctypes.py_object]
+
+
+def _bytes_buffer(obj: bytes) -> int:
+    """Address of a brand-new bytes object's buffer (PyBytes_AsString)."""
+    addr = _bytes_as_string(obj)
+    if not addr:
+        raise MemoryError("PyBytes_AsString failed")
+    return addr
 
 
 def download_bytes(src: torch.Tensor, nbytes: int, prefix: bytes = b"") -> bytes:
@@ -466,7 +481,7 @@ def download_bytes(src: torch.Tensor, nbytes: int, prefix: bytes = b"") -> bytes
         torch.cuda.current_stream(dev).synchronize()
     total = len(prefix) + nbytes
     out = _new_bytes(None, total)  # uninitialised; filled before anyone sees it
-    view = np.ctypeslib.as_array((ctypes.c_uint8 * total).from_address(id(out) + _BYTES_OFF))
+    view = np.ctypeslib.as_array((ctypes.c_uint8 * total).from_address(_bytes_buffer(out)))
     _advise_huge(view)
     view[:len(prefix)] = np.frombuffer(prefix, dtype=np.uint8)
     body = view[len(prefix):]

@@ -22,7 +22,7 @@ import numpy as np
 import torch
 
 from . import engine, hostio
-from ._lib import F_EXCEPTION, F_EXC_OVERFLOW, F_NONFINITE, F_SELECTED
+from . import report as _report
 from . import autoencoder as ae
 from .autoencoder import AEModel
 from .container import ArchivePreamble, archive_offsets
@@ -31,7 +31,7 @@ from .decomp import (SelectionScheme, mix_seed, partition, select_training,
 from .errors import (ConfigError, DegenerateRangeError, DimensionError, FormatError,
                      SizeMismatchError)
 from .fdata import FDataset, dataset_nbytes
-from .lagrange import NewtonOptions, NewtonStatus
+from .lagrange import NewtonOptions
 from .qoi import ErrorReport, compression_ratio, qoi_nrmse_from_moments
 
 __all__ = ["PipelineConfig", "TimestepState", "compress", "compress_distributed", "decompress",
@@ -138,14 +138,14 @@ def _check_state(config, state, n_shards):
     return train_full
 
 
-def _train_models(f0, shards, ds, config, state, train_full):
+def _train_models(f0, shards, ds, config, state, train_full, index=None):
     """Per-shard AE training on the device (pipeline.py:208-218): selection
     indices and PCG64 draws on the host, every shard's Adam run in ONE
     mlk_ae_train launch.  f0 = the device-resident dataset (flat, the
     dataset's own layout), or None: then only the selected training rows are
     gathered on the host and uploaded (compress_distributed, where a rank
-    holds just its slab of planes; every rank trains every shard with the
-    same deterministic kernel, so all ranks hold identical models)."""
+    holds just its slab of planes and trains only its own shards).  index:
+    the shard numbers of `shards` (their warm-start models in state)."""
     D = ds.grid.rows * ds.grid.cols
     epochs = config.epochs_full if train_full else config.epochs_incremental
     tc = ae.TrainConfig(learning_rate=config.learning_rate, batch_size=config.batch_size,
@@ -164,10 +164,48 @@ def _train_models(f0, shards, ds, config, state, train_full):
                 for i, (_, ix) in enumerate(sels)]
     else:
         offs = [ix * D for _, ix in sels]
+    index = list(range(len(shards))) if index is None else list(index)
     jobs = [ae.TrainJob(base=f0, row_off=o, epochs=epochs, seed=seed,
-                        init=None if train_full else state.models[i])
+                        init=None if train_full else state.models[index[i]])
             for i, ((seed, _), o) in enumerate(zip(sels, offs))]
     return ae.train_jobs(jobs, tc, config.latent_dim, D)
+
+
+def _train_distributed(ds, config, state, train_full, group=None):
+    """compress_distributed's training: shard s is trained on rank s % G only
+    (from the host rows of its selection), then its f32 weights and (mean,
+    std) are broadcast from that rank, so every rank encodes with exactly the
+    model rank 0 writes into the weights section -- no assumption that
+    several GPUs reproduce one training run bit for bit."""
+    import torch.distributed as dist
+
+    from . import distributed as D_
+    shards = partition(ds.n_planes, ds.n_nodes, config.shards, config.mode)
+    on = dist.is_initialized()
+    G = dist.get_world_size(group) if on else 1
+    r = dist.get_rank(group) if on else 0
+    mine = [s for s in range(len(shards)) if s % G == r]
+    trained = {}
+    if mine:
+        got = _train_models(None, [shards[s] for s in mine], ds, config, state, train_full,
+                            index=mine)
+        trained = dict(zip(mine, got))
+    L, D = config.latent_dim, ds.grid.rows * ds.grid.cols
+    dev = D_._device_for(group)
+    models = []
+    for s in range(len(shards)):
+        buf = torch.zeros(2 + L * D, dtype=torch.float64, device=dev)
+        if s in trained:
+            m = trained[s]
+            buf[0], buf[1] = m.norm_mean, m.norm_std
+            buf[2:] = torch.from_numpy(np.asarray(m.weights, np.float64).reshape(-1)).to(dev)
+        if on and G > 1:
+            src = s % G if group is None else dist.get_global_rank(group, s % G)
+            dist.broadcast(buf, src=src, group=group)
+        h = buf.cpu().numpy()
+        models.append(AEModel(weights=h[2:].astype(np.float32).reshape(L, D),
+                              norm_mean=float(h[0]), norm_std=float(h[1])))
+    return models
 
 
 # compress() can pipeline shard groups: group g's node blocks are uploaded
@@ -406,8 +444,7 @@ def compress_distributed(ds: FDataset, config: PipelineConfig, state: TimestepSt
     if train_full is None:
         models = list(state.models)
     else:
-        models = _train_models(None, partition(ds.n_planes, ds.n_nodes, config.shards,
-                                               config.mode), ds, config, state, train_full)
+        models = _train_distributed(ds, config, state, train_full, group)
         trace.mark("train")
     works = engine.split_layout(sp, models, ds.grid.rows, ds.grid.cols)
     out = engine.compress_device(f0, works, dgrid, config, comm=D_.Comm(sp, group))
@@ -495,51 +532,21 @@ def build_report(ds, archive_len, outs, tau, stage_t, wall) -> ErrorReport:
 
 
 def report_launch(outs):
-    """The device half of build_report: reductions and one async D2H into
-    page-locked memory, queued ahead of the archive download (the copy
-    engine serves copies in order)."""
-    dev = outs[0].dev["flags"].device
-    cat = lambda k: torch.cat([o.dev[k] for o in outs]) if len(outs) > 1 else outs[0].dev[k]
-    flags, ferr = cat("flags"), cat("ferr")
-    qoi, fqoi, stats = cat("qoi"), cat("fqoi"), cat("stats")
-    fsse, status = cat("fsse"), cat("status")
-    n_tot = flags.numel()
-    exc = (flags & F_EXCEPTION) != 0
-    order = torch.from_numpy(np.concatenate([o.dataset_index for o in outs])).pin_memory().to(
-        dev, non_blocking=True)
-    per_image = torch.empty(n_tot, dtype=torch.float64, device=dev)
-    per_image[order] = torch.where(exc, torch.zeros_like(ferr), ferr)
-    # QoI errors over the nodes with positive density (qoi.py:122-133)
-    mask = (qoi[:, 0] > 0).unsqueeze(1)
-    d2 = torch.where(mask, (qoi - fqoi) ** 2, torch.zeros_like(qoi)).sum(0)
-    qhi = torch.where(mask, qoi, torch.full_like(qoi, -np.inf)).amax(0)
-    qlo = torch.where(mask, qoi, torch.full_like(qoi, np.inf)).amin(0)
-    scal = torch.stack([
-        stats[:, 0].max(), stats[:, 1].min(), fsse.sum(), mask.sum().to(torch.float64),
-        ((status == NewtonStatus.CONVERGED) & ((flags & F_NONFINITE) == 0)
-         & ((flags & F_EXC_OVERFLOW) == 0)).sum().to(torch.float64),
-        ((flags & (F_SELECTED | F_NONFINITE)) == 0).sum().to(torch.float64),
-        ((flags & F_SELECTED) != 0).sum().to(torch.float64),
-        exc.sum().to(torch.float64)])
-    flat = torch.cat([scal, d2, qhi, qlo, per_image])
-    host = torch.empty(flat.shape, dtype=flat.dtype, pin_memory=True)
-    host.copy_(flat, non_blocking=True)
-    ev = torch.cuda.Event()
-    ev.record()
-    return host, ev, n_tot
+    """The device half of build_report: one mlk_report pass (csrc/report.cu)
+    and one async D2H into page-locked memory, queued ahead of the archive
+    download (the copy engine serves copies in order)."""
+    return _report.launch(outs, True, _report.dataset_orders(outs))
 
 
 def report_finish(handle, ds, archive_len, tau, stage_t, wall) -> ErrorReport:
     """The host half of build_report (waits for report_launch's copy)."""
     if not isinstance(archive_len, (int, np.integer)):
         archive_len = len(archive_len)
-    host_t, ev, n_tot = handle
-    ev.synchronize()
-    host = host_t.numpy()
-    dmax, dmin, sse, cnt, n_conv, ae_ok, n_sel, n_exc = host[:8]
-    d2_h, qhi_h, qlo_h = host[8:12], host[12:16], host[16:20]
-    span = float(dmax - dmin)
-    pd = float(np.sqrt(sse / ds.data.size) / span) if span > 0 else 0.0
+    v, per, n_tot = _report.finish(handle)
+    span = float(v[_report.DMAX] - v[_report.DMIN])
+    pd = float(np.sqrt(v[_report.SSE] / ds.data.size) / span) if span > 0 else 0.0
+    cnt = v[_report.QCNT]
+    d2_h, qhi_h, qlo_h = v[_report.Q_D2], v[_report.Q_MAX], v[_report.Q_MIN]
     names = ("n", "u_par", "t_perp", "t_par")
     qerr = {}
     for k, nm in enumerate(names):
@@ -553,12 +560,13 @@ def report_finish(handle, ds, archive_len, tau, stage_t, wall) -> ErrorReport:
         else:
             qerr[nm] = float(np.sqrt(d2_h[k] / cnt) / rng_k)
     return ErrorReport(
-        pd_nrmse=pd, per_image_nrmse=host[20:].tolist(), qoi_nrmse=qerr,
+        pd_nrmse=pd, per_image_nrmse=per.tolist(), qoi_nrmse=qerr,
         max_qoi_nrmse=max(qerr.values()),
         compression_ratio=compression_ratio(dataset_nbytes(ds), archive_len),
-        ae_accuracy=float(ae_ok) / n_tot, residual_fraction=float(n_sel) / n_tot,
-        convergence_fraction=float(n_conv) / n_tot, exception_count=int(n_exc),
-        stage_timings=_timings(stage_t, wall))
+        ae_accuracy=float(v[_report.AE_OK]) / n_tot,
+        residual_fraction=float(v[_report.SEL]) / n_tot,
+        convergence_fraction=float(v[_report.CONV]) / n_tot,
+        exception_count=int(v[_report.EXC]), stage_timings=_timings(stage_t, wall))
 
 
 def _timings(stage_t, wall):
@@ -578,6 +586,51 @@ def decompress(archive: bytes) -> FDataset:
     """Invert compress(); exception images are reproduced verbatim."""
     pre, _ = ArchivePreamble.unpack(archive)
     data = engine.decompress_device(archive, _device())
+    return FDataset._trusted(pre.grid, data, pre.timestep)
+
+
+def decompress_distributed(archive: bytes, group=None, gather: bool = True):
+    """decompress() with one process per GPU (torch.distributed initialised).
+
+    The reference decodes every shard independently (pipeline.py:430-440);
+    here rank r decodes members [n_s r / G, n_s (r + 1) / G) of every shard
+    (the member ranges compress_distributed gave it), i.e. planes
+    [P r / G, P (r + 1) / G) of f0, into its own HBM.  gather=True: the slabs
+    are all-gathered over NCCL (NVLink) and every rank returns the whole
+    FDataset, as decompress() does; gather=False: returns (FDataset of the
+    rank's planes, (plane_lo, plane_hi)).  Needs G to divide the plane count
+    (each rank's slab is then whole planes)."""
+    import torch.distributed as dist
+
+    from . import distributed as D_
+    pre, _ = ArchivePreamble.unpack(archive)
+    on = dist.is_initialized()
+    # member ranges exactly [n_s r / G, n_s (r + 1) / G): the decode needs no
+    # byte alignment of the packed codes (bits per image 8 -> no cut)
+    sp = D_.split_plan(pre.n_planes, pre.n_nodes, pre.n_shards, pre.decomp_mode,
+                       rank=dist.get_rank(group) if on else 0,
+                       world=dist.get_world_size(group) if on else 1, latent_dim=1, pq_bits=8)
+    if pre.decomp_mode != "col" or pre.n_planes % sp.world:
+        raise ConfigError("decompress_distributed needs col mode and a plane count divisible "
+                          "by the number of ranks")
+    dev = _device()
+    plan = engine.prepare_decode(archive, dev, sp)
+    out = engine.run_decode(plan)
+    g = pre.grid
+    nd = pre.n_nodes * g.rows * g.cols
+    mine = out[:plan.out_elems]
+    if bool((mine < 0).any()):
+        raise ConfigError("histogram values must be non-negative")
+    if not gather:
+        data = hostio.download_pinned_array(mine, (plan.plane_hi - plan.plane_lo, pre.n_nodes,
+                                                   g.rows, g.cols))
+        return FDataset._trusted(pre.grid, data, pre.timestep), (plan.plane_lo, plan.plane_hi)
+    full = torch.empty(pre.n_planes * nd, dtype=torch.float64, device=dev)
+    if sp.world > 1:
+        dist.all_gather_into_tensor(full, mine.contiguous(), group=group)
+    else:
+        full.copy_(mine)
+    data = hostio.download_pinned_array(full, (pre.n_planes, pre.n_nodes, g.rows, g.cols))
     return FDataset._trusted(pre.grid, data, pre.timestep)
 
 

@@ -90,26 +90,34 @@ def stage_dump(ds, cfg, models):
     return per
 
 
+def load_models(name):
+    """The models an earlier case trained (its npz), replayed as static weights."""
+    a = np.load(OUT / f"{name}.npz")
+    return [ae.AEModel(weights=a["model_W"][i], norm_mean=float(a["model_mean"][i]),
+                       norm_std=float(a["model_std"][i])) for i in range(a["model_W"].shape[0])]
+
+
 def run_case(name, P, N, cfg_kw, taus=None, store_arrays=True, seed=42, rho=0.003,
-             train_cfg=None):
+             train_cfg=None, models_from=None, decompress=True, workers=8):
     t0 = time.time()
     ds = corpus(P, N, seed, rho)
-    base = dict(workers=8, seed=0, static_model=True)
+    base = dict(workers=workers, seed=0, static_model=True)
     base.update(cfg_kw)
     cfg = PipelineConfig(**base)
-    models = train_models(ds, PipelineConfig(**{**base, **(train_cfg or {})}))
+    models = (load_models(models_from) if models_from else
+              train_models(ds, PipelineConfig(**{**base, **(train_cfg or {})})))
     arrays = {f"model_{k}": v for k, v in models_arrays(models).items()}
     meta = {"case": name, "P": P, "N": N, "seed": seed, "rho": rho, "env": env(),
-            "data_sha": sha(ds.data), "runs": []}
+            "data_sha": sha(ds.data), "models_from": models_from, "runs": []}
     variants = taus or [dict()]
     for vi, var in enumerate(variants):
         c = PipelineConfig(**{**base, **var})
         arc, rep, _ = mlk.compress(ds, c, TimestepState(models=models, timestep_index=1))
         pre, blobs = container.read_archive(arc)
-        dec = mlk.decompress(arc).data
+        dec = mlk.decompress(arc).data if decompress else None
         run = {"cfg": c.to_dict(), "digest": c.digest().hex(), "archive_len": len(arc),
                "archive_sha": sha(arc), "blob_len": [len(b) for b in blobs],
-               "blob_sha": [sha(b) for b in blobs], "decomp_sha": sha(dec),
+               "blob_sha": [sha(b) for b in blobs], "decomp_sha": sha(dec) if dec is not None else None,
                "ratio": rep.compression_ratio, "exceptions": rep.exception_count,
                "residual_fraction": rep.residual_fraction,
                "convergence_fraction": rep.convergence_fraction,
@@ -137,6 +145,7 @@ def run_case(name, P, N, cfg_kw, taus=None, store_arrays=True, seed=42, rho=0.00
                 if len(s["residuals"]) < 100_000:
                     arrays[f"r{vi}_s{si}_res"] = np.frombuffer(s["residuals"], np.uint8)
         meta["runs"].append(run)
+        del arc, dec
         if store_arrays and vi == 0:
             for si, d in enumerate(stage_dump(ds, c, models)):
                 for k, v in d.items():
@@ -238,6 +247,15 @@ CASES = {
                              taus=[dict(), dict(tau=1e-2), dict(tau=1e-4)]),
     # config 3 (configs[2]): 8 x 16395, S=8 -- the bench workload's weights
     "cfg3": lambda: run_case("cfg3", 8, 16395, dict(shards=8), store_arrays=False),
+    # configs[3]'s remaining points on the config-2 corpus with cfg2's models:
+    # tau=1e-5 (every selected image falls back to lossless) and f64 lambdas
+    "cfg2x": lambda: run_case("cfg2x", 1, 16395, dict(shards=8), store_arrays=False,
+                              models_from="cfg2",
+                              taus=[dict(tau=1e-5), dict(lambda_precision="f64")]),
+    # configs[4]: 64 x 16395 (12.8 GB), S=8 col shards of ~131k members with
+    # config 3's node blocks and weights; shard hashes only (2 workers: memory)
+    "cfg5": lambda: run_case("cfg5", 64, 16395, dict(shards=8), store_arrays=False,
+                             models_from="cfg3", decompress=False, workers=2),
 }
 
 if __name__ == "__main__":

@@ -11,6 +11,7 @@ import numpy as np
 
 from oracle import port
 from paper_2212_10733_b200 import fdata
+from workload import synth
 
 GOLDEN = Path(__file__).resolve().parent / "golden"
 
@@ -36,7 +37,7 @@ def grid():
 @functools.lru_cache(maxsize=4)
 def corpus(name):
     meta, _ = load(name)
-    ds = fdata.gen_synthetic(meta["P"], meta["N"], grid(),
+    ds = synth.gen_synthetic(meta["P"], meta["N"], grid(),
                              fdata.SyntheticParams(seed=meta["seed"], rho=meta["rho"]))
     return ds, sha(ds.data) == meta["data_sha"]
 

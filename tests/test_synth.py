@@ -1,4 +1,4 @@
-"""On-device synthetic corpus (csrc/synth.cu, fdata.gen_synthetic_device):
+"""On-device synthetic corpus (csrc/synth.cu, workload.synth.gen_synthetic_device):
 the PCG64 jump-ahead restatement on CPU, bit-identical planes on the GPU."""
 
 from __future__ import annotations
@@ -7,6 +7,7 @@ import numpy as np
 import pytest
 
 from paper_2212_10733_b200 import fdata
+from workload import synth
 
 
 def _grid():
@@ -52,8 +53,8 @@ def test_device_planes_bit_identical(P, N, lo, hi, rho):
     import torch
     dev = torch.device("cuda", 0)
     params = fdata.SyntheticParams(seed=42, rho=rho)
-    host = fdata.gen_synthetic(P, N, _grid(), params).data[lo:hi]
-    got = fdata.gen_synthetic_device(P, N, _grid(), params, dev, (lo, hi))
+    host = synth.gen_synthetic(P, N, _grid(), params).data[lo:hi]
+    got = synth.gen_synthetic_device(P, N, _grid(), params, dev, (lo, hi))
     nd = N * 39 * 39
     arr = got.cpu().numpy()
     assert np.array_equal(arr[:(hi - lo) * nd].view(np.uint64),
@@ -81,8 +82,8 @@ def test_config5_shape_device_corpus_matches_oracle():
     P, N = 64, 512
     dev = torch.device("cuda", 0)
     params = fdata.SyntheticParams(seed=42, rho=0.003)
-    ds = fdata.gen_synthetic(P, N, _grid(), params)
-    got = fdata.gen_synthetic_device(P, N, _grid(), params, dev).cpu().numpy()
+    ds = synth.gen_synthetic(P, N, _grid(), params)
+    got = synth.gen_synthetic_device(P, N, _grid(), params, dev).cpu().numpy()
     assert np.array_equal(got[:ds.data.size].view(np.uint64), ds.data.reshape(-1).view(np.uint64))
     cfg = mb.PipelineConfig(workers=8, shards=8, seed=0, tau=1e-3, lambda_precision="f32",
                             static_model=True)
