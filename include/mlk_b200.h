@@ -194,6 +194,41 @@ int mlk_synth_planes(const double* base, int64_t nd, int64_t plane0, int32_t n_p
                      const uint64_t* pcg_h, double rho, double value_min, double* out,
                      cudaStream_t stream);
 
+/* ---- per-call operators of the reference's public stage API
+ * (mlk/__init__.py:9-38), used by quantizer / residual / lagrange /
+ * autoencoder here; every one is elementwise in the reference's order. */
+
+/* quantizer._nearest (quantizer.py:91-93) over lat (n, L) with the
+ * float64-upcast centroids cents (L, K) f32: first minimum, NaN first. */
+int mlk_pq_nearest(const double* lat, int64_t n, int32_t L, const float* cents, int32_t K,
+                   uint16_t* idx, cudaStream_t stream);
+/* quantizer.pq_decode's lookup (quantizer.py:132-138): out (n, L) f64;
+ * *bad = 1 when an index is >= K (SizeMismatchError). */
+int mlk_pq_lookup(const uint16_t* idx, int64_t n, int32_t L, const float* cents, int32_t K,
+                  double* out, int32_t* bad, cudaStream_t stream);
+/* BuiltinCodec.compress's codes (residual.py:63-69): z = zigzag(rint(r / 2eb));
+ * *err |= 1 for a non-finite residual, 2 for |q| >= 2**62. */
+int mlk_quantize_codes(const double* r, int64_t n, double eb, uint64_t* z, int32_t* err,
+                       cudaStream_t stream);
+/* BuiltinCodec.decompress's values (residual.py:92-99): mode 0 = q * 2eb,
+ * mode 1 = raw float64 bits. */
+int mlk_dequantize(const uint64_t* z, int64_t n, double eb, int32_t mode, double* out,
+                   cudaStream_t stream);
+/* quantize_roundtrip (residual.py:100-102); with recon != NULL the corrected
+ * images recon + roundtrip(a - recon) of find_error_bound (residual.py:149-155). */
+int mlk_quantize_roundtrip(const double* a, const double* recon, int64_t n, double eb,
+                           double* out, cudaStream_t stream);
+/* lagrange.apply_lambda (lagrange.py:136-149) for n images f (n, D) with
+ * lam (n, 4) and constraint rows a (4, D) at a + i * a_stride. */
+int mlk_apply_lambda_rows(const double* f, int64_t n, int32_t D, const double* lam,
+                          const double* a, int64_t a_stride, double floor_, double* out,
+                          cudaStream_t stream);
+/* autoencoder.decode_batch on raw f64 latents (autoencoder.py:106-110),
+ * OpenBLAS bracketing per column from tree_cols (may be NULL). */
+int mlk_ae_decode(const double* lat, int64_t n, int32_t L, const float* W, int32_t D,
+                  double mean, double sd, const uint8_t* tree_cols, double* out,
+                  cudaStream_t stream);
+
 /* ======================= (2) stage API (one launch covers all shards) ====== */
 
 /* Pass 1 over f0 (autoencoder.encode_batch autoencoder.py:99-103 in OpenBLAS
@@ -207,11 +242,13 @@ int mlk_stage1(const double* f0, const MlkShard* shards, int32_t n_shards, int32
  * (shard, dim): first_idx / draws are the PCG64 draws kmeans_1d consumes
  * (one integers() then K-1 random(), computed by the host from the seed).
  * shards (device) and shards_h (the same table on the host, for validation).  cents (n_shards, L, K) float32, sorted;
- * scratch >= 4 * L * total doubles; info (n_shards, L, 4). */
+ * scratch >= 4 * L * total doubles; info (n_shards, L, 4); cents64 (may be
+ * NULL) receives the same centroids before the float32 cast (kmeans_1d's
+ * float64 result). */
 int mlk_kmeans(const double* lat, const MlkShard* shards, const MlkShard* shards_h,
                int32_t n_shards, int32_t L, int32_t K, const int64_t* first_idx,
-               const double* draws, double* scratch, float* cents, int32_t* info,
-               cudaStream_t stream);
+               const double* draws, double* scratch, float* cents, double* cents64,
+               int32_t* info, cudaStream_t stream);
 
 /* diagnostics: cycles of CTA 0 of the last mlk_kmeans launch in its phases
  * (load + distinct test, k-means++ seeding, Lloyd), its Lloyd sweeps and six

@@ -84,7 +84,7 @@ _SIGS = {
     "mlk_gather_segments": [_P, _P, _P, _I32, _P, _P, _P],
     "mlk_zlib_decompress": [_P, _P, _P, _I32, _P, _P, _I64, _P, _P],
     "mlk_stage1": [_P, _P, _I32, _I32, _P, _P, _I32, _P, _P, _P, _P],
-    "mlk_kmeans": [_P, _P, _P, _I32, _I32, _I32, _P, _P, _P, _P, _P, _P],
+    "mlk_kmeans": [_P, _P, _P, _I32, _I32, _I32, _P, _P, _P, _P, _P, _P, _P],
     "mlk_kmeans_prof": [_P, _P],
     "mlk_synth_planes": [_P, _I64, _I64, _I32, _P, _D, _D, _P, _P],
     "mlk_select": [_P, _P, _P, _I32, _I32, _P, _P, _I32, _I32, _P, _D, _P, _P, _P, _P, _P],
@@ -105,6 +105,13 @@ _SIGS = {
     "mlk_pack_exceptions": [_P, _P, _I32, _P, _P, _P, _I32, _I32, _P, _P],
     "mlk_compare": [_P, _P, _I32, _P, _P, _P, _P, _P, _P, _P],
     "mlk_report": [_P, _I32, _P, _I64, _P, _P, _P],
+    "mlk_pq_nearest": [_P, _I64, _I32, _P, _I32, _P, _P],
+    "mlk_pq_lookup": [_P, _I64, _I32, _P, _I32, _P, _P, _P],
+    "mlk_quantize_codes": [_P, _I64, _D, _P, _P, _P],
+    "mlk_dequantize": [_P, _I64, _D, _I32, _P, _P],
+    "mlk_quantize_roundtrip": [_P, _P, _I64, _D, _P, _P],
+    "mlk_apply_lambda_rows": [_P, _I64, _I32, _P, _P, _I64, _D, _P, _P],
+    "mlk_ae_decode": [_P, _I64, _I32, _P, _I32, _D, _D, _P, _P, _P],
     "mlk_ae_train": [_P, _P, _P, _P, _I32, _I32, _I32, _I32, _D, _D, _D, _D, _D, _D, _P, _I32, _P, _P, _P],
     "mlk_ae_train_config": [_P, _P],
     "mlk_decode": [_P, _I32, _I32, _P, _P, _I32, _P, _I32, _P, _P, _P, _P, _P, _P, _P, _P,

@@ -242,3 +242,32 @@ def train(images, config: TrainConfig, init: AEModel | None = None,
     job = TrainJob(base=x.reshape(-1), row_off=np.arange(n, dtype=np.int64) * d,
                    epochs=config.epochs, seed=config.seed, init=init)
     return train_jobs([job], config, latent_dim, d)[0]
+
+
+def ae_accuracy(images, model: AEModel, tau: float) -> float:
+    """Fraction of images whose AE-only reconstruction meets the bound
+    (autoencoder.py:180-188): encode (OpenBLAS order, mlk_stage1), decode
+    (mlk_ae_decode) and the exact per-image NRMSE (mlk_compare) on the
+    device."""
+    import torch
+
+    from . import _ops
+    from ._lib import call
+    if tau <= 0:
+        raise ConfigError("tau must be positive")
+    images = np.asarray(images, dtype=np.float64)
+    n = images.shape[0]
+    flat = images.reshape(n, -1)
+    d = flat.shape[1]
+    if d != model.input_dim:
+        raise DimensionError(f"images have {d} entries, model expects {model.input_dim}")
+    if n == 0:
+        return float(np.mean(np.zeros(0) <= tau))
+    lat, imgs, W, grid = _ops.ae_encode(flat, model)
+    recon = torch.empty(n * d, dtype=torch.float64, device=lat.device)
+    # OpenBLAS's small-matrix kernel sums every column sequentially
+    tree = grid.t["tree"] if n * model.latent_dim * d > 1e6 else None
+    call("mlk_ae_decode", lat, n, model.latent_dim, W, d, float(model.norm_mean),
+         float(model.norm_std), tree, recon)
+    err, _ = _ops.image_nrmse(imgs, recon, n, d)
+    return float(np.mean(err.cpu().numpy() <= tau))

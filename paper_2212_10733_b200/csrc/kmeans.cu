@@ -286,7 +286,8 @@ __device__ void block_pw_sums(const double* x, const int* seg_start, const int* 
 __global__ void __launch_bounds__(KT, 1)
 k_kmeans(const double* __restrict__ lat, const MlkShard* __restrict__ shards, int L, int K,
          const long long* __restrict__ first_idx, const double* __restrict__ draws,
-         double* __restrict__ scratch, float* __restrict__ cents, int* __restrict__ info) {
+         double* __restrict__ scratch, float* __restrict__ cents, double* __restrict__ cents64,
+         int* __restrict__ info) {
     __shared__ KmSmem S;
     extern __shared__ double dyn[];  // pairwise heap slots, slot kinds, warp counters
     double* val = dyn;
@@ -304,6 +305,7 @@ k_kmeans(const double* __restrict__ lat, const MlkShard* __restrict__ shards, in
     unsigned short* lab = reinterpret_cast<unsigned short*>(base + 3 * n);
     unsigned short* lab2 = lab + n;
     float* out = cents + ((long long)s * L + dim) * K;
+    double* out64 = cents64 ? cents64 + ((long long)s * L + dim) * K : nullptr;
     int* inf = info + (s * L + dim) * 4;
 
     const long long kp_t0 = clock64();
@@ -330,7 +332,11 @@ k_kmeans(const double* __restrict__ lat, const MlkShard* __restrict__ shards, in
         }
         __syncthreads();
         if (cnt <= K) {
-            if (tid < K) out[tid] = (float)S.distinct[tid < cnt ? tid : cnt - 1];
+            if (tid < K) {
+                const double c = S.distinct[tid < cnt ? tid : cnt - 1];
+                out[tid] = (float)c;
+                if (out64) out64[tid] = c;
+            }
             if (tid == 0) { inf[0] = 0; inf[1] = cnt; inf[2] = 0; inf[3] = 0; }
             return;
         }
@@ -541,23 +547,26 @@ k_kmeans(const double* __restrict__ lat, const MlkShard* __restrict__ shards, in
         inf[0] = 1; inf[1] = K; inf[2] = sweeps; inf[3] = fallbacks;
     }
     __syncthreads();
-    if (tid < K) out[tid] = (float)S.cent[tid];
+    if (tid < K) {
+        out[tid] = (float)S.cent[tid];
+        if (out64) out64[tid] = S.cent[tid];
+    }
 }
 
 }  // namespace
 
 extern "C" int mlk_kmeans(const double* lat, const MlkShard* shards, const MlkShard* shards_h,
                           int32_t n_shards, int32_t L, int32_t K, const int64_t* first_idx,
-                          const double* draws, double* scratch, float* cents, int32_t* info,
-                          cudaStream_t stream) {
-    if (K < 2 || K > MLK_MAXK || L < 1 || L > MLK_MAXL) return MLK_ERR_CONFIG;
+                          const double* draws, double* scratch, float* cents, double* cents64,
+                          int32_t* info, cudaStream_t stream) {
+    if (K < 1 || K > MLK_MAXK || L < 1 || L > MLK_MAXL) return MLK_ERR_CONFIG;
     for (int s = 0; s < n_shards; ++s)
         if (shards_h[s].n_img < 1 || shards_h[s].n_img > (1 << 18)) return MLK_ERR_DIM;
     size_t dyn = (size_t)KM_MAX_SLOTS * (sizeof(double) + 1) + (size_t)KW * MLK_MAXK * sizeof(int);
     cudaFuncSetAttribute(k_kmeans, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
     k_kmeans<<<n_shards * L, KT, dyn, stream>>>(lat, shards, L, K,
                                                 reinterpret_cast<const long long*>(first_idx),
-                                                draws, scratch, cents, info);
+                                                draws, scratch, cents, cents64, info);
     return cudaGetLastError() == cudaSuccess ? MLK_OK : MLK_ERR_CUDA;
 }
 

@@ -21,6 +21,8 @@
 // exponent tables for the next iteration.  Two barriers per iteration.
 #include "common.cuh"
 
+#include <algorithm>
+
 namespace {
 
 constexpr int PJ_T = 128;
@@ -444,208 +446,414 @@ __device__ double block_pairwise(const double* v, const PwPlan& pw, PjCtl& C) {
     return C.bval;
 }
 
+// ===========================================================================
+// k_project_w: ONE WARP per histogram, persistent.  Each warp owns a private
+// slice of shared memory (the TMA-staged original O, the working image F and
+// its Newton tables) and walks images img = blockIdx.x, + gridDim.x, ...; the
+// bulk copy of the next image's original is issued as soon as the current
+// one's final NRMSE has consumed O, so it lands under the next image's AE
+// decode.  No block barriers: every reduction is a warp shuffle, the 4x4
+// Newton solve runs once per warp (warp-uniform), and the Newton sums use a
+// lane-per-column layout (lane c owns column c; the columns past 31 are split
+// into row groups over the lanes) with the interior rows factorised out of
+// the per-cell work:
+//   per interior cell: m = F * eb[r];  S0 += m;  S1 += p2_r m;  S2 += p2_r^2 m
+// (the column's exp(-w A_c), the volume class and the column factors of the
+// 14 sums are applied once per column).
+
+constexpr int PW_MAXRC = 64;   // rows, cols <= 64 on the separable path
+
+struct WarpTabs {              // offsets (doubles) of the per-warp tables
+    int ea, eb, vp1, p3c, p2r, p2s, a2c, vp2, n;
+};
+
+__host__ __device__ inline WarpTabs warp_tabs(int rows, int cols) {
+    WarpTabs t;
+    int o = 0;
+    t.ea = o; o += 2 * cols;    // exp(-w(re, ce_c) A_c)        [re][c]
+    t.eb = o; o += 2 * rows;    // exp(-w(re_r, ce) B_r)        [ce][r]
+    t.vp1 = o; o += cols;       // vpar_c / s1                  (grid)
+    t.p3c = o; o += cols;       // hm (vpar_c - u)^2 / s4       (image)
+    t.p2r = o; o += rows;       // hm vperp2_r / s2             (grid)
+    t.p2s = o; o += rows;       // p2r^2                        (grid)
+    t.a2c = o; o += 2 * rows;   // ash row 2 by (col edge, row) (grid, exact table values)
+    t.vp2 = o; o += rows;       // vperp2_r                     (grid)
+    t.n = (o + 1) & ~1;
+    return t;
+}
+
+// per-warp shared memory: O (D + 2), F (D, even), tables, pairwise leaves
+__host__ __device__ inline int warp_slice_doubles(int D, int rows, int cols) {
+    return ((D + 3) / 2) * 2 + ((D + 1) / 2) * 2 + warp_tabs(rows, cols).n + MLK_PW_MAX_LEAVES;
+}
+
+__device__ __forceinline__ double wsum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+    return v;
+}
+
+// the 14 Newton sums of one column from its five factorised accumulators
+__device__ __forceinline__ void add_column(double (&v)[16], double q0, double q1, double q3,
+                                           double G1, double G2, double H1, double H2,
+                                           double H3) {
+    v[0] += q0 * G1; v[1] += q1 * G1; v[2] += G2; v[3] += q3 * G1;
+    v[4] += q0 * q0 * H1; v[5] += q0 * q1 * H1; v[6] += q0 * H2; v[7] += q0 * q3 * H1;
+    v[8] += q1 * q1 * H1; v[9] += q1 * H2; v[10] += q1 * q3 * H1;
+    v[11] += H3; v[12] += q3 * H2; v[13] += q3 * q3 * H1;
+}
+
+// Newton tables for lam (one warp); true when some exponent could pass the
+// reference's +-700 clamp (that iteration is then evaluated cell by cell)
+__device__ __forceinline__ bool warp_tables(const double (&lam)[4], const double (&w)[4],
+                                            double is0, int rows, int cols, double* T,
+                                            const WarpTabs& tb) {
+    const int lane = threadIdx.x & 31;
+    bool big = false;
+    for (int q = lane; q < 2 * (rows + cols); q += 32) {
+        double x;
+        if (q < 2 * cols) {
+            const int re = q >= cols, c = q - re * cols;
+            const bool ce = (c == 0) | (c == cols - 1);
+            x = cls_val(w, re, ce) * (lam[0] * is0 + lam[1] * T[tb.vp1 + c] + lam[3] * T[tb.p3c + c]);
+            T[tb.ea + q] = exp(-x);
+        } else {
+            const int q2 = q - 2 * cols;
+            const int ce = q2 >= rows, r = q2 - ce * rows;
+            const bool re = (r == 0) | (r == rows - 1);
+            x = cls_val(w, re, ce) * (lam[2] * T[tb.p2r + r]);
+            T[tb.eb + q2] = exp(-x);
+        }
+        if (!(fabs(x) <= 349.0)) big = true;
+    }
+    __syncwarp();
+    return __any_sync(FULL, big);
+}
+
+// one warp's Newton iteration (_ckernels.pyx:62-137 semantics via newton_step)
 template <bool SEP>
-__global__ void __launch_bounds__(PJ_T, 6)
-k_project(const double* __restrict__ f0, const double* __restrict__ stats,
-          const double* __restrict__ qoi, const MlkShard* __restrict__ shards, int n_shards,
-          MlkGrid g, PwPlan pw, const float* __restrict__ W, int L, const float* __restrict__ cents,
-          int K, const unsigned char* __restrict__ codes, const int* __restrict__ sel_rank,
-          const int* __restrict__ slot_base, MlkNewton opt, unsigned char* __restrict__ flags,
-          double* __restrict__ lam_out, double* __restrict__ qst_out,
-          int* __restrict__ status_out, int* __restrict__ iters_out,
-          double* __restrict__ ferr_out, double* __restrict__ fqoi_out,
-          double* __restrict__ fsse_out, unsigned char* __restrict__ varint, long long vcap,
-          long long* __restrict__ vlen, int* __restrict__ err_flag) {
-    __shared__ PjCtl C;
+__device__ void newton_warp(const double* F, const MlkGrid& g, const double (&w)[4], double is0,
+                            double is4, double u, const double* b, double bmax, double step,
+                            int max_iter, double tol, double* T, const WarpTabs& tb,
+                            double (&lam)[4], int& status, int& iters) {
+    const int lane = threadIdx.x & 31;
+    const int D = g.D, rows = g.rows, cols = g.cols;
+    bool clamped = false;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) lam[k] = 0.0;
+    status = MLK_NEWTON_MAX_ITER;
+    iters = max_iter;
+    // the lane's columns: A = column `lane` (all rows), B = one row group of
+    // a column past 31
+    const int nA = cols < 32 ? cols : 32;
+    const int nx = cols > 32 ? cols - 32 : 0;
+    const int grp = nx ? 32 / nx : 0;
+    const bool hasA = lane < nA, hasB = nx && lane < nx * grp;
+    const int cB = hasB ? 32 + lane % nx : 0, gB = hasB ? lane / nx : 0;
+    const int rB0 = hasB ? gB * rows / grp : 0, rB1 = hasB ? (gB + 1) * rows / grp : 0;
+    bool big = SEP ? warp_tables(lam, w, is0, rows, cols, T, tb) : true;
+    for (int it = 0;; ++it) {
+        double v[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) v[k] = 0.0;
+        if (SEP && !big) {
+            const double* p2r = T + tb.p2r;
+            const double* p2s = T + tb.p2s;
+            if (hasA) {
+                const int c = lane;
+                const bool ce = (c == 0) | (c == cols - 1);
+                const double* ebp = T + tb.eb + ce * rows;
+                const double w_in = cls_val(w, false, ce), w_ed = cls_val(w, true, ce);
+                double S0 = 0.0, S1 = 0.0, S2 = 0.0, U0 = 0.0, U1 = 0.0, U2 = 0.0;
+                int r = 1;
+                // two rows per step: independent accumulator chains
+                for (; r + 1 < rows - 1; r += 2) {
+                    const double m0 = F[r * cols + c] * ebp[r];
+                    const double m1 = F[(r + 1) * cols + c] * ebp[r + 1];
+                    S0 += m0; S1 = fma(p2r[r], m0, S1); S2 = fma(p2s[r], m0, S2);
+                    U0 += m1; U1 = fma(p2r[r + 1], m1, U1); U2 = fma(p2s[r + 1], m1, U2);
+                }
+                for (; r < rows - 1; ++r) {
+                    const double m0 = F[r * cols + c] * ebp[r];
+                    S0 += m0; S1 = fma(p2r[r], m0, S1); S2 = fma(p2s[r], m0, S2);
+                }
+                S0 += U0; S1 += U1; S2 += U2;
+                const int rl = rows - 1;
+                const double e0 = F[c] * ebp[0], e1 = F[rl * cols + c] * ebp[rl];
+                const double E0 = e0 + e1, E1 = p2r[0] * e0 + p2r[rl] * e1,
+                             E2 = p2s[0] * e0 + p2s[rl] * e1;
+                const double ai = w_in * T[tb.ea + c], ae = w_ed * T[tb.ea + cols + c];
+                const double G1 = ai * S0 + ae * E0, G2 = ai * S1 + ae * E1;
+                const double H1 = w_in * ai * S0 + w_ed * ae * E0;
+                const double H2 = w_in * ai * S1 + w_ed * ae * E1;
+                const double H3 = w_in * ai * S2 + w_ed * ae * E2;
+                add_column(v, is0, T[tb.vp1 + c], T[tb.p3c + c], G1, G2, H1, H2, H3);
+            }
+            if (hasB) {
+                const int c = cB;
+                const bool ce = (c == 0) | (c == cols - 1);
+                const double* ebp = T + tb.eb + ce * rows;
+                const double w_in = cls_val(w, false, ce), w_ed = cls_val(w, true, ce);
+                const double ea0 = T[tb.ea + c], ea1 = T[tb.ea + cols + c];
+                double G1 = 0.0, G2 = 0.0, H1 = 0.0, H2 = 0.0, H3 = 0.0;
+                for (int r = rB0; r < rB1; ++r) {
+                    const bool re = (r == 0) | (r == rows - 1);
+                    const double ww = re ? w_ed : w_in;
+                    const double wf = ww * (F[r * cols + c] * (re ? ea1 : ea0) * ebp[r]);
+                    const double w2f = ww * wf, t2 = p2r[r] * w2f;
+                    G1 += wf; G2 = fma(p2r[r], wf, G2);
+                    H1 += w2f; H2 += t2; H3 = fma(p2r[r], t2, H3);
+                }
+                add_column(v, is0, T[tb.vp1 + c], T[tb.p3c + c], G1, G2, H1, H2, H3);
+            }
+        } else {
+            const double l0 = lam[0], l1 = lam[1], l2 = lam[2], l3 = lam[3];
+            for (int j = lane; j < D; j += 32) {
+                const double a0 = __ldg(g.ash + j), a1 = __ldg(g.ash + D + j),
+                             a2 = __ldg(g.ash + 2 * D + j);
+                const double dv = __ldg(g.vpar + j) - u;
+                const double a3 = __ldg(g.hmvol + j) * dv * dv * is4;
+                double t = l0 * a0 + l1 * a1 + l2 * a2 + l3 * a3;
+                if (fabs(t) > 700.0) { v[14] = 1.0; t = t > 0 ? 700.0 : -700.0; }
+                cell_sums(v, a0, a1, a2, a3, F[j] * exp(-t));
+            }
+        }
+        const double part = warp_rs16(v);   // lane l: warp sum of value l >> 1
+        double sums[15];
+#pragma unroll
+        for (int k = 0; k < 15; ++k) sums[k] = __shfl_sync(FULL, part, 2 * k);
+        if (!newton_step(sums, b, bmax, step, max_iter, tol, it, lam, clamped, status, iters))
+            break;  // warp-uniform: every lane holds the same sums
+        if (SEP) big = warp_tables(lam, w, is0, rows, cols, T, tb);
+    }
+}
+
+template <bool SEP>
+__global__ void __launch_bounds__(32)
+k_project_w(const double* __restrict__ f0, const double* __restrict__ stats,
+            const double* __restrict__ qoi, const MlkShard* __restrict__ shards, int n_shards,
+            int total, MlkGrid g, PwPlan pw, const float* __restrict__ W, int L,
+            const float* __restrict__ cents, int K, const unsigned char* __restrict__ codes,
+            const int* __restrict__ sel_rank, const int* __restrict__ slot_base, MlkNewton opt,
+            unsigned char* __restrict__ flags, double* __restrict__ lam_out,
+            double* __restrict__ qst_out, int* __restrict__ status_out,
+            int* __restrict__ iters_out, double* __restrict__ ferr_out,
+            double* __restrict__ fqoi_out, double* __restrict__ fsse_out,
+            unsigned char* __restrict__ varint, long long vcap, long long* __restrict__ vlen,
+            int* __restrict__ err_flag) {
     __shared__ unsigned long long bar;
     extern __shared__ __align__(16) double sm[];
-    const int D = g.D;
-    const int img = blockIdx.x;
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    int ph = 0;
-    const int s = find_shard(shards, n_shards, img);
-    const MlkShard sh = shards[s];
-    const double* x = shard_image(f0, sh, img - sh.img_off, D);
-    double* Ob = sm;                     // TMA target: the original, later d^2
-    double* F = sm + ((D + 3) / 2) * 2;  // recon -> corrected -> f_plus -> final
-
-    // ---- one bulk copy of the original; the AE decode overlaps it
-    if (tid == 0) mbar_init(&bar, 1);
-    __syncthreads();
-    int shift;
-    if (warp == 0) {
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        shift = stage_histogram(Ob, x, D, &bar);
-    } else {
-        shift = (int)((reinterpret_cast<unsigned long long>(x) & 15ull) >> 3);
-    }
-    double* O = Ob + shift;
-    double z[MLK_MAXL];
-#pragma unroll
-    for (int k = 0; k < MLK_MAXL; ++k)
-        z[k] = k < L ? (double)cents[((long long)s * L + k) * K + codes[(long long)img * L + k]]
-                     : 0.0;
-    const float* Ws = W + sh.w_off;
-    const bool blas_tree = !sh.small_blas;
-    for (int j = tid; j < D; j += PJ_T)
-        F[j] = decode_cell(z, Ws, L, D, j, blas_tree && g.tree_cols[j], sh.mean, sh.std);
-    // per-grid / per-image column and row tables of the separable Newton
-    const double4 q4 = reinterpret_cast<const double4*>(qoi)[img];
-    double qs[4] = {q4.x, q4.y, q4.z, q4.w};
-    if (opt.lam_f32) {
-#pragma unroll
-        for (int k = 0; k < 4; ++k) qs[k] = (double)__double2float_rn(qs[k]);
-    }
+    const int D = g.D, rows = g.rows, cols = g.cols;
+    const int lane = threadIdx.x;
+    double* Obuf = sm;                        // TMA target: the original, later d^2
+    double* F = sm + ((D + 3) / 2) * 2;       // recon -> corrected -> f_plus -> final
+    double* T = F + ((D + 1) / 2) * 2;        // Newton / apply tables
+    const WarpTabs tb = warp_tabs(rows, cols);
+    double* leaf = T + tb.n;
     const double hm = 0.5 * g.mass;
-    if (SEP) {
-        if (tid < g.cols) {
-            const double vp = g.vpar[tid];
-            C.vp1[tid] = vp / g.s1;
-            const double dv = vp - qs[1];
-            C.p3c[tid] = hm * dv * dv;  // / s4 once s4 is known
-        } else if (tid >= 64 && tid - 64 < g.rows) {
-            C.p2r[tid - 64] = hm * g.vperp2[(tid - 64) * g.cols] / g.s2;
-        }
-    }
-    mbar_wait(&bar, 0);
-    __syncthreads();
-
-    // ---- residual stage for selected images (contiguous cells per thread so
-    //      the varint stream is written in cell order after one block scan)
-    const int rank = sel_rank[img];
-    if (rank >= 0) {  // block-uniform
-        const double eb2 = 2.0 * sh.eb;
-        const double inv = 1.0 / eb2;
-        const bool lossless = sh.lossless != 0;
-        const int per = (D + PJ_T - 1) / PJ_T;
-        const int c0 = min(D, tid * per), c1 = min(D, c0 + per);
-        int nb = 0;
-        bool too_big = false;
-        for (int j = c0; j < c1; ++j) {
-            const double r = __dsub_rn(O[j], F[j]);
-            unsigned long long zz;
-            if (lossless) {
-                zz = (unsigned long long)__double_as_longlong(r);
-            } else {
-                const double q = qround(r, eb2, inv);
-                if (!(fabs(q) < 4611686018427387904.0)) too_big = true;
-                const long long qi = (long long)q;
-                zz = ((unsigned long long)qi << 1) ^ (unsigned long long)(qi >> 63);
-            }
-            nb += varint_len(zz);
-        }
-        if (too_big) atomicExch(err_flag, MLK_ERR_CONFIG);
-        int tot = 0;
-        int pos = block_exscan_int(nb, &tot, C);
-        const long long slot = slot_base[s] + rank;
-        unsigned char* out = varint + slot * vcap;
-        for (int j = c0; j < c1; ++j) {
-            const double r = __dsub_rn(O[j], F[j]);
-            unsigned long long zz;
-            if (lossless) {
-                zz = (unsigned long long)__double_as_longlong(r);
-                F[j] = __dadd_rn(F[j], r);
-            } else {
-                const double q = qround(r, eb2, inv);
-                const long long qi = (long long)q;
-                zz = ((unsigned long long)qi << 1) ^ (unsigned long long)(qi >> 63);
-                F[j] = __dadd_rn(F[j], __dmul_rn(q, eb2));
-            }
-            while (zz >= 0x80ull) {
-                out[pos++] = (unsigned char)(zz | 0x80ull);
-                zz >>= 7;
-            }
-            out[pos++] = (unsigned char)zz;
-        }
-        if (tid == 0) vlen[slot] = tot;
-        __syncthreads();
-    }
-
-    // ---- stored QoIs (pipeline.py:254-260) and the per-image system:
-    //      top = max(corrected), s4 = max |a3| (lagrange.py:199-204)
-    double top = -INFINITY, amax = 0.0;
-    bool nan_t = false, nan_a = false;  // numpy max propagates NaN
-    for (int j = tid; j < D; j += PJ_T) {
-        const double fj = F[j];
-        nan_t |= fj != fj;
-        top = fmax(top, fj);
-    }
-    if (SEP) {
-        // a3 = hmvol * (vpar - u)^2 takes one value per (row edge, column)
-        if (tid < g.cols) {
-            const double dv = __dsub_rn(__ldg(g.vpar + tid), qs[1]);
-            const double dv2 = __dmul_rn(dv, dv);
-            const int r_in = g.rows > 2 ? 1 : 0;
+    double w[4];
 #pragma unroll
-            for (int e = 0; e < 2; ++e) {
-                const double a3 = fabs(__dmul_rn(__ldg(g.hmvol + (e ? 0 : r_in) * g.cols + tid),
-                                                 dv2));
+    for (int k = 0; k < 4; ++k) w[k] = g.vcls[k];
+    if (SEP) {  // grid-constant tables, once per warp
+        for (int c = lane; c < cols; c += 32) T[tb.vp1 + c] = g.vpar[c] / g.s1;
+        const int cin = cols > 2 ? 1 : 0;
+        for (int r = lane; r < rows; r += 32) {
+            const double p2 = hm * g.vperp2[r * cols] / g.s2;
+            T[tb.p2r + r] = p2;
+            T[tb.p2s + r] = p2 * p2;
+            T[tb.a2c + r] = __ldg(g.ash + 2 * D + r * cols + cin);          // interior column
+            T[tb.a2c + rows + r] = __ldg(g.ash + 2 * D + r * cols);         // edge column
+            T[tb.vp2 + r] = g.vperp2[r * cols];
+        }
+    }
+    if (lane == 0) mbar_init(&bar, 1);
+    __syncwarp();
+    unsigned phase = 0;
+    int img = blockIdx.x;
+    int shift = 0;
+    if (img < total) {
+        const int s0 = find_shard(shards, n_shards, img);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        shift = stage_histogram(Obuf, shard_image(f0, shards[s0], img - shards[s0].img_off, D),
+                                D, &bar);
+    }
+    // the lane's columns for the apply pass (same split as the Newton sums)
+    const int nA = cols < 32 ? cols : 32;
+    const int nx = cols > 32 ? cols - 32 : 0;
+    const int grp = nx ? 32 / nx : 0;
+    const bool hasA = lane < nA, hasB = nx && lane < nx * grp;
+    const int cB = hasB ? 32 + lane % nx : 0, gB = hasB ? lane / nx : 0;
+    const int rB0 = hasB ? gB * rows / grp : 0, rB1 = hasB ? (gB + 1) * rows / grp : 0;
+
+    for (; img < total; img += gridDim.x) {
+        const int s = find_shard(shards, n_shards, img);
+        const MlkShard sh = shards[s];
+        // ---- AE decode into F while the original is in flight
+        double z[MLK_MAXL];
+#pragma unroll
+        for (int k = 0; k < MLK_MAXL; ++k)
+            z[k] = k < L ? (double)cents[((long long)s * L + k) * K + codes[(long long)img * L + k]]
+                         : 0.0;
+        const float* Ws = W + sh.w_off;
+        const bool blas_tree = !sh.small_blas;
+        for (int j = lane; j < D; j += 32)
+            F[j] = decode_cell(z, Ws, L, D, j, blas_tree && g.tree_cols[j], sh.mean, sh.std);
+        const double4 q4 = reinterpret_cast<const double4*>(qoi)[img];
+        double qs[4] = {q4.x, q4.y, q4.z, q4.w};
+        if (opt.lam_f32) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) qs[k] = (double)__double2float_rn(qs[k]);
+        }
+        mbar_wait(&bar, phase);
+        phase ^= 1;
+        const double* Oc = Obuf + shift;
+        double* O = Obuf + shift;
+        (void)Oc;
+        __syncwarp();
+
+        // ---- residual stage (selected images): contiguous cells per lane so
+        //      the varint stream is written in cell order after one warp scan
+        const int rank = sel_rank[img];
+        if (rank >= 0) {  // warp-uniform
+            const double eb2 = 2.0 * sh.eb;
+            const double inv = 1.0 / eb2;
+            const bool lossless = sh.lossless != 0;
+            const int per = (D + 31) / 32;
+            const int c0 = min(D, lane * per), c1 = min(D, c0 + per);
+            int nb = 0;
+            bool too_big = false;
+            for (int j = c0; j < c1; ++j) {
+                const double r = __dsub_rn(O[j], F[j]);
+                unsigned long long zz;
+                if (lossless) {
+                    zz = (unsigned long long)__double_as_longlong(r);
+                } else {
+                    const double q = qround(r, eb2, inv);
+                    if (!(fabs(q) < 4611686018427387904.0)) too_big = true;
+                    const long long qi = (long long)q;
+                    zz = ((unsigned long long)qi << 1) ^ (unsigned long long)(qi >> 63);
+                }
+                nb += varint_len(zz);
+            }
+            if (too_big) atomicExch(err_flag, MLK_ERR_CONFIG);
+            int inc = nb;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int t = __shfl_up_sync(FULL, inc, o);
+                if (lane >= o) inc += t;
+            }
+            const int tot = __shfl_sync(FULL, inc, 31);
+            int pos = inc - nb;
+            const long long slot = slot_base[s] + rank;
+            unsigned char* out = varint + slot * vcap;
+            for (int j = c0; j < c1; ++j) {
+                const double r = __dsub_rn(O[j], F[j]);
+                unsigned long long zz;
+                if (lossless) {
+                    zz = (unsigned long long)__double_as_longlong(r);
+                    F[j] = __dadd_rn(F[j], r);
+                } else {
+                    const double q = qround(r, eb2, inv);
+                    const long long qi = (long long)q;
+                    zz = ((unsigned long long)qi << 1) ^ (unsigned long long)(qi >> 63);
+                    F[j] = __dadd_rn(F[j], __dmul_rn(q, eb2));
+                }
+                while (zz >= 0x80ull) {
+                    out[pos++] = (unsigned char)(zz | 0x80ull);
+                    zz >>= 7;
+                }
+                out[pos++] = (unsigned char)zz;
+            }
+            if (lane == 0) vlen[slot] = tot;
+            __syncwarp();
+        }
+
+        // ---- stored QoIs (pipeline.py:254-260) and the per-image system:
+        //      top = max(corrected), s4 = max |a3| (lagrange.py:199-204)
+        double top = -INFINITY, amax = 0.0;
+        bool nan_t = false, nan_a = false;  // numpy max propagates NaN
+        for (int j = lane; j < D; j += 32) {
+            const double fj = F[j];
+            nan_t |= fj != fj;
+            top = fmax(top, fj);
+        }
+        if (SEP) {
+            // a3 = hmvol * (vpar - u)^2 takes one value per (row edge, column)
+            for (int c = lane; c < cols; c += 32) {
+                const double dv = __dsub_rn(__ldg(g.vpar + c), qs[1]);
+                const double dv2 = __dmul_rn(dv, dv);
+                const int r_in = rows > 2 ? 1 : 0;
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const double a3 = fabs(__dmul_rn(__ldg(g.hmvol + (e ? 0 : r_in) * cols + c),
+                                                     dv2));
+                    nan_a |= a3 != a3;
+                    amax = fmax(amax, a3);
+                }
+                T[tb.p3c + c] = hm * dv * dv;  // / s4 below
+            }
+        } else {
+            for (int j = lane; j < D; j += 32) {
+                const double dv = __dsub_rn(__ldg(g.vpar + j), qs[1]);
+                const double a3 = fabs(__dmul_rn(__ldg(g.hmvol + j), __dmul_rn(dv, dv)));
                 nan_a |= a3 != a3;
                 amax = fmax(amax, a3);
             }
         }
-    } else {
-        for (int j = tid; j < D; j += PJ_T) {
-            const double dv = __dsub_rn(__ldg(g.vpar + j), qs[1]);
-            const double a3 = fabs(__dmul_rn(__ldg(g.hmvol + j), __dmul_rn(dv, dv)));
-            nan_a |= a3 != a3;
-            amax = fmax(amax, a3);
+        if (__any_sync(FULL, nan_t)) top = __longlong_as_double(0x7ff8000000000000ll);
+        if (__any_sync(FULL, nan_a)) amax = __longlong_as_double(0x7ff8000000000000ll);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            top = np_max2(top, __shfl_xor_sync(FULL, top, o));
+            amax = np_max2(amax, __shfl_xor_sync(FULL, amax, o));
         }
-    }
-    if (nan_t) top = __longlong_as_double(0x7ff8000000000000ll);
-    if (nan_a) amax = __longlong_as_double(0x7ff8000000000000ll);
-    block_allmax2(top, amax, C, ph);
-    const double s4 = amax;
-    const double sc4 = s4 > 0 ? s4 : 1.0;
-    // f_plus = max(corrected, floor * top) (lagrange.py:103-107) is applied on
-    // every read below when top > 0 (no NaN then); F keeps the corrected image
-    const double fl = top > 0 ? __dmul_rn(opt.floor, top) : 0.0;
-    if (SEP && tid < g.cols) C.p3c[tid] /= sc4;
+        const double s4 = amax;
+        const double sc4 = s4 > 0 ? s4 : 1.0;
+        // f_plus = max(corrected, floor * top) (lagrange.py:103-107); top > 0
+        // excludes NaN, and the apply below reads the same f_plus
+        const double fl = top > 0 ? __dmul_rn(opt.floor, top) : 0.0;
+        if (top > 0) {
+            for (int j = lane; j < D; j += 32) {
+                const double fj = F[j];
+                F[j] = fj < fl ? fl : fj;
+            }
+        }
+        if (SEP) {
+            for (int c = lane; c < cols; c += 32) T[tb.p3c + c] /= sc4;
+        }
+        __syncwarp();
 
-    double lam[4] = {0.0, 0.0, 0.0, 0.0};
-    int status = MLK_NEWTON_DEGENERATE, iters = 0;
-    const bool valid = qs[0] > 0 && isfinite(qs[0]) && isfinite(qs[1]) && isfinite(qs[2]) &&
-                       isfinite(qs[3]) && s4 > 0 && top > 0;
-    if (valid) {  // block-uniform
-        const double b[4] = {__ddiv_rn(qs[0], g.s0), __ddiv_rn(__dmul_rn(qs[0], qs[1]), g.s1),
-                             __ddiv_rn(__dmul_rn(qs[0], qs[2]), g.s2),
-                             __ddiv_rn(__dmul_rn(qs[0], qs[3]), s4)};
-        double bmax = 0.0;
+        double lam[4] = {0.0, 0.0, 0.0, 0.0};
+        int status = MLK_NEWTON_DEGENERATE, iters = 0;
+        const bool valid = qs[0] > 0 && isfinite(qs[0]) && isfinite(qs[1]) && isfinite(qs[2]) &&
+                           isfinite(qs[3]) && s4 > 0 && top > 0;
+        if (valid) {  // warp-uniform
+            const double b[4] = {__ddiv_rn(qs[0], g.s0), __ddiv_rn(__dmul_rn(qs[0], qs[1]), g.s1),
+                                 __ddiv_rn(__dmul_rn(qs[0], qs[2]), g.s2),
+                                 __ddiv_rn(__dmul_rn(qs[0], qs[3]), s4)};
+            double bmax = 0.0;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) bmax = fmax(bmax, fabs(b[k]));
-        if (bmax > 0.0 && isfinite(bmax)) {
-            NtCtx X;
+            for (int k = 0; k < 4; ++k) bmax = fmax(bmax, fabs(b[k]));
+            if (bmax > 0.0 && isfinite(bmax)) {
+                const double is0 = 1.0 / g.s0, is4 = 1.0 / s4;
+                newton_warp<SEP>(F, g, w, is0, is4, qs[1], b, bmax, opt.step, opt.max_iter,
+                                 opt.tol, T, tb, lam, status, iters);
+                if (opt.retry && status == MLK_NEWTON_MAX_ITER) {
+                    double lam2[4];
+                    int st2 = 0, it2 = 0;
+                    newton_warp<SEP>(F, g, w, is0, is4, qs[1], b, bmax, opt.retry_step,
+                                     opt.retry_max_iter, opt.tol, T, tb, lam2, st2, it2);
+                    if (st2 == MLK_NEWTON_CONVERGED) {
 #pragma unroll
-            for (int k = 0; k < 4; ++k) X.w[k] = g.vcls[k];
-            X.is0 = 1.0 / g.s0;
-            X.is4 = 1.0 / s4;
-            X.u = qs[1];
-            X.rows = g.rows;
-            X.cols = g.cols;
-            __syncthreads();  // the p3c tables
-            newton_block<SEP>(F, fl, g, X, b, bmax, opt.step, opt.max_iter, opt.tol, C, lam, status,
-                              iters);
-            // warp 0 holds the result: publish its status so the retry
-            // decision is block-uniform
-            if (warp == 0 && lane == 0) C.status = status;
-            __syncthreads();
-            if (opt.retry && C.status == MLK_NEWTON_MAX_ITER) {
-                double lam2[4];
-                int st2 = 0, it2 = 0;
-                newton_block<SEP>(F, fl, g, X, b, bmax, opt.retry_step, opt.retry_max_iter, opt.tol,
-                                  C, lam2, st2, it2);
-                if (warp == 0 && st2 == MLK_NEWTON_CONVERGED) {
-#pragma unroll
-                    for (int k = 0; k < 4; ++k) lam[k] = lam2[k];
-                    status = st2;
-                    iters += it2;
+                        for (int k = 0; k < 4; ++k) lam[k] = lam2[k];
+                        status = st2;
+                        iters += it2;
+                    }
                 }
             }
         }
-    }
 
-    // ---- exception bookkeeping (pipeline.py:263-277), warp 0
-    if (warp == 0) {
+        // ---- exception bookkeeping (pipeline.py:263-277), warp-uniform
         unsigned fl8 = flags[img];
         double lu[4] = {0.0, 0.0, 0.0, 0.0};
         if (!(fl8 & MLK_F_NONFINITE)) {
@@ -655,7 +863,7 @@ k_project(const double* __restrict__ f0, const double* __restrict__ stats,
                 bool over = false;
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
-                    float f = __double2float_rn(lam[k]);
+                    const float f = __double2float_rn(lam[k]);
                     if (!isfinite(f)) over = true;
                     lu[k] = (double)f;
                 }
@@ -669,124 +877,133 @@ k_project(const double* __restrict__ f0, const double* __restrict__ stats,
                 for (int k = 0; k < 4; ++k) lu[k] = lam[k];
             }
         }
-        if (lane == 0) {
-#pragma unroll
-            for (int k = 0; k < 4; ++k) C.lu[k] = lu[k];
-            C.flags = fl8;
-            C.status = status;
-            C.iters = iters;
-        }
-    }
-    __syncthreads();
 
-    // ---- apply_lambda_batch (exact elementwise order) + final NRMSE
-    const double lu0 = C.lu[0], lu1 = C.lu[1], lu2 = C.lu[2], lu3 = C.lu[3];
-    const double* ash = g.ash;
-    double sv[3] = {0.0, 0.0, 0.0};
-    if (SEP) {
-        // column-fixed threads: ash0, ash1, a3 and vol depend on (row edge,
-        // column) only, so the first two and the last product of t are two
-        // per-thread constants; the order of the additions is unchanged
-        const int cols = g.cols, rows = g.rows, ngrp = PJ_T / cols;
-        const int c = tid % cols, g0 = tid / cols;
-        if (g0 < ngrp) {
-            double P[2], Q[2], V[2];
+        // ---- apply_lambda_batch (exact elementwise order) + final NRMSE
+        const double lu0 = lu[0], lu1 = lu[1], lu2 = lu[2], lu3 = lu[3];
+        const double* ash = g.ash;
+        double sv0 = 0.0, sv1 = 0.0, sv2 = 0.0;
+        if (SEP) {
+            // a column's ash0, ash1, a3 and vol depend on (row edge, column)
+            // only: the first two products of t and the last are per-column
+            // constants, the additions keep the reference's order
+            for (int item = 0; item < 2; ++item) {
+                const bool act = item == 0 ? hasA : hasB;
+                if (!act) continue;
+                const int c = item == 0 ? lane : cB;
+                const int r0 = item == 0 ? 0 : rB0, r1 = item == 0 ? rows : rB1;
+                const bool ce = (c == 0) | (c == cols - 1);
+                double P[2], Q[2], V[2];
 #pragma unroll
-            for (int e = 0; e < 2; ++e) {
-                const int jj = (e == 0 && rows > 2 ? cols : 0) + c;  // row 1: interior; row 0: edge
-                const double dv = __dsub_rn(__ldg(g.vpar + jj), qs[1]);
-                const double a3 = __ddiv_rn(__dmul_rn(__ldg(g.hmvol + jj), __dmul_rn(dv, dv)), sc4);
-                P[e] = __dadd_rn(__dmul_rn(lu0, __ldg(ash + jj)), __dmul_rn(lu1, __ldg(ash + D + jj)));
-                Q[e] = __dmul_rn(lu3, a3);
-                V[e] = __ldg(g.vol + jj);
+                for (int e = 0; e < 2; ++e) {
+                    const int jj = (e == 0 && rows > 2 ? cols : 0) + c;  // row 1: interior; row 0: edge
+                    const double dv = __dsub_rn(__ldg(g.vpar + jj), qs[1]);
+                    const double a3 = __ddiv_rn(__dmul_rn(__ldg(g.hmvol + jj), __dmul_rn(dv, dv)),
+                                                sc4);
+                    P[e] = __dadd_rn(__dmul_rn(lu0, __ldg(ash + jj)),
+                                     __dmul_rn(lu1, __ldg(ash + D + jj)));
+                    Q[e] = __dmul_rn(lu3, a3);
+                    V[e] = __ldg(g.vol + jj);
+                }
+                const double vpc = __ldg(g.vpar + c);
+                const double* a2r = T + tb.a2c + (ce ? rows : 0);
+                for (int r = r0; r < r1; ++r) {
+                    const bool re = (r == 0) | (r == rows - 1);
+                    const int j = r * cols + c;
+                    double outv = F[j];
+                    if (top > 0) {
+                        double t = __dadd_rn(__dadd_rn(re ? P[1] : P[0], __dmul_rn(lu2, a2r[r])),
+                                             re ? Q[1] : Q[0]);
+                        t = t < -700.0 ? -700.0 : (t > 700.0 ? 700.0 : t);
+                        outv = __dmul_rn(outv, exp(-t));
+                    }
+                    F[j] = outv;
+                    const double d = __dsub_rn(O[j], outv);
+                    O[j] = __dmul_rn(d, d);
+                    const double fv = outv * (re ? V[1] : V[0]);
+                    sv0 += fv;
+                    sv1 += fv * vpc;
+                    sv2 += fv * T[tb.vp2 + r];
+                }
             }
-            const double vpc = __ldg(g.vpar + c);
-            for (int r = g0; r < rows; r += ngrp) {
-                const bool re = (r == 0) | (r == rows - 1);
-                const int j = r * cols + c;
+        } else {
+            for (int j = lane; j < D; j += 32) {
                 double outv = F[j];
                 if (top > 0) {
-                    double t = __dadd_rn(__dadd_rn(re ? P[1] : P[0],
+                    const double dv = __dsub_rn(__ldg(g.vpar + j), qs[1]);
+                    const double a3 =
+                        __ddiv_rn(__dmul_rn(__ldg(g.hmvol + j), __dmul_rn(dv, dv)), sc4);
+                    double t = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(lu0, __ldg(ash + j)),
+                                                             __dmul_rn(lu1, __ldg(ash + D + j))),
                                                    __dmul_rn(lu2, __ldg(ash + 2 * D + j))),
-                                         re ? Q[1] : Q[0]);
+                                         __dmul_rn(lu3, a3));
                     t = t < -700.0 ? -700.0 : (t > 700.0 ? 700.0 : t);
-                    outv = __dmul_rn(fmax(outv, fl), exp(-t));
+                    outv = __dmul_rn(outv, exp(-t));
                 }
                 F[j] = outv;
                 const double d = __dsub_rn(O[j], outv);
                 O[j] = __dmul_rn(d, d);
-                const double fv = outv * (re ? V[1] : V[0]);
-                sv[0] += fv;
-                sv[1] += fv * vpc;
-                sv[2] += fv * __ldg(g.vperp2 + j);
+                const double fv = outv * __ldg(g.vol + j);
+                sv0 += fv;
+                sv1 += fv * __ldg(g.vpar + j);
+                sv2 += fv * __ldg(g.vperp2 + j);
             }
         }
-    } else {
-        for (int j = tid; j < D; j += PJ_T) {
-            double outv = F[j];
-            if (top > 0) {
-                const double dv = __dsub_rn(__ldg(g.vpar + j), qs[1]);
-                const double a3 =
-                    __ddiv_rn(__dmul_rn(__ldg(g.hmvol + j), __dmul_rn(dv, dv)), sc4);
-                double t = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(lu0, __ldg(ash + j)),
-                                                         __dmul_rn(lu1, __ldg(ash + D + j))),
-                                               __dmul_rn(lu2, __ldg(ash + 2 * D + j))),
-                                     __dmul_rn(lu3, a3));
-                t = t < -700.0 ? -700.0 : (t > 700.0 ? 700.0 : t);
-                outv = __dmul_rn(fmax(outv, fl), exp(-t));
+        sv0 = wsum(sv0);
+        sv1 = wsum(sv1);
+        sv2 = wsum(sv2);
+        __syncwarp();
+        const double sse = warp_pairwise_sum(O, pw, leaf);
+        // O is free: stage the next image's original under the tail of this one
+        {
+            const int nxt = img + gridDim.x;
+            if (nxt < total) {
+                const int s1 = find_shard(shards, n_shards, nxt);
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                shift = stage_histogram(
+                    Obuf, shard_image(f0, shards[s1], nxt - shards[s1].img_off, D), D, &bar);
             }
-            F[j] = outv;
-            const double d = __dsub_rn(O[j], outv);
-            O[j] = __dmul_rn(d, d);  // each thread only reads/writes its own cells here
-            const double fv = outv * __ldg(g.vol + j);
-            sv[0] += fv;
-            sv[1] += fv * __ldg(g.vpar + j);
-            sv[2] += fv * __ldg(g.vperp2 + j);
         }
-    }
-    block_allsum(sv, C, ph);  // barrier: every d^2 is in O
-    const double sse = block_pairwise(O, pw, C);
-    unsigned fl8 = C.flags;
-    const double4 st = reinterpret_cast<const double4*>(stats)[img];
-    const double range = __dsub_rn(st.x, st.y);
-    const double rms = sqrt(__ddiv_rn(sse, (double)D));
-    const double ferr = range > 0 ? __ddiv_rn(rms, range) : (rms == 0.0 ? 0.0 : INFINITY);
-    if (!(ferr <= opt.tau)) fl8 |= MLK_F_EXC_GATE;
-    const bool exc = (fl8 & MLK_F_EXCEPTION) != 0;
+        const double4 st = reinterpret_cast<const double4*>(stats)[img];
+        const double range = __dsub_rn(st.x, st.y);
+        const double rms = sqrt(__ddiv_rn(sse, (double)D));
+        const double ferr = range > 0 ? __ddiv_rn(rms, range) : (rms == 0.0 ? 0.0 : INFINITY);
+        if (!(ferr <= opt.tau)) fl8 |= MLK_F_EXC_GATE;
+        const bool exc = (fl8 & MLK_F_EXCEPTION) != 0;
 
-    const double n = sv[0];
-    const double u = sv[1] / n;
-    double tl = 0.0;
-    if (!exc) {
-        double t1[1] = {0.0};
-        for (int j = tid; j < D; j += PJ_T) {
-            const double dv = __ldg(g.vpar + j) - u;
-            t1[0] += F[j] * __ldg(g.vol + j) * dv * dv;
+        const double n = sv0;
+        const double u = sv1 / n;
+        double tl = 0.0;
+        if (!exc) {
+            double t1 = 0.0;
+            for (int j = lane; j < D; j += 32) {
+                const double dv = __ldg(g.vpar + j) - u;
+                t1 += F[j] * __ldg(g.vol + j) * dv * dv;
+            }
+            tl = wsum(t1);
         }
-        block_allsum(t1, C, ph);
-        tl = t1[0];
-    }
-    if (tid == 0) {
-        flags[img] = (unsigned char)fl8;
-        status_out[img] = C.status;
-        iters_out[img] = C.iters;
-        ferr_out[img] = ferr;
-        double4* lo = reinterpret_cast<double4*>(lam_out) + img;
-        double4* qo = reinterpret_cast<double4*>(qst_out) + img;
-        double4* fo = reinterpret_cast<double4*>(fqoi_out) + img;
-        if (exc) {
-            *lo = make_double4(0.0, 0.0, 0.0, 0.0);
-            *qo = make_double4(0.0, 0.0, 0.0, 0.0);
-            *fo = q4;
-            fsse_out[img] = 0.0;
-        } else {
-            *lo = make_double4(lu0, lu1, lu2, lu3);
-            *qo = make_double4(qs[0], qs[1], qs[2], qs[3]);
-            const double nan = __longlong_as_double(0x7ff8000000000000ll);
-            *fo = n > 0 ? make_double4(n, u, hm * sv[2] / n, hm * tl / n)
-                        : make_double4(n, nan, nan, nan);
-            fsse_out[img] = sse;
+        if (lane == 0) {
+            flags[img] = (unsigned char)fl8;
+            status_out[img] = status;
+            iters_out[img] = iters;
+            ferr_out[img] = ferr;
+            double4* lo = reinterpret_cast<double4*>(lam_out) + img;
+            double4* qo = reinterpret_cast<double4*>(qst_out) + img;
+            double4* fo = reinterpret_cast<double4*>(fqoi_out) + img;
+            if (exc) {
+                *lo = make_double4(0.0, 0.0, 0.0, 0.0);
+                *qo = make_double4(0.0, 0.0, 0.0, 0.0);
+                *fo = q4;
+                fsse_out[img] = 0.0;
+            } else {
+                *lo = make_double4(lu0, lu1, lu2, lu3);
+                *qo = make_double4(qs[0], qs[1], qs[2], qs[3]);
+                const double nan = __longlong_as_double(0x7ff8000000000000ll);
+                *fo = n > 0 ? make_double4(n, u, hm * sv2 / n, hm * tl / n)
+                            : make_double4(n, nan, nan, nan);
+                fsse_out[img] = sse;
+            }
         }
+        __syncwarp();
     }
 }
 
@@ -828,15 +1045,26 @@ extern "C" int mlk_project(const double* f0, const double* stats, const double* 
     const int D = grid_h->D;
     if (D > MLK_MAX_D || L < 1 || L > MLK_MAXL) return MLK_ERR_DIM;
     PwPlan pw = mlk_make_pw_plan(D);
-    const size_t sm = (size_t)(((D + 3) / 2) * 2 + D) * sizeof(double);
-    const bool sep = grid_h->sep && grid_h->rows <= 64 && grid_h->cols <= 64 && grid_h->cols > 0;
+    const bool sep = grid_h->sep && grid_h->rows <= PW_MAXRC && grid_h->cols <= PW_MAXRC &&
+                     grid_h->cols > 0 && grid_h->rows >= 2;
+    const size_t sm = (size_t)warp_slice_doubles(D, grid_h->rows, grid_h->cols) * sizeof(double);
+    if (sm > 200 * 1024) return MLK_ERR_DIM;
     const MlkNewton opt = *opts_h;
-#define MLK_PJ_LAUNCH(SEP)                                                                     \
-    cudaFuncSetAttribute(k_project<SEP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); \
-    k_project<SEP><<<total, PJ_T, sm, stream>>>(                                               \
-        f0, stats, qoi, shards, n_shards, *grid_h, pw, W, L, cents, K, codes, sel_rank,         \
-        slot_base, opt, flags, lam, qst, status, iters, ferr, fqoi, fsse, varint,               \
-        (long long)varint_cap, reinterpret_cast<long long*>(varint_len), err_flag)
+    int dev = 0, n_sm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+#define MLK_PJ_LAUNCH(SEP)                                                                      \
+    do {                                                                                        \
+        cudaFuncSetAttribute(k_project_w<SEP>, cudaFuncAttributeMaxDynamicSharedMemorySize,     \
+                             (int)sm);                                                          \
+        int per_sm = 1;                                                                         \
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_project_w<SEP>, 32, sm);      \
+        const int grid = (int)std::min<long long>(total, (long long)n_sm * std::max(per_sm, 1)); \
+        k_project_w<SEP><<<grid, 32, sm, stream>>>(                                             \
+            f0, stats, qoi, shards, n_shards, total, *grid_h, pw, W, L, cents, K, codes,        \
+            sel_rank, slot_base, opt, flags, lam, qst, status, iters, ferr, fqoi, fsse, varint,  \
+            (long long)varint_cap, reinterpret_cast<long long*>(varint_len), err_flag);         \
+    } while (0)
     if (sep) {
         MLK_PJ_LAUNCH(true);
     } else {

@@ -612,7 +612,7 @@ def compress_device(f0: torch.Tensor, specs, dgrid: DeviceGrid, cfg, timer: Time
     cents = T("cents", (S, L, K), torch.float32)
     kinfo = T("kinfo", (S, L, 4), i32)
     call("mlk_kmeans", lat_km, shf_d, ctypes.addressof(table_full), S, L, K, first_d, draws_d,
-         scratch, cents, kinfo)
+         scratch, cents, None, kinfo)
 
     timer.mark("find_eb")
     codes = T("codes", (total, L), torch.uint8)

@@ -1,4 +1,8 @@
-"""Error metrics and the report type (reference qoi.py:79-162)."""
+"""Moments, error metrics and the report type (reference qoi.py).
+
+compute_qoi / compute_qoi_batch run on the device (mlk_compare); the
+pipeline computes the moments inside its stage kernels.
+"""
 
 from __future__ import annotations
 
@@ -8,7 +12,67 @@ import numpy as np
 
 from .errors import DegenerateRangeError, DimensionError
 
-__all__ = ["ErrorReport", "nrmse", "compression_ratio", "qoi_nrmse_from_moments"]
+__all__ = ["ErrorReport", "QoISet", "compute_qoi", "compute_qoi_batch", "nrmse",
+           "compression_ratio", "qoi_nrmse_from_moments"]
+
+
+@dataclass(frozen=True)
+class QoISet:
+    """Per-(plane, node) moments; ratio entries are NaN where n == 0 (qoi.py:30-40)."""
+
+    n: np.ndarray
+    u_par: np.ndarray
+    t_perp: np.ndarray
+    t_par: np.ndarray
+
+    def defined_mask(self) -> np.ndarray:
+        return self.n > 0
+
+
+def _moments_device(images: np.ndarray, grid) -> np.ndarray:
+    """(N, 4) moments of a (N, rows, cols) stack on the device (mlk_compare's
+    moment pass, the compute_qoi_batch formulas of qoi.py:60-76)."""
+    import torch
+
+    from . import _ops
+    from ._lib import call
+    from .pipeline import _device_grid
+    n = images.shape[0]
+    d = grid.rows * grid.cols
+    dv = _ops.dev()
+    x = _ops.to_dev(images.reshape(n, d))
+    f64 = dict(dtype=torch.float64, device=dv)
+    err, sse, q, ext = (torch.empty(n, **f64), torch.empty(n, **f64),
+                        torch.empty((n, 4), **f64), torch.empty((n, 2), **f64))
+    call("mlk_compare", x, x, n, _device_grid(grid, dv, 4).addr, err, sse, q, None, ext)
+    return q.cpu().numpy()
+
+
+def compute_qoi(image: np.ndarray, grid):
+    """Moments of one histogram: (n, u_par, t_perp, t_par), NaN ratios where
+    n <= 0 (qoi.py:42-57); computed on the device."""
+    image = np.asarray(image, dtype=np.float64)
+    if image.shape != (grid.rows, grid.cols):
+        raise DimensionError(f"image shape {image.shape} does not match grid "
+                             f"({grid.rows}, {grid.cols})")
+    q = _moments_device(image[None], grid)[0]
+    n = float(q[0])
+    if n <= 0.0:
+        return n, float("nan"), float("nan"), float("nan")
+    return n, float(q[1]), float(q[2]), float(q[3])
+
+
+def compute_qoi_batch(images: np.ndarray, grid) -> QoISet:
+    """Moments of a (N, rows, cols) stack (qoi.py:60-76), on the device."""
+    images = np.asarray(images, dtype=np.float64)
+    if images.shape[1:] != (grid.rows, grid.cols):
+        raise DimensionError("image stack does not match the grid")
+    if images.shape[0] == 0:
+        z = np.zeros(0)
+        return QoISet(n=z, u_par=z.copy(), t_perp=z.copy(), t_par=z.copy())
+    q = _moments_device(images, grid)
+    return QoISet(n=q[:, 0].copy(), u_par=q[:, 1].copy(), t_perp=q[:, 2].copy(),
+                  t_par=q[:, 3].copy())
 
 
 def nrmse(u, f) -> float:
