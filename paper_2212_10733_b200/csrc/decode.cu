@@ -87,7 +87,7 @@ k_decode(const MlkShard* __restrict__ shards, int n_shards, int total, MlkGrid g
                                        __dmul_rn(l2, __ldg(g.ash + 2 * D + j))),
                              __dmul_rn(l3, a3));
         t = t < -700.0 ? -700.0 : (t > 700.0 ? 700.0 : t);
-        y[j] = __dmul_rn(np_max2(c, fl), exp(-t));
+        y[j] = __dmul_rn(np_max2(c, fl), mlk_exp(-t));
     }
 }
 

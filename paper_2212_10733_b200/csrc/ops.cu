@@ -152,7 +152,7 @@ k_apply_lambda_rows(const double* __restrict__ f, int D, const double* __restric
                                        __dmul_rn(l2, ai[2 * D + j])),
                              __dmul_rn(l3, ai[3 * D + j]));
         if (t == t) t = t < -700.0 ? -700.0 : (t > 700.0 ? 700.0 : t);
-        oi[j] = __dmul_rn(fp, exp(-t));
+        oi[j] = __dmul_rn(fp, mlk_exp(-t));
     }
 }
 

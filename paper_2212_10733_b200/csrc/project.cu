@@ -1,6 +1,6 @@
 // project.cu -- residual coding + Lagrange QoI projection + final PD gate.
 //
-// One CTA (128 threads) per histogram.  Replaces, per image,
+// Replaces, per image,
 // pipeline.py:239-292:
 //   * residual q = rint(r / 2eb), zigzag, LEB128 (residual.py:60-79,
 //     _ckernels.pyx:143-171) for selected images -- the varint stream goes
@@ -13,12 +13,9 @@
 //     reference's exact elementwise order, the final per-image NRMSE in
 //     numpy's pairwise order and the tau gate (pipeline.py:284-292).
 //
-// Shared memory holds two histogram-sized buffers (the TMA-staged original,
-// later the squared errors; the working image) so 6-7 CTAs fit an SM.  The
-// Newton iteration is split: every thread accumulates its cells' 14 sums,
-// a warp reduce-scatter + one shared-memory pass combine them, and warp 0
-// alone solves the 4x4 system, updates lambda and (separable grids) the
-// exponent tables for the next iteration.  Two barriers per iteration.
+// The kernel is k_project_s below (one warp per histogram, one image buffer;
+// its header explains the layout).  k_newton_batch at the end serves the
+// reference's per-image operator API (kernels.newton_solve).
 #include "common.cuh"
 
 #include <algorithm>
@@ -65,50 +62,6 @@ __device__ __forceinline__ void block_allsum(double (&v)[NV], PjCtl& C, int& ph)
         v[k] = t;
     }
     ph ^= 1;
-}
-
-// NaN-propagating max of two values over the block
-__device__ __forceinline__ void block_allmax2(double& a, double& b, PjCtl& C, int& ph) {
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        a = np_max2(a, __shfl_xor_sync(FULL, a, o));
-        b = np_max2(b, __shfl_xor_sync(FULL, b, o));
-    }
-    if (lane == 0) {
-        C.red[ph][w][0] = a;
-        C.red[ph][w][1] = b;
-    }
-    __syncthreads();
-    a = C.red[ph][0][0];
-    b = C.red[ph][0][1];
-#pragma unroll
-    for (int q = 1; q < PJ_W; ++q) {
-        a = np_max2(a, C.red[ph][q][0]);
-        b = np_max2(b, C.red[ph][q][1]);
-    }
-    ph ^= 1;
-}
-
-__device__ __forceinline__ int block_exscan_int(int v, int* total, PjCtl& C) {
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    int inc = v;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        int t = __shfl_up_sync(FULL, inc, o);
-        if (lane >= o) inc += t;
-    }
-    __syncthreads();
-    if (lane == 31) C.iscan[w] = inc;
-    __syncthreads();
-    int base = 0, tot = 0;
-#pragma unroll
-    for (int q = 0; q < PJ_W; ++q) {
-        if (q < w) base += C.iscan[q];
-        tot += C.iscan[q];
-    }
-    *total = tot;
-    return base + inc - v;
 }
 
 // 16 per-lane values -> lane l holds the warp sum of value l >> 1
@@ -271,226 +224,68 @@ __device__ int newton_generic(const double* fp, const double* __restrict__ a, in
     return status;
 }
 
-// ---------------------------------------------------------------------------
-// Separable exponent (trapezoid make_grid grids, fdata.py:151-167): every
-// feature row carries vol, so t = vol_rc * (A_c + B_r) with
-//   A_c = l0/s0 + l1 vpar_c/s1 + l3 hm (vpar_c - u)^2/s4,  B_r = l2 hm vperp_r^2/s2,
-// and vol_rc takes one of 4 values set by (row edge, col edge).  exp(-t)
-// is then ea[row edge][c] * eb[col edge][r]: 2 (rows + cols) exps per
-// iteration instead of rows * cols.  Only the Newton iterate uses it
-// (tolerance-level, like the reference's own summation order); the stored
-// image uses the exact per-cell formula.
-
-__device__ __forceinline__ double cls_val(const double (&w)[4], bool re, bool ce) {
-    return re ? (ce ? w[3] : w[2]) : (ce ? w[1] : w[0]);
-}
-
-struct NtCtx {
-    double w[4];  // vol by class (2 re + ce)
-    double is0, is4, u;
-    int rows, cols;
-};
-
-// Exponent tables for lam, entries spread over the block; returns true
-// (warp-uniform) when this warp saw some |t| that could exceed the
-// reference's +-700 clamp (that iteration is then evaluated cell by cell).
-__device__ __forceinline__ bool sep_tables(const double (&lam)[4], const NtCtx& X, PjCtl& C) {
-    const int rows = X.rows, cols = X.cols;
-    bool big = false;
-    for (int q = threadIdx.x; q < 2 * (rows + cols); q += PJ_T) {
-        double x;
-        if (q < 2 * cols) {
-            const int re = q >= cols, c = q - re * cols;
-            const bool ce = (c == 0) | (c == cols - 1);
-            x = cls_val(X.w, re, ce) * (lam[0] * X.is0 + lam[1] * C.vp1[c] + lam[3] * C.p3c[c]);
-            C.ea[re][c] = exp(-x);
-        } else {
-            const int q2 = q - 2 * cols;
-            const int ce = q2 >= rows, r = q2 - ce * rows;
-            const bool re = (r == 0) | (r == rows - 1);
-            x = cls_val(X.w, re, ce) * (lam[2] * C.p2r[r]);
-            C.eb[ce][r] = exp(-x);
-        }
-        if (!(fabs(x) <= 349.0)) big = true;
-    }
-    return __any_sync(FULL, big);
-}
-
-// The block's Newton iteration for one image.  All threads call it.  Every
-// warp combines the per-warp partial sums and takes the (identical) Newton
-// step itself, so lambda never needs a broadcast; the next iteration's
-// exponent tables are computed by the whole block.  Two barriers per step.
-template <bool SEP>
-__device__ void newton_block(const double* fp, double fl, const MlkGrid& g, const NtCtx& X,
-                             const double* b,
-                             double bmax, double step, int max_iter, double tol, PjCtl& C,
-                             double (&lam)[4], int& status, int& iters) {
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int D = g.D, rows = X.rows, cols = X.cols;
-    (void)rows;
-    bool clamped = false;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) lam[k] = 0.0;
-    status = MLK_NEWTON_MAX_ITER;
-    iters = max_iter;
-    if (SEP) {
-        const bool big = sep_tables(lam, X, C);
-        if (lane == 0) C.big[warp] = big;
-    }
-    __syncthreads();
-    for (int it = 0;; ++it) {
-        bool direct = !SEP;
-        if (SEP) {
-#pragma unroll
-            for (int q = 0; q < PJ_W; ++q) direct |= C.big[q] != 0;
-        }
-        double v[16];
-#pragma unroll
-        for (int k = 0; k < 16; ++k) v[k] = 0.0;
-        if (SEP && !direct) {
-            // thread = (row group, column): exp(-t) = ea[re][c] eb[ce][r] and
-            // a_k = w * p_k with w the class volume, so with the column fixed
-            // the 14 sums factor into 5 row accumulations per thread
-            const int ngrp = PJ_T / cols, c = tid % cols, g0 = tid / cols;
-            if (g0 < ngrp) {
-                const bool ce = (c == 0) | (c == cols - 1);
-                const double ea0 = C.ea[0][c], ea1 = C.ea[1][c];
-                const double w_in = cls_val(X.w, false, ce), w_ed = cls_val(X.w, true, ce);
-                const double* ebp = C.eb[ce];
-                double G1 = 0.0, G2 = 0.0, H1 = 0.0, H2 = 0.0, H3 = 0.0;
-                for (int r = g0; r < rows; r += ngrp) {
-                    const bool re = (r == 0) | (r == rows - 1);
-                    const double w = re ? w_ed : w_in;
-                    const double wf = w * (fmax(fp[r * cols + c], fl) * (re ? ea1 : ea0) * ebp[r]);
-                    const double p2 = C.p2r[r];
-                    const double w2f = w * wf, t2 = p2 * w2f;
-                    G1 += wf;
-                    G2 = fma(p2, wf, G2);
-                    H1 += w2f;
-                    H2 += t2;
-                    H3 = fma(p2, t2, H3);
-                }
-                const double q0 = X.is0, q1 = C.vp1[c], q3 = C.p3c[c];
-                v[0] = q0 * G1; v[1] = q1 * G1; v[2] = G2; v[3] = q3 * G1;
-                v[4] = q0 * q0 * H1; v[5] = q0 * q1 * H1; v[6] = q0 * H2; v[7] = q0 * q3 * H1;
-                v[8] = q1 * q1 * H1; v[9] = q1 * H2; v[10] = q1 * q3 * H1;
-                v[11] = H3; v[12] = q3 * H2; v[13] = q3 * q3 * H1;
-            }
-        } else {
-            const double l0 = lam[0], l1 = lam[1], l2 = lam[2], l3 = lam[3];
-            for (int j = tid; j < D; j += PJ_T) {
-                const double a0 = __ldg(g.ash + j), a1 = __ldg(g.ash + D + j),
-                             a2 = __ldg(g.ash + 2 * D + j);
-                const double dv = __ldg(g.vpar + j) - X.u;
-                const double a3 = __ldg(g.hmvol + j) * dv * dv * X.is4;
-                double t = l0 * a0 + l1 * a1 + l2 * a2 + l3 * a3;
-                if (fabs(t) > 700.0) { v[14] = 1.0; t = t > 0 ? 700.0 : -700.0; }
-                cell_sums(v, a0, a1, a2, a3, fmax(fp[j], fl) * exp(-t));
-            }
-        }
-        const double part = warp_rs16(v);
-        if (!(lane & 1)) C.part[warp][lane >> 1] = part;
-        __syncthreads();
-        double tot = 0.0;
-        if (lane < 16) {
-            tot = C.part[0][lane];
-#pragma unroll
-            for (int q = 1; q < PJ_W; ++q) tot += C.part[q][lane];
-        }
-        double sums[15];
-#pragma unroll
-        for (int k = 0; k < 15; ++k) sums[k] = __shfl_sync(FULL, tot, k);
-        if (!newton_step(sums, b, bmax, step, max_iter, tol, it, lam, clamped, status, iters))
-            break;  // block-uniform: every warp saw the same sums
-        if (SEP) {
-            const bool big = sep_tables(lam, X, C);
-            if (lane == 0) C.big[warp] = big;
-        }
-        __syncthreads();
-    }
-}
-
 __device__ __forceinline__ int varint_len(unsigned long long z) {
     return z == 0ull ? 1 : (64 - __clzll(z) + 6) / 7;
 }
 
-// exact numpy pairwise sum of v[0..n) by the whole block: thread (leaf,
-// accumulator) pairs run the 8 strided accumulators, the ((r0+r1)+(r2+r3))+
-// ((r4+r5)+(r6+r7)) tree runs over 8-lane groups, thread 0 combines leaves.
-__device__ double block_pairwise(const double* v, const PwPlan& pw, PjCtl& C) {
-    const int tid = threadIdx.x, a = tid & 7;
-    for (int l0 = 0; l0 < pw.n_leaves; l0 += PJ_T / 8) {
-        const int l = l0 + (tid >> 3);
-        int st = 0, len = 0;
-        if (l < pw.n_leaves) { st = pw.start[l]; len = pw.len[l]; }
-        const int lim = len - (len % 8);
-        double r = 0.0;
-        if (len >= 8) {
-            r = v[st + a];
-            for (int i = a + 8; i < lim; i += 8) r = __dadd_rn(r, v[st + i]);
-        }
-        r = __dadd_rn(r, __shfl_down_sync(FULL, r, 1));
-        r = __dadd_rn(r, __shfl_down_sync(FULL, r, 2));
-        r = __dadd_rn(r, __shfl_down_sync(FULL, r, 4));
-        if (a == 0 && l < pw.n_leaves) {
-            double s = 0.0;
-            int i = 0;
-            if (len >= 8) { s = r; i = lim; }
-            for (; i < len; ++i) s = __dadd_rn(s, v[st + i]);
-            C.leaf[l] = s;
-        }
-    }
-    __syncthreads();
-    if (tid == 0) C.bval = pw_combine_ops(C.leaf, pw);
-    __syncthreads();
-    return C.bval;
-}
-
 // ===========================================================================
-// k_project_w: ONE WARP per histogram, persistent.  Each warp owns a private
-// slice of shared memory (the TMA-staged original O, the working image F and
-// its Newton tables) and walks images img = blockIdx.x, + gridDim.x, ...; the
-// bulk copy of the next image's original is issued as soon as the current
-// one's final NRMSE has consumed O, so it lands under the next image's AE
-// decode.  No block barriers: every reduction is a warp shuffle, the 4x4
-// Newton solve runs once per warp (warp-uniform), and the Newton sums use a
-// lane-per-column layout (lane c owns column c; the columns past 31 are split
-// into row groups over the lanes) with the interior rows factorised out of
-// the per-cell work:
-//   per interior cell: m = F * eb[r];  S0 += m;  S1 += p2_r m;  S2 += p2_r^2 m
-// (the column's exp(-w A_c), the volume class and the column factors of the
-// 14 sums are applied once per column).
+// k_project_s: ONE WARP per histogram, persistent, ONE image-sized buffer.
+//
+// The original O is not kept in shared memory: each warp issues an L2 bulk
+// prefetch (cp.async.bulk.prefetch.L2) of its NEXT image when it starts the
+// current one, so by the time it gets there O is L2-resident.  Then
+//   * non-selected images: F = AE decode, straight from the codes;
+//   * selected images (the residual stage): O is bulk-copied (TMA) into F's
+//     buffer and replaced in place by recon + q * 2eb (the recon recomputed
+//     per cell, exactly as decode_cell gives it);
+//   * the exact apply reads O again from L2 for d = O - final.
+// One 12 KB buffer instead of two doubles the warps an SM holds.  The final
+// NRMSE is gated on a fast sum of d^2 (lane partials + shuffles) with a
+// rigorous bound against numpy's pairwise sum; only when the gate decision
+// is inside that bound are the d^2 rewritten into F and summed in the exact
+// pairwise order (the report keeps the fast value, relative error < 1e-14).
+//
+// Layout of the separable Newton sums and of the apply: lane c owns column c
+// (c < 32); the columns past 31 are split into row groups over the lanes.
+// Per Newton evaluation a lane sums its interior cells as
+//     S0 += F * R0[r],  S1 += F * R1[r],  S2 += F * R2[r]
+// with per-iteration row tables R0 = exp(-w B_r), R1 = R0 p2_r, R2 = R0 p2_r^2
+// (the column's exp(-w A_c), volume class and factors are applied once per
+// column), and the edge rows separately.  The 4x4 solve runs once per warp.
+constexpr int PS_MAXRC = 64;     // rows, cols <= 64 on the separable path
+constexpr int PS_MAXS = 64;      // shard offsets cached in shared memory
 
-constexpr int PW_MAXRC = 64;   // rows, cols <= 64 on the separable path
-
-struct WarpTabs {              // offsets (doubles) of the per-warp tables
-    int ea, eb, vp1, p3c, p2r, p2s, a2c, vp2, n;
+struct PsTabs {                  // offsets (doubles) of the per-warp tables
+    int ea, rt, vp1, p3c, p2r, p2s, a2c, vp2, leaf, n;
 };
 
-__host__ __device__ inline WarpTabs warp_tabs(int rows, int cols) {
-    WarpTabs t;
+__host__ __device__ inline PsTabs ps_tabs(int rows, int cols, int n_leaves) {
+    PsTabs t;
     int o = 0;
-    t.ea = o; o += 2 * cols;    // exp(-w(re, ce_c) A_c)        [re][c]
-    t.eb = o; o += 2 * rows;    // exp(-w(re_r, ce) B_r)        [ce][r]
-    t.vp1 = o; o += cols;       // vpar_c / s1                  (grid)
-    t.p3c = o; o += cols;       // hm (vpar_c - u)^2 / s4       (image)
-    t.p2r = o; o += rows;       // hm vperp2_r / s2             (grid)
-    t.p2s = o; o += rows;       // p2r^2                        (grid)
-    t.a2c = o; o += 2 * rows;   // ash row 2 by (col edge, row) (grid, exact table values)
-    t.vp2 = o; o += rows;       // vperp2_r                     (grid)
+    t.ea = o; o += 2 * cols;    // exp(-w(re, ce_c) A_c)                 [re][c]
+    t.rt = o; o += 6 * rows;    // R0/R1/R2 row tables by column edge    [ce][r][3]
+    t.vp1 = o; o += cols;       // vpar_c / s1                           (grid)
+    t.p3c = o; o += cols;       // hm (vpar_c - u)^2 / s4                (image)
+    t.p2r = o; o += rows;       // hm vperp2_r / s2                      (grid)
+    t.p2s = o; o += rows;       // p2r^2                                 (grid)
+    t.a2c = o; o += 2 * rows;   // ash row 2 by (col edge, row): exact table values
+    t.vp2 = o; o += rows;       // vperp2_r                              (grid)
+    t.leaf = o; o += n_leaves;  // pairwise leaves (exact NRMSE fallback)
     t.n = (o + 1) & ~1;
     return t;
 }
 
-// per-warp shared memory: O (D + 2), F (D, even), tables, pairwise leaves
-__host__ __device__ inline int warp_slice_doubles(int D, int rows, int cols) {
-    return ((D + 3) / 2) * 2 + ((D + 1) / 2) * 2 + warp_tabs(rows, cols).n + MLK_PW_MAX_LEAVES;
+// per-warp shared memory: the image buffer (D + 2) and the tables
+__host__ __device__ inline int ps_warp_doubles(int D, int rows, int cols, int n_leaves) {
+    return ((D + 3) / 2) * 2 + ps_tabs(rows, cols, n_leaves).n;
 }
 
-__device__ __forceinline__ double wsum(double v) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
-    return v;
+__device__ __forceinline__ void prefetch_l2_histogram(const double* x, int D) {
+    const unsigned long long a = reinterpret_cast<unsigned long long>(x);
+    const int shift = (int)((a & 15ull) >> 3);
+    const unsigned bytes = (unsigned)(((D + shift) * 8 + 15) & ~15);
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(x - shift), "r"(bytes)
+                 : "memory");
 }
 
 // the 14 Newton sums of one column from its five factorised accumulators
@@ -503,39 +298,98 @@ __device__ __forceinline__ void add_column(double (&v)[16], double q0, double q1
     v[11] += H3; v[12] += q3 * H2; v[13] += q3 * q3 * H1;
 }
 
-// Newton tables for lam (one warp); true when some exponent could pass the
-// reference's +-700 clamp (that iteration is then evaluated cell by cell)
-__device__ __forceinline__ bool warp_tables(const double (&lam)[4], const double (&w)[4],
-                                            double is0, int rows, int cols, double* T,
-                                            const WarpTabs& tb) {
+__device__ __forceinline__ double cls_val(const double (&w)[4], bool re, bool ce) {
+    return re ? (ce ? w[3] : w[2]) : (ce ? w[1] : w[0]);
+}
+
+// Newton tables for lam; returns true (warp-uniform) when some exponent
+// could pass the reference's +-700 clamp (the iteration then goes cell by cell)
+__device__ __forceinline__ bool ps_tables(const double (&lam)[4], const double (&w)[4],
+                                          double is0, int rows, int cols, double* T,
+                                          const PsTabs& tb) {
     const int lane = threadIdx.x & 31;
     bool big = false;
     for (int q = lane; q < 2 * (rows + cols); q += 32) {
-        double x;
         if (q < 2 * cols) {
             const int re = q >= cols, c = q - re * cols;
             const bool ce = (c == 0) | (c == cols - 1);
-            x = cls_val(w, re, ce) * (lam[0] * is0 + lam[1] * T[tb.vp1 + c] + lam[3] * T[tb.p3c + c]);
-            T[tb.ea + q] = exp(-x);
+            const double x = cls_val(w, re, ce) * (lam[0] * is0 + lam[1] * T[tb.vp1 + c] +
+                                                   lam[3] * T[tb.p3c + c]);
+            if (!(fabs(x) <= 349.0)) big = true;
+            T[tb.ea + q] = mlk_exp(-fmax(fmin(x, 700.0), -700.0));
         } else {
             const int q2 = q - 2 * cols;
             const int ce = q2 >= rows, r = q2 - ce * rows;
             const bool re = (r == 0) | (r == rows - 1);
-            x = cls_val(w, re, ce) * (lam[2] * T[tb.p2r + r]);
-            T[tb.eb + q2] = exp(-x);
+            const double x = cls_val(w, re, ce) * (lam[2] * T[tb.p2r + r]);
+            if (!(fabs(x) <= 349.0)) big = true;
+            const double e = mlk_exp(-fmax(fmin(x, 700.0), -700.0));
+            double* rt = T + tb.rt + 3 * q2;
+            rt[0] = e;
+            rt[1] = e * T[tb.p2r + r];
+            rt[2] = e * T[tb.p2s + r];
         }
-        if (!(fabs(x) <= 349.0)) big = true;
     }
     __syncwarp();
     return __any_sync(FULL, big);
 }
 
+struct PsItem {
+    bool act;
+    int c, r0, r1;   // column, rows [r0, r1)
+    bool ce;         // column edge
+};
+
+// one item's five factorised accumulators
+__device__ __forceinline__ void item_sums(const double* F, const PsItem& it, int rows, int cols,
+                                          const double (&w)[4], const double* T,
+                                          const PsTabs& tb, double& G1, double& G2, double& H1,
+                                          double& H2, double& H3) {
+    const int c = it.c;
+    const double* rt = T + tb.rt + (it.ce ? 3 * rows : 0);
+    double S0 = 0.0, S1 = 0.0, S2 = 0.0, U0 = 0.0, U1 = 0.0, U2 = 0.0;
+    const int ri0 = it.r0 > 0 ? it.r0 : 1;
+    const int ri1 = it.r1 < rows - 1 ? it.r1 : rows - 1;
+    int r = ri0;
+    for (; r + 1 < ri1; r += 2) {  // two rows per step: independent chains
+        const double f0 = F[r * cols + c], f1 = F[(r + 1) * cols + c];
+        const double* a = rt + 3 * r;
+        S0 = fma(f0, a[0], S0); S1 = fma(f0, a[1], S1); S2 = fma(f0, a[2], S2);
+        U0 = fma(f1, a[3], U0); U1 = fma(f1, a[4], U1); U2 = fma(f1, a[5], U2);
+    }
+    if (r < ri1) {
+        const double f0 = F[r * cols + c];
+        const double* a = rt + 3 * r;
+        S0 = fma(f0, a[0], S0); S1 = fma(f0, a[1], S1); S2 = fma(f0, a[2], S2);
+    }
+    S0 += U0; S1 += U1; S2 += U2;
+    double E0 = 0.0, E1 = 0.0, E2 = 0.0;
+    if (it.r0 == 0) {
+        const double f0 = F[c];
+        E0 = f0 * rt[0]; E1 = f0 * rt[1]; E2 = f0 * rt[2];
+    }
+    if (it.r1 == rows && rows > 1) {
+        const int rl = rows - 1;
+        const double f0 = F[rl * cols + c];
+        const double* a = rt + 3 * rl;
+        E0 = fma(f0, a[0], E0); E1 = fma(f0, a[1], E1); E2 = fma(f0, a[2], E2);
+    }
+    const double w_in = cls_val(w, false, it.ce), w_ed = cls_val(w, true, it.ce);
+    const double ai = w_in * T[tb.ea + c], ae = w_ed * T[tb.ea + cols + c];
+    G1 = ai * S0 + ae * E0;
+    G2 = ai * S1 + ae * E1;
+    H1 = w_in * ai * S0 + w_ed * ae * E0;
+    H2 = w_in * ai * S1 + w_ed * ae * E1;
+    H3 = w_in * ai * S2 + w_ed * ae * E2;
+}
+
 // one warp's Newton iteration (_ckernels.pyx:62-137 semantics via newton_step)
 template <bool SEP>
-__device__ void newton_warp(const double* F, const MlkGrid& g, const double (&w)[4], double is0,
-                            double is4, double u, const double* b, double bmax, double step,
-                            int max_iter, double tol, double* T, const WarpTabs& tb,
-                            double (&lam)[4], int& status, int& iters) {
+__device__ void newton_ps(const double* F, const MlkGrid& g, const double (&w)[4], double is0,
+                          double is4, double u, const double* b, double bmax, double step,
+                          int max_iter, double tol, double* T, const PsTabs& tb,
+                          const PsItem& iA, const PsItem& iB, double (&lam)[4], int& status,
+                          int& iters) {
     const int lane = threadIdx.x & 31;
     const int D = g.D, rows = g.rows, cols = g.cols;
     bool clamped = false;
@@ -543,68 +397,20 @@ __device__ void newton_warp(const double* F, const MlkGrid& g, const double (&w)
     for (int k = 0; k < 4; ++k) lam[k] = 0.0;
     status = MLK_NEWTON_MAX_ITER;
     iters = max_iter;
-    // the lane's columns: A = column `lane` (all rows), B = one row group of
-    // a column past 31
-    const int nA = cols < 32 ? cols : 32;
-    const int nx = cols > 32 ? cols - 32 : 0;
-    const int grp = nx ? 32 / nx : 0;
-    const bool hasA = lane < nA, hasB = nx && lane < nx * grp;
-    const int cB = hasB ? 32 + lane % nx : 0, gB = hasB ? lane / nx : 0;
-    const int rB0 = hasB ? gB * rows / grp : 0, rB1 = hasB ? (gB + 1) * rows / grp : 0;
-    bool big = SEP ? warp_tables(lam, w, is0, rows, cols, T, tb) : true;
+    bool big = SEP ? ps_tables(lam, w, is0, rows, cols, T, tb) : true;
     for (int it = 0;; ++it) {
         double v[16];
 #pragma unroll
         for (int k = 0; k < 16; ++k) v[k] = 0.0;
         if (SEP && !big) {
-            const double* p2r = T + tb.p2r;
-            const double* p2s = T + tb.p2s;
-            if (hasA) {
-                const int c = lane;
-                const bool ce = (c == 0) | (c == cols - 1);
-                const double* ebp = T + tb.eb + ce * rows;
-                const double w_in = cls_val(w, false, ce), w_ed = cls_val(w, true, ce);
-                double S0 = 0.0, S1 = 0.0, S2 = 0.0, U0 = 0.0, U1 = 0.0, U2 = 0.0;
-                int r = 1;
-                // two rows per step: independent accumulator chains
-                for (; r + 1 < rows - 1; r += 2) {
-                    const double m0 = F[r * cols + c] * ebp[r];
-                    const double m1 = F[(r + 1) * cols + c] * ebp[r + 1];
-                    S0 += m0; S1 = fma(p2r[r], m0, S1); S2 = fma(p2s[r], m0, S2);
-                    U0 += m1; U1 = fma(p2r[r + 1], m1, U1); U2 = fma(p2s[r + 1], m1, U2);
-                }
-                for (; r < rows - 1; ++r) {
-                    const double m0 = F[r * cols + c] * ebp[r];
-                    S0 += m0; S1 = fma(p2r[r], m0, S1); S2 = fma(p2s[r], m0, S2);
-                }
-                S0 += U0; S1 += U1; S2 += U2;
-                const int rl = rows - 1;
-                const double e0 = F[c] * ebp[0], e1 = F[rl * cols + c] * ebp[rl];
-                const double E0 = e0 + e1, E1 = p2r[0] * e0 + p2r[rl] * e1,
-                             E2 = p2s[0] * e0 + p2s[rl] * e1;
-                const double ai = w_in * T[tb.ea + c], ae = w_ed * T[tb.ea + cols + c];
-                const double G1 = ai * S0 + ae * E0, G2 = ai * S1 + ae * E1;
-                const double H1 = w_in * ai * S0 + w_ed * ae * E0;
-                const double H2 = w_in * ai * S1 + w_ed * ae * E1;
-                const double H3 = w_in * ai * S2 + w_ed * ae * E2;
-                add_column(v, is0, T[tb.vp1 + c], T[tb.p3c + c], G1, G2, H1, H2, H3);
+            double G1, G2, H1, H2, H3;
+            if (iA.act) {
+                item_sums(F, iA, rows, cols, w, T, tb, G1, G2, H1, H2, H3);
+                add_column(v, is0, T[tb.vp1 + iA.c], T[tb.p3c + iA.c], G1, G2, H1, H2, H3);
             }
-            if (hasB) {
-                const int c = cB;
-                const bool ce = (c == 0) | (c == cols - 1);
-                const double* ebp = T + tb.eb + ce * rows;
-                const double w_in = cls_val(w, false, ce), w_ed = cls_val(w, true, ce);
-                const double ea0 = T[tb.ea + c], ea1 = T[tb.ea + cols + c];
-                double G1 = 0.0, G2 = 0.0, H1 = 0.0, H2 = 0.0, H3 = 0.0;
-                for (int r = rB0; r < rB1; ++r) {
-                    const bool re = (r == 0) | (r == rows - 1);
-                    const double ww = re ? w_ed : w_in;
-                    const double wf = ww * (F[r * cols + c] * (re ? ea1 : ea0) * ebp[r]);
-                    const double w2f = ww * wf, t2 = p2r[r] * w2f;
-                    G1 += wf; G2 = fma(p2r[r], wf, G2);
-                    H1 += w2f; H2 += t2; H3 = fma(p2r[r], t2, H3);
-                }
-                add_column(v, is0, T[tb.vp1 + c], T[tb.p3c + c], G1, G2, H1, H2, H3);
+            if (iB.act) {
+                item_sums(F, iB, rows, cols, w, T, tb, G1, G2, H1, H2, H3);
+                add_column(v, is0, T[tb.vp1 + iB.c], T[tb.p3c + iB.c], G1, G2, H1, H2, H3);
             }
         } else {
             const double l0 = lam[0], l1 = lam[1], l2 = lam[2], l3 = lam[3];
@@ -615,7 +421,7 @@ __device__ void newton_warp(const double* F, const MlkGrid& g, const double (&w)
                 const double a3 = __ldg(g.hmvol + j) * dv * dv * is4;
                 double t = l0 * a0 + l1 * a1 + l2 * a2 + l3 * a3;
                 if (fabs(t) > 700.0) { v[14] = 1.0; t = t > 0 ? 700.0 : -700.0; }
-                cell_sums(v, a0, a1, a2, a3, F[j] * exp(-t));
+                cell_sums(v, a0, a1, a2, a3, F[j] * mlk_exp(-t));
             }
         }
         const double part = warp_rs16(v);   // lane l: warp sum of value l >> 1
@@ -624,13 +430,13 @@ __device__ void newton_warp(const double* F, const MlkGrid& g, const double (&w)
         for (int k = 0; k < 15; ++k) sums[k] = __shfl_sync(FULL, part, 2 * k);
         if (!newton_step(sums, b, bmax, step, max_iter, tol, it, lam, clamped, status, iters))
             break;  // warp-uniform: every lane holds the same sums
-        if (SEP) big = warp_tables(lam, w, is0, rows, cols, T, tb);
+        if (SEP) big = ps_tables(lam, w, is0, rows, cols, T, tb);
     }
 }
 
 template <bool SEP>
-__global__ void __launch_bounds__(32)
-k_project_w(const double* __restrict__ f0, const double* __restrict__ stats,
+__global__ void __launch_bounds__(32, 13)
+k_project_s(const double* __restrict__ f0, const double* __restrict__ stats,
             const double* __restrict__ qoi, const MlkShard* __restrict__ shards, int n_shards,
             int total, MlkGrid g, PwPlan pw, const float* __restrict__ W, int L,
             const float* __restrict__ cents, int K, const unsigned char* __restrict__ codes,
@@ -642,18 +448,37 @@ k_project_w(const double* __restrict__ f0, const double* __restrict__ stats,
             unsigned char* __restrict__ varint, long long vcap, long long* __restrict__ vlen,
             int* __restrict__ err_flag) {
     __shared__ unsigned long long bar;
+    __shared__ int s_off[PS_MAXS + 1];
     extern __shared__ __align__(16) double sm[];
     const int D = g.D, rows = g.rows, cols = g.cols;
     const int lane = threadIdx.x;
-    double* Obuf = sm;                        // TMA target: the original, later d^2
-    double* F = sm + ((D + 3) / 2) * 2;       // recon -> corrected -> f_plus -> final
-    double* T = F + ((D + 1) / 2) * 2;        // Newton / apply tables
-    const WarpTabs tb = warp_tabs(rows, cols);
-    double* leaf = T + tb.n;
+    double* Fbuf = sm;                         // the image buffer (D + 2 doubles)
+    double* T = sm + ((D + 3) / 2) * 2;        // tables
+    const PsTabs tb = ps_tabs(rows, cols, pw.n_leaves);
+    double* leaf = T + tb.leaf;
     const double hm = 0.5 * g.mass;
     double w[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) w[k] = g.vcls[k];
+    // the lane's columns: A = column `lane` (all rows), B = one row group of
+    // a column past 31
+    PsItem iA, iB;
+    {
+        const int nA = cols < 32 ? cols : 32;
+        const int nx = cols > 32 ? cols - 32 : 0;
+        const int grp = nx ? 32 / nx : 0;
+        iA.act = SEP && lane < nA;
+        iA.c = lane;
+        iA.r0 = 0;
+        iA.r1 = rows;
+        iA.ce = (iA.c == 0) | (iA.c == cols - 1);
+        iB.act = SEP && nx && lane < nx * grp;
+        iB.c = iB.act ? 32 + lane % nx : 0;
+        const int gB = iB.act ? lane / nx : 0;
+        iB.r0 = iB.act ? gB * rows / grp : 0;
+        iB.r1 = iB.act ? (gB + 1) * rows / grp : 0;
+        iB.ce = (iB.c == 0) | (iB.c == cols - 1);
+    }
     if (SEP) {  // grid-constant tables, once per warp
         for (int c = lane; c < cols; c += 32) T[tb.vp1 + c] = g.vpar[c] / g.s1;
         const int cin = cols > 2 ? 1 : 0;
@@ -661,34 +486,42 @@ k_project_w(const double* __restrict__ f0, const double* __restrict__ stats,
             const double p2 = hm * g.vperp2[r * cols] / g.s2;
             T[tb.p2r + r] = p2;
             T[tb.p2s + r] = p2 * p2;
-            T[tb.a2c + r] = __ldg(g.ash + 2 * D + r * cols + cin);          // interior column
-            T[tb.a2c + rows + r] = __ldg(g.ash + 2 * D + r * cols);         // edge column
+            T[tb.a2c + r] = __ldg(g.ash + 2 * D + r * cols + cin);   // interior column
+            T[tb.a2c + rows + r] = __ldg(g.ash + 2 * D + r * cols);  // edge column
             T[tb.vp2 + r] = g.vperp2[r * cols];
         }
     }
+    const bool cache_sh = n_shards <= PS_MAXS;
+    if (cache_sh)
+        for (int q = lane; q <= n_shards; q += 32)
+            s_off[q] = q < n_shards ? shards[q].img_off : 0x7fffffff;
     if (lane == 0) mbar_init(&bar, 1);
     __syncwarp();
+    auto shard_of = [&](int im) {
+        if (!cache_sh) return find_shard(shards, n_shards, im);
+        int q = 0;
+        while (s_off[q + 1] <= im) ++q;
+        return q;
+    };
     unsigned phase = 0;
     int img = blockIdx.x;
-    int shift = 0;
-    if (img < total) {
-        const int s0 = find_shard(shards, n_shards, img);
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        shift = stage_histogram(Obuf, shard_image(f0, shards[s0], img - shards[s0].img_off, D),
-                                D, &bar);
+    if (img < total && lane == 0) {
+        const int s0 = shard_of(img);
+        prefetch_l2_histogram(shard_image(f0, shards[s0], img - shards[s0].img_off, D), D);
     }
-    // the lane's columns for the apply pass (same split as the Newton sums)
-    const int nA = cols < 32 ? cols : 32;
-    const int nx = cols > 32 ? cols - 32 : 0;
-    const int grp = nx ? 32 / nx : 0;
-    const bool hasA = lane < nA, hasB = nx && lane < nx * grp;
-    const int cB = hasB ? 32 + lane % nx : 0, gB = hasB ? lane / nx : 0;
-    const int rB0 = hasB ? gB * rows / grp : 0, rB1 = hasB ? (gB + 1) * rows / grp : 0;
 
     for (; img < total; img += gridDim.x) {
-        const int s = find_shard(shards, n_shards, img);
+        const int s = shard_of(img);
         const MlkShard sh = shards[s];
-        // ---- AE decode into F while the original is in flight
+        const double* Og = shard_image(f0, sh, img - sh.img_off, D);
+        {   // the next image of this warp into L2 while this one is processed
+            const int nxt = img + gridDim.x;
+            if (nxt < total && lane == 0) {
+                const int s1 = shard_of(nxt);
+                prefetch_l2_histogram(shard_image(f0, shards[s1], nxt - shards[s1].img_off, D),
+                                      D);
+            }
+        }
         double z[MLK_MAXL];
 #pragma unroll
         for (int k = 0; k < MLK_MAXL; ++k)
@@ -696,25 +529,36 @@ k_project_w(const double* __restrict__ f0, const double* __restrict__ stats,
                          : 0.0;
         const float* Ws = W + sh.w_off;
         const bool blas_tree = !sh.small_blas;
-        for (int j = lane; j < D; j += 32)
-            F[j] = decode_cell(z, Ws, L, D, j, blas_tree && g.tree_cols[j], sh.mean, sh.std);
         const double4 q4 = reinterpret_cast<const double4*>(qoi)[img];
         double qs[4] = {q4.x, q4.y, q4.z, q4.w};
         if (opt.lam_f32) {
 #pragma unroll
             for (int k = 0; k < 4; ++k) qs[k] = (double)__double2float_rn(qs[k]);
         }
-        mbar_wait(&bar, phase);
-        phase ^= 1;
-        const double* Oc = Obuf + shift;
-        double* O = Obuf + shift;
-        (void)Oc;
-        __syncwarp();
-
-        // ---- residual stage (selected images): contiguous cells per lane so
-        //      the varint stream is written in cell order after one warp scan
         const int rank = sel_rank[img];
-        if (rank >= 0) {  // warp-uniform
+        double* F;
+        double tmax = -INFINITY;
+        bool nan_t = false;
+        if (rank < 0) {  // warp-uniform
+            // ---- F = AE decode (autoencoder.py:106-110)
+            F = Fbuf;
+            for (int j = lane; j < D; j += 32) {
+                const double fj =
+                    decode_cell(z, Ws, L, D, j, blas_tree && g.tree_cols[j], sh.mean, sh.std);
+                F[j] = fj;
+                nan_t |= fj != fj;
+                tmax = fmax(tmax, fj);
+            }
+        } else {
+            // ---- residual stage (residual.py:60-79, 194-203): O into the
+            //      buffer, replaced in place by recon + q 2eb; contiguous cells
+            //      per lane so the varint stream is written in cell order
+            __syncwarp();
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            const int shift = stage_histogram(Fbuf, Og, D, &bar);
+            F = Fbuf + shift;
+            mbar_wait(&bar, phase);
+            phase ^= 1;
             const double eb2 = 2.0 * sh.eb;
             const double inv = 1.0 / eb2;
             const bool lossless = sh.lossless != 0;
@@ -723,7 +567,9 @@ k_project_w(const double* __restrict__ f0, const double* __restrict__ stats,
             int nb = 0;
             bool too_big = false;
             for (int j = c0; j < c1; ++j) {
-                const double r = __dsub_rn(O[j], F[j]);
+                const double rc =
+                    decode_cell(z, Ws, L, D, j, blas_tree && g.tree_cols[j], sh.mean, sh.std);
+                const double r = __dsub_rn(F[j], rc);
                 unsigned long long zz;
                 if (lossless) {
                     zz = (unsigned long long)__double_as_longlong(r);
@@ -747,17 +593,23 @@ k_project_w(const double* __restrict__ f0, const double* __restrict__ stats,
             const long long slot = slot_base[s] + rank;
             unsigned char* out = varint + slot * vcap;
             for (int j = c0; j < c1; ++j) {
-                const double r = __dsub_rn(O[j], F[j]);
+                const double rc =
+                    decode_cell(z, Ws, L, D, j, blas_tree && g.tree_cols[j], sh.mean, sh.std);
+                const double r = __dsub_rn(F[j], rc);
                 unsigned long long zz;
+                double fj;
                 if (lossless) {
                     zz = (unsigned long long)__double_as_longlong(r);
-                    F[j] = __dadd_rn(F[j], r);
+                    fj = __dadd_rn(rc, r);
                 } else {
                     const double q = qround(r, eb2, inv);
                     const long long qi = (long long)q;
                     zz = ((unsigned long long)qi << 1) ^ (unsigned long long)(qi >> 63);
-                    F[j] = __dadd_rn(F[j], __dmul_rn(q, eb2));
+                    fj = __dadd_rn(rc, __dmul_rn(q, eb2));
                 }
+                F[j] = fj;
+                nan_t |= fj != fj;
+                tmax = fmax(tmax, fj);
                 while (zz >= 0x80ull) {
                     out[pos++] = (unsigned char)(zz | 0x80ull);
                     zz >>= 7;
@@ -765,20 +617,13 @@ k_project_w(const double* __restrict__ f0, const double* __restrict__ stats,
                 out[pos++] = (unsigned char)zz;
             }
             if (lane == 0) vlen[slot] = tot;
-            __syncwarp();
         }
 
-        // ---- stored QoIs (pipeline.py:254-260) and the per-image system:
-        //      top = max(corrected), s4 = max |a3| (lagrange.py:199-204)
-        double top = -INFINITY, amax = 0.0;
-        bool nan_t = false, nan_a = false;  // numpy max propagates NaN
-        for (int j = lane; j < D; j += 32) {
-            const double fj = F[j];
-            nan_t |= fj != fj;
-            top = fmax(top, fj);
-        }
+        // ---- top = max(corrected), s4 = max |a3| (lagrange.py:199-204),
+        //      NaN-propagating like numpy's max
+        double amax = 0.0;
+        bool nan_a = false;
         if (SEP) {
-            // a3 = hmvol * (vpar - u)^2 takes one value per (row edge, column)
             for (int c = lane; c < cols; c += 32) {
                 const double dv = __dsub_rn(__ldg(g.vpar + c), qs[1]);
                 const double dv2 = __dmul_rn(dv, dv);
@@ -800,22 +645,36 @@ k_project_w(const double* __restrict__ f0, const double* __restrict__ stats,
                 amax = fmax(amax, a3);
             }
         }
-        if (__any_sync(FULL, nan_t)) top = __longlong_as_double(0x7ff8000000000000ll);
+        if (__any_sync(FULL, nan_t)) tmax = __longlong_as_double(0x7ff8000000000000ll);
         if (__any_sync(FULL, nan_a)) amax = __longlong_as_double(0x7ff8000000000000ll);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
-            top = np_max2(top, __shfl_xor_sync(FULL, top, o));
+            tmax = np_max2(tmax, __shfl_xor_sync(FULL, tmax, o));
             amax = np_max2(amax, __shfl_xor_sync(FULL, amax, o));
         }
-        const double s4 = amax;
+        const double top = tmax, s4 = amax;
         const double sc4 = s4 > 0 ? s4 : 1.0;
-        // f_plus = max(corrected, floor * top) (lagrange.py:103-107); top > 0
-        // excludes NaN, and the apply below reads the same f_plus
+        __syncwarp();  // F complete (the residual pass wrote other lanes' cells)
+        // f_plus = max(corrected, floor * top) (lagrange.py:103-107) in place;
+        // top > 0 excludes NaN.  Separable: each lane rewrites the cells it
+        // reads from here on (its columns).
         const double fl = top > 0 ? __dmul_rn(opt.floor, top) : 0.0;
         if (top > 0) {
-            for (int j = lane; j < D; j += 32) {
-                const double fj = F[j];
-                F[j] = fj < fl ? fl : fj;
+            if (SEP) {
+#pragma unroll
+                for (int q = 0; q < 2; ++q) {
+                    const PsItem& it = q ? iB : iA;
+                    if (!it.act) continue;
+                    for (int r = it.r0; r < it.r1; ++r) {
+                        const double fj = F[r * cols + it.c];
+                        F[r * cols + it.c] = fj < fl ? fl : fj;
+                    }
+                }
+            } else {
+                for (int j = lane; j < D; j += 32) {
+                    const double fj = F[j];
+                    F[j] = fj < fl ? fl : fj;
+                }
             }
         }
         if (SEP) {
@@ -836,13 +695,13 @@ k_project_w(const double* __restrict__ f0, const double* __restrict__ stats,
             for (int k = 0; k < 4; ++k) bmax = fmax(bmax, fabs(b[k]));
             if (bmax > 0.0 && isfinite(bmax)) {
                 const double is0 = 1.0 / g.s0, is4 = 1.0 / s4;
-                newton_warp<SEP>(F, g, w, is0, is4, qs[1], b, bmax, opt.step, opt.max_iter,
-                                 opt.tol, T, tb, lam, status, iters);
+                newton_ps<SEP>(F, g, w, is0, is4, qs[1], b, bmax, opt.step, opt.max_iter,
+                               opt.tol, T, tb, iA, iB, lam, status, iters);
                 if (opt.retry && status == MLK_NEWTON_MAX_ITER) {
                     double lam2[4];
                     int st2 = 0, it2 = 0;
-                    newton_warp<SEP>(F, g, w, is0, is4, qs[1], b, bmax, opt.retry_step,
-                                     opt.retry_max_iter, opt.tol, T, tb, lam2, st2, it2);
+                    newton_ps<SEP>(F, g, w, is0, is4, qs[1], b, bmax, opt.retry_step,
+                                   opt.retry_max_iter, opt.tol, T, tb, iA, iB, lam2, st2, it2);
                     if (st2 == MLK_NEWTON_CONVERGED) {
 #pragma unroll
                         for (int k = 0; k < 4; ++k) lam[k] = lam2[k];
@@ -878,20 +737,17 @@ k_project_w(const double* __restrict__ f0, const double* __restrict__ stats,
             }
         }
 
-        // ---- apply_lambda_batch (exact elementwise order) + final NRMSE
+        // ---- apply_lambda_batch (exact elementwise order, lagrange.py:152-185),
+        //      the final moments and the fast sum of d^2 (O read from L2)
         const double lu0 = lu[0], lu1 = lu[1], lu2 = lu[2], lu3 = lu[3];
         const double* ash = g.ash;
-        double sv0 = 0.0, sv1 = 0.0, sv2 = 0.0;
+        double sv0 = 0.0, sv1 = 0.0, sv2 = 0.0, ssf = 0.0;
         if (SEP) {
-            // a column's ash0, ash1, a3 and vol depend on (row edge, column)
-            // only: the first two products of t and the last are per-column
-            // constants, the additions keep the reference's order
-            for (int item = 0; item < 2; ++item) {
-                const bool act = item == 0 ? hasA : hasB;
-                if (!act) continue;
-                const int c = item == 0 ? lane : cB;
-                const int r0 = item == 0 ? 0 : rB0, r1 = item == 0 ? rows : rB1;
-                const bool ce = (c == 0) | (c == cols - 1);
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                const PsItem& it = q ? iB : iA;
+                if (!it.act) continue;
+                const int c = it.c;
                 double P[2], Q[2], V[2];
 #pragma unroll
                 for (int e = 0; e < 2; ++e) {
@@ -905,20 +761,21 @@ k_project_w(const double* __restrict__ f0, const double* __restrict__ stats,
                     V[e] = __ldg(g.vol + jj);
                 }
                 const double vpc = __ldg(g.vpar + c);
-                const double* a2r = T + tb.a2c + (ce ? rows : 0);
-                for (int r = r0; r < r1; ++r) {
+                const double* a2r = T + tb.a2c + (it.ce ? rows : 0);
+                for (int r = it.r0; r < it.r1; ++r) {
                     const bool re = (r == 0) | (r == rows - 1);
                     const int j = r * cols + c;
+                    const double o = __ldg(Og + j);
                     double outv = F[j];
                     if (top > 0) {
                         double t = __dadd_rn(__dadd_rn(re ? P[1] : P[0], __dmul_rn(lu2, a2r[r])),
                                              re ? Q[1] : Q[0]);
                         t = t < -700.0 ? -700.0 : (t > 700.0 ? 700.0 : t);
-                        outv = __dmul_rn(outv, exp(-t));
+                        outv = __dmul_rn(outv, mlk_exp(-t));
                     }
                     F[j] = outv;
-                    const double d = __dsub_rn(O[j], outv);
-                    O[j] = __dmul_rn(d, d);
+                    const double d = __dsub_rn(o, outv);
+                    ssf = fma(d, d, ssf);
                     const double fv = outv * (re ? V[1] : V[0]);
                     sv0 += fv;
                     sv1 += fv * vpc;
@@ -927,6 +784,7 @@ k_project_w(const double* __restrict__ f0, const double* __restrict__ stats,
             }
         } else {
             for (int j = lane; j < D; j += 32) {
+                const double o = __ldg(Og + j);
                 double outv = F[j];
                 if (top > 0) {
                     const double dv = __dsub_rn(__ldg(g.vpar + j), qs[1]);
@@ -937,50 +795,64 @@ k_project_w(const double* __restrict__ f0, const double* __restrict__ stats,
                                                    __dmul_rn(lu2, __ldg(ash + 2 * D + j))),
                                          __dmul_rn(lu3, a3));
                     t = t < -700.0 ? -700.0 : (t > 700.0 ? 700.0 : t);
-                    outv = __dmul_rn(outv, exp(-t));
+                    outv = __dmul_rn(outv, mlk_exp(-t));
                 }
                 F[j] = outv;
-                const double d = __dsub_rn(O[j], outv);
-                O[j] = __dmul_rn(d, d);
+                const double d = __dsub_rn(o, outv);
+                ssf = fma(d, d, ssf);
                 const double fv = outv * __ldg(g.vol + j);
                 sv0 += fv;
                 sv1 += fv * __ldg(g.vpar + j);
                 sv2 += fv * __ldg(g.vperp2 + j);
             }
         }
-        sv0 = wsum(sv0);
-        sv1 = wsum(sv1);
-        sv2 = wsum(sv2);
-        __syncwarp();
-        const double sse = warp_pairwise_sum(O, pw, leaf);
-        // O is free: stage the next image's original under the tail of this one
-        {
-            const int nxt = img + gridDim.x;
-            if (nxt < total) {
-                const int s1 = find_shard(shards, n_shards, nxt);
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                shift = stage_histogram(
-                    Obuf, shard_image(f0, shards[s1], nxt - shards[s1].img_off, D), D, &bar);
+        const double n = warp_sum(sv0);
+        const double u = warp_sum(sv1) / n;
+        const double n2 = warp_sum(sv2);
+        double sse = warp_sum(ssf);
+        // T_par numerator over the own cells (kept only when not an exception)
+        double t1 = 0.0;
+        if (SEP) {
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                const PsItem& it = q ? iB : iA;
+                if (!it.act) continue;
+                const int c = it.c;
+                const double dv = __ldg(g.vpar + c) - u;
+                const double dv2 = dv * dv;
+                const double vi = __ldg(g.vol + (rows > 2 ? cols : 0) + c), ve = __ldg(g.vol + c);
+                for (int r = it.r0; r < it.r1; ++r) {
+                    const bool re = (r == 0) | (r == rows - 1);
+                    t1 += F[r * cols + c] * (re ? ve : vi) * dv2;
+                }
             }
-        }
-        const double4 st = reinterpret_cast<const double4*>(stats)[img];
-        const double range = __dsub_rn(st.x, st.y);
-        const double rms = sqrt(__ddiv_rn(sse, (double)D));
-        const double ferr = range > 0 ? __ddiv_rn(rms, range) : (rms == 0.0 ? 0.0 : INFINITY);
-        if (!(ferr <= opt.tau)) fl8 |= MLK_F_EXC_GATE;
-        const bool exc = (fl8 & MLK_F_EXCEPTION) != 0;
-
-        const double n = sv0;
-        const double u = sv1 / n;
-        double tl = 0.0;
-        if (!exc) {
-            double t1 = 0.0;
+        } else {
             for (int j = lane; j < D; j += 32) {
                 const double dv = __ldg(g.vpar + j) - u;
                 t1 += F[j] * __ldg(g.vol + j) * dv * dv;
             }
-            tl = wsum(t1);
         }
+        const double tl = warp_sum(t1);
+        const double4 st4 = reinterpret_cast<const double4*>(stats)[img];
+        const double range = __dsub_rn(st4.x, st4.y);
+        double ferr = range > 0 ? sqrt(sse / (double)D) / range : (sse == 0.0 ? 0.0 : INFINITY);
+        // numpy's pairwise order decides only when the fast sum (|rel err| <
+        // (D + 16) u with u = 2^-53, against < (log2 D + 8) u for the pairwise
+        // sum) cannot: within 1e-12 relative of tau
+        if (range > 0 && isfinite(ferr) &&
+            fabs(ferr - opt.tau) <= 1e-12 * opt.tau + 2.0 * (double)(D + 64) * 0x1p-53 * ferr) {
+            __syncwarp();
+            for (int j = lane; j < D; j += 32) {
+                const double d = __dsub_rn(__ldg(Og + j), F[j]);
+                F[j] = __dmul_rn(d, d);
+            }
+            __syncwarp();
+            sse = warp_pairwise_sum(F, pw, leaf);
+            const double rms = sqrt(__ddiv_rn(sse, (double)D));
+            ferr = __ddiv_rn(rms, range);
+        }
+        if (!(ferr <= opt.tau)) fl8 |= MLK_F_EXC_GATE;
+        const bool exc = (fl8 & MLK_F_EXCEPTION) != 0;
         if (lane == 0) {
             flags[img] = (unsigned char)fl8;
             status_out[img] = status;
@@ -998,7 +870,7 @@ k_project_w(const double* __restrict__ f0, const double* __restrict__ stats,
                 *lo = make_double4(lu0, lu1, lu2, lu3);
                 *qo = make_double4(qs[0], qs[1], qs[2], qs[3]);
                 const double nan = __longlong_as_double(0x7ff8000000000000ll);
-                *fo = n > 0 ? make_double4(n, u, hm * sv2 / n, hm * tl / n)
+                *fo = n > 0 ? make_double4(n, u, hm * n2 / n, hm * tl / n)
                             : make_double4(n, nan, nan, nan);
                 fsse_out[img] = sse;
             }
@@ -1045,9 +917,10 @@ extern "C" int mlk_project(const double* f0, const double* stats, const double* 
     const int D = grid_h->D;
     if (D > MLK_MAX_D || L < 1 || L > MLK_MAXL) return MLK_ERR_DIM;
     PwPlan pw = mlk_make_pw_plan(D);
-    const bool sep = grid_h->sep && grid_h->rows <= PW_MAXRC && grid_h->cols <= PW_MAXRC &&
+    const bool sep = grid_h->sep && grid_h->rows <= PS_MAXRC && grid_h->cols <= PS_MAXRC &&
                      grid_h->cols > 0 && grid_h->rows >= 2;
-    const size_t sm = (size_t)warp_slice_doubles(D, grid_h->rows, grid_h->cols) * sizeof(double);
+    const size_t sm =
+        (size_t)ps_warp_doubles(D, grid_h->rows, grid_h->cols, pw.n_leaves) * sizeof(double);
     if (sm > 200 * 1024) return MLK_ERR_DIM;
     const MlkNewton opt = *opts_h;
     int dev = 0, n_sm = 148;
@@ -1055,12 +928,12 @@ extern "C" int mlk_project(const double* f0, const double* stats, const double* 
     cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
 #define MLK_PJ_LAUNCH(SEP)                                                                      \
     do {                                                                                        \
-        cudaFuncSetAttribute(k_project_w<SEP>, cudaFuncAttributeMaxDynamicSharedMemorySize,     \
+        cudaFuncSetAttribute(k_project_s<SEP>, cudaFuncAttributeMaxDynamicSharedMemorySize,     \
                              (int)sm);                                                          \
         int per_sm = 1;                                                                         \
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_project_w<SEP>, 32, sm);      \
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_project_s<SEP>, 32, sm);      \
         const int grid = (int)std::min<long long>(total, (long long)n_sm * std::max(per_sm, 1)); \
-        k_project_w<SEP><<<grid, 32, sm, stream>>>(                                             \
+        k_project_s<SEP><<<grid, 32, sm, stream>>>(                                             \
             f0, stats, qoi, shards, n_shards, total, *grid_h, pw, W, L, cents, K, codes,        \
             sel_rank, slot_base, opt, flags, lam, qst, status, iters, ferr, fqoi, fsse, varint,  \
             (long long)varint_cap, reinterpret_cast<long long*>(varint_len), err_flag);         \

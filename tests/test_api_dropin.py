@@ -332,9 +332,13 @@ def test_compute_qoi_matches_reference_moments():
     grid = G.grid()
     q = qoi.compute_qoi_batch(a["nr_o"], grid)
     got = np.stack([q.n, q.u_par, q.t_perp, q.t_par], axis=1)
-    np.testing.assert_allclose(got, a["qoi"], rtol=1e-12, atol=1e-300)
+    # u_par cancels to ~1e-2 of the thermal speed: summation-order noise is
+    # absolute there (~1e-16), relative everywhere else
+    np.testing.assert_allclose(got[:, [0, 2, 3]], a["qoi"][:, [0, 2, 3]], rtol=1e-12)
+    np.testing.assert_allclose(got[:, 1], a["qoi"][:, 1], rtol=1e-12, atol=1e-14)
     for i in range(3):
-        assert mb.compute_qoi(a["nr_o"][i], grid) == pytest.approx(tuple(a["qoi"][i]), rel=1e-12)
+        want = tuple(a["qoi"][i])
+        assert mb.compute_qoi(a["nr_o"][i], grid) == pytest.approx(want, rel=1e-12, abs=1e-14)
 
 
 @gpu
