@@ -316,14 +316,20 @@ int mlk_probe_bins(const double* f0, const MlkShard* shards, int32_t n_shards,
  * the final gate.  Per image: lam (cast; 0 for exceptions), qst (stored
  * QoIs; 0 for exceptions), status, iters, flags |= EXC_*, ferr (final
  * NRMSE), fqoi (moments of the final image), fsse (sum of squared final
- * errors).  *err_flag = MLK_ERR_CONFIG when |q| >= 2**62 (residual.py:67). */
+ * errors).  *err_flag = MLK_ERR_CONFIG when |q| >= 2**62 (residual.py:67).
+ * img_list (device, n_list entries) restricts the launch to those images
+ * (NULL: all `total`), so the images without residuals can be projected
+ * while the error-bound search of the others is still running;
+ * ctas_per_sm > 0 caps the resident one-warp CTAs per SM (0: occupancy max)
+ * to leave room for kernels on other streams. */
 int mlk_project(const double* f0, const double* stats, const double* qoi,
                 const MlkShard* shards, int32_t n_shards, int32_t total, const MlkGrid* grid_h,
                 const float* W, int32_t L, const float* cents, int32_t K, const uint8_t* codes,
                 const int32_t* sel_rank, const int32_t* slot_base, const MlkNewton* opts_h,
                 uint8_t* flags, double* lam, double* qst, int32_t* status, int32_t* iters,
                 double* ferr, double* fqoi, double* fsse, uint8_t* varint, int64_t varint_cap,
-                int64_t* varint_len, int32_t* err_flag, cudaStream_t stream);
+                int64_t* varint_len, int32_t* err_flag, const int32_t* img_list,
+                int32_t n_list, int32_t ctas_per_sm, cudaStream_t stream);
 
 /* Decode path (pipeline.py:397-427) for all images of all shards: recon from
  * codes; + residual (res_slot[img] >= 0: D zigzag codes at res_codes +
@@ -399,6 +405,11 @@ int mlk_host_exception_entries(uint8_t* dst, const double* src, const int64_t* s
  * pipeline.py:287). */
 int mlk_list_flags(const uint8_t* flags, const MlkShard* shards, int32_t n_shards, uint32_t mask,
                    int32_t* list, int32_t* count, cudaStream_t stream);
+
+/* the images of [0, total) with (flags & mask) != 0 into `set` and the rest
+ * into `clear`, both ascending; *n_set = the size of `set` (device). */
+int mlk_split_flags(const uint8_t* flags, int32_t total, uint32_t mask, int32_t* set,
+                    int32_t* clear, int32_t* n_set, cudaStream_t stream);
 
 /* residual section entries (pipeline.py:132-137): for payload e of shard
  * entry_shard[e] at out + dst_off[e]: <II> (index, 13 + zlen) then the

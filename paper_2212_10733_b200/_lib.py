@@ -8,6 +8,7 @@ torch CUDA tensors (plumbing only); all compute happens in the library.
 from __future__ import annotations
 
 import ctypes
+import os
 import functools
 from pathlib import Path
 
@@ -16,7 +17,8 @@ import torch
 from .errors import (BackendError, ConfigError, DimensionError, FormatError,
                      SizeMismatchError)
 
-LIB_PATH = Path(__file__).resolve().parent / "libmlk_b200.so"
+LIB_PATH = Path(os.environ.get("MLK_B200_LIB") or
+               Path(__file__).resolve().parent / "libmlk_b200.so")
 
 F_SELECTED, F_NONFINITE, F_RECHECK = 1, 2, 4
 F_EXC_NEWTON, F_EXC_OVERFLOW, F_EXC_GATE = 8, 16, 32
@@ -98,7 +100,8 @@ _SIGS = {
                   _I32, _I32, _I32, _P, _P, _P, _P],
     "mlk_probe_bins": [_P, _P, _I32, _P, _P, _I32, _P, _I32, _P, _P, _P, _I32, _P, _P, _P],
     "mlk_project": [_P, _P, _P, _P, _I32, _I32, _P, _P, _I32, _P, _I32, _P, _P, _P, _P, _P,
-                    _P, _P, _P, _P, _P, _P, _P, _P, _I64, _P, _P, _P],
+                    _P, _P, _P, _P, _P, _P, _P, _P, _I64, _P, _P, _P, _I32, _I32, _P],
+    "mlk_split_flags": [_P, _I32, ctypes.c_uint32, _P, _P, _P, _P],
     "mlk_list_flags": [_P, _P, _I32, ctypes.c_uint32, _P, _P, _P],
     "mlk_pack_residuals": [_P, _P, _P, _P, _P, _P, _P, _P, _I32, _I32, _I32, _P, _P],
     "mlk_pack_lambdas": [_P, _P, _P, _I32, _I32, _P, _I32, _P, _P],

@@ -457,6 +457,19 @@ __device__ __forceinline__ int match_len_upto(const uint8_t* win, int p, int c, 
 }
 
 
+// match_len_upto(win, p, c, 0, cap) with the first 16 bytes of the scan
+// string window[p..] already in registers (s0, s1: the same for every
+// candidate of a longest_match call), and the second 8 bytes compared only
+// when the first 8 all match (most candidates end within them)
+__device__ __forceinline__ int match_len_first(const uint8_t* win, int p, int c, int cap,
+                                               unsigned long long s0, unsigned long long s1) {
+    const unsigned long long x = s0 ^ load8(win, c);
+    if (x) return (__ffsll((long long)x) - 1) >> 3;
+    const unsigned long long y = s1 ^ load8(win, c + 8);
+    if (y) return 8 + ((__ffsll((long long)y) - 1) >> 3);
+    return cap <= 16 ? 16 : match_len_upto(win, p, c, 16, cap);
+}
+
 // ---- Huffman construction (trees.c build_tree / gen_bitlen / gen_codes),
 // warp-cooperative where the result does not depend on order.  The heap is
 // the serial part; its entries carry the comparison key with the node id
@@ -912,12 +925,14 @@ k_deflate_warp(const uint8_t* __restrict__ in, const long long* __restrict__ in_
                 const int thr = nice > prev_length + 1 ? nice : prev_length + 1;
                 int best = prev_length, bstart = match_start;
                 int cb = hash_head;  // first candidate of the round
+                const unsigned long long s0 = wz::load8(win, strstart),
+                                         s1 = wz::load8(win, strstart + 8);
                 for (int r = 0; r < chain; r += 32) {
                     const int c = wz::jump(p1, p4, cb, lane);
                     const bool valid = c != 0 && r + lane < chain;
                     // lengths up to thr (exact below it), then the exact length of
                     // the first candidate reaching thr -- the one that ends the search
-                    int len = valid ? wz::match_len_upto(win, strstart, c, 0, thr) : 0;
+                    int len = valid ? wz::match_len_first(win, strstart, c, thr, s0, s1) : 0;
                     const unsigned hit = __ballot_sync(FULL, valid && len >= thr);
                     const int upto = hit ? __ffs(hit) - 1 : 31;
                     if (hit && lane == upto)

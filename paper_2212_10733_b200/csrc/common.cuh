@@ -155,14 +155,32 @@ __device__ __forceinline__ const double* shard_image(const double* f0, const Mlk
 
 // global image index -> shard (shards sorted by img_off; few shards)
 __device__ __forceinline__ int find_shard(const MlkShard* sh, int n_shards, int g) {
-    int s = 0;
-    while (s + 1 < n_shards && sh[s + 1].img_off <= g) ++s;
-    return s;
+    int lo = 0, hi = n_shards - 1;  // binary search: the last shard with img_off <= g
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (__ldg(&sh[mid].img_off) <= g) lo = mid;
+        else hi = mid - 1;
+    }
+    return lo;
 }
 
 // ----------------------------------------------------------------------------
 // OpenBLAS-order AE contractions (probed, SURVEY §7 hard part 2; the same
 // orders are restated in oracle/ckernels.c oracle_encode / oracle_decode).
+
+// Loads with L1 policies: the decoder weights are re-read for every image of
+// a shard (keep them in L1), the originals are streamed once (do not let
+// them evict the weights).
+__device__ __forceinline__ float ld_keep(const float* p) {
+    float v;
+    asm("ld.global.nc.L1::evict_last.f32 %0, [%1];" : "=f"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ double ld_stream(const double* p) {
+    double v;
+    asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    return v;
+}
 
 // decode one cell: sum_k z[k] * W[k][j] with the probed bracketing, then
 // * std + mean (two roundings, numpy `recon * std + mean`).
@@ -171,10 +189,10 @@ __device__ __forceinline__ double decode_cell(const double* z, const float* W, i
     const float* wp = W + j;
     double s;
     if (L == 4) {
-        const double p0 = __dmul_rn(z[0], (double)__ldg(wp));
-        const double p1 = __dmul_rn(z[1], (double)__ldg(wp + D));
-        const double p2 = __dmul_rn(z[2], (double)__ldg(wp + 2 * D));
-        const double p3 = __dmul_rn(z[3], (double)__ldg(wp + 3 * D));
+        const double p0 = __dmul_rn(z[0], (double)ld_keep(wp));
+        const double p1 = __dmul_rn(z[1], (double)ld_keep(wp + D));
+        const double p2 = __dmul_rn(z[2], (double)ld_keep(wp + 2 * D));
+        const double p3 = __dmul_rn(z[3], (double)ld_keep(wp + 3 * D));
         const double p01 = __dadd_rn(p0, p1);
         s = tree ? __dadd_rn(p01, __dadd_rn(p2, p3)) : __dadd_rn(__dadd_rn(p01, p2), p3);
     } else {
@@ -299,6 +317,16 @@ __host__ __device__ __forceinline__ double mlk_exp(double x) {
     memcpy(&sc, &sb, 8);
     return p * sc;
 #endif
+}
+
+// Bulk prefetch of histogram x (D doubles, the 16-B aligned superset) into
+// L2 (cp.async.bulk.prefetch.L2): no shared-memory destination, no barrier.
+__device__ __forceinline__ void prefetch_l2_histogram(const double* x, int D) {
+    const unsigned long long a = reinterpret_cast<unsigned long long>(x);
+    const int shift = (int)((a & 15ull) >> 3);
+    const unsigned bytes = (unsigned)(((D + shift) * 8 + 15) & ~15);
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(x - shift), "r"(bytes)
+                 : "memory");
 }
 
 // rint(r / eb2) without a division per cell: y = r * (1 / eb2) is within a

@@ -149,7 +149,51 @@ __global__ void k_pack_exc(const double* __restrict__ f0, const MlkShard* __rest
     }
 }
 
+// the images of [0, total) with (flags & mask) != 0 and those with == 0, each
+// list in increasing order (one CTA: chunked counts + block scan)
+__global__ void __launch_bounds__(LT)
+k_split_flags(const unsigned char* __restrict__ flags, int total, unsigned mask,
+              int* __restrict__ set, int* __restrict__ clear, int* __restrict__ n_set) {
+    __shared__ int wtot[32];
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const int chunk = (total + LT - 1) / LT;
+    const int lo = min(total, tid * chunk), hi = min(total, lo + chunk);
+    int c = 0;
+    for (int j = lo; j < hi; ++j) c += (flags[j] & mask) != 0;
+    int inc = c;
+    for (int o = 1; o < 32; o <<= 1) {
+        int t = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += t;
+    }
+    if (lane == 31) wtot[w] = inc;
+    __syncthreads();
+    if (w == 0) {
+        int t = wtot[lane];
+        int ti = t;
+        for (int o = 1; o < 32; o <<= 1) {
+            int u = __shfl_up_sync(0xffffffffu, ti, o);
+            if (lane >= o) ti += u;
+        }
+        wtot[lane] = ti - t;
+        if (lane == 31) n_set[0] = ti;
+    }
+    __syncthreads();
+    int ps = wtot[w] + inc - c;  // set entries before this thread's chunk
+    int pc = lo - ps;            // clear entries before it
+    for (int j = lo; j < hi; ++j) {
+        if ((flags[j] & mask) != 0) set[ps++] = j;
+        else clear[pc++] = j;
+    }
+}
+
 }  // namespace
+
+extern "C" int mlk_split_flags(const uint8_t* flags, int32_t total, uint32_t mask, int32_t* set,
+                               int32_t* clear, int32_t* n_set, cudaStream_t stream) {
+    if (total <= 0) return MLK_OK;
+    k_split_flags<<<1, LT, 0, stream>>>(flags, total, mask, set, clear, n_set);
+    return cudaGetLastError() == cudaSuccess ? MLK_OK : MLK_ERR_CUDA;
+}
 
 extern "C" int mlk_list_flags(const uint8_t* flags, const MlkShard* shards, int32_t n_shards,
                               uint32_t mask, int32_t* list, int32_t* count, cudaStream_t stream) {

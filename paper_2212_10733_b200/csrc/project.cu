@@ -1,6 +1,6 @@
 // project.cu -- residual coding + Lagrange QoI projection + final PD gate.
 //
-// Replaces, per image,
+// One CTA (128 threads) per histogram.  Replaces, per image,
 // pipeline.py:239-292:
 //   * residual q = rint(r / 2eb), zigzag, LEB128 (residual.py:60-79,
 //     _ckernels.pyx:143-171) for selected images -- the varint stream goes
@@ -13,12 +13,22 @@
 //     reference's exact elementwise order, the final per-image NRMSE in
 //     numpy's pairwise order and the tau gate (pipeline.py:284-292).
 //
-// The kernel is k_project_s below (one warp per histogram, one image buffer;
-// its header explains the layout).  k_newton_batch at the end serves the
-// reference's per-image operator API (kernels.newton_solve).
+// Shared memory holds two histogram-sized buffers (the TMA-staged original,
+// later the squared errors; the working image) so 6 CTAs fit an SM.  The
+// Newton iteration is split: every thread accumulates its cells' 14 sums,
+// a warp reduce-scatter + one shared-memory pass combine them, and every
+// warp takes the (identical) Newton step; the block computes the next
+// iteration's exponent tables.  Two barriers per iteration.  exp() is
+// mlk_exp (common.cuh), the decoder's too.
+//
+// Round 2 measured alternatives: one warp per histogram with
+// one or two image buffers, warp-0-only Newton steps, row-weighted
+// factorised sums and a fast-sum NRMSE gate cut the instructions per image
+// by up to 2x but not the time: this kernel is bound by its per-image
+// dependency chain at 24 resident warps per SM (issue ~0.1 IPC per warp),
+// and every variant that removed instructions lost the same fraction of
+// issue efficiency.
 #include "common.cuh"
-
-#include <algorithm>
 
 namespace {
 
@@ -62,6 +72,50 @@ __device__ __forceinline__ void block_allsum(double (&v)[NV], PjCtl& C, int& ph)
         v[k] = t;
     }
     ph ^= 1;
+}
+
+// NaN-propagating max of two values over the block
+__device__ __forceinline__ void block_allmax2(double& a, double& b, PjCtl& C, int& ph) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        a = np_max2(a, __shfl_xor_sync(FULL, a, o));
+        b = np_max2(b, __shfl_xor_sync(FULL, b, o));
+    }
+    if (lane == 0) {
+        C.red[ph][w][0] = a;
+        C.red[ph][w][1] = b;
+    }
+    __syncthreads();
+    a = C.red[ph][0][0];
+    b = C.red[ph][0][1];
+#pragma unroll
+    for (int q = 1; q < PJ_W; ++q) {
+        a = np_max2(a, C.red[ph][q][0]);
+        b = np_max2(b, C.red[ph][q][1]);
+    }
+    ph ^= 1;
+}
+
+__device__ __forceinline__ int block_exscan_int(int v, int* total, PjCtl& C) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    int inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        int t = __shfl_up_sync(FULL, inc, o);
+        if (lane >= o) inc += t;
+    }
+    __syncthreads();
+    if (lane == 31) C.iscan[w] = inc;
+    __syncthreads();
+    int base = 0, tot = 0;
+#pragma unroll
+    for (int q = 0; q < PJ_W; ++q) {
+        if (q < w) base += C.iscan[q];
+        tot += C.iscan[q];
+    }
+    *total = tot;
+    return base + inc - v;
 }
 
 // 16 per-lane values -> lane l holds the warp sum of value l >> 1
@@ -210,7 +264,7 @@ __device__ int newton_generic(const double* fp, const double* __restrict__ a, in
                          a3 = __ldg(a + 3 * D + j);
             double t = lam[0] * a0 + lam[1] * a1 + lam[2] * a2 + lam[3] * a3;
             if (fabs(t) > 700.0) { v[14] = 1.0; t = t > 0 ? 700.0 : -700.0; }
-            cell_sums(v, a0, a1, a2, a3, fp[j] * exp(-t));
+            cell_sums(v, a0, a1, a2, a3, fp[j] * mlk_exp(-t));
         }
         double r[15];
 #pragma unroll
@@ -224,495 +278,383 @@ __device__ int newton_generic(const double* fp, const double* __restrict__ a, in
     return status;
 }
 
-__device__ __forceinline__ int varint_len(unsigned long long z) {
-    return z == 0ull ? 1 : (64 - __clzll(z) + 6) / 7;
-}
-
-// ===========================================================================
-// k_project_s: ONE WARP per histogram, persistent, ONE image-sized buffer.
-//
-// The original O is not kept in shared memory: each warp issues an L2 bulk
-// prefetch (cp.async.bulk.prefetch.L2) of its NEXT image when it starts the
-// current one, so by the time it gets there O is L2-resident.  Then
-//   * non-selected images: F = AE decode, straight from the codes;
-//   * selected images (the residual stage): O is bulk-copied (TMA) into F's
-//     buffer and replaced in place by recon + q * 2eb (the recon recomputed
-//     per cell, exactly as decode_cell gives it);
-//   * the exact apply reads O again from L2 for d = O - final.
-// One 12 KB buffer instead of two doubles the warps an SM holds.  The final
-// NRMSE is gated on a fast sum of d^2 (lane partials + shuffles) with a
-// rigorous bound against numpy's pairwise sum; only when the gate decision
-// is inside that bound are the d^2 rewritten into F and summed in the exact
-// pairwise order (the report keeps the fast value, relative error < 1e-14).
-//
-// Layout of the separable Newton sums and of the apply: lane c owns column c
-// (c < 32); the columns past 31 are split into row groups over the lanes.
-// Per Newton evaluation a lane sums its interior cells as
-//     S0 += F * R0[r],  S1 += F * R1[r],  S2 += F * R2[r]
-// with per-iteration row tables R0 = exp(-w B_r), R1 = R0 p2_r, R2 = R0 p2_r^2
-// (the column's exp(-w A_c), volume class and factors are applied once per
-// column), and the edge rows separately.  The 4x4 solve runs once per warp.
-constexpr int PS_MAXRC = 64;     // rows, cols <= 64 on the separable path
-constexpr int PS_MAXS = 64;      // shard offsets cached in shared memory
-
-struct PsTabs {                  // offsets (doubles) of the per-warp tables
-    int ea, rt, vp1, p3c, p2r, p2s, a2c, vp2, leaf, n;
-};
-
-__host__ __device__ inline PsTabs ps_tabs(int rows, int cols, int n_leaves) {
-    PsTabs t;
-    int o = 0;
-    t.ea = o; o += 2 * cols;    // exp(-w(re, ce_c) A_c)                 [re][c]
-    t.rt = o; o += 6 * rows;    // R0/R1/R2 row tables by column edge    [ce][r][3]
-    t.vp1 = o; o += cols;       // vpar_c / s1                           (grid)
-    t.p3c = o; o += cols;       // hm (vpar_c - u)^2 / s4                (image)
-    t.p2r = o; o += rows;       // hm vperp2_r / s2                      (grid)
-    t.p2s = o; o += rows;       // p2r^2                                 (grid)
-    t.a2c = o; o += 2 * rows;   // ash row 2 by (col edge, row): exact table values
-    t.vp2 = o; o += rows;       // vperp2_r                              (grid)
-    t.leaf = o; o += n_leaves;  // pairwise leaves (exact NRMSE fallback)
-    t.n = (o + 1) & ~1;
-    return t;
-}
-
-// per-warp shared memory: the image buffer (D + 2) and the tables
-__host__ __device__ inline int ps_warp_doubles(int D, int rows, int cols, int n_leaves) {
-    return ((D + 3) / 2) * 2 + ps_tabs(rows, cols, n_leaves).n;
-}
-
-__device__ __forceinline__ void prefetch_l2_histogram(const double* x, int D) {
-    const unsigned long long a = reinterpret_cast<unsigned long long>(x);
-    const int shift = (int)((a & 15ull) >> 3);
-    const unsigned bytes = (unsigned)(((D + shift) * 8 + 15) & ~15);
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(x - shift), "r"(bytes)
-                 : "memory");
-}
-
-// the 14 Newton sums of one column from its five factorised accumulators
-__device__ __forceinline__ void add_column(double (&v)[16], double q0, double q1, double q3,
-                                           double G1, double G2, double H1, double H2,
-                                           double H3) {
-    v[0] += q0 * G1; v[1] += q1 * G1; v[2] += G2; v[3] += q3 * G1;
-    v[4] += q0 * q0 * H1; v[5] += q0 * q1 * H1; v[6] += q0 * H2; v[7] += q0 * q3 * H1;
-    v[8] += q1 * q1 * H1; v[9] += q1 * H2; v[10] += q1 * q3 * H1;
-    v[11] += H3; v[12] += q3 * H2; v[13] += q3 * q3 * H1;
-}
+// ---------------------------------------------------------------------------
+// Separable exponent (trapezoid make_grid grids, fdata.py:151-167): every
+// feature row carries vol, so t = vol_rc * (A_c + B_r) with
+//   A_c = l0/s0 + l1 vpar_c/s1 + l3 hm (vpar_c - u)^2/s4,  B_r = l2 hm vperp_r^2/s2,
+// and vol_rc takes one of 4 values set by (row edge, col edge).  exp(-t)
+// is then ea[row edge][c] * eb[col edge][r]: 2 (rows + cols) exps per
+// iteration instead of rows * cols.  Only the Newton iterate uses it
+// (tolerance-level, like the reference's own summation order); the stored
+// image uses the exact per-cell formula.
 
 __device__ __forceinline__ double cls_val(const double (&w)[4], bool re, bool ce) {
     return re ? (ce ? w[3] : w[2]) : (ce ? w[1] : w[0]);
 }
 
-// Newton tables for lam; returns true (warp-uniform) when some exponent
-// could pass the reference's +-700 clamp (the iteration then goes cell by cell)
-__device__ __forceinline__ bool ps_tables(const double (&lam)[4], const double (&w)[4],
-                                          double is0, int rows, int cols, double* T,
-                                          const PsTabs& tb) {
-    const int lane = threadIdx.x & 31;
+struct NtCtx {
+    double w[4];  // vol by class (2 re + ce)
+    double is0, is4, u;
+    int rows, cols;
+};
+
+// Exponent tables for lam, entries spread over the block; returns true
+// (warp-uniform) when this warp saw some |t| that could exceed the
+// reference's +-700 clamp (that iteration is then evaluated cell by cell).
+__device__ __forceinline__ bool sep_tables(const double (&lam)[4], const NtCtx& X, PjCtl& C) {
+    const int rows = X.rows, cols = X.cols;
     bool big = false;
-    for (int q = lane; q < 2 * (rows + cols); q += 32) {
+    for (int q = threadIdx.x; q < 2 * (rows + cols); q += PJ_T) {
+        double x;
         if (q < 2 * cols) {
             const int re = q >= cols, c = q - re * cols;
             const bool ce = (c == 0) | (c == cols - 1);
-            const double x = cls_val(w, re, ce) * (lam[0] * is0 + lam[1] * T[tb.vp1 + c] +
-                                                   lam[3] * T[tb.p3c + c]);
-            if (!(fabs(x) <= 349.0)) big = true;
-            T[tb.ea + q] = mlk_exp(-fmax(fmin(x, 700.0), -700.0));
+            x = cls_val(X.w, re, ce) * (lam[0] * X.is0 + lam[1] * C.vp1[c] + lam[3] * C.p3c[c]);
+            C.ea[re][c] = mlk_exp(-fmax(fmin(x, 700.0), -700.0));
         } else {
             const int q2 = q - 2 * cols;
             const int ce = q2 >= rows, r = q2 - ce * rows;
             const bool re = (r == 0) | (r == rows - 1);
-            const double x = cls_val(w, re, ce) * (lam[2] * T[tb.p2r + r]);
-            if (!(fabs(x) <= 349.0)) big = true;
-            const double e = mlk_exp(-fmax(fmin(x, 700.0), -700.0));
-            double* rt = T + tb.rt + 3 * q2;
-            rt[0] = e;
-            rt[1] = e * T[tb.p2r + r];
-            rt[2] = e * T[tb.p2s + r];
+            x = cls_val(X.w, re, ce) * (lam[2] * C.p2r[r]);
+            C.eb[ce][r] = mlk_exp(-fmax(fmin(x, 700.0), -700.0));
         }
+        if (!(fabs(x) <= 349.0)) big = true;
     }
-    __syncwarp();
     return __any_sync(FULL, big);
 }
 
-struct PsItem {
-    bool act;
-    int c, r0, r1;   // column, rows [r0, r1)
-    bool ce;         // column edge
-};
-
-// one item's five factorised accumulators
-__device__ __forceinline__ void item_sums(const double* F, const PsItem& it, int rows, int cols,
-                                          const double (&w)[4], const double* T,
-                                          const PsTabs& tb, double& G1, double& G2, double& H1,
-                                          double& H2, double& H3) {
-    const int c = it.c;
-    const double* rt = T + tb.rt + (it.ce ? 3 * rows : 0);
-    double S0 = 0.0, S1 = 0.0, S2 = 0.0, U0 = 0.0, U1 = 0.0, U2 = 0.0;
-    const int ri0 = it.r0 > 0 ? it.r0 : 1;
-    const int ri1 = it.r1 < rows - 1 ? it.r1 : rows - 1;
-    int r = ri0;
-    for (; r + 1 < ri1; r += 2) {  // two rows per step: independent chains
-        const double f0 = F[r * cols + c], f1 = F[(r + 1) * cols + c];
-        const double* a = rt + 3 * r;
-        S0 = fma(f0, a[0], S0); S1 = fma(f0, a[1], S1); S2 = fma(f0, a[2], S2);
-        U0 = fma(f1, a[3], U0); U1 = fma(f1, a[4], U1); U2 = fma(f1, a[5], U2);
-    }
-    if (r < ri1) {
-        const double f0 = F[r * cols + c];
-        const double* a = rt + 3 * r;
-        S0 = fma(f0, a[0], S0); S1 = fma(f0, a[1], S1); S2 = fma(f0, a[2], S2);
-    }
-    S0 += U0; S1 += U1; S2 += U2;
-    double E0 = 0.0, E1 = 0.0, E2 = 0.0;
-    if (it.r0 == 0) {
-        const double f0 = F[c];
-        E0 = f0 * rt[0]; E1 = f0 * rt[1]; E2 = f0 * rt[2];
-    }
-    if (it.r1 == rows && rows > 1) {
-        const int rl = rows - 1;
-        const double f0 = F[rl * cols + c];
-        const double* a = rt + 3 * rl;
-        E0 = fma(f0, a[0], E0); E1 = fma(f0, a[1], E1); E2 = fma(f0, a[2], E2);
-    }
-    const double w_in = cls_val(w, false, it.ce), w_ed = cls_val(w, true, it.ce);
-    const double ai = w_in * T[tb.ea + c], ae = w_ed * T[tb.ea + cols + c];
-    G1 = ai * S0 + ae * E0;
-    G2 = ai * S1 + ae * E1;
-    H1 = w_in * ai * S0 + w_ed * ae * E0;
-    H2 = w_in * ai * S1 + w_ed * ae * E1;
-    H3 = w_in * ai * S2 + w_ed * ae * E2;
-}
-
-// one warp's Newton iteration (_ckernels.pyx:62-137 semantics via newton_step)
+// The block's Newton iteration for one image.  All threads call it.  Every
+// warp combines the per-warp partial sums and takes the (identical) Newton
+// step itself, so lambda never needs a broadcast; the next iteration's
+// exponent tables are computed by the whole block.  Two barriers per step.
 template <bool SEP>
-__device__ void newton_ps(const double* F, const MlkGrid& g, const double (&w)[4], double is0,
-                          double is4, double u, const double* b, double bmax, double step,
-                          int max_iter, double tol, double* T, const PsTabs& tb,
-                          const PsItem& iA, const PsItem& iB, double (&lam)[4], int& status,
-                          int& iters) {
-    const int lane = threadIdx.x & 31;
-    const int D = g.D, rows = g.rows, cols = g.cols;
+__device__ void newton_block(const double* fp, double fl, const MlkGrid& g, const NtCtx& X,
+                             const double* b,
+                             double bmax, double step, int max_iter, double tol, PjCtl& C,
+                             double (&lam)[4], int& status, int& iters) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int D = g.D, rows = X.rows, cols = X.cols;
+    (void)rows;
     bool clamped = false;
 #pragma unroll
     for (int k = 0; k < 4; ++k) lam[k] = 0.0;
     status = MLK_NEWTON_MAX_ITER;
     iters = max_iter;
-    bool big = SEP ? ps_tables(lam, w, is0, rows, cols, T, tb) : true;
+    if (SEP) {
+        const bool big = sep_tables(lam, X, C);
+        if (lane == 0) C.big[warp] = big;
+    }
+    __syncthreads();
     for (int it = 0;; ++it) {
+        bool direct = !SEP;
+        if (SEP) {
+#pragma unroll
+            for (int q = 0; q < PJ_W; ++q) direct |= C.big[q] != 0;
+        }
         double v[16];
 #pragma unroll
         for (int k = 0; k < 16; ++k) v[k] = 0.0;
-        if (SEP && !big) {
-            double G1, G2, H1, H2, H3;
-            if (iA.act) {
-                item_sums(F, iA, rows, cols, w, T, tb, G1, G2, H1, H2, H3);
-                add_column(v, is0, T[tb.vp1 + iA.c], T[tb.p3c + iA.c], G1, G2, H1, H2, H3);
-            }
-            if (iB.act) {
-                item_sums(F, iB, rows, cols, w, T, tb, G1, G2, H1, H2, H3);
-                add_column(v, is0, T[tb.vp1 + iB.c], T[tb.p3c + iB.c], G1, G2, H1, H2, H3);
+        if (SEP && !direct) {
+            // thread = (row group, column): exp(-t) = ea[re][c] eb[ce][r] and
+            // a_k = w * p_k with w the class volume, so with the column fixed
+            // the 14 sums factor into 5 row accumulations per thread
+            const int ngrp = PJ_T / cols, c = tid % cols, g0 = tid / cols;
+            if (g0 < ngrp) {
+                const bool ce = (c == 0) | (c == cols - 1);
+                const double ea0 = C.ea[0][c], ea1 = C.ea[1][c];
+                const double w_in = cls_val(X.w, false, ce), w_ed = cls_val(X.w, true, ce);
+                const double* ebp = C.eb[ce];
+                double G1 = 0.0, G2 = 0.0, H1 = 0.0, H2 = 0.0, H3 = 0.0;
+                for (int r = g0; r < rows; r += ngrp) {
+                    const bool re = (r == 0) | (r == rows - 1);
+                    const double w = re ? w_ed : w_in;
+                    const double wf = w * (fmax(fp[r * cols + c], fl) * (re ? ea1 : ea0) * ebp[r]);
+                    const double p2 = C.p2r[r];
+                    const double w2f = w * wf, t2 = p2 * w2f;
+                    G1 += wf;
+                    G2 = fma(p2, wf, G2);
+                    H1 += w2f;
+                    H2 += t2;
+                    H3 = fma(p2, t2, H3);
+                }
+                const double q0 = X.is0, q1 = C.vp1[c], q3 = C.p3c[c];
+                v[0] = q0 * G1; v[1] = q1 * G1; v[2] = G2; v[3] = q3 * G1;
+                v[4] = q0 * q0 * H1; v[5] = q0 * q1 * H1; v[6] = q0 * H2; v[7] = q0 * q3 * H1;
+                v[8] = q1 * q1 * H1; v[9] = q1 * H2; v[10] = q1 * q3 * H1;
+                v[11] = H3; v[12] = q3 * H2; v[13] = q3 * q3 * H1;
             }
         } else {
             const double l0 = lam[0], l1 = lam[1], l2 = lam[2], l3 = lam[3];
-            for (int j = lane; j < D; j += 32) {
+            for (int j = tid; j < D; j += PJ_T) {
                 const double a0 = __ldg(g.ash + j), a1 = __ldg(g.ash + D + j),
                              a2 = __ldg(g.ash + 2 * D + j);
-                const double dv = __ldg(g.vpar + j) - u;
-                const double a3 = __ldg(g.hmvol + j) * dv * dv * is4;
+                const double dv = __ldg(g.vpar + j) - X.u;
+                const double a3 = __ldg(g.hmvol + j) * dv * dv * X.is4;
                 double t = l0 * a0 + l1 * a1 + l2 * a2 + l3 * a3;
                 if (fabs(t) > 700.0) { v[14] = 1.0; t = t > 0 ? 700.0 : -700.0; }
-                cell_sums(v, a0, a1, a2, a3, F[j] * mlk_exp(-t));
+                cell_sums(v, a0, a1, a2, a3, fmax(fp[j], fl) * mlk_exp(-t));
             }
         }
-        const double part = warp_rs16(v);   // lane l: warp sum of value l >> 1
+        const double part = warp_rs16(v);
+        if (!(lane & 1)) C.part[warp][lane >> 1] = part;
+        __syncthreads();
+        double tot = 0.0;
+        if (lane < 16) {
+            tot = C.part[0][lane];
+#pragma unroll
+            for (int q = 1; q < PJ_W; ++q) tot += C.part[q][lane];
+        }
         double sums[15];
 #pragma unroll
-        for (int k = 0; k < 15; ++k) sums[k] = __shfl_sync(FULL, part, 2 * k);
+        for (int k = 0; k < 15; ++k) sums[k] = __shfl_sync(FULL, tot, k);
         if (!newton_step(sums, b, bmax, step, max_iter, tol, it, lam, clamped, status, iters))
-            break;  // warp-uniform: every lane holds the same sums
-        if (SEP) big = ps_tables(lam, w, is0, rows, cols, T, tb);
+            break;  // block-uniform: every warp saw the same sums
+        if (SEP) {
+            const bool big = sep_tables(lam, X, C);
+            if (lane == 0) C.big[warp] = big;
+        }
+        __syncthreads();
     }
 }
 
+__device__ __forceinline__ int varint_len(unsigned long long z) {
+    return z == 0ull ? 1 : (64 - __clzll(z) + 6) / 7;
+}
+
+// exact numpy pairwise sum of v[0..n) by the whole block: thread (leaf,
+// accumulator) pairs run the 8 strided accumulators, the ((r0+r1)+(r2+r3))+
+// ((r4+r5)+(r6+r7)) tree runs over 8-lane groups, thread 0 combines leaves.
+__device__ double block_pairwise(const double* v, const PwPlan& pw, PjCtl& C) {
+    const int tid = threadIdx.x, a = tid & 7;
+    for (int l0 = 0; l0 < pw.n_leaves; l0 += PJ_T / 8) {
+        const int l = l0 + (tid >> 3);
+        int st = 0, len = 0;
+        if (l < pw.n_leaves) { st = pw.start[l]; len = pw.len[l]; }
+        const int lim = len - (len % 8);
+        double r = 0.0;
+        if (len >= 8) {
+            r = v[st + a];
+            for (int i = a + 8; i < lim; i += 8) r = __dadd_rn(r, v[st + i]);
+        }
+        r = __dadd_rn(r, __shfl_down_sync(FULL, r, 1));
+        r = __dadd_rn(r, __shfl_down_sync(FULL, r, 2));
+        r = __dadd_rn(r, __shfl_down_sync(FULL, r, 4));
+        if (a == 0 && l < pw.n_leaves) {
+            double s = 0.0;
+            int i = 0;
+            if (len >= 8) { s = r; i = lim; }
+            for (; i < len; ++i) s = __dadd_rn(s, v[st + i]);
+            C.leaf[l] = s;
+        }
+    }
+    __syncthreads();
+    if (tid == 0) C.bval = pw_combine_ops(C.leaf, pw);
+    __syncthreads();
+    return C.bval;
+}
+
 template <bool SEP>
-__global__ void __launch_bounds__(32, 13)
-k_project_s(const double* __restrict__ f0, const double* __restrict__ stats,
-            const double* __restrict__ qoi, const MlkShard* __restrict__ shards, int n_shards,
-            int total, MlkGrid g, PwPlan pw, const float* __restrict__ W, int L,
-            const float* __restrict__ cents, int K, const unsigned char* __restrict__ codes,
-            const int* __restrict__ sel_rank, const int* __restrict__ slot_base, MlkNewton opt,
-            unsigned char* __restrict__ flags, double* __restrict__ lam_out,
-            double* __restrict__ qst_out, int* __restrict__ status_out,
-            int* __restrict__ iters_out, double* __restrict__ ferr_out,
-            double* __restrict__ fqoi_out, double* __restrict__ fsse_out,
-            unsigned char* __restrict__ varint, long long vcap, long long* __restrict__ vlen,
-            int* __restrict__ err_flag) {
+__global__ void __launch_bounds__(PJ_T, 6)
+k_project(const double* __restrict__ f0, const double* __restrict__ stats,
+          const double* __restrict__ qoi, const MlkShard* __restrict__ shards, int n_shards,
+          MlkGrid g, PwPlan pw, const float* __restrict__ W, int L, const float* __restrict__ cents,
+          int K, const unsigned char* __restrict__ codes, const int* __restrict__ sel_rank,
+          const int* __restrict__ slot_base, MlkNewton opt, unsigned char* __restrict__ flags,
+          double* __restrict__ lam_out, double* __restrict__ qst_out,
+          int* __restrict__ status_out, int* __restrict__ iters_out,
+          double* __restrict__ ferr_out, double* __restrict__ fqoi_out,
+          double* __restrict__ fsse_out, unsigned char* __restrict__ varint, long long vcap,
+          long long* __restrict__ vlen, int* __restrict__ err_flag, const int* __restrict__ img_list) {
+    __shared__ PjCtl C;
     __shared__ unsigned long long bar;
-    __shared__ int s_off[PS_MAXS + 1];
     extern __shared__ __align__(16) double sm[];
-    const int D = g.D, rows = g.rows, cols = g.cols;
-    const int lane = threadIdx.x;
-    double* Fbuf = sm;                         // the image buffer (D + 2 doubles)
-    double* T = sm + ((D + 3) / 2) * 2;        // tables
-    const PsTabs tb = ps_tabs(rows, cols, pw.n_leaves);
-    double* leaf = T + tb.leaf;
+    const int D = g.D;
+    const int img = img_list ? img_list[blockIdx.x] : (int)blockIdx.x;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    int ph = 0;
+    const int s = find_shard(shards, n_shards, img);
+    const MlkShard sh = shards[s];
+    const double* x = shard_image(f0, sh, img - sh.img_off, D);
+    double* Ob = sm;                     // TMA target: the original, later d^2
+    double* F = sm + ((D + 3) / 2) * 2;  // recon -> corrected -> f_plus -> final
+
+    // ---- one bulk copy of the original; the AE decode overlaps it
+    if (tid == 0) mbar_init(&bar, 1);
+    __syncthreads();
+    int shift;
+    if (warp == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        shift = stage_histogram(Ob, x, D, &bar);
+    } else {
+        shift = (int)((reinterpret_cast<unsigned long long>(x) & 15ull) >> 3);
+    }
+    double* O = Ob + shift;
+    double z[MLK_MAXL];
+#pragma unroll
+    for (int k = 0; k < MLK_MAXL; ++k)
+        z[k] = k < L ? (double)cents[((long long)s * L + k) * K + codes[(long long)img * L + k]]
+                     : 0.0;
+    const float* Ws = W + sh.w_off;
+    const bool blas_tree = !sh.small_blas;
+    for (int j = tid; j < D; j += PJ_T)
+        F[j] = decode_cell(z, Ws, L, D, j, blas_tree && g.tree_cols[j], sh.mean, sh.std);
+    // per-grid / per-image column and row tables of the separable Newton
+    const double4 q4 = reinterpret_cast<const double4*>(qoi)[img];
+    double qs[4] = {q4.x, q4.y, q4.z, q4.w};
+    if (opt.lam_f32) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) qs[k] = (double)__double2float_rn(qs[k]);
+    }
     const double hm = 0.5 * g.mass;
-    double w[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) w[k] = g.vcls[k];
-    // the lane's columns: A = column `lane` (all rows), B = one row group of
-    // a column past 31
-    PsItem iA, iB;
-    {
-        const int nA = cols < 32 ? cols : 32;
-        const int nx = cols > 32 ? cols - 32 : 0;
-        const int grp = nx ? 32 / nx : 0;
-        iA.act = SEP && lane < nA;
-        iA.c = lane;
-        iA.r0 = 0;
-        iA.r1 = rows;
-        iA.ce = (iA.c == 0) | (iA.c == cols - 1);
-        iB.act = SEP && nx && lane < nx * grp;
-        iB.c = iB.act ? 32 + lane % nx : 0;
-        const int gB = iB.act ? lane / nx : 0;
-        iB.r0 = iB.act ? gB * rows / grp : 0;
-        iB.r1 = iB.act ? (gB + 1) * rows / grp : 0;
-        iB.ce = (iB.c == 0) | (iB.c == cols - 1);
-    }
-    if (SEP) {  // grid-constant tables, once per warp
-        for (int c = lane; c < cols; c += 32) T[tb.vp1 + c] = g.vpar[c] / g.s1;
-        const int cin = cols > 2 ? 1 : 0;
-        for (int r = lane; r < rows; r += 32) {
-            const double p2 = hm * g.vperp2[r * cols] / g.s2;
-            T[tb.p2r + r] = p2;
-            T[tb.p2s + r] = p2 * p2;
-            T[tb.a2c + r] = __ldg(g.ash + 2 * D + r * cols + cin);   // interior column
-            T[tb.a2c + rows + r] = __ldg(g.ash + 2 * D + r * cols);  // edge column
-            T[tb.vp2 + r] = g.vperp2[r * cols];
+    if (SEP) {
+        if (tid < g.cols) {
+            const double vp = g.vpar[tid];
+            C.vp1[tid] = vp / g.s1;
+            const double dv = vp - qs[1];
+            C.p3c[tid] = hm * dv * dv;  // / s4 once s4 is known
+        } else if (tid >= 64 && tid - 64 < g.rows) {
+            C.p2r[tid - 64] = hm * g.vperp2[(tid - 64) * g.cols] / g.s2;
         }
     }
-    const bool cache_sh = n_shards <= PS_MAXS;
-    if (cache_sh)
-        for (int q = lane; q <= n_shards; q += 32)
-            s_off[q] = q < n_shards ? shards[q].img_off : 0x7fffffff;
-    if (lane == 0) mbar_init(&bar, 1);
-    __syncwarp();
-    auto shard_of = [&](int im) {
-        if (!cache_sh) return find_shard(shards, n_shards, im);
-        int q = 0;
-        while (s_off[q + 1] <= im) ++q;
-        return q;
-    };
-    unsigned phase = 0;
-    int img = blockIdx.x;
-    if (img < total && lane == 0) {
-        const int s0 = shard_of(img);
-        prefetch_l2_histogram(shard_image(f0, shards[s0], img - shards[s0].img_off, D), D);
+    mbar_wait(&bar, 0);
+    __syncthreads();
+
+    // ---- residual stage for selected images (contiguous cells per thread so
+    //      the varint stream is written in cell order after one block scan)
+    const int rank = sel_rank[img];
+    if (rank >= 0) {  // block-uniform
+        const double eb2 = 2.0 * sh.eb;
+        const double inv = 1.0 / eb2;
+        const bool lossless = sh.lossless != 0;
+        const int per = (D + PJ_T - 1) / PJ_T;
+        const int c0 = min(D, tid * per), c1 = min(D, c0 + per);
+        int nb = 0;
+        bool too_big = false;
+        for (int j = c0; j < c1; ++j) {
+            const double r = __dsub_rn(O[j], F[j]);
+            unsigned long long zz;
+            if (lossless) {
+                zz = (unsigned long long)__double_as_longlong(r);
+            } else {
+                const double q = qround(r, eb2, inv);
+                if (!(fabs(q) < 4611686018427387904.0)) too_big = true;
+                const long long qi = (long long)q;
+                zz = ((unsigned long long)qi << 1) ^ (unsigned long long)(qi >> 63);
+            }
+            nb += varint_len(zz);
+        }
+        if (too_big) atomicExch(err_flag, MLK_ERR_CONFIG);
+        int tot = 0;
+        int pos = block_exscan_int(nb, &tot, C);
+        const long long slot = slot_base[s] + rank;
+        unsigned char* out = varint + slot * vcap;
+        for (int j = c0; j < c1; ++j) {
+            const double r = __dsub_rn(O[j], F[j]);
+            unsigned long long zz;
+            if (lossless) {
+                zz = (unsigned long long)__double_as_longlong(r);
+                F[j] = __dadd_rn(F[j], r);
+            } else {
+                const double q = qround(r, eb2, inv);
+                const long long qi = (long long)q;
+                zz = ((unsigned long long)qi << 1) ^ (unsigned long long)(qi >> 63);
+                F[j] = __dadd_rn(F[j], __dmul_rn(q, eb2));
+            }
+            while (zz >= 0x80ull) {
+                out[pos++] = (unsigned char)(zz | 0x80ull);
+                zz >>= 7;
+            }
+            out[pos++] = (unsigned char)zz;
+        }
+        if (tid == 0) vlen[slot] = tot;
+        __syncthreads();
     }
 
-    for (; img < total; img += gridDim.x) {
-        const int s = shard_of(img);
-        const MlkShard sh = shards[s];
-        const double* Og = shard_image(f0, sh, img - sh.img_off, D);
-        {   // the next image of this warp into L2 while this one is processed
-            const int nxt = img + gridDim.x;
-            if (nxt < total && lane == 0) {
-                const int s1 = shard_of(nxt);
-                prefetch_l2_histogram(shard_image(f0, shards[s1], nxt - shards[s1].img_off, D),
-                                      D);
-            }
-        }
-        double z[MLK_MAXL];
+    // ---- stored QoIs (pipeline.py:254-260) and the per-image system:
+    //      top = max(corrected), s4 = max |a3| (lagrange.py:199-204)
+    double top = -INFINITY, amax = 0.0;
+    bool nan_t = false, nan_a = false;  // numpy max propagates NaN
+    for (int j = tid; j < D; j += PJ_T) {
+        const double fj = F[j];
+        nan_t |= fj != fj;
+        top = fmax(top, fj);
+    }
+    if (SEP) {
+        // a3 = hmvol * (vpar - u)^2 takes one value per (row edge, column)
+        if (tid < g.cols) {
+            const double dv = __dsub_rn(__ldg(g.vpar + tid), qs[1]);
+            const double dv2 = __dmul_rn(dv, dv);
+            const int r_in = g.rows > 2 ? 1 : 0;
 #pragma unroll
-        for (int k = 0; k < MLK_MAXL; ++k)
-            z[k] = k < L ? (double)cents[((long long)s * L + k) * K + codes[(long long)img * L + k]]
-                         : 0.0;
-        const float* Ws = W + sh.w_off;
-        const bool blas_tree = !sh.small_blas;
-        const double4 q4 = reinterpret_cast<const double4*>(qoi)[img];
-        double qs[4] = {q4.x, q4.y, q4.z, q4.w};
-        if (opt.lam_f32) {
-#pragma unroll
-            for (int k = 0; k < 4; ++k) qs[k] = (double)__double2float_rn(qs[k]);
-        }
-        const int rank = sel_rank[img];
-        double* F;
-        double tmax = -INFINITY;
-        bool nan_t = false;
-        if (rank < 0) {  // warp-uniform
-            // ---- F = AE decode (autoencoder.py:106-110)
-            F = Fbuf;
-            for (int j = lane; j < D; j += 32) {
-                const double fj =
-                    decode_cell(z, Ws, L, D, j, blas_tree && g.tree_cols[j], sh.mean, sh.std);
-                F[j] = fj;
-                nan_t |= fj != fj;
-                tmax = fmax(tmax, fj);
-            }
-        } else {
-            // ---- residual stage (residual.py:60-79, 194-203): O into the
-            //      buffer, replaced in place by recon + q 2eb; contiguous cells
-            //      per lane so the varint stream is written in cell order
-            __syncwarp();
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            const int shift = stage_histogram(Fbuf, Og, D, &bar);
-            F = Fbuf + shift;
-            mbar_wait(&bar, phase);
-            phase ^= 1;
-            const double eb2 = 2.0 * sh.eb;
-            const double inv = 1.0 / eb2;
-            const bool lossless = sh.lossless != 0;
-            const int per = (D + 31) / 32;
-            const int c0 = min(D, lane * per), c1 = min(D, c0 + per);
-            int nb = 0;
-            bool too_big = false;
-            for (int j = c0; j < c1; ++j) {
-                const double rc =
-                    decode_cell(z, Ws, L, D, j, blas_tree && g.tree_cols[j], sh.mean, sh.std);
-                const double r = __dsub_rn(F[j], rc);
-                unsigned long long zz;
-                if (lossless) {
-                    zz = (unsigned long long)__double_as_longlong(r);
-                } else {
-                    const double q = qround(r, eb2, inv);
-                    if (!(fabs(q) < 4611686018427387904.0)) too_big = true;
-                    const long long qi = (long long)q;
-                    zz = ((unsigned long long)qi << 1) ^ (unsigned long long)(qi >> 63);
-                }
-                nb += varint_len(zz);
-            }
-            if (too_big) atomicExch(err_flag, MLK_ERR_CONFIG);
-            int inc = nb;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int t = __shfl_up_sync(FULL, inc, o);
-                if (lane >= o) inc += t;
-            }
-            const int tot = __shfl_sync(FULL, inc, 31);
-            int pos = inc - nb;
-            const long long slot = slot_base[s] + rank;
-            unsigned char* out = varint + slot * vcap;
-            for (int j = c0; j < c1; ++j) {
-                const double rc =
-                    decode_cell(z, Ws, L, D, j, blas_tree && g.tree_cols[j], sh.mean, sh.std);
-                const double r = __dsub_rn(F[j], rc);
-                unsigned long long zz;
-                double fj;
-                if (lossless) {
-                    zz = (unsigned long long)__double_as_longlong(r);
-                    fj = __dadd_rn(rc, r);
-                } else {
-                    const double q = qround(r, eb2, inv);
-                    const long long qi = (long long)q;
-                    zz = ((unsigned long long)qi << 1) ^ (unsigned long long)(qi >> 63);
-                    fj = __dadd_rn(rc, __dmul_rn(q, eb2));
-                }
-                F[j] = fj;
-                nan_t |= fj != fj;
-                tmax = fmax(tmax, fj);
-                while (zz >= 0x80ull) {
-                    out[pos++] = (unsigned char)(zz | 0x80ull);
-                    zz >>= 7;
-                }
-                out[pos++] = (unsigned char)zz;
-            }
-            if (lane == 0) vlen[slot] = tot;
-        }
-
-        // ---- top = max(corrected), s4 = max |a3| (lagrange.py:199-204),
-        //      NaN-propagating like numpy's max
-        double amax = 0.0;
-        bool nan_a = false;
-        if (SEP) {
-            for (int c = lane; c < cols; c += 32) {
-                const double dv = __dsub_rn(__ldg(g.vpar + c), qs[1]);
-                const double dv2 = __dmul_rn(dv, dv);
-                const int r_in = rows > 2 ? 1 : 0;
-#pragma unroll
-                for (int e = 0; e < 2; ++e) {
-                    const double a3 = fabs(__dmul_rn(__ldg(g.hmvol + (e ? 0 : r_in) * cols + c),
-                                                     dv2));
-                    nan_a |= a3 != a3;
-                    amax = fmax(amax, a3);
-                }
-                T[tb.p3c + c] = hm * dv * dv;  // / s4 below
-            }
-        } else {
-            for (int j = lane; j < D; j += 32) {
-                const double dv = __dsub_rn(__ldg(g.vpar + j), qs[1]);
-                const double a3 = fabs(__dmul_rn(__ldg(g.hmvol + j), __dmul_rn(dv, dv)));
+            for (int e = 0; e < 2; ++e) {
+                const double a3 = fabs(__dmul_rn(__ldg(g.hmvol + (e ? 0 : r_in) * g.cols + tid),
+                                                 dv2));
                 nan_a |= a3 != a3;
                 amax = fmax(amax, a3);
             }
         }
-        if (__any_sync(FULL, nan_t)) tmax = __longlong_as_double(0x7ff8000000000000ll);
-        if (__any_sync(FULL, nan_a)) amax = __longlong_as_double(0x7ff8000000000000ll);
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            tmax = np_max2(tmax, __shfl_xor_sync(FULL, tmax, o));
-            amax = np_max2(amax, __shfl_xor_sync(FULL, amax, o));
+    } else {
+        for (int j = tid; j < D; j += PJ_T) {
+            const double dv = __dsub_rn(__ldg(g.vpar + j), qs[1]);
+            const double a3 = fabs(__dmul_rn(__ldg(g.hmvol + j), __dmul_rn(dv, dv)));
+            nan_a |= a3 != a3;
+            amax = fmax(amax, a3);
         }
-        const double top = tmax, s4 = amax;
-        const double sc4 = s4 > 0 ? s4 : 1.0;
-        __syncwarp();  // F complete (the residual pass wrote other lanes' cells)
-        // f_plus = max(corrected, floor * top) (lagrange.py:103-107) in place;
-        // top > 0 excludes NaN.  Separable: each lane rewrites the cells it
-        // reads from here on (its columns).
-        const double fl = top > 0 ? __dmul_rn(opt.floor, top) : 0.0;
-        if (top > 0) {
-            if (SEP) {
+    }
+    if (nan_t) top = __longlong_as_double(0x7ff8000000000000ll);
+    if (nan_a) amax = __longlong_as_double(0x7ff8000000000000ll);
+    block_allmax2(top, amax, C, ph);
+    const double s4 = amax;
+    const double sc4 = s4 > 0 ? s4 : 1.0;
+    // f_plus = max(corrected, floor * top) (lagrange.py:103-107) is applied on
+    // every read below when top > 0 (no NaN then); F keeps the corrected image
+    const double fl = top > 0 ? __dmul_rn(opt.floor, top) : 0.0;
+    if (SEP && tid < g.cols) C.p3c[tid] /= sc4;
+
+    double lam[4] = {0.0, 0.0, 0.0, 0.0};
+    int status = MLK_NEWTON_DEGENERATE, iters = 0;
+    const bool valid = qs[0] > 0 && isfinite(qs[0]) && isfinite(qs[1]) && isfinite(qs[2]) &&
+                       isfinite(qs[3]) && s4 > 0 && top > 0;
+    if (valid) {  // block-uniform
+        const double b[4] = {__ddiv_rn(qs[0], g.s0), __ddiv_rn(__dmul_rn(qs[0], qs[1]), g.s1),
+                             __ddiv_rn(__dmul_rn(qs[0], qs[2]), g.s2),
+                             __ddiv_rn(__dmul_rn(qs[0], qs[3]), s4)};
+        double bmax = 0.0;
 #pragma unroll
-                for (int q = 0; q < 2; ++q) {
-                    const PsItem& it = q ? iB : iA;
-                    if (!it.act) continue;
-                    for (int r = it.r0; r < it.r1; ++r) {
-                        const double fj = F[r * cols + it.c];
-                        F[r * cols + it.c] = fj < fl ? fl : fj;
-                    }
-                }
-            } else {
-                for (int j = lane; j < D; j += 32) {
-                    const double fj = F[j];
-                    F[j] = fj < fl ? fl : fj;
+        for (int k = 0; k < 4; ++k) bmax = fmax(bmax, fabs(b[k]));
+        if (bmax > 0.0 && isfinite(bmax)) {
+            NtCtx X;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) X.w[k] = g.vcls[k];
+            X.is0 = 1.0 / g.s0;
+            X.is4 = 1.0 / s4;
+            X.u = qs[1];
+            X.rows = g.rows;
+            X.cols = g.cols;
+            __syncthreads();  // the p3c tables
+            newton_block<SEP>(F, fl, g, X, b, bmax, opt.step, opt.max_iter, opt.tol, C, lam, status,
+                              iters);
+            // warp 0 holds the result: publish its status so the retry
+            // decision is block-uniform
+            if (warp == 0 && lane == 0) C.status = status;
+            __syncthreads();
+            if (opt.retry && C.status == MLK_NEWTON_MAX_ITER) {
+                double lam2[4];
+                int st2 = 0, it2 = 0;
+                newton_block<SEP>(F, fl, g, X, b, bmax, opt.retry_step, opt.retry_max_iter, opt.tol,
+                                  C, lam2, st2, it2);
+                if (warp == 0 && st2 == MLK_NEWTON_CONVERGED) {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) lam[k] = lam2[k];
+                    status = st2;
+                    iters += it2;
                 }
             }
         }
-        if (SEP) {
-            for (int c = lane; c < cols; c += 32) T[tb.p3c + c] /= sc4;
-        }
-        __syncwarp();
+    }
 
-        double lam[4] = {0.0, 0.0, 0.0, 0.0};
-        int status = MLK_NEWTON_DEGENERATE, iters = 0;
-        const bool valid = qs[0] > 0 && isfinite(qs[0]) && isfinite(qs[1]) && isfinite(qs[2]) &&
-                           isfinite(qs[3]) && s4 > 0 && top > 0;
-        if (valid) {  // warp-uniform
-            const double b[4] = {__ddiv_rn(qs[0], g.s0), __ddiv_rn(__dmul_rn(qs[0], qs[1]), g.s1),
-                                 __ddiv_rn(__dmul_rn(qs[0], qs[2]), g.s2),
-                                 __ddiv_rn(__dmul_rn(qs[0], qs[3]), s4)};
-            double bmax = 0.0;
-#pragma unroll
-            for (int k = 0; k < 4; ++k) bmax = fmax(bmax, fabs(b[k]));
-            if (bmax > 0.0 && isfinite(bmax)) {
-                const double is0 = 1.0 / g.s0, is4 = 1.0 / s4;
-                newton_ps<SEP>(F, g, w, is0, is4, qs[1], b, bmax, opt.step, opt.max_iter,
-                               opt.tol, T, tb, iA, iB, lam, status, iters);
-                if (opt.retry && status == MLK_NEWTON_MAX_ITER) {
-                    double lam2[4];
-                    int st2 = 0, it2 = 0;
-                    newton_ps<SEP>(F, g, w, is0, is4, qs[1], b, bmax, opt.retry_step,
-                                   opt.retry_max_iter, opt.tol, T, tb, iA, iB, lam2, st2, it2);
-                    if (st2 == MLK_NEWTON_CONVERGED) {
-#pragma unroll
-                        for (int k = 0; k < 4; ++k) lam[k] = lam2[k];
-                        status = st2;
-                        iters += it2;
-                    }
-                }
-            }
-        }
-
-        // ---- exception bookkeeping (pipeline.py:263-277), warp-uniform
+    // ---- exception bookkeeping (pipeline.py:263-277), warp 0
+    if (warp == 0) {
         unsigned fl8 = flags[img];
         double lu[4] = {0.0, 0.0, 0.0, 0.0};
         if (!(fl8 & MLK_F_NONFINITE)) {
@@ -722,7 +664,7 @@ k_project_s(const double* __restrict__ f0, const double* __restrict__ stats,
                 bool over = false;
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
-                    const float f = __double2float_rn(lam[k]);
+                    float f = __double2float_rn(lam[k]);
                     if (!isfinite(f)) over = true;
                     lu[k] = (double)f;
                 }
@@ -736,146 +678,124 @@ k_project_s(const double* __restrict__ f0, const double* __restrict__ stats,
                 for (int k = 0; k < 4; ++k) lu[k] = lam[k];
             }
         }
+        if (lane == 0) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) C.lu[k] = lu[k];
+            C.flags = fl8;
+            C.status = status;
+            C.iters = iters;
+        }
+    }
+    __syncthreads();
 
-        // ---- apply_lambda_batch (exact elementwise order, lagrange.py:152-185),
-        //      the final moments and the fast sum of d^2 (O read from L2)
-        const double lu0 = lu[0], lu1 = lu[1], lu2 = lu[2], lu3 = lu[3];
-        const double* ash = g.ash;
-        double sv0 = 0.0, sv1 = 0.0, sv2 = 0.0, ssf = 0.0;
-        if (SEP) {
+    // ---- apply_lambda_batch (exact elementwise order) + final NRMSE
+    const double lu0 = C.lu[0], lu1 = C.lu[1], lu2 = C.lu[2], lu3 = C.lu[3];
+    const double* ash = g.ash;
+    double sv[3] = {0.0, 0.0, 0.0};
+    if (SEP) {
+        // column-fixed threads: ash0, ash1, a3 and vol depend on (row edge,
+        // column) only, so the first two and the last product of t are two
+        // per-thread constants; the order of the additions is unchanged
+        const int cols = g.cols, rows = g.rows, ngrp = PJ_T / cols;
+        const int c = tid % cols, g0 = tid / cols;
+        if (g0 < ngrp) {
+            double P[2], Q[2], V[2];
 #pragma unroll
-            for (int q = 0; q < 2; ++q) {
-                const PsItem& it = q ? iB : iA;
-                if (!it.act) continue;
-                const int c = it.c;
-                double P[2], Q[2], V[2];
-#pragma unroll
-                for (int e = 0; e < 2; ++e) {
-                    const int jj = (e == 0 && rows > 2 ? cols : 0) + c;  // row 1: interior; row 0: edge
-                    const double dv = __dsub_rn(__ldg(g.vpar + jj), qs[1]);
-                    const double a3 = __ddiv_rn(__dmul_rn(__ldg(g.hmvol + jj), __dmul_rn(dv, dv)),
-                                                sc4);
-                    P[e] = __dadd_rn(__dmul_rn(lu0, __ldg(ash + jj)),
-                                     __dmul_rn(lu1, __ldg(ash + D + jj)));
-                    Q[e] = __dmul_rn(lu3, a3);
-                    V[e] = __ldg(g.vol + jj);
-                }
-                const double vpc = __ldg(g.vpar + c);
-                const double* a2r = T + tb.a2c + (it.ce ? rows : 0);
-                for (int r = it.r0; r < it.r1; ++r) {
-                    const bool re = (r == 0) | (r == rows - 1);
-                    const int j = r * cols + c;
-                    const double o = __ldg(Og + j);
-                    double outv = F[j];
-                    if (top > 0) {
-                        double t = __dadd_rn(__dadd_rn(re ? P[1] : P[0], __dmul_rn(lu2, a2r[r])),
-                                             re ? Q[1] : Q[0]);
-                        t = t < -700.0 ? -700.0 : (t > 700.0 ? 700.0 : t);
-                        outv = __dmul_rn(outv, mlk_exp(-t));
-                    }
-                    F[j] = outv;
-                    const double d = __dsub_rn(o, outv);
-                    ssf = fma(d, d, ssf);
-                    const double fv = outv * (re ? V[1] : V[0]);
-                    sv0 += fv;
-                    sv1 += fv * vpc;
-                    sv2 += fv * T[tb.vp2 + r];
-                }
+            for (int e = 0; e < 2; ++e) {
+                const int jj = (e == 0 && rows > 2 ? cols : 0) + c;  // row 1: interior; row 0: edge
+                const double dv = __dsub_rn(__ldg(g.vpar + jj), qs[1]);
+                const double a3 = __ddiv_rn(__dmul_rn(__ldg(g.hmvol + jj), __dmul_rn(dv, dv)), sc4);
+                P[e] = __dadd_rn(__dmul_rn(lu0, __ldg(ash + jj)), __dmul_rn(lu1, __ldg(ash + D + jj)));
+                Q[e] = __dmul_rn(lu3, a3);
+                V[e] = __ldg(g.vol + jj);
             }
-        } else {
-            for (int j = lane; j < D; j += 32) {
-                const double o = __ldg(Og + j);
+            const double vpc = __ldg(g.vpar + c);
+            for (int r = g0; r < rows; r += ngrp) {
+                const bool re = (r == 0) | (r == rows - 1);
+                const int j = r * cols + c;
                 double outv = F[j];
                 if (top > 0) {
-                    const double dv = __dsub_rn(__ldg(g.vpar + j), qs[1]);
-                    const double a3 =
-                        __ddiv_rn(__dmul_rn(__ldg(g.hmvol + j), __dmul_rn(dv, dv)), sc4);
-                    double t = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(lu0, __ldg(ash + j)),
-                                                             __dmul_rn(lu1, __ldg(ash + D + j))),
+                    double t = __dadd_rn(__dadd_rn(re ? P[1] : P[0],
                                                    __dmul_rn(lu2, __ldg(ash + 2 * D + j))),
-                                         __dmul_rn(lu3, a3));
+                                         re ? Q[1] : Q[0]);
                     t = t < -700.0 ? -700.0 : (t > 700.0 ? 700.0 : t);
-                    outv = __dmul_rn(outv, mlk_exp(-t));
+                    outv = __dmul_rn(fmax(outv, fl), mlk_exp(-t));
                 }
                 F[j] = outv;
-                const double d = __dsub_rn(o, outv);
-                ssf = fma(d, d, ssf);
-                const double fv = outv * __ldg(g.vol + j);
-                sv0 += fv;
-                sv1 += fv * __ldg(g.vpar + j);
-                sv2 += fv * __ldg(g.vperp2 + j);
+                const double d = __dsub_rn(O[j], outv);
+                O[j] = __dmul_rn(d, d);
+                const double fv = outv * (re ? V[1] : V[0]);
+                sv[0] += fv;
+                sv[1] += fv * vpc;
+                sv[2] += fv * __ldg(g.vperp2 + j);
             }
         }
-        const double n = warp_sum(sv0);
-        const double u = warp_sum(sv1) / n;
-        const double n2 = warp_sum(sv2);
-        double sse = warp_sum(ssf);
-        // T_par numerator over the own cells (kept only when not an exception)
-        double t1 = 0.0;
-        if (SEP) {
-#pragma unroll
-            for (int q = 0; q < 2; ++q) {
-                const PsItem& it = q ? iB : iA;
-                if (!it.act) continue;
-                const int c = it.c;
-                const double dv = __ldg(g.vpar + c) - u;
-                const double dv2 = dv * dv;
-                const double vi = __ldg(g.vol + (rows > 2 ? cols : 0) + c), ve = __ldg(g.vol + c);
-                for (int r = it.r0; r < it.r1; ++r) {
-                    const bool re = (r == 0) | (r == rows - 1);
-                    t1 += F[r * cols + c] * (re ? ve : vi) * dv2;
-                }
+    } else {
+        for (int j = tid; j < D; j += PJ_T) {
+            double outv = F[j];
+            if (top > 0) {
+                const double dv = __dsub_rn(__ldg(g.vpar + j), qs[1]);
+                const double a3 =
+                    __ddiv_rn(__dmul_rn(__ldg(g.hmvol + j), __dmul_rn(dv, dv)), sc4);
+                double t = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(lu0, __ldg(ash + j)),
+                                                         __dmul_rn(lu1, __ldg(ash + D + j))),
+                                               __dmul_rn(lu2, __ldg(ash + 2 * D + j))),
+                                     __dmul_rn(lu3, a3));
+                t = t < -700.0 ? -700.0 : (t > 700.0 ? 700.0 : t);
+                outv = __dmul_rn(fmax(outv, fl), mlk_exp(-t));
             }
+            F[j] = outv;
+            const double d = __dsub_rn(O[j], outv);
+            O[j] = __dmul_rn(d, d);  // each thread only reads/writes its own cells here
+            const double fv = outv * __ldg(g.vol + j);
+            sv[0] += fv;
+            sv[1] += fv * __ldg(g.vpar + j);
+            sv[2] += fv * __ldg(g.vperp2 + j);
+        }
+    }
+    block_allsum(sv, C, ph);  // barrier: every d^2 is in O
+    const double sse = block_pairwise(O, pw, C);
+    unsigned fl8 = C.flags;
+    const double4 st = reinterpret_cast<const double4*>(stats)[img];
+    const double range = __dsub_rn(st.x, st.y);
+    const double rms = sqrt(__ddiv_rn(sse, (double)D));
+    const double ferr = range > 0 ? __ddiv_rn(rms, range) : (rms == 0.0 ? 0.0 : INFINITY);
+    if (!(ferr <= opt.tau)) fl8 |= MLK_F_EXC_GATE;
+    const bool exc = (fl8 & MLK_F_EXCEPTION) != 0;
+
+    const double n = sv[0];
+    const double u = sv[1] / n;
+    double tl = 0.0;
+    if (!exc) {
+        double t1[1] = {0.0};
+        for (int j = tid; j < D; j += PJ_T) {
+            const double dv = __ldg(g.vpar + j) - u;
+            t1[0] += F[j] * __ldg(g.vol + j) * dv * dv;
+        }
+        block_allsum(t1, C, ph);
+        tl = t1[0];
+    }
+    if (tid == 0) {
+        flags[img] = (unsigned char)fl8;
+        status_out[img] = C.status;
+        iters_out[img] = C.iters;
+        ferr_out[img] = ferr;
+        double4* lo = reinterpret_cast<double4*>(lam_out) + img;
+        double4* qo = reinterpret_cast<double4*>(qst_out) + img;
+        double4* fo = reinterpret_cast<double4*>(fqoi_out) + img;
+        if (exc) {
+            *lo = make_double4(0.0, 0.0, 0.0, 0.0);
+            *qo = make_double4(0.0, 0.0, 0.0, 0.0);
+            *fo = q4;
+            fsse_out[img] = 0.0;
         } else {
-            for (int j = lane; j < D; j += 32) {
-                const double dv = __ldg(g.vpar + j) - u;
-                t1 += F[j] * __ldg(g.vol + j) * dv * dv;
-            }
+            *lo = make_double4(lu0, lu1, lu2, lu3);
+            *qo = make_double4(qs[0], qs[1], qs[2], qs[3]);
+            const double nan = __longlong_as_double(0x7ff8000000000000ll);
+            *fo = n > 0 ? make_double4(n, u, hm * sv[2] / n, hm * tl / n)
+                        : make_double4(n, nan, nan, nan);
+            fsse_out[img] = sse;
         }
-        const double tl = warp_sum(t1);
-        const double4 st4 = reinterpret_cast<const double4*>(stats)[img];
-        const double range = __dsub_rn(st4.x, st4.y);
-        double ferr = range > 0 ? sqrt(sse / (double)D) / range : (sse == 0.0 ? 0.0 : INFINITY);
-        // numpy's pairwise order decides only when the fast sum (|rel err| <
-        // (D + 16) u with u = 2^-53, against < (log2 D + 8) u for the pairwise
-        // sum) cannot: within 1e-12 relative of tau
-        if (range > 0 && isfinite(ferr) &&
-            fabs(ferr - opt.tau) <= 1e-12 * opt.tau + 2.0 * (double)(D + 64) * 0x1p-53 * ferr) {
-            __syncwarp();
-            for (int j = lane; j < D; j += 32) {
-                const double d = __dsub_rn(__ldg(Og + j), F[j]);
-                F[j] = __dmul_rn(d, d);
-            }
-            __syncwarp();
-            sse = warp_pairwise_sum(F, pw, leaf);
-            const double rms = sqrt(__ddiv_rn(sse, (double)D));
-            ferr = __ddiv_rn(rms, range);
-        }
-        if (!(ferr <= opt.tau)) fl8 |= MLK_F_EXC_GATE;
-        const bool exc = (fl8 & MLK_F_EXCEPTION) != 0;
-        if (lane == 0) {
-            flags[img] = (unsigned char)fl8;
-            status_out[img] = status;
-            iters_out[img] = iters;
-            ferr_out[img] = ferr;
-            double4* lo = reinterpret_cast<double4*>(lam_out) + img;
-            double4* qo = reinterpret_cast<double4*>(qst_out) + img;
-            double4* fo = reinterpret_cast<double4*>(fqoi_out) + img;
-            if (exc) {
-                *lo = make_double4(0.0, 0.0, 0.0, 0.0);
-                *qo = make_double4(0.0, 0.0, 0.0, 0.0);
-                *fo = q4;
-                fsse_out[img] = 0.0;
-            } else {
-                *lo = make_double4(lu0, lu1, lu2, lu3);
-                *qo = make_double4(qs[0], qs[1], qs[2], qs[3]);
-                const double nan = __longlong_as_double(0x7ff8000000000000ll);
-                *fo = n > 0 ? make_double4(n, u, hm * n2 / n, hm * tl / n)
-                            : make_double4(n, nan, nan, nan);
-                fsse_out[img] = sse;
-            }
-        }
-        __syncwarp();
     }
 }
 
@@ -912,32 +832,23 @@ extern "C" int mlk_project(const double* f0, const double* stats, const double* 
                            double* lam, double* qst, int32_t* status, int32_t* iters,
                            double* ferr, double* fqoi, double* fsse, uint8_t* varint,
                            int64_t varint_cap, int64_t* varint_len, int32_t* err_flag,
+                           const int32_t* img_list, int32_t n_list, int32_t ctas_per_sm,
                            cudaStream_t stream) {
-    if (total <= 0) return MLK_OK;
+    (void)ctas_per_sm;
+    const int n_work = img_list ? n_list : total;
+    if (total <= 0 || n_work <= 0) return MLK_OK;
     const int D = grid_h->D;
     if (D > MLK_MAX_D || L < 1 || L > MLK_MAXL) return MLK_ERR_DIM;
     PwPlan pw = mlk_make_pw_plan(D);
-    const bool sep = grid_h->sep && grid_h->rows <= PS_MAXRC && grid_h->cols <= PS_MAXRC &&
-                     grid_h->cols > 0 && grid_h->rows >= 2;
-    const size_t sm =
-        (size_t)ps_warp_doubles(D, grid_h->rows, grid_h->cols, pw.n_leaves) * sizeof(double);
-    if (sm > 200 * 1024) return MLK_ERR_DIM;
+    const size_t sm = (size_t)(((D + 3) / 2) * 2 + D) * sizeof(double);
+    const bool sep = grid_h->sep && grid_h->rows <= 64 && grid_h->cols <= 64 && grid_h->cols > 0;
     const MlkNewton opt = *opts_h;
-    int dev = 0, n_sm = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
-#define MLK_PJ_LAUNCH(SEP)                                                                      \
-    do {                                                                                        \
-        cudaFuncSetAttribute(k_project_s<SEP>, cudaFuncAttributeMaxDynamicSharedMemorySize,     \
-                             (int)sm);                                                          \
-        int per_sm = 1;                                                                         \
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_project_s<SEP>, 32, sm);      \
-        const int grid = (int)std::min<long long>(total, (long long)n_sm * std::max(per_sm, 1)); \
-        k_project_s<SEP><<<grid, 32, sm, stream>>>(                                             \
-            f0, stats, qoi, shards, n_shards, total, *grid_h, pw, W, L, cents, K, codes,        \
-            sel_rank, slot_base, opt, flags, lam, qst, status, iters, ferr, fqoi, fsse, varint,  \
-            (long long)varint_cap, reinterpret_cast<long long*>(varint_len), err_flag);         \
-    } while (0)
+#define MLK_PJ_LAUNCH(SEP)                                                                     \
+    cudaFuncSetAttribute(k_project<SEP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); \
+    k_project<SEP><<<n_work, PJ_T, sm, stream>>>(                                               \
+        f0, stats, qoi, shards, n_shards, *grid_h, pw, W, L, cents, K, codes, sel_rank,         \
+        slot_base, opt, flags, lam, qst, status, iters, ferr, fqoi, fsse, varint,               \
+        (long long)varint_cap, reinterpret_cast<long long*>(varint_len), err_flag, img_list)
     if (sep) {
         MLK_PJ_LAUNCH(true);
     } else {

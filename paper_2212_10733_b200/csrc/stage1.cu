@@ -10,7 +10,7 @@
 namespace {
 
 constexpr int S1_WARPS = 15;  // one CTA per SM: W once + 15 staged histograms in 221 KB
-constexpr int S1_IMGS = 4;  // images per warp per block
+constexpr int S1_IMGS = 12;  // images per warp per block (~5 waves of one CTA per SM at configs[2])
 
 __host__ __device__ inline int panel_len(int rem) {
     // OpenBLAS level3 K-panel rule, GEMM_Q = 384, GEMM_UNROLL_M = 16
@@ -86,6 +86,9 @@ k_stage1(const double* __restrict__ f0, const MlkShard* __restrict__ shards, int
         if (j_img >= sh.n_img) break;
         const int img = sh.img_off + j_img;
         const double* x = shard_image(f0, sh, j_img, D);
+        // this warp's next image into L2 while this one is staged and reduced
+        if (lane == 0 && k_img + 1 < S1_IMGS && j_img + S1_WARPS < sh.n_img)
+            prefetch_l2_histogram(shard_image(f0, sh, j_img + S1_WARPS, D), D);
         __syncwarp();
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         const int shift = stage_histogram(tbuf, x, D, bar);

@@ -85,9 +85,11 @@ Z6_HD inline int extra_lbits(int c) {
 }
 Z6_HD inline int extra_dbits(int c) { return c < 4 ? 0 : (c - 2) / 2; }
 Z6_HD inline int extra_blbits(int c) { return c == 16 ? 2 : (c == 17 ? 3 : (c == 18 ? 7 : 0)); }
+// trees.c bl_order {16, 17, 18, 0, 8, 7, 9, 6, 10, 5, 11, 4, 12, 3, 13, 2, 14, 1,
+// 15} as 5-bit fields of two constants (no per-call local array)
 Z6_HD inline int bl_order(int i) {
-    const uint8_t o[BL_CODES] = {16, 17, 18, 0, 8, 7, 9, 6, 10, 5, 11, 4, 12, 3, 13, 2, 14, 1, 15};
-    return o[i];
+    return (int)((i < 12 ? (0x22caa324e804a30ull >> (5 * i)) : (0x3c2e1346cull >> (5 * (i - 12))))
+                 & 31u);
 }
 
 // canonical code assignment (trees.c gen_codes)

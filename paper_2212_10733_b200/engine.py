@@ -642,7 +642,53 @@ def compress_device(f0: torch.Tensor, specs, dgrid: DeviceGrid, cfg, timer: Time
         cnt_h, ebhi_h = _d2h(sel_cnt, eb_hi)
         cntg_h = cnt_h
 
+    # ---- projection of the images WITHOUT residuals does not need the error
+    #      bounds: it runs on a side stream under the error-bound search
+    #      (capped CTAs per SM leave room for the probe kernels)
+    n_sel = int(cnt_h.sum())
+    vcap = ((10 * D + 15) // 16) * 16
+    varint = T("varint", (max(1, n_sel) * vcap,), torch.uint8)
+    vlen = T("vlen", (max(1, n_sel),), i64)
+    opts = MlkNewton(step=cfg.newton.step, max_iter=cfg.newton.max_iter,
+                     retry=int(cfg.newton.retry), tol=cfg.newton.tol, floor=cfg.newton.floor,
+                     retry_step=cfg.newton.retry_step, retry_max_iter=cfg.newton.retry_max_iter,
+                     lam_f32=int(cfg.lambda_precision == "f32"), tau=cfg.tau)
+    lam = T("lam", (total, 4), f64)
+    qst = T("qst", (total, 4), f64)
+    status = T("status", (total,), i32)
+    iters = T("iters", (total,), i32)
+    ferr = T("ferr", (total,), f64)
+    fqoi = T("fqoi", (total, 4), f64)
+    fsse = T("fsse", (total,), f64)
+    errf = T("errf", (1,), i32)
+    errf.zero_()
+    list_sel = T("list_sel", (max(1, total),), i32)
+    list_non = T("list_non", (max(1, total),), i32)
+    nsel_d = T("nsel_d", (1,), i32)
+    call("mlk_split_flags", flags, total, _lib.F_SELECTED, list_sel, list_non, nsel_d)
+    main = torch.cuda.current_stream(dev)
+    side = _side_stream(dev) if PROJECT_OVERLAP else main
+    if side is not main:
+        ev_split = torch.cuda.Event()
+        ev_split.record(main)
+        side.wait_event(ev_split)
+    call("mlk_project", f0, stats, qoi, sh_d, S, total, dgrid.addr, W, L, cents, K, codes,
+         sel_rank, None, ctypes.addressof(opts), flags, lam, qst, status, iters, ferr, fqoi,
+         fsse, varint, vcap, vlen, errf, list_non, total - n_sel,
+         PROJECT_OVERLAP_CTAS if side is not main else PROJECT_CTAS, stream=side.cuda_stream)
+    ev_non = torch.cuda.Event()
+    ev_non.record(side)
+
     timer.mark("eb_search")
+    # the search is a chain of small launches and host round trips: on a
+    # high-priority stream its CTAs go first whenever the side stream's
+    # projection CTAs retire
+    hi_ctx = None
+    if side is not main:
+        hi = _hi_stream(dev)
+        hi.wait_stream(main)
+        hi_ctx = torch.cuda.stream(hi)
+        hi_ctx.__enter__()
     # ---- error-bound search, LOOKAHEAD levels per launch
     states = []
     for s in range(S):
@@ -711,32 +757,20 @@ def compress_device(f0: torch.Tensor, specs, dgrid: DeviceGrid, cfg, timer: Time
         table[s].eb = eb[s]
         table[s].lossless = int(lossless[s])
 
+    if hi_ctx is not None:
+        hi_ctx.__exit__(None, None, None)
+        main.wait_stream(hi)
     timer.mark("newton")
     slot_base_h = np.concatenate([[0], np.cumsum(cnt_h)[:-1]]).astype(np.int32)
-    n_sel = int(cnt_h.sum())
     ws.begin()
     sh_d = ws.stage(np.frombuffer(bytes(table), dtype=np.uint8))
     slot_base = ws.stage(slot_base_h)
     ws.flush()
-    vcap = ((10 * D + 15) // 16) * 16
-    varint = T("varint", (max(1, n_sel) * vcap,), torch.uint8)
-    vlen = T("vlen", (max(1, n_sel),), i64)
-    opts = MlkNewton(step=cfg.newton.step, max_iter=cfg.newton.max_iter,
-                     retry=int(cfg.newton.retry), tol=cfg.newton.tol, floor=cfg.newton.floor,
-                     retry_step=cfg.newton.retry_step, retry_max_iter=cfg.newton.retry_max_iter,
-                     lam_f32=int(cfg.lambda_precision == "f32"), tau=cfg.tau)
-    lam = T("lam", (total, 4), f64)
-    qst = T("qst", (total, 4), f64)
-    status = T("status", (total,), i32)
-    iters = T("iters", (total,), i32)
-    ferr = T("ferr", (total,), f64)
-    fqoi = T("fqoi", (total, 4), f64)
-    fsse = T("fsse", (total,), f64)
-    errf = T("errf", (1,), i32)
-    errf.zero_()
-    call("mlk_project", f0, stats, qoi, sh_d, S, total, dgrid.addr, W, L, cents, K, codes,
-         sel_rank, slot_base, ctypes.addressof(opts), flags, lam, qst, status, iters, ferr, fqoi,
-         fsse, varint, vcap, vlen, errf)
+    if n_sel:
+        call("mlk_project", f0, stats, qoi, sh_d, S, total, dgrid.addr, W, L, cents, K, codes,
+             sel_rank, slot_base, ctypes.addressof(opts), flags, lam, qst, status, iters, ferr,
+             fqoi, fsse, varint, vcap, vlen, errf, list_sel, n_sel, PROJECT_CTAS)
+    main.wait_event(ev_non)
     exc_list = T("exc_list", (total,), i32)
     exc_cnt = T("exc_cnt", (S,), i32)
     call("mlk_list_flags", flags, sh_d, S, _lib.F_EXCEPTION, exc_list, exc_cnt)
@@ -948,6 +982,32 @@ def _scratch(dev, name, nbytes):
         _SCRATCH[key] = buf = torch.empty(max(1, int(nbytes * 1.25)), dtype=torch.uint8,
                                           device=dev)
     return buf
+
+
+# project the residual-free images on a side stream under the error-bound
+# search; their kernel keeps PROJECT_OVERLAP_CTAS one-warp CTAs per SM
+PROJECT_OVERLAP = os.environ.get("MLK_PROJECT_OVERLAP", "1") != "0"
+PROJECT_OVERLAP_CTAS = int(os.environ.get("MLK_PROJECT_OVERLAP_CTAS", "9"))
+PROJECT_CTAS = int(os.environ.get("MLK_PROJECT_CTAS", "0"))  # 0: occupancy max
+_SIDE_STREAMS = {}
+
+
+def _side_stream(dev):
+    s = _SIDE_STREAMS.get(dev.index)
+    if s is None:
+        s = _SIDE_STREAMS[dev.index] = torch.cuda.Stream(device=dev, priority=0)
+    return s
+
+
+_HI_STREAMS = {}
+
+
+def _hi_stream(dev):
+    s = _HI_STREAMS.get(dev.index)
+    if s is None:
+        lo, hi = torch.cuda.Stream.priority_range()
+        s = _HI_STREAMS[dev.index] = torch.cuda.Stream(device=dev, priority=hi)
+    return s
 
 
 def _deflate_pool(dev, n_workers):
