@@ -157,8 +157,11 @@ int mlk_zlib_compress6(const uint8_t* in, const int64_t* in_off, const int64_t* 
 /* Same bytes as mlk_zlib_compress6, one warp per stream with the working set
  * in shared memory, for the streams with nmin < in_len <= nmax (<= 16000);
  * run it over the size tiers, then mlk_zlib_compress6 for larger streams.
- * sym_scratch: n * sym_cap bytes (sym_cap >= 3 * nmax + 3) for the LZ77
- * symbol buffers; prof (may be NULL): 10 u64 cycle/counter accumulators. */
+ * Two launches on `stream`: the LZ77 parse, then the Huffman trees and the
+ * bit stream (one fused launch when prof is given).  sym_scratch: n *
+ * sym_cap bytes (sym_cap >= 3 * nmax + 19, a multiple of 16) for the LZ77
+ * symbol buffers, whose last 16 bytes carry the parse's summary to the
+ * second launch; prof (may be NULL): 12 u64 cycle/counter accumulators. */
 int mlk_zlib_compress6_warp(const uint8_t* in, const int64_t* in_off, const int64_t* in_len,
                             int32_t n, int32_t nmin, int32_t nmax, uint8_t* out,
                             const int64_t* out_off, int64_t out_cap, int64_t* out_len,

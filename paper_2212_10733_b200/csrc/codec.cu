@@ -391,6 +391,8 @@ namespace wz {
 struct Lay {
     int nmax, T, direct;  // direct: a 32K-entry table indexed by the hash
     int win, p1, p4, hash, trees, hist, total;
+    int total_lz;         // phase 1 only (window + chain tables)
+    int total_fl;         // phase 2 only (trees + histogram, from offset 0)
 };
 
 __host__ __device__ inline int pow2ge(int x) {
@@ -748,6 +750,8 @@ __host__ __device__ inline Lay layout(int nmax) {
     L.trees = b0;
     L.hist = b0 + al16((int)sizeof(DTrees));
     const int flush = al16((int)sizeof(DTrees)) + 4 * 320;
+    L.total_lz = o + chains;
+    L.total_fl = flush;
     o += chains > flush ? chains : flush;
     L.total = o;
     return L;
@@ -755,7 +759,13 @@ __host__ __device__ inline Lay layout(int nmax) {
 
 }  // namespace wz
 
-template <bool PROF>
+// PH = 3: the whole stream per warp.  PH = 1: the LZ77 parse only (window,
+// hash chains, lazy matching -> the symbol buffer; the stream's symbol count
+// and Adler-32 go to the last 16 bytes of its symbol slot).  PH = 2: Huffman
+// trees + bit stream from those.  The two halves as separate launches keep
+// each kernel's code and shared memory small: more resident warps, fewer
+// instruction-cache misses.
+template <bool PROF, int PH>
 __global__ void __launch_bounds__(512)
 k_deflate_warp(const uint8_t* __restrict__ in, const long long* __restrict__ in_off,
                const long long* __restrict__ in_len, int n_streams, uint8_t* __restrict__ out,
@@ -770,12 +780,13 @@ k_deflate_warp(const uint8_t* __restrict__ in, const long long* __restrict__ in_
     const wz::Lay Ly = wz::layout(nmax);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int ZW = blockDim.x >> 5;
-    uint8_t* base = zsm + (size_t)warp * Ly.total;
+    uint8_t* base = zsm + (size_t)warp * (PH == 3 ? Ly.total : (PH == 1 ? Ly.total_lz
+                                                                          : Ly.total_fl));
     uint8_t* win = base + Ly.win;
     uint16_t* p1 = reinterpret_cast<uint16_t*>(base + Ly.p1);
     uint16_t* p4 = reinterpret_cast<uint16_t*>(base + Ly.p4);
     uint16_t* htab = reinterpret_cast<uint16_t*>(base + Ly.hash);
-    wz::DTrees* trees = reinterpret_cast<wz::DTrees*>(base + Ly.trees);
+    wz::DTrees* trees = reinterpret_cast<wz::DTrees*>(base + (PH == 2 ? 0 : Ly.trees));
     const unsigned FULL = 0xffffffffu;
     const unsigned lt_mask = (1u << lane) - 1u;
     const int gw = blockIdx.x * ZW + warp, nw = gridDim.x * ZW;
@@ -798,6 +809,12 @@ k_deflate_warp(const uint8_t* __restrict__ in, const long long* __restrict__ in_
         const uint8_t* src = in + in_off[s];
         uint8_t* sym = sym_g + (long long)s * sym_cap;
         long long t_0 = PROF ? clock64() : 0;
+        unsigned ad_a = 0, ad_b = 0;
+        int sym_next = 0, strstart = 0;
+        long long t_1 = 0, t_2 = 0, t_3 = 0, t_lm = 0;
+        int n_calls = 0, n_rounds = 0, n_cands = 0;
+        unsigned* meta = reinterpret_cast<unsigned*>(sym + sym_cap - 16);
+        if constexpr ((PH & 1) != 0) {
         // ---- window + zero pad, Adler-32 (lane-parallel sums)
         unsigned long long sa = 0, sb = 0;
         for (int i = lane; i < n; i += 32) {
@@ -811,11 +828,11 @@ k_deflate_warp(const uint8_t* __restrict__ in, const long long* __restrict__ in_
             sa += __shfl_xor_sync(FULL, sa, o);
             sb += __shfl_xor_sync(FULL, sb, o);
         }
-        const unsigned ad_a = (unsigned)((1 + sa) % 65521ull);
-        const unsigned ad_b = (unsigned)(((unsigned long long)n + sb) % 65521ull);
+        ad_a = (unsigned)((1 + sa) % 65521ull);
+        ad_b = (unsigned)(((unsigned long long)n + sb) % 65521ull);
         for (int i = lane; i < Ly.T; i += 32) htab[i] = 0;
         __syncwarp();
-        long long t_1 = PROF ? clock64() : 0;
+        t_1 = PROF ? clock64() : 0;
         // ---- prev[] (hash chains), 32 positions per step.  Table entries
         //      are position + 1; a probed entry's key is re-derived from the
         //      window (no key storage), direct mode indexes by the hash.
@@ -869,7 +886,7 @@ k_deflate_warp(const uint8_t* __restrict__ in, const long long* __restrict__ in_
             }
             __syncwarp();
         }
-        long long t_2 = PROF ? clock64() : 0;
+        t_2 = PROF ? clock64() : 0;
         for (int p = lane; p < n; p += 32)
             if (p >= n_ins) p1[p] = 0;
         __syncwarp();
@@ -881,13 +898,13 @@ k_deflate_warp(const uint8_t* __restrict__ in, const long long* __restrict__ in_
             p4[p] = (uint16_t)x;
         }
         __syncwarp();
-        long long t_3 = PROF ? clock64() : 0;
-        long long t_lm = 0;
-        int n_calls = 0, n_rounds = 0, n_cands = 0;
+        t_3 = PROF ? clock64() : 0;
         // ---- deflate_slow, warp-uniform state
-        int strstart = 0, lookahead = n;
+        strstart = 0;
+        int lookahead = n;
         int match_length = z6::MIN_MATCH - 1, prev_length, prev_match, match_start = 0;
-        int match_available = 0, sym_next = 0;
+        int match_available = 0;
+        sym_next = 0;
         while (lookahead > 0) {
             if (match_length < z6::MIN_MATCH) {
                 // no pending match: a run of positions with an empty hash head
@@ -997,10 +1014,27 @@ k_deflate_warp(const uint8_t* __restrict__ in, const long long* __restrict__ in_
             sym_next += 3;
         }
         __syncwarp();
+        if constexpr (PH == 1) {
+            if (lane == 0) {
+                meta[0] = (unsigned)sym_next;
+                meta[1] = (unsigned)strstart;
+                meta[2] = ad_a;
+                meta[3] = ad_b;
+            }
+            __syncwarp();
+            continue;
+        }
+        } else {  // PH == 2: the parse phase 1 left in the symbol slot
+            sym_next = (int)meta[0];
+            strstart = (int)meta[1];
+            ad_a = meta[2];
+            ad_b = meta[3];
+        }
         long long t_4 = PROF ? clock64() : 0;
         // ---- trees (lane 0) + bit stream (all lanes); prev tables are dead now
         wz::DTrees& t = *trees;
-        unsigned* hist = reinterpret_cast<unsigned*>(base + Ly.hist);
+        unsigned* hist = reinterpret_cast<unsigned*>(base + (PH == 2 ? Ly.hist - Ly.trees
+                                                                   : Ly.hist));
         __shared__ int sh_kind[16];
         __shared__ long long sh_hbits[16];
         for (int i = lane; i < 320; i += 32) hist[i] = 0u;
@@ -1085,7 +1119,8 @@ k_deflate_warp(const uint8_t* __restrict__ in, const long long* __restrict__ in_
                 dst[b0 + 2] = (uint8_t)~strstart;
                 dst[b0 + 3] = (uint8_t)(~strstart >> 8);
             }
-            for (int i = lane; i < strstart; i += 32) dst[b0 + 4 + i] = win[i];
+            for (int i = lane; i < strstart; i += 32)
+                dst[b0 + 4 + i] = (PH & 1) ? win[i] : src[i];
             nbytes = b0 + 4 + strstart;
         } else {
             const uint16_t* lcode = kind == 1 ? tb.sl_code : t.lt.code;
@@ -1201,35 +1236,48 @@ extern "C" int mlk_zlib_compress6(const uint8_t* in, const int64_t* in_off, cons
     return cudaGetLastError() == cudaSuccess ? MLK_OK : MLK_ERR_CUDA;
 }
 
+// launches one size tier: PROF -> the whole-stream kernel with phase clocks;
+// otherwise phase 1 (LZ77) then phase 2 (trees + bits) on the same stream
+template <int PH>
+static int launch_phase(const uint8_t* in, const int64_t* in_off, const int64_t* in_len,
+                        int32_t n, int32_t nmin, int32_t nmax, uint8_t* out,
+                        const int64_t* out_off, int64_t out_cap, int64_t* out_len,
+                        int32_t n_blocks, uint8_t* sym_scratch, int64_t sym_cap, uint64_t* prof,
+                        int32_t* counter, cudaStream_t stream) {
+    const wz::Lay Ly = wz::layout(nmax);
+    const int per_warp = PH == 3 ? Ly.total : (PH == 1 ? Ly.total_lz : Ly.total_fl);
+    // two blocks per SM when they fit, up to 16 warps each
+    int zw = (110 * 1024) / per_warp;
+    if (zw < 1) zw = (220 * 1024) / per_warp;
+    zw = zw < 1 ? 1 : (zw > 16 ? 16 : zw);
+    const size_t sm = (size_t)zw * per_warp;
+    if (sm > 227 * 1024) return MLK_ERR_CONFIG;
+    auto kern = prof ? k_deflate_warp<true, PH> : k_deflate_warp<false, PH>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    kern<<<n_blocks, 32 * zw, sm, stream>>>(
+        in, reinterpret_cast<const long long*>(in_off), reinterpret_cast<const long long*>(in_len),
+        n, out, reinterpret_cast<const long long*>(out_off), (long long)out_cap,
+        reinterpret_cast<long long*>(out_len), nmin, nmax, sym_scratch, (long long)sym_cap,
+        reinterpret_cast<unsigned long long*>(prof), counter);
+    return cudaGetLastError() == cudaSuccess ? MLK_OK : MLK_ERR_CUDA;
+}
+
 static int launch_deflate_warp(const uint8_t* in, const int64_t* in_off, const int64_t* in_len,
                                int32_t n, int32_t nmin, int32_t nmax, uint8_t* out,
                                const int64_t* out_off, int64_t out_cap, int64_t* out_len,
                                int32_t n_blocks, uint8_t* sym_scratch, int64_t sym_cap,
                                uint64_t* prof, int32_t* counter, cudaStream_t stream) {
     if (n <= 0) return MLK_OK;
-    if (nmax > 16000 || nmax < 1 || sym_cap < 3LL * nmax + 3) return MLK_ERR_CONFIG;
+    if (nmax > 16000 || nmax < 1 || sym_cap < 3LL * nmax + 19) return MLK_ERR_CONFIG;
     if (ensure_tables() != MLK_OK) return MLK_ERR_CUDA;
-    const wz::Lay Ly = wz::layout(nmax);
-    // two blocks per SM when they fit, up to 16 warps each
-    int zw = (110 * 1024) / Ly.total;
-    if (zw < 1) zw = (220 * 1024) / Ly.total;
-    zw = zw < 1 ? 1 : (zw > 16 ? 16 : zw);
-    size_t sm = (size_t)zw * Ly.total;
-    if (sm > 227 * 1024) return MLK_ERR_CONFIG;
-#define MLK_DW_LAUNCH(P)                                                                        \
-    cudaFuncSetAttribute(k_deflate_warp<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); \
-    k_deflate_warp<P><<<n_blocks, 32 * zw, sm, stream>>>(                                        \
-        in, reinterpret_cast<const long long*>(in_off), reinterpret_cast<const long long*>(in_len), \
-        n, out, reinterpret_cast<const long long*>(out_off), (long long)out_cap,                  \
-        reinterpret_cast<long long*>(out_len), nmin, nmax, sym_scratch, (long long)sym_cap,        \
-        reinterpret_cast<unsigned long long*>(prof), counter)
-    if (prof) {
-        MLK_DW_LAUNCH(true);
-    } else {
-        MLK_DW_LAUNCH(false);
-    }
-#undef MLK_DW_LAUNCH
-    return cudaGetLastError() == cudaSuccess ? MLK_OK : MLK_ERR_CUDA;
+    if (prof)
+        return launch_phase<3>(in, in_off, in_len, n, nmin, nmax, out, out_off, out_cap, out_len,
+                               n_blocks, sym_scratch, sym_cap, prof, counter, stream);
+    int rc = launch_phase<1>(in, in_off, in_len, n, nmin, nmax, out, out_off, out_cap, out_len,
+                             n_blocks, sym_scratch, sym_cap, nullptr, counter, stream);
+    if (rc != MLK_OK) return rc;
+    return launch_phase<2>(in, in_off, in_len, n, nmin, nmax, out, out_off, out_cap, out_len,
+                           n_blocks, sym_scratch, sym_cap, nullptr, nullptr, stream);
 }
 
 extern "C" int mlk_zlib_compress6_warp(const uint8_t* in, const int64_t* in_off,

@@ -770,13 +770,14 @@ def compress_device(f0: torch.Tensor, specs, dgrid: DeviceGrid, cfg, timer: Time
         call("mlk_project", f0, stats, qoi, sh_d, S, total, dgrid.addr, W, L, cents, K, codes,
              sel_rank, slot_base, ctypes.addressof(opts), flags, lam, qst, status, iters, ferr,
              fqoi, fsse, varint, vcap, vlen, errf, list_sel, n_sel, PROJECT_CTAS)
+    timer.mark("deflate")
+    # DEFLATE needs only the residual images' varint streams: it starts while
+    # the side stream may still be projecting the others
+    zout, zoff, zlen = deflate_launch(ws, varint, vcap, vlen, n_sel, dev)
     main.wait_event(ev_non)
     exc_list = T("exc_list", (total,), i32)
     exc_cnt = T("exc_cnt", (S,), i32)
     call("mlk_list_flags", flags, sh_d, S, _lib.F_EXCEPTION, exc_list, exc_cnt)
-
-    timer.mark("deflate")
-    zout, zoff, zlen = deflate_launch(ws, varint, vcap, vlen, n_sel, dev)
     if comm is None:
         zlen_h, exc_h, errf_h, excl_h = _d2h(zlen[:max(1, n_sel)], exc_cnt, errf, exc_list)
     else:
@@ -1051,7 +1052,7 @@ def _run_deflate(ws, varint, in_off, vlen, n, zout, zoff, zcap, zlen, dev, max_w
     streams (a sparse tier is bounded by single-stream latency, not throughput);
     one thread per stream beyond the last tier."""
     sms = _sm_count(dev)
-    sym_cap = 3 * DEFLATE_TIERS[-1] + 16
+    sym_cap = 3 * DEFLATE_TIERS[-1] + 32  # symbols + the 16-byte phase-1 record
     sym = ws.tensor("deflate_sym", (n * sym_cap,), torch.uint8)
     main = torch.cuda.current_stream(dev)
     streams = _tier_streams(dev, len(DEFLATE_TIERS) + 1)
