@@ -516,8 +516,24 @@ __device__ __forceinline__ void hdown(uint32_t* hk, int heap_len, int k) {
 }
 
 // kind: 0 literal/length, 1 distance, 2 bit-length tree.  Whole warp.
+// A view of one DTree<NL> so the tree code exists once in the binary (three
+// template copies made the flush kernel too large for the instruction cache)
+struct TreeRef {
+    uint16_t* freq;
+    uint16_t* code;
+    uint16_t* len;
+    uint16_t* dad;
+    int* max_code_p;
+    int NL;
+};
 template <int NL>
-__device__ void build_tree_warp(DTrees& W, DTree<NL>& t, int kind, const z6::Tables& tb) {
+__device__ __forceinline__ TreeRef tref(DTree<NL>& t) {
+    return TreeRef{t.freq, t.code, t.len, t.dad, &t.max_code, NL};
+}
+
+__device__ __noinline__ void build_tree_warp(DTrees& W, TreeRef t, int kind,
+                                             const z6::Tables& tb) {
+    const int NL = t.NL;
     const unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31;
     const unsigned lt_mask = (1u << lane) - 1u;
@@ -548,7 +564,7 @@ __device__ void build_tree_warp(DTrees& W, DTree<NL>& t, int kind, const z6::Tab
             if (kind == 0) W.static_len -= tb.sl_len[node];
             else if (kind == 1) W.static_len -= tb.sd_len[node];
         }
-        t.max_code = max_code;
+        *t.max_code_p = max_code;
         for (int k = heap_len / 2; k >= 1; --k) hdown(hk, heap_len, k);
         int node = NL, heap_max = z6::HEAP_SIZE;
         do {
@@ -653,9 +669,8 @@ __device__ void build_tree_warp(DTrees& W, DTree<NL>& t, int kind, const z6::Tab
 }
 
 // trees.c scan_tree / send_tree over a DTree (lane 0)
-template <int NL>
-__device__ void scan_tree_d(DTrees& W, DTree<NL>& t) {
-    const int max_code = t.max_code;
+__device__ __noinline__ void scan_tree_d(DTrees& W, TreeRef t) {
+    const int max_code = *t.max_code_p;
     int prevlen = -1, curlen, nextlen = t.len[0], count = 0, max_count = 7, min_count = 4;
     if (nextlen == 0) max_count = 138, min_count = 3;
     t.len[max_code + 1] = 0xffff;
@@ -677,9 +692,9 @@ __device__ void scan_tree_d(DTrees& W, DTree<NL>& t) {
     }
 }
 
-template <int NL, class BO>
-__device__ void send_tree_d(const DTrees& W, const DTree<NL>& t, BO& bo) {
-    const int max_code = t.max_code;
+template <class BO>
+__device__ void send_tree_d(const DTrees& W, TreeRef t, BO& bo) {
+    const int max_code = *t.max_code_p;
     int prevlen = -1, curlen, nextlen = t.len[0], count = 0, max_count = 7, min_count = 4;
     if (nextlen == 0) max_count = 138, min_count = 3;
     const auto& bt = W.bt;
@@ -1057,14 +1072,14 @@ k_deflate_warp(const uint8_t* __restrict__ in, const long long* __restrict__ in_
         for (int i = lane; i < z6::BL_CODES; i += 32) t.bt.freq[i] = 0;
         if (lane == 0) t.opt_len = t.static_len = 0;
         __syncwarp();
-        wz::build_tree_warp(t, t.lt, 0, tb);
-        wz::build_tree_warp(t, t.dt, 1, tb);
+        wz::build_tree_warp(t, wz::tref(t.lt), 0, tb);
+        wz::build_tree_warp(t, wz::tref(t.dt), 1, tb);
         if (lane == 0) {
-            wz::scan_tree_d(t, t.lt);
-            wz::scan_tree_d(t, t.dt);
+            wz::scan_tree_d(t, wz::tref(t.lt));
+            wz::scan_tree_d(t, wz::tref(t.dt));
         }
         __syncwarp();
-        wz::build_tree_warp(t, t.bt, 2, tb);
+        wz::build_tree_warp(t, wz::tref(t.bt), 2, tb);
         // ---- output: zero the stream's bytes (it is at most n + 11 long),
         //      then OR the bit stream into them
         uint8_t* dst = out + out_off[s];
@@ -1100,8 +1115,8 @@ k_deflate_warp(const uint8_t* __restrict__ in, const long long* __restrict__ in_
                 sb.bits((unsigned)(dcodes - 1), 5);
                 sb.bits((unsigned)(blcodes - 4), 4);
                 for (int r = 0; r < blcodes; r++) sb.bits(t.bt.len[z6::bl_order(r)], 3);
-                wz::send_tree_d(t, t.lt, sb);
-                wz::send_tree_d(t, t.dt, sb);
+                wz::send_tree_d(t, wz::tref(t.lt), sb);
+                wz::send_tree_d(t, wz::tref(t.dt), sb);
             }
             sh_kind[warp] = kind;
             sh_hbits[warp] = sb.bit;

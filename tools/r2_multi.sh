@@ -6,7 +6,7 @@ TAG=$1
 O=gpurun_out/$TAG
 mkdir -p $O
 nvidia-smi topo -m > $O/topo.txt 2>&1
-timeout 1200 python -m pytest tests/test_multi_gpu.py -m gpu -x -q -p no:cacheprovider > $O/multi_tests.log 2>&1
+timeout 1500 python -m pytest tests/test_multi_gpu.py tests/test_gpu_parity.py -m gpu -x -q -p no:cacheprovider -k "multi or distributed or zlib or benchmark_configs" > $O/multi_tests.log 2>&1
 echo "rc=$?" >> $O/multi_tests.log
 NG=$(nvidia-smi -L | wc -l)
 timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-train > $O/bench_1.log 2>&1
