@@ -206,7 +206,9 @@ def decode_tree_cols(d: int, l: int) -> bytes:
     n = max(512, int(1e6 // (l * d)) + 64)
     w = rng.standard_normal((l, d)).astype(np.float32).astype(np.float64)
     z = (rng.standard_normal((n, l)) * 37.0).astype(np.float32).astype(np.float64)
-    ref = z @ w
+    from threadpoolctl import threadpool_limits  # the reference ran on one BLAS thread
+    with threadpool_limits(limits=1, user_api="blas"):
+        ref = z @ w
     p = [z[:, k:k + 1] * w[k][None, :] for k in range(4)]
     seq = ((p[0] + p[1]) + p[2]) + p[3]
     tree = (p[0] + p[1]) + (p[2] + p[3])

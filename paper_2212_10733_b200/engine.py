@@ -40,7 +40,8 @@ _PAYLOAD_HEAD = struct.Struct("<BHHd")
 @functools.lru_cache(maxsize=None)
 def decode_tree_cols(d: int, l: int) -> bytes:
     """Columns where numpy/OpenBLAS sums the L=4 decode products as
-    (p0+p1)+(p2+p3) in its blocked kernel (autoencoder.py:109); probed once."""
+    (p0+p1)+(p2+p3) in its blocked kernel (autoencoder.py:109); probed once,
+    on one BLAS thread."""
     out = np.zeros(d, dtype=np.uint8)
     if l != 4:
         return out.tobytes()
@@ -48,7 +49,15 @@ def decode_tree_cols(d: int, l: int) -> bytes:
     n = max(512, int(1e6 // (l * d)) + 64)
     w = rng.standard_normal((l, d)).astype(np.float32).astype(np.float64)
     z = (rng.standard_normal((n, l)) * 37.0).astype(np.float32).astype(np.float64)
-    ref = z @ w
+    # the reference's orders are single-threaded OpenBLAS's: probe
+    # that kernel whatever this process's BLAS thread count is (a threaded
+    # run partitions the product differently)
+    try:
+        from threadpoolctl import threadpool_limits
+        with threadpool_limits(limits=1, user_api="blas"):
+            ref = z @ w
+    except ImportError:  # pragma: no cover - threadpoolctl ships with the image
+        ref = z @ w
     p = [z[:, k:k + 1] * w[k][None, :] for k in range(4)]
     seq = ((p[0] + p[1]) + p[2]) + p[3]
     tree = (p[0] + p[1]) + (p[2] + p[3])
@@ -757,9 +766,6 @@ def compress_device(f0: torch.Tensor, specs, dgrid: DeviceGrid, cfg, timer: Time
         table[s].eb = eb[s]
         table[s].lossless = int(lossless[s])
 
-    if hi_ctx is not None:
-        hi_ctx.__exit__(None, None, None)
-        main.wait_stream(hi)
     timer.mark("newton")
     slot_base_h = np.concatenate([[0], np.cumsum(cnt_h)[:-1]]).astype(np.int32)
     ws.begin()
@@ -767,9 +773,14 @@ def compress_device(f0: torch.Tensor, specs, dgrid: DeviceGrid, cfg, timer: Time
     slot_base = ws.stage(slot_base_h)
     ws.flush()
     if n_sel:
+        # the residual images feed DEFLATE (the critical path): still on the
+        # high-priority stream, ahead of the side stream's remaining CTAs
         call("mlk_project", f0, stats, qoi, sh_d, S, total, dgrid.addr, W, L, cents, K, codes,
              sel_rank, slot_base, ctypes.addressof(opts), flags, lam, qst, status, iters, ferr,
              fqoi, fsse, varint, vcap, vlen, errf, list_sel, n_sel, PROJECT_CTAS)
+    if hi_ctx is not None:
+        hi_ctx.__exit__(None, None, None)
+        main.wait_stream(hi)
     timer.mark("deflate")
     # DEFLATE needs only the residual images' varint streams: it starts while
     # the side stream may still be projecting the others
@@ -1043,7 +1054,10 @@ def _sm_count(dev):
 def _tier_streams(dev, n):
     key = dev.index
     if key not in _TIER_STREAMS:
-        _TIER_STREAMS[key] = [torch.cuda.Stream(device=dev) for _ in range(n)]
+        # high priority: DEFLATE is the tail of the step; the residual-free
+        # projection on the low-priority side stream fills in around it
+        hi = torch.cuda.Stream.priority_range()[1]
+        _TIER_STREAMS[key] = [torch.cuda.Stream(device=dev, priority=hi) for _ in range(n)]
     return _TIER_STREAMS[key]
 
 

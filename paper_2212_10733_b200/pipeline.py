@@ -589,7 +589,8 @@ def decompress(archive: bytes) -> FDataset:
     return FDataset._trusted(pre.grid, data, pre.timestep)
 
 
-def decompress_distributed(archive: bytes, group=None, gather: bool = True):
+def decompress_distributed(archive: bytes, group=None, gather: bool = True,
+                           out_path: str | None = None):
     """decompress() with one process per GPU (torch.distributed initialised).
 
     The reference decodes every shard independently (pipeline.py:430-440);
@@ -598,8 +599,11 @@ def decompress_distributed(archive: bytes, group=None, gather: bool = True):
     [P r / G, P (r + 1) / G) of f0, into its own HBM.  gather=True: the slabs
     are all-gathered over NCCL (NVLink) and every rank returns the whole
     FDataset, as decompress() does; gather=False: returns (FDataset of the
-    rank's planes, (plane_lo, plane_hi)).  Needs G to divide the plane count
-    (each rank's slab is then whole planes)."""
+    rank's planes, (plane_lo, plane_hi)); out_path: every rank copies its
+    planes straight into that file (the (P, N, rows, cols) little-endian
+    float64 payload, created by rank 0) over its own PCIe link, and every rank
+    returns (out_path, (plane_lo, plane_hi)).  Needs G to divide the plane
+    count (each rank's slab is then whole planes)."""
     import torch.distributed as dist
 
     from . import distributed as D_
@@ -621,6 +625,39 @@ def decompress_distributed(archive: bytes, group=None, gather: bool = True):
     mine = out[:plan.out_elems]
     if bool((mine < 0).any()):
         raise ConfigError("histogram values must be non-negative")
+    if out_path is not None:
+        total = pre.n_planes * nd * 8
+        if sp.rank == 0:
+            fd = os.open(out_path, os.O_RDWR | os.O_CREAT, 0o644)
+            try:
+                os.ftruncate(fd, total)
+            finally:
+                os.close(fd)
+        if on and sp.world > 1:
+            dist.barrier(group=group)
+        host = hostio.download_view(mine.view(torch.uint8), plan.out_elems * 8)
+        fd = os.open(out_path, os.O_RDWR)
+        try:
+            mm = mmap.mmap(fd, total, mmap.MAP_SHARED, mmap.PROT_WRITE | mmap.PROT_READ)
+            try:
+                dst = np.frombuffer(mm, dtype=np.uint8)
+                o0 = plan.plane_lo * nd * 8
+                step = 8 << 20
+                spans = [(a, min(plan.out_elems * 8, a + step)) for a in
+                         range(0, plan.out_elems * 8, step)]
+
+                def put(x):
+                    dst[o0 + x[0]:o0 + x[1]] = host[x[0]:x[1]]
+
+                list(hostio._pool().map(put, spans))
+                del dst
+            finally:
+                mm.close()
+        finally:
+            os.close(fd)
+        if on and sp.world > 1:
+            dist.barrier(group=group)
+        return out_path, (plan.plane_lo, plan.plane_hi)
     if not gather:
         data = hostio.download_pinned_array(mine, (plan.plane_hi - plan.plane_lo, pre.n_nodes,
                                                    g.rows, g.cols))
