@@ -292,6 +292,8 @@ def decompress_measure(arc, world, total_hist, dev):
         dist.barrier()
         if dist.get_rank() == 0 and os.path.exists(dec_path):
             os.unlink(dec_path)
+        from paper_2212_10733_b200 import hostio
+        hostio.release_maps()
     return {"value": total_hist / e2e_s, "unit": "hist/s (e2e decompress via public API)",
             "raw_gb_s": total_hist * HIST_BYTES / e2e_s / 1e9,
             "api": "decompress(archive)" if world == 1 else
@@ -511,6 +513,8 @@ def main():
             dist.barrier()  # every rank has read the archive size
             if rank == 0 and os.path.exists(shm):
                 os.unlink(shm)
+            from paper_2212_10733_b200 import hostio
+            hostio.release_maps()
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not devgen:

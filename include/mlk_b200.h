@@ -161,7 +161,7 @@ int mlk_zlib_compress6(const uint8_t* in, const int64_t* in_off, const int64_t* 
  * bit stream (one fused launch when prof is given).  sym_scratch: n *
  * sym_cap bytes (sym_cap >= 3 * nmax + 19, a multiple of 16) for the LZ77
  * symbol buffers, whose last 16 bytes carry the parse's summary to the
- * second launch; prof (may be NULL): 12 u64 cycle/counter accumulators. */
+ * second launch; prof (may be NULL): 16 u64 cycle/counter accumulators. */
 int mlk_zlib_compress6_warp(const uint8_t* in, const int64_t* in_off, const int64_t* in_len,
                             int32_t n, int32_t nmin, int32_t nmax, uint8_t* out,
                             const int64_t* out_off, int64_t out_cap, int64_t* out_len,

@@ -389,34 +389,16 @@ k_inflate_warp(const uint8_t* __restrict__ in, const long long* __restrict__ in_
 namespace wz {
 
 struct Lay {
-    int nmax, T, direct;  // direct: a 32K-entry table indexed by the hash
-    int win, p1, p4, hash, trees, hist, total;
+    int nmax;
+    int win, srt, gi, p1, trees, hist, total;
     int total_lz;         // phase 1 only (window + chain tables)
     int total_fl;         // phase 2 only (trees + histogram, from offset 0)
 };
 
-__host__ __device__ inline int pow2ge(int x) {
-    int p = 1;
-    while (p < x) p <<= 1;
-    return p;
-}
 __host__ __device__ inline int al16(int x) { return (x + 15) & ~15; }
 
 __device__ __forceinline__ unsigned hkey(const uint8_t* w) {
     return (((unsigned)w[0] << 10) ^ ((unsigned)w[1] << 5) ^ w[2]) & 0x7fffu;
-}
-
-// the i-th chain successor of x: p4^(i/4) o p1^(i%4), as predicated steps
-// (no divergent loop; 0 ends a chain and stays 0)
-__device__ __forceinline__ int jump(const uint16_t* p1, const uint16_t* p4, int x, int i) {
-    const int a = i & 3, b = i >> 2;
-#pragma unroll
-    for (int k = 1; k <= 3; ++k)
-        if (a >= k && x) x = p1[x];
-#pragma unroll
-    for (int k = 1; k <= 7; ++k)
-        if (b >= k && x) x = p4[x];
-    return x;
 }
 
 // zlib longest_match length of window[c..] against window[p..], 8 bytes at
@@ -743,25 +725,25 @@ struct GBits {
 };
 
 // Per-warp shared memory: the window, then one region reused by phase:
-//   chain build  : p1 | hash table (u16 entries, aliasing where p4 will go)
-//   matching     : p1 | p4
+//   chain build  : sorted positions | radix scratch (later gi) | p1 (its
+//                  first 1.5 KB the radix histograms until p1 is written)
+//   matching     : sorted positions | gi | p1
 //   flush        : Huffman trees | u32 symbol histogram
 // The symbol buffer lives in global scratch; the bit stream is OR-ed into
 // the zeroed global output.
+constexpr int RADIX_HIST_BYTES = 4 * (256 + 128);
+
 __host__ __device__ inline Lay layout(int nmax) {
     Lay L;
     L.nmax = nmax;
-    L.direct = nmax > 4096;
-    L.T = L.direct ? 32768 : pow2ge(nmax + 2);
     int o = 0;
     L.win = o;
     o += al16(nmax + z6::MAX_MATCH + 24);
     const int b0 = o;
-    L.p1 = b0;
-    L.p4 = b0 + al16(2 * nmax);
-    L.hash = L.p4;
-    const int chains = al16(2 * nmax) + (al16(2 * nmax) > al16(2 * L.T) ? al16(2 * nmax)
-                                                                          : al16(2 * L.T));
+    L.srt = b0;
+    L.gi = L.srt + al16(2 * nmax);
+    L.p1 = L.gi + al16(2 * nmax);
+    const int chains = L.p1 - b0 + al16(2 * nmax > RADIX_HIST_BYTES ? 2 * nmax : RADIX_HIST_BYTES);
     L.trees = b0;
     L.hist = b0 + al16((int)sizeof(DTrees));
     const int flush = al16((int)sizeof(DTrees)) + 4 * 320;
@@ -798,9 +780,9 @@ k_deflate_warp(const uint8_t* __restrict__ in, const long long* __restrict__ in_
     uint8_t* base = zsm + (size_t)warp * (PH == 3 ? Ly.total : (PH == 1 ? Ly.total_lz
                                                                           : Ly.total_fl));
     uint8_t* win = base + Ly.win;
+    uint16_t* srt = reinterpret_cast<uint16_t*>(base + Ly.srt);
+    uint16_t* gi = reinterpret_cast<uint16_t*>(base + Ly.gi);
     uint16_t* p1 = reinterpret_cast<uint16_t*>(base + Ly.p1);
-    uint16_t* p4 = reinterpret_cast<uint16_t*>(base + Ly.p4);
-    uint16_t* htab = reinterpret_cast<uint16_t*>(base + Ly.hash);
     wz::DTrees* trees = reinterpret_cast<wz::DTrees*>(base + (PH == 2 ? 0 : Ly.trees));
     const unsigned FULL = 0xffffffffu;
     const unsigned lt_mask = (1u << lane) - 1u;
@@ -826,7 +808,7 @@ k_deflate_warp(const uint8_t* __restrict__ in, const long long* __restrict__ in_
         long long t_0 = PROF ? clock64() : 0;
         unsigned ad_a = 0, ad_b = 0;
         int sym_next = 0, strstart = 0;
-        long long t_1 = 0, t_2 = 0, t_3 = 0, t_lm = 0;
+        long long t_1 = 0, t_2 = 0, t_3 = 0, t_lm = 0, t_h = 0, t_pa = 0, t_pb = 0;
         int n_calls = 0, n_rounds = 0, n_cands = 0;
         unsigned* meta = reinterpret_cast<unsigned*>(sym + sym_cap - 16);
         if constexpr ((PH & 1) != 0) {
@@ -845,73 +827,94 @@ k_deflate_warp(const uint8_t* __restrict__ in, const long long* __restrict__ in_
         }
         ad_a = (unsigned)((1 + sa) % 65521ull);
         ad_b = (unsigned)(((unsigned long long)n + sb) % 65521ull);
-        for (int i = lane; i < Ly.T; i += 32) htab[i] = 0;
         __syncwarp();
         t_1 = PROF ? clock64() : 0;
-        // ---- prev[] (hash chains), 32 positions per step.  Table entries
-        //      are position + 1; a probed entry's key is re-derived from the
-        //      window (no key storage), direct mode indexes by the hash.
+        // ---- hash chains as sorted runs.  Every position 0 .. n-3 is
+        //      inserted before the search that could see it (deflate_slow), so
+        //      a position's chain is exactly the earlier positions with its
+        //      hash, latest first: a stable two-digit LSD radix sort of the
+        //      positions by hash (low 8 bits, then high 7) makes each chain a
+        //      contiguous run of srt[], the i-th candidate of a search from p
+        //      is srt[gi[p] - 1 - i], and bit 15 of an entry marks the first
+        //      position of its run (the end of every chain through it).
         const int n_ins = n - z6::MIN_MATCH + 1;  // positions 0 .. n-3
-        for (int b0 = 0; b0 < n_ins; b0 += 32) {
-            const int p = b0 + lane;
-            const bool v = p < n_ins;
-            const unsigned h = v ? wz::hkey(win + p) : (0x80000000u | lane);
-            const unsigned m = __match_any_sync(FULL, h);
-            if (v) {
-                const unsigned lower = m & lt_mask;
-                int pr = 0;
-                if (lower) {
-                    pr = b0 + 31 - __clz(lower);
-                } else if (Ly.direct) {
-                    pr = htab[h];
-                    pr = pr ? pr - 1 : 0;
-                } else {
-                    unsigned i = (h * 2654435761u) & (Ly.T - 1);
-                    for (;;) {
-                        const unsigned e = htab[i];
-                        if (e == 0u) break;
-                        if (wz::hkey(win + e - 1) == h) { pr = (int)e - 1; break; }
-                        i = (i + 1) & (Ly.T - 1);
-                    }
-                }
-                p1[p] = (uint16_t)pr;
-            }
-            __syncwarp();
-            if (v && (31 - __clz(m)) == lane) {  // last of its group updates the table
-                if (Ly.direct) {
-                    htab[h] = (uint16_t)(p + 1);
-                } else {
-                    unsigned i = (h * 2654435761u) & (Ly.T - 1);
-                    for (;;) {
-                        unsigned* w32 = reinterpret_cast<unsigned*>(htab) + (i >> 1);
-                        const int sh = (i & 1) * 16;
-                        unsigned old = *w32;
-                        unsigned e = (old >> sh) & 0xffffu;
-                        while (e == 0u) {  // claim the empty half-word
-                            const unsigned prev = atomicCAS(w32, old, old | ((unsigned)(p + 1) << sh));
-                            if (prev == old) break;
-                            old = prev;
-                            e = (old >> sh) & 0xffffu;
-                        }
-                        if (e == 0u) break;  // claimed
-                        if (wz::hkey(win + e - 1) == h) { htab[i] = (uint16_t)(p + 1); break; }
-                        i = (i + 1) & (Ly.T - 1);
-                    }
-                }
-            }
-            __syncwarp();
-        }
-        t_2 = PROF ? clock64() : 0;
-        for (int p = lane; p < n; p += 32)
-            if (p >= n_ins) p1[p] = 0;
+        unsigned* hA = reinterpret_cast<unsigned*>(p1);  // 256 low-digit counters
+        unsigned* hB = hA + 256;                         // 128 high-digit counters
+        for (int i = lane; i < 384; i += 32) hA[i] = 0u;
         __syncwarp();
-        for (int p = lane; p < n; p += 32) {  // the hash table is dead: p4 reuses it
-            int x = p1[p];
-            x = x ? p1[x] : 0;
-            x = x ? p1[x] : 0;
-            x = x ? p1[x] : 0;
-            p4[p] = (uint16_t)x;
+        for (int p = lane; p < n_ins; p += 32) {
+            const unsigned h = wz::hkey(win + p);
+            atomicAdd(hA + (h & 255u), 1u);
+            atomicAdd(hB + (h >> 8), 1u);
         }
+        __syncwarp();
+        {  // exclusive scans: 8 low-digit and 4 high-digit counters per lane
+            unsigned a[8], b[4], sa_ = 0, sb_ = 0;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) { a[k] = hA[8 * lane + k]; sa_ += a[k]; }
+#pragma unroll
+            for (int k = 0; k < 4; ++k) { b[k] = hB[4 * lane + k]; sb_ += b[k]; }
+            unsigned xa = sa_, xb = sb_;
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned ya = __shfl_up_sync(FULL, xa, o), yb = __shfl_up_sync(FULL, xb, o);
+                if (lane >= o) { xa += ya; xb += yb; }
+            }
+            xa -= sa_;
+            xb -= sb_;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) { hA[8 * lane + k] = xa; xa += a[k]; }
+#pragma unroll
+            for (int k = 0; k < 4; ++k) { hB[4 * lane + k] = xb; xb += b[k]; }
+        }
+        __syncwarp();
+        t_h = PROF ? clock64() : 0;
+        // stable scatter, 32 positions per step: lanes with the same digit
+        // take consecutive slots in lane order, the last of them advances
+        // the digit's cursor
+#pragma unroll 1
+        for (int pass = 0; pass < 2; ++pass) {
+            const uint16_t* from = gi;  // pass 1 reads pass 0's output
+            uint16_t* to = pass ? srt : gi;
+            unsigned* cur = pass ? hB : hA;
+            for (int b0 = 0; b0 < n_ins; b0 += 32) {
+                const int j = b0 + lane;
+                const bool v = j < n_ins;
+                const int p = v ? (pass ? (int)from[j] : j) : 0;
+                const unsigned h = wz::hkey(win + p);
+                const unsigned d = v ? (pass ? h >> 8 : h & 255u) : 512u + lane;
+                const unsigned m = __match_any_sync(FULL, d);
+                const unsigned at = v ? cur[d] : 0u;
+                __syncwarp();
+                if (v) {
+                    to[at + __popc(m & lt_mask)] = (uint16_t)p;
+                    if ((31 - __clz(m)) == lane) cur[d] = at + __popc(m);
+                }
+                __syncwarp();
+            }
+            if (PROF && pass == 0) t_pa = clock64();
+        }
+        t_pb = PROF ? clock64() : 0;
+        // run starts, each position's sorted index, and prev[] (hash_head)
+        unsigned carry_h = 0xffffffffu, carry_p = 0u;
+        for (int b0 = 0; b0 < n_ins; b0 += 32) {
+            const int j = b0 + lane;
+            const bool v = j < n_ins;
+            const unsigned p = v ? srt[j] : 0u;
+            const unsigned h = v ? wz::hkey(win + p) : 0xfffffffeu;
+            unsigned hp = __shfl_up_sync(FULL, h, 1), pp = __shfl_up_sync(FULL, p, 1);
+            if (lane == 0) { hp = carry_h; pp = carry_p; }
+            carry_h = __shfl_sync(FULL, h, 31);
+            carry_p = __shfl_sync(FULL, p, 31);
+            if (v) {
+                const bool first = hp != h;
+                if (first) srt[j] = (uint16_t)(p | 0x8000u);
+                gi[p] = (uint16_t)j;
+                p1[p] = first ? 0 : (uint16_t)pp;
+            }
+        }
+        __syncwarp();
+        t_2 = PROF ? clock64() : 0;
+        for (int p = (n_ins > 0 ? n_ins : 0) + lane; p < n; p += 32) p1[p] = 0;
         __syncwarp();
         t_3 = PROF ? clock64() : 0;
         // ---- deflate_slow, warp-uniform state
@@ -956,11 +959,15 @@ k_deflate_warp(const uint8_t* __restrict__ in, const long long* __restrict__ in_
                 const int nice = lookahead < z6::NICE ? lookahead : z6::NICE;
                 const int thr = nice > prev_length + 1 ? nice : prev_length + 1;
                 int best = prev_length, bstart = match_start;
-                int cb = hash_head;  // first candidate of the round
+                // candidates srt[j0 - 1 - i] down to the run's first entry
+                const int j0 = gi[strstart];
                 const unsigned long long s0 = wz::load8(win, strstart),
                                          s1 = wz::load8(win, strstart + 8);
                 for (int r = 0; r < chain; r += 32) {
-                    const int c = wz::jump(p1, p4, cb, lane);
+                    const int idx = j0 - 1 - r - lane;
+                    const unsigned e = idx >= 0 ? srt[idx] : 0x8000u;
+                    const unsigned fb = __ballot_sync(FULL, (e & 0x8000u) != 0u);
+                    const int c = (fb && lane > __ffs(fb) - 1) ? 0 : (int)(e & 0x7fffu);
                     const bool valid = c != 0 && r + lane < chain;
                     // lengths up to thr (exact below it), then the exact length of
                     // the first candidate reaching thr -- the one that ends the search
@@ -981,9 +988,7 @@ k_deflate_warp(const uint8_t* __restrict__ in, const long long* __restrict__ in_
                         ++n_rounds;
                         n_cands += __popc(hit ? (alive & (0xffffffffu >> (31 - upto))) : alive);
                     }
-                    if (hit || alive != FULL) break;
-                    cb = __shfl_sync(FULL, c ? (int)p1[c] : 0, 31);
-                    if (cb == 0) break;
+                    if (hit || alive != FULL || fb) break;
                 }
                 match_start = bstart;
                 match_length = best <= lookahead ? best : lookahead;
@@ -1226,6 +1231,9 @@ k_deflate_warp(const uint8_t* __restrict__ in, const long long* __restrict__ in_
                 atomicAdd(prof + 9, (unsigned long long)(sym_next / 3));
                 atomicAdd(prof + 10, (unsigned long long)n_rounds);
                 atomicAdd(prof + 11, (unsigned long long)n_cands);
+                atomicAdd(prof + 12, (unsigned long long)(t_h - t_1));
+                atomicAdd(prof + 13, (unsigned long long)(t_pa - t_h));
+                atomicAdd(prof + 14, (unsigned long long)(t_pb - t_pa));
             }
         }
         __syncwarp();

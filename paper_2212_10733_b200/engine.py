@@ -1033,7 +1033,7 @@ def _deflate_pool(dev, n_workers):
 DEFLATE_TIERS = (1024, 1600, 2048, 3072, 4096, 8192, 16000)
 
 
-DEFLATE_PROF = None   # set to a (12,) uint64 CUDA tensor to collect phase cycles
+DEFLATE_PROF = None   # set to a (16,) uint64 CUDA tensor to collect phase cycles
 # tier warps claim streams from an atomic counter (dynamic balance)
 DEFLATE_DYNAMIC = os.environ.get("MLK_DEFLATE_DYNAMIC", "1") != "0"
 

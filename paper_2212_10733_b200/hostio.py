@@ -24,7 +24,7 @@ import numpy as np
 import torch
 
 __all__ = ["upload_planes", "upload_pieces", "upload_bytes", "download_bytes", "download_view",
-           "download_array", "download_pinned_array", "pinned", "pinned_empty", "ArchiveWriter"]
+           "download_array", "download_pinned_array", "download_into", "mapped_file", "release_maps", "pinned", "pinned_empty", "ArchiveWriter"]
 
 CHUNK = 64 << 20
 UP_CHUNK = 2 << 20    # upload_pieces copy granularity
@@ -569,6 +569,61 @@ def download_array(src: torch.Tensor, shape, dtype=np.float64) -> np.ndarray:
 
     list(_pool().map(cp, range(len(spans))))
     return out
+
+
+_MAPS = {}
+
+
+def mapped_file(fd: int, total: int) -> np.ndarray:
+    """A shared, writable uint8 view of the first `total` bytes of an open
+    file, cached per (device, inode, size): a file rewritten step after step
+    keeps its page-table entries, so filling it costs a memcpy, not a page
+    fault per 4 KiB (the mapping pins the inode, so the key cannot be reused
+    by another file while it is cached)."""
+    import mmap
+    st = os.fstat(fd)
+    key = (st.st_dev, st.st_ino, total)
+    m = _MAPS.get(key)
+    if m is None:
+        for k in [k for k in _MAPS if k[:2] == key[:2]]:
+            del _MAPS[k]  # unmapped once no view of it is left
+        flags = mmap.MAP_SHARED | getattr(mmap, "MAP_POPULATE", 0)
+        m = _MAPS[key] = mmap.mmap(fd, total, flags, mmap.PROT_WRITE | mmap.PROT_READ)
+    return np.frombuffer(m, dtype=np.uint8)
+
+
+def release_maps() -> None:
+    """Unmap every cached mapped_file view (call after deleting the files)."""
+    _MAPS.clear()  # each mapping goes once no view of it is left
+
+
+def download_into(src: torch.Tensor, nbytes: int, dst: np.ndarray) -> None:
+    """The first nbytes of a device tensor into a writable host uint8 array
+    (e.g. a mapped_file view): chunked async D2H into pinned memory, each
+    chunk copied out by a pool thread as soon as it lands."""
+    if nbytes == 0:
+        return
+    dev = src.device
+    s8 = src.reshape(-1).view(torch.uint8)[:nbytes]
+    stage = pinned(f"dli{dev.index}", nbytes)
+    st_np = stage.numpy()
+    cs = _copy_stream(dev)
+    cs.wait_stream(torch.cuda.current_stream(dev))
+    spans = [(a, min(nbytes, a + DOWN_CHUNK)) for a in range(0, nbytes, DOWN_CHUNK)]
+    events = []
+    with torch.cuda.stream(cs):
+        for a, b in spans:
+            stage[a:b].copy_(s8[a:b], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(cs)
+            events.append(ev)
+
+    def put(k):
+        a, b = spans[k]
+        events[k].synchronize()
+        dst[a:b] = st_np[a:b]
+
+    list(_pool().map(put, range(len(spans))))
 
 
 def download_pinned_array(src: torch.Tensor, shape, dtype=np.float64) -> np.ndarray:

@@ -12,7 +12,6 @@ from __future__ import annotations
 import ctypes
 import hashlib
 import json
-import mmap
 import os
 import struct
 import time
@@ -477,22 +476,18 @@ def compress_distributed(ds: FDataset, config: PipelineConfig, state: TimestepSt
         fd = os.open(out_path, os.O_RDWR)
         try:
             total = int(offs[-1] + sizes[-1])
-            mm = mmap.mmap(fd, total, mmap.MAP_SHARED, mmap.PROT_WRITE | mmap.PROT_READ)
-            try:
-                dst = np.frombuffer(mm, dtype=np.uint8)
-                base = int(offs[0])
-                spans = []
-                for lo, goff, n in out.segments:
-                    spans += [(lo + a, base + goff + a, min(n, a + (8 << 20)) - a)
-                              for a in range(0, n, 8 << 20)]
+            dst = hostio.mapped_file(fd, total)
+            base = int(offs[0])
+            spans = []
+            for lo, goff, n in out.segments:
+                spans += [(lo + a, base + goff + a, min(n, a + (8 << 20)) - a)
+                          for a in range(0, n, 8 << 20)]
 
-                def put(x):
-                    dst[x[1]:x[1] + x[2]] = body[x[0]:x[0] + x[2]]
+            def put(x):
+                dst[x[1]:x[1] + x[2]] = body[x[0]:x[0] + x[2]]
 
-                list(hostio._pool().map(put, spans))
-                del dst
-            finally:
-                mm.close()
+            list(hostio._pool().map(put, spans))
+            del dst
         finally:
             os.close(fd)
         trace.mark("pwrite")
@@ -635,24 +630,12 @@ def decompress_distributed(archive: bytes, group=None, gather: bool = True,
                 os.close(fd)
         if on and sp.world > 1:
             dist.barrier(group=group)
-        host = hostio.download_view(mine.view(torch.uint8), plan.out_elems * 8)
         fd = os.open(out_path, os.O_RDWR)
         try:
-            mm = mmap.mmap(fd, total, mmap.MAP_SHARED, mmap.PROT_WRITE | mmap.PROT_READ)
-            try:
-                dst = np.frombuffer(mm, dtype=np.uint8)
-                o0 = plan.plane_lo * nd * 8
-                step = 8 << 20
-                spans = [(a, min(plan.out_elems * 8, a + step)) for a in
-                         range(0, plan.out_elems * 8, step)]
-
-                def put(x):
-                    dst[o0 + x[0]:o0 + x[1]] = host[x[0]:x[1]]
-
-                list(hostio._pool().map(put, spans))
-                del dst
-            finally:
-                mm.close()
+            o0 = plan.plane_lo * nd * 8
+            dst = hostio.mapped_file(fd, total)[o0:o0 + plan.out_elems * 8]
+            hostio.download_into(mine, plan.out_elems * 8, dst)
+            del dst
         finally:
             os.close(fd)
         if on and sp.world > 1:

@@ -49,6 +49,9 @@ def main():
     short = re.search(r"(k_\w+)", kern).group(1)
     tmpl = ("ILb1E" if re.search(r"<\(bool\)1>|<1>|<true>", kern) else
             "ILb0E" if re.search(r"<\(bool\)0>|<0>|<false>", kern) else "")
+    mi = re.search(r"\(int\)(\d+)>", kern)
+    if mi:
+        tmpl += f"Li{mi.group(1)}E"
     for fblk in funcs:
         head = fblk.split("\n", 1)[0]
         if short in head and (not tmpl or tmpl in head):
