@@ -347,7 +347,10 @@ def rooflines(out, stage_ms, n, dev, traffic_ok=True):
     ]
     table = []
     for kern, stage, nbytes, launches, note in rows:
-        ms = stage_ms.get(stage)
+        # DEFLATE's own span: its launch to the join of its tier streams (the
+        # stage itself also waits for the side stream's projection)
+        ms = stage_ms.get("deflate_done") if stage == "deflate" else None
+        ms = ms if ms is not None else stage_ms.get(stage)
         if ms is None:
             continue
         e = {"kernel": kern, "stage": stage, "ms_per_step": ms, "note": note}

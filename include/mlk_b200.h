@@ -322,9 +322,7 @@ int mlk_probe_bins(const double* f0, const MlkShard* shards, int32_t n_shards,
  * errors).  *err_flag = MLK_ERR_CONFIG when |q| >= 2**62 (residual.py:67).
  * img_list (device, n_list entries) restricts the launch to those images
  * (NULL: all `total`), so the images without residuals can be projected
- * while the error-bound search of the others is still running;
- * ctas_per_sm > 0 caps the resident one-warp CTAs per SM (0: occupancy max)
- * to leave room for kernels on other streams. */
+ * while the error-bound search of the others is still running. */
 int mlk_project(const double* f0, const double* stats, const double* qoi,
                 const MlkShard* shards, int32_t n_shards, int32_t total, const MlkGrid* grid_h,
                 const float* W, int32_t L, const float* cents, int32_t K, const uint8_t* codes,
@@ -332,7 +330,7 @@ int mlk_project(const double* f0, const double* stats, const double* qoi,
                 uint8_t* flags, double* lam, double* qst, int32_t* status, int32_t* iters,
                 double* ferr, double* fqoi, double* fsse, uint8_t* varint, int64_t varint_cap,
                 int64_t* varint_len, int32_t* err_flag, const int32_t* img_list,
-                int32_t n_list, int32_t ctas_per_sm, cudaStream_t stream);
+                int32_t n_list, cudaStream_t stream);
 
 /* Decode path (pipeline.py:397-427) for all images of all shards: recon from
  * codes; + residual (res_slot[img] >= 0: D zigzag codes at res_codes +

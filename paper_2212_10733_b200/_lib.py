@@ -100,7 +100,7 @@ _SIGS = {
                   _I32, _I32, _I32, _P, _P, _P, _P],
     "mlk_probe_bins": [_P, _P, _I32, _P, _P, _I32, _P, _I32, _P, _P, _P, _I32, _P, _P, _P],
     "mlk_project": [_P, _P, _P, _P, _I32, _I32, _P, _P, _I32, _P, _I32, _P, _P, _P, _P, _P,
-                    _P, _P, _P, _P, _P, _P, _P, _P, _I64, _P, _P, _P, _I32, _I32, _P],
+                    _P, _P, _P, _P, _P, _P, _P, _P, _I64, _P, _P, _P, _I32, _P],
     "mlk_split_flags": [_P, _I32, ctypes.c_uint32, _P, _P, _P, _P],
     "mlk_list_flags": [_P, _P, _I32, ctypes.c_uint32, _P, _P, _P],
     "mlk_pack_residuals": [_P, _P, _P, _P, _P, _P, _P, _P, _I32, _I32, _I32, _P, _P],

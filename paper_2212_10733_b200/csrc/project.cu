@@ -832,9 +832,7 @@ extern "C" int mlk_project(const double* f0, const double* stats, const double* 
                            double* lam, double* qst, int32_t* status, int32_t* iters,
                            double* ferr, double* fqoi, double* fsse, uint8_t* varint,
                            int64_t varint_cap, int64_t* varint_len, int32_t* err_flag,
-                           const int32_t* img_list, int32_t n_list, int32_t ctas_per_sm,
-                           cudaStream_t stream) {
-    (void)ctas_per_sm;
+                           const int32_t* img_list, int32_t n_list, cudaStream_t stream) {
     const int n_work = img_list ? n_list : total;
     if (total <= 0 || n_work <= 0) return MLK_OK;
     const int D = grid_h->D;

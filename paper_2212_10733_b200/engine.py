@@ -336,6 +336,16 @@ class Timer:
         self.enabled = enabled
         self.sync = os.environ.get("MLK_TIMING") == "sync"
         self.marks = []
+        self.points = []
+
+    def point(self, name, stream, since):
+        """An event on `stream`, reported as ms after the mark `since`
+        (points of concurrent streams: which one a join waited for)."""
+        if not self.enabled or self.sync:
+            return
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record(stream)
+        self.points.append((name, ev, since))
 
     def mark(self, name):
         if not self.enabled:
@@ -357,6 +367,10 @@ class Timer:
         for (n0, e0), (_, e1) in zip(self.marks, self.marks[1:]):
             dt = (e1 - e0) if self.sync else e0.elapsed_time(e1) / 1e3
             out[n0] = out.get(n0, 0.0) + dt
+        base = dict(self.marks)
+        for name, ev, since in self.points:
+            if since in base and not self.sync:
+                out[name] = out.get(name, 0.0) + base[since].elapsed_time(ev) / 1e3
         return out
 
 
@@ -683,8 +697,7 @@ def compress_device(f0: torch.Tensor, specs, dgrid: DeviceGrid, cfg, timer: Time
         side.wait_event(ev_split)
     call("mlk_project", f0, stats, qoi, sh_d, S, total, dgrid.addr, W, L, cents, K, codes,
          sel_rank, None, ctypes.addressof(opts), flags, lam, qst, status, iters, ferr, fqoi,
-         fsse, varint, vcap, vlen, errf, list_non, total - n_sel,
-         PROJECT_OVERLAP_CTAS if side is not main else PROJECT_CTAS, stream=side.cuda_stream)
+         fsse, varint, vcap, vlen, errf, list_non, total - n_sel, stream=side.cuda_stream)
     ev_non = torch.cuda.Event()
     ev_non.record(side)
 
@@ -777,7 +790,7 @@ def compress_device(f0: torch.Tensor, specs, dgrid: DeviceGrid, cfg, timer: Time
         # high-priority stream, ahead of the side stream's remaining CTAs
         call("mlk_project", f0, stats, qoi, sh_d, S, total, dgrid.addr, W, L, cents, K, codes,
              sel_rank, slot_base, ctypes.addressof(opts), flags, lam, qst, status, iters, ferr,
-             fqoi, fsse, varint, vcap, vlen, errf, list_sel, n_sel, PROJECT_CTAS)
+             fqoi, fsse, varint, vcap, vlen, errf, list_sel, n_sel)
     if hi_ctx is not None:
         hi_ctx.__exit__(None, None, None)
         main.wait_stream(hi)
@@ -785,6 +798,9 @@ def compress_device(f0: torch.Tensor, specs, dgrid: DeviceGrid, cfg, timer: Time
     # DEFLATE needs only the residual images' varint streams: it starts while
     # the side stream may still be projecting the others
     zout, zoff, zlen = deflate_launch(ws, varint, vcap, vlen, n_sel, dev)
+    timer.point("deflate_done", main, "deflate")
+    if side is not main:
+        timer.point("project_rest_done", side, "deflate")
     main.wait_event(ev_non)
     exc_list = T("exc_list", (total,), i32)
     exc_cnt = T("exc_cnt", (S,), i32)
@@ -996,11 +1012,9 @@ def _scratch(dev, name, nbytes):
     return buf
 
 
-# project the residual-free images on a side stream under the error-bound
-# search; their kernel keeps PROJECT_OVERLAP_CTAS one-warp CTAs per SM
+# project the residual-free images on a low-priority side stream under the
+# error-bound search
 PROJECT_OVERLAP = os.environ.get("MLK_PROJECT_OVERLAP", "1") != "0"
-PROJECT_OVERLAP_CTAS = int(os.environ.get("MLK_PROJECT_OVERLAP_CTAS", "9"))
-PROJECT_CTAS = int(os.environ.get("MLK_PROJECT_CTAS", "0"))  # 0: occupancy max
 _SIDE_STREAMS = {}
 
 
