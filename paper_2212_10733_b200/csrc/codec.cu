@@ -390,7 +390,7 @@ namespace wz {
 
 struct Lay {
     int nmax;
-    int win, srt, gi, p1, trees, hist, total;
+    int win, srt, gi, aux, trees, hist, total;
     int total_lz;         // phase 1 only (window + chain tables)
     int total_fl;         // phase 2 only (trees + histogram, from offset 0)
 };
@@ -725,9 +725,9 @@ struct GBits {
 };
 
 // Per-warp shared memory: the window, then one region reused by phase:
-//   chain build  : sorted positions | radix scratch (later gi) | p1 (its
-//                  first 1.5 KB the radix histograms until p1 is written)
-//   matching     : sorted positions | gi | p1
+//   chain build  : sorted positions | radix scratch (later gi) | radix
+//                  histograms (later the has-a-hash-head bit per position)
+//   matching     : sorted positions | gi | has-head bits
 //   flush        : Huffman trees | u32 symbol histogram
 // The symbol buffer lives in global scratch; the bit stream is OR-ed into
 // the zeroed global output.
@@ -742,8 +742,9 @@ __host__ __device__ inline Lay layout(int nmax) {
     const int b0 = o;
     L.srt = b0;
     L.gi = L.srt + al16(2 * nmax);
-    L.p1 = L.gi + al16(2 * nmax);
-    const int chains = L.p1 - b0 + al16(2 * nmax > RADIX_HIST_BYTES ? 2 * nmax : RADIX_HIST_BYTES);
+    L.aux = L.gi + al16(2 * nmax);
+    const int bits = 4 * ((nmax + 31) / 32 + 1);
+    const int chains = L.aux - b0 + al16(bits > RADIX_HIST_BYTES ? bits : RADIX_HIST_BYTES);
     L.trees = b0;
     L.hist = b0 + al16((int)sizeof(DTrees));
     const int flush = al16((int)sizeof(DTrees)) + 4 * 320;
@@ -782,7 +783,7 @@ k_deflate_warp(const uint8_t* __restrict__ in, const long long* __restrict__ in_
     uint8_t* win = base + Ly.win;
     uint16_t* srt = reinterpret_cast<uint16_t*>(base + Ly.srt);
     uint16_t* gi = reinterpret_cast<uint16_t*>(base + Ly.gi);
-    uint16_t* p1 = reinterpret_cast<uint16_t*>(base + Ly.p1);
+    unsigned* hbits = reinterpret_cast<unsigned*>(base + Ly.aux);
     wz::DTrees* trees = reinterpret_cast<wz::DTrees*>(base + (PH == 2 ? 0 : Ly.trees));
     const unsigned FULL = 0xffffffffu;
     const unsigned lt_mask = (1u << lane) - 1u;
@@ -838,7 +839,7 @@ k_deflate_warp(const uint8_t* __restrict__ in, const long long* __restrict__ in_
         //      is srt[gi[p] - 1 - i], and bit 15 of an entry marks the first
         //      position of its run (the end of every chain through it).
         const int n_ins = n - z6::MIN_MATCH + 1;  // positions 0 .. n-3
-        unsigned* hA = reinterpret_cast<unsigned*>(p1);  // 256 low-digit counters
+        unsigned* hA = hbits;                            // 256 low-digit counters
         unsigned* hB = hA + 256;                         // 128 high-digit counters
         for (int i = lane; i < 384; i += 32) hA[i] = 0u;
         __syncwarp();
@@ -894,7 +895,10 @@ k_deflate_warp(const uint8_t* __restrict__ in, const long long* __restrict__ in_
             if (PROF && pass == 0) t_pa = clock64();
         }
         t_pb = PROF ? clock64() : 0;
-        // run starts, each position's sorted index, and prev[] (hash_head)
+        // run starts, each position's sorted index, and whether its hash
+        // head (zlib's prev[] entry) is a position other than NIL = 0
+        for (int i = lane; i <= n / 32; i += 32) hbits[i] = 0u;
+        __syncwarp();
         unsigned carry_h = 0xffffffffu, carry_p = 0u;
         for (int b0 = 0; b0 < n_ins; b0 += 32) {
             const int j = b0 + lane;
@@ -909,13 +913,11 @@ k_deflate_warp(const uint8_t* __restrict__ in, const long long* __restrict__ in_
                 const bool first = hp != h;
                 if (first) srt[j] = (uint16_t)(p | 0x8000u);
                 gi[p] = (uint16_t)j;
-                p1[p] = first ? 0 : (uint16_t)pp;
+                if (!first && pp != 0u) atomicOr(hbits + (p >> 5), 1u << (p & 31));
             }
         }
         __syncwarp();
         t_2 = PROF ? clock64() : 0;
-        for (int p = (n_ins > 0 ? n_ins : 0) + lane; p < n; p += 32) p1[p] = 0;
-        __syncwarp();
         t_3 = PROF ? clock64() : 0;
         // ---- deflate_slow, warp-uniform state
         strstart = 0;
@@ -929,7 +931,8 @@ k_deflate_warp(const uint8_t* __restrict__ in, const long long* __restrict__ in_
                 // (or < 3 bytes left) only emits the previous byte as a
                 // literal -- take up to 32 of them in one step
                 const int q = strstart + lane;
-                const bool skip = q < n && (lookahead - lane < z6::MIN_MATCH || p1[q] == 0);
+                const bool skip = q < n && (lookahead - lane < z6::MIN_MATCH ||
+                                            ((hbits[q >> 5] >> (q & 31)) & 1u) == 0u);
                 const unsigned sk = __ballot_sync(FULL, skip);
                 const int f = sk == FULL ? 32 : __ffs(~sk) - 1;
                 if (f > 0) {
@@ -947,12 +950,13 @@ k_deflate_warp(const uint8_t* __restrict__ in, const long long* __restrict__ in_
                     continue;
                 }
             }
-            const int hash_head = lookahead >= z6::MIN_MATCH ? p1[strstart] : 0;
+            // a non-NIL hash head (strstart - head <= MAX_DIST always: n <= 16000)
+            const bool hash_head = lookahead >= z6::MIN_MATCH &&
+                                   ((hbits[strstart >> 5] >> (strstart & 31)) & 1u) != 0u;
             prev_length = match_length;
             prev_match = match_start;
             match_length = z6::MIN_MATCH - 1;
-            if (hash_head != 0 && prev_length < z6::LAZY &&
-                strstart - hash_head <= z6::MAX_DIST) {
+            if (hash_head && prev_length < z6::LAZY) {
                 const long long tlm0 = PROF ? clock64() : 0;
                 if (PROF) ++n_calls;
                 const int chain = prev_length >= z6::GOOD ? z6::CHAIN / 4 : z6::CHAIN;
