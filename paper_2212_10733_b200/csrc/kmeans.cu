@@ -14,7 +14,12 @@
 //    cluster's members in index order, dead clusters re-seeded at the first
 //    worst-served point against the partially updated centroids;
 //  * sorted result, cast to float32 (pq_train, quantizer.py:99-108).
-// One 1024-thread CTA per (shard, dim); members live in L2-resident scratch.
+// One 1024-thread CTA per (shard, dim).  When a shard's members fit (n <=
+// ~16.9k at K = 16, e.g. configs[2]'s 16,395), one n-double region of the
+// CTA's shared memory holds d2 during the seeding and the values during
+// Lloyd, next to both label arrays (SM = true); the values (seeding) and the
+// cluster-sorted copy (Lloyd) stay in L2-resident global scratch.  Larger
+// shards keep everything in the scratch.
 #include "common.cuh"
 
 // phase clocks of the last launch's CTA 0: load + distinct test, seeding,
@@ -25,9 +30,6 @@ namespace {
 
 constexpr int KT = 1024;           // threads per CTA
 constexpr int KW = KT / 32;        // warps
-constexpr int KM_MAX_N = 1 << 18;   // members per shard
-// heap slots of the pairwise trees: 2^(depth+1) < m / 28 per segment, + 2 per segment
-constexpr int KM_MAX_SLOTS = KM_MAX_N / 28 + 2 * MLK_MAXK + 64;
 
 struct KmSmem {
     double red[KW];
@@ -283,16 +285,18 @@ __device__ void block_pw_sums(const double* x, const int* seg_start, const int* 
     __syncthreads();
 }
 
+template <bool SM>
 __global__ void __launch_bounds__(KT, 1)
 k_kmeans(const double* __restrict__ lat, const MlkShard* __restrict__ shards, int L, int K,
          const long long* __restrict__ first_idx, const double* __restrict__ draws,
          double* __restrict__ scratch, float* __restrict__ cents, double* __restrict__ cents64,
-         int* __restrict__ info) {
+         int* __restrict__ info, int slots, int n_cap) {
     __shared__ KmSmem S;
-    extern __shared__ double dyn[];  // pairwise heap slots, slot kinds, warp counters
+    // pairwise heap slots, warp counters, slot kinds (+ SM: values, labels)
+    extern __shared__ double dyn[];
     double* val = dyn;
-    int* wcnt = reinterpret_cast<int*>(dyn + KM_MAX_SLOTS);   // [KW][K]
-    unsigned char* kind = reinterpret_cast<unsigned char*>(wcnt + KW * MLK_MAXK);
+    int* wcnt = reinterpret_cast<int*>(dyn + slots);   // [KW][K]
+    unsigned char* kind = reinterpret_cast<unsigned char*>(wcnt + KW * K);
 
     const int s = blockIdx.x / L, dim = blockIdx.x % L;
     const MlkShard sh = shards[s];
@@ -304,6 +308,12 @@ k_kmeans(const double* __restrict__ lat, const MlkShard* __restrict__ shards, in
     double* srt = base + 2 * n;
     unsigned short* lab = reinterpret_cast<unsigned short*>(base + 3 * n);
     unsigned short* lab2 = lab + n;
+    double* region = dyn + ((slots * 9 + KW * K * 4 + 15) / 16) * 2;
+    if (SM) {
+        d2 = region;
+        lab = reinterpret_cast<unsigned short*>(region + n_cap);
+        lab2 = lab + n_cap;
+    }
     float* out = cents + ((long long)s * L + dim) * K;
     double* out64 = cents64 ? cents64 + ((long long)s * L + dim) * K : nullptr;
     int* inf = info + (s * L + dim) * 4;
@@ -427,6 +437,12 @@ k_kmeans(const double* __restrict__ lat, const MlkShard* __restrict__ shards, in
         __syncthreads();
     }
 
+    if (SM) {  // d2 is dead: the region takes the values for Lloyd
+        __syncthreads();
+        for (int j = tid; j < n; j += KT) region[j] = v[j];
+        v = region;
+        __syncthreads();
+    }
     const long long kp_t2 = clock64();
     // ---- Lloyd (quantizer.py:78-90)
     for (int j = tid; j < n; j += KT) lab[j] = (unsigned short)nearest(v[j], S.cent, K);
@@ -562,11 +578,28 @@ extern "C" int mlk_kmeans(const double* lat, const MlkShard* shards, const MlkSh
     if (K < 1 || K > MLK_MAXK || L < 1 || L > MLK_MAXL) return MLK_ERR_CONFIG;
     for (int s = 0; s < n_shards; ++s)
         if (shards_h[s].n_img < 1 || shards_h[s].n_img > (1 << 18)) return MLK_ERR_DIM;
-    size_t dyn = (size_t)KM_MAX_SLOTS * (sizeof(double) + 1) + (size_t)KW * MLK_MAXK * sizeof(int);
-    cudaFuncSetAttribute(k_kmeans, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
-    k_kmeans<<<n_shards * L, KT, dyn, stream>>>(lat, shards, L, K,
-                                                reinterpret_cast<const long long*>(first_idx),
-                                                draws, scratch, cents, cents64, info);
+    int n_cap = 0;
+    for (int s = 0; s < n_shards; ++s) n_cap = shards_h[s].n_img > n_cap ? shards_h[s].n_img : n_cap;
+    // heap slots of the pairwise trees: 2^(depth+1) < m / 28 per segment, + 2 per segment
+    const int slots = n_cap / 28 + 2 * K + 64;
+    const size_t head = (size_t)((slots * 9 + KW * K * 4 + 15) / 16) * 16;
+    const size_t with_members = head + (size_t)n_cap * (sizeof(double) + 2 * sizeof(uint16_t));
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    if (with_members + sizeof(KmSmem) <= (size_t)optin) {
+        cudaFuncSetAttribute(k_kmeans<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)with_members);
+        k_kmeans<true><<<n_shards * L, KT, with_members, stream>>>(
+            lat, shards, L, K, reinterpret_cast<const long long*>(first_idx), draws, scratch,
+            cents, cents64, info, slots, n_cap);
+    } else {
+        cudaFuncSetAttribute(k_kmeans<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)head);
+        k_kmeans<false><<<n_shards * L, KT, head, stream>>>(
+            lat, shards, L, K, reinterpret_cast<const long long*>(first_idx), draws, scratch,
+            cents, cents64, info, slots, n_cap);
+    }
     return cudaGetLastError() == cudaSuccess ? MLK_OK : MLK_ERR_CUDA;
 }
 
