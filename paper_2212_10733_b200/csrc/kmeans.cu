@@ -45,6 +45,8 @@ struct KmSmem {
     int bcast_i;
     double bcast_d;
     double sums[MLK_MAXK];
+    double cs[MLK_MAXK];  // the centroids ascending (ties by index) ...
+    int ci[MLK_MAXK];     // ... and their indices
 };
 
 // ---------------------------------------------------------------- block helpers
@@ -153,14 +155,41 @@ __device__ double block_exscan(double v, double* total, KmSmem& S) {
     return r;
 }
 
-__device__ __forceinline__ int nearest(double v, const double* c, int K) {
-    int best = 0;
-    double bd = fabs(__dsub_rn(v, c[0]));
-    for (int k = 1; k < K; ++k) {
-        double d = fabs(__dsub_rn(v, c[k]));
-        if (d < bd) { bd = d; best = k; }
+// S.cs / S.ci = the centroids sorted ascending, equal values by index
+// (a rank per centroid: one pass, one barrier).  Whole CTA; c visible.
+__device__ void sort_cents(const double* c, int K, KmSmem& S) {
+    const int tid = threadIdx.x;
+    if (tid < K) {
+        const double x = c[tid];
+        int r = 0;
+        for (int j = 0; j < K; ++j) {
+            const double y = c[j];
+            r += (y < x) || (y == x && j < tid);
+        }
+        S.cs[r] = x;
+        S.ci[r] = tid;
     }
-    return best;
+    __syncthreads();
+}
+
+// quantizer._nearest (np.argmin |v - c_k|, quantizer.py:91-93) from the
+// sorted centroids: |v - c| rounded is non-increasing in
+// c up to v and non-decreasing after it, so the minimum is taken next to
+// v's insertion point p and the minimisers form one contiguous run around
+// it; the answer (np.argmin's first minimum) is the smallest index in that
+// run.  top = the largest power of two <= K.
+__device__ __forceinline__ int nearest_sorted(double v, const double* cs, const int* ci, int K,
+                                              int top) {
+    int p = 0;  // centroids < v (binary lifting over the sorted table)
+    for (int st = top; st; st >>= 1)
+        if (p + st <= K && cs[p + st - 1] < v) p += st;
+    const double dl = p > 0 ? fabs(__dsub_rn(v, cs[p - 1])) : INFINITY;
+    const double dr = p < K ? fabs(__dsub_rn(v, cs[p])) : INFINITY;
+    const double dm = dl < dr ? dl : dr;
+    int best = 0x7fffffff;
+    for (int i = p - 1; i >= 0 && fabs(__dsub_rn(v, cs[i])) == dm; --i) best = min(best, ci[i]);
+    for (int i = p; i < K && fabs(__dsub_rn(v, cs[i])) == dm; ++i) best = min(best, ci[i]);
+    return best == 0x7fffffff ? 0 : best;  // NaN v: every distance NaN -> index 0
 }
 
 // ---- numpy pairwise sums of many segments at once.  The recursion of
@@ -445,7 +474,10 @@ k_kmeans(const double* __restrict__ lat, const MlkShard* __restrict__ shards, in
     }
     const long long kp_t2 = clock64();
     // ---- Lloyd (quantizer.py:78-90)
-    for (int j = tid; j < n; j += KT) lab[j] = (unsigned short)nearest(v[j], S.cent, K);
+    const int ktop = 1 << (31 - __clz(K));
+    sort_cents(S.cent, K, S);
+    for (int j = tid; j < n; j += KT)
+        lab[j] = (unsigned short)nearest_sorted(v[j], S.cs, S.ci, K, ktop);
     __syncthreads();
     int sweeps = 0;
     const int wchunk = (n + KW - 1) / KW;
@@ -529,10 +561,11 @@ k_kmeans(const double* __restrict__ lat, const MlkShard* __restrict__ shards, in
         }
         if (tid < K) S.cent[tid] = S.newc[tid];
         __syncthreads();
+        sort_cents(S.cent, K, S);
         int changed = 0;
 #pragma unroll 2
         for (int j = tid; j < n; j += KT) {
-            unsigned short nl = (unsigned short)nearest(v[j], S.cent, K);
+            unsigned short nl = (unsigned short)nearest_sorted(v[j], S.cs, S.ci, K, ktop);
             lab2[j] = nl;
             changed |= (nl != lab[j]);
         }

@@ -65,6 +65,27 @@ def test_kmeans_matches_reference_vectors():
 
 @gpu
 @needs_cuda
+def test_kmeans_ties_and_duplicates_match_oracle():
+    """Lattice values (many duplicates, members exactly midway between two
+    centroids, centroids that coincide): the device's sorted-centroid
+    nearest must pick np.argmin's first minimum like the oracle."""
+    from oracle import port
+    rng = np.random.default_rng(21)
+    cases = [rng.integers(0, 24, 600) * 0.5,
+             np.concatenate([rng.integers(0, 40, 300).astype(float), np.full(50, 2.5),
+                             np.full(20, 7.5)]),
+             np.concatenate([np.zeros(100), np.full(100, 1e-300), np.ones(30),
+                             rng.integers(-40, 40, 200) * 0.25]),
+             rng.integers(0, 6, 400) * 1e16 + rng.integers(0, 4, 400)]
+    for i, v in enumerate(cases):
+        for seed in range(4):
+            got = mb.kmeans_1d(v, 16, seed)
+            want = port.kmeans(v, 16, seed)
+            assert np.array_equal(got, want), (i, seed)
+
+
+@gpu
+@needs_cuda
 def test_kmeans_deterministic_and_quality():
     rng = np.random.default_rng(12)
     v = np.concatenate([rng.normal(0, 1, 80), rng.normal(8, 0.5, 60), rng.normal(-5, 2, 60)])
