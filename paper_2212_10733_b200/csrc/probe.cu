@@ -209,6 +209,9 @@ k_probe_level(const double* __restrict__ f0, const double* __restrict__ stats,
     }
     if (!need) return;
     const double* x = shard_image(f0, sh, j, D);
+    // the whole image on its way to L2 at once: the lanes' loads below then
+    // wait for L2, not for one DRAM round trip per step
+    if (lane == 0) prefetch_l2_histogram(x, D);
     double z[MLK_MAXL];
 #pragma unroll
     for (int k = 0; k < MLK_MAXL; ++k)
