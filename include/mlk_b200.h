@@ -408,7 +408,8 @@ int mlk_list_flags(const uint8_t* flags, const MlkShard* shards, int32_t n_shard
                    int32_t* list, int32_t* count, cudaStream_t stream);
 
 /* the images of [0, total) with (flags & mask) != 0 into `set` and the rest
- * into `clear`, both ascending; *n_set = the size of `set` (device). */
+ * into `clear`, both ascending; *n_set = the size of `set` (device).  flags
+ * must be 4-byte aligned. */
 int mlk_split_flags(const uint8_t* flags, int32_t total, uint32_t mask, int32_t* set,
                     int32_t* clear, int32_t* n_set, cudaStream_t stream);
 

@@ -150,40 +150,44 @@ __global__ void k_pack_exc(const double* __restrict__ f0, const MlkShard* __rest
 }
 
 // the images of [0, total) with (flags & mask) != 0 and those with == 0, each
-// list in increasing order (one CTA: chunked counts + block scan)
+// list in increasing order.  One CTA per 1024-image tile: the set count of
+// all earlier tiles (re-counted from the flags, 4 per load: <= 128 KB of L2
+// reads per CTA), then ballot ranks and one block scan place the tile.
 __global__ void __launch_bounds__(LT)
 k_split_flags(const unsigned char* __restrict__ flags, int total, unsigned mask,
               int* __restrict__ set, int* __restrict__ clear, int* __restrict__ n_set) {
-    __shared__ int wtot[32];
+    __shared__ int wc[32], wp[32];
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-    const int chunk = (total + LT - 1) / LT;
-    const int lo = min(total, tid * chunk), hi = min(total, lo + chunk);
-    int c = 0;
-    for (int j = lo; j < hi; ++j) c += (flags[j] & mask) != 0;
-    int inc = c;
-    for (int o = 1; o < 32; o <<= 1) {
-        int t = __shfl_up_sync(0xffffffffu, inc, o);
-        if (lane >= o) inc += t;
+    const uchar4* f4 = reinterpret_cast<const uchar4*>(flags);
+    int pre = 0;  // set entries of the tiles before this one
+    for (int q = tid; q < (int)blockIdx.x * (LT / 4); q += LT) {
+        const uchar4 x = f4[q];
+        pre += ((x.x & mask) != 0) + ((x.y & mask) != 0) + ((x.z & mask) != 0) +
+               ((x.w & mask) != 0);
     }
-    if (lane == 31) wtot[w] = inc;
+    pre = warp_sum_int(pre);
+    if (lane == 0) wp[w] = pre;
+    const int j = blockIdx.x * LT + tid;
+    const bool v = j < total;
+    const bool f = v && (flags[j] & mask) != 0;
+    const unsigned b = __ballot_sync(0xffffffffu, f);
+    if (lane == 0) wc[w] = __popc(b);
     __syncthreads();
     if (w == 0) {
-        int t = wtot[lane];
-        int ti = t;
+        const int p = warp_sum_int(wp[lane]);
+        const int c = wc[lane];
+        int inc = c;
         for (int o = 1; o < 32; o <<= 1) {
-            int u = __shfl_up_sync(0xffffffffu, ti, o);
-            if (lane >= o) ti += u;
+            const int t = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += t;
         }
-        wtot[lane] = ti - t;
-        if (lane == 31) n_set[0] = ti;
+        wc[lane] = p + inc - c;
+        if (lane == 31 && blockIdx.x == gridDim.x - 1) n_set[0] = p + inc;
     }
     __syncthreads();
-    int ps = wtot[w] + inc - c;  // set entries before this thread's chunk
-    int pc = lo - ps;            // clear entries before it
-    for (int j = lo; j < hi; ++j) {
-        if ((flags[j] & mask) != 0) set[ps++] = j;
-        else clear[pc++] = j;
-    }
+    const int ps = wc[w] + __popc(b & ((1u << lane) - 1u));  // set entries before j
+    if (f) set[ps] = j;
+    else if (v) clear[j - ps] = j;
 }
 
 }  // namespace
@@ -191,7 +195,8 @@ k_split_flags(const unsigned char* __restrict__ flags, int total, unsigned mask,
 extern "C" int mlk_split_flags(const uint8_t* flags, int32_t total, uint32_t mask, int32_t* set,
                                int32_t* clear, int32_t* n_set, cudaStream_t stream) {
     if (total <= 0) return MLK_OK;
-    k_split_flags<<<1, LT, 0, stream>>>(flags, total, mask, set, clear, n_set);
+    if (reinterpret_cast<uintptr_t>(flags) & 3) return MLK_ERR_CONFIG;  // uchar4 counts
+    k_split_flags<<<(total + LT - 1) / LT, LT, 0, stream>>>(flags, total, mask, set, clear, n_set);
     return cudaGetLastError() == cudaSuccess ? MLK_OK : MLK_ERR_CUDA;
 }
 

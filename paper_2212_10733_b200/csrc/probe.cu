@@ -72,6 +72,7 @@ k_probe_bins(const double* __restrict__ f0, const MlkShard* __restrict__ shards,
     }
     const int e0 = pb_e0(eb_hi[s]);
     const double* x = shard_image(f0, sh, j, D);
+    if (lane == 0) prefetch_l2_histogram(x, D);
     double z[MLK_MAXL];
 #pragma unroll
     for (int k = 0; k < MLK_MAXL; ++k)

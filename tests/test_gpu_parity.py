@@ -316,6 +316,28 @@ def test_operator_api_newton_matches_compiled_reference():
         np.testing.assert_allclose(lam, a[f"nw{t}_lam"], rtol=1e-9, atol=1e-12)
 
 
+def test_split_flags_lists_match_numpy():
+    """mlk_split_flags (the selected / residual-free image lists): ascending
+    lists and the count for ragged totals, empty and full selections."""
+    from paper_2212_10733_b200._lib import call
+    dev = torch.device("cuda", 0)
+    rng = np.random.default_rng(8)
+    for total, p in [(1, 0.5), (1023, 0.3), (1024, 0.0), (1025, 1.0), (5000, 0.02),
+                     (131160, 0.22)]:
+        fl = (rng.random(total) < p).astype(np.uint8) * 4 + rng.integers(0, 2, total).astype(
+            np.uint8)
+        f_d = torch.from_numpy(fl).to(dev)
+        s_d = torch.full((total,), -1, dtype=torch.int32, device=dev)
+        c_d = torch.full((total,), -1, dtype=torch.int32, device=dev)
+        n_d = torch.zeros(1, dtype=torch.int32, device=dev)
+        call("mlk_split_flags", f_d, total, 4, s_d, c_d, n_d)
+        want = np.flatnonzero(fl & 4)
+        n = int(n_d.item())
+        assert n == want.size
+        assert np.array_equal(s_d[:n].cpu().numpy(), want)
+        assert np.array_equal(c_d[:total - n].cpu().numpy(), np.flatnonzero((fl & 4) == 0))
+
+
 def test_device_zlib_matches_host_zlib():
     import zlib
 
