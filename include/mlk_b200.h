@@ -392,6 +392,11 @@ int mlk_parse_residual_section(const uint8_t* sec, int64_t len, int32_t n_images
 /* HOST: 1 if p lies in page-locked host memory (cudaHostAlloc/Register). */
 int mlk_is_pinned(const void* p);
 
+/* HOST: page-lock / release an existing host range (cudaHostRegister), e.g.
+ * the shared mapping of an output file that device results are copied to. */
+int mlk_host_register(void* p, int64_t bytes);
+int mlk_host_unregister(void* p);
+
 /* HOST memory only: exception entries <I idx[k]> + 8 D bytes of the host
  * histogram at src + src_off[k] (elements), back to back at dst
  * (pipeline.py:116-184, 281-292).  compress() fills the archive's exception

@@ -95,6 +95,8 @@ _SIGS = {
     "mlk_parse_residual_section": [_P, _I64, _I32, _I32, _I32, _I64, _I32, _P, _P, _P, _P, _P,
                                    _P, _P],
     "mlk_is_pinned": [_P],
+    "mlk_host_register": [_P, _I64],
+    "mlk_host_unregister": [_P],
     "mlk_host_exception_entries": [_P, _P, _P, _P, _I64, _I32],
     "mlk_probe": [_P, _P, _P, _I32, _P, _P, _I32, _P, _I32, _P, _P, _P, _P, _I32, _P, _D, _P,
                   _I32, _I32, _I32, _P, _P, _P, _P],

@@ -281,6 +281,25 @@ extern "C" int mlk_parse_residual_section(const uint8_t* sec, int64_t len, int32
 
 // HOST: 1 if p points into page-locked (pinned) host memory -- the public
 // API then DMAs straight from the caller's array without a staging copy.
+// page-lock an existing host range (e.g. a shared file mapping) so copies
+// to it DMA straight from the device
+extern "C" int mlk_host_register(void* p, int64_t bytes) {
+    if (!p || bytes <= 0) return MLK_ERR_CONFIG;
+    if (cudaHostRegister(p, (size_t)bytes, cudaHostRegisterDefault) != cudaSuccess) {
+        cudaGetLastError();
+        return MLK_ERR_CUDA;
+    }
+    return MLK_OK;
+}
+
+extern "C" int mlk_host_unregister(void* p) {
+    if (cudaHostUnregister(p) != cudaSuccess) {
+        cudaGetLastError();
+        return MLK_ERR_CUDA;
+    }
+    return MLK_OK;
+}
+
 extern "C" int mlk_is_pinned(const void* p) {
     cudaPointerAttributes a;
     if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {

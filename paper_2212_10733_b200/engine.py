@@ -1341,7 +1341,18 @@ def prepare_decode(archive, dev, sp=None) -> DecodePlan:
             exc_src.append(np.zeros(0, np.int64))
     n_res = sum(len(x) for x in res_idx)
     n_exc = sum(len(x) for x in exc_idx)
-    arc_d = hostio.upload_bytes(archive, dev)
+    # everything but the exception images of members outside the range (the
+    # sorted exception list makes this rank's records one run per shard)
+    ranges, at = [], 0
+    for s, d in enumerate(secs):
+        eo = d["exceptions"][0] + 4
+        ranges.append((at, eo))
+        if len(exc_src[s]):
+            ranges.append((int(exc_src[s][0]) - 4, int(exc_src[s][-1]) + 8 * D))
+        at = eo + d["exceptions"][1] - 4
+    ranges.append((at, len(raw)))
+    ranges = [(a_, b_) for a_, b_ in ranges if b_ > a_]
+    arc_d = hostio.upload_bytes(archive, dev, ranges if sp is not None else None)
     if sp is not None:
         specs = split_layout(sp, models, rows, cols)
         plane_lo, plane_hi = sp.plane_lo, sp.plane_hi

@@ -24,7 +24,7 @@ import numpy as np
 import torch
 
 __all__ = ["upload_planes", "upload_pieces", "upload_bytes", "download_bytes", "download_view",
-           "download_array", "download_pinned_array", "download_into", "mapped_file", "release_maps", "pinned", "pinned_empty", "ArchiveWriter"]
+           "download_array", "download_pinned_array", "download_into", "download_to_file", "mapped_file", "release_maps", "pinned", "pinned_empty", "ArchiveWriter"]
 
 CHUNK = 64 << 20
 UP_CHUNK = 2 << 20    # upload_pieces copy granularity
@@ -506,8 +506,12 @@ def download_view(src: torch.Tensor, nbytes: int) -> np.ndarray:
     return stage.numpy()[:nbytes]
 
 
-def upload_bytes(raw, dev) -> torch.Tensor:
-    """A bytes-like object -> device uint8 tensor (pinned staging, chunked)."""
+def upload_bytes(raw, dev, ranges=None) -> torch.Tensor:
+    """A bytes-like object -> device uint8 tensor of the same length (pinned
+    staging, chunked).  ranges: [(start, end), ...] -- only those bytes are
+    copied (each to its own offset); the rest of the tensor is left
+    uninitialised (a rank decoding part of an archive skips the other
+    ranks' exception images)."""
     src = np.frombuffer(raw, dtype=np.uint8)
     n = src.size
     buf = torch.empty(max(n, 1), dtype=torch.uint8, device=dev)
@@ -518,7 +522,8 @@ def upload_bytes(raw, dev) -> torch.Tensor:
     if last is not None:
         last.synchronize()
     st_np = stage.numpy()
-    spans = [(a, min(n, a + CHUNK)) for a in range(0, n, CHUNK)]
+    spans = [(a, min(e, a + CHUNK)) for s0, e in (ranges or [(0, n)])
+             for a in range(s0, e, CHUNK)]
 
     def fill(span):
         a, b = span
@@ -571,7 +576,8 @@ def download_array(src: torch.Tensor, shape, dtype=np.float64) -> np.ndarray:
     return out
 
 
-_MAPS = {}
+_MAPS = {}   # (st_dev, st_ino, size) -> mmap
+_REGS = {}   # (map key, page-aligned start, end) -> registered address
 
 
 def mapped_file(fd: int, total: int) -> np.ndarray:
@@ -586,15 +592,53 @@ def mapped_file(fd: int, total: int) -> np.ndarray:
     m = _MAPS.get(key)
     if m is None:
         for k in [k for k in _MAPS if k[:2] == key[:2]]:
-            del _MAPS[k]  # unmapped once no view of it is left
+            _drop_map(k)
         flags = mmap.MAP_SHARED | getattr(mmap, "MAP_POPULATE", 0)
         m = _MAPS[key] = mmap.mmap(fd, total, flags, mmap.PROT_WRITE | mmap.PROT_READ)
     return np.frombuffer(m, dtype=np.uint8)
 
 
+def _drop_map(key):
+    from ._lib import lib
+    for rk in [rk for rk in _REGS if rk[0] == key]:
+        lib().mlk_host_unregister(ctypes.c_void_p(_REGS.pop(rk)))
+    del _MAPS[key]  # unmapped once no view of it is left
+
+
 def release_maps() -> None:
-    """Unmap every cached mapped_file view (call after deleting the files)."""
-    _MAPS.clear()  # each mapping goes once no view of it is left
+    """Unregister and drop every cached mapped_file mapping (call after
+    deleting the files)."""
+    for k in list(_MAPS):
+        _drop_map(k)
+
+
+def download_to_file(src: torch.Tensor, nbytes: int, fd: int, total: int, offset: int) -> None:
+    """The first nbytes of a device tensor into bytes [offset, offset + nbytes)
+    of an open file of size `total`, by DMA straight into its shared mapping:
+    the page range is page-locked once (cudaHostRegister, cached with the
+    mapping) and every later call is one device-to-host copy."""
+    if nbytes == 0:
+        return
+    from ._lib import lib
+    view = mapped_file(fd, total)
+    st = os.fstat(fd)
+    key = (st.st_dev, st.st_ino, total)
+    base = view.ctypes.data
+    page = os.sysconf("SC_PAGE_SIZE")
+    lo = (base + offset) // page * page
+    hi = -(-(base + offset + nbytes) // page) * page
+    hi = min(hi, -(-(base + total) // page) * page)
+    rk = (key, lo, hi)
+    if rk not in _REGS:
+        if lib().mlk_host_register(ctypes.c_void_p(lo), hi - lo) != 0:
+            del view
+            download_into(src, nbytes, mapped_file(fd, total)[offset:offset + nbytes])
+            return
+        _REGS[rk] = lo
+    dst = torch.from_numpy(view[offset:offset + nbytes])
+    dst.copy_(src.reshape(-1).view(torch.uint8)[:nbytes], non_blocking=True)
+    torch.cuda.current_stream(src.device).synchronize()
+    del dst, view
 
 
 def download_into(src: torch.Tensor, nbytes: int, dst: np.ndarray) -> None:

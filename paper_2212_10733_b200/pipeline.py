@@ -632,10 +632,7 @@ def decompress_distributed(archive: bytes, group=None, gather: bool = True,
             dist.barrier(group=group)
         fd = os.open(out_path, os.O_RDWR)
         try:
-            o0 = plan.plane_lo * nd * 8
-            dst = hostio.mapped_file(fd, total)[o0:o0 + plan.out_elems * 8]
-            hostio.download_into(mine, plan.out_elems * 8, dst)
-            del dst
+            hostio.download_to_file(mine, plan.out_elems * 8, fd, total, plan.plane_lo * nd * 8)
         finally:
             os.close(fd)
         if on and sp.world > 1:
