@@ -392,6 +392,15 @@ int mlk_parse_residual_section(const uint8_t* sec, int64_t len, int32_t n_images
 /* HOST: 1 if p lies in page-locked host memory (cudaHostAlloc/Register). */
 int mlk_is_pinned(const void* p);
 
+/* HOST: the next `depth` decisions of n error-bound searches as heap-ordered
+ * nodes (residual.py:129-173; engine._Search): kind[i * 2^depth + v] in {0
+ * ended, 1 eb_hi probe, 2 bisection, 3 floor probe} and the bisection
+ * midpoint 0.5 * (lo + hi) in log space (the caller exponentiates). */
+int mlk_search_tree(const int8_t* kind0, const int32_t* step0, const uint8_t* best0,
+                    const double* lo0, const double* hi0, const double* lo_end,
+                    const double* hi_end, int32_t n, int32_t depth, int32_t steps, int8_t* kind,
+                    double* mid);
+
 /* HOST: page-lock / release an existing host range (cudaHostRegister), e.g.
  * the shared mapping of an output file that device results are copied to. */
 int mlk_host_register(void* p, int64_t bytes);

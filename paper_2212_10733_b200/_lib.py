@@ -96,6 +96,7 @@ _SIGS = {
                                    _P, _P],
     "mlk_is_pinned": [_P],
     "mlk_host_register": [_P, _I64],
+    "mlk_search_tree": [_P, _P, _P, _P, _P, _P, _P, _I32, _I32, _I32, _P, _P],
     "mlk_host_unregister": [_P],
     "mlk_host_exception_entries": [_P, _P, _P, _P, _I64, _I32],
     "mlk_probe": [_P, _P, _P, _I32, _P, _P, _I32, _P, _I32, _P, _P, _P, _P, _I32, _P, _D, _P,
@@ -128,9 +129,9 @@ _ERRORS = {-1: DimensionError, -2: ConfigError, -3: FormatError, -4: SizeMismatc
 
 
 @functools.lru_cache(maxsize=None)
-def lib() -> ctypes.CDLL:
-    if not torch.cuda.is_available():
-        raise BackendError("no CUDA device: the B200 path has no CPU fallback")
+def host_lib() -> ctypes.CDLL:
+    """The library with its signatures set, for its HOST-only entry points
+    (search trees, archive parsing): loads without a GPU."""
     if not LIB_PATH.exists():
         raise BackendError(f"{LIB_PATH.name} not built; run __graft_entry__.build()")
     so = ctypes.CDLL(str(LIB_PATH))
@@ -141,6 +142,14 @@ def lib() -> ctypes.CDLL:
         fn.argtypes = argtypes
         fn.restype = ctypes.c_int
     so.mlk_version.restype = ctypes.c_char_p
+    return so
+
+
+@functools.lru_cache(maxsize=None)
+def lib() -> ctypes.CDLL:
+    if not torch.cuda.is_available():
+        raise BackendError("no CUDA device: the B200 path has no CPU fallback")
+    so = host_lib()
     torch.cuda.init()
     if so.mlk_device_check() != 0:
         raise BackendError("current CUDA device is not sm_100 (B200)")

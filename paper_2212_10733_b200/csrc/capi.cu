@@ -2,6 +2,7 @@
 // (mlk/kernels.py:20-32) as batched device entry points.
 #include <cstdio>
 #include <cstring>
+#include <vector>
 
 #include "common.cuh"
 
@@ -281,6 +282,61 @@ extern "C" int mlk_parse_residual_section(const uint8_t* sec, int64_t len, int32
 
 // HOST: 1 if p points into page-locked (pinned) host memory -- the public
 // API then DMAs straight from the caller's array without a staging copy.
+// HOST: the next `depth` decisions of n error-bound searches (engine._Search,
+// residual.py:129-173) as heap-ordered nodes 1 .. 2^depth - 1 per search:
+// kind (0 ended, 1 the eb_hi probe, 2 bisection, 3 the 2^-20 floor probe)
+// and, for bisection nodes, the log-space midpoint 0.5 * (lo + hi) (the
+// scalar machine's operation; the caller takes numpy's exp of it).  Accepted
+// (2v) -> (mid, hi) and a best bound, rejected (2v + 1) -> (lo, mid); after
+// `steps` bisections a search ends (best found) or probes the floor.
+extern "C" int mlk_search_tree(const int8_t* kind0, const int32_t* step0, const uint8_t* best0,
+                               const double* lo0, const double* hi0, const double* lo_end,
+                               const double* hi_end, int32_t n, int32_t depth, int32_t steps,
+                               int8_t* kind, double* mid) {
+    if (n < 0 || depth < 1 || depth > 20) return MLK_ERR_CONFIG;
+    const int N = 1 << depth;
+    std::vector<double> lo(N), hi(N);
+    std::vector<int32_t> st(N);
+    std::vector<uint8_t> bst(N);
+    for (int i = 0; i < n; ++i) {
+        int8_t* k = kind + (size_t)i * N;
+        double* m = mid + (size_t)i * N;
+        k[0] = 0;
+        m[0] = 0.0;
+        k[1] = kind0[i];
+        lo[1] = lo0[i];
+        hi[1] = hi0[i];
+        st[1] = step0[i];
+        bst[1] = best0[i];
+        for (int v = 1; v < N; ++v) {
+            m[v] = k[v] == 2 ? 0.5 * (lo[v] + hi[v]) : 0.0;
+            if (2 * v + 1 >= N) continue;
+            const int a = 2 * v, r = 2 * v + 1;
+            k[a] = k[r] = 0;
+            lo[a] = lo[r] = hi[a] = hi[r] = 0.0;
+            st[a] = st[r] = 0;
+            bst[a] = bst[r] = 0;
+            if (k[v] == 1) {  // eb_hi rejected -> bisection over [log(eb_hi 2^-20), log(eb_hi)]
+                k[r] = steps == 0 ? 3 : 2;
+                lo[r] = lo_end[i];
+                hi[r] = hi_end[i];
+            } else if (k[v] == 2) {
+                const int s1 = st[v] + 1;
+                lo[a] = m[v];
+                hi[a] = hi[v];
+                bst[a] = 1;
+                lo[r] = lo[v];
+                hi[r] = m[v];
+                bst[r] = bst[v];
+                st[a] = st[r] = s1;
+                k[a] = s1 == steps ? 0 : 2;
+                k[r] = s1 == steps ? (bst[r] ? 0 : 3) : 2;
+            }
+        }
+    }
+    return MLK_OK;
+}
+
 // page-lock an existing host range (e.g. a shared file mapping) so copies
 // to it DMA straight from the device
 extern "C" int mlk_host_register(void* p, int64_t bytes) {

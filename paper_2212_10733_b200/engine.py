@@ -172,85 +172,42 @@ class _Search:
         return self
 
 
-@functools.lru_cache(maxsize=64)
-def _heap_shape(code: int, step: int, has_best: bool, depth: int):
-    """Tree shape of the next `depth` search decisions from a root of the
-    given (stage code, bisection step, best-found): per level the node kinds
-    and, for the level below, where each child's (lo, hi) comes from in
-    [parent lo | parent mid | parent hi | log(eb_hi 2^-20) | log(eb_hi)]."""
-    NONE, HI, BIS, LOW = 0, 1, 2, 3
-    kind = np.array([code], dtype=np.int8)
-    best = np.array([has_best])
-    levels = []
-    for lvl in range(depth):
-        m = kind.size
-        if lvl + 1 == depth:
-            levels.append((kind, None, None))
-            break
-        k2, best2 = np.repeat(kind, 2), np.repeat(best, 2)
-        par = np.repeat(np.arange(m), 2)
-        acc = np.zeros(2 * m, dtype=bool)
-        acc[0::2] = True
-        lo_src, hi_src = par.copy(), 2 * m + par  # default: inherit (lo, hi)
-        nk = np.full(2 * m, NONE, dtype=np.int8)
-        hrej = (k2 == HI) & ~acc                 # hi rejected -> bisection over [lo0, hi0]
-        nk[hrej] = BIS
-        lo_src[hrej], hi_src[hrej], best2[hrej] = 3 * m, 3 * m + 1, False
-        bis = k2 == BIS                          # accepted -> (mid, hi); rejected -> (lo, mid)
-        ba, br = bis & acc, bis & ~acc
-        lo_src[ba], best2[ba] = m + par[ba], True
-        hi_src[br] = m + par[br]
-        nk[bis] = BIS
-        if (kind == BIS).any():                  # low: either outcome ends the search
-            step += 1
-            if step == STEPS:                    # settle: done with the best bound, else low
-                nk[bis & best2] = NONE
-                nk[bis & ~best2] = LOW
-        elif (kind == HI).any():
-            step = 0
-        levels.append((kind, lo_src, hi_src))
-        kind, best = nk, best2
-    return tuple(levels)
-
-
 def _search_heap(states, depth: int) -> np.ndarray:
     """Candidate bounds of the next `depth` decisions of each search, in heap
     order: column 1 is the state's query, 2i / 2i+1 the next query after node
-    i is accepted / rejected; NaN where the search has ended.  Built level by
-    level with vectorised numpy over all searches that share a tree shape --
-    the same float operations and the same numpy exp/log as the scalar state
-    machine, hence bit-identical values (compress_device re-checks every
-    node it walks against _Search.query)."""
+    i is accepted / rejected; NaN where the search has ended.  The tree's
+    structure and log-space midpoints come from mlk_search_tree (host C, the
+    scalar machine's own additions and halvings); the bounds are numpy's
+    exp of those midpoints and the same eb_hi / eb_hi 2^-20 products as
+    _Search.query -- bit-identical values (compress_device re-checks every
+    root against _Search.query; tests/test_host_logic.py pins whole trees)."""
     n = 1 << depth
-    out = np.full((len(states), n), np.nan)
+    S = len(states)
     codes = {"done": 0, "hi": 1, "bis": 2, "low": 3}
-    groups = {}
-    for i, st in enumerate(states):
-        sig = (codes[st.stage], st.step if st.stage == "bis" else 0, st.best is not None)
-        groups.setdefault(sig, []).append(i)
-    for (code, step, has_best), rows in groups.items():
-        if code == 0:
-            continue
-        sts = [states[i] for i in rows]
-        eb_hi = np.array([st.eb_hi for st in sts], dtype=np.float64)[:, None]
-        ends = np.concatenate([np.log(eb_hi * SPAN), np.log(eb_hi)], axis=1)
-        low_q = eb_hi * SPAN
-        lo = np.array([[st.lo if code == 2 else 0.0] for st in sts], dtype=np.float64)
-        hi = np.array([[st.hi if code == 2 else 0.0] for st in sts], dtype=np.float64)
-        cand = np.full((len(rows), n), np.nan)
-        for lvl, (kind, lo_src, hi_src) in enumerate(_heap_shape(code, step, has_best, depth)):
-            mid = 0.5 * (lo + hi)
-            q = cand[:, 1 << lvl:2 << lvl]
-            b = kind == 2
-            if b.any():
-                q[:, b] = np.exp(mid[:, b])
-            q[:, kind == 1] = eb_hi
-            q[:, kind == 3] = low_q
-            if lo_src is None:
-                break
-            src = np.concatenate([lo, mid, hi, ends], axis=1)
-            lo, hi = src[:, lo_src], src[:, hi_src]
-        out[rows] = cand
+    kind0 = np.array([codes[st.stage] for st in states], dtype=np.int8)
+    step0 = np.array([st.step if st.stage == "bis" else 0 for st in states], dtype=np.int32)
+    best0 = np.array([st.best is not None for st in states], dtype=np.uint8)
+    lo0 = np.array([st.lo if st.stage == "bis" else 0.0 for st in states], dtype=np.float64)
+    hi0 = np.array([st.hi if st.stage == "bis" else 0.0 for st in states], dtype=np.float64)
+    eb_hi = np.array([st.eb_hi for st in states], dtype=np.float64)
+    lo_end, hi_end = np.log(eb_hi * SPAN), np.log(eb_hi)
+    kind = np.empty((S, n), dtype=np.int8)
+    mid = np.empty((S, n), dtype=np.float64)
+    if S:
+        rc = _lib.host_lib().mlk_search_tree(
+            kind0.ctypes.data, step0.ctypes.data, best0.ctypes.data, lo0.ctypes.data,
+            hi0.ctypes.data, lo_end.ctypes.data, hi_end.ctypes.data, S, depth, STEPS,
+            kind.ctypes.data, mid.ctypes.data)
+        if rc != 0:
+            raise ConfigError("search tree depth out of range")
+    out = np.full((S, n), np.nan)
+    b = kind == 2
+    out[b] = np.exp(mid[b])
+    ebc = np.broadcast_to(eb_hi[:, None], (S, n))
+    h = kind == 1
+    out[h] = ebc[h]
+    lw = kind == 3
+    out[lw] = (ebc * SPAN)[lw]
     return out
 
 
