@@ -423,6 +423,7 @@ def main():
     if True:
         torch.cuda.synchronize()
         wall0 = time.perf_counter()
+        launches0 = _lib.LAUNCHES
         start.record()
         for _ in range(args.steps):
             timer = engine.Timer(True)
@@ -435,7 +436,7 @@ def main():
         wall_ms = 1e3 * (time.perf_counter() - wall0) / args.steps
     if not args.no_clocks:
         clk.__exit__(None, None, None)
-    launches = _lib.LAUNCHES
+    launches = _lib.LAUNCHES - launches0  # this rank's kernels in the timed region
     probe_rounds = out.timings.get("probe_rounds")
     it_h, st_h = out.host("iters"), out.host("status")
     newton = {"mean_iters": float(it_h.mean()), "max_iters": int(it_h.max()),
@@ -568,6 +569,7 @@ def main():
                 "stage_ms_by_rank": stage_by_rank, "probe_rounds": probe_rounds,
                 "newton": newton, "roofline": roofline, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e,
                 "decompress_and_report": dec, "gpu_launches": launches,
+                "gpu_launches_per_step": launches / args.steps,
                 "train": train, "clocks": clk.summary(),
                 "ratio": None if dec is None else dec["ratio"]}
         if world > 1:
