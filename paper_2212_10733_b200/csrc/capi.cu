@@ -94,30 +94,69 @@ k_varint_enc(const unsigned long long* v, const long long* off, unsigned char* o
     if (tid == 0) out_len[s] = carry;
 }
 
-__global__ void k_varint_dec(const unsigned char* in, const long long* in_off,
-                             const long long* in_len, int n_streams, const long long* count,
-                             unsigned long long* vals, const long long* val_off,
-                             long long* consumed) {
-    int s = blockIdx.x * blockDim.x + threadIdx.x;
+// kernels.varint_decode (_ckernels.pyx:174-211), one warp per stream, 32
+// bytes per step: the terminators (byte < 0x80) are balloted, so the lane
+// holding a value's last byte knows the value's index (terminators before
+// it) and first byte (the previous terminator + 1) and assembles it from
+// those <= 10 bytes (L1 hits).  Errors as the sequential loop raises them: a
+// value of index < count whose first 10 bytes all continue -> -2 (exceeds 64
+// bits; such a value precedes any truncation), else the stream ending inside
+// value `count - 1` or earlier -> -1, or -2 if that unfinished value already
+// has 10 continuation bytes.
+__global__ void k_varint_dec(const unsigned char* __restrict__ in,
+                             const long long* __restrict__ in_off,
+                             const long long* __restrict__ in_len, int n_streams,
+                             const long long* __restrict__ count,
+                             unsigned long long* __restrict__ vals,
+                             const long long* __restrict__ val_off,
+                             long long* __restrict__ consumed) {
+    const int s = (int)((blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5);
+    const int lane = threadIdx.x & 31;
     if (s >= n_streams) return;
+    const unsigned FULL = 0xffffffffu, lt = (1u << lane) - 1u;
     const unsigned char* p = in + in_off[s];
     const long long size = in_len[s], cnt = count[s];
     unsigned long long* o = vals + val_off[s];
-    long long pos = 0;
-    for (long long i = 0; i < cnt; ++i) {
-        unsigned long long x = 0;
-        int sh = 0;
-        for (;;) {
-            if (pos >= size) { consumed[s] = -1; return; }
-            unsigned char c = p[pos++];
-            x |= (unsigned long long)(c & 0x7f) << sh;
-            if (c < 0x80) break;
-            sh += 7;
-            if (sh > 63) { consumed[s] = -2; return; }
-        }
-        o[i] = x;
+    if (cnt <= 0) {
+        if (lane == 0) consumed[s] = 0;
+        return;
     }
-    consumed[s] = pos;
+    long long k0 = 0;     // values completed before this step
+    long long start = 0;  // first byte of the value in progress
+    bool bad = false;     // a value of index < count longer than 10 bytes
+    for (long long base = 0; base < size; base += 32) {
+        const long long q = base + lane;
+        const bool valid = q < size;
+        const unsigned c = valid ? p[q] : 0x80u;
+        const bool end = valid && c < 0x80u;
+        const unsigned term = __ballot_sync(FULL, end);
+        long long k = -1;
+        bool mybad = false;
+        if (end) {
+            k = k0 + __popc(term & lt);
+            if (k < cnt) {
+                const unsigned below = term & lt;
+                const long long st = below ? base + (31 - __clz(below)) + 1 : start;
+                const int len = (int)(q - st + 1);
+                if (len > 10) {
+                    mybad = true;
+                } else {
+                    unsigned long long x = 0;
+                    for (int i = 0; i < len; ++i)
+                        x |= (unsigned long long)(p[st + i] & 0x7fu) << (7 * i);
+                    o[k] = x;
+                }
+            }
+        }
+        bad |= __any_sync(FULL, mybad);
+        if (k0 + __popc(term) >= cnt) {  // value count - 1 ends in this step
+            if (k == cnt - 1) consumed[s] = bad ? -2 : q + 1;
+            return;
+        }
+        k0 += __popc(term);
+        if (term) start = base + (31 - __clz(term)) + 1;
+    }
+    if (lane == 0) consumed[s] = (bad || size - start >= 10) ? -2 : -1;
 }
 
 // ---------------------------------------------------------------- bit packing
@@ -204,7 +243,7 @@ extern "C" int mlk_varint_decode_batch(const uint8_t* in, const int64_t* in_off,
                                        const int64_t* val_off, int64_t* consumed,
                                        cudaStream_t stream) {
     if (n_streams <= 0) return MLK_OK;
-    k_varint_dec<<<(n_streams + 127) / 128, 128, 0, stream>>>(
+    k_varint_dec<<<(n_streams + 3) / 4, 128, 0, stream>>>(
         in, reinterpret_cast<const long long*>(in_off), reinterpret_cast<const long long*>(in_len),
         n_streams, reinterpret_cast<const long long*>(count),
         reinterpret_cast<unsigned long long*>(values), reinterpret_cast<const long long*>(val_off),

@@ -5,6 +5,10 @@
 // the stored lambdas/QoIs and the default floor (pipeline.py:422,
 // lagrange.py:152-185, exact elementwise order) -> exceptions copied
 // verbatim (pipeline.py:423-426).  The output histogram is written once.
+// The corrected reconstruction is evaluated twice (once for the image's
+// maximum, once for the apply) instead of being held in shared memory: no
+// shared memory per warp leaves L1 to the grid tables and W, and the
+// occupancy to the register file.
 #include "common.cuh"
 
 namespace {
@@ -19,7 +23,6 @@ k_decode(const MlkShard* __restrict__ shards, int n_shards, int total, MlkGrid g
          const unsigned char* __restrict__ res_mode, const double* __restrict__ lamq,
          const int* __restrict__ exc_slot, const double* __restrict__ exc_img, double floor_,
          double* __restrict__ out) {
-    extern __shared__ double smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int img = blockIdx.x * DW + warp;
     if (img >= total) return;
@@ -33,10 +36,11 @@ k_decode(const MlkShard* __restrict__ shards, int n_shards, int total, MlkGrid g
         for (int j = lane; j < D; j += 32) y[j] = src[j];
         return;
     }
-    double* cbuf = smem + warp * D;
     double z[MLK_MAXL];
-    for (int k = 0; k < L; ++k)
-        z[k] = (double)cents[((long long)s * L + k) * K + codes[(long long)img * L + k]];
+#pragma unroll
+    for (int k = 0; k < MLK_MAXL; ++k)  // unrolled + guarded: z stays in registers
+        z[k] = k < L ? (double)cents[((long long)s * L + k) * K + codes[(long long)img * L + k]]
+                     : 0.0;
     const float* Ws = W + sh.w_off;
     const bool blas_tree = !sh.small_blas;
     const int rs = res_slot[img];
@@ -45,12 +49,12 @@ k_decode(const MlkShard* __restrict__ shards, int n_shards, int total, MlkGrid g
     const double reb2 = rs >= 0 ? 2.0 * res_eb[rs] : 0.0;
     const double* lq = lamq + (long long)img * 8;
     const double l0 = lq[0], l1 = lq[1], l2 = lq[2], l3 = lq[3], u = lq[5];
-    double top = -INFINITY, amax = 0.0;
-    for (int j = lane; j < D; j += 32) {
+    // recon + decoded residual of cell j (BuiltinCodec.decompress,
+    // residual.py:93-97: zigzag_unmap(q) * (2 eb), or the raw float64 bits in
+    // lossless mode)
+    auto cell = [&](int j) {
         double c = decode_cell(z, Ws, L, D, j, blas_tree && g.tree_cols[j], sh.mean, sh.std);
         if (rv) {
-            // BuiltinCodec.decompress (residual.py:93-97): zigzag_unmap(q) * (2 eb),
-            // or the raw float64 bits in lossless mode
             const unsigned long long zc = rv[j];
             double r;
             if (rlossless) {
@@ -61,8 +65,11 @@ k_decode(const MlkShard* __restrict__ shards, int n_shards, int total, MlkGrid g
             }
             c = __dadd_rn(c, r);
         }
-        cbuf[j] = c;
-        top = np_max2(top, c);
+        return c;
+    };
+    double top = -INFINITY, amax = 0.0;
+    for (int j = lane; j < D; j += 32) {
+        top = np_max2(top, cell(j));
         const double dv = __dsub_rn(g.vpar[j], u);
         amax = np_max2(amax, fabs(__dmul_rn(g.hmvol[j], __dmul_rn(dv, dv))));
     }
@@ -71,11 +78,10 @@ k_decode(const MlkShard* __restrict__ shards, int n_shards, int total, MlkGrid g
         top = np_max2(top, __shfl_xor_sync(0xffffffffu, top, o));
         amax = np_max2(amax, __shfl_xor_sync(0xffffffffu, amax, o));
     }
-    __syncwarp();
     const double sc = amax > 0 ? amax : 1.0;
     const double fl = __dmul_rn(floor_, top);
     for (int j = lane; j < D; j += 32) {
-        const double c = cbuf[j];
+        const double c = cell(j);
         if (!(top > 0)) {
             y[j] = c;
             continue;
@@ -101,9 +107,7 @@ extern "C" int mlk_decode(const MlkShard* shards, int32_t n_shards, int32_t tota
                           const double* exc_img, double floor_, double* out,
                           cudaStream_t stream) {
     if (total <= 0) return MLK_OK;
-    size_t sm = (size_t)DW * grid_h->D * sizeof(double);
-    cudaFuncSetAttribute(k_decode, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    k_decode<<<(total + DW - 1) / DW, 32 * DW, sm, stream>>>(shards, n_shards, total, *grid_h, W,
+    k_decode<<<(total + DW - 1) / DW, 32 * DW, 0, stream>>>(shards, n_shards, total, *grid_h, W,
                                                             L, cents, K, codes, res_slot,
                                                             reinterpret_cast<const unsigned long long*>(res_codes),
                                                             res_eb, res_mode, lamq, exc_slot,

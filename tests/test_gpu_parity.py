@@ -338,6 +338,86 @@ def test_split_flags_lists_match_numpy():
         assert np.array_equal(c_d[:total - n].cpu().numpy(), np.flatnonzero((fl & 4) == 0))
 
 
+def _varint_ref(buf, cnt):
+    """kernels.varint_decode's loop (_ckernels.pyx:174-211): (values, consumed)."""
+    pos, out = 0, []
+    for _ in range(cnt):
+        x, sh = 0, 0
+        while True:
+            if pos >= len(buf):
+                return out, -1
+            c = buf[pos]
+            pos += 1
+            x |= ((c & 0x7F) << sh) & 0xFFFFFFFFFFFFFFFF
+            if c < 0x80:
+                break
+            sh += 7
+            if sh > 63:
+                return out, -2
+        out.append(x)
+    return out, pos
+
+
+def test_varint_decode_matches_sequential_loop():
+    """mlk_varint_decode_batch (one warp per stream) against the sequential
+    decode: values, bytes consumed, truncation (-1) and > 64-bit (-2) errors,
+    trailing bytes, streams spanning many 32-byte steps."""
+    from paper_2212_10733_b200._lib import call
+    dev = torch.device("cuda", 0)
+    rng = np.random.default_rng(17)
+
+    def enc(v):
+        out = bytearray()
+        while True:
+            b = v & 0x7F
+            v >>= 7
+            if v:
+                out.append(b | 0x80)
+            else:
+                out.append(b)
+                return bytes(out)
+
+    streams, counts = [], []
+    for t in range(300):
+        n = int(rng.integers(0, 120))
+        vals = [int(x) >> int(b) for x, b in zip(rng.integers(0, 2**63, n, dtype=np.uint64),
+                                                  rng.integers(0, 63, n))]
+        raw = b"".join(enc(v) for v in vals)
+        kind = t % 6
+        cnt = n
+        if kind == 1 and raw:                 # truncated
+            raw = raw[:int(rng.integers(0, len(raw)))]
+        elif kind == 2:                       # an over-long value
+            at = int(rng.integers(0, len(raw) + 1))
+            raw = raw[:at] + bytes([0x80 | int(rng.integers(0, 128))] * int(rng.integers(10, 14))) + \
+                b"\x01" + raw[at:]
+            cnt = n + 1
+        elif kind == 3:                       # trailing bytes beyond count
+            cnt = max(0, n - int(rng.integers(0, 4)))
+        elif kind == 4:                       # dangling continuation bytes at the end
+            raw = raw + bytes([0x81] * int(rng.integers(1, 13)))
+            cnt = n + 1
+        streams.append(raw)
+        counts.append(cnt)
+    off = np.concatenate([[0], np.cumsum([len(r) for r in streams])[:-1]]).astype(np.int64)
+    voff = np.concatenate([[0], np.cumsum(counts)[:-1]]).astype(np.int64)
+    blob = b"".join(streams) + b"\0"
+    i64 = dict(dtype=torch.int64, device=dev)
+    src = torch.frombuffer(bytearray(blob), dtype=torch.uint8).to(dev)
+    vals = torch.zeros(max(1, sum(counts)), **i64)
+    used = torch.zeros(len(streams), **i64)
+    call("mlk_varint_decode_batch", src, torch.tensor(off, **i64),
+         torch.tensor([len(r) for r in streams], **i64), len(streams),
+         torch.tensor(counts, **i64), vals, torch.tensor(voff, **i64), used)
+    got_v = vals.cpu().numpy().view(np.uint64)
+    got_u = used.cpu().numpy()
+    for i, (raw, cnt) in enumerate(zip(streams, counts)):
+        want, cons = _varint_ref(raw, cnt)
+        assert got_u[i] == cons, (i, got_u[i], cons)
+        if cons >= 0:
+            assert [int(x) for x in got_v[voff[i]:voff[i] + cnt]] == want, i
+
+
 def test_device_zlib_matches_host_zlib():
     import zlib
 

@@ -29,6 +29,8 @@ KEYS = {
     "dram_read_bytes": "dram__bytes_read.sum",
     "dram_write_bytes": "dram__bytes_write.sum",
     "dram_pct_peak": "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
+    "fp64_pipe_pct": "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+    "l2_hit_pct": "lts__t_sector_hit_rate.pct",
 }
 
 
