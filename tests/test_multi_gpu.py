@@ -79,6 +79,8 @@ def test_distributed_archive_is_the_single_process_archive(n, tmp_path):
         rel = float(np.max(np.abs(dec[p, q] - single[p, q]) / np.maximum(np.abs(single[p, q]),
                                                                            1e-300)))
     assert len(bad) == 0, (len(bad), bad[:8].tolist(), rel)
+    planes = np.fromfile(str(out) + ".planes.f64", dtype="<f8").reshape(single.shape)
+    assert np.array_equal(planes, dec)  # decompress_distributed(out_path=...)
 
 
 def test_distributed_training_gives_the_single_process_models(tmp_path):
