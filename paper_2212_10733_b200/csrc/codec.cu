@@ -978,8 +978,26 @@ k_deflate_warp(const uint8_t* __restrict__ in, const long long* __restrict__ in_
                     int len = valid ? wz::match_len_first(win, strstart, c, thr, s0, s1) : 0;
                     const unsigned hit = __ballot_sync(FULL, valid && len >= thr);
                     const int upto = hit ? __ffs(hit) - 1 : 31;
-                    if (hit && lane == upto)
-                        len = wz::match_len_upto(win, strstart, c, len, z6::MAX_MATCH);
+                    if (hit) {
+                        // the exact length of the candidate that ends the search,
+                        // by the whole warp: lane l compares bytes k + 8 l .. + 8
+                        // (k = its matched prefix), all 258 in one step
+                        const int cw = __shfl_sync(FULL, c, upto);
+                        const int k = __shfl_sync(FULL, len, upto);
+                        const int o = k + 8 * lane;
+                        const unsigned long long x =
+                            o < z6::MAX_MATCH
+                                ? wz::load8(win, strstart + o) ^ wz::load8(win, cw + o) : 0ull;
+                        const unsigned miss = __ballot_sync(FULL, x != 0ull);
+                        int ex = z6::MAX_MATCH;
+                        if (miss) {
+                            const int f = __ffs(miss) - 1;
+                            const unsigned long long xf = __shfl_sync(FULL, x, f);
+                            const int m = k + 8 * f + ((__ffsll((long long)xf) - 1) >> 3);
+                            ex = m < z6::MAX_MATCH ? m : z6::MAX_MATCH;
+                        }
+                        if (lane == upto) len = ex;
+                    }
                     __syncwarp();
                     const int mx = (int)__reduce_max_sync(FULL, lane <= upto ? (unsigned)len : 0u);
                     if (mx > best) {
