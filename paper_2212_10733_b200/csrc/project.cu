@@ -365,10 +365,8 @@ __device__ void newton_block(const double* fp, double fl, const MlkGrid& g, cons
                 const double w_in = cls_val(X.w, false, ce), w_ed = cls_val(X.w, true, ce);
                 const double* ebp = C.eb[ce];
                 double G1 = 0.0, G2 = 0.0, H1 = 0.0, H2 = 0.0, H3 = 0.0;
-                for (int r = g0; r < rows; r += ngrp) {
-                    const bool re = (r == 0) | (r == rows - 1);
-                    const double w = re ? w_ed : w_in;
-                    const double wf = w * (fmax(fp[r * cols + c], fl) * (re ? ea1 : ea0) * ebp[r]);
+                auto row = [&](int r, double w, double ea) {
+                    const double wf = w * (fmax(fp[r * cols + c], fl) * ea * ebp[r]);
                     const double p2 = C.p2r[r];
                     const double w2f = w * wf, t2 = p2 * w2f;
                     G1 += wf;
@@ -376,7 +374,17 @@ __device__ void newton_block(const double* fp, double fl, const MlkGrid& g, cons
                     H1 += w2f;
                     H2 += t2;
                     H3 = fma(p2, t2, H3);
+                };
+                // rows g0, g0 + ngrp, ... in order; the two edge rows (the
+                // only ones with the edge weight / exponent) peeled off the
+                // loop so its body has no selects
+                int r = g0;
+                if (r == 0) {
+                    row(0, w_ed, ea1);
+                    r += ngrp;
                 }
+                for (; r < rows - 1; r += ngrp) row(r, w_in, ea0);
+                if (r == rows - 1) row(r, w_ed, ea1);
                 const double q0 = X.is0, q1 = C.vp1[c], q3 = C.p3c[c];
                 v[0] = q0 * G1; v[1] = q1 * G1; v[2] = G2; v[3] = q3 * G1;
                 v[4] = q0 * q0 * H1; v[5] = q0 * q1 * H1; v[6] = q0 * H2; v[7] = q0 * q3 * H1;
