@@ -324,6 +324,55 @@ def _traffic(kernel, launches_per_step):
     return sum(k.get("dram_read_bytes", 0) + k.get("dram_write_bytes", 0) for k in ks)
 
 
+def _pcie_h2d_gbs(dev, nbytes=1 << 30):
+    """This rank's pinned host -> device copy bandwidth (CUDA events, best of
+    3): the floor of the e2e step's upload."""
+    import torch
+    host = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    buf = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    buf.copy_(host, non_blocking=True)
+    best = None
+    for _ in range(3):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        buf.copy_(host, non_blocking=True)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        best = ms if best is None else min(best, ms)
+    del host, buf
+    return nbytes / (best / 1e3) / 1e9
+
+
+def _fp64_block(stage_ms, out):
+    """k_project against the FP64 roofline: FP64 flops per
+    histogram from the committed ncu capture ((DADD + DMUL + 2 DFMA) thread
+    instructions of the residual-free launch, profiles/r2_kernels.json) x the
+    images of a launch / that launch's in-situ duration (CUDA events on its
+    own stream), against the DFMA peak measured on the box."""
+    kpath, ppath = ROOT / "profiles" / "r2_kernels.json", ROOT / "profiles" / "r2_fp64_peak.json"
+    if not kpath.exists() or not ppath.exists():
+        return None
+    ks = [k for k in json.loads(kpath.read_text())
+          if k["kernel"].startswith("k_project") and k.get("fp64_flops")]
+    if not ks:
+        return None
+    per_img = ks[0]["fp64_flops"] / ks[0]["grid"]
+    peak = json.loads(ppath.read_text())["fp64_dfma_tflops"]
+    n_sel = int(np.sum(out.sel_count))
+    total = int(sum(s.n_img for s in out.specs)) if hasattr(out, "specs") else None
+    blk = {"kernel": "k_project", "unit": "TFLOP/s", "peak": peak,
+           "peak_source": "profiles/r2_fp64_peak.json (measured DFMA chains)",
+           "flops_per_histogram": per_img}
+    for name, n_img in (("project_sel_launch", n_sel),
+                        ("project_non_launch", None if total is None else total - n_sel)):
+        ms = stage_ms.get(name)
+        if ms and n_img:
+            ach = per_img * n_img / (ms / 1e3) / 1e12
+            blk[name] = {"images": n_img, "ms": ms, "achieved": ach, "frac": ach / peak}
+    return blk
+
+
 def rooflines(out, stage_ms, n, dev, traffic_ok=True):
     """Per-kernel achieved GB/s = algorithmic bytes per step / stage time.
     traffic_ok: the committed capture (config 3, 1 GPU) describes this run."""
@@ -365,7 +414,8 @@ def rooflines(out, stage_ms, n, dev, traffic_ok=True):
                 "peak": peak, "unit": "GB/s", "frac": dom["frac"], "traffic": dom["traffic"],
                 "algorithmic_bytes_per_step": dom["algorithmic_bytes_per_step"],
                 "ms_per_step": dom["ms_per_step"], "peak_source": src,
-                "note": dom["note"] + "; per-kernel table in 'kernels'"}
+                "note": dom["note"] + "; per-kernel table in 'kernels'",
+                "fp64": _fp64_block(stage_ms, out)}
     return roofline, table
 
 
@@ -508,6 +558,12 @@ def main():
                "note": ("the archive's exception entries (the input's own histograms) are "
                         "written from the host f0; the rest of the archive is copied back")
                if world == 1 else None}
+        bw = _pcie_h2d_gbs(dev)
+        floor_ms = e2e["h2d_bytes_per_step"] / world / (bw * 1e9) * 1e3
+        e2e["pcie"] = {"h2d_gbs_measured": bw, "h2d_floor_ms": floor_ms,
+                       "floor_frac_of_step": floor_ms / (e2e_s * 1e3),
+                       "note": "this rank's pinned H2D bandwidth (1 GiB, best of 3); the "
+                               "upload of its f0 slab alone at that rate"}
         dec = decompress_measure(res[0] if world == 1 else Path(shm).read_bytes(), world,
                                  total_hist, dev)
         dec = dict(dec or {}, max_per_image_nrmse=rep.max_per_image_nrmse() if world == 1

@@ -294,6 +294,24 @@ class Timer:
         self.sync = os.environ.get("MLK_TIMING") == "sync"
         self.marks = []
         self.points = []
+        self.spans = []
+
+    def span_start(self, stream):
+        """An event on `stream` opening a span (span_end closes it)."""
+        if not self.enabled or self.sync:
+            return None
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record(stream)
+        return ev
+
+    def span_end(self, name, stream, ev0):
+        """Report the time between ev0 and now on `stream` as `name` (one
+        launch's in-situ duration on its own stream)."""
+        if ev0 is None:
+            return
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record(stream)
+        self.spans.append((name, ev0, ev))
 
     def point(self, name, stream, since):
         """An event on `stream`, reported as ms after the mark `since`
@@ -328,6 +346,8 @@ class Timer:
         for name, ev, since in self.points:
             if since in base and not self.sync:
                 out[name] = out.get(name, 0.0) + base[since].elapsed_time(ev) / 1e3
+        for name, ev0, ev1 in self.spans:
+            out[name] = out.get(name, 0.0) + ev0.elapsed_time(ev1) / 1e3
         return out
 
 
@@ -652,9 +672,11 @@ def compress_device(f0: torch.Tensor, specs, dgrid: DeviceGrid, cfg, timer: Time
         ev_split = torch.cuda.Event()
         ev_split.record(main)
         side.wait_event(ev_split)
+    sp_non = timer.span_start(side)
     call("mlk_project", f0, stats, qoi, sh_d, S, total, dgrid.addr, W, L, cents, K, codes,
          sel_rank, None, ctypes.addressof(opts), flags, lam, qst, status, iters, ferr, fqoi,
          fsse, varint, vcap, vlen, errf, list_non, total - n_sel, stream=side.cuda_stream)
+    timer.span_end("project_non_launch", side, sp_non)
     ev_non = torch.cuda.Event()
     ev_non.record(side)
 
@@ -745,9 +767,11 @@ def compress_device(f0: torch.Tensor, specs, dgrid: DeviceGrid, cfg, timer: Time
     if n_sel:
         # the residual images feed DEFLATE (the critical path): still on the
         # high-priority stream, ahead of the side stream's remaining CTAs
+        sp_sel = timer.span_start(torch.cuda.current_stream(dev))
         call("mlk_project", f0, stats, qoi, sh_d, S, total, dgrid.addr, W, L, cents, K, codes,
              sel_rank, slot_base, ctypes.addressof(opts), flags, lam, qst, status, iters, ferr,
              fqoi, fsse, varint, vcap, vlen, errf, list_sel, n_sel)
+        timer.span_end("project_sel_launch", torch.cuda.current_stream(dev), sp_sel)
     if hi_ctx is not None:
         hi_ctx.__exit__(None, None, None)
         main.wait_stream(hi)

@@ -56,6 +56,15 @@ def kernels(rep: Path):
                 k[name] = _num(d[m])
         if "duration_ms" in k and isinstance(k["duration_ms"], float):
             k["duration_ms"] /= 1e6  # base unit ns
+        # FP64 flops of the launch: (DADD + DMUL + 2 DFMA) thread instructions,
+        # from --set full's per-cycle rates x the elapsed SM cycles
+        try:
+            rate = sum(f * _num(d[f"smsp__sass_thread_inst_executed_op_{op}_pred_on"
+                                  ".sum.per_cycle_elapsed"])
+                       for op, f in (("dadd", 1), ("dmul", 1), ("dfma", 2)))
+            k["fp64_flops"] = rate * _num(d["sm__cycles_elapsed.avg"])
+        except (KeyError, TypeError):
+            pass
         stalls = {key.replace("smsp__average_warps_issue_stalled_", "")
                   .replace("_per_issue_active.ratio", ""): _num(v)
                   for key, v in d.items()
