@@ -497,6 +497,19 @@ __device__ __forceinline__ void hdown(uint32_t* hk, int heap_len, int k) {
     hk[k] = v;
 }
 
+// The warp kernels' dynamic shared memory and the static code tables, at
+// namespace scope so the out-of-line tree functions below address them as
+// shared memory (LDS/STS) rather than through generic pointers
+extern __shared__ __align__(16) uint8_t zsm[];
+__shared__ z6::Tables s_tb;
+
+// a generic pointer into the dynamic shared memory, re-derived from its base
+// (the compiler then knows the address space)
+template <class T>
+__device__ __forceinline__ T* shp(T* p) {
+    return reinterpret_cast<T*>(zsm + (reinterpret_cast<const uint8_t*>(p) - zsm));
+}
+
 // kind: 0 literal/length, 1 distance, 2 bit-length tree.  Whole warp.
 // A view of one DTree<NL> so the tree code exists once in the binary (three
 // template copies made the flush kernel too large for the instruction cache)
@@ -512,9 +525,14 @@ template <int NL>
 __device__ __forceinline__ TreeRef tref(DTree<NL>& t) {
     return TreeRef{t.freq, t.code, t.len, t.dad, &t.max_code, NL};
 }
+__device__ __forceinline__ TreeRef shared_ref(const TreeRef& t) {
+    return TreeRef{shp(t.freq), shp(t.code), shp(t.len), shp(t.dad), shp(t.max_code_p), t.NL};
+}
 
-__device__ __noinline__ void build_tree_warp(DTrees& W, TreeRef t, int kind,
-                                             const z6::Tables& tb) {
+__device__ __noinline__ void build_tree_warp(DTrees& W0, TreeRef t0, int kind) {
+    DTrees& W = *shp(&W0);
+    const TreeRef t = shared_ref(t0);
+    const z6::Tables& tb = s_tb;
     const int NL = t.NL;
     const unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31;
@@ -651,7 +669,9 @@ __device__ __noinline__ void build_tree_warp(DTrees& W, TreeRef t, int kind,
 }
 
 // trees.c scan_tree / send_tree over a DTree (lane 0)
-__device__ __noinline__ void scan_tree_d(DTrees& W, TreeRef t) {
+__device__ __noinline__ void scan_tree_d(DTrees& W0, TreeRef t0) {
+    DTrees& W = *shp(&W0);
+    const TreeRef t = shared_ref(t0);
     const int max_code = *t.max_code_p;
     int prevlen = -1, curlen, nextlen = t.len[0], count = 0, max_count = 7, min_count = 4;
     if (nextlen == 0) max_count = 138, min_count = 3;
@@ -771,8 +791,8 @@ k_deflate_warp(const uint8_t* __restrict__ in, const long long* __restrict__ in_
                long long* __restrict__ out_len, int nmin, int nmax,
                uint8_t* __restrict__ sym_g, long long sym_cap,
                unsigned long long* __restrict__ prof, int* __restrict__ counter) {
-    __shared__ z6::Tables tb;
-    extern __shared__ __align__(16) uint8_t zsm[];
+    z6::Tables& tb = wz::s_tb;
+    uint8_t* const zsm = wz::zsm;
     load_tables(tb);
     __syncthreads();
     const wz::Lay Ly = wz::layout(nmax);
@@ -1099,22 +1119,24 @@ k_deflate_warp(const uint8_t* __restrict__ in, const long long* __restrict__ in_
         for (int i = lane; i < z6::BL_CODES; i += 32) t.bt.freq[i] = 0;
         if (lane == 0) t.opt_len = t.static_len = 0;
         __syncwarp();
-        wz::build_tree_warp(t, wz::tref(t.lt), 0, tb);
-        wz::build_tree_warp(t, wz::tref(t.dt), 1, tb);
+        wz::build_tree_warp(t, wz::tref(t.lt), 0);
+        wz::build_tree_warp(t, wz::tref(t.dt), 1);
         if (lane == 0) {
             wz::scan_tree_d(t, wz::tref(t.lt));
             wz::scan_tree_d(t, wz::tref(t.dt));
         }
         __syncwarp();
-        wz::build_tree_warp(t, wz::tref(t.bt), 2, tb);
+        wz::build_tree_warp(t, wz::tref(t.bt), 2);
         // ---- output: zero the stream's bytes (it is at most n + 11 long),
         //      then OR the bit stream into them
         uint8_t* dst = out + out_off[s];
         const long long zlim = (long long)n + 16 < out_cap ? (long long)n + 16 : out_cap;
         for (long long i = lane; i < zlim; i += 32) dst[i] = 0;
         __syncwarp();
+        // (pointer arithmetic on dst, not an integer round trip: the atomics
+        // below stay global-space instructions)
         unsigned long long* gw =
-            reinterpret_cast<unsigned long long*>(reinterpret_cast<uintptr_t>(dst) & ~(uintptr_t)7);
+            reinterpret_cast<unsigned long long*>(dst - (reinterpret_cast<uintptr_t>(dst) & 7));
         const long long bit0 = (long long)(reinterpret_cast<uintptr_t>(dst) & 7) * 8;
         if (lane == 0) {
             int max_blindex;
