@@ -898,15 +898,24 @@ def blob_layout(specs, cfg, D, cnt_h, zlen_h, exc_h, ranks=None):
     L, bits, K = cfg.latent_dim, cfg.pq_bits, 2 ** cfg.pq_bits
     lb = 4 if cfg.lambda_precision == "f32" else 8
     S = len(specs)
-    zl_sum = np.array([int(np.sum(21 + zlen_h[a:a + c])) for a, c in
-                       zip(np.concatenate([[0], np.cumsum(cnt_h)[:-1]]).astype(np.int64), cnt_h)],
-                      dtype=np.int64)
+    cnt = np.asarray(cnt_h, dtype=np.int64)
+    e_start = np.concatenate([[0], np.cumsum(cnt)[:-1]]).astype(np.int64)
+    # entry bytes (21-byte entry header + zlib body), prefix-summed once
+    zcs = np.concatenate([[0], np.cumsum(21 + np.asarray(zlen_h, dtype=np.int64))])
+    zl_sum = zcs[e_start + cnt] - zcs[e_start]
     if ranks is None:
         ranks = dict(rank=0, n=np.array([[sp.n_img for sp in specs]], dtype=np.int64),
-                     cnt=np.asarray(cnt_h, np.int64)[None], res=zl_sum[None],
-                     exc=np.asarray(exc_h, np.int64)[None])
+                     cnt=cnt[None], res=zl_sum[None], exc=np.asarray(exc_h, np.int64)[None])
     r = ranks["rank"]
     n_all, res_all, exc_all = ranks["n"], ranks["res"], ranks["exc"]
+    # per-shard totals over every rank and the parts of the ranks before r
+    n_tot, n_pre, n_own = (n_all.sum(0).tolist(), n_all[:r].sum(0).tolist(),
+                           n_all[r].tolist())
+    res_tot, res_pre, res_own = (res_all.sum(0).tolist(), res_all[:r].sum(0).tolist(),
+                                 res_all[r].tolist())
+    exc_tot, exc_pre, exc_own = (exc_all.sum(0).tolist(), exc_all[:r].sum(0).tolist(),
+                                 exc_all[r].tolist())
+    cnt_l, e_start_l = cnt.tolist(), e_start.tolist()
     keys = ("blob_off", "blob_len", "hdr_off", "codes_off", "pq_off", "res_pre_off", "lam_off",
             "exc_pre_off", "exc_base", "exc_total")
     lay = {k: np.full(S, -1, dtype=np.int64) for k in keys}
@@ -927,14 +936,15 @@ def blob_layout(specs, cfg, D, cnt_h, zlen_h, exc_h, ranks=None):
         cur[0] += n
         return o
 
-    gpos, e0 = 0, 0
+    gpos = 0
+    rec = 4 + 8 * D
     for s, sp in enumerate(specs):
-        n = int(n_all[:, s].sum())
-        a = int(n_all[:r, s].sum())          # first member of this rank's range
-        m = int(n_all[r, s])
-        n_exc = int(exc_all[:, s].sum())
-        sec = [16 + 4 * L * D, (n * L * bits + 7) // 8, 4 * L * K,
-               12 + int(res_all[:, s].sum()), n * 8 * lb, 4 + n_exc * (4 + 8 * D)]
+        n = n_tot[s]
+        a = n_pre[s]          # first member of this rank's range
+        m = n_own[s]
+        n_exc = exc_tot[s]
+        sec = (16 + 4 * L * D, (n * L * bits + 7) // 8, 4 * L * K, 12 + res_tot[s], n * 8 * lb,
+               4 + n_exc * rec)
         g_codes = gpos + 44 + sec[0]
         g_pq = g_codes + sec[1]
         g_res = g_pq + sec[2]
@@ -949,26 +959,23 @@ def blob_layout(specs, cfg, D, cnt_h, zlen_h, exc_h, ranks=None):
         if own0:
             lay["pq_off"][s] = put(g_pq, sec[2])
             lay["res_pre_off"][s] = put(g_res, 12)
-        ent = put(g_res + 12 + int(res_all[:r, s].sum()), int(res_all[r, s]))
-        c = int(cnt_h[s])
+        ent = put(g_res + 12 + res_pre[s], res_own[s])
+        c, e0 = cnt_l[s], e_start_l[s]
         if c:
-            zl = zlen_h[e0:e0 + c]
-            entry_off[e0:e0 + c] = ent + np.concatenate([[0], np.cumsum(21 + zl)[:-1]])
+            entry_off[e0:e0 + c] = ent + (zcs[e0:e0 + c] - zcs[e0])
         lay["lam_off"][s] = put(g_lam + a * 8 * lb, m * 8 * lb)
         if own0:
             lay["exc_pre_off"][s] = put(g_exc, 4)
-        lay["exc_base"][s] = put(g_exc + 4 + int(exc_all[:r, s].sum()) * (4 + 8 * D),
-                                 int(exc_all[r, s]) * (4 + 8 * D)) - 4
+        lay["exc_base"][s] = put(g_exc + 4 + exc_pre[s] * rec, exc_own[s] * rec) - 4
         lay["exc_total"][s] = n_exc
         lay["blob_off"][s] = gpos
-        lay["blob_len"][s] = 44 + sum(sec)
+        blen = 44 + sum(sec)
+        lay["blob_len"][s] = blen
         lay["header"].append(ShardHeader(scheme=SCHEME_FULL, lambda_precision=lb,
-                                         section_lengths=tuple(int(x) for x in sec),
-                                         n_images=n, img_rows=specs[s].rows,
-                                         img_cols=specs[s].cols, latent_dim=L,
-                                         pq_bits=bits).pack())
-        gpos += int(lay["blob_len"][s])
-        e0 += c
+                                         section_lengths=sec, n_images=n,
+                                         img_rows=specs[s].rows, img_cols=specs[s].cols,
+                                         latent_dim=L, pq_bits=bits).pack())
+        gpos += blen
     lay["entry_off"] = entry_off
     lay["total"] = cur[0]
     lay["segments"] = [tuple(x) for x in segs]
