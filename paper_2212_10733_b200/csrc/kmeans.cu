@@ -20,6 +20,8 @@
 // Lloyd, next to both label arrays (SM = true); the values (seeding) and the
 // cluster-sorted copy (Lloyd) stay in L2-resident global scratch.  Larger
 // shards keep everything in the scratch.
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 
 // phase clocks of the last launch's CTA 0: load + distinct test, seeding,
@@ -27,6 +29,12 @@
 __device__ long long g_km_prof[12];
 
 namespace {
+
+// MLK_KMEANS_CLUSTER=0 keeps one CTA per (shard, dim) (A/B measurements)
+const bool KM_CLUSTER = [] {
+    const char* e = getenv("MLK_KMEANS_CLUSTER");
+    return !(e && e[0] == '0');
+}();
 
 constexpr int KT = 1024;           // threads per CTA
 constexpr int KW = KT / 32;        // warps
@@ -602,6 +610,431 @@ k_kmeans(const double* __restrict__ lat, const MlkShard* __restrict__ shards, in
     }
 }
 
+// ---------------------------------------------------------------------------
+// The same k-means on a 4-CTA thread-block cluster per (shard, dim) (shards
+// of >= 4096 members that fit): CTA q owns the members of the q-th depth-2
+// subtree of numpy's pairwise recursion over the shard, so its pairwise d2
+// sum is an exact subtree sum and the shard's is ((s0 + s1) + (s2 + s3)).
+// The members, d2 and both label arrays live in the CTA's shared memory;
+// every cross-CTA quantity (subtree sums, scan offsets, the choice counts,
+// label counts, cluster means, dead-cluster argmax, convergence) is
+// published in a small per-CTA block and read by the peers through
+// distributed shared memory between cluster barriers.  Same operations in
+// the same order as k_kmeans: the codebooks are bit-identical.
+constexpr int KC = 4;  // CTAs per cluster
+
+__device__ __forceinline__ void kc_range(int n, int q, int& lo, int& hi) {
+    const int l = pw_split(n);
+    const int a = q < 2 ? 0 : l, m = q < 2 ? l : n - l;
+    const int h = pw_split(m);
+    lo = (q & 1) ? a + h : a;
+    hi = (q & 1) ? a + m : a + h;
+}
+
+struct KcPub {  // per-CTA values the peers read
+    double dsum, loc_tot, vmin, amax_v;
+    long long ab;
+    int amax_i, changed, many, fb_idx;
+    int cnt[MLK_MAXK];
+    double msum[MLK_MAXK];
+};
+
+__global__ void __launch_bounds__(KT, 1)
+k_kmeans_cl(const double* __restrict__ lat, const MlkShard* __restrict__ shards, int L, int K,
+            const long long* __restrict__ first_idx, const double* __restrict__ draws,
+            double* __restrict__ scratch, float* __restrict__ cents, double* __restrict__ cents64,
+            int* __restrict__ info, int slots, int m_cap) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cl = cg::this_cluster();
+    const int q = (int)cl.block_rank();
+    __shared__ KmSmem S;
+    __shared__ KcPub P;
+    extern __shared__ double dyn[];
+    double* val = dyn;
+    int* wcnt = reinterpret_cast<int*>(dyn + slots);   // [KW][K]
+    unsigned char* kind = reinterpret_cast<unsigned char*>(wcnt + KW * K);
+    double* v = dyn + ((slots * 9 + KW * K * 4 + 15) / 16) * 2;
+    double* d2 = v + m_cap;
+    unsigned short* lab = reinterpret_cast<unsigned short*>(d2 + m_cap);
+    unsigned short* lab2 = lab + m_cap;
+
+    const int job = blockIdx.x / KC;
+    const int s = job / L, dim = job % L;
+    const MlkShard sh = shards[s];
+    const int n = sh.n_img;
+    int lo, hi;
+    kc_range(n, q, lo, hi);
+    const int m = hi - lo;
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    double* srt = scratch + (long long)4 * L * sh.img_off + (long long)4 * dim * n + 2 * n;
+    float* out = cents + ((long long)s * L + dim) * K;
+    double* out64 = cents64 ? cents64 + ((long long)s * L + dim) * K : nullptr;
+    int* inf = info + (s * L + dim) * 4;
+    KcPub* peer[KC];
+    double* pv[KC];
+    double* pd2[KC];
+    int plo[KC];
+#pragma unroll
+    for (int r = 0; r < KC; ++r) {
+        peer[r] = cl.map_shared_rank(&P, r);
+        pv[r] = cl.map_shared_rank(v, r);
+        pd2[r] = cl.map_shared_rank(d2, r);
+        int a, b;
+        kc_range(n, r, a, b);
+        plo[r] = a;
+    }
+    auto owner = [&](int j) {  // CTA holding shard member j
+        int r = 0;
+#pragma unroll
+        for (int t = 1; t < KC; ++t)
+            if (j >= plo[t]) r = t;
+        return r;
+    };
+    const long long kp_t0 = clock64();
+    for (int j = tid; j < m; j += KT) v[j] = lat[(long long)(sh.img_off + lo + j) * L + dim];
+    __syncthreads();
+
+    // ---- distinct shortcut (np.unique; quantizer.py:62-65): some CTA seeing
+    //      K + 1 distinct non-NaN values among its first 64 members settles
+    //      it; otherwise the exact successive-minimum walk, cluster-wide
+    if (w == 0) {
+        const double a = lane < m ? v[lane] : __longlong_as_double(0x7ff8000000000000ll);
+        const double b = lane + 32 < m ? v[lane + 32] : __longlong_as_double(0x7ff8000000000000ll);
+        bool fa = a == a, fb = b == b;
+        for (int k = 0; k < 32; ++k) {
+            const double xa = __shfl_sync(0xffffffffu, a, k), xb = __shfl_sync(0xffffffffu, b, k);
+            if (k < lane && xa == a) fa = false;
+            if (xa == b || (k < lane && xb == b)) fb = false;
+        }
+        const int nd = __popc(__ballot_sync(0xffffffffu, fa)) + __popc(__ballot_sync(0xffffffffu, fb));
+        if (lane == 0) P.many = nd >= K + 1;
+    }
+    cl.sync();
+    bool many = false;
+#pragma unroll
+    for (int r = 0; r < KC; ++r) many |= peer[r]->many != 0;
+    if (!many) {
+        double cur = INFINITY;
+        for (int j = tid; j < m; j += KT) cur = fmin(cur, v[j]);
+        cur = block_min(cur, S);
+        if (tid == 0) P.vmin = cur;
+        cl.sync();
+        cur = INFINITY;
+#pragma unroll
+        for (int r = 0; r < KC; ++r) cur = fmin(cur, peer[r]->vmin);
+        cl.sync();
+        int cnt = 1;
+        if (tid == 0) S.distinct[0] = cur;
+        while (cnt <= K) {
+            double nx = INFINITY;
+            for (int j = tid; j < m; j += KT)
+                if (v[j] > cur) nx = fmin(nx, v[j]);
+            nx = block_min(nx, S);
+            if (tid == 0) P.vmin = nx;
+            cl.sync();
+            nx = INFINITY;
+#pragma unroll
+            for (int r = 0; r < KC; ++r) nx = fmin(nx, peer[r]->vmin);
+            cl.sync();
+            if (nx == INFINITY) break;
+            if (tid == 0) S.distinct[cnt] = nx;
+            cur = nx;
+            ++cnt;
+        }
+        __syncthreads();
+        if (cnt <= K) {
+            if (q == 0) {
+                if (tid < K) {
+                    const double c = S.distinct[tid < cnt ? tid : cnt - 1];
+                    out[tid] = (float)c;
+                    if (out64) out64[tid] = c;
+                }
+                if (tid == 0) { inf[0] = 0; inf[1] = cnt; inf[2] = 0; inf[3] = 0; }
+            }
+            return;  // no peer reads this CTA's shared memory any more
+        }
+    }
+
+    const long long kp_t1 = clock64();
+    // ---- k-means++ seeding (quantizer.py:66-76)
+    if (tid == 0) {
+        S.one_start = 0;
+        S.one_len = m;
+        const long long f = first_idx[s * L + dim];
+        const int o = owner((int)f);
+        S.cent[0] = pv[o][f - plo[o]];
+    }
+    __syncthreads();
+    {
+        const double c0 = S.cent[0];
+        for (int j = tid; j < m; j += KT) {
+            const double t = __dsub_rn(v[j], c0);
+            d2[j] = __dmul_rn(t, t);
+        }
+    }
+    __syncthreads();
+    int fallbacks = 0;
+    const int chunk = (m + KT - 1) / KT;
+    const int j_lo = min(m, tid * chunk), j_hi = min(m, j_lo + chunk);
+    const double delta = (16.0 * (n + 8)) * 1.1102230246251565e-16;
+    const double* u_draw = draws + (long long)(s * L + dim) * (K - 1);
+    for (int i = 1; i < K; ++i) {
+        block_pw_sums(d2, &S.one_start, &S.one_len, 1, val, kind, S.seg_base, S.sums, S);
+        double loc = 0.0;
+        for (int j = j_lo; j < j_hi; ++j) loc += d2[j];
+        double ltot;
+        double run = block_exscan(loc, &ltot, S);
+        if (tid == 0) {
+            P.dsum = S.sums[0];
+            P.loc_tot = ltot;
+        }
+        cl.sync();
+        // the shard's pairwise sum: the top two levels over the subtrees
+        const double tot = __dadd_rn(__dadd_rn(peer[0]->dsum, peer[1]->dsum),
+                                     __dadd_rn(peer[2]->dsum, peer[3]->dsum));
+        if (tot <= 0) {
+            if (tid == 0)
+                for (int t = i; t < K; ++t) S.cent[t] = S.cent[0];
+            __syncthreads();
+            break;
+        }
+        double ctot = 0.0, off = 0.0;
+#pragma unroll
+        for (int r = 0; r < KC; ++r) {
+            if (r == q) off = ctot;
+            ctot += peer[r]->loc_tot;
+        }
+        run += off;
+        const double u = u_draw[i - 1];
+        const double thr_a = u * ctot * (1.0 - 2.0 * delta), thr_b = u * ctot * (1.0 + 2.0 * delta);
+        int a_cnt = 0, b_cnt = 0;
+        for (int j = j_lo; j < j_hi; ++j) {
+            run += d2[j];
+            if (run <= thr_a) ++a_cnt;        // cdf_j <= u for certain
+            else if (run > thr_b) ++b_cnt;    // cdf_j > u for certain
+        }
+        const long long ab = (long long)block_sum((double)a_cnt + 1048576.0 * b_cnt, S);
+        if (tid == 0) P.ab = ab;
+        cl.sync();
+        long long abt = 0;
+#pragma unroll
+        for (int r = 0; r < KC; ++r) abt += peer[r]->ab;
+        a_cnt = (int)(abt & 1048575ll);
+        b_cnt = (int)(abt >> 20);
+        const bool fb = a_cnt + b_cnt != n;
+        if (tid == 0) {
+            int idx = a_cnt;
+            if (fb) {  // exact sequential cumsum (numpy add.accumulate) over the shard -- rare
+                double c = 0.0;
+                for (int r = 0; r < KC; ++r) {
+                    const int len = (r + 1 < KC ? plo[r + 1] : n) - plo[r];
+                    for (int j = 0; j < len; ++j) c = __dadd_rn(c, __ddiv_rn(pd2[r][j], tot));
+                }
+                double run2 = 0.0;
+                idx = 0;
+                bool stop = false;
+                for (int r = 0; r < KC && !stop; ++r) {
+                    const int len = (r + 1 < KC ? plo[r + 1] : n) - plo[r];
+                    for (int j = 0; j < len; ++j) {
+                        run2 = __dadd_rn(run2, __ddiv_rn(pd2[r][j], tot));
+                        if (__ddiv_rn(run2, c) <= u) ++idx;
+                        else { stop = true; break; }
+                    }
+                }
+                ++fallbacks;
+            }
+            const int o = owner(idx);
+            S.cent[i] = pv[o][idx - plo[o]];
+        }
+        if (fb) cl.sync();  // every CTA has read the peers' d2 before it changes
+        __syncthreads();
+        const double ci = S.cent[i];
+        for (int j = tid; j < m; j += KT) {
+            const double t = __dsub_rn(v[j], ci);
+            const double qq = __dmul_rn(t, t);
+            d2[j] = d2[j] < qq ? d2[j] : qq;
+        }
+        __syncthreads();
+    }
+
+    const long long kp_t2 = clock64();
+    // ---- Lloyd (quantizer.py:78-90)
+    const int ktop = 1 << (31 - __clz(K));
+    sort_cents(S.cent, K, S);
+    for (int j = tid; j < m; j += KT)
+        lab[j] = (unsigned short)nearest_sorted(v[j], S.cs, S.ci, K, ktop);
+    __syncthreads();
+    int sweeps = 0;
+    const int wchunk = (m + KW - 1) / KW;
+    const int w_lo = min(m, w * wchunk), w_hi = min(m, w_lo + wchunk);
+    const unsigned lt = (1u << lane) - 1u;
+    for (int it = 0; it < 25; ++it) {
+        ++sweeps;
+        for (int t = tid; t < KW * K; t += KT) wcnt[t] = 0;
+        __syncthreads();
+        for (int j0 = w_lo; j0 < w_hi; j0 += 32) {
+            const int j = j0 + lane;
+            const unsigned key = j < w_hi ? lab[j] : 0xFFFFu;
+            const unsigned mm = __match_any_sync(0xffffffffu, key);
+            if (key != 0xFFFFu && (__ffs(mm) - 1) == lane) wcnt[w * K + key] += __popc(mm);
+            __syncwarp();
+        }
+        __syncthreads();
+        if (tid < K) {
+            int t = 0;
+            for (int r = 0; r < KW; ++r) t += wcnt[r * K + tid];
+            P.cnt[tid] = t;
+        }
+        cl.sync();
+        // cluster sizes, segment starts, and this CTA's place in each segment
+        if (tid < K) {
+            int tc = 0, before = 0;
+#pragma unroll
+            for (int r = 0; r < KC; ++r) {
+                const int c = peer[r]->cnt[tid];
+                if (r < q) before += c;
+                tc += c;
+            }
+            S.seg_cnt[tid] = tc;
+            S.seg_base[tid] = before;  // (scratch until the pairwise sums): lower CTAs' members
+        }
+        __syncthreads();
+        if (tid == 0) {
+            int acc = 0;
+            for (int k = 0; k < K; ++k) { S.seg_start[k] = acc; acc += S.seg_cnt[k]; }
+        }
+        __syncthreads();
+        if (tid < K) {
+            int acc = S.seg_start[tid] + S.seg_base[tid];
+            for (int r = 0; r < KW; ++r) {
+                const int c = wcnt[r * K + tid];
+                wcnt[r * K + tid] = acc;
+                acc += c;
+            }
+        }
+        __syncthreads();
+        for (int j0 = w_lo; j0 < w_hi; j0 += 32) {
+            const int j = j0 + lane;
+            const unsigned key = j < w_hi ? lab[j] : 0xFFFFu;
+            const unsigned mm = __match_any_sync(0xffffffffu, key);
+            const int basepos = key != 0xFFFFu ? wcnt[w * K + key] : 0;
+            __syncwarp();
+            if (key != 0xFFFFu) {
+                srt[basepos + __popc(mm & lt)] = v[j];
+                if ((__ffs(mm) - 1) == lane) wcnt[w * K + key] = basepos + __popc(mm);
+            }
+            __syncwarp();
+        }
+        cl.sync();  // srt complete (global memory, cluster scope)
+        // pairwise means of the clusters k = q, q + KC, ...
+        if (tid < K) S.oldc[tid] = S.cent[tid];
+        int nsub = 0;
+        if (tid == 0) {
+            for (int k = q; k < K; k += KC) {
+                S.seg_base[nsub] = k;  // (segment ids, copied below)
+                ++nsub;
+            }
+            S.bcast_i = nsub;
+        }
+        __syncthreads();
+        nsub = S.bcast_i;
+        __shared__ int sub_start[MLK_MAXK / KC + 1], sub_cnt[MLK_MAXK / KC + 1],
+            sub_id[MLK_MAXK / KC + 1];
+        if (tid < nsub) {
+            const int k = S.seg_base[tid];
+            sub_id[tid] = k;
+            sub_start[tid] = S.seg_start[k];
+            sub_cnt[tid] = S.seg_cnt[k];
+        }
+        __syncthreads();
+        block_pw_sums(srt, sub_start, sub_cnt, nsub, val, kind, S.seg_base, S.sums, S);
+        if (tid < nsub) P.msum[sub_id[tid]] = S.sums[tid];
+        cl.sync();
+        if (tid < K) {
+            const int c = S.seg_cnt[tid];
+            S.newc[tid] = c > 0 ? __ddiv_rn(peer[tid % KC]->msum[tid], (double)c) : S.oldc[tid];
+        }
+        __syncthreads();
+        // dead clusters, in index order, against the partially updated table
+        for (int k = 0; k < K; ++k) {
+            if (S.seg_cnt[k] != 0) continue;
+            double bv = -INFINITY;
+            int bi = 0x7fffffff;
+            for (int j = tid; j < m; j += KT) {
+                const int lj = lab[j];
+                const double cj = lj < k ? S.newc[lj] : S.oldc[lj];
+                const double dv = fabs(__dsub_rn(v[j], cj));
+                if (dv > bv || (dv == bv && lo + j < bi)) { bv = dv; bi = lo + j; }
+            }
+            const int far = block_argmax(bv, bi, S);
+            if (tid == 0) {
+                P.amax_i = far;
+                P.amax_v = far < 0x7fffffff ? fabs(__dsub_rn(v[far - lo],
+                    lab[far - lo] < k ? S.newc[lab[far - lo]] : S.oldc[lab[far - lo]])) : -INFINITY;
+            }
+            cl.sync();
+            if (tid == 0) {
+                double gv = -INFINITY;
+                int gi = 0x7fffffff;
+                for (int r = 0; r < KC; ++r) {
+                    const double pvv = peer[r]->amax_v;
+                    const int pi = peer[r]->amax_i;
+                    if (pvv > gv || (pvv == gv && pi < gi)) { gv = pvv; gi = pi; }
+                }
+                const int o = owner(gi);
+                S.newc[k] = pv[o][gi - plo[o]];
+            }
+            cl.sync();  // the argmax slots are read before they are rewritten
+            __syncthreads();
+        }
+        if (tid < K) S.cent[tid] = S.newc[tid];
+        __syncthreads();
+        sort_cents(S.cent, K, S);
+        int changed = 0;
+#pragma unroll 2
+        for (int j = tid; j < m; j += KT) {
+            const unsigned short nl = (unsigned short)nearest_sorted(v[j], S.cs, S.ci, K, ktop);
+            lab2[j] = nl;
+            changed |= (nl != lab[j]);
+        }
+        changed = block_sum_int(changed, S);
+        if (tid == 0) P.changed = changed;
+        cl.sync();
+        int any = 0;
+#pragma unroll
+        for (int r = 0; r < KC; ++r) any |= peer[r]->changed;
+        if (!any) break;
+        unsigned short* t = lab;
+        lab = lab2;
+        lab2 = t;
+        __syncthreads();
+    }
+    if (tid == 0 && blockIdx.x == 0) {  // phase clocks of cluster 0's CTA 0 (mlk_kmeans_prof)
+        g_km_prof[0] = kp_t1 - kp_t0;
+        g_km_prof[1] = kp_t2 - kp_t1;
+        g_km_prof[2] = clock64() - kp_t2;
+        g_km_prof[3] = sweeps;
+        for (int t = 0; t < 6; ++t) g_km_prof[4 + t] = 0;
+    }
+    if (q == 0) {  // ---- sorted float32 codebook row
+        if (tid == 0) {
+            for (int a = 1; a < K; ++a) {
+                const double x = S.cent[a];
+                int b = a - 1;
+                while (b >= 0 && S.cent[b] > x) { S.cent[b + 1] = S.cent[b]; --b; }
+                S.cent[b + 1] = x;
+            }
+            inf[0] = 1; inf[1] = K; inf[2] = sweeps; inf[3] = fallbacks;
+        }
+        __syncthreads();
+        if (tid < K) {
+            out[tid] = (float)S.cent[tid];
+            if (out64) out64[tid] = S.cent[tid];
+        }
+    }
+    cl.sync();  // no CTA leaves while a peer may still read its shared memory
+}
+
 }  // namespace
 
 extern "C" int mlk_kmeans(const double* lat, const MlkShard* shards, const MlkShard* shards_h,
@@ -620,6 +1053,39 @@ extern "C" int mlk_kmeans(const double* lat, const MlkShard* shards, const MlkSh
     int dev = 0, optin = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    // 4-CTA clusters when every shard is big enough for depth-2 subtrees and
+    // a CTA's members (values, d2, two label arrays) fit its shared memory
+    int n_min = n_cap, m_cap = 0;
+    for (int s = 0; s < n_shards; ++s) {
+        const int n = shards_h[s].n_img;
+        n_min = n < n_min ? n : n_min;
+        const int l = pw_split(n);
+        const int parts[4] = {pw_split(l), l - pw_split(l), pw_split(n - l), n - l - pw_split(n - l)};
+        for (int p : parts) m_cap = p > m_cap ? p : m_cap;
+    }
+    const size_t with_cluster = head + (size_t)m_cap * (2 * sizeof(double) + 2 * sizeof(uint16_t));
+    if (KM_CLUSTER && n_min >= 4096 &&
+        with_cluster + sizeof(KmSmem) + sizeof(KcPub) + 1024 <= (size_t)optin) {
+        cudaFuncSetAttribute(k_kmeans_cl, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)with_cluster);
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(n_shards * L * KC);
+        cfg.blockDim = dim3(KT);
+        cfg.dynamicSmemBytes = with_cluster;
+        cfg.stream = stream;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = KC;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        if (cudaLaunchKernelEx(&cfg, k_kmeans_cl, lat, shards, (int)L, (int)K,
+                               reinterpret_cast<const long long*>(first_idx), draws, scratch,
+                               cents, cents64, info, slots, m_cap) != cudaSuccess)
+            return MLK_ERR_CUDA;
+        return MLK_OK;
+    }
     if (with_members + sizeof(KmSmem) <= (size_t)optin) {
         cudaFuncSetAttribute(k_kmeans<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)with_members);

@@ -86,6 +86,24 @@ def test_kmeans_ties_and_duplicates_match_oracle():
 
 @gpu
 @needs_cuda
+@pytest.mark.parametrize("n", [4096, 9001, 16395, 30000])
+def test_kmeans_large_matches_oracle(n):
+    """Shards of >= 4096 members run on a 4-CTA cluster (csrc/kmeans.cu
+    k_kmeans_cl): the codebook equals the oracle's bit for bit, also with
+    duplicates, a cluster that dies and few distinct values."""
+    from oracle import port
+    rng = np.random.default_rng(n)
+    cases = [rng.normal(0, 1, n) * 3.0,
+             np.round(rng.normal(0, 1, n) * 8) / 4,                      # many duplicates
+             np.concatenate([rng.normal(0, 1, n - 40), np.full(40, 1e6)]),  # far outliers
+             rng.integers(0, 9, n).astype(np.float64)]                   # <= 16 distinct
+    for i, v in enumerate(cases):
+        for seed in (0, 5):
+            assert np.array_equal(mb.kmeans_1d(v, 16, seed), port.kmeans(v, 16, seed)), (i, seed)
+
+
+@gpu
+@needs_cuda
 def test_kmeans_deterministic_and_quality():
     rng = np.random.default_rng(12)
     v = np.concatenate([rng.normal(0, 1, 80), rng.normal(8, 0.5, 60), rng.normal(-5, 2, 60)])
