@@ -163,6 +163,23 @@ __device__ double block_exscan(double v, double* total, KmSmem& S) {
     return r;
 }
 
+// warp 0: 1 when the first 64 members already hold >= K + 1 distinct
+// non-NaN values (then np.unique's shortcut cannot apply); other warps 0
+__device__ __forceinline__ int many_distinct64(const double* v, int m, int K) {
+    const int lane = threadIdx.x & 31;
+    if ((threadIdx.x >> 5) != 0) return 0;
+    const double nan = __longlong_as_double(0x7ff8000000000000ll);
+    const double a = lane < m ? v[lane] : nan, b = lane + 32 < m ? v[lane + 32] : nan;
+    bool fa = a == a, fb = b == b;
+    for (int k = 0; k < 32; ++k) {
+        const double xa = __shfl_sync(0xffffffffu, a, k), xb = __shfl_sync(0xffffffffu, b, k);
+        if (k < lane && xa == a) fa = false;
+        if (xa == b || (k < lane && xb == b)) fb = false;
+    }
+    return __popc(__ballot_sync(0xffffffffu, fa)) + __popc(__ballot_sync(0xffffffffu, fb)) >=
+           K + 1;
+}
+
 // S.cs / S.ci = the centroids sorted ascending, equal values by index
 // (a rank per centroid: one pass, one barrier).  Whole CTA; c visible.
 __device__ void sort_cents(const double* c, int K, KmSmem& S) {
@@ -360,8 +377,14 @@ k_kmeans(const double* __restrict__ lat, const MlkShard* __restrict__ shards, in
     for (int j = tid; j < n; j += KT) v[j] = lat[(long long)(sh.img_off + j) * L + dim];
     __syncthreads();
 
-    // ---- distinct shortcut (np.unique; quantizer.py:62-65)
+    // ---- distinct shortcut (np.unique; quantizer.py:62-65), unless the first
+    //      64 members already settle it
     {
+        const int many = many_distinct64(v, n, K);
+        if (tid == 0) S.bcast_i = many;
+    }
+    __syncthreads();
+    if (!S.bcast_i) {
         double cur = INFINITY;
         for (int j = tid; j < n; j += KT) cur = fmin(cur, v[j]);
         cur = block_min(cur, S);
@@ -697,17 +720,9 @@ k_kmeans_cl(const double* __restrict__ lat, const MlkShard* __restrict__ shards,
     // ---- distinct shortcut (np.unique; quantizer.py:62-65): some CTA seeing
     //      K + 1 distinct non-NaN values among its first 64 members settles
     //      it; otherwise the exact successive-minimum walk, cluster-wide
-    if (w == 0) {
-        const double a = lane < m ? v[lane] : __longlong_as_double(0x7ff8000000000000ll);
-        const double b = lane + 32 < m ? v[lane + 32] : __longlong_as_double(0x7ff8000000000000ll);
-        bool fa = a == a, fb = b == b;
-        for (int k = 0; k < 32; ++k) {
-            const double xa = __shfl_sync(0xffffffffu, a, k), xb = __shfl_sync(0xffffffffu, b, k);
-            if (k < lane && xa == a) fa = false;
-            if (xa == b || (k < lane && xb == b)) fb = false;
-        }
-        const int nd = __popc(__ballot_sync(0xffffffffu, fa)) + __popc(__ballot_sync(0xffffffffu, fb));
-        if (lane == 0) P.many = nd >= K + 1;
+    {
+        const int many0 = many_distinct64(v, m, K);
+        if (tid == 0) P.many = many0;
     }
     cl.sync();
     bool many = false;
