@@ -17,6 +17,7 @@ import functools
 import os
 import math
 import struct
+import time
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -31,6 +32,7 @@ SPAN = 2.0 ** -20
 STEPS = 20
 LOOKAHEAD = int(os.environ.get("MLK_LOOKAHEAD", 8))  # levels per host round trip
 PASS_LEVELS = int(os.environ.get("MLK_PASS_LEVELS", 2))  # levels per probe launch
+EB_TRACE = None  # a list: the search appends (event, host time) per round (diagnostics)
 _PAYLOAD_HEAD = struct.Struct("<BHHd")
 
 
@@ -709,8 +711,11 @@ def compress_device(f0: torch.Tensor, specs, dgrid: DeviceGrid, cfg, timer: Time
     rounds = 0
     fail = T("fail", (S, n_nodes), i32)
     zero_start = None
+    tr = EB_TRACE.append if EB_TRACE is not None else None
     while any(st is not None and st.stage != "done" for st in states):
         rounds += 1
+        if tr:
+            tr(("round", time.perf_counter()))
         cnt_act = np.zeros(S, dtype=np.int32)
         live = []
         for s, st in enumerate(states):
@@ -726,13 +731,19 @@ def compress_device(f0: torch.Tensor, specs, dgrid: DeviceGrid, cfg, timer: Time
             zero_start = ws.stage(np.zeros(S, dtype=np.int32))
         ws.flush()
         fail.zero_()
+        if tr:
+            tr(("staged", time.perf_counter()))
         for level in range(0, LOOKAHEAD, PASS_LEVELS):  # several levels per pass
             call("mlk_probe", f0, stats, sh_d, S, dgrid.addr, W, L, cents, K, codes, sel_rng,
                  off_d, zero_start, int(off[-1]), rbound, cfg.tau, cand_d, n_nodes, level,
                  min(PASS_LEVELS, LOOKAHEAD - level), fail, bins, eb_hi)
+        if tr:
+            tr(("launched", time.perf_counter()))
         if comm is not None:
             comm.all_reduce_(fail, "max")
         (fail_h,) = _d2h(fail)
+        if tr:
+            tr(("synced", time.perf_counter()))
         for s, st in enumerate(states):
             if st is None or st.stage == "done":
                 continue
@@ -749,6 +760,8 @@ def compress_device(f0: torch.Tensor, specs, dgrid: DeviceGrid, cfg, timer: Time
                 st = st.advance(ok)
                 node = 2 * node + (0 if ok else 1)
             states[s] = st
+        if tr:
+            tr(("decided", time.perf_counter()))
     eb = [0.0] * S
     lossless = [False] * S
     for s, st in enumerate(states):
