@@ -314,8 +314,8 @@ def _peak():
 
 def _traffic(kernel, launches_per_step):
     """DRAM bytes per step of `kernel` from the committed ncu --set full
-    capture (profiles/r1_kernels.json), when every launch of a step is in it."""
-    path = ROOT / "profiles" / "r1_kernels.json"
+    capture (profiles/r2_kernels.json), when every launch of a step is in it."""
+    path = ROOT / "profiles" / "r2_kernels.json"
     if not path.exists():
         return None
     ks = [k for k in json.loads(path.read_text()) if k["kernel"].startswith(kernel)]
@@ -387,9 +387,9 @@ def rooflines(out, stage_ms, n, dev, traffic_ok=True):
     rows = [
         ("k_stage1", "encode", n * (HIST_BYTES + 96), 1,
          "reads every histogram once (TMA) + 96 B of latents/stats/moments"),
-        ("k_project", "newton", n * (HIST_BYTES + 185) + vlen, 1,
+        ("k_project", "newton", n * (HIST_BYTES + 185) + vlen, 2,
          "reads every histogram again + per-image outputs + varint streams"),
-        ("k_deflate_warp", "deflate", vlen + zlen, 7,
+        ("k_deflate_warp", "deflate", vlen + zlen, 14,
          "varint bytes in + zlib bytes out; serial LZ77/Huffman per stream (latency-bound)"),
         ("k_probe", "eb_search", None, None, "re-reads selected histograms per round; L2/latency"),
         ("k_kmeans", "pq", None, None, "32 B of latents per histogram; barrier/latency-bound"),
