@@ -387,8 +387,10 @@ def rooflines(out, stage_ms, n, dev, traffic_ok=True):
     rows = [
         ("k_stage1", "encode", n * (HIST_BYTES + 96), 1,
          "reads every histogram once (TMA) + 96 B of latents/stats/moments"),
-        ("k_project", "newton", n * (HIST_BYTES + 185) + vlen, 2,
-         "reads every histogram again + per-image outputs + varint streams"),
+        ("k_project", "project_sel_launch", n_sel * (HIST_BYTES + 185) + vlen, None,
+         "the residual-image launch (its CUDA-event span on its own stream): reads each "
+         "selected histogram + per-image outputs + varint streams; the residual-free launch "
+         "runs under the search on the side stream (stage_ms.project_non_launch)"),
         ("k_deflate_warp", "deflate", vlen + zlen, 14,
          "varint bytes in + zlib bytes out; serial LZ77/Huffman per stream (latency-bound)"),
         ("k_probe", "eb_search", None, None, "re-reads selected histograms per round; L2/latency"),
