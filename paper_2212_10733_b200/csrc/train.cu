@@ -1,8 +1,9 @@
 // train.cu -- tied-weight AE training on device.
 //
 // Restates autoencoder.train (autoencoder.py:137-177) for a batch of
-// independent jobs (one per shard, pipeline.py:209-218), one CTA per job for
-// the whole run (every epoch and every Adam step in one launch):
+// independent jobs (one per shard, pipeline.py:209-218), one thread-block
+// cluster per job for the whole run (every epoch and every Adam step in one
+// launch; layout below):
 //  * fit_normalizer (autoencoder.py:77-84): mean and population std over all
 //    scalar entries of the training selection, floored at STD_FLOOR;
 //  * per step, on the rows order[e*n + start ...] (rng.permutation, drawn by
