@@ -710,7 +710,18 @@ def compress_device(f0: torch.Tensor, specs, dgrid: DeviceGrid, cfg, timer: Time
     n_nodes = 1 << LOOKAHEAD
     rounds = 0
     fail = T("fail", (S, n_nodes), i32)
-    zero_start = None
+    zero_start = ws.stage(np.zeros(S, dtype=np.int32))
+    ws.flush()
+    # each round's lookahead tree and work offsets: one pinned host block and
+    # one copy into fixed device views (the previous round's copy has landed:
+    # its verdicts were read back)
+    nb_cand = 8 * S * n_nodes
+    h_round = hostio.pinned(f"eb_round{dev.index}", nb_cand + 4 * (S + 1))
+    d_round = T("eb_round", (nb_cand + 4 * (S + 1),), torch.uint8)
+    h_cand = h_round.numpy()[:nb_cand].view(np.float64).reshape(S, n_nodes)
+    h_off = h_round.numpy()[nb_cand:nb_cand + 4 * (S + 1)].view(np.int32)
+    cand_d = d_round[:nb_cand].view(torch.float64).view(S, n_nodes)
+    off_d = d_round[nb_cand:].view(torch.int32)
     tr = EB_TRACE.append if EB_TRACE is not None else None
     while any(st is not None and st.stage != "done" for st in states):
         rounds += 1
@@ -722,14 +733,17 @@ def compress_device(f0: torch.Tensor, specs, dgrid: DeviceGrid, cfg, timer: Time
             if st is not None and st.stage != "done":
                 live.append(s)
                 cnt_act[s] = int(cnt_h[s])
-        cand = np.full((S, n_nodes), np.nan)
+        cand = h_cand
+        cand.fill(np.nan)
         cand[live] = _search_heap([states[s] for s in live], LOOKAHEAD)
-        off = np.concatenate([[0], np.cumsum(cnt_act)]).astype(np.int32)
-        cand_d = ws.stage(cand)
-        off_d = ws.stage(off)
-        if zero_start is None:
-            zero_start = ws.stage(np.zeros(S, dtype=np.int32))
-        ws.flush()
+        if tr:
+            tr(("tree", time.perf_counter()))
+        off = h_off
+        off[0] = 0
+        np.cumsum(cnt_act, out=off[1:])
+        d_round.copy_(h_round[:nb_cand + 4 * (S + 1)], non_blocking=True)
+        if tr:
+            tr(("flush", time.perf_counter()))
         fail.zero_()
         if tr:
             tr(("staged", time.perf_counter()))
