@@ -644,14 +644,17 @@ k_kmeans(const double* __restrict__ lat, const MlkShard* __restrict__ shards, in
 // published in a small per-CTA block and read by the peers through
 // distributed shared memory between cluster barriers.  Same operations in
 // the same order as k_kmeans: the codebooks are bit-identical.
-constexpr int KC = 4;  // CTAs per cluster
-
-__device__ __forceinline__ void kc_range(int n, int q, int& lo, int& hi) {
-    const int l = pw_split(n);
-    const int a = q < 2 ? 0 : l, m = q < 2 ? l : n - l;
-    const int h = pw_split(m);
-    lo = (q & 1) ? a + h : a;
-    hi = (q & 1) ? a + m : a + h;
+// CTA q's members: the q-th subtree at depth log2(KC) of the pairwise
+// recursion over n (the bits of q, most significant first, pick the halves)
+template <int KC>
+__host__ __device__ inline void kc_range(int n, int q, int& lo, int& hi) {
+    lo = 0;
+    int m = n;
+    for (int b = KC >> 1; b >= 1; b >>= 1) {
+        const int h = pw_split(m);
+        if (q & b) { lo += h; m -= h; } else { m = h; }
+    }
+    hi = lo + m;
 }
 
 struct KcPub {  // per-CTA values the peers read
@@ -662,6 +665,11 @@ struct KcPub {  // per-CTA values the peers read
     double msum[MLK_MAXK];
 };
 
+// KC CTAs per cluster; SMALL: d2 and the pairwise-tree slots in shared
+// memory too (else d2 in the shard's global scratch and the slots in the
+// scratch's label slice, which this kernel keeps in shared memory -- for
+// shards whose members alone fill a CTA)
+template <int KC, bool SMALL>
 __global__ void __launch_bounds__(KT, 1)
 k_kmeans_cl(const double* __restrict__ lat, const MlkShard* __restrict__ shards, int L, int K,
             const long long* __restrict__ first_idx, const double* __restrict__ draws,
@@ -673,20 +681,32 @@ k_kmeans_cl(const double* __restrict__ lat, const MlkShard* __restrict__ shards,
     __shared__ KmSmem S;
     __shared__ KcPub P;
     extern __shared__ double dyn[];
-    double* val = dyn;
-    int* wcnt = reinterpret_cast<int*>(dyn + slots);   // [KW][K]
-    unsigned char* kind = reinterpret_cast<unsigned char*>(wcnt + KW * K);
-    double* v = dyn + ((slots * 9 + KW * K * 4 + 15) / 16) * 2;
-    double* d2 = v + m_cap;
-    unsigned short* lab = reinterpret_cast<unsigned short*>(d2 + m_cap);
-    unsigned short* lab2 = lab + m_cap;
-
     const int job = blockIdx.x / KC;
     const int s = job / L, dim = job % L;
     const MlkShard sh = shards[s];
     const int n = sh.n_img;
     int lo, hi;
-    kc_range(n, q, lo, hi);
+    kc_range<KC>(n, q, lo, hi);
+    double *val, *v, *d2;
+    int* wcnt;  // [KW][K]
+    unsigned char* kind;
+    if (SMALL) {
+        val = dyn;
+        wcnt = reinterpret_cast<int*>(dyn + slots);
+        kind = reinterpret_cast<unsigned char*>(wcnt + KW * K);
+        v = dyn + ((slots * 9 + KW * K * 4 + 15) / 16) * 2;
+        d2 = v + m_cap;
+    } else {
+        wcnt = reinterpret_cast<int*>(dyn);
+        v = dyn + ((KW * K * 4 + 15) / 16) * 2;
+        double* base = scratch + (long long)4 * L * sh.img_off + (long long)4 * dim * n;
+        val = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(base + 3 * n) +
+                                        (size_t)q * (((size_t)slots * 9 + 15) / 16) * 16);
+        kind = reinterpret_cast<unsigned char*>(val + slots);
+        d2 = base + n + lo;
+    }
+    unsigned short* lab = reinterpret_cast<unsigned short*>((SMALL ? d2 : v) + m_cap);
+    unsigned short* lab2 = lab + m_cap;
     const int m = hi - lo;
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     double* srt = scratch + (long long)4 * L * sh.img_off + (long long)4 * dim * n + 2 * n;
@@ -701,10 +721,11 @@ k_kmeans_cl(const double* __restrict__ lat, const MlkShard* __restrict__ shards,
     for (int r = 0; r < KC; ++r) {
         peer[r] = cl.map_shared_rank(&P, r);
         pv[r] = cl.map_shared_rank(v, r);
-        pd2[r] = cl.map_shared_rank(d2, r);
+        pd2[r] = SMALL ? cl.map_shared_rank(d2, r) : nullptr;  // (global: set below)
         int a, b;
-        kc_range(n, r, a, b);
+        kc_range<KC>(n, r, a, b);
         plo[r] = a;
+        if (!SMALL) pd2[r] = d2 - lo + a;
     }
     auto owner = [&](int j) {  // CTA holding shard member j
         int r = 0;
@@ -804,9 +825,15 @@ k_kmeans_cl(const double* __restrict__ lat, const MlkShard* __restrict__ shards,
             P.loc_tot = ltot;
         }
         cl.sync();
-        // the shard's pairwise sum: the top two levels over the subtrees
-        const double tot = __dadd_rn(__dadd_rn(peer[0]->dsum, peer[1]->dsum),
-                                     __dadd_rn(peer[2]->dsum, peer[3]->dsum));
+        // the shard's pairwise sum: the top log2(KC) levels over the subtrees
+        double tt[KC];
+#pragma unroll
+        for (int r = 0; r < KC; ++r) tt[r] = peer[r]->dsum;
+#pragma unroll
+        for (int wdt = KC; wdt > 1; wdt >>= 1)
+#pragma unroll
+            for (int i2 = 0; i2 < wdt / 2; ++i2) tt[i2] = __dadd_rn(tt[2 * i2], tt[2 * i2 + 1]);
+        const double tot = tt[0];
         if (tot <= 0) {
             if (tid == 0)
                 for (int t = i; t < K; ++t) S.cent[t] = S.cent[0];
@@ -953,8 +980,8 @@ k_kmeans_cl(const double* __restrict__ lat, const MlkShard* __restrict__ shards,
         }
         __syncthreads();
         nsub = S.bcast_i;
-        __shared__ int sub_start[MLK_MAXK / KC + 1], sub_cnt[MLK_MAXK / KC + 1],
-            sub_id[MLK_MAXK / KC + 1];
+        __shared__ int sub_start[MLK_MAXK / 4 + 1], sub_cnt[MLK_MAXK / 4 + 1],
+            sub_id[MLK_MAXK / 4 + 1];
         if (tid < nsub) {
             const int k = S.seg_base[tid];
             sub_id[tid] = k;
@@ -1068,38 +1095,52 @@ extern "C" int mlk_kmeans(const double* lat, const MlkShard* shards, const MlkSh
     int dev = 0, optin = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    // 4-CTA clusters when every shard is big enough for depth-2 subtrees and
-    // a CTA's members (values, d2, two label arrays) fit its shared memory
-    int n_min = n_cap, m_cap = 0;
-    for (int s = 0; s < n_shards; ++s) {
-        const int n = shards_h[s].n_img;
-        n_min = n < n_min ? n : n_min;
-        const int l = pw_split(n);
-        const int parts[4] = {pw_split(l), l - pw_split(l), pw_split(n - l), n - l - pw_split(n - l)};
-        for (int p : parts) m_cap = p > m_cap ? p : m_cap;
-    }
-    const size_t with_cluster = head + (size_t)m_cap * (2 * sizeof(double) + 2 * sizeof(uint16_t));
-    if (KM_CLUSTER && n_min >= 4096 &&
-        with_cluster + sizeof(KmSmem) + sizeof(KcPub) + 1024 <= (size_t)optin) {
-        cudaFuncSetAttribute(k_kmeans_cl, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)with_cluster);
+    // clusters: 4 CTAs with everything in shared memory when every shard has
+    // >= 4096 members and a quarter fits; else 8 CTAs keeping only the
+    // values and labels in shared memory (d2 and the tree slots in scratch)
+    int n_min = n_cap;
+    for (int s = 0; s < n_shards; ++s) n_min = shards_h[s].n_img < n_min ? shards_h[s].n_img : n_min;
+    auto part_cap = [&](int kc) {
+        int mc = 0;
+        for (int s = 0; s < n_shards; ++s)
+            for (int q = 0; q < kc; ++q) {
+                int a, b;
+                if (kc == 4) kc_range<4>(shards_h[s].n_img, q, a, b);
+                else kc_range<8>(shards_h[s].n_img, q, a, b);
+                mc = b - a > mc ? b - a : mc;
+            }
+        return mc;
+    };
+    const size_t stat = sizeof(KmSmem) + sizeof(KcPub) + 1024;
+    auto launch_cl = [&](auto kern, int kc, size_t dyn_b, int m_cap) -> int {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn_b);
         cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3(n_shards * L * KC);
+        cfg.gridDim = dim3(n_shards * L * kc);
         cfg.blockDim = dim3(KT);
-        cfg.dynamicSmemBytes = with_cluster;
+        cfg.dynamicSmemBytes = dyn_b;
         cfg.stream = stream;
         cudaLaunchAttribute at[1];
         at[0].id = cudaLaunchAttributeClusterDimension;
-        at[0].val.clusterDim.x = KC;
+        at[0].val.clusterDim.x = kc;
         at[0].val.clusterDim.y = 1;
         at[0].val.clusterDim.z = 1;
         cfg.attrs = at;
         cfg.numAttrs = 1;
-        if (cudaLaunchKernelEx(&cfg, k_kmeans_cl, lat, shards, (int)L, (int)K,
-                               reinterpret_cast<const long long*>(first_idx), draws, scratch,
-                               cents, cents64, info, slots, m_cap) != cudaSuccess)
-            return MLK_ERR_CUDA;
-        return MLK_OK;
+        return cudaLaunchKernelEx(&cfg, kern, lat, shards, (int)L, (int)K,
+                                  reinterpret_cast<const long long*>(first_idx), draws, scratch,
+                                  cents, cents64, info, slots, m_cap) == cudaSuccess
+                   ? MLK_OK : MLK_ERR_CUDA;
+    };
+    if (KM_CLUSTER && n_min >= 4096) {
+        const int m4 = part_cap(4);
+        const size_t d4 = head + (size_t)m4 * (2 * sizeof(double) + 2 * sizeof(uint16_t));
+        if (d4 + stat <= (size_t)optin) return launch_cl(k_kmeans_cl<4, true>, 4, d4, m4);
+        const int m8 = part_cap(8);
+        const size_t d8 = (size_t)((KW * K * 4 + 15) / 16) * 16 +
+                          (size_t)m8 * (sizeof(double) + 2 * sizeof(uint16_t));
+        const size_t slot_bytes = 8 * (((size_t)slots * 9 + 15) / 16) * 16;
+        if (d8 + stat <= (size_t)optin && slot_bytes <= (size_t)8 * n_min)
+            return launch_cl(k_kmeans_cl<8, false>, 8, d8, m8);
     }
     if (with_members + sizeof(KmSmem) <= (size_t)optin) {
         cudaFuncSetAttribute(k_kmeans<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -86,11 +86,13 @@ def test_kmeans_ties_and_duplicates_match_oracle():
 
 @gpu
 @needs_cuda
-@pytest.mark.parametrize("n", [4096, 9001, 16395, 30000])
+@pytest.mark.parametrize("n", [4096, 9001, 16395, 30000, 60000, 131160])
 def test_kmeans_large_matches_oracle(n):
-    """Shards of >= 4096 members run on a 4-CTA cluster (csrc/kmeans.cu
-    k_kmeans_cl): the codebook equals the oracle's bit for bit, also with
-    duplicates, a cluster that dies and few distinct values."""
+    """Shards of >= 4096 members run on a thread-block cluster (csrc/kmeans.cu
+    k_kmeans_cl: 4 CTAs with everything in shared memory, or 8 CTAs with d2
+    in global scratch beyond ~40k members): the codebook equals the oracle's
+    bit for bit, also with duplicates, a cluster that dies and few distinct
+    values."""
     from oracle import port
     rng = np.random.default_rng(n)
     cases = [rng.normal(0, 1, n) * 3.0,
