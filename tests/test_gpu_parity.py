@@ -441,7 +441,17 @@ def test_device_zlib_matches_host_zlib():
     streams.append(rng.permutation(sym)[:15000].tobytes())
     sym = np.concatenate([np.full(f, 3 * k + 1, np.uint8) for k, f in enumerate(fib[:12])])
     streams.append(rng.permutation(sym).tobytes())
-    vcap = 15216
+    # chain / match extremes: long zero runs (258-byte matches), short periods
+    # (deep hash chains hitting max_chain), a 3-symbol alphabet, and every
+    # size-tier boundary of the warp kernel
+    streams.append(bytes(15999))
+    streams.append((b"abc" * 5400)[:16000])
+    streams.append(rng.integers(0, 3, 16000, dtype=np.uint8).tobytes())
+    streams.append((bytes(range(7)) * 2400)[:16000])
+    for n in [1024, 1025, 1600, 1601, 2048, 2049, 3072, 3073, 4096, 4097, 8192, 8193, 16000]:
+        z = rng.geometric(0.3, n)
+        streams.append(np.minimum(z, 255).astype(np.uint8).tobytes())
+    vcap = 16000
     var = torch.zeros(len(streams) * vcap, dtype=torch.uint8, device=dev)
     vlen = torch.tensor([len(s) for s in streams], dtype=torch.int64, device=dev)
     for i, s in enumerate(streams):
