@@ -343,12 +343,13 @@ __device__ __forceinline__ double qround(double r, double eb2, double inv) {
 // a / b correctly rounded from y = RN(1/b) (b fixed across many a): Markstein's
 // correction q' = RN(q + RN(a - q b) y), q = RN(a y), is the IEEE quotient
 // for normal-range results (checked against a / b on 2e8 random pairs);
-// zero, tiny, huge or non-finite quotients take the IEEE division.
+// quotients outside [2^-1000, 2^999) (zero, tiny, huge, non-finite) take the
+// IEEE division -- one integer range test on the exponent field.
 __device__ __forceinline__ double div_by_recip(double a, double b, double y) {
     const double q = __dmul_rn(a, y);
     const double r = __fma_rn(-q, b, a);
     const double q2 = __fma_rn(r, y, q);
-    const double m = fabs(q2);
-    if (a == 0.0 || (m >= 0x1p-1000 && m <= 0x1p+1000)) return q2;
+    const unsigned hi = (unsigned)__double2hiint(q2) & 0x7fffffffu;
+    if (hi - 0x01700000u < 0x7CF00000u) return q2;  // biased exponent 23 .. 2021
     return __ddiv_rn(a, b);
 }

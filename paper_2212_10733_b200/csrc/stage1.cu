@@ -43,6 +43,7 @@ k_stage1(const double* __restrict__ f0, const MlkShard* __restrict__ shards, int
     extern __shared__ __align__(16) double smem[];
     __shared__ unsigned long long bars[S1_WARPS];
     __shared__ double gvp[64], gvq[64];  // separable grids: v_par by column, v_perp^2 by row
+    __shared__ double svcls[4];          // cell volume by (row edge, column edge) class
     __shared__ int pstart[16];           // OpenBLAS K-panel starts (GEMM path)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int D = g.D;
@@ -60,6 +61,7 @@ k_stage1(const double* __restrict__ f0, const MlkShard* __restrict__ shards, int
     const float* Wg = W + sh.w_off;
     for (int i = threadIdx.x; i < L * D; i += blockDim.x) Wsm[i] = __ldg(Wg + i);
     const bool sep = g.sep && g.rows <= 64 && g.cols <= 64;
+    if (threadIdx.x < 4) svcls[threadIdx.x] = g.vcls[threadIdx.x];
     if (sep) {
         for (int i = threadIdx.x; i < g.cols; i += blockDim.x) gvp[i] = g.vpar[i];
         for (int i = threadIdx.x; i < g.rows; i += blockDim.x) gvq[i] = g.vperp2[i * g.cols];
@@ -106,12 +108,14 @@ k_stage1(const double* __restrict__ f0, const MlkShard* __restrict__ shards, int
             for (int j = lane; j < D; j += 32) {
                 const double v = buf[j];
                 has_nan |= v != v;
-                mx = fmax(mx, v);
-                mn = fmin(mn, v);
+                // (NaN is handled by has_nan; the sign of a zero extremum
+                // never matters: the stats enter only as mx - mn)
+                mx = v > mx ? v : mx;
+                mn = v < mn ? v : mn;
                 so += v;
                 soo = fma(v, v, soo);
-                const bool re = (r == 0) | (r == rows - 1), ce = (c == 0) | (c == cols - 1);
-                const double vol = re ? (ce ? g.vcls[3] : g.vcls[2]) : (ce ? g.vcls[1] : g.vcls[0]);
+                const int re = (r == 0) | (r == rows - 1), ce = (c == 0) | (c == cols - 1);
+                const double vol = svcls[2 * re + ce];
                 const double fv = v * vol;
                 n0 += fv;
                 n1 = fma(fv, gvp[c], n1);
@@ -125,8 +129,8 @@ k_stage1(const double* __restrict__ f0, const MlkShard* __restrict__ shards, int
             for (int j = lane; j < D; j += 32) {
                 double v = buf[j];
                 has_nan |= v != v;
-                mx = fmax(mx, v);
-                mn = fmin(mn, v);
+                mx = v > mx ? v : mx;
+                mn = v < mn ? v : mn;
                 so += v;
                 soo = fma(v, v, soo);
                 double fv = v * __ldg(g.vol + j);
@@ -152,8 +156,8 @@ k_stage1(const double* __restrict__ f0, const MlkShard* __restrict__ shards, int
             int r = lane / cols, c = lane - (lane / cols) * cols;
             const int dr = 32 / cols, dc = 32 - (32 / cols) * cols;
             for (int j = lane; j < D; j += 32) {
-                const bool re = (r == 0) | (r == rows - 1), ce = (c == 0) | (c == cols - 1);
-                const double vol = re ? (ce ? g.vcls[3] : g.vcls[2]) : (ce ? g.vcls[1] : g.vcls[0]);
+                const int re = (r == 0) | (r == rows - 1), ce = (c == 0) | (c == cols - 1);
+                const double vol = svcls[2 * re + ce];
                 const double dv = gvp[c] - u;
                 n3 = fma(buf[j] * vol, dv * dv, n3);
                 c += dc;
