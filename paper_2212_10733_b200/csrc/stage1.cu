@@ -184,14 +184,22 @@ k_stage1(const double* __restrict__ f0, const MlkShard* __restrict__ shards, int
         if (padded) {
             // descending, so every write (to j + panel(j) >= j) lands on a slot
             // that has already been read
+            // panel of this lane's element: found once, then stepped down
+            // (j falls by 32 per step, less than any panel's length)
+            int p = 0;
+            {
+                const int j = D - 1 - lane;
+                if (j >= 0) {
+                    p = j < 384 * k0 ? j / 384 : (j < b1 ? k0 : k0 + 1);
+                    if (p > np_ - 1) p = np_ - 1;
+                }
+            }
             for (int t = 0; t < (D + 31) / 32; ++t) {  // warp-uniform trip count
                 const int j = D - 1 - lane - 32 * t;
                 double xn = 0.0;
-                int p = 0;
                 if (j >= 0) {
                     xn = div_by_recip(__dsub_rn(buf[j], sh.mean), sh.std, rstd);
-                    p = j < 384 * k0 ? j / 384 : (j < b1 ? k0 : k0 + 1);
-                    if (p > np_ - 1) p = np_ - 1;
+                    if (p > 0 && j < pstart[p]) --p;
                 }
                 __syncwarp();
                 if (j >= 0) buf[j + p] = xn;
