@@ -88,7 +88,10 @@ k_probe_bins(const double* __restrict__ f0, const MlkShard* __restrict__ shards,
         int bin;
         if (!(ar > 0.0)) bin = 0;  // zero (NaN images are never selected)
         else {
-            const int e = ilogb(ar);
+            // floor(log2 |r|): the exponent field for normal values (ilogb
+            // only for subnormals)
+            const int fe = (__double2hiint(ar) >> 20) & 0x7ff;
+            const int e = fe ? fe - 1023 : ilogb(ar);
             bin = e < e0 ? 0 : (e >= e0 + 32 ? PB_NB - 1 : e - e0 + 1);
         }
         bc[bin][lane] += 1;
