@@ -189,6 +189,11 @@ __global__ void k_unpack(const unsigned char* buf, long long count, int bits, un
 }
 
 // one warp per segment, byte copies (segments are short and unaligned)
+// segment copies, one warp per segment: the head bytes up to an 8-byte
+// aligned destination, then one aligned 8-byte word per lane per step built
+// from the two aligned source words it straddles (funnel shift), then the
+// tail bytes.  A source word is only read when it holds a byte of the
+// segment, so nothing outside an allocation's 8-byte words is touched.
 __global__ void k_gather(const unsigned char* __restrict__ src, const long long* __restrict__ soff,
                          const long long* __restrict__ len, int n, unsigned char* __restrict__ dst,
                          const long long* __restrict__ doff) {
@@ -198,7 +203,23 @@ __global__ void k_gather(const unsigned char* __restrict__ src, const long long*
     const unsigned char* s = src + soff[seg];
     unsigned char* d = dst + doff[seg];
     const long long l = len[seg];
-    for (long long i = lane; i < l; i += 32) d[i] = s[i];
+    const long long h = ((8 - (long long)(reinterpret_cast<uintptr_t>(d) & 7)) & 7) < l
+                            ? ((8 - (long long)(reinterpret_cast<uintptr_t>(d) & 7)) & 7) : l;
+    if (lane < h) d[lane] = s[lane];
+    const long long nw = (l - h) >> 3;  // whole destination words
+    unsigned long long* dw = reinterpret_cast<unsigned long long*>(d + h);
+    const unsigned char* sb = s + h;
+    const int sa = (int)(reinterpret_cast<uintptr_t>(sb) & 7);
+    const unsigned long long* sw = reinterpret_cast<const unsigned long long*>(sb - sa);
+    if (sa == 0) {
+#pragma unroll 4  // several independent loads in flight per lane
+        for (long long i = lane; i < nw; i += 32) dw[i] = sw[i];
+    } else {
+        const int lo = 8 * sa, hi = 64 - lo;
+#pragma unroll 4
+        for (long long i = lane; i < nw; i += 32) dw[i] = (sw[i] >> lo) | (sw[i + 1] << hi);
+    }
+    for (long long i = h + 8 * nw + lane; i < l; i += 32) d[i] = s[i];
 }
 
 }  // namespace
