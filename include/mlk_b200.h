@@ -338,12 +338,15 @@ int mlk_project(const double* f0, const double* stats, const double* qoi,
  * (lossless f64 bits), BuiltinCodec.decompress residual.py:81-98); apply
  * lambda with the stored QoIs and floor_ (lamq (total, 8) = [lam, qoi]);
  * exceptions (exc_slot[img] >= 0) copied from exc_img.  Output images are
- * written at the shard addresses of `out`. */
+ * written at the shard addresses of `out`; *neg (device, may be NULL) is
+ * OR-ed with 1 when a written value is < 0 (FDataset's check, fdata.py:70-
+ * 103, without a second pass over the output). */
 int mlk_decode(const MlkShard* shards, int32_t n_shards, int32_t total, const MlkGrid* grid_h,
                const float* W, int32_t L, const float* cents, int32_t K, const uint8_t* codes,
                const int32_t* res_slot, const uint64_t* res_codes, const double* res_eb,
                const uint8_t* res_mode, const double* lamq, const int32_t* exc_slot,
-               const double* exc_img, double floor_, double* out, cudaStream_t stream);
+               const double* exc_img, double floor_, double* out, int32_t* neg,
+               cudaStream_t stream);
 
 /* image_nrmse_batch(a, b) (qoi.py:107-119, exact) + per-image squared-error
  * sums, moments of a and b (compute_qoi_batch; qa/qb may be NULL) and

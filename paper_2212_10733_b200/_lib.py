@@ -121,7 +121,7 @@ _SIGS = {
     "mlk_ae_train": [_P, _P, _P, _P, _I32, _I32, _I32, _I32, _D, _D, _D, _D, _D, _D, _P, _I32, _P, _P, _P],
     "mlk_ae_train_config": [_P, _P],
     "mlk_decode": [_P, _I32, _I32, _P, _P, _I32, _P, _I32, _P, _P, _P, _P, _P, _P, _P, _P,
-                   _D, _P, _P],
+                   _D, _P, _P, _P],
 }
 
 _ERRORS = {-1: DimensionError, -2: ConfigError, -3: FormatError, -4: SizeMismatchError,

@@ -22,7 +22,7 @@ k_decode(const MlkShard* __restrict__ shards, int n_shards, int total, MlkGrid g
          const unsigned long long* __restrict__ res_codes, const double* __restrict__ res_eb,
          const unsigned char* __restrict__ res_mode, const double* __restrict__ lamq,
          const int* __restrict__ exc_slot, const double* __restrict__ exc_img, double floor_,
-         double* __restrict__ out) {
+         double* __restrict__ out, int* __restrict__ neg) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int img = blockIdx.x * DW + warp;
     if (img >= total) return;
@@ -33,7 +33,13 @@ k_decode(const MlkShard* __restrict__ shards, int n_shards, int total, MlkGrid g
     const int es = exc_slot[img];
     if (es >= 0) {
         const double* src = exc_img + (long long)es * D;
-        for (int j = lane; j < D; j += 32) y[j] = src[j];
+        bool anyneg = false;
+        for (int j = lane; j < D; j += 32) {
+            const double e = src[j];
+            anyneg |= e < 0.0;
+            y[j] = e;
+        }
+        if (neg && __any_sync(0xffffffffu, anyneg) && lane == 0) atomicOr(neg, 1);
         return;
     }
     double z[MLK_MAXL];
@@ -80,9 +86,11 @@ k_decode(const MlkShard* __restrict__ shards, int n_shards, int total, MlkGrid g
     }
     const double sc = amax > 0 ? amax : 1.0;
     const double fl = __dmul_rn(floor_, top);
+    bool anyneg = false;
     for (int j = lane; j < D; j += 32) {
         const double c = cell(j);
         if (!(top > 0)) {
+            anyneg |= c < 0.0;
             y[j] = c;
             continue;
         }
@@ -93,8 +101,11 @@ k_decode(const MlkShard* __restrict__ shards, int n_shards, int total, MlkGrid g
                                        __dmul_rn(l2, __ldg(g.ash + 2 * D + j))),
                              __dmul_rn(l3, a3));
         t = t < -700.0 ? -700.0 : (t > 700.0 ? 700.0 : t);
-        y[j] = __dmul_rn(np_max2(c, fl), mlk_exp(-t));
+        const double yv = __dmul_rn(np_max2(c, fl), mlk_exp(-t));
+        anyneg |= yv < 0.0;
+        y[j] = yv;
     }
+    if (neg && __any_sync(0xffffffffu, anyneg) && lane == 0) atomicOr(neg, 1);
 }
 
 }  // namespace
@@ -104,13 +115,13 @@ extern "C" int mlk_decode(const MlkShard* shards, int32_t n_shards, int32_t tota
                           int32_t K, const uint8_t* codes, const int32_t* res_slot,
                           const uint64_t* res_codes, const double* res_eb,
                           const uint8_t* res_mode, const double* lamq, const int32_t* exc_slot,
-                          const double* exc_img, double floor_, double* out,
+                          const double* exc_img, double floor_, double* out, int32_t* neg,
                           cudaStream_t stream) {
     if (total <= 0) return MLK_OK;
     k_decode<<<(total + DW - 1) / DW, 32 * DW, 0, stream>>>(shards, n_shards, total, *grid_h, W,
                                                             L, cents, K, codes, res_slot,
                                                             reinterpret_cast<const unsigned long long*>(res_codes),
                                                             res_eb, res_mode, lamq, exc_slot,
-                                                            exc_img, floor_, out);
+                                                            exc_img, floor_, out, neg);
     return cudaGetLastError() == cudaSuccess ? MLK_OK : MLK_ERR_CUDA;
 }

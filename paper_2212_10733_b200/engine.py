@@ -1236,6 +1236,7 @@ class DecodePlan:
     plane_lo: int = 0
     plane_hi: int = 0
     codes: object = None    # the unpacked codes of the last run_decode
+    neg: object = None      # device flag: the last run_decode wrote a value < 0
 
 
 def prepare_decode(archive, dev, sp=None) -> DecodePlan:
@@ -1485,11 +1486,18 @@ def run_decode(pl: DecodePlan, check: bool = True, out: torch.Tensor | None = No
              exc_img.view(torch.uint8), ex_dst)
     if out is None:
         out = torch.empty(pl.out_elems + 2, dtype=torch.float64, device=dev)
+    pl.neg = ws.tensor("dec_neg", (1,), torch.int32)
+    pl.neg.zero_()
     if total:
         call("mlk_decode", pl.sh_d, len(pl.specs), total, pl.dgrid.addr, pl.W, L, pl.cents,
              pl.K, codes, pl.res_slot, vals, res_eb_d, res_mode_d, lamq, pl.exc_slot, exc_img,
-             1e-12, out)
+             1e-12, out, pl.neg)
     return out
+
+
+def decoded_negative(pl: DecodePlan) -> bool:
+    """Whether the last run_decode of `pl` wrote a value < 0 (one int D2H)."""
+    return bool(int(pl.neg.item()))
 
 
 def decode_archive(archive, dev) -> DecodedArchive:
@@ -1505,13 +1513,14 @@ def decompress_device(archive, dev) -> np.ndarray:
     """Decode an archive on `dev`; returns the (P, N, R, C) array.  Raises
     ConfigError, like FDataset (fdata.py:70-103), if a value is negative --
     checked on the device, so the host never rescans the array."""
-    dec = decode_archive(archive, dev)
-    pre = dec.preamble
+    pl = prepare_decode(archive, dev)
+    out = run_decode(pl)
+    pre = pl.preamble
     g = pre.grid
-    vals = dec.out[:pre.n_planes * pre.n_nodes * g.rows * g.cols]
-    if bool((vals < 0).any()):
+    if decoded_negative(pl):
         raise ConfigError("histogram values must be non-negative")
-    return hostio.download_pinned_array(vals, (pre.n_planes, pre.n_nodes, g.rows, g.cols))
+    return hostio.download_pinned_array(out[:pre.n_planes * pre.n_nodes * g.rows * g.cols],
+                                        (pre.n_planes, pre.n_nodes, g.rows, g.cols))
 
 
 def shard_layout(shards, models, n_nodes, rows, cols, node_lo=0):

@@ -618,7 +618,7 @@ def decompress_distributed(archive: bytes, group=None, gather: bool = True,
     g = pre.grid
     nd = pre.n_nodes * g.rows * g.cols
     mine = out[:plan.out_elems]
-    if bool((mine < 0).any()):
+    if engine.decoded_negative(plan):
         raise ConfigError("histogram values must be non-negative")
     if out_path is not None:
         total = pre.n_planes * nd * 8

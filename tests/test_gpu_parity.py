@@ -494,6 +494,21 @@ def test_decompress_rejects_corrupt_archives():
     bad[off:off + 8] = (len(arc) + 5).to_bytes(8, "little")  # shard offset past the end
     with pytest.raises(FormatError):
         mb.decompress(bytes(bad))
+    # a negative value in an exception image: FDataset's check (fdata.py:70-103),
+    # raised from the decode kernel's flag
+    _, blobs = container.read_archive(arc)
+    shard_offs = struct.unpack_from(f"<{len(blobs)}Q", arc, off)
+    for si, b in enumerate(blobs):
+        sb = container.read_shard(b)
+        if struct.unpack_from("<I", sb.sections["exceptions"], 0)[0]:
+            exc_at = shard_offs[si] + len(b) - len(sb.sections["exceptions"])
+            neg = bytearray(arc)
+            neg[exc_at + 8:exc_at + 16] = struct.pack("<d", -1.0)  # first cell of entry 0
+            with pytest.raises(mb.ConfigError):
+                mb.decompress(bytes(neg))
+            break
+    else:
+        pytest.fail("the tiny archive has no exception to corrupt")
 
 
 def test_device_inflate_matches_host_zlib():

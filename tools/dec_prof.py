@@ -39,7 +39,7 @@ for rep in range(4):
     plan = engine.prepare_decode(arc, dev, sp); torch.cuda.synchronize(); t.append(time.perf_counter())
     out = engine.run_decode(plan); torch.cuda.synchronize(); t.append(time.perf_counter())
     mine = out[:plan.out_elems]
-    bad = bool((mine < 0).any()); t.append(time.perf_counter())
+    bad = engine.decoded_negative(plan); t.append(time.perf_counter())
     if rank == 0:
         fd = os.open(out_path, os.O_RDWR | os.O_CREAT, 0o644); os.ftruncate(fd, total); os.close(fd)
     if world > 1:
