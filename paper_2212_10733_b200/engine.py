@@ -813,11 +813,8 @@ def compress_device(f0: torch.Tensor, specs, dgrid: DeviceGrid, cfg, timer: Time
     exc_list = T("exc_list", (total,), i32)
     exc_cnt = T("exc_cnt", (S,), i32)
     call("mlk_list_flags", flags, sh_d, S, _lib.F_EXCEPTION, exc_list, exc_cnt)
-    if comm is None:
-        zlen_h, exc_h, errf_h, excl_h = _d2h(zlen[:max(1, n_sel)], exc_cnt, errf, exc_list)
-    else:
-        zlen_h, exc_h, errf_h = _d2h(zlen[:max(1, n_sel)], exc_cnt, errf)
-        excl_h = None
+    # (the exception lists too: callers write those entries from host f0)
+    zlen_h, exc_h, errf_h, excl_h = _d2h(zlen[:max(1, n_sel)], exc_cnt, errf, exc_list)
     zlen_h = zlen_h[:n_sel]
     bad = [int(errf_h[0]), int(np.any(zlen_h < 0))]
     ranks = None

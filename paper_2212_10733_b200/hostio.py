@@ -24,7 +24,9 @@ import numpy as np
 import torch
 
 __all__ = ["upload_planes", "upload_pieces", "upload_bytes", "download_bytes", "download_view",
-           "download_array", "download_pinned_array", "download_into", "download_to_file", "mapped_file", "release_maps", "pinned", "pinned_empty", "ArchiveWriter"]
+           "download_array", "download_pinned_array", "download_into", "download_ranges",
+           "download_to_file", "mapped_file", "release_maps", "pinned", "pinned_empty",
+           "ArchiveWriter"]
 
 CHUNK = 64 << 20
 UP_CHUNK = 2 << 20    # upload_pieces copy granularity
@@ -503,6 +505,18 @@ def download_view(src: torch.Tensor, nbytes: int) -> np.ndarray:
     if nbytes:
         stage[:nbytes].copy_(src[:nbytes], non_blocking=True)
         torch.cuda.current_stream(src.device).synchronize()
+    return stage.numpy()[:nbytes]
+
+
+def download_ranges(src: torch.Tensor, nbytes: int, ranges) -> np.ndarray:
+    """download_view of a device uint8 tensor restricted to `ranges` [(a, b),
+    ...]: only those bytes are copied (to the same offsets of the pinned
+    view; the rest of it is stale)."""
+    stage = pinned(f"down{src.device.index}", nbytes)
+    for a, b in ranges:
+        if b > a:
+            stage[a:b].copy_(src[a:b], non_blocking=True)
+    torch.cuda.current_stream(src.device).synchronize()
     return stage.numpy()[:nbytes]
 
 

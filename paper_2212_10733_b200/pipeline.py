@@ -457,7 +457,26 @@ def compress_distributed(ds: FDataset, config: PipelineConfig, state: TimestepSt
     offs = np.asarray(archive_offsets(len(head), [int(x) for x in sizes]), dtype=np.int64)
     if out_path is not None:
         nbytes = max([o + n for o, _, n in out.segments], default=0)
-        body = hostio.download_view(out.blob_buf, nbytes)
+        # this rank's exception entries are its input's own histograms: they
+        # are written into the file from the host f0, only the rest of its
+        # pieces comes back over PCIe
+        D = ds.grid.rows * ds.grid.cols
+        row = 4 + 8 * D
+        shards = partition(ds.n_planes, ds.n_nodes, config.shards, config.mode)
+        holes = []  # (buffer offset, entries, member indices, shard)
+        if HOST_EXCEPTIONS and out.exceptions is not None:
+            for (off, members), sh in zip(out.exceptions, shards):
+                if members.size:
+                    holes.append((off, members.size * row, members, sh))
+        holes.sort(key=lambda h: h[0])
+        keep, at = [], 0  # buffer ranges that are not exception entries
+        for off, ln, _, _ in holes:
+            if off > at:
+                keep.append((at, off))
+            at = max(at, off + ln)
+        if nbytes > at:
+            keep.append((at, nbytes))
+        body = hostio.download_ranges(out.blob_buf, nbytes, keep)
         if sp.rank == 0:
             # rewrite in place (no truncate-to-zero: an existing archive file's
             # pages are reused instead of re-allocated)
@@ -478,15 +497,47 @@ def compress_distributed(ds: FDataset, config: PipelineConfig, state: TimestepSt
             total = int(offs[-1] + sizes[-1])
             dst = hostio.mapped_file(fd, total)
             base = int(offs[0])
+
+            def to_file(o):  # buffer offset -> file offset (segments are disjoint)
+                for lo, goff, n in out.segments:
+                    if lo <= o < lo + n:
+                        return base + goff + (o - lo)
+                raise AssertionError("buffer offset outside every segment")
+
             spans = []
             for lo, goff, n in out.segments:
-                spans += [(lo + a, base + goff + a, min(n, a + (8 << 20)) - a)
-                          for a in range(0, n, 8 << 20)]
+                for ka, kb in keep:
+                    a0, b0 = max(lo, ka), min(lo + n, kb)
+                    spans += [(c, base + goff + (c - lo), min(b0, c + (8 << 20)) - c)
+                              for c in range(a0, b0, 8 << 20)]
 
             def put(x):
                 dst[x[1]:x[1] + x[2]] = body[x[0]:x[0] + x[2]]
 
-            list(hostio._pool().map(put, spans))
+            jobs = [hostio._pool().submit(put, x) for x in spans]
+            src = np.ascontiguousarray(ds.data)
+            from ._lib import lib
+            per = max(1, (8 << 20) // row)
+            for off, ln, members, sh in holes:
+                (p0, _), (x0, x1) = sh.planes_range, sh.nodes_range
+                bn = x1 - x0
+                elem = np.ascontiguousarray(((p0 + members // bn) * ds.n_nodes + x0
+                                             + members % bn) * D, dtype=np.int64)
+                idx = np.ascontiguousarray(members, dtype=np.uint32)
+                fo = to_file(off)
+
+                def fill(a, fo=fo, elem=elem, idx=idx):
+                    k = min(idx.size, a + per) - a
+                    if lib().mlk_host_exception_entries(
+                            ctypes.c_void_p(dst[fo + a * row:].ctypes.data),
+                            ctypes.c_void_p(src.ctypes.data),
+                            ctypes.c_void_p(elem[a:].ctypes.data),
+                            ctypes.c_void_p(idx[a:].ctypes.data), k, D) != 0:
+                        raise RuntimeError("mlk_host_exception_entries failed")
+
+                jobs += [hostio._pool().submit(fill, a) for a in range(0, idx.size, per)]
+            for j in jobs:
+                j.result()
             del dst
         finally:
             os.close(fd)
