@@ -366,7 +366,10 @@ __device__ void newton_block(const double* fp, double fl, const MlkGrid& g, cons
                 const double* ebp = C.eb[ce];
                 double G1 = 0.0, G2 = 0.0, H1 = 0.0, H2 = 0.0, H3 = 0.0;
                 auto row = [&](int r, double w, double ea) {
-                    const double wf = w * (fmax(fp[r * cols + c], fl) * ea * ebp[r]);
+                    // f_plus = max(f, fl) as a compare-select (fl is finite
+                    // here and a NaN f maps to fl, as with fmax)
+                    const double f = fp[r * cols + c];
+                    const double wf = w * ((f > fl ? f : fl) * ea * ebp[r]);
                     const double p2 = C.p2r[r];
                     const double w2f = w * wf, t2 = p2 * w2f;
                     G1 += wf;
