@@ -106,6 +106,18 @@ def test_kmeans_large_matches_oracle(n):
 
 @gpu
 @needs_cuda
+def test_kmeans_cluster_path_with_256_centroids():
+    """pq_bits = 8 (K = 256) on the cluster path (>= 4096 members)."""
+    from oracle import port
+    rng = np.random.default_rng(256)
+    v = np.concatenate([rng.normal(0, 1, 12000), rng.normal(6, 0.3, 6000),
+                        np.round(rng.normal(-4, 2, 2500) * 4) / 4])
+    for seed in (0, 3):
+        assert np.array_equal(mb.kmeans_1d(v, 256, seed), port.kmeans(v, 256, seed)), seed
+
+
+@gpu
+@needs_cuda
 def test_kmeans_deterministic_and_quality():
     rng = np.random.default_rng(12)
     v = np.concatenate([rng.normal(0, 1, 80), rng.normal(8, 0.5, 60), rng.normal(-5, 2, 60)])
