@@ -392,10 +392,11 @@ def rooflines(out, stage_ms, n, dev, traffic_ok=True):
     rows = [
         ("k_stage1", "encode", n * (HIST_BYTES + 96), 1,
          "reads every histogram once (TMA) + 96 B of latents/stats/moments"),
-        ("k_project", "project_sel_launch", n_sel * (HIST_BYTES + 185) + vlen, None,
-         "the residual-image launch (its CUDA-event span on its own stream): reads each "
-         "selected histogram + per-image outputs + varint streams; the residual-free launch "
-         "runs under the search on the side stream (stage_ms.project_non_launch)"),
+        ("k_project", "project_launches", n * (HIST_BYTES + 185) + vlen, 2,
+         "both launches (residual-free on the side stream under the search, residual images "
+         "on the high-priority stream), each over its CUDA-event span on its own stream: "
+         "every histogram read again + per-image outputs + varint streams; FP64-bound, see "
+         "'fp64'"),
         ("k_deflate_warp", "deflate", vlen + zlen, 14,
          "varint bytes in + zlib bytes out; serial LZ77/Huffman per stream (latency-bound)"),
         ("k_probe", "eb_search", None, None, "re-reads selected histograms per round; L2/latency"),
@@ -406,6 +407,9 @@ def rooflines(out, stage_ms, n, dev, traffic_ok=True):
         # DEFLATE's own span: its launch to the join of its tier streams (the
         # stage itself also waits for the side stream's projection)
         ms = stage_ms.get("deflate_done") if stage == "deflate" else None
+        if stage == "project_launches":
+            spans = [stage_ms.get(k) for k in ("project_sel_launch", "project_non_launch")]
+            ms = sum(x for x in spans if x) or None
         ms = ms if ms is not None else stage_ms.get(stage)
         if ms is None:
             continue
@@ -416,6 +420,7 @@ def rooflines(out, stage_ms, n, dev, traffic_ok=True):
                      algorithmic_bytes_per_step=int(nbytes),
                      traffic=_traffic(kern, launches) if launches and traffic_ok else None)
         table.append(e)
+    # the dominant kernel: the most time on its own stream(s) per step
     dom = max((e for e in table if "achieved" in e), key=lambda e: e["ms_per_step"])
     roofline = {"bound": "hbm", "kernel": dom["kernel"], "achieved": dom["achieved"],
                 "peak": peak, "unit": "GB/s", "frac": dom["frac"], "traffic": dom["traffic"],
