@@ -15,7 +15,6 @@ from __future__ import annotations
 import ctypes
 import functools
 import os
-import math
 import struct
 import time
 from dataclasses import dataclass, field

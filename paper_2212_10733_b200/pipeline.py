@@ -27,8 +27,7 @@ from .autoencoder import AEModel
 from .container import ArchivePreamble, archive_offsets
 from .decomp import (SelectionScheme, mix_seed, partition, select_training,
                      shard_dataset_index)
-from .errors import (ConfigError, DegenerateRangeError, DimensionError, FormatError,
-                     SizeMismatchError)
+from .errors import ConfigError, DegenerateRangeError, DimensionError
 from .fdata import FDataset, dataset_nbytes
 from .lagrange import NewtonOptions
 from .qoi import ErrorReport, compression_ratio, qoi_nrmse_from_moments
