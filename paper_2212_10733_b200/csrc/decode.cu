@@ -85,6 +85,7 @@ k_decode(const MlkShard* __restrict__ shards, int n_shards, int total, MlkGrid g
         amax = np_max2(amax, __shfl_xor_sync(0xffffffffu, amax, o));
     }
     const double sc = amax > 0 ? amax : 1.0;
+    const double rsc = __drcp_rn(sc);  // a3 = x / sc exactly via div_by_recip
     const double fl = __dmul_rn(floor_, top);
     bool anyneg = false;
     for (int j = lane; j < D; j += 32) {
@@ -95,7 +96,7 @@ k_decode(const MlkShard* __restrict__ shards, int n_shards, int total, MlkGrid g
             continue;
         }
         const double dv = __dsub_rn(g.vpar[j], u);
-        const double a3 = __ddiv_rn(__dmul_rn(g.hmvol[j], __dmul_rn(dv, dv)), sc);
+        const double a3 = div_by_recip(__dmul_rn(g.hmvol[j], __dmul_rn(dv, dv)), sc, rsc);
         double t = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(l0, __ldg(g.ash + j)),
                                                  __dmul_rn(l1, __ldg(g.ash + D + j))),
                                        __dmul_rn(l2, __ldg(g.ash + 2 * D + j))),
