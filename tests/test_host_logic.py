@@ -113,3 +113,32 @@ def test_archive_bound_covers_every_fixture_archive():
                                    config_digest=cfg.digest()).pack()
             bound = pipeline._archive_bound(ds, cfg, cfg.shards, len(head))
             assert run["archive_len"] <= bound, (path.name, run["archive_len"], bound)
+
+
+def test_mapped_file_cache_follows_inode_and_size(tmp_path):
+    """hostio.mapped_file: one cached shared mapping per (inode, size); a
+    rewrite through it lands in the file, a size change maps afresh, and
+    release_maps drops every mapping."""
+    import os
+
+    from paper_2212_10733_b200 import hostio
+    path = tmp_path / "out.bin"
+    fd = os.open(path, os.O_RDWR | os.O_CREAT, 0o644)
+    try:
+        os.ftruncate(fd, 4096)
+        v = hostio.mapped_file(fd, 4096)
+        v[:4] = np.frombuffer(b"abcd", np.uint8)
+        assert hostio.mapped_file(fd, 4096).ctypes.data == v.ctypes.data  # cached
+        del v
+        os.ftruncate(fd, 8192)
+        w = hostio.mapped_file(fd, 8192)
+        assert len(w) == 8192 and bytes(w[:4]) == b"abcd"
+        del w
+        st = os.fstat(fd)
+        assert [k for k in hostio._MAPS if k[:2] == (st.st_dev, st.st_ino)] == [
+            (st.st_dev, st.st_ino, 8192)]
+    finally:
+        os.close(fd)
+        hostio.release_maps()
+    assert hostio._MAPS == {}
+    assert path.read_bytes()[:4] == b"abcd"
