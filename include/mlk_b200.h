@@ -293,7 +293,10 @@ int mlk_compact(const uint8_t* flags, const double* stats, const MlkShard* shard
  * shard s misses tau at node i.  Launches queue on one stream, so walking
  * the tree needs no host round trip.  The launch visits positions
  * act_start[s] .. act_start[s] + (act_off[s+1] - act_off[s]) of shard s's
- * range-ordered selection (smallest ranges fail first). */
+ * range-ordered selection (smallest ranges fail first).  recon (may be
+ * NULL): the reconstructions mlk_probe_bins stored, read instead of decoding
+ * the latent codes again (sel_count then required: row = the shard's
+ * selection base + pos). */
 int mlk_probe(const double* f0, const double* stats, const MlkShard* shards,
               int32_t n_shards, const MlkGrid* grid_h, const float* W, int32_t L,
               const float* cents, int32_t K, const uint8_t* codes,
@@ -301,17 +304,20 @@ int mlk_probe(const double* f0, const double* stats, const MlkShard* shards,
               int32_t n_work,
               const double* recon_bound, double tau, const double* cand, int32_t n_nodes,
               int32_t level, int32_t span, int32_t* fail, const double* bins,
-              const double* eb_hi, cudaStream_t stream);
+              const double* eb_hi, const int32_t* sel_count, const double* recon,
+              cudaStream_t stream);
 
 /* Residual-magnitude profile of every selected image (34 counts + 34 sums of
  * r^2 over log2 bins anchored at eb_hi[s]) at bins[(img_off + pos) * 68],
  * pos = the image's place in the range-ordered selection; mlk_probe uses it
- * (bins may be NULL) to certify passes without re-reading the image. */
+ * (bins may be NULL) to certify passes without re-reading the image.
+ * recon (may be NULL; n_sel * D doubles): each selected image's decoder
+ * reconstruction at row sum(sel_count[0..s-1]) + pos, for mlk_probe. */
 int mlk_probe_bins(const double* f0, const MlkShard* shards, int32_t n_shards,
                    const MlkGrid* grid_h, const float* W, int32_t L, const float* cents,
                    int32_t K, const uint8_t* codes, const int32_t* sel_by_range,
                    const int32_t* sel_count, int32_t n_sel, const double* eb_hi, double* bins,
-                   cudaStream_t stream);
+                   double* recon, cudaStream_t stream);
 
 /* Stage 4 encode + stage 5 (pipeline.py:239-292): residual q / zigzag /
  * varint for selected images into varint + (slot_base[s] + sel_rank) *

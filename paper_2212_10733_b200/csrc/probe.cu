@@ -50,12 +50,13 @@ k_probe_bins(const double* __restrict__ f0, const MlkShard* __restrict__ shards,
              const float* __restrict__ W, int L, const float* __restrict__ cents, int K,
              const unsigned char* __restrict__ codes, const int* __restrict__ sel_by_range,
              const int* __restrict__ sel_count, int n_shards, const double* __restrict__ eb_hi,
-             double* __restrict__ bins) {
+             double* __restrict__ bins, double* __restrict__ recon) {
     __shared__ double ssum[PW_WARPS][PB_NB][32];
     __shared__ unsigned short scnt[PW_WARPS][PB_NB][32];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int D = g.D;
-    int gw = blockIdx.x * PW_WARPS + warp;
+    const int row = blockIdx.x * PW_WARPS + warp;  // = sel_base[s] + pos
+    int gw = row;
     int s = 0;
     while (s < n_shards && gw >= sel_count[s]) gw -= sel_count[s++];
     if (s >= n_shards) return;
@@ -80,9 +81,11 @@ k_probe_bins(const double* __restrict__ f0, const MlkShard* __restrict__ shards,
                      : 0.0;
     const float* Ws = W + sh.w_off;
     const bool blas_tree = !sh.small_blas;
+    double* rrow = recon ? recon + (long long)row * D : nullptr;
     #pragma unroll 2  // two cells' loads in flight per lane
     for (int q = lane; q < D; q += 32) {
         const double rc = decode_cell(z, Ws, L, D, q, blas_tree && g.tree_cols[q], sh.mean, sh.std);
+        if (rrow) __stcg(rrow + q, rc);  // the probes' copy: read again from L2/HBM
         const double r = __dsub_rn(x[q], rc);
         const double ar = fabs(r);
         int bin;
@@ -134,8 +137,11 @@ __device__ __forceinline__ void pb_bounds(const double* pb, int e0, double eb, d
 
 
 // PB_MAXC candidates per image: 3 (span <= 2) or 7 (span 3: a node, its
-// children and grandchildren), each with its own register budget
-template <int PB_MAXC>
+// children and grandchildren), each with its own register budget.  RC: the
+// reconstructions k_probe_bins stored (recon[(sel_base[s] + pos) * D]) are
+// read instead of re-decoding every cell from the latent codes -- the same
+// doubles, so every comparison below is unchanged.
+template <int PB_MAXC, bool RC>
 __global__ void __launch_bounds__(32 * PW_WARPS, PB_MAXC == 3 ? 6 : 3)
 k_probe_level(const double* __restrict__ f0, const double* __restrict__ stats,
               const MlkShard* __restrict__ shards, MlkGrid g, PwPlan pw,
@@ -144,14 +150,18 @@ k_probe_level(const double* __restrict__ f0, const double* __restrict__ stats,
               const int* __restrict__ act_off, const int* __restrict__ act_start, int n_shards,
               const double* __restrict__ recon_bound, double tau,
               const double* __restrict__ cand, int n_nodes, int level, int span, int* fail,
-              const double* __restrict__ bins, const double* __restrict__ eb_hi) {
+              const double* __restrict__ bins, const double* __restrict__ eb_hi,
+              const int* __restrict__ sel_count, const double* __restrict__ recon) {
     __shared__ double sh_leaf[PW_WARPS][MLK_PW_MAX_LEAVES];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int D = g.D;
     const int gw = blockIdx.x * PW_WARPS + warp;
     if (gw >= act_off[n_shards]) return;
-    int s = 0;
-    while (act_off[s + 1] <= gw) ++s;
+    int s = 0, base = 0;
+    while (act_off[s + 1] <= gw) {
+        if (RC) base += sel_count[s];
+        ++s;
+    }
     int* fl = fail + (long long)s * n_nodes;
     int node = 1;
     for (int l = 0; l < level; ++l) node = 2 * node + (fl[node] ? 1 : 0);
@@ -216,18 +226,26 @@ k_probe_level(const double* __restrict__ f0, const double* __restrict__ stats,
     // the whole image on its way to L2 at once: the lanes' loads below then
     // wait for L2, not for one DRAM round trip per step
     if (lane == 0) prefetch_l2_histogram(x, D);
+    const double* rcx = RC ? recon + (long long)(base + pos) * D : nullptr;
+    if (RC && lane == 1) prefetch_l2_histogram(rcx, D);
     double z[MLK_MAXL];
+    if (!RC) {
 #pragma unroll
-    for (int k = 0; k < MLK_MAXL; ++k)
-        z[k] = k < L ? (double)cents[((long long)s * L + k) * K + codes[(long long)img * L + k]]
-                     : 0.0;
+        for (int k = 0; k < MLK_MAXL; ++k)
+            z[k] = k < L ? (double)cents[((long long)s * L + k) * K + codes[(long long)img * L + k]]
+                         : 0.0;
+    }
     const float* Ws = W + sh.w_off;
     const bool blas_tree = !sh.small_blas;
+    auto recon_at = [&](int q) {
+        return RC ? rcx[q]
+                  : decode_cell(z, Ws, L, D, q, blas_tree && g.tree_cols[q], sh.mean, sh.std);
+    };
     // approximate SSEs (any order), exact only near the threshold
     #pragma unroll 2  // two cells' loads in flight per lane
     for (int q = lane; q < D; q += 32) {
         const double o = x[q];
-        const double rc = decode_cell(z, Ws, L, D, q, blas_tree && g.tree_cols[q], sh.mean, sh.std);
+        const double rc = recon_at(q);
         const double r = __dsub_rn(o, rc);
 #pragma unroll
         for (int c = 0; c < PB_MAXC; ++c) {
@@ -256,8 +274,7 @@ k_probe_level(const double* __restrict__ f0, const double* __restrict__ stats,
                 leaf[l] = pw_leaf(
                     [&](int q) {
                         const double o = x[q];
-                        const double rc = decode_cell(z, Ws, L, D, q,
-                                                      blas_tree && g.tree_cols[q], sh.mean, sh.std);
+                        const double rc = recon_at(q);
                         const double r = __dsub_rn(o, rc);
                         const double d =
                             __dsub_rn(o, __dadd_rn(rc, __dmul_rn(rint(__ddiv_rn(r, e2)), e2)));
@@ -293,15 +310,19 @@ extern "C" int mlk_probe(const double* f0, const double* stats, const MlkShard* 
                          const int32_t* act_start, int32_t n_work,
                          const double* recon_bound, double tau, const double* cand,
                          int32_t n_nodes, int32_t level, int32_t span, int32_t* fail,
-                         const double* bins, const double* eb_hi, cudaStream_t stream) {
+                         const double* bins, const double* eb_hi, const int32_t* sel_count,
+                         const double* recon, cudaStream_t stream) {
     if (n_work <= 0) return MLK_OK;
-    if (n_nodes < 2 || level < 0 || span < 1 || span > 3 || (1 << level) >= n_nodes)
+    if (n_nodes < 2 || level < 0 || span < 1 || span > 3 || (1 << level) >= n_nodes ||
+        (recon && !sel_count))
         return MLK_ERR_CONFIG;
     PwPlan pw = mlk_make_pw_plan(grid_h->D);
-    auto kern = span > 2 ? k_probe_level<7> : k_probe_level<3>;
+    auto kern = recon ? (span > 2 ? k_probe_level<7, true> : k_probe_level<3, true>)
+                      : (span > 2 ? k_probe_level<7, false> : k_probe_level<3, false>);
     kern<<<(n_work + PW_WARPS - 1) / PW_WARPS, 32 * PW_WARPS, 0, stream>>>(
         f0, stats, shards, *grid_h, pw, W, L, cents, K, codes, sel_by_range, act_off, act_start,
-        n_shards, recon_bound, tau, cand, n_nodes, level, span, fail, bins, eb_hi);
+        n_shards, recon_bound, tau, cand, n_nodes, level, span, fail, bins, eb_hi, sel_count,
+        recon);
     return cudaGetLastError() == cudaSuccess ? MLK_OK : MLK_ERR_CUDA;
 }
 
@@ -309,10 +330,10 @@ extern "C" int mlk_probe_bins(const double* f0, const MlkShard* shards, int32_t 
                               const MlkGrid* grid_h, const float* W, int32_t L, const float* cents,
                               int32_t K, const uint8_t* codes, const int32_t* sel_by_range,
                               const int32_t* sel_count, int32_t n_sel, const double* eb_hi,
-                              double* bins, cudaStream_t stream) {
+                              double* bins, double* recon, cudaStream_t stream) {
     if (n_sel <= 0) return MLK_OK;
     k_probe_bins<<<(n_sel + PW_WARPS - 1) / PW_WARPS, 32 * PW_WARPS, 0, stream>>>(
         f0, shards, *grid_h, W, L, cents, K, codes, sel_by_range, sel_count, n_shards, eb_hi,
-        bins);
+        bins, recon);
     return cudaGetLastError() == cudaSuccess ? MLK_OK : MLK_ERR_CUDA;
 }

@@ -31,6 +31,7 @@ SPAN = 2.0 ** -20
 STEPS = 20
 LOOKAHEAD = int(os.environ.get("MLK_LOOKAHEAD", 8))  # levels per host round trip
 PASS_LEVELS = int(os.environ.get("MLK_PASS_LEVELS", 2))  # levels per probe launch
+PROBE_RECON = os.environ.get("MLK_PROBE_RECON", "1") != "0"  # probes read stored reconstructions
 EB_TRACE = None  # a list: the search appends (event, host time) per round (diagnostics)
 _PAYLOAD_HEAD = struct.Struct("<BHHd")
 
@@ -704,8 +705,10 @@ def compress_device(f0: torch.Tensor, specs, dgrid: DeviceGrid, cfg, timer: Time
             states.append(_Search("hi", eb_hi_s))
     n_sel_all = int(cnt_h.sum())
     bins = T("probe_bins", (max(1, total) * 68,), f64)
+    # the selected images' reconstructions, stored once for the probes
+    recon = T("probe_recon", (max(1, n_sel_all) * D,), f64) if PROBE_RECON else None
     call("mlk_probe_bins", f0, sh_d, S, dgrid.addr, W, L, cents, K, codes, sel_rng, sel_cnt,
-         n_sel_all, eb_hi, bins)
+         n_sel_all, eb_hi, bins, recon)
     n_nodes = 1 << LOOKAHEAD
     rounds = 0
     fail = T("fail", (S, n_nodes), i32)
@@ -749,7 +752,8 @@ def compress_device(f0: torch.Tensor, specs, dgrid: DeviceGrid, cfg, timer: Time
         for level in range(0, LOOKAHEAD, PASS_LEVELS):  # several levels per pass
             call("mlk_probe", f0, stats, sh_d, S, dgrid.addr, W, L, cents, K, codes, sel_rng,
                  off_d, zero_start, int(off[-1]), rbound, cfg.tau, cand_d, n_nodes, level,
-                 min(PASS_LEVELS, LOOKAHEAD - level), fail, bins, eb_hi)
+                 min(PASS_LEVELS, LOOKAHEAD - level), fail, bins, eb_hi,
+                 sel_cnt if recon is not None else None, recon)
         if tr:
             tr(("launched", time.perf_counter()))
         if comm is not None:

@@ -84,11 +84,14 @@ def _check_lambdas(got: bytes, want: bytes, precision: str):
         np.testing.assert_allclose(g[:, :4], w[:, :4], rtol=1e-7, atol=1e-13)
 
 
-@pytest.mark.parametrize("newton", ["separable", "per-cell"])
+@pytest.mark.parametrize("newton", ["separable", "per-cell", "probe-decodes"])
 @pytest.mark.parametrize("name", CASES)
 def test_compress_matches_reference(name, newton, monkeypatch):
+    """(probe-decodes: the search probes decode the latent codes again
+    instead of reading k_probe_bins' stored reconstructions)"""
     from paper_2212_10733_b200 import engine
-    monkeypatch.setattr(engine, "SEPARABLE_NEWTON", newton == "separable")
+    monkeypatch.setattr(engine, "SEPARABLE_NEWTON", newton != "per-cell")
+    monkeypatch.setattr(engine, "PROBE_RECON", newton != "probe-decodes")
     meta, a = G.load(name)
     ds, same = G.corpus(name)
     if not same:
