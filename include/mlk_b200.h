@@ -295,8 +295,7 @@ int mlk_compact(const uint8_t* flags, const double* stats, const MlkShard* shard
  * act_start[s] .. act_start[s] + (act_off[s+1] - act_off[s]) of shard s's
  * range-ordered selection (smallest ranges fail first).  recon (may be
  * NULL): the reconstructions mlk_probe_bins stored, read instead of decoding
- * the latent codes again (sel_count then required: row = the shard's
- * selection base + pos). */
+ * the latent codes again (sel_count and sel_rank then required). */
 int mlk_probe(const double* f0, const double* stats, const MlkShard* shards,
               int32_t n_shards, const MlkGrid* grid_h, const float* W, int32_t L,
               const float* cents, int32_t K, const uint8_t* codes,
@@ -304,20 +303,22 @@ int mlk_probe(const double* f0, const double* stats, const MlkShard* shards,
               int32_t n_work,
               const double* recon_bound, double tau, const double* cand, int32_t n_nodes,
               int32_t level, int32_t span, int32_t* fail, const double* bins,
-              const double* eb_hi, const int32_t* sel_count, const double* recon,
-              cudaStream_t stream);
+              const double* eb_hi, const int32_t* sel_count, const int32_t* sel_rank,
+              const double* recon, cudaStream_t stream);
 
 /* Residual-magnitude profile of every selected image (34 counts + 34 sums of
  * r^2 over log2 bins anchored at eb_hi[s]) at bins[(img_off + pos) * 68],
  * pos = the image's place in the range-ordered selection; mlk_probe uses it
  * (bins may be NULL) to certify passes without re-reading the image.
- * recon (may be NULL; n_sel * D doubles): each selected image's decoder
- * reconstruction at row sum(sel_count[0..s-1]) + pos, for mlk_probe. */
+ * recon (may be NULL; n_sel rows of (D + 1) & ~1 doubles): each selected
+ * image's decoder reconstruction at row sum(sel_count[0..s-1]) +
+ * sel_rank[img] (= the projection's residual slot), for mlk_probe and
+ * mlk_project. */
 int mlk_probe_bins(const double* f0, const MlkShard* shards, int32_t n_shards,
                    const MlkGrid* grid_h, const float* W, int32_t L, const float* cents,
                    int32_t K, const uint8_t* codes, const int32_t* sel_by_range,
                    const int32_t* sel_count, int32_t n_sel, const double* eb_hi, double* bins,
-                   double* recon, cudaStream_t stream);
+                   const int32_t* sel_rank, double* recon, cudaStream_t stream);
 
 /* Stage 4 encode + stage 5 (pipeline.py:239-292): residual q / zigzag /
  * varint for selected images into varint + (slot_base[s] + sel_rank) *
@@ -328,7 +329,9 @@ int mlk_probe_bins(const double* f0, const MlkShard* shards, int32_t n_shards,
  * errors).  *err_flag = MLK_ERR_CONFIG when |q| >= 2**62 (residual.py:67).
  * img_list (device, n_list entries) restricts the launch to those images
  * (NULL: all `total`), so the images without residuals can be projected
- * while the error-bound search of the others is still running. */
+ * while the error-bound search of the others is still running.  recon (may
+ * be NULL; needs slot_base): mlk_probe_bins' stored reconstructions, read
+ * (one bulk copy per image) for the selected images instead of decoding. */
 int mlk_project(const double* f0, const double* stats, const double* qoi,
                 const MlkShard* shards, int32_t n_shards, int32_t total, const MlkGrid* grid_h,
                 const float* W, int32_t L, const float* cents, int32_t K, const uint8_t* codes,
@@ -336,7 +339,7 @@ int mlk_project(const double* f0, const double* stats, const double* qoi,
                 uint8_t* flags, double* lam, double* qst, int32_t* status, int32_t* iters,
                 double* ferr, double* fqoi, double* fsse, uint8_t* varint, int64_t varint_cap,
                 int64_t* varint_len, int32_t* err_flag, const int32_t* img_list,
-                int32_t n_list, cudaStream_t stream);
+                int32_t n_list, const double* recon, cudaStream_t stream);
 
 /* Decode path (pipeline.py:397-427) for all images of all shards: recon from
  * codes; + residual (res_slot[img] >= 0: D zigzag codes at res_codes +

@@ -100,11 +100,11 @@ _SIGS = {
     "mlk_host_unregister": [_P],
     "mlk_host_exception_entries": [_P, _P, _P, _P, _I64, _I32],
     "mlk_probe": [_P, _P, _P, _I32, _P, _P, _I32, _P, _I32, _P, _P, _P, _P, _I32, _P, _D, _P,
-                  _I32, _I32, _I32, _P, _P, _P, _P, _P, _P],
+                  _I32, _I32, _I32, _P, _P, _P, _P, _P, _P, _P],
     "mlk_probe_bins": [_P, _P, _I32, _P, _P, _I32, _P, _I32, _P, _P, _P, _I32, _P, _P, _P,
-                       _P],
+                       _P, _P],
     "mlk_project": [_P, _P, _P, _P, _I32, _I32, _P, _P, _I32, _P, _I32, _P, _P, _P, _P, _P,
-                    _P, _P, _P, _P, _P, _P, _P, _P, _I64, _P, _P, _P, _I32, _P],
+                    _P, _P, _P, _P, _P, _P, _P, _P, _I64, _P, _P, _P, _I32, _P, _P],
     "mlk_split_flags": [_P, _I32, ctypes.c_uint32, _P, _P, _P, _P],
     "mlk_list_flags": [_P, _P, _I32, ctypes.c_uint32, _P, _P, _P],
     "mlk_pack_residuals": [_P, _P, _P, _P, _P, _P, _P, _P, _I32, _I32, _I32, _P, _P],

@@ -226,6 +226,17 @@ __device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned
                  "r"(bytes)
                  : "memory");
 }
+// row stride (doubles) of the stored selected-image reconstructions
+// (mlk_probe_bins -> mlk_probe, mlk_project): even, so every row is 16-byte
+// aligned for a bulk copy
+__host__ __device__ constexpr int recon_stride(int D) { return (D + 1) & ~1; }
+
+// raise the barrier's expected transaction bytes without arriving
+__device__ __forceinline__ void mbar_expect_tx_only(unsigned long long* bar, unsigned bytes) {
+    asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes,
                                          unsigned long long* bar) {
     asm volatile(

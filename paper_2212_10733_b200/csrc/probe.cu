@@ -50,13 +50,13 @@ k_probe_bins(const double* __restrict__ f0, const MlkShard* __restrict__ shards,
              const float* __restrict__ W, int L, const float* __restrict__ cents, int K,
              const unsigned char* __restrict__ codes, const int* __restrict__ sel_by_range,
              const int* __restrict__ sel_count, int n_shards, const double* __restrict__ eb_hi,
-             double* __restrict__ bins, double* __restrict__ recon) {
+             double* __restrict__ bins, const int* __restrict__ sel_rank,
+             double* __restrict__ recon) {
     __shared__ double ssum[PW_WARPS][PB_NB][32];
     __shared__ unsigned short scnt[PW_WARPS][PB_NB][32];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int D = g.D;
-    const int row = blockIdx.x * PW_WARPS + warp;  // = sel_base[s] + pos
-    int gw = row;
+    int gw = blockIdx.x * PW_WARPS + warp;  // = sel_base[s] + pos
     int s = 0;
     while (s < n_shards && gw >= sel_count[s]) gw -= sel_count[s++];
     if (s >= n_shards) return;
@@ -64,6 +64,7 @@ k_probe_bins(const double* __restrict__ f0, const MlkShard* __restrict__ shards,
     const int pos = gw;
     const int j = sel_by_range[sh.img_off + pos];
     const int img = sh.img_off + j;
+    const int base = blockIdx.x * PW_WARPS + warp - pos;
     double (*bs)[32] = ssum[warp];
     unsigned short (*bc)[32] = scnt[warp];
 #pragma unroll
@@ -81,7 +82,7 @@ k_probe_bins(const double* __restrict__ f0, const MlkShard* __restrict__ shards,
                      : 0.0;
     const float* Ws = W + sh.w_off;
     const bool blas_tree = !sh.small_blas;
-    double* rrow = recon ? recon + (long long)row * D : nullptr;
+    double* rrow = recon ? recon + (long long)(base + sel_rank[img]) * recon_stride(D) : nullptr;
     #pragma unroll 2  // two cells' loads in flight per lane
     for (int q = lane; q < D; q += 32) {
         const double rc = decode_cell(z, Ws, L, D, q, blas_tree && g.tree_cols[q], sh.mean, sh.std);
@@ -151,7 +152,8 @@ k_probe_level(const double* __restrict__ f0, const double* __restrict__ stats,
               const double* __restrict__ recon_bound, double tau,
               const double* __restrict__ cand, int n_nodes, int level, int span, int* fail,
               const double* __restrict__ bins, const double* __restrict__ eb_hi,
-              const int* __restrict__ sel_count, const double* __restrict__ recon) {
+              const int* __restrict__ sel_count, const int* __restrict__ sel_rank,
+              const double* __restrict__ recon) {
     __shared__ double sh_leaf[PW_WARPS][MLK_PW_MAX_LEAVES];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int D = g.D;
@@ -226,7 +228,7 @@ k_probe_level(const double* __restrict__ f0, const double* __restrict__ stats,
     // the whole image on its way to L2 at once: the lanes' loads below then
     // wait for L2, not for one DRAM round trip per step
     if (lane == 0) prefetch_l2_histogram(x, D);
-    const double* rcx = RC ? recon + (long long)(base + pos) * D : nullptr;
+    const double* rcx = RC ? recon + (long long)(base + sel_rank[img]) * recon_stride(D) : nullptr;
     if (RC && lane == 1) prefetch_l2_histogram(rcx, D);
     double z[MLK_MAXL];
     if (!RC) {
@@ -311,10 +313,10 @@ extern "C" int mlk_probe(const double* f0, const double* stats, const MlkShard* 
                          const double* recon_bound, double tau, const double* cand,
                          int32_t n_nodes, int32_t level, int32_t span, int32_t* fail,
                          const double* bins, const double* eb_hi, const int32_t* sel_count,
-                         const double* recon, cudaStream_t stream) {
+                         const int32_t* sel_rank, const double* recon, cudaStream_t stream) {
     if (n_work <= 0) return MLK_OK;
     if (n_nodes < 2 || level < 0 || span < 1 || span > 3 || (1 << level) >= n_nodes ||
-        (recon && !sel_count))
+        (recon && (!sel_count || !sel_rank)))
         return MLK_ERR_CONFIG;
     PwPlan pw = mlk_make_pw_plan(grid_h->D);
     auto kern = recon ? (span > 2 ? k_probe_level<7, true> : k_probe_level<3, true>)
@@ -322,7 +324,7 @@ extern "C" int mlk_probe(const double* f0, const double* stats, const MlkShard* 
     kern<<<(n_work + PW_WARPS - 1) / PW_WARPS, 32 * PW_WARPS, 0, stream>>>(
         f0, stats, shards, *grid_h, pw, W, L, cents, K, codes, sel_by_range, act_off, act_start,
         n_shards, recon_bound, tau, cand, n_nodes, level, span, fail, bins, eb_hi, sel_count,
-        recon);
+        sel_rank, recon);
     return cudaGetLastError() == cudaSuccess ? MLK_OK : MLK_ERR_CUDA;
 }
 
@@ -330,10 +332,12 @@ extern "C" int mlk_probe_bins(const double* f0, const MlkShard* shards, int32_t 
                               const MlkGrid* grid_h, const float* W, int32_t L, const float* cents,
                               int32_t K, const uint8_t* codes, const int32_t* sel_by_range,
                               const int32_t* sel_count, int32_t n_sel, const double* eb_hi,
-                              double* bins, double* recon, cudaStream_t stream) {
+                              double* bins, const int32_t* sel_rank, double* recon,
+                              cudaStream_t stream) {
     if (n_sel <= 0) return MLK_OK;
+    if (recon && !sel_rank) return MLK_ERR_CONFIG;
     k_probe_bins<<<(n_sel + PW_WARPS - 1) / PW_WARPS, 32 * PW_WARPS, 0, stream>>>(
         f0, shards, *grid_h, W, L, cents, K, codes, sel_by_range, sel_count, n_shards, eb_hi,
-        bins, recon);
+        bins, sel_rank, recon);
     return cudaGetLastError() == cudaSuccess ? MLK_OK : MLK_ERR_CUDA;
 }

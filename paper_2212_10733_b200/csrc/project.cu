@@ -475,7 +475,8 @@ k_project(const double* __restrict__ f0, const double* __restrict__ stats,
           int* __restrict__ status_out, int* __restrict__ iters_out,
           double* __restrict__ ferr_out, double* __restrict__ fqoi_out,
           double* __restrict__ fsse_out, unsigned char* __restrict__ varint, long long vcap,
-          long long* __restrict__ vlen, int* __restrict__ err_flag, const int* __restrict__ img_list) {
+          long long* __restrict__ vlen, int* __restrict__ err_flag, const int* __restrict__ img_list,
+          const double* __restrict__ recon) {
     __shared__ PjCtl C;
     __shared__ unsigned long long bar;
     extern __shared__ __align__(16) double sm[];
@@ -488,27 +489,40 @@ k_project(const double* __restrict__ f0, const double* __restrict__ stats,
     const double* x = shard_image(f0, sh, img - sh.img_off, D);
     double* Ob = sm;                     // TMA target: the original, later d^2
     double* F = sm + ((D + 3) / 2) * 2;  // recon -> corrected -> f_plus -> final
+    const int rank = sel_rank[img];
+    // a selected image's reconstruction as mlk_probe_bins stored it (the
+    // same doubles decode_cell gives), else decoded here
+    const double* rrow =
+        recon && rank >= 0 ? recon + (long long)(slot_base[s] + rank) * recon_stride(D) : nullptr;
 
-    // ---- one bulk copy of the original; the AE decode overlaps it
+    // ---- one bulk copy of the original (+ the stored reconstruction); the
+    //      AE decode overlaps it
     if (tid == 0) mbar_init(&bar, 1);
     __syncthreads();
     int shift;
     if (warp == 0) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        if (rrow && lane == 0) {
+            const unsigned fb = (unsigned)recon_stride(D) * 8u;
+            mbar_expect_tx_only(&bar, fb);
+            bulk_g2s(F, rrow, fb, &bar);
+        }
         shift = stage_histogram(Ob, x, D, &bar);
     } else {
         shift = (int)((reinterpret_cast<unsigned long long>(x) & 15ull) >> 3);
     }
     double* O = Ob + shift;
-    double z[MLK_MAXL];
+    if (!rrow) {
+        double z[MLK_MAXL];
 #pragma unroll
-    for (int k = 0; k < MLK_MAXL; ++k)
-        z[k] = k < L ? (double)cents[((long long)s * L + k) * K + codes[(long long)img * L + k]]
-                     : 0.0;
-    const float* Ws = W + sh.w_off;
-    const bool blas_tree = !sh.small_blas;
-    for (int j = tid; j < D; j += PJ_T)
-        F[j] = decode_cell(z, Ws, L, D, j, blas_tree && g.tree_cols[j], sh.mean, sh.std);
+        for (int k = 0; k < MLK_MAXL; ++k)
+            z[k] = k < L ? (double)cents[((long long)s * L + k) * K + codes[(long long)img * L + k]]
+                         : 0.0;
+        const float* Ws = W + sh.w_off;
+        const bool blas_tree = !sh.small_blas;
+        for (int j = tid; j < D; j += PJ_T)
+            F[j] = decode_cell(z, Ws, L, D, j, blas_tree && g.tree_cols[j], sh.mean, sh.std);
+    }
     // per-grid / per-image column and row tables of the separable Newton
     const double4 q4 = reinterpret_cast<const double4*>(qoi)[img];
     double qs[4] = {q4.x, q4.y, q4.z, q4.w};
@@ -532,7 +546,6 @@ k_project(const double* __restrict__ f0, const double* __restrict__ stats,
 
     // ---- residual stage for selected images (contiguous cells per thread so
     //      the varint stream is written in cell order after one block scan)
-    const int rank = sel_rank[img];
     if (rank >= 0) {  // block-uniform
         const double eb2 = 2.0 * sh.eb;
         const double inv = 1.0 / eb2;
@@ -843,13 +856,15 @@ extern "C" int mlk_project(const double* f0, const double* stats, const double* 
                            double* lam, double* qst, int32_t* status, int32_t* iters,
                            double* ferr, double* fqoi, double* fsse, uint8_t* varint,
                            int64_t varint_cap, int64_t* varint_len, int32_t* err_flag,
-                           const int32_t* img_list, int32_t n_list, cudaStream_t stream) {
+                           const int32_t* img_list, int32_t n_list, const double* recon,
+                           cudaStream_t stream) {
     const int n_work = img_list ? n_list : total;
     if (total <= 0 || n_work <= 0) return MLK_OK;
     const int D = grid_h->D;
     if (D > MLK_MAX_D || L < 1 || L > MLK_MAXL) return MLK_ERR_DIM;
     PwPlan pw = mlk_make_pw_plan(D);
-    const size_t sm = (size_t)(((D + 3) / 2) * 2 + D) * sizeof(double);
+    if (recon && !slot_base) return MLK_ERR_CONFIG;
+    const size_t sm = (size_t)(((D + 3) / 2) * 2 + recon_stride(D)) * sizeof(double);
     const bool sep = grid_h->sep && grid_h->rows <= 64 && grid_h->cols <= 64 && grid_h->cols > 0;
     const MlkNewton opt = *opts_h;
 #define MLK_PJ_LAUNCH(SEP)                                                                     \
@@ -857,7 +872,7 @@ extern "C" int mlk_project(const double* f0, const double* stats, const double* 
     k_project<SEP><<<n_work, PJ_T, sm, stream>>>(                                               \
         f0, stats, qoi, shards, n_shards, *grid_h, pw, W, L, cents, K, codes, sel_rank,         \
         slot_base, opt, flags, lam, qst, status, iters, ferr, fqoi, fsse, varint,               \
-        (long long)varint_cap, reinterpret_cast<long long*>(varint_len), err_flag, img_list)
+        (long long)varint_cap, reinterpret_cast<long long*>(varint_len), err_flag, img_list, recon)
     if (sep) {
         MLK_PJ_LAUNCH(true);
     } else {

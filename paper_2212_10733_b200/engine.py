@@ -29,7 +29,7 @@ from .errors import ConfigError, FormatError, SizeMismatchError
 
 SPAN = 2.0 ** -20
 STEPS = 20
-LOOKAHEAD = int(os.environ.get("MLK_LOOKAHEAD", 8))  # levels per host round trip
+LOOKAHEAD = int(os.environ.get("MLK_LOOKAHEAD", 12))  # levels per host round trip
 PASS_LEVELS = int(os.environ.get("MLK_PASS_LEVELS", 2))  # levels per probe launch
 PROBE_RECON = os.environ.get("MLK_PROBE_RECON", "1") != "0"  # probes read stored reconstructions
 EB_TRACE = None  # a list: the search appends (event, host time) per round (diagnostics)
@@ -677,7 +677,7 @@ def compress_device(f0: torch.Tensor, specs, dgrid: DeviceGrid, cfg, timer: Time
     sp_non = timer.span_start(side)
     call("mlk_project", f0, stats, qoi, sh_d, S, total, dgrid.addr, W, L, cents, K, codes,
          sel_rank, None, ctypes.addressof(opts), flags, lam, qst, status, iters, ferr, fqoi,
-         fsse, varint, vcap, vlen, errf, list_non, total - n_sel, stream=side.cuda_stream)
+         fsse, varint, vcap, vlen, errf, list_non, total - n_sel, None, stream=side.cuda_stream)
     timer.span_end("project_non_launch", side, sp_non)
     ev_non = torch.cuda.Event()
     ev_non.record(side)
@@ -706,9 +706,10 @@ def compress_device(f0: torch.Tensor, specs, dgrid: DeviceGrid, cfg, timer: Time
     n_sel_all = int(cnt_h.sum())
     bins = T("probe_bins", (max(1, total) * 68,), f64)
     # the selected images' reconstructions, stored once for the probes
-    recon = T("probe_recon", (max(1, n_sel_all) * D,), f64) if PROBE_RECON else None
+    recon = (T("probe_recon", (max(1, n_sel_all) * ((D + 1) & ~1),), f64) if PROBE_RECON
+             else None)
     call("mlk_probe_bins", f0, sh_d, S, dgrid.addr, W, L, cents, K, codes, sel_rng, sel_cnt,
-         n_sel_all, eb_hi, bins, recon)
+         n_sel_all, eb_hi, bins, sel_rank, recon)
     n_nodes = 1 << LOOKAHEAD
     rounds = 0
     fail = T("fail", (S, n_nodes), i32)
@@ -753,7 +754,7 @@ def compress_device(f0: torch.Tensor, specs, dgrid: DeviceGrid, cfg, timer: Time
             call("mlk_probe", f0, stats, sh_d, S, dgrid.addr, W, L, cents, K, codes, sel_rng,
                  off_d, zero_start, int(off[-1]), rbound, cfg.tau, cand_d, n_nodes, level,
                  min(PASS_LEVELS, LOOKAHEAD - level), fail, bins, eb_hi,
-                 sel_cnt if recon is not None else None, recon)
+                 sel_cnt if recon is not None else None, sel_rank, recon)
         if tr:
             tr(("launched", time.perf_counter()))
         if comm is not None:
@@ -800,7 +801,7 @@ def compress_device(f0: torch.Tensor, specs, dgrid: DeviceGrid, cfg, timer: Time
         sp_sel = timer.span_start(torch.cuda.current_stream(dev))
         call("mlk_project", f0, stats, qoi, sh_d, S, total, dgrid.addr, W, L, cents, K, codes,
              sel_rank, slot_base, ctypes.addressof(opts), flags, lam, qst, status, iters, ferr,
-             fqoi, fsse, varint, vcap, vlen, errf, list_sel, n_sel)
+             fqoi, fsse, varint, vcap, vlen, errf, list_sel, n_sel, recon)
         timer.span_end("project_sel_launch", torch.cuda.current_stream(dev), sp_sel)
     if hi_ctx is not None:
         hi_ctx.__exit__(None, None, None)
