@@ -817,15 +817,37 @@ def compress_device(f0: torch.Tensor, specs, dgrid: DeviceGrid, cfg, timer: Time
     exc_list = T("exc_list", (total,), i32)
     exc_cnt = T("exc_cnt", (S,), i32)
     call("mlk_list_flags", flags, sh_d, S, _lib.F_EXCEPTION, exc_list, exc_cnt)
+    # while DEFLATE runs: the host copies of what the pack stage stages that
+    # does not depend on the compressed sizes (weights sections, entry shards,
+    # each shard's entry range)
+    own0 = comm is None or comm.sp.rank == 0
+    ws.begin()
+    wraw = [sp.model.to_bytes() for sp in specs] if own0 else []
+    w_d = ws.stage(np.frombuffer(b"".join(wraw), dtype=np.uint8)) if own0 else None
+    ent_shard = ws.stage(np.repeat(np.arange(S, dtype=np.int32), cnt_h))
+    e_lo = slot_base_h.astype(np.int64)
+    rng_d = ws.stage(np.concatenate([e_lo, e_lo + cnt_h]))
+    ws.flush()
+    # entry bytes (21-byte header + zlib body) prefix-summed on the device:
+    # the host reads back only each shard's total and the smallest length
+    zinc = T("zinc", (n_sel + 1,), i64)
+    zsm = T("zsmall", (S + 1,), i64)
+    zinc[:1].zero_()
+    if n_sel:
+        torch.cumsum(zlen[:n_sel] + 21, 0, out=zinc[1:])
+        torch.sub(zinc.index_select(0, rng_d[S:]), zinc.index_select(0, rng_d[:S]), out=zsm[:S])
+        zsm[S:].copy_(zlen[:n_sel].amin().view(1))
+    else:
+        zsm.zero_()
     # (the exception lists too: callers write those entries from host f0)
-    zlen_h, exc_h, errf_h, excl_h = _d2h(zlen[:max(1, n_sel)], exc_cnt, errf, exc_list)
-    zlen_h = zlen_h[:n_sel]
-    bad = [int(errf_h[0]), int(np.any(zlen_h < 0))]
+    zsm_h, exc_h, errf_h, excl_h = _d2h(zsm, exc_cnt, errf, exc_list)
+    if tr:
+        tr(("zlen_synced", time.perf_counter()))
+    res_h = zsm_h[:S].astype(np.int64)
+    bad = [int(errf_h[0]), int(n_sel > 0 and zsm_h[S] < 0)]
     ranks = None
     if comm is not None:
         # every rank's section sizes: where its pieces go in each shard blob
-        res_h = np.array([int(np.sum(21 + zlen_h[a:b])) for a, b in
-                          zip(slot_base_h, slot_base_h + cnt_h)], dtype=np.int64)
         mine = np.concatenate([[sp.n_img for sp in specs], cnt_h, res_h, exc_h, bad]).astype(
             np.int64)
         allr = comm.all_gather(torch.from_numpy(mine).to(dev)).cpu().numpy()
@@ -838,16 +860,18 @@ def compress_device(f0: torch.Tensor, specs, dgrid: DeviceGrid, cfg, timer: Time
         raise ConfigError("residual stream exceeds the device DEFLATE limits")
 
     timer.mark("pack")
-    lay = blob_layout(specs, cfg, D, cnt_h, zlen_h, exc_h, ranks)
+    lay = blob_layout(specs, cfg, D, cnt_h, None, exc_h, ranks, res_h=res_h)
+    if tr:
+        tr(("layout", time.perf_counter()))
     buf = T("blob", (max(1, lay["total"]),), torch.uint8)
-    # fixed pieces (rank 0 of a split): 44-byte header + weights section,
-    # residual / exception section prefixes
+    # fixed pieces (rank 0 of a split): 44-byte header, residual / exception
+    # section prefixes; the weights sections from the copy staged above
     pieces, src, ln, dst = [], [], [], []
     pos = 0
     for s, sp in enumerate(specs):
         if lay["hdr_off"][s] < 0:
             continue
-        for off, raw in ((lay["hdr_off"][s], lay["header"][s] + sp.model.to_bytes()),
+        for off, raw in ((lay["hdr_off"][s], lay["header"][s]),
                          (lay["res_pre_off"][s], struct.pack("<dI", eb[s], int(cntg_h[s]))),
                          (lay["exc_pre_off"][s], struct.pack("<I", int(lay["exc_total"][s])))):
             pieces.append(raw)
@@ -865,14 +889,21 @@ def compress_device(f0: torch.Tensor, specs, dgrid: DeviceGrid, cfg, timer: Time
         pq_src = ws.stage(np.asarray([4 * L * K * s for s in pq_s], dtype=np.int64))
         pq_len = ws.stage(np.full(len(pq_s), 4 * L * K, dtype=np.int64))
         pq_off = ws.stage(lay["pq_off"][pq_s])
-    ent_shard = ws.stage(np.repeat(np.arange(S, dtype=np.int32), cnt_h))
-    entry_off = ws.stage(lay["entry_off"])
+        w_len = np.array([len(w) for w in wraw], dtype=np.int64)
+        w_src = ws.stage(np.concatenate([[0], np.cumsum(w_len)[:-1]]).astype(np.int64))
+        w_ln = ws.stage(w_len)
+        w_dst = ws.stage(lay["hdr_off"] + 44)
+    # each entry's buffer offset: its shard's first entry + the prefix sum
+    ent_base = ws.stage(lay["ent_off"] - np.concatenate([[0], np.cumsum(res_h)[:-1]]))
     lam_off = ws.stage(lay["lam_off"])
     exc_base = ws.stage(np.concatenate([[0], np.cumsum(exc_h)]).astype(np.int32))
     exc_off = ws.stage(lay["exc_base"])
     ws.flush()
+    if tr:
+        tr(("pack_staged", time.perf_counter()))
     if pieces:
         call("mlk_gather_segments", stage, src_d, ln_d, len(pieces), buf, dst_d)
+        call("mlk_gather_segments", w_d, w_src, w_ln, S, buf, w_dst)
         call("mlk_gather_segments", cents.view(torch.uint8).reshape(-1), pq_src, pq_len,
              len(pq_s), buf, pq_off)
     # codes: pack_indices straight into the blob (each piece starts on a byte)
@@ -887,12 +918,16 @@ def compress_device(f0: torch.Tensor, specs, dgrid: DeviceGrid, cfg, timer: Time
         call("mlk_pack_indices", c16[off * L:(off + sp.n_img) * L], sp.n_img * L, cfg.pq_bits,
              base + int(lay["codes_off"][s]), bad_d)
     if n_sel:
+        entry_off = T("entry_off", (n_sel,), i64)
+        torch.add(zinc[:n_sel], ent_base.index_select(0, ent_shard), out=entry_off)
         call("mlk_pack_residuals", sel, sh_d, ent_shard, entry_off, zoff, zlen, zout, slot_base,
              dgrid.struct.rows, dgrid.struct.cols, n_sel, buf)
     call("mlk_pack_lambdas", lam, qst, sh_d, S, total, lam_off,
          int(cfg.lambda_precision == "f32"), buf)
     call("mlk_pack_exceptions", f0, sh_d, S, exc_list, exc_base, exc_off, int(exc_h.sum()), D,
          buf)
+    if tr:
+        tr(("pack_launched", time.perf_counter()))
     out = CompressOut(specs=specs, blob_buf=buf, blob_lens=lay["blob_len"],
                       dev=dict(codes=codes, cents=cents, flags=flags, lam=lam, qst=qst,
                                status=status, iters=iters, ferr=ferr, fqoi=fqoi, fsse=fsse,
@@ -910,7 +945,7 @@ def compress_device(f0: torch.Tensor, specs, dgrid: DeviceGrid, cfg, timer: Time
     return out
 
 
-def blob_layout(specs, cfg, D, cnt_h, zlen_h, exc_h, ranks=None):
+def blob_layout(specs, cfg, D, cnt_h, zlen_h, exc_h, ranks=None, res_h=None):
     """Byte layout of every shard blob (container.py:30-95, pipeline.py:116-184)
     and of the pieces of it this rank writes.
 
@@ -921,16 +956,24 @@ def blob_layout(specs, cfg, D, cnt_h, zlen_h, exc_h, ranks=None):
     residual-entry and exception sections (rank 0 also the header, weights,
     PQ table and section prefixes).  Pieces are laid out in the rank's buffer
     in blob order; `segments` maps (buffer offset, blob-region offset, length).
-    With one rank the buffer IS the blob region (a single segment)."""
+    With one rank the buffer IS the blob region (a single segment).
+
+    zlen_h (zlib body length per residual entry) gives `entry_off`, every
+    entry's buffer offset; zlen_h=None with res_h (this rank's entry bytes per
+    shard, 21 + body each) skips it -- the caller derives the offsets from
+    `ent_off` (each shard's first entry) and its own prefix sums."""
     from .container import ShardHeader, SCHEME_FULL
     L, bits, K = cfg.latent_dim, cfg.pq_bits, 2 ** cfg.pq_bits
     lb = 4 if cfg.lambda_precision == "f32" else 8
     S = len(specs)
     cnt = np.asarray(cnt_h, dtype=np.int64)
     e_start = np.concatenate([[0], np.cumsum(cnt)[:-1]]).astype(np.int64)
-    # entry bytes (21-byte entry header + zlib body), prefix-summed once
-    zcs = np.concatenate([[0], np.cumsum(21 + np.asarray(zlen_h, dtype=np.int64))])
-    zl_sum = zcs[e_start + cnt] - zcs[e_start]
+    if zlen_h is not None:
+        # entry bytes (21-byte entry header + zlib body), prefix-summed once
+        zcs = np.concatenate([[0], np.cumsum(21 + np.asarray(zlen_h, dtype=np.int64))])
+        zl_sum = zcs[e_start + cnt] - zcs[e_start]
+    else:
+        zl_sum = np.asarray(res_h, dtype=np.int64)
     if ranks is None:
         ranks = dict(rank=0, n=np.array([[sp.n_img for sp in specs]], dtype=np.int64),
                      cnt=cnt[None], res=zl_sum[None], exc=np.asarray(exc_h, np.int64)[None])
@@ -944,11 +987,11 @@ def blob_layout(specs, cfg, D, cnt_h, zlen_h, exc_h, ranks=None):
     exc_tot, exc_pre, exc_own = (exc_all.sum(0).tolist(), exc_all[:r].sum(0).tolist(),
                                  exc_all[r].tolist())
     cnt_l, e_start_l = cnt.tolist(), e_start.tolist()
-    keys = ("blob_off", "blob_len", "hdr_off", "codes_off", "pq_off", "res_pre_off", "lam_off",
-            "exc_pre_off", "exc_base", "exc_total")
+    keys = ("blob_off", "blob_len", "hdr_off", "codes_off", "pq_off", "res_pre_off", "ent_off",
+            "lam_off", "exc_pre_off", "exc_base", "exc_total")
     lay = {k: np.full(S, -1, dtype=np.int64) for k in keys}
     lay["header"] = []
-    entry_off = np.zeros(len(zlen_h), dtype=np.int64)
+    entry_off = np.zeros(len(zlen_h), dtype=np.int64) if zlen_h is not None else None
     segs = []
     cur = [0]
 
@@ -988,8 +1031,9 @@ def blob_layout(specs, cfg, D, cnt_h, zlen_h, exc_h, ranks=None):
             lay["pq_off"][s] = put(g_pq, sec[2])
             lay["res_pre_off"][s] = put(g_res, 12)
         ent = put(g_res + 12 + res_pre[s], res_own[s])
+        lay["ent_off"][s] = ent
         c, e0 = cnt_l[s], e_start_l[s]
-        if c:
+        if c and entry_off is not None:
             entry_off[e0:e0 + c] = ent + (zcs[e0:e0 + c] - zcs[e0])
         lay["lam_off"][s] = put(g_lam + a * 8 * lb, m * 8 * lb)
         if own0:

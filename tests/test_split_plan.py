@@ -91,6 +91,18 @@ def test_split_pieces_tile_the_single_process_blobs(small_blobs, world):
         ranks = None if world == 1 else dict(rank=r, n=n_all, cnt=cnt_all, res=res_all,
                                                exc=exc_all)
         lay = engine.blob_layout(specs, cfg, D, cnt_all[r], zlen, exc_all[r], ranks)
+        # the engine's form: per-shard entry bytes, entry offsets from ent_off
+        # + the prefix sums of the entries (done on the device there)
+        lay2 = engine.blob_layout(specs, cfg, D, cnt_all[r], None, exc_all[r], ranks,
+                                  res_h=res_all[r])
+        for k in lay:
+            if k not in ("entry_off", "header", "segments"):
+                np.testing.assert_array_equal(lay2[k], lay[k], err_msg=k)
+        assert lay2["header"] == lay["header"] and lay2["segments"] == lay["segments"]
+        zinc = np.concatenate([[0], np.cumsum(zlen + 21)])
+        ent_shard = np.repeat(np.arange(S), cnt_all[r])
+        base = lay2["ent_off"] - np.concatenate([[0], np.cumsum(res_all[r])[:-1]])
+        np.testing.assert_array_equal(zinc[:-1] + base[ent_shard], lay["entry_off"])
         buf = bytearray(lay["total"])
         e0 = 0
         for s in range(S):

@@ -30,12 +30,14 @@ for rep in range(3):
     engine.EB_TRACE = []
     timer = engine.Timer(True)
     engine.compress_device(f0, works, dgrid, cfg, timer, comm=comm)
+    engine.EB_TRACE.append(("returned", time.perf_counter()))
     torch.cuda.synchronize()
+    engine.EB_TRACE.append(("gpu_done", time.perf_counter()))
     tr = engine.EB_TRACE
     engine.EB_TRACE = None
     t0 = tr[0][1]
     line = " ".join(f"{k}+{1e3 * (t - t0):.2f}" for k, t in tr)
-    st = {k: round(1e3 * v, 2) for k, v in timer.result().items() if k in ("eb_search", "newton")}
+    st = {k: round(1e3 * v, 2) for k, v in timer.result().items() if k in ("eb_search", "newton", "deflate", "pack")}
     print(f"rank {rank} rep {rep}: {line}  {st}", flush=True)
 if world > 1:
     dist.destroy_process_group()
