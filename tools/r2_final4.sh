@@ -11,5 +11,5 @@ for N in 2 4; do
     --master-port $((29500 + N)) bench.py --gpus $N --steps 5 --warmup 3 > $O/bench_$N.log 2>&1
   echo "rc=$?" >> $O/bench_$N.log
 done
-MLK_LOOKAHEAD=12 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 \
-  --master-port 29555 bench.py --gpus 4 --steps 5 --warmup 3 --no-cpu-baseline > $O/bench_4_la12.log 2>&1
+MLK_LOOKAHEAD=8 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 \
+  --master-port 29555 bench.py --gpus 4 --steps 5 --warmup 3 --no-cpu-baseline > $O/bench_4_la8.log 2>&1
