@@ -340,6 +340,12 @@ __device__ __forceinline__ void prefetch_l2_histogram(const double* x, int D) {
                  : "memory");
 }
 
+// the IEEE quotient out of line: a fallback taken by a few lanes in a
+// million must not be if-converted into every iteration of the caller's loop
+// (inlined, nvcc evaluates the division's reciprocal/refinement sequence
+// speculatively on every path and only branches for its own slow case)
+static __device__ __noinline__ double ddiv_cold(double a, double b) { return __ddiv_rn(a, b); }
+
 // rint(r / eb2) without a division per cell: y = r * (1 / eb2) is within a
 // few ulps of the quotient, so its nearest integer is the quotient's unless
 // y sits within that error of a .5 tie -- then divide exactly.
@@ -347,7 +353,7 @@ __device__ __forceinline__ double qround(double r, double eb2, double inv) {
     const double y = r * inv;
     const double fy = y - floor(y);
     if (fabs(y) >= 2251799813685248.0 || fabs(fy - 0.5) <= 8.9e-16 * fabs(y) + 1e-300)
-        return rint(__ddiv_rn(r, eb2));
+        return rint(ddiv_cold(r, eb2));
     return rint(y);
 }
 
@@ -362,5 +368,5 @@ __device__ __forceinline__ double div_by_recip(double a, double b, double y) {
     const double q2 = __fma_rn(r, y, q);
     const unsigned hi = (unsigned)__double2hiint(q2) & 0x7fffffffu;
     if (hi - 0x01700000u < 0x7CF00000u) return q2;  // biased exponent 23 .. 2021
-    return __ddiv_rn(a, b);
+    return ddiv_cold(a, b);
 }
