@@ -153,9 +153,18 @@ struct Bits {
     unsigned long long bb;
     int nb;
     __device__ void fill() {
-        while (nb <= 56 && pos < n) {
-            bb |= (unsigned long long)in[pos++] << nb;
-            nb += 8;
+        // up to 4 bytes per step from the aligned word holding in[pos] (never
+        // past that word; bytes at or beyond n are masked off)
+        while (nb <= 32 && pos < n) {
+            const uintptr_t a = reinterpret_cast<uintptr_t>(in + pos);
+            const int sh = (int)(a & 3u);
+            int k = 4 - sh;
+            if (n - pos < k) k = (int)(n - pos);
+            unsigned w = *reinterpret_cast<const unsigned*>(a - sh) >> (8 * sh);
+            if (k < 4) w &= (1u << (8 * k)) - 1u;
+            bb |= (unsigned long long)w << nb;
+            nb += 8 * k;
+            pos += k;
         }
     }
     __device__ int take(int k, bool& err) {  // k <= 32
@@ -341,7 +350,16 @@ k_inflate_warp(const uint8_t* __restrict__ in, const long long* __restrict__ in_
                     if (err || dist > o) { rc = -1; break; }
                     if (o + len > cap) { rc = -2; break; }
                     __syncwarp();
-                    for (int i = lane; i < len; i += 32) dst[o + i] = dst[o - dist + i % dist];
+                    {  // i % dist stepped, not divided: one remainder per copy at most
+                        const int d = (int)dist;
+                        const int s32 = d > 32 ? 32 : 32 % d;
+                        int m = lane < d ? lane : lane % d;
+                        for (int i = lane; i < len; i += 32) {
+                            dst[o + i] = dst[o - d + m];
+                            m += s32;
+                            if (m >= d) m -= d;
+                        }
+                    }
                     __syncwarp();
                     o += len;
                 }
