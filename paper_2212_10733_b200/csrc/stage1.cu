@@ -194,12 +194,18 @@ k_stage1(const double* __restrict__ f0, const MlkShard* __restrict__ shards, int
                     if (p > np_ - 1) p = np_ - 1;
                 }
             }
+            // (the current panel's start kept in a register: read from shared
+            // memory only when the panel changes)
+            int pb = p > 0 ? pstart[p] : -1;
             for (int t = 0; t < (D + 31) / 32; ++t) {  // warp-uniform trip count
                 const int j = D - 1 - lane - 32 * t;
                 double xn = 0.0;
                 if (j >= 0) {
                     xn = div_by_recip(__dsub_rn(buf[j], sh.mean), sh.std, rstd);
-                    if (p > 0 && j < pstart[p]) --p;
+                    if (j < pb) {
+                        --p;
+                        pb = p > 0 ? pstart[p] : -1;
+                    }
                 }
                 __syncwarp();
                 if (j >= 0) buf[j + p] = xn;
