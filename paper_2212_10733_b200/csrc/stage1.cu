@@ -39,7 +39,7 @@ __device__ __forceinline__ int block_shard(const MlkShard* sh, int n_shards, int
 __global__ void __launch_bounds__(32 * S1_WARPS)
 k_stage1(const double* __restrict__ f0, const MlkShard* __restrict__ shards, int n_shards,
          int total, MlkGrid g, const float* __restrict__ W, int L, double* __restrict__ lat,
-         double* __restrict__ stats, double* __restrict__ qoi) {
+         double* __restrict__ stats, double* __restrict__ qoi, int use_tab) {
     extern __shared__ __align__(16) double smem[];
     __shared__ unsigned long long bars[S1_WARPS];
     __shared__ double gvp[64], gvq[64];  // separable grids: v_par by column, v_perp^2 by row
@@ -62,9 +62,21 @@ k_stage1(const double* __restrict__ f0, const MlkShard* __restrict__ shards, int
     for (int i = threadIdx.x; i < L * D; i += blockDim.x) Wsm[i] = __ldg(Wg + i);
     const bool sep = g.sep && g.rows <= 64 && g.cols <= 64;
     if (threadIdx.x < 4) svcls[threadIdx.x] = g.vcls[threadIdx.x];
+    // separable grids with room for it: every cell's (row, column, volume
+    // class) packed once per CTA -- the cell order a lane visits is the same
+    // for every image
+    unsigned* ctab = reinterpret_cast<unsigned*>(smem + wdoubles + S1_WARPS * per_warp);
+    const bool tab = sep && use_tab;
     if (sep) {
         for (int i = threadIdx.x; i < g.cols; i += blockDim.x) gvp[i] = g.vpar[i];
         for (int i = threadIdx.x; i < g.rows; i += blockDim.x) gvq[i] = g.vperp2[i * g.cols];
+        if (tab) {
+            for (int j = threadIdx.x; j < D; j += blockDim.x) {
+                const int r = j / g.cols, c = j - r * g.cols;
+                const int re = (r == 0) | (r == g.rows - 1), ce = (c == 0) | (c == g.cols - 1);
+                ctab[j] = (unsigned)r | ((unsigned)c << 8) | ((unsigned)(2 * re + ce) << 16);
+            }
+        }
     }
     int np_ = 0;
     for (int j0 = 0; j0 < D; j0 += panel_len(D - j0)) {
@@ -101,7 +113,21 @@ k_stage1(const double* __restrict__ f0, const MlkShard* __restrict__ shards, int
         // ---- pass A: extrema, sums, first moments from the staged copy
         double mx = -INFINITY, mn = INFINITY, so = 0.0, soo = 0.0, n0 = 0.0, n1 = 0.0, n2 = 0.0;
         bool has_nan = false;  // numpy's max/min propagate NaN
-        if (sep) {  // grid values from the (row, column) tables
+        if (tab) {  // grid values from the (row, column) tables, cell classes packed
+            for (int j = lane; j < D; j += 32) {
+                const double v = buf[j];
+                const unsigned e = ctab[j];
+                has_nan |= v != v;
+                mx = v > mx ? v : mx;
+                mn = v < mn ? v : mn;
+                so += v;
+                soo = fma(v, v, soo);
+                const double fv = v * svcls[e >> 16];
+                n0 += fv;
+                n1 = fma(fv, gvp[(e >> 8) & 0xffu], n1);
+                n2 = fma(fv, gvq[e & 0xffu], n2);
+            }
+        } else if (sep) {  // grid values from the (row, column) tables
             const int rows = g.rows, cols = g.cols;
             int r = lane / cols, c = lane - (lane / cols) * cols;
             const int dr = 32 / cols, dc = 32 - (32 / cols) * cols;
@@ -151,7 +177,13 @@ k_stage1(const double* __restrict__ f0, const MlkShard* __restrict__ shards, int
         double u = n1 / n0;
         double tp = hm * n2 / n0;
         double n3 = 0.0;
-        if (sep) {
+        if (tab) {
+            for (int j = lane; j < D; j += 32) {
+                const unsigned e = ctab[j];
+                const double dv = gvp[(e >> 8) & 0xffu] - u;
+                n3 = fma(buf[j] * svcls[e >> 16], dv * dv, n3);
+            }
+        } else if (sep) {
             const int rows = g.rows, cols = g.cols;
             int r = lane / cols, c = lane - (lane / cols) * cols;
             const int dr = 32 / cols, dc = 32 - (32 / cols) * cols;
@@ -269,10 +301,14 @@ extern "C" int mlk_stage1(const double* f0, const MlkShard* shards, int32_t n_sh
     size_t sm = (size_t)(((L * D + 3) / 4) * 2) * sizeof(double) +
                 (size_t)S1_WARPS * (((D + 3) / 2) * 2 + 16 + 96) * sizeof(double);
     if (sm > 227 * 1024) return MLK_ERR_DIM;
+    // + the packed cell-class table when it fits
+    const size_t sm_tab = sm + (size_t)((D + 3) & ~3) * sizeof(unsigned);
+    const int use_tab = sm_tab <= 227 * 1024;
+    if (use_tab) sm = sm_tab;
     cudaFuncSetAttribute(k_stage1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     // sum_s ceil(n_s / per_block) <= total / per_block + n_shards; spare blocks exit
     dim3 grid(total / (S1_WARPS * S1_IMGS) + n_shards);
     k_stage1<<<grid, 32 * S1_WARPS, sm, stream>>>(f0, shards, n_shards, total, *grid_h, W, L,
-                                                   lat, stats, qoi);
+                                                   lat, stats, qoi, use_tab);
     return cudaGetLastError() == cudaSuccess ? MLK_OK : MLK_ERR_CUDA;
 }
