@@ -74,10 +74,23 @@ k_decode(const MlkShard* __restrict__ shards, int n_shards, int total, MlkGrid g
         return c;
     };
     double top = -INFINITY, amax = 0.0;
-    for (int j = lane; j < D; j += 32) {
-        top = np_max2(top, cell(j));
-        const double dv = __dsub_rn(g.vpar[j], u);
-        amax = np_max2(amax, fabs(__dmul_rn(g.hmvol[j], __dmul_rn(dv, dv))));
+    if (g.sep) {
+        // separable grid: hmvol takes one value per (row edge, column edge)
+        // class and vpar one per column, so the products over all cells are
+        // exactly those of row 0 and (if there are interior rows) row 1 --
+        // the same set, hence the same max (NaN included)
+        for (int j = lane; j < D; j += 32) top = np_max2(top, cell(j));
+        const int cols = g.cols, nq = g.rows > 2 ? 2 * cols : cols;
+        for (int j = lane; j < nq; j += 32) {
+            const double dv = __dsub_rn(g.vpar[j], u);
+            amax = np_max2(amax, fabs(__dmul_rn(g.hmvol[j], __dmul_rn(dv, dv))));
+        }
+    } else {
+        for (int j = lane; j < D; j += 32) {
+            top = np_max2(top, cell(j));
+            const double dv = __dsub_rn(g.vpar[j], u);
+            amax = np_max2(amax, fabs(__dmul_rn(g.hmvol[j], __dmul_rn(dv, dv))));
+        }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
