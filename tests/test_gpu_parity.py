@@ -555,6 +555,43 @@ def test_device_inflate_matches_host_zlib():
     assert ol[-2] < 0 and ol[-1] < 0
 
 
+def test_device_inflate_rejects_every_truncation():
+    """Every proper prefix of a stream is an error (the bit reader takes
+    whole aligned words and must mask the bytes past the stream's end --
+    here the next stream's bytes sit right behind it)."""
+    import zlib
+
+    from paper_2212_10733_b200._lib import call
+    dev = torch.device("cuda", 0)
+    rng = np.random.default_rng(11)
+    raw = np.minimum(rng.geometric(0.2, 3000), 255).astype(np.uint8).tobytes()
+    full = [zlib.compress(raw, 6), zlib.compress(raw[:600], 0), zlib.compress(raw, 1)]
+    comp, want = [], []
+    for f in full:
+        for m in sorted(set(rng.integers(0, len(f), 60).tolist()) | {0, 1, 2, len(f) - 1}):
+            comp.append(f[:m])
+            want.append(None)
+        comp.append(f)
+        want.append(zlib.decompress(f))
+    n = len(comp)
+    cap = 4096
+    in_off = np.concatenate([[0], np.cumsum([len(c) for c in comp])[:-1]]).astype(np.int64)
+    blob = torch.from_numpy(np.frombuffer(b"".join(comp) + bytes(16), np.uint8).copy()).to(dev)
+    i64 = dict(dtype=torch.int64, device=dev)
+    out = torch.zeros(n * cap, dtype=torch.uint8, device=dev)
+    out_len = torch.empty(n, **i64)
+    call("mlk_zlib_decompress", blob, torch.from_numpy(in_off).to(dev),
+         torch.tensor([len(c) for c in comp], **i64), n, out,
+         torch.arange(0, n * cap, cap, **i64), cap, out_len)
+    ol = out_len.cpu().numpy()
+    host = out.cpu().numpy()
+    for k, w in enumerate(want):
+        if w is None:
+            assert ol[k] < 0, (k, len(comp[k]))
+        else:
+            assert ol[k] == len(w) and host[k * cap:k * cap + len(w)].tobytes() == w, k
+
+
 def test_pinned_input_gives_the_same_archive():
     from paper_2212_10733_b200.hostio import pinned_empty
     meta, _ = G.load("small")
