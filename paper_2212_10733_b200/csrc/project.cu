@@ -365,10 +365,12 @@ __device__ void newton_block(const double* fp, double fl, const MlkGrid& g, cons
                 const double w_in = cls_val(X.w, false, ce), w_ed = cls_val(X.w, true, ce);
                 const double* ebp = C.eb[ce];
                 double G1 = 0.0, G2 = 0.0, H1 = 0.0, H2 = 0.0, H3 = 0.0;
+                const double* fc = fp + c;  // column c, stepped by whole rows
                 auto row = [&](int r, double w, double ea) {
                     // f_plus = max(f, fl) as a compare-select (fl is finite
                     // here and a NaN f maps to fl, as with fmax)
-                    const double f = fp[r * cols + c];
+                    const double f = *fc;
+                    fc += ngrp * cols;
                     const double wf = w * ((f > fl ? f : fl) * ea * ebp[r]);
                     const double p2 = C.p2r[r];
                     const double w2f = w * wf, t2 = p2 * w2f;
@@ -382,6 +384,7 @@ __device__ void newton_block(const double* fp, double fl, const MlkGrid& g, cons
                 // only ones with the edge weight / exponent) peeled off the
                 // loop so its body has no selects
                 int r = g0;
+                fc += r * cols;
                 if (r == 0) {
                     row(0, w_ed, ea1);
                     r += ngrp;
